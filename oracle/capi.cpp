@@ -1,0 +1,199 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp).
+// C ABI over the restatement so pytest / tools/make_goldens.py / bench.py's CPU legs can
+// drive it through ctypes. Mirrors the reference's run() (runner.cpp:126-155): build the
+// Workspace, dispatch the method, evaluate the field.
+#include <chrono>
+#include <cstring>
+#include <memory>
+
+#include "oracle.hpp"
+
+using namespace ddo;
+
+extern "C" {
+
+struct ddo_config {
+  const char* problem;
+  int s, n_grid, M;
+  double l;
+  unsigned long long seed;
+  int method;  // 0 ddelm, 1 ddelm-cs, 2 ddelm-nn
+  double theta;
+  int flux_variant;         // 0 pointwise, 1 mean_edge
+  int change_of_variables;  // 0 nodal, 1 change_of_variables
+  double cg_rel_tol;
+  int cg_max_iter, cg_stop_after;
+  int workers, cg_workers;
+  int debug_flip_flux_row;
+};
+
+struct ddo_handle {
+  std::unique_ptr<Workspace> ws;
+  SolveReport rep;
+  bool solved = false;
+  double build_seconds = 0;
+};
+
+static void set_err(char* err, int n, const char* msg) {
+  if (err && n > 0) {
+    std::strncpy(err, msg, n - 1);
+    err[n - 1] = 0;
+  }
+}
+
+void* ddo_create(const ddo_config* c, char* err, int errlen) {
+  try {
+    auto h = new ddo_handle;
+    SolverOptions o;
+    o.flux_variant = c->flux_variant ? FluxVariant::MeanEdge : FluxVariant::Pointwise;
+    o.change_of_variables = c->change_of_variables != 0;
+    o.workers = c->workers;
+    o.cg_workers = c->cg_workers;
+    o.debug_flip_flux_row = c->debug_flip_flux_row;
+    const auto t0 = std::chrono::steady_clock::now();
+    h->ws = std::make_unique<Workspace>(make_problem(c->problem), c->s, c->n_grid, c->M, c->l,
+                                        c->seed, o);
+    h->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return h;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return nullptr;
+  }
+}
+
+void ddo_destroy(void* p) { delete static_cast<ddo_handle*>(p); }
+
+int ddo_solve(void* p, int method, double theta, double rel_tol, int max_iter, int stop_after,
+              char* err, int errlen) {
+  auto h = static_cast<ddo_handle*>(p);
+  try {
+    CgOptions o{rel_tol, max_iter, stop_after};
+    if (method == 0) h->rep = ddelm_solve(*h->ws, o);
+    else if (method == 1) h->rep = ddelm_cs_solve(*h->ws, o);
+    else h->rep = ddelm_nn_solve(*h->ws, theta, o);
+    h->solved = true;
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    set_err(err, errlen, e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return 3;
+  }
+}
+
+/// info[0..]: n_subs, n_delta, n_pi, n_mu, M, rows, iterations, converged, negative_curvature,
+/// n_residuals, n_pi_flux
+void ddo_info(void* p, int* info) {
+  auto h = static_cast<ddo_handle*>(p);
+  const Workspace& ws = *h->ws;
+  info[0] = ws.n_subs();
+  info[1] = ws.n_delta();
+  info[2] = ws.n_pi();
+  info[3] = ws.n_mu();
+  info[4] = ws.layers[0].M;
+  info[5] = ws.blocks[0].rows();
+  info[6] = h->rep.iterations;
+  info[7] = h->rep.converged ? 1 : 0;
+  info[8] = h->rep.negative_curvature ? 1 : 0;
+  info[9] = static_cast<int>(h->rep.residual_history.size());
+  info[10] = ws.n_pi_flux();
+}
+
+/// t[0..5]: assembly, factorization, setup (coarse+neumann+rhs), cg, reconstruct, build total
+void ddo_timings(void* p, double* t) {
+  auto h = static_cast<ddo_handle*>(p);
+  t[0] = h->ws->assembly_seconds;
+  t[1] = h->ws->factorization_seconds;
+  t[2] = h->rep.setup_seconds;
+  t[3] = h->rep.cg_seconds;
+  t[4] = h->rep.reconstruct_seconds;
+  t[5] = h->build_seconds;
+}
+
+void ddo_residuals(void* p, double* out) {
+  auto h = static_cast<ddo_handle*>(p);
+  std::copy(h->rep.residual_history.begin(), h->rep.residual_history.end(), out);
+}
+
+void ddo_mu(void* p, double* out) {
+  auto h = static_cast<ddo_handle*>(p);
+  std::copy(h->rep.mu.begin(), h->rep.mu.end(), out);
+}
+
+void ddo_coeffs(void* p, double* out) {
+  auto h = static_cast<ddo_handle*>(p);
+  const int M = h->ws->layers[0].M;
+  for (size_t i = 0; i < h->rep.coeffs.size(); ++i)
+    std::copy(h->rep.coeffs[i].begin(), h->rep.coeffs[i].end(), out + i * M);
+}
+
+/// Per-subdomain ranks of K (and of Kbar when the Neumann layer was built, else -1).
+void ddo_ranks(void* p, int* rk, int* rkbar, double* qr_ratio) {
+  auto h = static_cast<ddo_handle*>(p);
+  const Workspace& ws = *h->ws;
+  for (int i = 0; i < ws.n_subs(); ++i) {
+    rk[i] = ws.fac[i].rank();
+    rkbar[i] = ws.neumann_built ? ws.nfac[i].rank() : -1;
+    qr_ratio[2 * i] = ws.fac[i].qr_diag_ratio;
+    qr_ratio[2 * i + 1] = ws.neumann_built ? ws.nfac[i].qr_diag_ratio : -1.0;
+  }
+}
+
+void ddo_layer(void* p, int i, double* w0, double* w1, double* b) {
+  auto h = static_cast<ddo_handle*>(p);
+  const FeatureLayer& L = h->ws->layers[i];
+  std::copy(L.w0.begin(), L.w0.end(), w0);
+  std::copy(L.w1.begin(), L.w1.end(), w1);
+  std::copy(L.b.begin(), L.b.end(), b);
+}
+
+/// Local matrix K_i (rows x M, column-major) and f_i.
+void ddo_local(void* p, int i, double* K, double* f) {
+  auto h = static_cast<ddo_handle*>(p);
+  const LocalBlocks& b = h->ws->blocks[i];
+  std::copy(b.K.a.begin(), b.K.a.end(), K);
+  std::copy(b.f.begin(), b.f.end(), f);
+}
+
+/// Neumann matrix Kbar_i (rows x M) — requires the Neumann layer.
+int ddo_kbar(void* p, int i, double* K) {
+  auto h = static_cast<ddo_handle*>(p);
+  if (!h->ws->neumann_built) return 1;
+  const Mat& Kb = h->ws->Kbar[i];
+  std::copy(Kb.a.begin(), Kb.a.end(), K);
+  return 0;
+}
+
+/// Field and gradient samples on the n x n grid (metrics.cpp:18-57), index b*n + a.
+void ddo_field(void* p, int n, double* u, double* gx, double* gy) {
+  auto h = static_cast<ddo_handle*>(p);
+  FieldSamples fs = sample_field(h->ws->part, h->ws->layers, h->rep.coeffs, n);
+  std::copy(fs.u.begin(), fs.u.end(), u);
+  std::copy(fs.gx.begin(), fs.gx.end(), gx);
+  std::copy(fs.gy.begin(), fs.gy.end(), gy);
+}
+
+/// Field of caller-supplied coefficients (N x M) with this workspace's layers.
+void ddo_field_of(void* p, const double* coeffs, int n, double* u, double* gx, double* gy) {
+  auto h = static_cast<ddo_handle*>(p);
+  const int N = h->ws->n_subs(), M = h->ws->layers[0].M;
+  LocalVecs c(N);
+  for (int i = 0; i < N; ++i) c[i].assign(coeffs + static_cast<size_t>(i) * M, coeffs + static_cast<size_t>(i + 1) * M);
+  FieldSamples fs = sample_field(h->ws->part, h->ws->layers, c, n);
+  std::copy(fs.u.begin(), fs.u.end(), u);
+  std::copy(fs.gx.begin(), fs.gx.end(), gx);
+  std::copy(fs.gy.begin(), fs.gy.end(), gy);
+}
+
+/// Relative L2 / H1 errors against the exact solution (runner.cpp:144-150).
+int ddo_errors(void* p, int n, double* l2, double* h1) {
+  auto h = static_cast<ddo_handle*>(p);
+  if (!h->ws->problem.has_exact()) return 1;
+  ErrorReport e = relative_errors_exact(h->ws->part, h->ws->layers, h->rep.coeffs, h->ws->problem, n);
+  *l2 = e.l2;
+  *h1 = e.h1;
+  return 0;
+}
+
+}  // extern "C"

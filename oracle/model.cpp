@@ -1,0 +1,439 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp).
+// Restates proj/src/geometry.cpp, features.cpp, problems.cpp (Poisson rows), assembly.cpp.
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <numbers>
+#include <random>
+
+#include "oracle.hpp"
+
+namespace ddo {
+
+// ------------------------------------------------------------------ geometry.cpp
+double Box::diam() const { return std::hypot(x1 - x0, y1 - y0); }  // geometry.cpp:10
+
+int DomainPartition::subdomain_of(const Point& x) const {  // geometry.cpp:12-18
+  auto clampi = [this](double v) {
+    int i = static_cast<int>(std::floor(v * s));
+    return std::clamp(i, 0, s - 1);
+  };
+  return clampi(x.y) * s + clampi(x.x);
+}
+
+DomainPartition partition_domain(int s, int n_grid) {  // geometry.cpp:20-66
+  if (s < 1) throw std::invalid_argument("partition_domain: s must be >= 1");
+  if (n_grid < 3) throw std::invalid_argument("partition_domain: n_grid must be >= 3");
+  DomainPartition p;
+  p.s = s;
+  p.n_grid = n_grid;
+  p.boxes.resize(s * s);
+  p.side_edge.assign(s * s, {-1, -1, -1, -1});
+  p.neighbors.resize(s * s);
+  const double h = 1.0 / s;
+  for (int iy = 0; iy < s; ++iy)
+    for (int ix = 0; ix < s; ++ix) p.boxes[iy * s + ix] = Box{ix * h, iy * h, (ix + 1) * h, (iy + 1) * h};
+  for (int k = 1; k <= s - 1; ++k)  // vertical edges first
+    for (int m = 0; m < s; ++m) {
+      Edge e;
+      e.id = (k - 1) * s + m;
+      e.vertical = true;
+      e.k = k;
+      e.m = m;
+      e.subs = {m * s + (k - 1), m * s + k};
+      p.edges.push_back(e);
+      p.side_edge[e.subs[0]][1] = e.id;
+      p.side_edge[e.subs[1]][0] = e.id;
+      p.neighbors[e.subs[0]].push_back({e.subs[1], e.id});
+      p.neighbors[e.subs[1]].push_back({e.subs[0], e.id});
+    }
+  const int nv = s * (s - 1);
+  for (int m = 1; m <= s - 1; ++m)
+    for (int k = 0; k < s; ++k) {
+      Edge e;
+      e.id = nv + (m - 1) * s + k;
+      e.vertical = false;
+      e.k = k;
+      e.m = m;
+      e.subs = {(m - 1) * s + k, m * s + k};
+      p.edges.push_back(e);
+      p.side_edge[e.subs[0]][3] = e.id;
+      p.side_edge[e.subs[1]][2] = e.id;
+      p.neighbors[e.subs[0]].push_back({e.subs[1], e.id});
+      p.neighbors[e.subs[1]].push_back({e.subs[0], e.id});
+    }
+  return p;
+}
+
+PointSets classify_points(const DomainPartition& p) {  // geometry.cpp:69-146
+  const int s = p.s, n = p.n_grid;
+  const int S = s * (n - 1);
+  PointSets ps;
+  const int N = p.n_subdomains();
+  ps.interior.resize(N);
+  ps.boundary.resize(N);
+  ps.interface.resize(N);
+  ps.gamma_meta.resize(N);
+  ps.local_edges.resize(N);
+  for (int iy = 0; iy < s; ++iy)
+    for (int ix = 0; ix < s; ++ix) {
+      const int i = iy * s + ix;
+      std::map<std::pair<int, int>, int> gamma_of;
+      for (int b = 0; b < n; ++b)
+        for (int a = 0; a < n; ++a) {
+          const int gx = ix * (n - 1) + a, gy = iy * (n - 1) + b;
+          const Point xy{static_cast<double>(gx) / S, static_cast<double>(gy) / S};
+          const bool on_outer = gx == 0 || gx == S || gy == 0 || gy == S;
+          const bool on_local = a == 0 || a == n - 1 || b == 0 || b == n - 1;
+          if (!on_local) {
+            ps.interior[i].push_back(xy);
+          } else if (on_outer) {
+            ps.boundary[i].push_back(xy);
+          } else {
+            GammaPoint g;
+            g.xy = xy;
+            const bool xl = a == 0 || a == n - 1, yl = b == 0 || b == n - 1;
+            if (xl && yl) {
+              g.is_cross = true;
+              g.cross_id = p.cross_id(gx / (n - 1), gy / (n - 1));
+            } else if (xl) {
+              const int k = (a == 0) ? ix : ix + 1;
+              g.edge_id = (k - 1) * s + iy;
+              g.t = b;
+            } else {
+              const int m = (b == 0) ? iy : iy + 1;
+              g.edge_id = s * (s - 1) + (m - 1) * s + ix;
+              g.t = a;
+            }
+            gamma_of[{a, b}] = static_cast<int>(ps.interface[i].size());
+            ps.interface[i].push_back(xy);
+            ps.gamma_meta[i].push_back(g);
+          }
+        }
+      const Point normals[4] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+      for (int side = 0; side < 4; ++side) {
+        const int eid = p.side_edge[i][side];
+        if (eid < 0) continue;
+        LocalEdge le;
+        le.edge_id = eid;
+        le.vertical = side < 2;
+        le.normal = normals[side];
+        for (int j = 0; j < n; ++j) {
+          const int a = le.vertical ? (side == 0 ? 0 : n - 1) : j;
+          const int b = le.vertical ? j : (side == 2 ? 0 : n - 1);
+          auto it = gamma_of.find({a, b});
+          if (it == gamma_of.end()) continue;
+          le.pts.push_back(it->second);
+          le.geom_j.push_back(j);
+          if (j == 0) le.first_corner = true;
+          if (j == n - 1) le.last_corner = true;
+        }
+        ps.local_edges[i].push_back(le);
+      }
+    }
+  return ps;
+}
+
+InterfaceIndex build_interface_index(const DomainPartition& p, const PointSets& ps, int cc) {
+  // geometry.cpp:148-179
+  if (cc != 1 && cc != 2) throw std::invalid_argument("build_interface_index: cc must be 1 or 2");
+  InterfaceIndex idx;
+  idx.cc = cc;
+  idx.interior_per_edge = p.n_grid - 2;
+  idx.n_delta = static_cast<int>(p.edges.size()) * cc * idx.interior_per_edge;
+  idx.n_pi = p.cross_count() * cc;
+  idx.multiplicity.assign(idx.n_mu(), 0);
+  idx.is_pi.assign(idx.n_mu(), 0);
+  for (int g = idx.n_delta; g < idx.n_mu(); ++g) idx.is_pi[g] = 1;
+  const int N = p.n_subdomains();
+  idx.local_to_global.resize(N);
+  for (int i = 0; i < N; ++i) {
+    const auto& meta = ps.gamma_meta[i];
+    const int ng = static_cast<int>(meta.size());
+    idx.local_to_global[i].resize(static_cast<size_t>(cc) * ng);
+    for (int c = 0; c < cc; ++c)
+      for (int q = 0; q < ng; ++q) {
+        const GammaPoint& g = meta[q];
+        const int gi = g.is_cross ? idx.pi_index(g.cross_id, c) : idx.delta_index(g.edge_id, c, g.t);
+        idx.local_to_global[i][c * ng + q] = gi;
+        idx.multiplicity[gi] += 1;
+      }
+  }
+  return idx;
+}
+
+// ------------------------------------------------------------------ features.cpp
+FeatureLayer init_layer(int M, const Box& box, double l, double r, uint64_t seed) {
+  // features.cpp:9-35: mt19937_64(seed); per neuron draw w0, w1 ~ U[-l,l], xi0, xi1 ~
+  // U(box +- r); b = -(w0 xi0 + w1 xi1).
+  if (M < 1) throw std::invalid_argument("init_layer: M must be positive");
+  if (l <= 0) throw std::invalid_argument("init_layer: l must be positive");
+  if (r <= 0) throw std::invalid_argument("init_layer: r must be positive");
+  FeatureLayer L;
+  L.M = M;
+  L.l = l;
+  L.r = r;
+  L.box = box;
+  L.seed = seed;
+  L.w0.resize(M);
+  L.w1.resize(M);
+  L.b.resize(M);
+  std::mt19937_64 gen(seed);
+  std::uniform_real_distribution<double> uw(-l, l);
+  std::uniform_real_distribution<double> ux(box.x0 - r, box.x1 + r);
+  std::uniform_real_distribution<double> uy(box.y0 - r, box.y1 + r);
+  for (int j = 0; j < M; ++j) {
+    const double w0 = uw(gen), w1 = uw(gen);
+    const double xi0 = ux(gen), xi1 = uy(gen);
+    L.w0[j] = w0;
+    L.w1[j] = w1;
+    L.b[j] = -(w0 * xi0 + w1 * xi1);
+  }
+  return L;
+}
+
+double scale_from_constant(double c, int M, const Box& box, double r) {  // features.cpp:37-40
+  const Box e{box.x0 - r, box.y0 - r, box.x1 + r, box.y1 + r};
+  return c * std::sqrt(static_cast<double>(M)) / e.diam();
+}
+
+Mat eval_derivative_matrix(const FeatureLayer& L, const std::vector<Point>& pts, int dx, int dy) {
+  // features.cpp:42-76: sigma' = 1 - s^2, sigma'' = -2 s s1, sigma''' = -2 s1^2 - 2 s s2,
+  // sigma'''' = -6 s1 s2 - 2 s s3; times w0^dx w1^dy.
+  if (dx < 0 || dy < 0 || dx + dy > 4)
+    throw std::invalid_argument("eval_derivative_matrix: derivative order must be in [0, 4]");
+  const int order = dx + dy;
+  const int np = static_cast<int>(pts.size());
+  Mat out(np, L.M);
+  for (int j = 0; j < L.M; ++j) {
+    const double w0 = L.w0[j], w1 = L.w1[j];
+    double wfac = 1.0;
+    for (int a = 0; a < dx; ++a) wfac *= w0;
+    for (int a = 0; a < dy; ++a) wfac *= w1;
+    for (int k = 0; k < np; ++k) {
+      const double z = w0 * pts[k].x + w1 * pts[k].y + L.b[j];
+      const double s0 = std::tanh(z);
+      double v = s0;
+      if (order > 0) {
+        const double s1 = 1.0 - s0 * s0;
+        const double s2 = -2.0 * s0 * s1;
+        const double s3 = -2.0 * s1 * s1 - 2.0 * s0 * s2;
+        const double s4 = -6.0 * s1 * s2 - 2.0 * s0 * s3;
+        switch (order) {
+          case 1: v = s1; break;
+          case 2: v = s2; break;
+          case 3: v = s3; break;
+          default: v = s4; break;
+        }
+        v *= wfac;
+      }
+      out(k, j) = v;
+    }
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ problems.cpp
+namespace {
+constexpr double kPi = std::numbers::pi;
+
+Mat add(const Mat& A, const Mat& B, double sa, double sb) {
+  Mat C(A.r, A.c);
+  for (size_t t = 0; t < A.a.size(); ++t) C.a[t] = sa * A.a[t] + sb * B.a[t];
+  return C;
+}
+}  // namespace
+
+Mat ProblemSpec::interior_rows(const FeatureLayer& L, const std::vector<Point>& pts) const {
+  // problems.cpp:71-73: -(D20 + D02)
+  const Mat a = eval_derivative_matrix(L, pts, 2, 0), b = eval_derivative_matrix(L, pts, 0, 2);
+  Mat C(a.r, a.c);
+  for (size_t t = 0; t < a.a.size(); ++t) C.a[t] = -(a.a[t] + b.a[t]);
+  return C;
+}
+
+Mat ProblemSpec::boundary_rows(const FeatureLayer& L, const std::vector<Point>& pts) const {
+  return trace_rows(L, pts);  // problems.cpp:96-100
+}
+
+Mat ProblemSpec::trace_rows(const FeatureLayer& L, const std::vector<Point>& pts) const {
+  return eval_derivative_matrix(L, pts, 0, 0);  // problems.cpp:102-108 (comp 0)
+}
+
+Mat ProblemSpec::flux_rows(const FeatureLayer& L, const std::vector<Point>& pts,
+                           const Point& n) const {
+  // problems.cpp:113-121: n_x D10 + n_y D01 (Eigen evaluates nx*A + ny*B elementwise)
+  return add(eval_derivative_matrix(L, pts, 1, 0), eval_derivative_matrix(L, pts, 0, 1), n.x, n.y);
+}
+
+ProblemSpec make_problem(const std::string& name) {  // problems.cpp:132-188
+  ProblemSpec p;
+  p.name = name;
+  if (name == "poisson_sinpi") {
+    p.exact = [](const Point& x) { return std::sin(kPi * x.x) * std::sin(kPi * x.y); };
+    p.exact_grad = [](const Point& x) {
+      return Point{kPi * std::cos(kPi * x.x) * std::sin(kPi * x.y),
+                   kPi * std::sin(kPi * x.x) * std::cos(kPi * x.y)};
+    };
+    p.forcing = [](const Point& x) {
+      return 2.0 * kPi * kPi * std::sin(kPi * x.x) * std::sin(kPi * x.y);
+    };
+    p.boundary = p.exact;
+  } else if (name == "poisson_sin2pi_exp") {
+    p.exact = [](const Point& x) { return std::sin(2 * kPi * x.x) * std::exp(x.y); };
+    p.exact_grad = [](const Point& x) {
+      return Point{2 * kPi * std::cos(2 * kPi * x.x) * std::exp(x.y),
+                   std::sin(2 * kPi * x.x) * std::exp(x.y)};
+    };
+    p.forcing = [](const Point& x) {
+      return (4.0 * kPi * kPi - 1.0) * std::sin(2 * kPi * x.x) * std::exp(x.y);
+    };
+    p.boundary = p.exact;
+  } else if (name == "poisson_sin2pi_cos3pi_x2y") {
+    // BASELINE.json config C4 (not in the reference catalogue):
+    // u = sin(2 pi x) cos(3 pi y) + x^2 y, f = -lap u = 13 pi^2 sin(2 pi x) cos(3 pi y) - 2y.
+    p.exact = [](const Point& x) {
+      return std::sin(2 * kPi * x.x) * std::cos(3 * kPi * x.y) + x.x * x.x * x.y;
+    };
+    p.exact_grad = [](const Point& x) {
+      return Point{2 * kPi * std::cos(2 * kPi * x.x) * std::cos(3 * kPi * x.y) + 2 * x.x * x.y,
+                   -3 * kPi * std::sin(2 * kPi * x.x) * std::sin(3 * kPi * x.y) + x.x * x.x};
+    };
+    p.forcing = [](const Point& x) {
+      return 13.0 * kPi * kPi * std::sin(2 * kPi * x.x) * std::cos(3 * kPi * x.y) - 2.0 * x.y;
+    };
+    p.boundary = p.exact;
+  } else {
+    throw std::invalid_argument("make_problem: unknown problem '" + name + "'");
+  }
+  return p;
+}
+
+// ------------------------------------------------------------------ assembly.cpp
+LocalBlocks assemble_local(const ProblemSpec& problem, const FeatureLayer& L, const PointSets& ps,
+                           int i) {
+  // assembly.cpp:9-46: K = [interior; boundary; trace], f = [f(x_I); g(x_B); 0]
+  LocalBlocks b;
+  b.n_int = static_cast<int>(ps.interior[i].size());
+  b.n_bnd = static_cast<int>(ps.boundary[i].size());
+  b.n_gamma = static_cast<int>(ps.interface[i].size());
+  b.bc = problem.boundary_components;
+  b.cc = problem.components;
+  b.K = Mat(b.rows(), L.M);
+  b.f.assign(b.rows(), 0.0);
+  auto put = [&](const Mat& src, int row0) {
+    for (int j = 0; j < src.c; ++j)
+      for (int k = 0; k < src.r; ++k) b.K(row0 + k, j) = src(k, j);
+  };
+  put(problem.interior_rows(L, ps.interior[i]), 0);
+  for (int k = 0; k < b.n_int; ++k) b.f[k] = problem.forcing(ps.interior[i][k]);
+  int row = b.n_int;
+  put(problem.boundary_rows(L, ps.boundary[i]), row);
+  for (int k = 0; k < b.n_bnd; ++k) b.f[row + k] = problem.boundary(ps.boundary[i][k]);
+  row += b.n_bnd;
+  put(problem.trace_rows(L, ps.interface[i]), row);
+  for (const LocalEdge& le : ps.local_edges[i]) {
+    std::vector<Point> pts;
+    for (int q : le.pts) pts.push_back(ps.interface[i][q]);
+    b.F_edges.push_back(problem.flux_rows(L, pts, le.normal));
+  }
+  return b;
+}
+
+Mat build_transition(int m) {  // assembly.cpp:48-57
+  if (m < 2) throw std::invalid_argument("build_transition: edge needs at least 2 points");
+  Mat T = Mat::identity(m);
+  for (int j = 0; j < m; ++j) {
+    const double frac = static_cast<double>(j) / (m - 1);
+    T(j, 0) = 1.0 - frac;
+    T(j, m - 1) = frac;
+  }
+  return T;
+}
+
+Transition build_subdomain_transition(const std::vector<LocalEdge>& edges, int n_gamma,
+                                      int n_grid) {
+  // assembly.cpp:59-78. T = I + E (E: non-corner rows x corner columns, E^2 = 0).
+  // partialPivLu of T pivots on the unit diagonal with no fill, so T^{-1} = I - E exactly.
+  Transition t;
+  t.T = Mat::identity(n_gamma);
+  for (const LocalEdge& le : edges) {
+    const int np = static_cast<int>(le.pts.size());
+    if (le.first_corner) {
+      const int col = le.pts.front();
+      for (int q = 1; q < np; ++q)
+        t.T(le.pts[q], col) = 1.0 - static_cast<double>(le.geom_j[q]) / (n_grid - 1);
+    }
+    if (le.last_corner) {
+      const int col = le.pts.back();
+      for (int q = 0; q + 1 < np; ++q)
+        t.T(le.pts[q], col) = static_cast<double>(le.geom_j[q]) / (n_grid - 1);
+    }
+  }
+  t.Tinv = Mat::identity(n_gamma);
+  for (int j = 0; j < n_gamma; ++j)
+    for (int i = 0; i < n_gamma; ++i)
+      if (i != j && t.T(i, j) != 0.0) t.Tinv(i, j) = -t.T(i, j);
+  return t;
+}
+
+void apply_change_of_variables(LocalBlocks& blocks, const Transition& t) {  // assembly.cpp:80-87
+  if (t.T.r != blocks.n_gamma)
+    throw std::invalid_argument("apply_change_of_variables: transition size mismatch");
+  const int r0 = blocks.trace_row(0, 0), ng = blocks.n_gamma;
+  for (int j = 0; j < blocks.K.c; ++j) {
+    std::vector<double> old(ng);
+    for (int q = 0; q < ng; ++q) old[q] = blocks.K(r0 + q, j);
+    for (int q = 0; q < ng; ++q) {
+      double s = 0;
+      for (int k = 0; k < ng; ++k) {
+        const double tq = t.Tinv(q, k);
+        if (tq != 0.0) s += tq * old[k];
+      }
+      blocks.K(r0 + q, j) = s;
+    }
+  }
+}
+
+FluxBlocks build_flux(const DomainPartition& p, const PointSets& ps, const InterfaceIndex& idx,
+                      FluxVariant variant) {  // assembly.cpp:89-133
+  FluxBlocks fb;
+  fb.variant = variant;
+  fb.n_delta = idx.n_delta;
+  fb.n_flux = idx.n_delta + p.cross_count() * idx.cc * 2;
+  const int N = p.n_subdomains();
+  fb.scatter.resize(N);
+  fb.edge_row0.resize(N);
+  const int n = p.n_grid;
+  for (int i = 0; i < N; ++i) {
+    int off = 0;
+    for (const LocalEdge& le : ps.local_edges[i]) {
+      fb.edge_row0[i].push_back(off);
+      const int np = static_cast<int>(le.pts.size());
+      const int dir = le.vertical ? 0 : 1;
+      for (int c = 0; c < idx.cc; ++c)
+        for (int q = 0; q < np; ++q) {
+          const int j = le.geom_j[q];
+          const int lrow = off + c * np + q;
+          if (j > 0 && j < n - 1) {
+            fb.scatter[i].push_back({idx.delta_index(le.edge_id, c, j), lrow, 1.0});
+            continue;
+          }
+          const GammaPoint& gp = ps.gamma_meta[i][le.pts[q]];
+          const int grow = idx.n_delta + (gp.cross_id * idx.cc + c) * 2 + dir;
+          if (variant == FluxVariant::Pointwise) {
+            fb.scatter[i].push_back({grow, lrow, 1.0});
+          } else {
+            const int opposing = (j == 0) ? n - 1 : 0;
+            const double w = 1.0 / (n - 1);
+            for (int q2 = 0; q2 < np; ++q2)
+              if (le.geom_j[q2] != opposing) fb.scatter[i].push_back({grow, off + c * np + q2, w});
+          }
+        }
+      off += idx.cc * np;
+    }
+  }
+  return fb;
+}
+
+}  // namespace ddo
