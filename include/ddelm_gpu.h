@@ -1,0 +1,123 @@
+/*
+ * ddelm_gpu.h — C-ABI boundary of the B200-native DDELM-NN hot path.
+ *
+ * Replaces the reference's C++ solver entry points (no torch types, plain pointers/sizes):
+ *   ddelm_gpu_create        Workspace::Workspace(problem, s, n_grid, M, l, seed, opts)
+ *                           (proj/include/ddelm/solvers.hpp:79-80, src/solvers.cpp:123-167)
+ *   ddelm_gpu_build         the assembly + LsFactor part of that constructor
+ *                           (solvers.cpp:131-151; features.cpp:42-76; assembly.cpp:9-87)
+ *   ddelm_gpu_build_coarse  Workspace::assemble_coarse      (solvers.cpp:278-326)
+ *   ddelm_gpu_build_neumann Workspace::build_neumann        (solvers.cpp:390-448)
+ *   ddelm_gpu_solve         ddelm_cs_solve / ddelm_nn_solve (solvers.cpp:582-605, 535-578)
+ *   ddelm_gpu_get_*         SolveReport fields               (solvers.hpp:162-171)
+ *   ddelm_gpu_destroy       ~Workspace
+ *
+ * Error convention (mirrors the reference's exceptions, solvers.hpp / SURVEY.md §8b):
+ *   DDELM_OK = 0
+ *   DDELM_ERR_INVALID_ARGUMENT  std::invalid_argument  (theta outside [0,1], s < 1,
+ *                               n_grid < 3, M < 1, l <= 0, non-tall K, unknown problem)
+ *   DDELM_ERR_RUNTIME           std::runtime_error     (coarse Schur matrix not SPD)
+ *   DDELM_ERR_CUDA              CUDA / NCCL failure (no device, launch error, OOM)
+ *   DDELM_ERR_CAPACITY          numerical rank above the device COD capacity
+ * Non-convergence is not an error: ddelm_report.converged = 0 (solvers.cpp:515,560).
+ * The message of the last error on the calling thread: ddelm_gpu_last_error().
+ *
+ * Ownership: device memory is owned by the workspace; host output buffers are caller
+ * allocated. One CUDA stream per workspace; calls are not reentrant per workspace.
+ */
+#ifndef DDELM_GPU_H
+#define DDELM_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DDELM_OK = 0,
+  DDELM_ERR_INVALID_ARGUMENT = 1,
+  DDELM_ERR_RUNTIME = 2,
+  DDELM_ERR_CUDA = 3,
+  DDELM_ERR_CAPACITY = 4
+};
+
+/* problem ids (make_problem, problems.cpp:132-188; C4's problem is an addition) */
+enum {
+  DDELM_POISSON_SINPI = 0,
+  DDELM_POISSON_SIN2PI_EXP = 1,
+  DDELM_POISSON_SIN2PI_COS3PI_X2Y = 2
+};
+
+enum { DDELM_METHOD_DDELM = 0, DDELM_METHOD_CS = 1, DDELM_METHOD_NN = 2 };
+enum { DDELM_FLUX_POINTWISE = 0, DDELM_FLUX_MEAN_EDGE = 1 };
+
+typedef struct ddelm_desc {
+  int problem;              /* DDELM_POISSON_* */
+  int s;                    /* s x s subdomains */
+  int n_grid;               /* collocation points per direction per subdomain */
+  int M;                    /* neurons per subdomain */
+  double l;                 /* weight scale (features.cpp:9-35) */
+  uint64_t seed;            /* per-subdomain seed + i (solvers.cpp:136) */
+  int flux_variant;         /* DDELM_FLUX_* */
+  int change_of_variables;  /* 0 nodal, 1 change of variables */
+  double rank_tol;          /* SolverOptions::rank_tol, 1e-10 */
+  int device;               /* CUDA device ordinal */
+  int debug_flip_flux_row;  /* validation hook (solvers.hpp:54-57); -1 = off */
+} ddelm_desc;
+
+typedef struct ddelm_report {
+  int iterations;
+  int converged;
+  int negative_curvature;
+  int n_delta, n_pi, n_mu, n_subdomains, M;
+  double assembly_seconds;       /* feature + matrix build (device time) */
+  double factorization_seconds;  /* QR / COD (device time) */
+  double setup_seconds;          /* coarse + Neumann layers + reduced RHS */
+  double cg_seconds;
+  double reconstruct_seconds;
+  double total_seconds;
+} ddelm_report;
+
+typedef struct ddelm_ws ddelm_ws;
+
+const char* ddelm_gpu_last_error(void);
+const char* ddelm_gpu_version(void);
+
+int ddelm_gpu_create(const ddelm_desc* desc, ddelm_ws** out);
+int ddelm_gpu_build(ddelm_ws* ws);
+int ddelm_gpu_build_coarse(ddelm_ws* ws);
+int ddelm_gpu_build_neumann(ddelm_ws* ws);
+/* method: DDELM_METHOD_CS or DDELM_METHOD_NN (theta in [0,1]; theta = 0 is exactly CS).
+ * max_iter <= 0 means 20 x n_delta (solvers.cpp:85). */
+int ddelm_gpu_solve(ddelm_ws* ws, int method, double theta, double rel_tol, int max_iter,
+                    ddelm_report* report);
+/* Re-seed the feature layers (seed + i per subdomain) and invalidate every built layer;
+ * the geometry / index plan is kept. */
+int ddelm_gpu_reseed(ddelm_ws* ws, uint64_t seed);
+void ddelm_gpu_destroy(ddelm_ws* ws);
+
+/* Results of the last solve (host buffers, caller allocated). */
+int ddelm_gpu_get_mu(ddelm_ws* ws, double* mu /* n_mu: Delta then Pi */);
+int ddelm_gpu_get_coeffs(ddelm_ws* ws, double* coeffs /* n_subdomains x M */);
+int ddelm_gpu_get_residuals(ddelm_ws* ws, double* hist, int cap);
+/* Per-subdomain numerical ranks of K_i and Kbar_i (-1 when the layer is not built) and the
+ * unpivoted-QR diagonal ratio min|R_ii|/max|R_ii| used by the branch test (solvers.cpp:27-32). */
+int ddelm_gpu_get_ranks(ddelm_ws* ws, int* rank_k, int* rank_kbar, double* qr_ratio /* 2N */);
+/* Feature layer of subdomain i (w0, w1, b: M each) — for field evaluation by the caller. */
+int ddelm_gpu_get_layer(ddelm_ws* ws, int i, double* w0, double* w1, double* b);
+/* Local matrices as built on the device (rows x M column-major), for parity tests. */
+int ddelm_gpu_get_local(ddelm_ws* ws, int i, int which /* 0 K, 1 Kbar */, double* K, int* rows);
+/* out = cs_reduced_apply(v, weight) on the device (solvers.cpp:372-386, weight 599-603;
+ * theta = 0: plain coarse operator). v, out: n_delta host doubles. Builds layers as needed. */
+int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double* out);
+/* Per-phase device timings of the last build/solve (ms): see workspace.cu for the order. */
+int ddelm_gpu_get_phase_ms(ddelm_ws* ws, double* ms, int cap);
+/* Kernel launches issued by the last ddelm_gpu_build..solve sequence (own kernels only). */
+long long ddelm_gpu_get_launch_count(ddelm_ws* ws);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DDELM_GPU_H */

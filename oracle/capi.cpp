@@ -186,6 +186,29 @@ void ddo_field_of(void* p, const double* coeffs, int n, double* u, double* gx, d
   std::copy(fs.gy.begin(), fs.gy.end(), gy);
 }
 
+/// cs_reduced_apply(v, weight) with the NN weight theta (theta = 0: plain coarse operator),
+/// solvers.cpp:372-386 + 599-603. Builds the coarse / Neumann layers on first use.
+int ddo_apply_cs(void* p, double theta, const double* v, double* out) {
+  auto h = static_cast<ddo_handle*>(p);
+  Workspace& ws = *h->ws;
+  ws.assemble_coarse();
+  LinOp weight = [](const Vec& x) { return x; };
+  if (theta > 0) {
+    ws.build_neumann();
+    weight = [&ws, theta](const Vec& x) {
+      Vec w = ws.apply_PT(ws.apply_P(x));
+      for (auto& e : w) e *= theta;
+      if (theta < 1.0)
+        for (size_t i = 0; i < w.size(); ++i) w[i] += (1.0 - theta) * x[i];
+      return w;
+    };
+  }
+  Vec in(v, v + ws.n_delta());
+  Vec o = ws.cs_reduced_apply(in, weight);
+  std::copy(o.begin(), o.end(), out);
+  return 0;
+}
+
 /// Relative L2 / H1 errors against the exact solution (runner.cpp:144-150).
 int ddo_errors(void* p, int n, double* l2, double* h1) {
   auto h = static_cast<ddo_handle*>(p);

@@ -4,6 +4,7 @@
 //   ColPivHouseholderQR/COD  solvers.cpp:35-40 (via Eigen::CompleteOrthogonalDecomposition)
 //   LLT                      solvers.cpp:322
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 
@@ -272,6 +273,12 @@ Mat COD::pseudo_inverse() const { return solve(Mat::identity(cpqr.qr.r)); }
 
 Mat COD::householderQ_cols(int ncols) const { return form_q(cpqr.qr, cpqr.hcoeffs, ncols); }
 
+namespace {
+Vec upper_solve(const Mat& R, const Vec& b);
+Vec upper_t_solve(const Mat& R, const Vec& b);
+}  // namespace
+static bool rinv_probe();
+
 // ------------------------------------------------------------- LsFactor (solvers.cpp:24-78)
 LsFactor::LsFactor(const Mat& K, double rank_tol) : rows_(K.r), cols_(K.c) {
   if (rows_ < cols_) throw std::invalid_argument("LsFactor: matrix must be square or tall");
@@ -299,6 +306,15 @@ LsFactor::LsFactor(const Mat& K, double rank_tol) : rows_(K.r), cols_(K.c) {
   for (int j = 0; j < cols_; ++j)
     for (int i = 0; i <= j; ++i) R_(i, j) = qr.qr(i, j);
   Q_ = qr.thinQ();
+  if (rinv_probe()) {
+    Rinv_ = Mat(cols_, cols_);
+    for (int c = 0; c < cols_; ++c) {
+      Vec e(cols_, 0.0);
+      e[c] = 1.0;
+      Vec x = upper_solve(R_, e);
+      std::copy(x.begin(), x.end(), Rinv_.col(c));
+    }
+  }
 }
 
 namespace {
@@ -325,13 +341,22 @@ Vec upper_t_solve(const Mat& R, const Vec& b) {  // R^T x = b
 }
 }  // namespace
 
+// Oracle-spread probe (test infrastructure): DDO_RINV=1 applies an explicit R^{-1} in the
+// full-rank branch (as the device path does) instead of triangular solves.
+static bool rinv_probe() {
+  static const bool on = std::getenv("DDO_RINV") != nullptr;
+  return on;
+}
+
 Vec LsFactor::apply_pinv(const Vec& v) const {
   if (deficient_) return gemv(pinv_, v);
+  if (rinv_probe()) return gemv(Rinv_, gemv_t(Q_, v));
   return upper_solve(R_, gemv_t(Q_, v));
 }
 
 Vec LsFactor::apply_pinv_transpose(const Vec& v) const {
   if (deficient_) return gemv_t(pinv_, v);
+  if (rinv_probe()) return gemv(Q_, gemv_t(Rinv_, v));
   return gemv(Q_, upper_t_solve(R_, v));
 }
 

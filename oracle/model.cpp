@@ -1,6 +1,9 @@
 // ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp).
 // Restates proj/src/geometry.cpp, features.cpp, problems.cpp (Poisson rows), assembly.cpp.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
 #include <cmath>
 #include <map>
 #include <numbers>
@@ -197,6 +200,32 @@ double scale_from_constant(double c, int M, const Box& box, double r) {  // feat
   return c * std::sqrt(static_cast<double>(M)) / e.diam();
 }
 
+namespace {
+// Oracle-spread probe (test infrastructure): DDO_PERTURB=<seed> multiplies every feature
+// entry by (1 + k eps), k in {-1, 0, 1} hashed from (seed, j, point, order). Measures how far
+// a 1-ulp difference in the tanh evaluation (GPU vs glibc) propagates to the solve.
+uint64_t perturb_seed() {
+  static const uint64_t s = [] {
+    const char* e = std::getenv("DDO_PERTURB");
+    return e ? static_cast<uint64_t>(std::strtoull(e, nullptr, 10)) : 0ull;
+  }();
+  return s;
+}
+double perturb(double v, uint64_t seed, int j, const Point& p, int order) {
+  uint64_t h = seed * 0x9E3779B97F4A7C15ull ^ (static_cast<uint64_t>(j) << 20) ^ static_cast<uint64_t>(order);
+  uint64_t xb, yb;
+  std::memcpy(&xb, &p.x, 8);
+  std::memcpy(&yb, &p.y, 8);
+  h ^= xb * 0xBF58476D1CE4E5B9ull;
+  h ^= yb * 0x94D049BB133111EBull;
+  h ^= h >> 31;
+  h *= 0xD6E8FEB86659FD93ull;
+  h ^= h >> 29;
+  const int k = static_cast<int>(h % 3) - 1;
+  return v * (1.0 + k * std::numeric_limits<double>::epsilon());
+}
+}  // namespace
+
 Mat eval_derivative_matrix(const FeatureLayer& L, const std::vector<Point>& pts, int dx, int dy) {
   // features.cpp:42-76: sigma' = 1 - s^2, sigma'' = -2 s s1, sigma''' = -2 s1^2 - 2 s s2,
   // sigma'''' = -6 s1 s2 - 2 s s3; times w0^dx w1^dy.
@@ -227,7 +256,7 @@ Mat eval_derivative_matrix(const FeatureLayer& L, const std::vector<Point>& pts,
         }
         v *= wfac;
       }
-      out(k, j) = v;
+      out(k, j) = perturb_seed() ? perturb(v, perturb_seed(), j, pts[k], order * 8 + dx) : v;
     }
   }
   return out;

@@ -260,7 +260,7 @@ class LsFactor {
  private:
   int rows_ = 0, cols_ = 0, rank_ = 0;
   bool deficient_ = false;
-  Mat Q_, R_, K_, pinv_;
+  Mat Q_, R_, K_, pinv_, Rinv_;
 };
 
 struct LLT {

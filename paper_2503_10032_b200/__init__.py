@@ -1,0 +1,286 @@
+"""B200-native DDELM-NN hot path (arXiv 2503.10032): Python mirror of the reference solver API.
+
+The reference's C++ surface (proj/include/ddelm/solvers.hpp) is
+
+    Workspace(problem, s, n_grid, M, l, seed, SolverOptions)   solvers.hpp:79-80
+    ddelm_cs_solve(ws, CgOptions) / ddelm_nn_solve(ws, theta, CgOptions)   solvers.hpp:178-181
+    SolveReport{coeffs, mu, mu_delta, mu_pi, iterations, converged, residual_history, ...}
+
+and this module exposes the same names over the C-ABI library libddelm_gpu.so
+(include/ddelm_gpu.h). Errors follow the reference: std::invalid_argument -> ValueError,
+std::runtime_error -> RuntimeError. There is no CPU fallback: without the built library or a
+CUDA device every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .configs import CONFIGS  # noqa: F401
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libddelm_gpu.so")
+
+PROBLEMS = {"poisson_sinpi": 0, "poisson_sin2pi_exp": 1, "poisson_sin2pi_cos3pi_x2y": 2}
+METHODS = {"ddelm": 0, "ddelm-cs": 1, "ddelm-nn": 2}
+
+DDELM_OK, DDELM_ERR_INVALID_ARGUMENT, DDELM_ERR_RUNTIME, DDELM_ERR_CUDA, DDELM_ERR_CAPACITY = range(5)
+
+# every symbol declared in include/ddelm_gpu.h
+EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "ddelm_gpu_build",
+           "ddelm_gpu_build_coarse", "ddelm_gpu_build_neumann", "ddelm_gpu_solve",
+           "ddelm_gpu_reseed", "ddelm_gpu_destroy", "ddelm_gpu_get_mu", "ddelm_gpu_get_coeffs",
+           "ddelm_gpu_get_residuals", "ddelm_gpu_get_ranks", "ddelm_gpu_get_layer",
+           "ddelm_gpu_get_local", "ddelm_gpu_apply_operator", "ddelm_gpu_get_phase_ms",
+           "ddelm_gpu_get_launch_count")
+
+
+class _Desc(C.Structure):
+    _fields_ = [("problem", C.c_int), ("s", C.c_int), ("n_grid", C.c_int), ("M", C.c_int),
+                ("l", C.c_double), ("seed", C.c_uint64), ("flux_variant", C.c_int),
+                ("change_of_variables", C.c_int), ("rank_tol", C.c_double), ("device", C.c_int),
+                ("debug_flip_flux_row", C.c_int)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("negative_curvature", C.c_int),
+                ("n_delta", C.c_int), ("n_pi", C.c_int), ("n_mu", C.c_int),
+                ("n_subdomains", C.c_int), ("M", C.c_int),
+                ("assembly_seconds", C.c_double), ("factorization_seconds", C.c_double),
+                ("setup_seconds", C.c_double), ("cg_seconds", C.c_double),
+                ("reconstruct_seconds", C.c_double), ("total_seconds", C.c_double)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the C-ABI library (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `make -C paper_2503_10032_b200/csrc` "
+                          "(the DDELM-NN path has no CPU fallback)")
+    L = C.CDLL(path)
+    L.ddelm_gpu_last_error.restype = C.c_char_p
+    L.ddelm_gpu_version.restype = C.c_char_p
+    L.ddelm_gpu_create.argtypes = [C.POINTER(_Desc), C.POINTER(C.c_void_p)]
+    for fn in ("ddelm_gpu_build", "ddelm_gpu_build_coarse", "ddelm_gpu_build_neumann"):
+        getattr(L, fn).argtypes = [C.c_void_p]
+    L.ddelm_gpu_solve.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int,
+                                  C.POINTER(_Report)]
+    L.ddelm_gpu_reseed.argtypes = [C.c_void_p, C.c_uint64]
+    L.ddelm_gpu_destroy.argtypes = [C.c_void_p]
+    L.ddelm_gpu_get_mu.argtypes = [C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_get_coeffs.argtypes = [C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_get_residuals.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+    L.ddelm_gpu_get_ranks.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_get_layer.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_get_local.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int)]
+    L.ddelm_gpu_apply_operator.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_get_phase_ms.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+    L.ddelm_gpu_get_launch_count.argtypes = [C.c_void_p]
+    L.ddelm_gpu_get_launch_count.restype = C.c_longlong
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc == DDELM_OK:
+        return
+    msg = load_library().ddelm_gpu_last_error().decode()
+    if rc == DDELM_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    raise RuntimeError(f"[ddelm_gpu rc={rc}] {msg}")
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+@dataclass
+class ProblemSpec:
+    """make_problem (problems.cpp:132-188) — Poisson problems on the device path."""
+    name: str
+
+    def __post_init__(self):
+        if self.name not in PROBLEMS:
+            raise ValueError(f"make_problem: unknown problem '{self.name}'")
+
+
+def make_problem(name: str) -> ProblemSpec:
+    return ProblemSpec(name)
+
+
+@dataclass
+class SolverOptions:
+    """SolverOptions (solvers.hpp:49-58)."""
+    flux_variant: str = "pointwise"      # pointwise | mean_edge
+    change_of_variables: bool = False
+    rank_tol: float = 1e-10
+    workers: int = 1                     # accepted for API parity; the device batches subdomains
+    debug_flip_flux_row: int = -1
+
+
+@dataclass
+class CgOptions:
+    """CgOptions (solvers.hpp:173-176)."""
+    rel_tol: float = 1e-9
+    max_iter: int = 0
+
+
+@dataclass
+class SolveReport:
+    """SolveReport (solvers.hpp:162-171)."""
+    coeffs: np.ndarray
+    mu: np.ndarray
+    mu_delta: np.ndarray
+    mu_pi: np.ndarray
+    iterations: int
+    converged: bool
+    negative_curvature: bool
+    residual_history: np.ndarray
+    setup_seconds: float = 0.0
+    cg_seconds: float = 0.0
+    reconstruct_seconds: float = 0.0
+    assembly_seconds: float = 0.0
+    factorization_seconds: float = 0.0
+    total_seconds: float = 0.0
+    phase_ms: dict = field(default_factory=dict)
+    launches: int = 0
+
+
+class Workspace:
+    """Device-resident Workspace (solvers.hpp:78-160) on one B200."""
+
+    def __init__(self, problem: ProblemSpec | str, s: int, n_grid: int, M: int, l: float, seed: int,
+                 opts: SolverOptions | None = None, device: int = 0):
+        L = load_library()
+        if isinstance(problem, str):
+            problem = make_problem(problem)
+        opts = opts or SolverOptions()
+        if opts.flux_variant not in ("pointwise", "mean_edge"):
+            raise ValueError("flux_variant must be pointwise or mean_edge")
+        d = _Desc(PROBLEMS[problem.name], s, n_grid, M, float(l), seed,
+                  1 if opts.flux_variant == "mean_edge" else 0, 1 if opts.change_of_variables else 0,
+                  float(opts.rank_tol), device, int(opts.debug_flip_flux_row))
+        h = C.c_void_p()
+        _check(L.ddelm_gpu_create(C.byref(d), C.byref(h)))
+        self._h = h
+        self.problem, self.s, self.n_grid, self.M, self.l, self.seed = problem, s, n_grid, M, l, seed
+        self.opts = opts
+        self.n_subs = s * s
+        self.n_delta = 2 * s * (s - 1) * (n_grid - 2)
+        self.n_pi = (s - 1) * (s - 1)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            load_library().ddelm_gpu_destroy(h)
+            self._h = None
+
+    # reference lazily builds layers; these mirror the member functions
+    def build(self):
+        _check(load_library().ddelm_gpu_build(self._h))
+
+    def assemble_coarse(self):
+        _check(load_library().ddelm_gpu_build_coarse(self._h))
+
+    def build_neumann(self):
+        _check(load_library().ddelm_gpu_build_neumann(self._h))
+
+    def reseed(self, seed: int):
+        _check(load_library().ddelm_gpu_reseed(self._h, seed))
+        self.seed = seed
+
+    def ranks(self):
+        N = self.n_subs
+        rk, rkb = np.zeros(N, np.int32), np.zeros(N, np.int32)
+        ratio = np.zeros(2 * N)
+        _check(load_library().ddelm_gpu_get_ranks(self._h, _ptr(rk), _ptr(rkb), _ptr(ratio)))
+        return rk, rkb, ratio.reshape(N, 2)
+
+    def layer(self, i: int):
+        w0, w1, b = np.zeros(self.M), np.zeros(self.M), np.zeros(self.M)
+        _check(load_library().ddelm_gpu_get_layer(self._h, i, _ptr(w0), _ptr(w1), _ptr(b)))
+        return w0, w1, b
+
+    def local_matrix(self, i: int, which: int = 0) -> np.ndarray:
+        """K_i (which=0) or Kbar_i (which=1) as built by the feature kernel (rows x M)."""
+        rows = C.c_int()
+        _check(load_library().ddelm_gpu_get_local(self._h, i, which, None, C.byref(rows)))
+        K = np.zeros((self.M, rows.value))
+        _check(load_library().ddelm_gpu_get_local(self._h, i, which, _ptr(K), C.byref(rows)))
+        return K.T.copy()
+
+    def apply_operator(self, v: np.ndarray, theta: float = 0.999) -> np.ndarray:
+        """cs_reduced_apply with the NN weight (theta = 0: coarse operator), on the device."""
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.zeros_like(v)
+        _check(load_library().ddelm_gpu_apply_operator(self._h, float(theta), _ptr(v), _ptr(out)))
+        return out
+
+    def _solve(self, method: str, theta: float, cg: CgOptions | None) -> SolveReport:
+        cg = cg or CgOptions()
+        L = load_library()
+        rep = _Report()
+        _check(L.ddelm_gpu_solve(self._h, METHODS[method], float(theta), float(cg.rel_tol),
+                                 int(cg.max_iter), C.byref(rep)))
+        nmu = rep.n_mu
+        mu = np.zeros(nmu)
+        _check(L.ddelm_gpu_get_mu(self._h, _ptr(mu)))
+        co = np.zeros((rep.n_subdomains, rep.M))
+        _check(L.ddelm_gpu_get_coeffs(self._h, _ptr(co)))
+        hist = np.zeros(max(rep.iterations, 1))
+        n = L.ddelm_gpu_get_residuals(self._h, _ptr(hist), hist.size)
+        ms = np.zeros(8)
+        L.ddelm_gpu_get_phase_ms(self._h, _ptr(ms), 8)
+        names = ["features", "qr", "cod", "coarse", "neumann", "rhs", "cg", "reconstruct"]
+        return SolveReport(coeffs=co, mu=mu, mu_delta=mu[:rep.n_delta], mu_pi=mu[rep.n_delta:],
+                           iterations=rep.iterations, converged=bool(rep.converged),
+                           negative_curvature=bool(rep.negative_curvature),
+                           residual_history=hist[:max(n, 0)],
+                           setup_seconds=rep.setup_seconds, cg_seconds=rep.cg_seconds,
+                           reconstruct_seconds=rep.reconstruct_seconds,
+                           assembly_seconds=rep.assembly_seconds,
+                           factorization_seconds=rep.factorization_seconds,
+                           total_seconds=rep.total_seconds,
+                           phase_ms=dict(zip(names, ms.tolist())),
+                           launches=int(L.ddelm_gpu_get_launch_count(self._h)))
+
+
+def ddelm_cs_solve(ws: Workspace, cg: CgOptions | None = None) -> SolveReport:
+    """ddelm_cs_solve (solvers.cpp:582-588)."""
+    return ws._solve("ddelm-cs", 0.0, cg)
+
+
+def ddelm_nn_solve(ws: Workspace, theta: float, cg: CgOptions | None = None) -> SolveReport:
+    """ddelm_nn_solve (solvers.cpp:590-605): theta in [0, 1]; theta == 0 is exactly CS."""
+    if theta < 0.0 or theta > 1.0:
+        raise ValueError("ddelm_nn_solve: theta must lie in [0, 1]")
+    return ws._solve("ddelm-nn", theta, cg)
+
+
+def ddelm_solve(ws: Workspace, cg: CgOptions | None = None) -> SolveReport:
+    """One-level DDELM (solvers.cpp:493-531) — SURVEY.md §8f 'next'; not on the device path yet."""
+    raise NotImplementedError("ddelm (one-level) is a §8f 'next' row; use ddelm_cs_solve / ddelm_nn_solve")
+
+
+def workspace_from_config(name_or_cfg, device: int = 0) -> Workspace:
+    cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
+    opts = SolverOptions(flux_variant=cfg["flux_variant"],
+                         change_of_variables=cfg["trace_basis"] == "change_of_variables")
+    return Workspace(cfg["problem"], cfg["s"], cfg["n_grid"], cfg["M"], cfg["l"], cfg["seed"], opts, device)
+
+
+def solve_config(name_or_cfg, device: int = 0, ws: Workspace | None = None) -> tuple[Workspace, SolveReport]:
+    cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
+    ws = ws or workspace_from_config(cfg, device)
+    cg = CgOptions(rel_tol=cfg["cg_rel_tol"])
+    if cfg["method"] == "ddelm-cs":
+        return ws, ddelm_cs_solve(ws, cg)
+    return ws, ddelm_nn_solve(ws, cfg["theta"], cg)

@@ -1,0 +1,26 @@
+"""Named workloads (BASELINE.json configs C1-C4 mapped onto the reference's RunConfig keys,
+runner.hpp:14-35) plus small full-rank cases used for tight parity.
+
+Mapping decisions: n_grid = N + 2 (N interior points and N interface points per
+edge), biases follow the reference init b = -w.xi (features.cpp:23-33), method ddelm-nn with the
+coarse-method defaults mean_edge + change_of_variables (runner.cpp:114-116), theta 0.999,
+cg_rel_tol 1e-9, seed 1.
+"""
+
+_BASE = dict(problem="poisson_sinpi", seed=1, method="ddelm-nn", theta=0.999,
+             flux_variant="mean_edge", trace_basis="change_of_variables", cg_rel_tol=1e-9)
+
+CONFIGS = {
+    # BASELINE.json configs (rank-deficient local matrices: COD branch)
+    "C1": dict(_BASE, s=2, M=200, l=1.0, n_grid=22),
+    "C2": dict(_BASE, s=4, M=400, l=2.0, n_grid=32),
+    "C3": dict(_BASE, s=8, M=800, l=3.0, n_grid=42),
+    "C4": dict(_BASE, problem="poisson_sin2pi_cos3pi_x2y", s=16, M=1000, l=4.0, n_grid=52),
+    # full-rank local matrices (Householder-QR branch); the first is the reference's own
+    # tiny_workspace (test_solvers.cpp:27-29) with the coarse-method defaults
+    "T1": dict(_BASE, s=2, M=64, l=8.0, n_grid=10),
+    "T2": dict(_BASE, s=4, M=64, l=10.0, n_grid=12),
+    "T3": dict(_BASE, s=8, M=48, l=12.0, n_grid=10),
+    "T4": dict(_BASE, s=3, M=100, l=20.0, n_grid=16),
+    "T1cs": dict(_BASE, s=2, M=64, l=8.0, n_grid=10, method="ddelm-cs"),
+}

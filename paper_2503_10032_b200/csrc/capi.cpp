@@ -1,0 +1,165 @@
+// C-ABI boundary (include/ddelm_gpu.h) over the device workspace. No CPU fallback: every entry
+// point fails with DDELM_ERR_CUDA when no CUDA device is usable.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/ddelm_gpu.h"
+#include "common.cuh"
+#include "plan.hpp"
+#include "workspace.hpp"
+
+struct ddelm_ws {
+  ddg::Workspace* w = nullptr;
+  ddelm_report last{};
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return DDELM_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return DDELM_ERR_INVALID_ARGUMENT;
+  } catch (const ddg::CapacityError& e) {
+    g_err = e.what();
+    return DDELM_ERR_CAPACITY;
+  } catch (const ddg::CudaError& e) {
+    g_err = e.what();
+    return DDELM_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DDELM_ERR_RUNTIME;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ddelm_gpu_last_error(void) { return g_err.c_str(); }
+const char* ddelm_gpu_version(void) { return "ddelm-b200 0.1 (sm_100a)"; }
+
+int ddelm_gpu_create(const ddelm_desc* d, ddelm_ws** out) {
+  return guarded([&] {
+    if (!d || !out) throw std::invalid_argument("ddelm_gpu_create: null argument");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw ddg::CudaError("ddelm_gpu_create: no CUDA device available (no CPU fallback)");
+    if (d->device < 0 || d->device >= ndev) throw std::invalid_argument("ddelm_gpu_create: bad device ordinal");
+    ddg::Plan p = ddg::build_plan(d->problem, d->s, d->n_grid, d->M, d->l, d->seed, d->flux_variant,
+                                  d->change_of_variables != 0, d->rank_tol > 0 ? d->rank_tol : 1e-10,
+                                  d->debug_flip_flux_row);
+    auto* h = new ddelm_ws;
+    try {
+      h->w = new ddg::Workspace(p, d->device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void ddelm_gpu_destroy(ddelm_ws* ws) {
+  if (!ws) return;
+  delete ws->w;
+  delete ws;
+}
+
+int ddelm_gpu_build(ddelm_ws* ws) {
+  return guarded([&] { ws->w->build(); });
+}
+int ddelm_gpu_build_coarse(ddelm_ws* ws) {
+  return guarded([&] { ws->w->build_coarse(); });
+}
+int ddelm_gpu_build_neumann(ddelm_ws* ws) {
+  return guarded([&] { ws->w->build_neumann(); });
+}
+
+int ddelm_gpu_reseed(ddelm_ws* ws, uint64_t seed) {
+  return guarded([&] { ws->w->reseed(seed); });
+}
+
+int ddelm_gpu_solve(ddelm_ws* ws, int method, double theta, double rel_tol, int max_iter,
+                    ddelm_report* rep) {
+  return guarded([&] {
+    ddg::SolveResult r = ws->w->solve(method, theta, rel_tol, max_iter);
+    ddelm_report o{};
+    const ddg::Plan& p = ws->w->plan;
+    o.iterations = r.iterations;
+    o.converged = r.converged ? 1 : 0;
+    o.negative_curvature = r.negative_curvature ? 1 : 0;
+    o.n_delta = p.n_delta;
+    o.n_pi = p.n_pi;
+    o.n_mu = p.n_delta + p.n_pi;
+    o.n_subdomains = p.N;
+    o.M = p.M;
+    o.assembly_seconds = r.phase_ms[0] / 1e3;
+    o.factorization_seconds = (r.phase_ms[1] + r.phase_ms[2]) / 1e3;
+    o.setup_seconds = (r.phase_ms[3] + r.phase_ms[4] + r.phase_ms[5]) / 1e3;
+    o.cg_seconds = r.phase_ms[6] / 1e3;
+    o.reconstruct_seconds = r.phase_ms[7] / 1e3;
+    o.total_seconds = r.host_ms / 1e3;
+    ws->last = o;
+    if (rep) *rep = o;
+  });
+}
+
+int ddelm_gpu_get_mu(ddelm_ws* ws, double* mu) {
+  return guarded([&] { ws->w->get_mu(mu); });
+}
+int ddelm_gpu_get_coeffs(ddelm_ws* ws, double* c) {
+  return guarded([&] { ws->w->get_coeffs(c); });
+}
+int ddelm_gpu_get_residuals(ddelm_ws* ws, double* h, int cap) {
+  int n = 0;
+  const int rc = guarded([&] { n = ws->w->get_residuals(h, cap); });
+  return rc == DDELM_OK ? n : -rc;
+}
+int ddelm_gpu_get_ranks(ddelm_ws* ws, int* rk, int* rkb, double* ratio) {
+  return guarded([&] { ws->w->get_ranks(rk, rkb, ratio); });
+}
+int ddelm_gpu_get_layer(ddelm_ws* ws, int i, double* w0, double* w1, double* b) {
+  return guarded([&] {
+    const ddg::Plan& p = ws->w->plan;
+    if (i < 0 || i >= p.N) throw std::invalid_argument("ddelm_gpu_get_layer: bad subdomain");
+    std::vector<double> a(p.M), c(p.M), e(p.M);
+    ddg::init_layer(p, i, a.data(), c.data(), e.data());
+    std::memcpy(w0, a.data(), sizeof(double) * p.M);
+    std::memcpy(w1, c.data(), sizeof(double) * p.M);
+    std::memcpy(b, e.data(), sizeof(double) * p.M);
+  });
+}
+int ddelm_gpu_get_local(ddelm_ws* ws, int i, int which, double* K, int* rows) {
+  return guarded([&] {
+    const ddg::Plan& p = ws->w->plan;
+    if (i < 0 || i >= p.N) throw std::invalid_argument("ddelm_gpu_get_local: bad subdomain");
+    if (rows) *rows = p.m;
+    if (K) ws->w->get_local(i, which, K);
+  });
+}
+int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double* out) {
+  return guarded([&] {
+    if (theta < 0.0 || theta > 1.0) throw std::invalid_argument("theta must lie in [0, 1]");
+    ws->w->apply_operator(theta, v, out);
+  });
+}
+int ddelm_gpu_get_phase_ms(ddelm_ws* ws, double* ms, int cap) {
+  const double* src = ws->w->phase_ms();
+  const int n = cap < 8 ? cap : 8;
+  for (int k = 0; k < n; ++k) ms[k] = src[k];
+  return n;
+}
+long long ddelm_gpu_get_launch_count(ddelm_ws* ws) { return ws->w->launches(); }
+
+}  // extern "C"

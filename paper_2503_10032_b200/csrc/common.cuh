@@ -1,0 +1,69 @@
+// Shared device helpers for the sm_100a DDELM kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace ddg {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define DDG_CUDA(call)                                                                      \
+  do {                                                                                      \
+    cudaError_t err__ = (call);                                                             \
+    if (err__ != cudaSuccess)                                                               \
+      throw ::ddg::CudaError(std::string(#call) + ": " + cudaGetErrorString(err__) + " @" + \
+                             __FILE__ + ":" + std::to_string(__LINE__));                    \
+  } while (0)
+
+#define DDG_LAUNCH_CHECK() DDG_CUDA(cudaGetLastError())
+
+#ifdef __CUDACC__
+// ------------------------------------------------------------------ reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+/// Block-wide sum (result broadcast to all threads). `sh` needs >= 32 doubles.
+/// Deterministic: fixed warp order.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0;
+  if (wid == 0) {
+    t = lane < nw ? sh[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sh[0] = t;
+  }
+  __syncthreads();
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ FP64 tensor core (DMMA)
+// mma.sync m8n8k4 f64 (SASS DMMA.8). Fragment layout (PTX ISA, m8n8k4 .f64):
+//   A 8x4 row-major:  a  = A[lane >> 2][lane & 3]
+//   B 4x8 col-major:  b  = B[lane & 3][lane >> 2]
+//   C/D 8x8:          c0 = C[lane >> 2][2 * (lane & 3)], c1 = C[lane >> 2][2 * (lane & 3) + 1]
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+#endif  // __CUDACC__
+
+inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace ddg

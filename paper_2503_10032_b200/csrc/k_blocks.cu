@@ -1,0 +1,284 @@
+// Interface-level blocks and the coarse problem (sm_100a, fp64).
+//
+// With K^+ = C Q_r^T (k_cod.cu), every operator the interface iteration applies reduces to
+// small dense per-subdomain blocks (SURVEY.md §8d representation (ii)/(iii)):
+//   FC   = F C         (nF x r)   flux rows of K^+:   F K^+ = FC Q_r^T
+//   CCb  = Cdelta Cbar (nd x r~)  Neumann-to-Dirichlet: Cdelta Kbar^+ = CCb Qbar_r^T
+//   Zc   = Q_G FC^T w  (per cross-flux row): the Dpp / Dpd rows of assemble_coarse
+//   Gc   = -Q_Pi Q_Pi^T           the Gpi rows entering S_Pi
+// Reference: assemble_coarse (solvers.cpp:278-326), build_neumann Cdelta (solvers.cpp:436-438).
+// The coarse Schur matrix S_Pi is assembled and inverted (Cholesky) on one CTA; its inverse is
+// applied as a GEMV twice per interface iteration.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace ddg {
+
+namespace {
+
+/// out[l][k] = sum_j X[j*ldx + l] * Cm[j*R + k]   for l < rows, k < r   (batched; DFMA tiles)
+__global__ void __launch_bounds__(256) jmajor_gemm_kernel(int M, int R, const double* X, int ldx,
+                                                          size_t xstride, const int* rows_of, int rows_cls,
+                                                          const ClassDims* dims, const int* sub_cls,
+                                                          const double* Cm, size_t cstride,
+                                                          const int* rank, int rank_off,
+                                                          double* out, int ldo, size_t ostride) {
+  const int i = blockIdx.z;
+  const ClassDims d = dims[sub_cls[i]];
+  const int rows = rows_cls == 0 ? d.nF : d.nd;
+  (void)rows_of;
+  const int r = rank[rank_off + i];
+  const int l0 = blockIdx.x * 64, k0 = blockIdx.y * 64;
+  double* o = out + i * ostride;
+  if (l0 >= rows || k0 >= R) return;
+  const double* Xi = X + i * xstride;
+  const double* Ci = Cm + (rank_off + i) * cstride;
+  __shared__ double Xs[16][64];
+  __shared__ double Cs[16][64];
+  const int tl = (threadIdx.x & 15) * 4, tk = (threadIdx.x >> 4) * 4;
+  double acc[4][4] = {};
+  for (int j0 = 0; j0 < M; j0 += 16) {
+    for (int idx = threadIdx.x; idx < 16 * 64; idx += 256) {
+      const int jj = idx / 64, c = idx % 64;
+      const int j = j0 + jj;
+      Xs[jj][c] = (j < M && l0 + c < rows) ? Xi[static_cast<size_t>(j) * ldx + l0 + c] : 0.0;
+      Cs[jj][c] = (j < M && k0 + c < r) ? Ci[static_cast<size_t>(j) * R + k0 + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      double xv[4], cv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        xv[q] = Xs[jj][tl + q];
+        cv[q] = Cs[jj][tk + q];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(xv[p], cv[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int l = l0 + tl + p, k = k0 + tk + q;
+      if (l < rows && k < R) o[static_cast<size_t>(l) * ldo + k] = (k < r) ? acc[p][q] : 0.0;
+    }
+}
+
+/// Per subdomain: Zc rows, flux data pd of F K^+ f, corner Gram Gc (solvers.cpp:286-313).
+__global__ void __launch_bounds__(256) coarse_local_kernel(BlockArgs a, const int* cr_row,
+                                                           const int* cr_off, const int* cr_l,
+                                                           const double* cr_w) {
+  const int i = blockIdx.x;
+  const ClassDims d = a.dims[a.sub_cls[i]];
+  const int r = a.rank[i];
+  const int R = a.rmax, E = a.ext;
+  const double* QtX = a.QtX + static_cast<size_t>(i) * R * E;  // QGt(k, g) = QtX[k*E + 1 + g]
+  const double* FC = a.FC + static_cast<size_t>(i) * a.fmax * R;
+  extern __shared__ double sm[];
+  double* u = sm;                  // r
+  double* vals = u + R;            // nF: FC qf
+  __shared__ int cq[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int g = 0; g < d.n_gamma; ++g)
+      if (a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] >= 0 && n < 4) cq[n++] = g;
+    for (; n < 4; ++n) cq[n] = -1;
+  }
+  // vals = FC qf  (F K^+ f, the data of the flux rows)
+  for (int l = warp; l < d.nF; l += nwarp) {
+    double s = 0;
+    for (int k = lane; k < r; k += 32) s += FC[static_cast<size_t>(l) * R + k] * QtX[static_cast<size_t>(k) * E];
+    s = warp_sum(s);
+    if (lane == 0) vals[l] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) a.corner_q[i * 4 + threadIdx.x] = cq[threadIdx.x];
+  const int* off = cr_off + static_cast<size_t>(i) * (a.crmax + 1);
+  for (int rho = 0; rho < a.crmax; ++rho) {
+    const int row = cr_row[static_cast<size_t>(i) * a.crmax + rho];
+    double* z = a.Zc + (static_cast<size_t>(i) * a.crmax + rho) * a.gmax;
+    if (row < 0) {
+      for (int g = threadIdx.x; g < a.gmax; g += blockDim.x) z[g] = 0.0;
+      if (threadIdx.x == 0) a.pd[static_cast<size_t>(i) * a.crmax + rho] = 0.0;
+      continue;
+    }
+    // u = FC^T w  (entries in scatter order)
+    for (int k = threadIdx.x; k < r; k += blockDim.x) {
+      double s = 0;
+      for (int e = off[rho]; e < off[rho + 1]; ++e) s += cr_w[e] * FC[static_cast<size_t>(cr_l[e]) * R + k];
+      u[k] = s;
+    }
+    if (threadIdx.x == 0) {
+      double s = 0;
+      for (int e = off[rho]; e < off[rho + 1]; ++e) s += cr_w[e] * vals[cr_l[e]];
+      a.pd[static_cast<size_t>(i) * a.crmax + rho] = s;
+    }
+    __syncthreads();
+    // z = QGt^T u on all gamma points
+    for (int g = threadIdx.x; g < a.gmax; g += blockDim.x) {
+      double s = 0;
+      if (g < d.n_gamma)
+        for (int k = 0; k < r; ++k) s += QtX[static_cast<size_t>(k) * E + 1 + g] * u[k];
+      z[g] = s;
+    }
+    __syncthreads();
+  }
+  // Gc = -(Q_Pi Q_Pi^T) over the corners
+  if (threadIdx.x < 16) {
+    const int p = threadIdx.x / 4, q = threadIdx.x % 4;
+    double s = 0;
+    if (cq[p] >= 0 && cq[q] >= 0)
+      for (int k = 0; k < r; ++k)
+        s += QtX[static_cast<size_t>(k) * E + 1 + cq[p]] * QtX[static_cast<size_t>(k) * E + 1 + cq[q]];
+    a.Gc[static_cast<size_t>(i) * 16 + threadIdx.x] = -s;
+  }
+}
+
+/// Dpp rows and dpi from per-subdomain contributions, in subdomain order (one CTA per row).
+__global__ void coarse_rows_kernel(BlockArgs a, const int* row_owner /* npf x 4 : i*crmax+rho */) {
+  const int rrow = blockIdx.x;
+  double* drow = a.Dpp + static_cast<size_t>(rrow) * a.n_pi;
+  for (int c = threadIdx.x; c < a.n_pi; c += blockDim.x) drow[c] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int q = 0; q < 4; ++q) {
+      const int own = row_owner[rrow * 4 + q];
+      if (own < 0) continue;
+      const int i = own / a.crmax, rho = own % a.crmax;
+      s += a.pd[own];
+      const double* z = a.Zc + (static_cast<size_t>(i) * a.crmax + rho) * a.gmax;
+      for (int p = 0; p < 4; ++p) {
+        const int g = a.corner_q[i * 4 + p];
+        if (g < 0) continue;
+        const int gp = a.gamma_pi[static_cast<size_t>(i) * a.gmax + g];
+        drow[gp] += z[g];
+      }
+    }
+    // dpi = -(A K^+ f) on the cross rows (solvers.cpp:293-296), with the debug flip hook
+    const double sign = (a.flip_row == a.n_delta + rrow) ? -1.0 : 1.0;
+    a.dpi[rrow] = -(sign * s);
+  }
+}
+
+/// S = diag(mult) + Dpp^T Dpp + sum_i Gpi rows; symmetrise; Cholesky; S^{-1}. One CTA.
+__global__ void __launch_bounds__(1024) coarse_schur_kernel(BlockArgs a) {
+  const int n = a.n_pi, npf = a.npf;
+  double* S = a.S;
+  double* L = a.Sinv;  // scratch for L, overwritten by the inverse at the end
+  __shared__ int fail;
+  if (threadIdx.x == 0) fail = 0;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int p = idx / n, q = idx % n;
+    double s = 0;
+    for (int rr = 0; rr < npf; ++rr) s += a.Dpp[static_cast<size_t>(rr) * n + p] * a.Dpp[static_cast<size_t>(rr) * n + q];
+    S[idx] = (p == q ? static_cast<double>(a.mult_pi[p]) : 0.0) + s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.N; ++i)
+      for (int p = 0; p < 4; ++p) {
+        const int gp_ = a.corner_q[i * 4 + p];
+        if (gp_ < 0) continue;
+        const int rp = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gp_];
+        for (int q = 0; q < 4; ++q) {
+          const int gq_ = a.corner_q[i * 4 + q];
+          if (gq_ < 0) continue;
+          const int rq = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gq_];
+          S[static_cast<size_t>(rp) * n + rq] += a.Gc[static_cast<size_t>(i) * 16 + p * 4 + q];
+        }
+      }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int p = idx / n, q = idx % n;
+    L[idx] = 0.5 * (S[static_cast<size_t>(p) * n + q] + S[static_cast<size_t>(q) * n + p]);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) S[idx] = L[idx];
+  __syncthreads();
+  // right-looking Cholesky in L (lower triangle)
+  for (int k = 0; k < n; ++k) {
+    if (threadIdx.x == 0) {
+      const double dkk = L[static_cast<size_t>(k) * n + k];
+      if (!(dkk > 0)) fail = 1;
+      L[static_cast<size_t>(k) * n + k] = sqrt(fmax(dkk, DBL_MIN));
+    }
+    __syncthreads();
+    const double dk = L[static_cast<size_t>(k) * n + k];
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) L[static_cast<size_t>(i) * n + k] /= dk;
+    __syncthreads();
+    const int rem = n - k - 1;
+    for (int idx = threadIdx.x; idx < rem * rem; idx += blockDim.x) {
+      const int i = k + 1 + idx / rem, j = k + 1 + idx % rem;
+      if (j <= i) L[static_cast<size_t>(i) * n + j] -= L[static_cast<size_t>(i) * n + k] * L[static_cast<size_t>(j) * n + k];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && fail) *a.spd_fail = 1;
+  // Linv (upper part of S scratch is free after the copy): column c of L^{-1} by forward subst.
+  double* Li = S;  // reuse S storage for L^{-1} (S itself is not needed after factorisation)
+  __syncthreads();
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    for (int i = 0; i < n; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      if (i < c) { Li[static_cast<size_t>(i) * n + c] = 0.0; continue; }
+      for (int u = c; u < i; ++u) s -= L[static_cast<size_t>(i) * n + u] * Li[static_cast<size_t>(u) * n + c];
+      Li[static_cast<size_t>(i) * n + c] = s / L[static_cast<size_t>(i) * n + i];
+    }
+  }
+  __syncthreads();
+  // S^{-1} = L^{-T} L^{-1}
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int p = idx / n, q = idx % n;
+    double s = 0;
+    for (int u = max(p, q); u < n; ++u) s += Li[static_cast<size_t>(u) * n + p] * Li[static_cast<size_t>(u) * n + q];
+    L[idx] = s;
+  }
+}
+
+}  // namespace
+
+void launch_blocks(const BlockArgs& a, bool neumann, cudaStream_t st) {
+  const size_t xs_f = static_cast<size_t>(a.M) * a.ldF, xs_c = static_cast<size_t>(a.M) * a.ldC;
+  const size_t cs = static_cast<size_t>(a.M) * a.rmax;
+  if (!neumann) {
+    dim3 g(ceil_div(a.fmax, 64), ceil_div(a.rmax, 64), a.N);
+    jmajor_gemm_kernel<<<g, 256, 0, st>>>(a.M, a.rmax, a.F, a.ldF, xs_f, nullptr, 0, a.dims, a.sub_cls,
+                                          a.C, cs, a.rank, 0, a.FC, a.rmax,
+                                          static_cast<size_t>(a.fmax) * a.rmax);
+  } else {
+    dim3 g(ceil_div(a.dmax, 64), ceil_div(a.rmax, 64), a.N);
+    jmajor_gemm_kernel<<<g, 256, 0, st>>>(a.M, a.rmax, a.Cd, a.ldC, xs_c, nullptr, 1, a.dims, a.sub_cls,
+                                          a.C, cs, a.rank, a.N, a.CCb, a.rmax,
+                                          static_cast<size_t>(a.dmax) * a.rmax);
+  }
+  DDG_LAUNCH_CHECK();
+}
+
+void launch_coarse_local(const BlockArgs& a, const int* cr_row, const int* cr_off, const int* cr_l,
+                         const double* cr_w, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (a.rmax + a.fmax);
+  coarse_local_kernel<<<a.N, 256, smem, st>>>(a, cr_row, cr_off, cr_l, cr_w);
+  DDG_LAUNCH_CHECK();
+}
+
+void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t st) {
+  coarse_rows_kernel<<<a.npf, 128, 0, st>>>(a, row_owner);
+  DDG_LAUNCH_CHECK();
+}
+
+void launch_coarse_schur(const BlockArgs& a, cudaStream_t st) {
+  coarse_schur_kernel<<<1, 1024, 0, st>>>(a);
+  DDG_LAUNCH_CHECK();
+}
+
+}  // namespace ddg

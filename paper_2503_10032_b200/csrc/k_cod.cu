@@ -1,0 +1,415 @@
+// Rank-revealing branch of LsFactor on the device (sm_100a, fp64).
+//
+// Reference: solvers.cpp:32-41 — when the unpivoted R diagonal signals deficiency, Eigen's
+// CompleteOrthogonalDecomposition (column-pivoted Householder QR with max-norm pivoting,
+// first-index ties, LAPACK-style norm downdating with recomputation below sqrt(eps);
+// rank = #{|R_ii| > tol * max|R_ii|}; RZ of [R11 R12]) yields K^+ = P Z^T [T^{-1}; 0] Q_r^T.
+//
+// B200 design: column norms and pivots of K equal those of its R-factor R0 (K = Q0 R0), so the
+// pivoted factorisation runs on the M x M upper-triangular R0 produced by the batched QR,
+// never touching the m x M matrix again. It is blocked LAPACK-dlaqps style (no trailing
+// update: the updated matrix is A - V F^T, F accumulated one column per step), one CTA per
+// matrix, and stops as soon as every remaining column norm is below half the rank
+// threshold, i.e. after ~rank steps instead of M. Outputs, per matrix:
+//   C      = P Z^T [I_r; 0] T^{-1}   (M x r)      so that  K^+ = C Q_r^T
+//   QtX    = Q_r^T [f | E]           (r x ext)    (Q_r = Q0 Q1[:, :r])
+// The full-rank branch (solvers.cpp:43-44) is the same contract with r = M, C = R0^{-1}.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace ddg {
+
+namespace {
+
+struct ArgMax {
+  double v;
+  int i;
+};
+
+__device__ __forceinline__ ArgMax better(ArgMax a, ArgMax b) {
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+
+__device__ ArgMax block_argmax(ArgMax x, ArgMax* sh) {
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax y{__shfl_xor_sync(0xffffffffu, x.v, o), __shfl_xor_sync(0xffffffffu, x.i, o)};
+    x = better(x, y);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    ArgMax y = lane < nw ? sh[lane] : ArgMax{-1.0, 0x7fffffff};
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMax z{__shfl_xor_sync(0xffffffffu, y.v, o), __shfl_xor_sync(0xffffffffu, y.i, o)};
+      y = better(y, z);
+    }
+    if (lane == 0) sh[0] = y;
+  }
+  __syncthreads();
+  ArgMax r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) cod_pivqr_kernel(CodArgs a) {
+  const int t = blockIdx.x;
+  const int M = a.M, K = a.kmax;
+  const double mn = a.ratio[2 * t], mx = a.ratio[2 * t + 1];
+  const bool deficient = !(mx > 0) || mn < a.rank_tol * mx;  // solvers.cpp:32
+  if (threadIdx.x == 0) {
+    a.deficient[t] = deficient ? 1 : 0;
+    a.status[t] = 0;
+  }
+  if (!deficient) {
+    if (threadIdx.x == 0) a.rank[t] = M;
+    return;
+  }
+  const double* R0 = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
+  const size_t ld = a.ld;
+  double* V1 = a.V1 + static_cast<size_t>(t) * K * M;
+  double* F1 = a.F1 + static_cast<size_t>(t) * M * K;
+  double* Rr = a.Rr + static_cast<size_t>(t) * K * M;
+  double* tau1 = a.tau1 + static_cast<size_t>(t) * K;
+  double* upd = a.upd + static_cast<size_t>(t) * M;
+  double* dir = a.dir + static_cast<size_t>(t) * M;
+  int* perm = a.perm + static_cast<size_t>(t) * M;
+
+  extern __shared__ double sm[];
+  double* v = sm;            // M
+  double* w = v + M;         // K
+  double* vk = w + K;        // K  (row k of V)
+  __shared__ double red[32];
+  __shared__ ArgMax ared[32];
+  __shared__ double s_tau, s_maxpivot;
+  __shared__ int s_stop;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const double eps = DBL_EPSILON;
+  const double downdate_thr = sqrt(eps);
+
+  // initial column norms (of R0 = of K up to rounding)
+  for (int j = warp; j < M; j += nwarp) {
+    double s = 0;
+    for (int i = lane; i <= j; i += 32) {
+      const double e = R0[static_cast<size_t>(j) * ld + i];
+      s += e * e;
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      upd[j] = dir[j] = sqrt(s);
+      perm[j] = j;
+    }
+  }
+  if (threadIdx.x == 0) {
+    s_maxpivot = 0;
+    s_stop = 0;
+  }
+  __syncthreads();
+
+  int k = 0;
+  for (; k < M; ++k) {
+    // ---- pivot: largest updated norm, first index on ties
+    ArgMax best{-1.0, 0x7fffffff};
+    for (int j = k + threadIdx.x; j < M; j += blockDim.x) best = better(best, ArgMax{upd[j], j});
+    best = block_argmax(best, ared);
+    if (k > 0 && best.v < 0.5 * a.rank_tol * s_maxpivot) break;
+    if (k >= K) {
+      if (threadIdx.x == 0) a.status[t] = 1;
+      break;
+    }
+    const int p = best.i;
+    if (p != k) {
+      if (threadIdx.x == 0) {
+        double tmp = upd[k]; upd[k] = upd[p]; upd[p] = tmp;
+        tmp = dir[k]; dir[k] = dir[p]; dir[p] = tmp;
+        const int ti = perm[k]; perm[k] = perm[p]; perm[p] = ti;
+      }
+      for (int u = threadIdx.x; u < k; u += blockDim.x) {
+        double tmp = F1[static_cast<size_t>(k) * K + u];
+        F1[static_cast<size_t>(k) * K + u] = F1[static_cast<size_t>(p) * K + u];
+        F1[static_cast<size_t>(p) * K + u] = tmp;
+        tmp = Rr[static_cast<size_t>(u) * M + k];
+        Rr[static_cast<size_t>(u) * M + k] = Rr[static_cast<size_t>(u) * M + p];
+        Rr[static_cast<size_t>(u) * M + p] = tmp;
+      }
+    }
+    __syncthreads();
+    // ---- updated pivot column (rows k..M-1): R0(:, perm[k]) - V F(k, :)^T
+    const int ck = perm[k];
+    for (int u = threadIdx.x; u < k; u += blockDim.x) w[u] = F1[static_cast<size_t>(k) * K + u];
+    __syncthreads();
+    for (int i = k + threadIdx.x; i < M; i += blockDim.x) {
+      double s = (i <= ck) ? R0[static_cast<size_t>(ck) * ld + i] : 0.0;
+      for (int u = 0; u < k; ++u) s -= V1[static_cast<size_t>(u) * M + i] * w[u];
+      v[i] = s;
+    }
+    __syncthreads();
+    // ---- Householder (makeHouseholderInPlace)
+    double part = 0;
+    for (int i = k + 1 + threadIdx.x; i < M; i += blockDim.x) part += v[i] * v[i];
+    const double tail = block_sum(part, red);
+    const double alpha = v[k];
+    double tau = 0, beta = alpha, scale = 0;
+    const bool triv = !(tail > DBL_MIN);
+    if (!triv) {
+      beta = sqrt(alpha * alpha + tail);
+      if (alpha >= 0) beta = -beta;
+      scale = 1.0 / (alpha - beta);
+      tau = (beta - alpha) / beta;
+    }
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+      double e;
+      if (i < k) e = 0.0;
+      else if (i == k) e = 1.0;
+      else e = triv ? 0.0 : v[i] * scale;
+      if (i >= k) v[i] = e;
+      V1[static_cast<size_t>(k) * M + i] = e;
+    }
+    if (threadIdx.x == 0) {
+      Rr[static_cast<size_t>(k) * M + k] = beta;
+      tau1[k] = tau;
+      s_tau = tau;
+      s_maxpivot = fmax(s_maxpivot, fabs(beta));
+    }
+    __syncthreads();
+    // ---- w = V(:, 0:k)^T v ; vk = V(k, 0:k]
+    for (int u = warp; u < k; u += nwarp) {
+      double s = 0;
+      for (int i = k + lane; i < M; i += 32) s += V1[static_cast<size_t>(u) * M + i] * v[i];
+      s = warp_sum(s);
+      if (lane == 0) w[u] = s;
+    }
+    for (int u = threadIdx.x; u <= k; u += blockDim.x) vk[u] = V1[static_cast<size_t>(u) * M + k];
+    __syncthreads();
+    // ---- F(:, k) = tau (A^T v - F V^T v) for positions j > k   (one warp per column)
+    for (int j = k + 1 + warp; j < M; j += nwarp) {
+      const int cj = perm[j];
+      const double* col = R0 + static_cast<size_t>(cj) * ld;
+      double g = 0;
+      for (int i = k + lane; i <= cj && i < M; i += 32) g += col[i] * v[i];
+      double fw = 0;
+      for (int u = lane; u < k; u += 32) fw += F1[static_cast<size_t>(j) * K + u] * w[u];
+      g = warp_sum(g);
+      fw = warp_sum(fw);
+      if (lane == 0) F1[static_cast<size_t>(j) * K + k] = s_tau * (g - fw);
+    }
+    __syncthreads();
+    // ---- row k of R and norm downdating (thread per column)
+    for (int j = k + 1 + threadIdx.x; j < M; j += blockDim.x) {
+      const int cj = perm[j];
+      double rkj = (k <= cj) ? R0[static_cast<size_t>(cj) * ld + k] : 0.0;
+      for (int u = 0; u <= k; ++u) rkj -= vk[u] * F1[static_cast<size_t>(j) * K + u];
+      Rr[static_cast<size_t>(k) * M + j] = rkj;
+      if (upd[j] != 0.0) {
+        double tmp = fabs(rkj) / upd[j];
+        tmp = (1.0 + tmp) * (1.0 - tmp);
+        if (tmp < 0) tmp = 0;
+        const double ratio = upd[j] / dir[j];
+        const double tmp2 = tmp * ratio * ratio;
+        if (tmp2 <= downdate_thr) dir[j] = -1.0;  // flag: recompute exactly below
+        else upd[j] *= sqrt(tmp);
+      }
+    }
+    __syncthreads();
+    // ---- exact recomputation of flagged norms: ||(A - V F^T)(k+1:M, j)||
+    for (int j = k + 1 + warp; j < M; j += nwarp) {
+      if (dir[j] != -1.0) continue;
+      const int cj = perm[j];
+      const double* col = R0 + static_cast<size_t>(cj) * ld;
+      double s = 0;
+      for (int i = k + 1 + lane; i < M; i += 32) {
+        double e = (i <= cj) ? col[i] : 0.0;
+        for (int u = 0; u <= k; ++u) e -= V1[static_cast<size_t>(u) * M + i] * F1[static_cast<size_t>(j) * K + u];
+        s += e * e;
+      }
+      s = warp_sum(s);
+      if (lane == 0) upd[j] = dir[j] = sqrt(s);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double pre = s_maxpivot * a.rank_tol;
+    int r = 0;
+    for (int u = 0; u < k; ++u) r += fabs(Rr[static_cast<size_t>(u) * M + u]) > pre ? 1 : 0;
+    a.rank[t] = r;
+  }
+}
+
+/// RZ + C + Q^T X for a deficient matrix; C = R0^{-1}, Q^T X = X for a full-rank one.
+__global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
+  const int t = blockIdx.x;
+  const int M = a.M, K = a.kmax, R = a.rmax, E = a.ext;
+  const size_t ld = a.ld;
+  double* A = const_cast<double*>(a.A) + static_cast<size_t>(t) * a.ld * a.ncol;
+  double* C = a.C + static_cast<size_t>(t) * M * R;
+  double* QtX = a.QtX + static_cast<size_t>(t) * R * E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int r = a.rank[t];
+  if (a.status[t] != 0) return;
+  double* X = A + static_cast<size_t>(M) * ld;  // appended columns: X(i, e) = X[e*ld + i]
+
+  if (!a.deficient[t]) {
+    // full-rank branch: C = R0^{-1} (thread per column), QtX = top M rows of Q0^T [f E]
+    for (int c = threadIdx.x; c < M; c += blockDim.x) {
+      for (int i = M - 1; i >= 0; --i) {
+        double s = (i == c) ? 1.0 : 0.0;
+        if (i <= c) {
+          for (int u = i + 1; u <= c; ++u) s -= A[static_cast<size_t>(u) * ld + i] * C[static_cast<size_t>(u) * R + c];
+          s /= A[static_cast<size_t>(i) * ld + i];
+        } else {
+          s = 0.0;
+        }
+        C[static_cast<size_t>(i) * R + c] = s;
+      }
+    }
+    for (int idx = threadIdx.x; idx < M * E; idx += blockDim.x) {
+      const int i = idx / E, e = idx % E;
+      QtX[static_cast<size_t>(i) * E + e] = X[static_cast<size_t>(e) * ld + i];
+    }
+    return;
+  }
+
+  double* Rr = a.Rr + static_cast<size_t>(t) * K * M;
+  double* V1 = a.V1 + static_cast<size_t>(t) * K * M;
+  const double* tau1 = a.tau1 + static_cast<size_t>(t) * K;
+  const int* perm = a.perm + static_cast<size_t>(t) * M;
+  double* zc = a.zc + static_cast<size_t>(t) * K;
+  double* Y = a.Ywork + static_cast<size_t>(t) * M * R;  // Y(i, c) = Y[i*R + c]
+  __shared__ double red[32];
+  __shared__ double s_tau, s_beta, s_scale;
+
+  // ---- RZ (COD::compute): rows k = r-1 .. 0 of [R11 R12], columns {k} U {r..M-1}
+  if (r < M) {
+    for (int k = r - 1; k >= 0; --k) {
+      if (k != r - 1)
+        for (int u = threadIdx.x; u <= k; u += blockDim.x) {
+          const double tmp = Rr[static_cast<size_t>(u) * M + k];
+          Rr[static_cast<size_t>(u) * M + k] = Rr[static_cast<size_t>(u) * M + r - 1];
+          Rr[static_cast<size_t>(u) * M + r - 1] = tmp;
+        }
+      __syncthreads();
+      double* row = Rr + static_cast<size_t>(k) * M;
+      double part = 0;
+      for (int j = r + threadIdx.x; j < M; j += blockDim.x) part += row[j] * row[j];
+      const double tail = block_sum(part, red);
+      if (threadIdx.x == 0) {
+        const double c0 = row[r - 1];
+        double tau = 0, beta = c0, scale = 0;
+        if (tail > DBL_MIN) {
+          beta = sqrt(c0 * c0 + tail);
+          if (c0 >= 0) beta = -beta;
+          scale = 1.0 / (c0 - beta);
+          tau = (beta - c0) / beta;
+        }
+        s_tau = tau;
+        s_beta = beta;
+        s_scale = (tail > DBL_MIN) ? scale : 0.0;
+        zc[k] = tau;
+      }
+      __syncthreads();
+      for (int j = r + threadIdx.x; j < M; j += blockDim.x) row[j] *= s_scale;
+      __syncthreads();
+      if (threadIdx.x == 0) row[r - 1] = s_beta;
+      // apply Z(k) from the right to rows 0..k-1 (warp per row)
+      if (s_tau != 0.0)
+        for (int u = warp; u < k; u += nwarp) {
+          double* ru = Rr + static_cast<size_t>(u) * M;
+          double s = 0;
+          for (int j = r + lane; j < M; j += 32) s += ru[j] * row[j];
+          s = warp_sum(s);
+          s = (s + ru[r - 1]) * s_tau;
+          __syncwarp();
+          if (lane == 0) ru[r - 1] -= s;
+          for (int j = r + lane; j < M; j += 32) ru[j] -= s * row[j];
+        }
+      __syncthreads();
+      if (k != r - 1)
+        for (int u = threadIdx.x; u <= k; u += blockDim.x) {
+          const double tmp = Rr[static_cast<size_t>(u) * M + k];
+          Rr[static_cast<size_t>(u) * M + k] = Rr[static_cast<size_t>(u) * M + r - 1];
+          Rr[static_cast<size_t>(u) * M + r - 1] = tmp;
+        }
+      __syncthreads();
+    }
+  }
+  // ---- Y = Z^T [I_r; 0]  (COD::solve's Z^* application, column by column)
+  for (int idx = threadIdx.x; idx < M * R; idx += blockDim.x) {
+    const int i = idx / R, c = idx % R;
+    Y[idx] = (i == c && i < r) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (r < M) {
+    for (int k = 0; k < r; ++k) {
+      const double tau = zc[k];
+      if (tau == 0.0) continue;
+      const double* zr = Rr + static_cast<size_t>(k) * M;
+      for (int c = warp; c < r; c += nwarp) {
+        // rows {k} U {r..M-1}, with row k playing position r-1
+        const int lead = (k != r - 1) ? k : r - 1;
+        // swapping rows k and r-1 then operating on r-1 is equivalent to: leading element at
+        // row k, and row r-1 untouched (unless k == r-1)
+        double s = 0;
+        for (int j = r + lane; j < M; j += 32) s += zr[j] * Y[static_cast<size_t>(j) * R + c];
+        s = warp_sum(s);
+        const double yl = Y[static_cast<size_t>(lead) * R + c];
+        s = (s + yl) * tau;
+        __syncwarp();
+        if (lane == 0) Y[static_cast<size_t>(lead) * R + c] = yl - s;
+        for (int j = r + lane; j < M; j += 32) Y[static_cast<size_t>(j) * R + c] -= s * zr[j];
+        __syncwarp();
+      }
+      __syncthreads();
+    }
+  }
+  // ---- C(perm[i], :) = (Y T^{-1})(i, :), T = upper triangle of Rr(0:r, 0:r)
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    double* yi = Y + static_cast<size_t>(i) * R;
+    for (int c = 0; c < r; ++c) {
+      double s = yi[c];
+      for (int u = 0; u < c; ++u) s -= yi[u] * Rr[static_cast<size_t>(u) * M + c];
+      yi[c] = s / Rr[static_cast<size_t>(c) * M + c];
+    }
+    double* ci = C + static_cast<size_t>(perm[i]) * R;
+    for (int c = 0; c < R; ++c) ci[c] = c < r ? yi[c] : 0.0;
+  }
+  // ---- Q1_r^T applied to the top M rows of Q0^T [f E] (in place), keep r rows
+  for (int u = 0; u < r; ++u) {
+    const double tau = tau1[u];
+    const double* vu = V1 + static_cast<size_t>(u) * M;
+    if (tau != 0.0)
+      for (int e = warp; e < E; e += nwarp) {
+        double* xe = X + static_cast<size_t>(e) * ld;
+        double s = 0;
+        for (int i = u + lane; i < M; i += 32) s += vu[i] * xe[i];
+        s = warp_sum(s) * tau;
+        __syncwarp();
+        for (int i = u + lane; i < M; i += 32) xe[i] -= s * vu[i];
+        __syncwarp();
+      }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < R * E; idx += blockDim.x) {
+    const int c = idx / E, e = idx % E;
+    QtX[idx] = c < r ? X[static_cast<size_t>(e) * ld + c] : 0.0;
+  }
+}
+
+}  // namespace
+
+void launch_cod_pivqr(const CodArgs& a, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (a.M + 2 * a.kmax);
+  cod_pivqr_kernel<<<a.nmat, 1024, smem, st>>>(a);
+  DDG_LAUNCH_CHECK();
+}
+
+void launch_cod_finish(const CodArgs& a, cudaStream_t st) {
+  cod_finish_kernel<<<a.nmat, 512, 0, st>>>(a);
+  DDG_LAUNCH_CHECK();
+}
+
+}  // namespace ddg

@@ -1,0 +1,156 @@
+// Fused ELM feature / collocation-row builder (sm_100a).
+//
+// One pass over (row task, neuron) writes every matrix the solve needs — K (with the
+// change-of-variables epilogue T^{-1} = I - E), the Neumann matrix Kbar (its interior/boundary
+// rows shared with K, tanh evaluated once), the flux blocks F and the Neumann trace rows Cdelta.
+// Reference semantics: eval_derivative_matrix (features.cpp:42-76), Poisson rows
+// (problems.cpp:71-121), assemble_local (assembly.cpp:9-46), apply_change_of_variables
+// (assembly.cpp:80-87), build_neumann rows (solvers.cpp:418-438).
+//
+// HBM roofline: writes 8*(2 m M + nF M + nd M) bytes per subdomain; threads
+// map to consecutive rows of a column-major matrix so every store is coalesced.
+#include "common.cuh"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+namespace ddg {
+
+namespace {
+
+struct Feat {
+  double w0, w1, b;
+};
+
+__device__ __forceinline__ double feat_z(const Feat& f, double x, double y) {
+  // w0 * x + w1 * y + b in the reference's evaluation order, no FMA contraction
+  return __dadd_rn(__dadd_rn(__dmul_rn(f.w0, x), __dmul_rn(f.w1, y)), f.b);
+}
+
+__device__ __forceinline__ double coord(int i0, int a, int S) {
+  return static_cast<double>(i0 + a) / static_cast<double>(S);
+}
+
+__global__ void __launch_bounds__(256) build_features_kernel(FeatureArgs p) {
+  constexpr int JT = 32;
+  __shared__ Feat sf[JT];
+  const int i = blockIdx.y;
+  const int j0 = blockIdx.x * JT;
+  if (threadIdx.x < JT) {
+    const int j = j0 + threadIdx.x;
+    if (j < p.M) sf[threadIdx.x] = Feat{p.w0[i * p.M + j], p.w1[i * p.M + j], p.b[i * p.M + j]};
+  }
+  __syncthreads();
+  const int jn = min(JT, p.M - j0);
+  const int cls = p.sub_cls[i];
+  const int ix = p.sub_ix[i], iy = p.sub_iy[i];
+  const int n = p.n_grid, S = p.S;
+  const int gx0 = ix * (n - 1), gy0 = iy * (n - 1);
+  const Task* tasks = p.tasks + p.cls_task_off[cls];
+  const int ntask = p.cls_task_cnt[cls];
+  const size_t mstride = static_cast<size_t>(p.ld) * p.ncol;
+  double* K = p.A + static_cast<size_t>(i) * mstride;
+  double* Kb = p.A + static_cast<size_t>(p.N + i) * mstride;
+  double* F = p.F + static_cast<size_t>(i) * p.M * p.ldF;
+  double* Cd = p.Cd + static_cast<size_t>(i) * p.M * p.ldC;
+  const double inv_n1 = 1.0 / (n - 1);
+  (void)inv_n1;
+
+  for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
+    const Task tk = tasks[t];
+    const double x = coord(gx0, tk.a, S), y = coord(gy0, tk.b, S);
+    const int dst = tk.dst & 0x0f;
+    const bool dual = (tk.dst & kDual) != 0;
+    double* out;
+    size_t ldo;
+    if (dst == kDstK) { out = K; ldo = p.ld; }
+    else if (dst == kDstKbar) { out = Kb; ldo = p.ld; }
+    else if (dst == kDstF) { out = F; ldo = p.ldF; }
+    else { out = Cd; ldo = p.ldC; }
+    // change-of-variables corner points (assembly.cpp:59-75)
+    double cx1 = 0, cy1 = 0, cx2 = 0, cy2 = 0, e1 = 0, e2 = 0;
+    double nx = 0, ny = 0;
+    if (tk.kind == kValueCov) {
+      const bool vert = tk.side < 2;
+      const int jj = vert ? tk.b : tk.a;  // geom_j along the edge
+      const int ae = vert ? (tk.side == 0 ? 0 : n - 1) : 0;
+      const int be = vert ? 0 : (tk.side == 2 ? 0 : n - 1);
+      if (vert) {
+        cx1 = coord(gx0, ae, S); cy1 = coord(gy0, 0, S);
+        cx2 = coord(gx0, ae, S); cy2 = coord(gy0, n - 1, S);
+      } else {
+        cx1 = coord(gx0, 0, S); cy1 = coord(gy0, be, S);
+        cx2 = coord(gx0, n - 1, S); cy2 = coord(gy0, be, S);
+      }
+      // Tinv entries: -(1 - j/(n-1)) for the first corner, -(j/(n-1)) for the last
+      e1 = 1.0 - static_cast<double>(jj) / (n - 1);
+      e2 = static_cast<double>(jj) / (n - 1);
+    } else if (tk.kind == kFlux) {
+      const double nxs[4] = {-1.0, 1.0, 0.0, 0.0}, nys[4] = {0.0, 0.0, -1.0, 1.0};
+      nx = nxs[tk.side];
+      ny = nys[tk.side];
+    }
+    for (int jj = 0; jj < jn; ++jj) {
+      const Feat f = sf[jj];
+      const double s0 = tanh(feat_z(f, x, y));
+      double v;
+      if (tk.kind == kValue) {
+        v = s0;
+      } else if (tk.kind == kLap) {
+        const double s1 = __dadd_rn(1.0, -__dmul_rn(s0, s0));
+        const double s2 = __dmul_rn(__dmul_rn(-2.0, s0), s1);
+        const double d20 = __dmul_rn(s2, __dmul_rn(f.w0, f.w0));
+        const double d02 = __dmul_rn(s2, __dmul_rn(f.w1, f.w1));
+        v = -__dadd_rn(d20, d02);
+      } else if (tk.kind == kFlux) {
+        const double s1 = __dadd_rn(1.0, -__dmul_rn(s0, s0));
+        v = __dadd_rn(__dmul_rn(nx, __dmul_rn(s1, f.w0)), __dmul_rn(ny, __dmul_rn(s1, f.w1)));
+      } else {  // kValueCov: sum over gamma index order first corner, point, last corner
+        v = 0.0;
+        if (tk.flags & 1) v = -__dmul_rn(e1, tanh(feat_z(f, cx1, cy1)));
+        v = (tk.flags & 1) ? __dadd_rn(v, s0) : s0;
+        if (tk.flags & 2) v = __dadd_rn(v, -__dmul_rn(e2, tanh(feat_z(f, cx2, cy2))));
+      }
+      const size_t col = static_cast<size_t>(j0 + jj);
+      out[col * ldo + tk.row] = v;
+      if (dual) Kb[col * p.ld + tk.row] = v;
+    }
+  }
+}
+
+/// Appended right-hand-side columns of the batched QR: column M holds f (K) / 0 (Kbar);
+/// columns M+1+q hold unit vectors at the trace rows (K) / Neumann flux rows (Kbar), so the
+/// QR's trailing updates produce Q^T [f E] for free.
+__global__ void fill_append_kernel(FeatureArgs p) {
+  const int c = blockIdx.x;  // appended column index 0..ncol-M-1
+  const int t = blockIdx.y;  // matrix 0..2N-1
+  const int i = t < p.N ? t : t - p.N;
+  const bool bar = t >= p.N;
+  const int cls = p.sub_cls[i];
+  const ClassDims d = p.dims[cls];
+  double* col = p.A + static_cast<size_t>(t) * p.ld * p.ncol + static_cast<size_t>(p.M + c) * p.ld;
+  int unit_row = -1;
+  if (c >= 1) {
+    const int q = c - 1;
+    if (!bar && q < d.n_gamma) unit_row = d.fixed + q;
+    if (bar && q < d.nd) unit_row = d.fixed + d.nc + q;
+  }
+  for (int r = threadIdx.x; r < p.ld; r += blockDim.x) {
+    double v = 0.0;
+    if (c == 0 && !bar && r < p.m) v = p.f[static_cast<size_t>(i) * p.m + r];
+    if (r == unit_row) v = 1.0;
+    col[r] = v;
+  }
+}
+
+}  // namespace
+
+void launch_build_features(const FeatureArgs& a, cudaStream_t st) {
+  dim3 grid(ceil_div(a.M, 32), a.N);
+  build_features_kernel<<<grid, 256, 0, st>>>(a);
+  DDG_LAUNCH_CHECK();
+  dim3 g2(a.ncol - a.M, 2 * a.N);
+  fill_append_kernel<<<g2, 256, 0, st>>>(a);
+  DDG_LAUNCH_CHECK();
+}
+
+}  // namespace ddg

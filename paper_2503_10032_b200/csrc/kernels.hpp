@@ -1,0 +1,182 @@
+// Kernel launch interfaces of the DDELM-NN device path (all sm_100a, fp64).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "plan.hpp"
+
+namespace ddg {
+
+struct ClassDims {
+  int n_int, n_bnd, n_gamma, m, fixed, nc, nd, nF;
+};
+
+// ---------------------------------------------------------------- features (k_features.cu)
+struct FeatureArgs {
+  int N, M, m, ld, ncol, n_grid, S, ldF, ldC;
+  const Task* tasks;
+  const int* cls_task_off;
+  const int* cls_task_cnt;
+  const ClassDims* dims;
+  const int* sub_cls;
+  const int* sub_ix;
+  const int* sub_iy;
+  const double* w0;
+  const double* w1;
+  const double* b;
+  const double* f;  // N x m
+  double* A;        // 2N matrices, ld x ncol column-major (K_i then Kbar_i)
+  double* F;        // N x (M x ldF)
+  double* Cd;       // N x (M x ldC)
+};
+void launch_build_features(const FeatureArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- QR (k_qr.cu)
+struct QrArgs {
+  int nmat, m, ld, ncol, M;
+  double* A;    // nmat x ld x ncol
+  double* tau;  // nmat x M
+  double* T;    // nmat x 32 x 32 (block reflector of the current panel)
+};
+constexpr int kQrNB = 32;
+void launch_qr_panel(const QrArgs& a, int k0, cudaStream_t st);
+void launch_qr_trailing(const QrArgs& a, int k0, cudaStream_t st);
+/// |R_ii| min / max per matrix -> ratio (branch test of LsFactor, solvers.cpp:27-32)
+void launch_qr_diag_ratio(const QrArgs& a, double* ratio, cudaStream_t st);
+
+// ---------------------------------------------------------------- COD (k_cod.cu)
+struct CodArgs {
+  int nmat, m, ld, ncol, M, kmax, rmax, ext;  // ext = appended columns used (1 + gmax)
+  double rank_tol;
+  const double* A;       // factored QR (R0 in the upper triangle of the top M x M block)
+  const double* ratio;   // per matrix: unpivoted min/max |R_ii|
+  int* deficient;        // per matrix: branch taken (1 = COD)
+  // pivoted-QR state (per matrix)
+  double* V1;    // kmax x M  (reflector t at V1[t*M + i])
+  double* F1;    // M x kmax  (F1[j*kmax + t])
+  double* Rr;    // kmax x M  (R rows by column position)
+  double* tau1;  // kmax
+  double* upd;   // M
+  double* dir;   // M
+  int* perm;     // M
+  int* rank;     // per matrix
+  int* status;   // per matrix: 0 ok, 1 capacity exceeded
+  double* zc;    // kmax RZ reflector coefficients
+  // outputs (rmax-strided, allocated after ranks are known)
+  double* C;     // nmat x M x rmax   : K^+ = C Q_r^T (C row i = original column i)
+  double* QtX;   // nmat x rmax x ext : Q_r^T [f E] (top r rows)
+  double* Ywork; // nmat x M x rmax scratch
+};
+void launch_cod_pivqr(const CodArgs& a, cudaStream_t st);
+void launch_cod_finish(const CodArgs& a, cudaStream_t st);  // RZ, C, Q^T X (both branches)
+
+// ---------------------------------------------------------------- interface blocks (k_blocks.cu)
+struct BlockArgs {
+  int N, M, rmax, ext, gmax, fmax, dmax, crmax, ldF, ldC, n_pi, npf, n_delta;
+  const int* rank;       // 2N
+  const ClassDims* dims;
+  const int* sub_cls;
+  const double* F;       // N x M x ldF
+  const double* Cd;      // N x M x ldC
+  const double* C;       // 2N x M x rmax
+  const double* QtX;     // 2N x rmax x ext
+  double* FC;            // N x fmax x rmax
+  double* CCb;           // N x dmax x rmax
+  // coarse
+  const int* gamma_pi;   // N x gmax (-1 or Pi index)
+  const int* cr_row;     // N x crmax (cross-flux row index r or -1)
+  const int* cr_off;     // N x (crmax+1) offsets into cr_l / cr_w
+  const int* cr_l;
+  const double* cr_w;
+  double* Zc;            // N x crmax x gmax : (K^+)^T a restricted to gamma rows
+  double* pd;            // N x crmax : flux data F K^+ f per cross row (before scatter)
+  double* Gc;            // N x 4 x 4  : -(Q_Pi Q_Pi^T)
+  int* corner_q;         // N x 4 gamma positions of the corners (-1 pad)
+  double* Dpp;           // npf x n_pi
+  double* dpi;           // npf
+  double* S;             // n_pi x n_pi
+  double* Sinv;          // n_pi x n_pi
+  const int* mult_pi;    // n_pi
+  int* spd_fail;         // 1 flag
+  int flip_row;          // debug_flip_flux_row (global flux row) or -1
+  const int* row_owner;  // npf x 4 : contributing (i * crmax + rho), subdomain order, -1 pad
+};
+void launch_blocks(const BlockArgs& a, bool neumann, cudaStream_t st);
+void launch_coarse_local(const BlockArgs& a, const int* cr_row, const int* cr_off, const int* cr_l,
+                         const double* cr_w, cudaStream_t st);
+void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t st);
+void launch_coarse_schur(const BlockArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- CG (k_cg.cu)
+struct CgArgs {
+  int N, n_delta, n_pi, npf, gmax, fmax, dmax, crmax, rmax, ext, M;
+  double theta;
+  int use_neumann;  // theta > 0
+  // 1: apply K^+ as the reference does — coefficients c = C s (M-vector) first, then the flux
+  //    rows F c / F^T a (solvers.cpp:215-218, 240-241); 0: pre-multiplied FC = F C blocks
+  int coeff_space;
+  const double* F;         // N x M x ldF (flux rows, j-major)
+  int ldF;
+  double* cwork;           // N x M scratch (coefficients / F^T a)
+  double rel_tol;
+  int max_iter;
+  const int* rank;      // 2N
+  const ClassDims* dims;
+  const int* sub_cls;
+  const int* gamma_delta;  // N x gmax
+  const int* gamma_pi;     // N x gmax
+  const int* fluxrow_delta;  // N x fmax
+  const int* ndelta_map;   // N x dmax
+  const int* cr_row;       // N x crmax
+  const int* corner_q;     // N x 4
+  const int* own_gamma;    // 2 n_delta
+  const int* own_flux;
+  const int* own_nd;
+  const int* pi_owner;     // n_pi x 4 : (i * 4 + corner slot), subdomain order, -1 pad
+  const int* row_owner;    // npf x 4 : (i * crmax + rho)
+  const double* flip_sign; // n_delta (+1 / -1 debug hook)
+  const double* QtX;       // 2N x rmax x ext (QGt = cols 1.., qf = col 0)
+  const double* FC;        // N x fmax x rmax
+  const double* CCb;       // N x dmax x rmax
+  const double* Zc;        // N x crmax x gmax
+  const double* Dpp;       // npf x n_pi
+  const double* Sinv;      // n_pi x n_pi
+  const double* dpi;       // npf
+  const double* C;         // 2N x M x rmax
+  // work
+  double* s;      // N x rmax
+  double* tpart;  // N x 4 (corner contributions)
+  double* psipart;// N x crmax
+  double* mu;     // n_pi
+  double* d1;     // npf
+  double* d2;     // npf
+  double* o;      // N x gmax
+  double* xf;     // N x fmax
+  double* tr;     // N x dmax
+  double* zz;     // N x dmax
+  double* u;      // N x rmax
+  double* nu;     // n_pi
+  double* bot;    // npf
+  // CG vectors
+  double* x;
+  double* r;
+  double* p;
+  double* Ap;
+  double* rhs;
+  double* partial;  // reduction scratch
+  double* hist;     // max_iter
+  int* state;       // [0] it, [1] done, [2] converged, [3] negcurv
+  double* scal;     // [0] rr, [1] bnorm, [2] alpha, [3] pAp
+  double* coeffs;   // N x M output
+  double* mu_pi_out;  // n_pi
+};
+/// out = cs_reduced_apply(v) (mode 0) or the reduced right-hand side (mode 1, v unused)
+void cg_launch_operator(const CgArgs& a, const double* v, double* out, int mode, cudaStream_t st);
+void cg_launch_init(const CgArgs& a, cudaStream_t st);
+/// One CG iteration (solvers.cpp:95-117). With use_cond the last kernel drives the graph's
+/// while-conditional; every kernel is a no-op once the solve is done.
+void cg_launch_step(const CgArgs& a, cudaStream_t st, unsigned long long cond_handle, bool use_cond);
+void cg_launch_reconstruct(const CgArgs& a, cudaStream_t st);
+int cg_kernels_per_step(const CgArgs& a);
+
+}  // namespace ddg

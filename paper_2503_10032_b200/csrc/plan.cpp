@@ -1,0 +1,349 @@
+// Host-side layout for the DDELM-NN device path (see plan.hpp for the reference map).
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <numbers>
+#include <random>
+#include <stdexcept>
+
+namespace ddg {
+
+namespace {
+
+constexpr double kPi = std::numbers::pi;
+
+int class_mask(int s, int ix, int iy) {
+  int m = 0;
+  if (ix == 0) m |= 1;
+  if (ix == s - 1) m |= 2;
+  if (iy == 0) m |= 4;
+  if (iy == s - 1) m |= 8;
+  return m;
+}
+
+/// Point classes of one side class (geometry.cpp:80-142 restricted to one subdomain).
+ClassPlan build_class(int mask, int n, bool cov) {
+  ClassPlan c;
+  c.mask = mask;
+  const bool outer[4] = {(mask & 1) != 0, (mask & 2) != 0, (mask & 4) != 0, (mask & 8) != 0};
+  std::vector<std::pair<int, int>> interior, boundary;
+  std::map<std::pair<int, int>, int> gamma_of;
+  for (int b = 0; b < n; ++b)
+    for (int a = 0; a < n; ++a) {
+      const bool on_local = a == 0 || a == n - 1 || b == 0 || b == n - 1;
+      const bool on_outer = (a == 0 && outer[0]) || (a == n - 1 && outer[1]) ||
+                            (b == 0 && outer[2]) || (b == n - 1 && outer[3]);
+      if (!on_local) {
+        interior.push_back({a, b});
+      } else if (on_outer) {
+        boundary.push_back({a, b});
+      } else {
+        GammaPt g{a, b, false, -1, -1};
+        const bool xl = a == 0 || a == n - 1, yl = b == 0 || b == n - 1;
+        if (xl && yl) {
+          g.is_cross = true;
+        } else if (xl) {
+          g.side = (a == 0) ? 0 : 1;
+          g.t = b;
+        } else {
+          g.side = (b == 0) ? 2 : 3;
+          g.t = a;
+        }
+        gamma_of[{a, b}] = static_cast<int>(c.gamma.size());
+        c.gamma.push_back(g);
+      }
+    }
+  c.n_int = static_cast<int>(interior.size());
+  c.n_bnd = static_cast<int>(boundary.size());
+  c.n_gamma = static_cast<int>(c.gamma.size());
+  c.m = c.n_int + c.n_bnd + c.n_gamma;
+  c.fixed = c.n_int + c.n_bnd;
+  for (int side = 0; side < 4; ++side) {
+    if (outer[side]) continue;
+    LocalEdgeC le;
+    le.side = side;
+    for (int j = 0; j < n; ++j) {
+      const bool vert = side < 2;
+      const int a = vert ? (side == 0 ? 0 : n - 1) : j;
+      const int b = vert ? j : (side == 2 ? 0 : n - 1);
+      auto it = gamma_of.find({a, b});
+      if (it == gamma_of.end()) continue;
+      le.pts.push_back(it->second);
+      le.geom_j.push_back(j);
+      if (j == 0) le.first_corner = true;
+      if (j == n - 1) le.last_corner = true;
+    }
+    c.edges.push_back(le);
+  }
+  // Edge-local position of each non-corner gamma point (solvers.cpp:408-413).
+  std::vector<std::pair<int, int>> where(c.n_gamma, {-1, -1});
+  std::vector<int> edge_row0;
+  int off = 0;
+  for (int e = 0; e < static_cast<int>(c.edges.size()); ++e) {
+    edge_row0.push_back(off);
+    const LocalEdgeC& le = c.edges[e];
+    for (int pos = 0; pos < static_cast<int>(le.pts.size()); ++pos) {
+      c.flux_rows.push_back({e, pos});
+      if (!c.gamma[le.pts[pos]].is_cross) where[le.pts[pos]] = {e, pos};
+    }
+    off += static_cast<int>(le.pts.size());
+  }
+  c.nF = off;
+  for (int q = 0; q < c.n_gamma; ++q) (c.gamma[q].is_cross ? c.corner_idx : c.delta_idx).push_back(q);
+  c.nc = static_cast<int>(c.corner_idx.size());
+  c.nd = static_cast<int>(c.delta_idx.size());
+  for (int k = 0; k < c.nd; ++k) {
+    auto [e, pos] = where[c.delta_idx[k]];
+    c.flux_row_of_delta.push_back(edge_row0[e] + pos);
+  }
+
+  // ---- row-generation tasks
+  auto task = [](int a, int b, uint8_t kind, uint8_t dst, uint8_t side, uint8_t flags, int row) {
+    Task t;
+    t.a = static_cast<int16_t>(a);
+    t.b = static_cast<int16_t>(b);
+    t.kind = kind;
+    t.dst = dst;
+    t.side = side;
+    t.flags = flags;
+    t.row = row;
+    t.pad = 0;
+    return t;
+  };
+  int row = 0;
+  for (auto [a, b] : interior) c.tasks.push_back(task(a, b, kLap, kDstK | kDual, 0, 0, row++));
+  for (auto [a, b] : boundary) c.tasks.push_back(task(a, b, kValue, kDstK | kDual, 0, 0, row++));
+  for (int q = 0; q < c.n_gamma; ++q) {
+    const GammaPt& g = c.gamma[q];
+    if (!cov || g.is_cross) {
+      c.tasks.push_back(task(g.a, g.b, kValue, kDstK, 0, 0, row++));
+      continue;
+    }
+    uint8_t flags = 0;
+    for (const LocalEdgeC& le : c.edges)
+      if (le.side == g.side) flags = (le.first_corner ? 1 : 0) | (le.last_corner ? 2 : 0);
+    c.tasks.push_back(task(g.a, g.b, flags ? kValueCov : kValue, kDstK, static_cast<uint8_t>(g.side), flags, row++));
+  }
+  c.n_tasks_k = row;
+  // Kbar tail: corner trace rows (nodal basis), then Delta flux rows (solvers.cpp:418-431)
+  int rb = c.fixed;
+  for (int q : c.corner_idx) c.tasks.push_back(task(c.gamma[q].a, c.gamma[q].b, kValue, kDstKbar, 0, 0, rb++));
+  for (int k = 0; k < c.nd; ++k) {
+    const GammaPt& g = c.gamma[c.delta_idx[k]];
+    c.tasks.push_back(task(g.a, g.b, kFlux, kDstKbar, static_cast<uint8_t>(g.side), 0, rb++));
+  }
+  c.n_tasks_kbar = rb - c.fixed;
+  for (int l = 0; l < c.nF; ++l) {
+    auto [e, pos] = c.flux_rows[l];
+    const GammaPt& g = c.gamma[c.edges[e].pts[pos]];
+    c.tasks.push_back(task(g.a, g.b, kFlux, kDstF, static_cast<uint8_t>(c.edges[e].side), 0, l));
+  }
+  c.n_tasks_f = c.nF;
+  for (int k = 0; k < c.nd; ++k) {
+    const GammaPt& g = c.gamma[c.delta_idx[k]];
+    c.tasks.push_back(task(g.a, g.b, kValue, kDstCd, 0, 0, k));
+  }
+  c.n_tasks_cd = c.nd;
+  return c;
+}
+
+}  // namespace
+
+bool problem_known(int problem) { return problem >= 0 && problem <= 2; }
+
+double problem_forcing(int problem, double x, double y) {
+  switch (problem) {
+    case 0: return 2.0 * kPi * kPi * std::sin(kPi * x) * std::sin(kPi * y);
+    case 1: return (4.0 * kPi * kPi - 1.0) * std::sin(2 * kPi * x) * std::exp(y);
+    default: return 13.0 * kPi * kPi * std::sin(2 * kPi * x) * std::cos(3 * kPi * y) - 2.0 * y;
+  }
+}
+
+double problem_boundary(int problem, double x, double y) {
+  switch (problem) {
+    case 0: return std::sin(kPi * x) * std::sin(kPi * y);
+    case 1: return std::sin(2 * kPi * x) * std::exp(y);
+    default: return std::sin(2 * kPi * x) * std::cos(3 * kPi * y) + x * x * y;
+  }
+}
+
+Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, int flux_variant,
+                bool cov, double rank_tol, int debug_flip_flux_row) {
+  if (!problem_known(problem)) throw std::invalid_argument("make_problem: unknown problem id");
+  if (s < 1) throw std::invalid_argument("partition_domain: s must be >= 1");
+  if (n_grid < 3) throw std::invalid_argument("partition_domain: n_grid must be >= 3");
+  if (M < 1) throw std::invalid_argument("init_layer: M must be positive");
+  if (!(l > 0)) throw std::invalid_argument("init_layer: l must be positive");
+  Plan p;
+  p.problem = problem;
+  p.s = s;
+  p.n_grid = n_grid;
+  p.M = M;
+  p.l = l;
+  p.seed = seed;
+  p.flux_variant = flux_variant;
+  p.cov = cov;
+  p.rank_tol = rank_tol;
+  p.debug_flip_flux_row = debug_flip_flux_row;
+  const int n = n_grid;
+  p.N = s * s;
+  p.m = n * n;
+  if (p.m < M) throw std::invalid_argument("LsFactor: matrix must be square or tall");
+  p.n_delta = 2 * s * (s - 1) * (n - 2);
+  p.n_pi = (s - 1) * (s - 1);
+  p.npf = 2 * p.n_pi;
+  p.multiplicity_pi.assign(p.n_pi, 0);
+
+  std::map<int, int> cls_of_mask;
+  p.subs.resize(p.N);
+  for (int iy = 0; iy < s; ++iy)
+    for (int ix = 0; ix < s; ++ix) {
+      const int i = iy * s + ix;
+      const int mask = class_mask(s, ix, iy);
+      auto it = cls_of_mask.find(mask);
+      if (it == cls_of_mask.end()) {
+        it = cls_of_mask.emplace(mask, static_cast<int>(p.classes.size())).first;
+        p.classes.push_back(build_class(mask, n, cov));
+      }
+      SubPlan& sp = p.subs[i];
+      sp.ix = ix;
+      sp.iy = iy;
+      sp.cls = it->second;
+      sp.seed = seed + static_cast<uint64_t>(i);
+    }
+  for (const ClassPlan& c : p.classes) {
+    p.gmax = std::max(p.gmax, c.n_gamma);
+    p.fmax = std::max(p.fmax, c.nF);
+    p.dmax = std::max(p.dmax, c.nd);
+    p.tmax = std::max(p.tmax, static_cast<int>(c.tasks.size()));
+  }
+  p.gmax = std::max(p.gmax, 1);
+  p.fmax = std::max(p.fmax, 1);
+  p.dmax = std::max(p.dmax, 1);
+
+  // ---- global numbering per subdomain (geometry.cpp:148-179, assembly.cpp:89-133)
+  auto edge_id = [s](int ix, int iy, int side) {
+    switch (side) {
+      case 0: return (ix - 1) * s + iy;
+      case 1: return ix * s + iy;
+      case 2: return s * (s - 1) + (iy - 1) * s + ix;
+      default: return s * (s - 1) + iy * s + ix;
+    }
+  };
+  auto cross_of = [&](int ix, int iy, int a, int b) {
+    const int gx = ix * (n - 1) + a, gy = iy * (n - 1) + b;
+    return (gy / (n - 1) - 1) * (s - 1) + (gx / (n - 1) - 1);
+  };
+  p.own_gamma.assign(2 * static_cast<size_t>(p.n_delta), -1);
+  p.own_flux.assign(2 * static_cast<size_t>(p.n_delta), -1);
+  p.own_nd.assign(2 * static_cast<size_t>(p.n_delta), -1);
+  auto own = [](std::vector<int>& v, int g, int val) {
+    if (v[2 * g] < 0) v[2 * g] = val;
+    else v[2 * g + 1] = val;
+  };
+  for (int i = 0; i < p.N; ++i) {
+    SubPlan& sp = p.subs[i];
+    const ClassPlan& c = p.classes[sp.cls];
+    sp.gamma_delta.assign(c.n_gamma, -1);
+    sp.gamma_pi.assign(c.n_gamma, -1);
+    for (int q = 0; q < c.n_gamma; ++q) {
+      const GammaPt& g = c.gamma[q];
+      if (g.is_cross) {
+        const int cid = cross_of(sp.ix, sp.iy, g.a, g.b);
+        sp.gamma_pi[q] = cid;
+        p.multiplicity_pi[cid] += 1;
+      } else {
+        const int d = edge_id(sp.ix, sp.iy, g.side) * (n - 2) + (g.t - 1);
+        sp.gamma_delta[q] = d;
+        own(p.own_gamma, d, i * p.gmax + q);
+      }
+    }
+    // flux scatter, in the reference's order (edges L,R,B,T; points by arclength)
+    std::map<int, int> cross_slot;
+    sp.fluxrow_delta.assign(c.nF, -1);
+    int off = 0;
+    for (const LocalEdgeC& le : c.edges) {
+      const int np = static_cast<int>(le.pts.size());
+      const int dir = le.side < 2 ? 0 : 1;
+      for (int q = 0; q < np; ++q) {
+        const int j = le.geom_j[q];
+        const int lrow = off + q;
+        if (j > 0 && j < n - 1) {
+          const int d = edge_id(sp.ix, sp.iy, le.side) * (n - 2) + (j - 1);
+          sp.fluxrow_delta[lrow] = d;
+          own(p.own_flux, d, i * p.fmax + lrow);
+          continue;
+        }
+        const GammaPt& g = c.gamma[le.pts[q]];
+        const int r = cross_of(sp.ix, sp.iy, g.a, g.b) * 2 + dir;
+        auto it = cross_slot.find(r);
+        if (it == cross_slot.end()) {
+          it = cross_slot.emplace(r, static_cast<int>(sp.cross_rows.size())).first;
+          sp.cross_rows.push_back(CrossRow{r, {}});
+        }
+        CrossRow& cr = sp.cross_rows[it->second];
+        if (flux_variant == 0) {
+          cr.e.push_back({lrow, 1.0});
+        } else {
+          const int opposing = (j == 0) ? n - 1 : 0;
+          const double w = 1.0 / (n - 1);
+          for (int q2 = 0; q2 < np; ++q2)
+            if (le.geom_j[q2] != opposing) cr.e.push_back({off + q2, w});
+        }
+      }
+      off += np;
+    }
+    // the reference groups cross entries with std::map<grow,...> (solvers.cpp:302-304):
+    // rows in increasing global order, entries in scatter order
+    std::sort(sp.cross_rows.begin(), sp.cross_rows.end(),
+              [](const CrossRow& x, const CrossRow& y) { return x.r < y.r; });
+    p.crmax = std::max(p.crmax, static_cast<int>(sp.cross_rows.size()));
+    sp.ndelta_map.assign(c.nd, -1);
+    for (int k = 0; k < c.nd; ++k) {
+      const GammaPt& g = c.gamma[c.delta_idx[k]];
+      const int d = edge_id(sp.ix, sp.iy, g.side) * (n - 2) + (g.t - 1);
+      sp.ndelta_map[k] = d;
+      own(p.own_nd, d, i * p.dmax + k);
+    }
+  }
+  p.crmax = std::max(p.crmax, 1);
+
+  // ---- right-hand sides f (assembly.cpp:21-33): forcing, boundary data, zero on traces
+  const int S = s * (n - 1);
+  p.f.assign(static_cast<size_t>(p.N) * p.m, 0.0);
+  for (int i = 0; i < p.N; ++i) {
+    const SubPlan& sp = p.subs[i];
+    const ClassPlan& c = p.classes[sp.cls];
+    for (int t = 0; t < c.n_tasks_k; ++t) {
+      const Task& tk = c.tasks[t];
+      if (tk.row >= c.fixed) continue;
+      const double x = static_cast<double>(sp.ix * (n - 1) + tk.a) / S;
+      const double y = static_cast<double>(sp.iy * (n - 1) + tk.b) / S;
+      p.f[static_cast<size_t>(i) * p.m + tk.row] =
+          tk.kind == kLap ? problem_forcing(problem, x, y) : problem_boundary(problem, x, y);
+    }
+  }
+  return p;
+}
+
+void init_layer(const Plan& p, int i, double* w0, double* w1, double* b) {
+  const SubPlan& sp = p.subs[i];
+  const double h = 1.0 / p.s;
+  const double x0 = sp.ix * h, y0 = sp.iy * h, x1 = (sp.ix + 1) * h, y1 = (sp.iy + 1) * h;
+  const double r = std::hypot(x1 - x0, y1 - y0) / 2.0;
+  std::mt19937_64 gen(p.seed + static_cast<uint64_t>(i));
+  std::uniform_real_distribution<double> uw(-p.l, p.l);
+  std::uniform_real_distribution<double> ux(x0 - r, x1 + r);
+  std::uniform_real_distribution<double> uy(y0 - r, y1 + r);
+  for (int j = 0; j < p.M; ++j) {
+    const double a0 = uw(gen), a1 = uw(gen);
+    const double xi0 = ux(gen), xi1 = uy(gen);
+    w0[j] = a0;
+    w1[j] = a1;
+    b[j] = -(a0 * xi0 + a1 * xi1);
+  }
+}
+
+}  // namespace ddg

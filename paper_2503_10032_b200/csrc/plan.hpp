@@ -1,0 +1,117 @@
+// Host-side layout of the DDELM-NN hot path: decomposition geometry, point classes,
+// interface numbering, flux scatter and the index tables the device kernels read.
+//
+// Semantics follow the reference's host code (layout source, not a kernel):
+//   partition / classification   proj/src/geometry.cpp:20-146
+//   interface numbering          proj/src/geometry.cpp:148-179
+//   local block row order        proj/src/assembly.cpp:9-46 (interior, boundary, trace)
+//   change of variables T^{-1}   proj/src/assembly.cpp:59-87 (T = I + E, E^2 = 0 => I - E)
+//   flux scatter (A / A_m)       proj/src/assembly.cpp:89-133
+//   Neumann rows of Kbar         proj/src/solvers.cpp:401-444
+//
+// B200 layout decision: every subdomain's point set is determined by which of its four sides
+// lie on the outer boundary, so row-generation "tasks" are stored once per side class (at most
+// 9 classes) and the feature kernel derives coordinates from (ix, iy, a, b) exactly as the
+// host would. Only the small global index maps are per subdomain.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ddg {
+
+enum RowKind : uint8_t { kLap = 0, kValue = 1, kValueCov = 2, kFlux = 3 };
+enum RowDst : uint8_t { kDstK = 0, kDstKbar = 1, kDstF = 2, kDstCd = 3, kDual = 0x10 };
+
+/// One matrix row to generate (16 bytes). Coordinates come from the local grid (a, b).
+struct Task {
+  int16_t a, b;
+  uint8_t kind;   // RowKind
+  uint8_t dst;    // RowDst, optionally | kDual (K row also written into Kbar)
+  uint8_t side;   // normal side for kFlux (0 L, 1 R, 2 B, 3 T); edge side for kValueCov
+  uint8_t flags;  // kValueCov: bit0 first corner present, bit1 last corner present
+  int32_t row;    // destination row
+  int32_t pad;
+};
+static_assert(sizeof(Task) == 16, "Task must stay 16 bytes");
+
+struct GammaPt {
+  int a, b;
+  bool is_cross;
+  int side;  // side of the (single) local edge of a non-corner point
+  int t;     // arclength index 1..n-2 along its edge (non-corner)
+};
+
+struct LocalEdgeC {
+  int side;                 // 0 L, 1 R, 2 B, 3 T
+  std::vector<int> pts;     // local gamma indices, arclength order
+  std::vector<int> geom_j;  // 0..n-1 along the edge
+  bool first_corner = false, last_corner = false;
+};
+
+/// Rows and points of one side class (mask bit k set = side k lies on the outer boundary).
+struct ClassPlan {
+  int mask = 0;
+  int n_int = 0, n_bnd = 0, n_gamma = 0, m = 0, fixed = 0, nc = 0, nd = 0, nF = 0;
+  std::vector<GammaPt> gamma;
+  std::vector<LocalEdgeC> edges;
+  std::vector<int> corner_idx, delta_idx;            // gamma indices
+  std::vector<std::pair<int, int>> flux_rows;        // (edge, pos) per concatenated F row
+  std::vector<int> flux_row_of_delta;                // per delta point k: its F row
+  std::vector<Task> tasks;                           // K (m), Kbar tail (m-fixed), F (nF), Cd (nd)
+  int n_tasks_k = 0, n_tasks_kbar = 0, n_tasks_f = 0, n_tasks_cd = 0;
+};
+
+struct CrossRow {
+  int r;                                   // cross-flux row index (global row - n_delta)
+  std::vector<std::pair<int, double>> e;   // (local F row, weight)
+};
+
+struct SubPlan {
+  int ix = 0, iy = 0, cls = 0;
+  std::vector<int> gamma_delta;  // per gamma point: Delta index, or -1 (corner)
+  std::vector<int> gamma_pi;     // per gamma point: Pi index (0..n_pi-1), or -1
+  std::vector<int> fluxrow_delta;  // per F row: Delta index of a weight-1 Delta scatter, or -1
+  std::vector<CrossRow> cross_rows;
+  std::vector<int> ndelta_map;   // per Neumann Delta row k: Delta index
+  uint64_t seed = 0;
+};
+
+struct Plan {
+  int problem = 0, s = 1, n_grid = 3, M = 1;
+  double l = 1;
+  uint64_t seed = 1;
+  int flux_variant = 1;  // 0 pointwise, 1 mean_edge
+  bool cov = true;
+  double rank_tol = 1e-10;
+  int debug_flip_flux_row = -1;
+
+  int N = 1, m = 0, n_delta = 0, n_pi = 0, npf = 0;
+  int gmax = 0, fmax = 0, dmax = 0, tmax = 0, crmax = 0;  // per-subdomain maxima
+  std::vector<ClassPlan> classes;
+  std::vector<SubPlan> subs;
+  std::vector<int> multiplicity_pi;  // per Pi index
+
+  // owners of each Delta index: (subdomain, local position) pairs in subdomain order
+  std::vector<int> own_gamma;  // 2 * n_delta entries: i * gmax + q
+  std::vector<int> own_flux;   // 2 * n_delta: i * fmax + l
+  std::vector<int> own_nd;     // 2 * n_delta: i * dmax + k
+
+  std::vector<double> f;  // N x m right-hand sides (problem data, assembly.cpp:21-33)
+};
+
+/// Builds the plan; throws std::invalid_argument like the reference (geometry.cpp:21-22).
+Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, int flux_variant,
+                bool cov, double rank_tol, int debug_flip_flux_row);
+
+/// Seeded feature layer of subdomain i (features.cpp:9-35 via solvers.cpp:134-137):
+/// w0, w1, b (M each) from std::mt19937_64(seed + i).
+void init_layer(const Plan& p, int i, double* w0, double* w1, double* b);
+
+/// Problem data (problems.cpp:135-156 + C4's added problem).
+double problem_forcing(int problem, double x, double y);
+double problem_boundary(int problem, double x, double y);
+bool problem_known(int problem);
+
+}  // namespace ddg

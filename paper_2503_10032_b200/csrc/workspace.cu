@@ -1,0 +1,658 @@
+// Device workspace and orchestration of the DDELM-NN hot path (one process, one B200).
+//
+// Mirrors Workspace (solvers.hpp:78-160) and the drivers (solvers.cpp:535-605):
+//   build()          features -> batched QR (K_i and Kbar_i together) -> branch test -> COD
+//   build_coarse()   FC, Zc, Dpp, dpi, S_Pi and its inverse          (assemble_coarse)
+//   build_neumann()  CCb = Cdelta Cbar                                (build_neumann)
+//   solve()          reduced RHS, CG (one CUDA graph with a device-side while loop), reconstruct
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.hpp"
+#include "plan.hpp"
+#include "workspace.hpp"
+
+namespace ddg {
+
+template <typename T>
+void DevBuf<T>::alloc(size_t n) {
+  if (n == count && ptr) return;
+  free();
+  count = n;
+  if (n) DDG_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+}
+
+template <typename T>
+void DevBuf<T>::free() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  count = 0;
+}
+
+template <typename T>
+void DevBuf<T>::upload(const std::vector<T>& v, cudaStream_t st) {
+  alloc(std::max<size_t>(v.size(), 1));
+  if (!v.empty()) DDG_CUDA(cudaMemcpyAsync(ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+template struct DevBuf<double>;
+template struct DevBuf<int>;
+template struct DevBuf<Task>;
+template struct DevBuf<ClassDims>;
+
+Workspace::Workspace(const Plan& p, int device) : plan(p), device_(device) {
+  DDG_CUDA(cudaSetDevice(device_));
+  DDG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  DDG_CUDA(cudaStreamCreateWithFlags(&cap_, cudaStreamNonBlocking));
+  for (auto& e : ev_) DDG_CUDA(cudaEventCreate(&e));
+  DDG_CUDA(cudaMallocHost(&pinned_state_, 64));
+  upload_plan();
+}
+
+Workspace::~Workspace() {
+  cudaSetDevice(device_);
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  for (auto& e : ev_) cudaEventDestroy(e);
+  if (pinned_state_) cudaFreeHost(pinned_state_);
+  cudaStreamDestroy(cap_);
+  cudaStreamDestroy(st_);
+}
+
+void Workspace::upload_plan() {
+  const Plan& p = plan;
+  const int N = p.N;
+  // class tables
+  std::vector<Task> tasks;
+  std::vector<int> off, cnt;
+  std::vector<ClassDims> dims;
+  for (const ClassPlan& c : p.classes) {
+    off.push_back(static_cast<int>(tasks.size()));
+    cnt.push_back(c.n_tasks_k + c.n_tasks_kbar + c.n_tasks_f + c.n_tasks_cd);
+    tasks.insert(tasks.end(), c.tasks.begin(), c.tasks.end());
+    dims.push_back(ClassDims{c.n_int, c.n_bnd, c.n_gamma, c.m, c.fixed, c.nc, c.nd, c.nF});
+  }
+  d_tasks.upload(tasks, st_);
+  d_task_off.upload(off, st_);
+  d_task_cnt.upload(cnt, st_);
+  d_dims.upload(dims, st_);
+  std::vector<int> cls(N), ix(N), iy(N);
+  std::vector<int> gdel(static_cast<size_t>(N) * p.gmax, -1), gpi(static_cast<size_t>(N) * p.gmax, -1);
+  std::vector<int> fdel(static_cast<size_t>(N) * p.fmax, -1), nmap(static_cast<size_t>(N) * p.dmax, -1);
+  std::vector<int> crr(static_cast<size_t>(N) * p.crmax, -1), croff(static_cast<size_t>(N) * (p.crmax + 1), 0);
+  std::vector<int> crl;
+  std::vector<double> crw;
+  std::vector<int> row_owner(static_cast<size_t>(std::max(p.npf, 1)) * 4, -1);
+  std::vector<int> pi_owner(static_cast<size_t>(std::max(p.n_pi, 1)) * 4, -1);
+  auto push_owner = [](std::vector<int>& v, int row, int val) {
+    for (int q = 0; q < 4; ++q)
+      if (v[static_cast<size_t>(row) * 4 + q] < 0) {
+        v[static_cast<size_t>(row) * 4 + q] = val;
+        return;
+      }
+    throw std::logic_error("owner table overflow");
+  };
+  for (int i = 0; i < N; ++i) {
+    const SubPlan& sp = p.subs[i];
+    cls[i] = sp.cls;
+    ix[i] = sp.ix;
+    iy[i] = sp.iy;
+    for (size_t q = 0; q < sp.gamma_delta.size(); ++q) {
+      gdel[static_cast<size_t>(i) * p.gmax + q] = sp.gamma_delta[q];
+      gpi[static_cast<size_t>(i) * p.gmax + q] = sp.gamma_pi[q];
+    }
+    int slot = 0;
+    for (size_t q = 0; q < sp.gamma_pi.size(); ++q)
+      if (sp.gamma_pi[q] >= 0) push_owner(pi_owner, sp.gamma_pi[q], i * 4 + slot++);
+    for (size_t l = 0; l < sp.fluxrow_delta.size(); ++l) fdel[static_cast<size_t>(i) * p.fmax + l] = sp.fluxrow_delta[l];
+    for (size_t k = 0; k < sp.ndelta_map.size(); ++k) nmap[static_cast<size_t>(i) * p.dmax + k] = sp.ndelta_map[k];
+    int* o = croff.data() + static_cast<size_t>(i) * (p.crmax + 1);
+    for (int rho = 0; rho < p.crmax; ++rho) {
+      o[rho] = static_cast<int>(crl.size());
+      if (rho < static_cast<int>(sp.cross_rows.size())) {
+        const CrossRow& cr = sp.cross_rows[rho];
+        crr[static_cast<size_t>(i) * p.crmax + rho] = cr.r;
+        push_owner(row_owner, cr.r, i * p.crmax + rho);
+        for (auto [l, w] : cr.e) {
+          crl.push_back(l);
+          crw.push_back(w);
+        }
+      }
+    }
+    o[p.crmax] = static_cast<int>(crl.size());
+  }
+  d_cls.upload(cls, st_);
+  d_ix.upload(ix, st_);
+  d_iy.upload(iy, st_);
+  d_gamma_delta.upload(gdel, st_);
+  d_gamma_pi.upload(gpi, st_);
+  d_fluxrow_delta.upload(fdel, st_);
+  d_ndelta_map.upload(nmap, st_);
+  d_cr_row.upload(crr, st_);
+  d_cr_off.upload(croff, st_);
+  d_cr_l.upload(crl, st_);
+  d_cr_w.upload(crw, st_);
+  d_row_owner.upload(row_owner, st_);
+  d_pi_owner.upload(pi_owner, st_);
+  d_own_gamma.upload(p.own_gamma, st_);
+  d_own_flux.upload(p.own_flux, st_);
+  d_own_nd.upload(p.own_nd, st_);
+  d_mult_pi.upload(p.multiplicity_pi, st_);
+  std::vector<double> flip(std::max(p.n_delta, 1), 1.0);
+  if (p.debug_flip_flux_row >= 0 && p.debug_flip_flux_row < p.n_delta) flip[p.debug_flip_flux_row] = -1.0;
+  d_flip.upload(flip, st_);
+  d_f.upload(p.f, st_);
+
+  // fixed-size device storage
+  ld_ = (p.m + 3) / 4 * 4;
+  ext_ = 1 + p.gmax;
+  ncol_ = p.M + ext_;
+  kmax_ = std::min(p.M, 192);
+  const size_t nmat = 2 * static_cast<size_t>(N);
+  d_A.alloc(nmat * ld_ * ncol_);
+  d_tau.alloc(nmat * p.M);
+  d_T.alloc(nmat * kQrNB * kQrNB);
+  d_ratio.alloc(2 * nmat);
+  d_deficient.alloc(nmat);
+  d_rank.alloc(nmat);
+  d_status.alloc(nmat);
+  d_V1.alloc(nmat * kmax_ * p.M);
+  d_F1.alloc(nmat * p.M * kmax_);
+  d_Rr.alloc(nmat * kmax_ * p.M);
+  d_tau1.alloc(nmat * kmax_);
+  d_zc.alloc(nmat * kmax_);
+  d_upd.alloc(nmat * p.M);
+  d_dir.alloc(nmat * p.M);
+  d_perm.alloc(nmat * p.M);
+  d_w0.alloc(static_cast<size_t>(N) * p.M);
+  d_w1.alloc(static_cast<size_t>(N) * p.M);
+  d_b.alloc(static_cast<size_t>(N) * p.M);
+  d_F.alloc(static_cast<size_t>(N) * p.M * p.fmax);
+  d_Cd.alloc(static_cast<size_t>(N) * p.M * p.dmax);
+  d_Zc.alloc(static_cast<size_t>(N) * p.crmax * p.gmax);
+  d_pd.alloc(static_cast<size_t>(N) * p.crmax);
+  d_Gc.alloc(static_cast<size_t>(N) * 16);
+  d_corner_q.alloc(static_cast<size_t>(N) * 4);
+  const size_t npf = std::max(p.npf, 1), npi = std::max(p.n_pi, 1);
+  d_Dpp.alloc(npf * npi);
+  d_dpi.alloc(npf);
+  d_S.alloc(npi * npi);
+  d_Sinv.alloc(npi * npi);
+  d_spd_fail.alloc(1);
+  const size_t nd = std::max(p.n_delta, 1);
+  for (auto* b : {&d_x, &d_r, &d_p, &d_Ap, &d_rhs}) b->alloc(nd);
+  d_partial.alloc(2 * static_cast<size_t>(ceil_div(static_cast<int>(nd), 256)) + 2);
+  d_state.alloc(8);
+  d_scal.alloc(8);
+  d_mu.alloc(npi);
+  d_nu.alloc(npi);
+  d_mu_pi_out.alloc(npi);
+  d_d1.alloc(npf);
+  d_d2.alloc(npf);
+  d_bot.alloc(npf);
+  d_tpart.alloc(static_cast<size_t>(N) * 4);
+  d_psipart.alloc(static_cast<size_t>(N) * p.crmax);
+  d_o.alloc(static_cast<size_t>(N) * p.gmax);
+  d_xf.alloc(static_cast<size_t>(N) * p.fmax);
+  d_tr.alloc(static_cast<size_t>(N) * p.dmax);
+  d_zz.alloc(static_cast<size_t>(N) * p.dmax);
+  d_coeffs.alloc(static_cast<size_t>(N) * p.M);
+  DDG_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Workspace::init_layers() {
+  const Plan& p = plan;
+  const int N = p.N;
+  h_w0.resize(static_cast<size_t>(N) * p.M);
+  h_w1.resize(h_w0.size());
+  h_b.resize(h_w0.size());
+  const int nth = std::max(1, std::min<int>(N, static_cast<int>(std::thread::hardware_concurrency())));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nth; ++t)
+    th.emplace_back([&, t] {
+      for (int i = t; i < N; i += nth)
+        init_layer(p, i, h_w0.data() + static_cast<size_t>(i) * p.M, h_w1.data() + static_cast<size_t>(i) * p.M,
+                   h_b.data() + static_cast<size_t>(i) * p.M);
+    });
+  for (auto& x : th) x.join();
+  d_w0.upload(h_w0, st_);
+  d_w1.upload(h_w1, st_);
+  d_b.upload(h_b, st_);
+}
+
+void Workspace::reseed(uint64_t seed) {
+  plan.seed = seed;
+  for (size_t i = 0; i < plan.subs.size(); ++i) plan.subs[i].seed = seed + i;
+  built_ = coarse_built_ = neumann_built_ = false;
+}
+
+FeatureArgs Workspace::feature_args() {
+  const Plan& p = plan;
+  FeatureArgs a;
+  a.N = p.N;
+  a.M = p.M;
+  a.m = p.m;
+  a.ld = ld_;
+  a.ncol = ncol_;
+  a.n_grid = p.n_grid;
+  a.S = p.s * (p.n_grid - 1);
+  a.ldF = p.fmax;
+  a.ldC = p.dmax;
+  a.tasks = d_tasks.ptr;
+  a.cls_task_off = d_task_off.ptr;
+  a.cls_task_cnt = d_task_cnt.ptr;
+  a.dims = d_dims.ptr;
+  a.sub_cls = d_cls.ptr;
+  a.sub_ix = d_ix.ptr;
+  a.sub_iy = d_iy.ptr;
+  a.w0 = d_w0.ptr;
+  a.w1 = d_w1.ptr;
+  a.b = d_b.ptr;
+  a.f = d_f.ptr;
+  a.A = d_A.ptr;
+  a.F = d_F.ptr;
+  a.Cd = d_Cd.ptr;
+  return a;
+}
+
+CodArgs Workspace::cod_args() {
+  CodArgs c;
+  c.nmat = 2 * plan.N;
+  c.m = plan.m;
+  c.ld = ld_;
+  c.ncol = ncol_;
+  c.M = plan.M;
+  c.kmax = kmax_;
+  c.rmax = rmax_;
+  c.ext = ext_;
+  c.rank_tol = plan.rank_tol;
+  c.A = d_A.ptr;
+  c.ratio = d_ratio.ptr;
+  c.deficient = d_deficient.ptr;
+  c.V1 = d_V1.ptr;
+  c.F1 = d_F1.ptr;
+  c.Rr = d_Rr.ptr;
+  c.tau1 = d_tau1.ptr;
+  c.upd = d_upd.ptr;
+  c.dir = d_dir.ptr;
+  c.perm = d_perm.ptr;
+  c.rank = d_rank.ptr;
+  c.status = d_status.ptr;
+  c.zc = d_zc.ptr;
+  c.C = d_C.ptr;
+  c.QtX = d_QtX.ptr;
+  c.Ywork = d_Y.ptr;
+  return c;
+}
+
+void Workspace::build() {
+  DDG_CUDA(cudaSetDevice(device_));
+  const Plan& p = plan;
+  launches_ = 0;
+  const auto h0 = std::chrono::steady_clock::now();
+  init_layers();
+  DDG_CUDA(cudaEventRecord(ev_[0], st_));
+  launch_build_features(feature_args(), st_);
+  launches_ += 2;
+  DDG_CUDA(cudaEventRecord(ev_[1], st_));
+  QrArgs q{2 * p.N, p.m, ld_, ncol_, p.M, d_A.ptr, d_tau.ptr, d_T.ptr};
+  for (int k0 = 0; k0 < p.M; k0 += kQrNB) {
+    launch_qr_panel(q, k0, st_);
+    launch_qr_trailing(q, k0, st_);
+    launches_ += (ncol_ - std::min(k0 + kQrNB, p.M) > 0) ? 2 : 1;
+  }
+  launch_qr_diag_ratio(q, d_ratio.ptr, st_);
+  launches_ += 1;
+  DDG_CUDA(cudaEventRecord(ev_[2], st_));
+  CodArgs c = cod_args();
+  launch_cod_pivqr(c, st_);
+  launches_ += 1;
+  // ranks decide the packed strides of everything downstream
+  std::vector<int> rank(2 * p.N), status(2 * p.N);
+  DDG_CUDA(cudaMemcpyAsync(rank.data(), d_rank.ptr, rank.size() * sizeof(int), cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaMemcpyAsync(status.data(), d_status.ptr, status.size() * sizeof(int), cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
+  for (int t = 0; t < 2 * p.N; ++t)
+    if (status[t] != 0)
+      throw CapacityError("numerical rank of local matrix " + std::to_string(t) + " exceeds the device COD capacity (" +
+                          std::to_string(kmax_) + ")");
+  int rmax = 1;
+  for (int r : rank) rmax = std::max(rmax, r);
+  rmax_ = rmax;
+  h_rank = rank;
+  const size_t nmat = 2 * static_cast<size_t>(p.N);
+  d_C.alloc(nmat * p.M * rmax_);
+  d_Y.alloc(nmat * p.M * rmax_);
+  d_QtX.alloc(nmat * rmax_ * ext_);
+  d_FC.alloc(static_cast<size_t>(p.N) * p.fmax * rmax_);
+  d_CCb.alloc(static_cast<size_t>(p.N) * p.dmax * rmax_);
+  d_s.alloc(static_cast<size_t>(p.N) * rmax_);
+  d_u.alloc(static_cast<size_t>(p.N) * rmax_);
+  c = cod_args();
+  launch_cod_finish(c, st_);
+  launches_ += 1;
+  DDG_CUDA(cudaEventRecord(ev_[3], st_));
+  built_ = true;
+  coarse_built_ = neumann_built_ = false;
+  host_build_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+}
+
+BlockArgs Workspace::block_args() {
+  const Plan& p = plan;
+  BlockArgs b;
+  b.N = p.N;
+  b.M = p.M;
+  b.rmax = rmax_;
+  b.ext = ext_;
+  b.gmax = p.gmax;
+  b.fmax = p.fmax;
+  b.dmax = p.dmax;
+  b.crmax = p.crmax;
+  b.ldF = p.fmax;
+  b.ldC = p.dmax;
+  b.n_pi = p.n_pi;
+  b.npf = p.npf;
+  b.n_delta = p.n_delta;
+  b.rank = d_rank.ptr;
+  b.dims = d_dims.ptr;
+  b.sub_cls = d_cls.ptr;
+  b.F = d_F.ptr;
+  b.Cd = d_Cd.ptr;
+  b.C = d_C.ptr;
+  b.QtX = d_QtX.ptr;
+  b.FC = d_FC.ptr;
+  b.CCb = d_CCb.ptr;
+  b.gamma_pi = d_gamma_pi.ptr;
+  b.cr_row = d_cr_row.ptr;
+  b.cr_off = d_cr_off.ptr;
+  b.cr_l = d_cr_l.ptr;
+  b.cr_w = d_cr_w.ptr;
+  b.Zc = d_Zc.ptr;
+  b.pd = d_pd.ptr;
+  b.Gc = d_Gc.ptr;
+  b.corner_q = d_corner_q.ptr;
+  b.Dpp = d_Dpp.ptr;
+  b.dpi = d_dpi.ptr;
+  b.S = d_S.ptr;
+  b.Sinv = d_Sinv.ptr;
+  b.mult_pi = d_mult_pi.ptr;
+  b.spd_fail = d_spd_fail.ptr;
+  b.flip_row = p.debug_flip_flux_row;
+  b.row_owner = d_row_owner.ptr;
+  return b;
+}
+
+void Workspace::build_coarse() {
+  if (!built_) build();
+  if (coarse_built_) return;
+  DDG_CUDA(cudaSetDevice(device_));
+  DDG_CUDA(cudaEventRecord(ev_[4], st_));
+  BlockArgs b = block_args();
+  DDG_CUDA(cudaMemsetAsync(d_spd_fail.ptr, 0, sizeof(int), st_));
+  launch_blocks(b, false, st_);
+  launch_coarse_local(b, d_cr_row.ptr, d_cr_off.ptr, d_cr_l.ptr, d_cr_w.ptr, st_);
+  launches_ += 2;
+  if (plan.n_pi > 0) {
+    launch_coarse_rows(b, d_row_owner.ptr, st_);
+    launch_coarse_schur(b, st_);
+    launches_ += 2;
+  }
+  DDG_CUDA(cudaEventRecord(ev_[5], st_));
+  int fail = 0;
+  DDG_CUDA(cudaMemcpyAsync(&fail, d_spd_fail.ptr, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
+  if (fail) throw std::runtime_error("assemble_coarse: coarse Schur matrix is not positive definite");
+  coarse_built_ = true;
+}
+
+void Workspace::build_neumann() {
+  build_coarse();
+  if (neumann_built_) return;
+  DDG_CUDA(cudaSetDevice(device_));
+  DDG_CUDA(cudaEventRecord(ev_[6], st_));
+  launch_blocks(block_args(), true, st_);
+  launches_ += 1;
+  DDG_CUDA(cudaEventRecord(ev_[7], st_));
+  neumann_built_ = true;
+}
+
+CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
+  const Plan& p = plan;
+  CgArgs a;
+  a.N = p.N;
+  a.n_delta = p.n_delta;
+  a.n_pi = p.n_pi;
+  a.npf = p.npf;
+  a.gmax = p.gmax;
+  a.fmax = p.fmax;
+  a.dmax = p.dmax;
+  a.crmax = p.crmax;
+  a.rmax = rmax_;
+  a.ext = ext_;
+  a.M = p.M;
+  a.theta = theta;
+  a.use_neumann = theta > 0.0 ? 1 : 0;
+  {
+    const char* op = std::getenv("DDELM_OPERATOR");
+    a.coeff_space = (op && std::strcmp(op, "coeff") == 0) ? 1 : 0;
+  }
+  a.F = d_F.ptr;
+  a.ldF = p.fmax;
+  d_cwork.alloc(static_cast<size_t>(p.N) * p.M);
+  a.cwork = d_cwork.ptr;
+  a.rel_tol = tol;
+  a.max_iter = max_iter;
+  a.rank = d_rank.ptr;
+  a.dims = d_dims.ptr;
+  a.sub_cls = d_cls.ptr;
+  a.gamma_delta = d_gamma_delta.ptr;
+  a.gamma_pi = d_gamma_pi.ptr;
+  a.fluxrow_delta = d_fluxrow_delta.ptr;
+  a.ndelta_map = d_ndelta_map.ptr;
+  a.cr_row = d_cr_row.ptr;
+  a.corner_q = d_corner_q.ptr;
+  a.own_gamma = d_own_gamma.ptr;
+  a.own_flux = d_own_flux.ptr;
+  a.own_nd = d_own_nd.ptr;
+  a.pi_owner = d_pi_owner.ptr;
+  a.row_owner = d_row_owner.ptr;
+  a.flip_sign = d_flip.ptr;
+  a.QtX = d_QtX.ptr;
+  a.FC = d_FC.ptr;
+  a.CCb = d_CCb.ptr;
+  a.Zc = d_Zc.ptr;
+  a.Dpp = d_Dpp.ptr;
+  a.Sinv = d_Sinv.ptr;
+  a.dpi = d_dpi.ptr;
+  a.C = d_C.ptr;
+  a.s = d_s.ptr;
+  a.tpart = d_tpart.ptr;
+  a.psipart = d_psipart.ptr;
+  a.mu = d_mu.ptr;
+  a.d1 = d_d1.ptr;
+  a.d2 = d_d2.ptr;
+  a.o = d_o.ptr;
+  a.xf = d_xf.ptr;
+  a.tr = d_tr.ptr;
+  a.zz = d_zz.ptr;
+  a.u = d_u.ptr;
+  a.nu = d_nu.ptr;
+  a.bot = d_bot.ptr;
+  a.x = d_x.ptr;
+  a.r = d_r.ptr;
+  a.p = d_p.ptr;
+  a.Ap = d_Ap.ptr;
+  a.rhs = d_rhs.ptr;
+  a.partial = d_partial.ptr;
+  a.hist = d_hist.ptr;
+  a.state = d_state.ptr;
+  a.scal = d_scal.ptr;
+  a.coeffs = d_coeffs.ptr;
+  a.mu_pi_out = d_mu_pi_out.ptr;
+  return a;
+}
+
+void Workspace::run_cg_graph(const CgArgs& a) {
+  const char* mode = std::getenv("DDELM_CG_MODE");
+  const bool use_cond = !(mode && std::strcmp(mode, "loop") == 0);
+  if (graph_exec_) {
+    cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+  }
+  if (graph_) {
+    cudaGraphDestroy(graph_);
+    graph_ = nullptr;
+  }
+  if (use_cond) {
+    DDG_CUDA(cudaGraphCreate(&graph_, 0));
+    cudaGraphConditionalHandle h;
+    DDG_CUDA(cudaGraphConditionalHandleCreate(&h, graph_, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    DDG_CUDA(cudaGraphAddNode(&node, graph_, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    DDG_CUDA(cudaStreamBeginCaptureToGraph(cap_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    cg_launch_step(a, cap_, static_cast<unsigned long long>(h), true);
+    DDG_CUDA(cudaStreamEndCapture(cap_, &body));
+    DDG_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
+    DDG_CUDA(cudaGraphLaunch(graph_exec_, st_));
+  } else {
+    // fallback: a graph of 16 iterations, relaunched until the device flags completion
+    DDG_CUDA(cudaStreamBeginCapture(cap_, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < 16; ++k) cg_launch_step(a, cap_, 0ull, false);
+    DDG_CUDA(cudaStreamEndCapture(cap_, &graph_));
+    DDG_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
+    for (;;) {
+      DDG_CUDA(cudaGraphLaunch(graph_exec_, st_));
+      DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+      DDG_CUDA(cudaStreamSynchronize(st_));
+      if (pinned_state_[1]) break;
+    }
+  }
+}
+
+SolveResult Workspace::solve(int method, double theta, double tol, int max_iter) {
+  if (method == 2 && (theta < 0.0 || theta > 1.0))
+    throw std::invalid_argument("ddelm_nn_solve: theta must lie in [0, 1]");
+  if (method == 0) throw std::invalid_argument("method ddelm (one-level) is not on the device path");
+  if (method == 1 || theta == 0.0) {
+    method = 1;
+    theta = 0.0;
+  }
+  DDG_CUDA(cudaSetDevice(device_));
+  const auto h0 = std::chrono::steady_clock::now();
+  const long long l0 = launches_;
+  if (!built_) build();
+  build_coarse();
+  if (method == 2) build_neumann();
+  const Plan& p = plan;
+  SolveResult res;
+  if (max_iter <= 0) max_iter = 20 * p.n_delta;
+  if (p.n_delta == 0) throw std::invalid_argument("s = 1 (local-only solve) is not on the device path");
+  d_hist.alloc(static_cast<size_t>(max_iter));
+  CgArgs a = cg_args(theta, tol, max_iter);
+  DDG_CUDA(cudaEventRecord(ev_[8], st_));
+  cg_launch_operator(a, nullptr, d_rhs.ptr, 1, st_);
+  cg_launch_init(a, st_);
+  launches_ += cg_kernels_per_step(a) - 3 + 2;
+  DDG_CUDA(cudaEventRecord(ev_[9], st_));
+  run_cg_graph(a);
+  DDG_CUDA(cudaEventRecord(ev_[10], st_));
+  cg_launch_reconstruct(a, st_);
+  launches_ += 3;
+  DDG_CUDA(cudaEventRecord(ev_[11], st_));
+  int state[8];
+  DDG_CUDA(cudaMemcpyAsync(state, d_state.ptr, sizeof(state), cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
+  res.iterations = state[5];
+  res.converged = state[2] != 0;
+  res.negative_curvature = state[3] != 0;
+  // every iteration runs the whole captured step (kernels no-op only after completion)
+  launches_ += static_cast<long long>(std::max(res.iterations, 1)) * cg_kernels_per_step(a);
+  last_iterations_ = res.iterations;
+  auto ms = [&](int e0, int e1) {
+    float t = 0;
+    cudaEventElapsedTime(&t, ev_[e0], ev_[e1]);
+    return static_cast<double>(t);
+  };
+  phase_ms_[0] = ms(0, 1);   // features
+  phase_ms_[1] = ms(1, 2);   // unpivoted QR
+  phase_ms_[2] = ms(2, 3);   // COD
+  phase_ms_[3] = ms(4, 5);   // coarse
+  phase_ms_[4] = method == 2 ? ms(6, 7) : 0.0;  // neumann blocks
+  phase_ms_[5] = ms(8, 9);   // reduced rhs
+  phase_ms_[6] = ms(9, 10);  // cg
+  phase_ms_[7] = ms(10, 11); // reconstruct
+  res.phase_ms.assign(phase_ms_, phase_ms_ + 8);
+  res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+  solve_launches_ = launches_ - l0;
+  solved_ = true;
+  return res;
+}
+
+void Workspace::apply_operator(double theta, const double* v, double* out) {
+  DDG_CUDA(cudaSetDevice(device_));
+  if (!built_) build();
+  build_coarse();
+  if (theta > 0.0) build_neumann();
+  CgArgs a = cg_args(theta, 1e-9, 1);
+  const size_t nd = plan.n_delta;
+  DDG_CUDA(cudaMemsetAsync(d_state.ptr, 0, 8 * sizeof(int), st_));
+  DDG_CUDA(cudaMemcpyAsync(d_p.ptr, v, nd * sizeof(double), cudaMemcpyHostToDevice, st_));
+  cg_launch_operator(a, d_p.ptr, d_Ap.ptr, 0, st_);
+  DDG_CUDA(cudaMemcpyAsync(out, d_Ap.ptr, nd * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Workspace::get_mu(double* mu) {
+  const Plan& p = plan;
+  DDG_CUDA(cudaMemcpy(mu, d_x.ptr, sizeof(double) * p.n_delta, cudaMemcpyDeviceToHost));
+  if (p.n_pi) DDG_CUDA(cudaMemcpy(mu + p.n_delta, d_mu_pi_out.ptr, sizeof(double) * p.n_pi, cudaMemcpyDeviceToHost));
+}
+
+void Workspace::get_coeffs(double* c) {
+  DDG_CUDA(cudaMemcpy(c, d_coeffs.ptr, sizeof(double) * plan.N * plan.M, cudaMemcpyDeviceToHost));
+}
+
+int Workspace::get_residuals(double* h, int cap) {
+  const int n = std::min(cap, last_iterations_);
+  if (n > 0) DDG_CUDA(cudaMemcpy(h, d_hist.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return n;
+}
+
+void Workspace::get_ranks(int* rk, int* rkb, double* ratio) {
+  const int N = plan.N;
+  std::vector<double> rt(4 * static_cast<size_t>(N));
+  DDG_CUDA(cudaMemcpy(rt.data(), d_ratio.ptr, rt.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < N; ++i) {
+    rk[i] = built_ ? h_rank[i] : -1;
+    rkb[i] = built_ ? h_rank[N + i] : -1;
+    if (ratio) {
+      ratio[2 * i] = rt[2 * i + 1] > 0 ? rt[2 * i] / rt[2 * i + 1] : 0.0;
+      ratio[2 * i + 1] = rt[2 * (N + i) + 1] > 0 ? rt[2 * (N + i)] / rt[2 * (N + i) + 1] : 0.0;
+    }
+  }
+}
+
+void Workspace::get_local(int i, int which, double* K) {
+  // The factorisation overwrites the matrices in place, so re-run the feature kernel (with the
+  // current seed's layers) and invalidate the built layers.
+  init_layers();
+  launch_build_features(feature_args(), st_);
+  const size_t t = static_cast<size_t>(which ? plan.N + i : i);
+  DDG_CUDA(cudaMemcpy2DAsync(K, sizeof(double) * plan.m, d_A.ptr + t * ld_ * ncol_, sizeof(double) * ld_,
+                             sizeof(double) * plan.m, plan.M, cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
+  built_ = coarse_built_ = neumann_built_ = false;
+}
+
+}  // namespace ddg

@@ -1,0 +1,108 @@
+// Device workspace of the DDELM-NN hot path (see workspace.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+
+namespace ddg {
+
+struct CapacityError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { free(); }
+  void alloc(size_t n);
+  void free();
+  void upload(const std::vector<T>& v, cudaStream_t st);
+};
+
+struct SolveResult {
+  int iterations = 0;
+  bool converged = false, negative_curvature = false;
+  std::vector<double> phase_ms;  // features, qr, cod, coarse, neumann, rhs, cg, reconstruct
+  double host_ms = 0;
+};
+
+class Workspace {
+ public:
+  Workspace(const Plan& p, int device);
+  ~Workspace();
+  Workspace(const Workspace&) = delete;
+  Workspace& operator=(const Workspace&) = delete;
+
+  void build();
+  void build_coarse();
+  void build_neumann();
+  SolveResult solve(int method, double theta, double tol, int max_iter);
+  void reseed(uint64_t seed);
+  void apply_operator(double theta, const double* v, double* out);
+
+  void get_mu(double* mu);
+  void get_coeffs(double* c);
+  int get_residuals(double* h, int cap);
+  void get_ranks(int* rk, int* rkb, double* ratio);
+  void get_local(int i, int which, double* K);
+  const double* phase_ms() const { return phase_ms_; }
+  long long launches() const { return solve_launches_; }
+  double host_build_ms() const { return host_build_ms_; }
+  int rmax() const { return rmax_; }
+  cudaStream_t stream() const { return st_; }
+
+  Plan plan;
+  std::vector<double> h_w0, h_w1, h_b;
+  std::vector<int> h_rank;
+
+ private:
+  void upload_plan();
+  void init_layers();
+  FeatureArgs feature_args();
+  CodArgs cod_args();
+  BlockArgs block_args();
+  CgArgs cg_args(double theta, double tol, int max_iter);
+  void run_cg_graph(const CgArgs& a);
+
+  int device_ = 0;
+  cudaStream_t st_ = nullptr, cap_ = nullptr;
+  cudaEvent_t ev_[12] = {};
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  int* pinned_state_ = nullptr;
+  int ld_ = 0, ext_ = 0, ncol_ = 0, kmax_ = 0, rmax_ = 1;
+  bool built_ = false, coarse_built_ = false, neumann_built_ = false, solved_ = false;
+  int last_iterations_ = 0;
+  long long launches_ = 0, solve_launches_ = 0;
+  double phase_ms_[8] = {};
+  double host_build_ms_ = 0;
+
+  // plan tables
+  DevBuf<Task> d_tasks;
+  DevBuf<int> d_task_off, d_task_cnt, d_cls, d_ix, d_iy, d_gamma_delta, d_gamma_pi, d_fluxrow_delta,
+      d_ndelta_map, d_cr_row, d_cr_off, d_cr_l, d_row_owner, d_pi_owner, d_own_gamma, d_own_flux,
+      d_own_nd, d_mult_pi;
+  DevBuf<ClassDims> d_dims;
+  DevBuf<double> d_cr_w, d_flip, d_f;
+  // layers and matrices
+  DevBuf<double> d_w0, d_w1, d_b, d_A, d_tau, d_T, d_ratio, d_F, d_Cd;
+  DevBuf<int> d_deficient, d_rank, d_status, d_perm, d_corner_q, d_spd_fail, d_state;
+  DevBuf<double> d_V1, d_F1, d_Rr, d_tau1, d_zc, d_upd, d_dir, d_C, d_Y, d_QtX;
+  // interface blocks / coarse
+  DevBuf<double> d_FC, d_CCb, d_Zc, d_pd, d_Gc, d_Dpp, d_dpi, d_S, d_Sinv;
+  // CG
+  DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu, d_nu, d_mu_pi_out, d_d1,
+      d_d2, d_bot, d_tpart, d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_cwork;
+};
+
+}  // namespace ddg

@@ -1,0 +1,72 @@
+"""CPU tests of the C-ABI boundary: the library loads, exports exactly what include/ddelm_gpu.h
+declares, and fails loudly (no CPU fallback) when there is no CUDA device."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_2503_10032_b200 as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ddelm_gpu.h")
+
+
+def header_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(ddelm_gpu_\w+)\s*\(", text)))
+
+
+def test_header_matches_python_exports():
+    assert header_symbols() == sorted(P.EXPORTS)
+
+
+def test_library_exports_every_header_symbol():
+    L = P.load_library()
+    for name in header_symbols():
+        assert hasattr(L, name), name
+    assert b"sm_100a" in L.ddelm_gpu_version()
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """Compile a C probe against the header: the ctypes mirrors must have the same layout."""
+    import subprocess
+    src = tmp_path / "probe.c"
+    src.write_text('''#include <stdio.h>
+#include <stddef.h>
+#include "ddelm_gpu.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu\\n", sizeof(ddelm_desc), sizeof(ddelm_report),
+         offsetof(ddelm_desc, seed), offsetof(ddelm_desc, rank_tol), offsetof(ddelm_report, total_seconds));
+  return 0;
+}
+''')
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert vals == [C.sizeof(P._Desc), C.sizeof(P._Report), P._Desc.seed.offset,
+                    P._Desc.rank_tol.offset, P._Report.total_seconds.offset]
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-device error path")
+def test_no_device_fails_loudly():
+    with pytest.raises(RuntimeError, match="no CUDA device|CUDA"):
+        P.Workspace("poisson_sinpi", 2, 10, 64, 8.0, 1)
+
+
+def test_invalid_arguments_mirror_reference():
+    with pytest.raises(ValueError):
+        P.make_problem("no_such_problem")
+    with pytest.raises(ValueError):
+        P.ddelm_nn_solve(None, 1.5)
+    with pytest.raises(ValueError):
+        P.SolverOptions(flux_variant="bogus") and P.Workspace("poisson_sinpi", 2, 10, 64, 8.0, 1,
+                                                              P.SolverOptions(flux_variant="bogus"))
