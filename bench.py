@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""bench.py — DDELM-NN solve throughput on B200 (driver contract).
+
+A step is one complete DDELM-NN solve of the named BASELINE config (default C3: 8x8
+subdomains, M=800, the config BASELINE.json's metric is quoted on at 1/2/4/8 GPUs): feature /
+collocation build, batched QR + COD of every K_i and Kbar_i, coarse + Neumann layers, reduced
+RHS, the interface CG to rel 1e-9 and the coefficient reconstruction.
+
+  value  subdomains/s with inputs (the seeded feature layers) resident in HBM; device time from
+         CUDA events on the library's stream, K steps bracketed by barrier + synchronize.
+  e2e    the same through the public C-ABI from the host: reseed (host RNG -> pinned -> H2D),
+         solve, D2H of coefficients and mu, every step.
+
+--impl reference times the reference's CPU algorithm (the oracle restatement; the reference
+itself cannot be built here) on the host cores, bounded sample + extrapolation.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.2  # measured DMMA loop on this pool's B200 (profiles/r01_fp64_peaks.json)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm = 6554.2
+    try:
+        with open(p) as f:
+            hbm = float(json.load(f).get("hbm_gbs", hbm))
+    except Exception:  # noqa: BLE001
+        pass
+    return hbm
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def dist_init(world):
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if backend == "nccl":
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dist.init_process_group(backend)
+    return dist
+
+
+def max_over_ranks(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# --------------------------------------------------------------------------- CPU (oracle)
+def cpu_solve_sample(cfg_name: str, cg_iters: int = 5):
+    """Bounded sample of the reference algorithm on the host (oracle restatement): full
+    Workspace build (all local factorisations, workers = nproc as the reference's only knob),
+    coarse + Neumann layers and `cg_iters` CG iterations; the CG is extrapolated to the golden
+    iteration count."""
+    import numpy as np
+
+    from oracle.pyoracle import OracleWorkspace
+    from paper_2503_10032_b200.configs import CONFIGS
+
+    c = CONFIGS[cfg_name]
+    nproc = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    ws = OracleWorkspace(problem=c["problem"], s=c["s"], n_grid=c["n_grid"], M=c["M"], l=c["l"],
+                         seed=c["seed"], flux_variant=c["flux_variant"],
+                         trace_basis=c["trace_basis"], workers=nproc, cg_workers=nproc)
+    t1 = time.perf_counter()
+    r = ws.solve(c["method"], c["theta"], c["cg_rel_tol"], 0, cg_iters)
+    t2 = time.perf_counter()
+    tim = r.timings
+    per_it = tim["cg"] / max(r.iterations, 1)
+    gpath = os.path.join(ROOT, "tests", "golden", f"{cfg_name}.npz")
+    golden_it = int(np.load(gpath)["iterations"]) if os.path.exists(gpath) else r.iterations
+    total = (t1 - t0) + tim["setup"] + per_it * golden_it + tim["reconstruction"]
+    return {"seconds_extrapolated": total, "build_s": t1 - t0, "setup_s": tim["setup"],
+            "cg_s_per_iter": per_it, "golden_iterations": golden_it, "cores": nproc,
+            "sample_wall_s": t2 - t0,
+            "sample": (f"{cfg_name}: full Workspace build ({2 * c['s'] ** 2} local LS factorisations, "
+                       f"{nproc} workers) + coarse/Neumann + {r.iterations} CG iterations; CG "
+                       f"extrapolated to the oracle's {golden_it} iterations")}
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    nsub = cfg["s"] ** 2
+    for _ in range(args.warmup):
+        cpu_solve_sample(args.config, args.cpu_cg_iters)
+    secs = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_solve_sample(args.config, args.cpu_cg_iters)
+        secs.append(last["seconds_extrapolated"])
+    mean_s = sum(secs) / len(secs)
+    value = nsub / mean_s
+    line = {"impl": "reference", "metric": "ddelm_nn_solve_throughput", "value": value,
+            "unit": "subdomains/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, cfg),
+            "cpu_baseline": {"value": value, "unit": "subdomains/s", "cores": last["cores"],
+                             "kind": "port", "sample": last["sample"]},
+            "e2e": {"value": value, "unit": "subdomains/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "solve_seconds": mean_s, "detail": last}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, cfg):
+    return {"workload": f"{args.config}: DDELM-NN (theta {cfg['theta']}) {cfg['s']}x{cfg['s']} subdomains, "
+                        f"M={cfg['M']}, n_grid={cfg['n_grid']}, l={cfg['l']}, {cfg['problem']}, "
+                        f"{cfg['flux_variant']} + {cfg['trace_basis']}, cg_rel_tol {cfg['cg_rel_tol']}",
+            "subdomains": cfg["s"] ** 2, "neurons_per_subdomain": cfg["M"],
+            "collocation_points_per_subdomain": cfg["n_grid"] ** 2,
+            "l2_policy": "working set (2N local matrices, >1 GB at C3) far exceeds the 126 MB L2",
+            "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU"}
+
+
+# --------------------------------------------------------------------------- ours
+def run_ours(args, cfg, world, rank, local, dist):
+    import torch
+
+    import paper_2503_10032_b200 as P
+
+    torch.cuda.set_device(local)
+    ws = P.workspace_from_config(args.config, device=local)
+    cg = P.CgOptions(rel_tol=cfg["cg_rel_tol"])
+    theta = cfg["theta"] if cfg["method"] == "ddelm-nn" else 0.0
+    nsub = cfg["s"] ** 2
+    M = cfg["M"]
+    seed = cfg["seed"]
+    stream = torch.cuda.ExternalStream(ws.stream_handle)
+
+    def solve(fetch=True):
+        return ws._solve("ddelm-nn" if theta > 0 else "ddelm-cs", theta, cg, fetch=fetch)
+
+    for _ in range(args.warmup):
+        ws.reseed(seed)
+        solve()
+    torch.cuda.synchronize()
+
+    # ---- device-resident throughput (value)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier(dist)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    iters, launches = [], 0
+    spans = []
+    for _ in range(args.steps):
+        ws.invalidate()
+        rep = solve(fetch=False)
+        iters.append(rep.iterations)
+        launches += rep.launches
+        spans.append(ws.device_span_ms())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    dev_ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    dev_ms_max = max_over_ranks(dist, dev_ms)
+    value = world * nsub * args.steps / (dev_ms_max / 1e3)
+
+    # ---- end-to-end through the public API (host buffers, H2D + D2H inside)
+    barrier(dist)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        ws.reseed(seed)
+        rep = solve()  # includes reading coefficients, mu and the residual history back
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    e2e_ms = max_over_ranks(dist, t0.elapsed_time(t1))
+    e2e_value = world * nsub * args.steps / (e2e_ms / 1e3)
+    n_mu = ws.n_delta + ws.n_pi
+    h2d = 3 * nsub * M * 8
+    d2h = (nsub * M + n_mu + max(rep.iterations, 1)) * 8
+
+    # ---- roofline: one profiled solve with per-kernel-family CUDA events
+    ws.set_profiling(True)
+    ws.invalidate()
+    solve()
+    ws.set_profiling(False)
+    fam = {}
+    for f in ("build_features", "qr_panel", "qr_trailing", "cod_pivqr", "cod_finish", "cg_iterations"):
+        try:
+            fam[f] = ws.kernel_stats(f)
+        except Exception:  # noqa: BLE001
+            pass
+    dominant = max(fam.items(), key=lambda kv: kv[1]["ms"])[0] if fam else None
+    hbm = load_peaks()
+    roof = None
+    if dominant:
+        s = fam[dominant]
+        if s["flops"] > 0:
+            ach = s["flops"] / (s["ms"] / 1e3) / 1e12
+            roof = {"kernel": dominant, "bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS,
+                    "peak_source": "measured FP64 DMMA loop (profiles/r01_fp64_peaks.json); "
+                                   "MEASURED_PEAKS.json carries no FP64 entry",
+                    "traffic": None, "launches": s["launches"], "avg_launch_ms": s["ms"] / s["launches"]}
+        else:
+            ach = s["bytes"] / (s["ms"] / 1e3) / 1e9 if s["bytes"] > 0 else None
+            roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": (ach / hbm) if ach else None, "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs", "launches": s["launches"],
+                    "avg_launch_ms": s["ms"] / s["launches"]}
+    qr = fam.get("qr_trailing")
+    families = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
+                    "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["flops"] else None,
+                    "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["bytes"] else None}
+                for k, v in fam.items()}
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        c = cpu_solve_sample(args.config, args.cpu_cg_iters)
+        cpu = {"value": nsub / c["seconds_extrapolated"], "unit": "subdomains/s", "cores": c["cores"],
+               "kind": "port", "sample": c["sample"], "seconds_extrapolated": c["seconds_extrapolated"]}
+    ms_step = dev_ms_max / args.steps
+    line = {"metric": "ddelm_nn_solve_throughput", "value": value, "unit": "subdomains/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded feature layers; manufactured Poisson data)",
+            "config": workload_config(args, cfg),
+            "solve_seconds": ms_step / 1e3, "iterations": iters,
+            "e2e": {"value": e2e_value, "unit": "subdomains/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
+            "roofline": roof, "kernel_families": families,
+            "phase_ms": {k: round(v, 3) for k, v in rep.phase_ms.items()},
+            "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
+            "fp64_trailing_tflops": (qr["flops"] / (qr["ms"] / 1e3) / 1e12) if qr else None}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--cpu-cg-iters", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_2503_10032_b200.configs import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+    dist = dist_init(world)
+    run_ours(args, cfg, world, rank, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

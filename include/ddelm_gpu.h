@@ -111,6 +111,18 @@ int ddelm_gpu_get_local(ddelm_ws* ws, int i, int which /* 0 K, 1 Kbar */, double
 /* out = cs_reduced_apply(v, weight) on the device (solvers.cpp:372-386, weight 599-603;
  * theta = 0: plain coarse operator). v, out: n_delta host doubles. Builds layers as needed. */
 int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double* out);
+/* Drop every built layer (features, factors, coarse, Neumann) but keep the feature layers
+ * already uploaded to the device: the next solve re-runs the whole device pipeline. */
+int ddelm_gpu_invalidate(ddelm_ws* ws);
+/* The workspace's CUDA stream (cudaStream_t), for callers that time on the device. */
+void* ddelm_gpu_stream(ddelm_ws* ws);
+/* Per-kernel-family CUDA-event timers (off by default). family: "build_features", "qr_panel",
+ * "qr_trailing", "cod_pivqr", "cod_finish", "cg_iterations". Values accumulate until reset. */
+int ddelm_gpu_set_profiling(ddelm_ws* ws, int on);
+int ddelm_gpu_get_kernel_stats(ddelm_ws* ws, const char* family, double* total_ms,
+                               long long* launches, double* flops, double* bytes);
+/* Device time of the last solve from the first feature kernel to the reconstruction (ms). */
+double ddelm_gpu_get_device_span_ms(ddelm_ws* ws);
 /* Per-phase device timings of the last build/solve (ms): see workspace.cu for the order. */
 int ddelm_gpu_get_phase_ms(ddelm_ws* ws, double* ms, int cap);
 /* Kernel launches issued by the last ddelm_gpu_build..solve sequence (own kernels only). */

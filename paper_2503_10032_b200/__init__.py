@@ -34,8 +34,9 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_build_coarse", "ddelm_gpu_build_neumann", "ddelm_gpu_solve",
            "ddelm_gpu_reseed", "ddelm_gpu_destroy", "ddelm_gpu_get_mu", "ddelm_gpu_get_coeffs",
            "ddelm_gpu_get_residuals", "ddelm_gpu_get_ranks", "ddelm_gpu_get_layer",
-           "ddelm_gpu_get_local", "ddelm_gpu_apply_operator", "ddelm_gpu_get_phase_ms",
-           "ddelm_gpu_get_launch_count")
+           "ddelm_gpu_get_local", "ddelm_gpu_apply_operator", "ddelm_gpu_invalidate",
+           "ddelm_gpu_stream", "ddelm_gpu_set_profiling", "ddelm_gpu_get_kernel_stats",
+           "ddelm_gpu_get_device_span_ms", "ddelm_gpu_get_phase_ms", "ddelm_gpu_get_launch_count")
 
 
 class _Desc(C.Structure):
@@ -82,6 +83,15 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_get_layer.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_get_local.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int)]
     L.ddelm_gpu_apply_operator.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_invalidate.argtypes = [C.c_void_p]
+    L.ddelm_gpu_stream.argtypes = [C.c_void_p]
+    L.ddelm_gpu_stream.restype = C.c_void_p
+    L.ddelm_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
+    L.ddelm_gpu_get_kernel_stats.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_double),
+                                             C.POINTER(C.c_longlong), C.POINTER(C.c_double),
+                                             C.POINTER(C.c_double)]
+    L.ddelm_gpu_get_device_span_ms.argtypes = [C.c_void_p]
+    L.ddelm_gpu_get_device_span_ms.restype = C.c_double
     L.ddelm_gpu_get_phase_ms.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
     L.ddelm_gpu_get_launch_count.argtypes = [C.c_void_p]
     L.ddelm_gpu_get_launch_count.restype = C.c_longlong
@@ -217,6 +227,26 @@ class Workspace:
         _check(load_library().ddelm_gpu_get_local(self._h, i, which, _ptr(K), C.byref(rows)))
         return K.T.copy()
 
+    def invalidate(self):
+        """Drop built layers, keep the device-resident feature layers."""
+        _check(load_library().ddelm_gpu_invalidate(self._h))
+
+    @property
+    def stream_handle(self) -> int:
+        return int(load_library().ddelm_gpu_stream(self._h) or 0)
+
+    def set_profiling(self, on: bool = True):
+        _check(load_library().ddelm_gpu_set_profiling(self._h, 1 if on else 0))
+
+    def kernel_stats(self, family: str) -> dict:
+        ms, n, fl, by = C.c_double(), C.c_longlong(), C.c_double(), C.c_double()
+        _check(load_library().ddelm_gpu_get_kernel_stats(self._h, family.encode(), C.byref(ms),
+                                                         C.byref(n), C.byref(fl), C.byref(by)))
+        return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+
+    def device_span_ms(self) -> float:
+        return float(load_library().ddelm_gpu_get_device_span_ms(self._h))
+
     def apply_operator(self, v: np.ndarray, theta: float = 0.999) -> np.ndarray:
         """cs_reduced_apply with the NN weight (theta = 0: coarse operator), on the device."""
         v = np.ascontiguousarray(v, dtype=np.float64)
@@ -224,7 +254,8 @@ class Workspace:
         _check(load_library().ddelm_gpu_apply_operator(self._h, float(theta), _ptr(v), _ptr(out)))
         return out
 
-    def _solve(self, method: str, theta: float, cg: CgOptions | None) -> SolveReport:
+    def _solve(self, method: str, theta: float, cg: CgOptions | None, fetch: bool = True) -> SolveReport:
+        """fetch=False leaves mu / coefficients / history on the device (device-resident timing)."""
         cg = cg or CgOptions()
         L = load_library()
         rep = _Report()
@@ -232,11 +263,13 @@ class Workspace:
                                  int(cg.max_iter), C.byref(rep)))
         nmu = rep.n_mu
         mu = np.zeros(nmu)
-        _check(L.ddelm_gpu_get_mu(self._h, _ptr(mu)))
         co = np.zeros((rep.n_subdomains, rep.M))
-        _check(L.ddelm_gpu_get_coeffs(self._h, _ptr(co)))
         hist = np.zeros(max(rep.iterations, 1))
-        n = L.ddelm_gpu_get_residuals(self._h, _ptr(hist), hist.size)
+        n = 0
+        if fetch:
+            _check(L.ddelm_gpu_get_mu(self._h, _ptr(mu)))
+            _check(L.ddelm_gpu_get_coeffs(self._h, _ptr(co)))
+            n = L.ddelm_gpu_get_residuals(self._h, _ptr(hist), hist.size)
         ms = np.zeros(8)
         L.ddelm_gpu_get_phase_ms(self._h, _ptr(ms), 8)
         names = ["features", "qr", "cod", "coarse", "neumann", "rhs", "cg", "reconstruct"]

@@ -154,6 +154,25 @@ int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double
     ws->w->apply_operator(theta, v, out);
   });
 }
+int ddelm_gpu_invalidate(ddelm_ws* ws) {
+  return guarded([&] { ws->w->invalidate(); });
+}
+void* ddelm_gpu_stream(ddelm_ws* ws) { return static_cast<void*>(ws->w->stream()); }
+int ddelm_gpu_set_profiling(ddelm_ws* ws, int on) {
+  return guarded([&] { ws->w->set_profiling(on != 0); });
+}
+int ddelm_gpu_get_kernel_stats(ddelm_ws* ws, const char* family, double* total_ms, long long* launches,
+                               double* flops, double* bytes) {
+  return guarded([&] {
+    ddg::KernelStat s;
+    if (!ws->w->kernel_stat(family ? family : "", &s)) throw std::invalid_argument("no timings for that kernel family");
+    if (total_ms) *total_ms = s.ms;
+    if (launches) *launches = s.launches;
+    if (flops) *flops = s.flops;
+    if (bytes) *bytes = s.bytes;
+  });
+}
+double ddelm_gpu_get_device_span_ms(ddelm_ws* ws) { return ws->w->device_span_ms(); }
 int ddelm_gpu_get_phase_ms(ddelm_ws* ws, double* ms, int cap) {
   const double* src = ws->w->phase_ms();
   const int n = cap < 8 ? cap : 8;

@@ -140,6 +140,15 @@ __global__ void __launch_bounds__(256) coarse_local_kernel(BlockArgs a, const in
         s += QtX[static_cast<size_t>(k) * E + 1 + cq[p]] * QtX[static_cast<size_t>(k) * E + 1 + cq[q]];
     a.Gc[static_cast<size_t>(i) * 16 + threadIdx.x] = -s;
   }
+  // Ypi = K^+ B_Pi = -C Q_Pi^T (the corner columns; solvers.cpp:287-289)
+  const double* Ci = a.C + static_cast<size_t>(i) * a.M * R;
+  for (int j = threadIdx.x; j < a.M; j += blockDim.x)
+    for (int q = 0; q < 4; ++q) {
+      double s = 0;
+      if (cq[q] >= 0)
+        for (int k = 0; k < r; ++k) s += Ci[static_cast<size_t>(j) * R + k] * QtX[static_cast<size_t>(k) * E + 1 + cq[q]];
+      a.Ypi[(static_cast<size_t>(i) * a.M + j) * 4 + q] = -s;
+    }
 }
 
 /// Dpp rows and dpi from per-subdomain contributions, in subdomain order (one CTA per row).

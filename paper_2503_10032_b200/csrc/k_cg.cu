@@ -1,34 +1,47 @@
 // Interface Krylov iteration of DDELM-NN on the device (sm_100a, fp64).
 //
 // cs_reduced_apply (solvers.cpp:372-386) with the theta-mixed Neumann-Neumann weight
-// (solvers.cpp:599-603), expressed on the interface-level blocks of k_blocks.cu:
-//   s    = Q_G^T phi (+ Q_r^T f)          phi = B_Delta v   (local, op1)
-//   mu   = S^{-1}(t + Dpp^T psi)          coarse solve     (one CTA, coarse1)
-//   s~   = s + Q_Pi^T mu ; x = -A_Delta C s~ = -FC s~       (op2)
-//   w    = theta P^T P x + (1 - theta) x  P = Cdelta Kbar^+ Bbar (nn1, nn2, op3)
-//   u    = FC^T a(w) ; nu = S^{-1} t'     (op3, coarse2)
-//   out  = gather over the two owners of each Delta index of
-//          -phi + Q_G (s~ + u + Q_Pi^T nu) + Zc^T (psi - Dpp mu - Dpp nu)  (op4, gather)
-// followed by the Hestenes-Stiefel CG update (solvers.cpp:82-119). All cross-subdomain sums are
-// gathers over precomputed owner lists in subdomain order: deterministic, no atomics.
+// (solvers.cpp:599-603), expressed on the per-subdomain factors of k_cod.cu / k_blocks.cu:
+//   op1   s = Q_G^T phi (+ Q_r^T f), corner rows of K K^+ phi, psi = Dpd v       (local)
+//   c1    mu = S^{-1}(t + Dpp^T psi), d1 = psi - Dpp mu                        (coarse)
+//   op2   c = K^+ phi - Ypi mu = C s - Ypi mu ; x = -A_Delta c = -F c           (local)
+//   nn1   P x   = Cdelta Kbar^+ (-x|flux rows)                                  (Neumann)
+//   nn2   P^T u = -(Kbar^+)^T Cdelta^T u |flux rows
+//   op3   w = theta P^T P x + (1-theta) x ; u = C^T (F^T a(w))                  (local)
+//   c2    nu = S^{-1} t' ; d2 = d1 - Dpp nu                                    (coarse)
+//   op4   out_i = -phi + Q_G (s~ + u + Q_Pi^T nu) + Zc^T d2                    (local)
+//   gather over the two owners of each Delta index, then the Hestenes-Stiefel CG update
+//   (solvers.cpp:82-119).
+// "coeff_space" keeps the reference's grouping (K^+ applied into coefficient space, then the
+// flux / Cdelta rows), which reproduces its finite-precision CG behaviour; the fused mode uses
+// pre-multiplied FC / CCb blocks (fewer bytes, converges in fewer iterations).
+//
+// The whole iteration loop runs as ONE persistent cooperative kernel: phases are separated by
+// grid-wide barriers, every CTA keeps identical copies of the CG scalars (sums of per-CTA
+// partials in a fixed order), so there is no host round trip and no atomics: deterministic.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 
 #include "common.cuh"
 #include "kernels.hpp"
+
+namespace cgs = cooperative_groups;
 
 namespace ddg {
 
 namespace {
 
 constexpr int kBlk = 256;
+constexpr int kPersistBlk = 512;
 
 struct SubCtx {
   ClassDims d;
   int r;
-  const double* QtX;  // (k, e) at QtX[k*E + e]; QGt(k, g) = e = 1 + g
+  const double* QtX;  // (k, e) at QtX[k*E + e]; Q_G^T(k, g) at e = 1 + g, Q_r^T f at e = 0
 };
 
-__device__ __forceinline__ SubCtx sub_ctx(const CgArgs& a, int t /* matrix index */, int i) {
+__device__ __forceinline__ SubCtx sub_ctx(const CgArgs& a, int t /* matrix */, int i /* subdomain */) {
   SubCtx c;
   c.d = a.dims[a.sub_cls[i]];
   c.r = a.rank[t];
@@ -36,24 +49,85 @@ __device__ __forceinline__ SubCtx sub_ctx(const CgArgs& a, int t /* matrix index
   return c;
 }
 
-__device__ __forceinline__ bool cg_done(const CgArgs& a) { return a.state && a.state[1] != 0; }
+/// Shared-memory carve-up used by every local phase.
+struct Smem {
+  double* v1;   // big  (phi / rhs / px / a)
+  double* cw;   // M    (coefficient-space vector)
+  double* s0;   // rmax
+  double* s1;   // rmax
+  double* red;  // blockDim (partials of coldot)
+};
+
+__device__ __forceinline__ Smem carve(const CgArgs& a) {
+  extern __shared__ double sm[];
+  const int big = max(max(a.gmax, a.fmax), a.dmax);
+  const int cwsize = max(a.M, 3 * a.n_pi + 2 * a.npf);  // also hosts the coarse-solve vectors
+  Smem s;
+  s.v1 = sm;
+  s.cw = s.v1 + big;
+  s.s0 = s.cw + cwsize;
+  s.s1 = s.s0 + a.rmax;
+  s.red = s.s1 + a.rmax;
+  return s;
+}
+
+// y[j] = sum_k A[j*lda + k] x[k], j < rows (warp per row; lanes over the contiguous k)
+__device__ __forceinline__ void rowdot(const double* A, size_t lda, int rows, int cols, const double* x,
+                                       double* y, double scale = 1.0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < rows; j += nw) {
+    const double* aj = A + static_cast<size_t>(j) * lda;
+    double acc = 0;
+    for (int k = lane; k < cols; k += 32) acc += aj[k] * x[k];
+    acc = warp_sum(acc);
+    if (lane == 0) y[j] = scale * acc;
+  }
+}
+
+// y[k] = sum_j A[j*lda + k] x[j], k < cols (threads over (k, row group); fixed-order combine)
+__device__ __forceinline__ void coldot(const double* A, size_t lda, int rows, int cols, const double* x,
+                                       double* y, double* red, double scale = 1.0) {
+  for (int k0 = 0; k0 < cols; k0 += blockDim.x) {
+    const int cc = min(cols - k0, static_cast<int>(blockDim.x));
+    const int pad = (cc + 31) & ~31;
+    const int groups = max(1, static_cast<int>(blockDim.x) / pad);
+    const int t = threadIdx.x;
+    const int k = t % pad, grp = t / pad;
+    double acc = 0;
+    if (grp < groups && k < cc) {
+      const double* ak = A + k0 + k;
+#pragma unroll 4
+      for (int j = grp; j < rows; j += groups) acc += ak[static_cast<size_t>(j) * lda] * x[j];
+    }
+    red[t] = acc;
+    __syncthreads();
+    if (t < cc) {
+      double s = 0;
+      for (int g = 0; g < groups; ++g) s += red[g * pad + t];
+      y[k0 + t] = scale * s;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ double gather_x(const CgArgs& a, int g) {
+  return a.flip_sign[g] * (a.xf[a.own_flux[2 * g]] + a.xf[a.own_flux[2 * g + 1]]);
+}
 
 // ---------------------------------------------------------------- op1: s, t-part, psi-part
-__global__ void __launch_bounds__(kBlk) op1_kernel(CgArgs a, const double* v, int mode, int guard) {
-  if (guard && cg_done(a)) return;
-  const int i = blockIdx.x;
+__device__ void dev_op1(const CgArgs& a, int i, const double* v, int mode) {
   const SubCtx c = sub_ctx(a, i, i);
   const int R = a.rmax, E = a.ext;
-  extern __shared__ double sm[];
-  double* phi = sm;          // gmax
-  double* s = phi + a.gmax;  // rmax
+  Smem sm = carve(a);
+  double* vg = sm.cw;   // v at the gamma points (0 at corners)
+  double* phi = sm.v1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int* gd = a.gamma_delta + static_cast<size_t>(i) * a.gmax;
   for (int g = threadIdx.x; g < c.d.n_gamma; g += blockDim.x) {
     const int dg = gd[g];
-    double ph = 0.0;
-    if (dg >= 0) ph = (mode == 0) ? -v[dg] : (mode == 2 ? v[dg] : 0.0);
-    phi[g] = ph;
+    const double vv = (dg >= 0 && mode != 1) ? v[dg] : 0.0;
+    vg[g] = vv;
+    phi[g] = (mode == 0) ? -vv : vv;  // B_Delta v = -v (operator); +mu_Delta (reconstruction)
   }
   __syncthreads();
   for (int k = warp; k < c.r; k += nw) {
@@ -64,7 +138,7 @@ __global__ void __launch_bounds__(kBlk) op1_kernel(CgArgs a, const double* v, in
     acc = warp_sum(acc);
     if (mode >= 1) acc += c.QtX[static_cast<size_t>(k) * E];
     if (lane == 0) {
-      s[k] = acc;
+      sm.s0[k] = acc;
       a.s[static_cast<size_t>(i) * R + k] = acc;
     }
   }
@@ -74,33 +148,24 @@ __global__ void __launch_bounds__(kBlk) op1_kernel(CgArgs a, const double* v, in
     const int g = cq[warp];
     double acc = 0;
     if (g >= 0)
-      for (int k = lane; k < c.r; k += 32) acc += c.QtX[static_cast<size_t>(k) * E + 1 + g] * s[k];
+      for (int k = lane; k < c.r; k += 32) acc += c.QtX[static_cast<size_t>(k) * E + 1 + g] * sm.s0[k];
     acc = warp_sum(acc);
-    if (lane == 0) a.tpart[i * 4 + warp] = acc;
+    if (lane == 0) a.tpart[i * 4 + warp] = acc;  // t(gp) -= phi - Ky at corners (phi = 0 there)
   }
-  if (mode != 1) {
-    for (int rho = warp; rho < a.crmax; rho += nw) {
-      const double* z = a.Zc + (static_cast<size_t>(i) * a.crmax + rho) * a.gmax;
-      double acc = 0;
-      for (int g = lane; g < c.d.n_gamma; g += 32) {
-        const int dg = gd[g];
-        if (dg >= 0) acc += z[g] * v[dg];
-      }
-      acc = warp_sum(acc);
-      if (lane == 0) a.psipart[static_cast<size_t>(i) * a.crmax + rho] = acc;
-    }
-  }
+  if (mode != 1)
+    rowdot(a.Zc + static_cast<size_t>(i) * a.crmax * a.gmax, a.gmax, a.crmax, c.d.n_gamma, vg,
+           a.psipart + static_cast<size_t>(i) * a.crmax);
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- coarse solves (one CTA)
-__global__ void __launch_bounds__(kBlk) coarse1_kernel(CgArgs a, int mode, int guard) {
-  if (guard && cg_done(a)) return;
-  extern __shared__ double sm[];
+__device__ void dev_coarse1(const CgArgs& a, int mode) {
+  Smem sm = carve(a);
   const int n = a.n_pi, npf = a.npf;
-  double* t = sm;         // n
-  double* psi = t + n;    // npf
-  double* rhs = psi + npf;  // n
-  double* mu = rhs + n;   // n
+  double* t = sm.cw;       // n
+  double* psi = t + n;     // npf
+  double* rhs = psi + npf; // n
+  double* mu = rhs + n;    // n
   for (int gp = threadIdx.x; gp < n; gp += blockDim.x) {
     double acc = 0;
     for (int q = 0; q < 4; ++q) {
@@ -119,36 +184,29 @@ __global__ void __launch_bounds__(kBlk) coarse1_kernel(CgArgs a, int mode, int g
     psi[rr] = (mode == 0) ? acc : (mode == 1 ? a.dpi[rr] : a.dpi[rr] - acc);
   }
   __syncthreads();
-  for (int gp = threadIdx.x; gp < n; gp += blockDim.x) {
-    double acc = 0;
-    for (int rr = 0; rr < npf; ++rr) acc += a.Dpp[static_cast<size_t>(rr) * n + gp] * psi[rr];
-    rhs[gp] = t[gp] + acc;
-  }
+  coldot(a.Dpp, n, npf, n, psi, rhs, sm.red);  // Dpp^T psi
+  for (int gp = threadIdx.x; gp < n; gp += blockDim.x) rhs[gp] += t[gp];
+  __syncthreads();
+  rowdot(a.Sinv, n, n, n, rhs, mu);
   __syncthreads();
   for (int gp = threadIdx.x; gp < n; gp += blockDim.x) {
-    double acc = 0;
-    for (int q = 0; q < n; ++q) acc += a.Sinv[static_cast<size_t>(gp) * n + q] * rhs[q];
-    mu[gp] = acc;
-    a.mu[gp] = acc;
-    if (mode == 2) a.mu_pi_out[gp] = acc;
+    a.mu[gp] = mu[gp];
+    if (mode == 2) a.mu_pi_out[gp] = mu[gp];
+  }
+  if (mode != 2) {
+    double* pb = mu + n;  // npf: proj_bottom = Dpp mu
+    rowdot(a.Dpp, n, npf, n, mu, pb);
+    __syncthreads();
+    for (int rr = threadIdx.x; rr < npf; rr += blockDim.x) a.d1[rr] = psi[rr] - pb[rr];
   }
   __syncthreads();
-  if (mode != 2)
-    for (int rr = threadIdx.x; rr < npf; rr += blockDim.x) {
-      double acc = 0;
-      for (int gp = 0; gp < n; ++gp) acc += a.Dpp[static_cast<size_t>(rr) * n + gp] * mu[gp];
-      a.d1[rr] = psi[rr] - acc;
-    }
 }
 
-// ---------------------------------------------------------------- op2: s~, xf (or coefficients)
-__global__ void __launch_bounds__(kBlk) op2_kernel(CgArgs a, int mode, int guard) {
-  if (guard && cg_done(a)) return;
-  const int i = blockIdx.x;
+// ---------------------------------------------------------------- op2: s~, x (or coefficients)
+__device__ void dev_op2(const CgArgs& a, int i, int mode) {
   const SubCtx c = sub_ctx(a, i, i);
   const int R = a.rmax, E = a.ext;
-  extern __shared__ double sm[];
-  double* st = sm;  // rmax
+  Smem sm = carve(a);
   __shared__ double muc[4];
   __shared__ int gq[4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -159,122 +217,95 @@ __global__ void __launch_bounds__(kBlk) op2_kernel(CgArgs a, int mode, int guard
   }
   __syncthreads();
   for (int k = threadIdx.x; k < c.r; k += blockDim.x) {
-    double acc = a.s[static_cast<size_t>(i) * R + k];
+    const double sk = a.s[static_cast<size_t>(i) * R + k];
+    double acc = sk;
     for (int q = 0; q < 4; ++q)
       if (gq[q] >= 0) acc += c.QtX[static_cast<size_t>(k) * E + 1 + gq[q]] * muc[q];
-    st[k] = acc;
-    a.s[static_cast<size_t>(i) * R + k] = acc;
+    sm.s0[k] = sk;
+    sm.s1[k] = acc;
+    a.s[static_cast<size_t>(i) * R + k] = acc;  // s~ = s + Q_Pi^T mu
   }
   __syncthreads();
-  if (mode == 2) {
-    const double* Ci = a.C + static_cast<size_t>(i) * a.M * R;
-    for (int j = threadIdx.x; j < a.M; j += blockDim.x) {
-      double acc = 0;
-      for (int k = 0; k < c.r; ++k) acc += Ci[static_cast<size_t>(j) * R + k] * st[k];
-      a.coeffs[static_cast<size_t>(i) * a.M + j] = acc;
-    }
-    return;
-  }
+  const double* Ci = a.C + static_cast<size_t>(i) * a.M * R;
   if (a.coeff_space) {
-    // reference order: c = K^+ phi - Ypi mu (M-vector), then F c
-    const double* Ci = a.C + static_cast<size_t>(i) * a.M * R;
-    double* cw = a.cwork + static_cast<size_t>(i) * a.M;
+    // reference grouping (solvers.cpp:336, 342): c = K^+ phi - Ypi mu, then F c
+    const double* Yp = a.Ypi + static_cast<size_t>(i) * a.M * 4;
+    double* cw = (mode == 2) ? a.coeffs + static_cast<size_t>(i) * a.M : sm.cw;
     for (int j = warp; j < a.M; j += nw) {
+      const double* cj = Ci + static_cast<size_t>(j) * R;
       double acc = 0;
-      for (int k = lane; k < c.r; k += 32) acc += Ci[static_cast<size_t>(j) * R + k] * st[k];
+      for (int k = lane; k < c.r; k += 32) acc += cj[k] * sm.s0[k];
       acc = warp_sum(acc);
-      if (lane == 0) cw[j] = acc;
+      if (lane == 0) {
+        double yp = 0;
+        for (int q = 0; q < 4; ++q) yp += Yp[static_cast<size_t>(j) * 4 + q] * muc[q];
+        cw[j] = acc - yp;
+      }
     }
     __syncthreads();
-    const double* Fi = a.F + static_cast<size_t>(i) * a.M * a.ldF;
-    for (int l = threadIdx.x; l < c.d.nF; l += blockDim.x) {
-      double acc = 0;
-      for (int j = 0; j < a.M; ++j) acc += Fi[static_cast<size_t>(j) * a.ldF + l] * cw[j];
-      a.xf[static_cast<size_t>(i) * a.fmax + l] = -acc;
-    }
+    if (mode == 2) return;
+    coldot(a.F + static_cast<size_t>(i) * a.M * a.ldF, a.ldF, a.M, c.d.nF, sm.cw,
+           a.xf + static_cast<size_t>(i) * a.fmax, sm.red, -1.0);
     return;
   }
-  const double* FC = a.FC + static_cast<size_t>(i) * a.fmax * R;
-  for (int l = warp; l < c.d.nF; l += nw) {
-    double acc = 0;
-    for (int k = lane; k < c.r; k += 32) acc += FC[static_cast<size_t>(l) * R + k] * st[k];
-    acc = warp_sum(acc);
-    if (lane == 0) a.xf[static_cast<size_t>(i) * a.fmax + l] = -acc;
+  if (mode == 2) {
+    rowdot(Ci, R, a.M, c.r, sm.s1, a.coeffs + static_cast<size_t>(i) * a.M);
+    __syncthreads();
+    return;
   }
-}
-
-__device__ __forceinline__ double gather_x(const CgArgs& a, int g) {
-  return a.flip_sign[g] * (a.xf[a.own_flux[2 * g]] + a.xf[a.own_flux[2 * g + 1]]);
+  rowdot(a.FC + static_cast<size_t>(i) * a.fmax * R, R, c.d.nF, c.r, sm.s1,
+         a.xf + static_cast<size_t>(i) * a.fmax, -1.0);
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- Neumann-to-Dirichlet map
-__global__ void __launch_bounds__(kBlk) nn1_kernel(CgArgs a, int guard) {
-  if (guard && cg_done(a)) return;
-  const int i = blockIdx.x;
+__device__ void dev_nn1(const CgArgs& a, int i) {
   const SubCtx c = sub_ctx(a, a.N + i, i);
   const int R = a.rmax, E = a.ext, nd = c.d.nd;
-  extern __shared__ double sm[];
-  double* rhs = sm;        // dmax
-  double* sb = rhs + a.dmax;  // rmax
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  Smem sm = carve(a);
   const int* nmap = a.ndelta_map + static_cast<size_t>(i) * a.dmax;
-  for (int kk = threadIdx.x; kk < nd; kk += blockDim.x) rhs[kk] = -gather_x(a, nmap[kk]);
+  for (int kk = threadIdx.x; kk < nd; kk += blockDim.x) sm.v1[kk] = -gather_x(a, nmap[kk]);
   __syncthreads();
-  for (int k = warp; k < c.r; k += nw) {
-    const double* q = c.QtX + static_cast<size_t>(k) * E + 1;
-    double acc = 0;
-    for (int kk = lane; kk < nd; kk += 32) acc += q[kk] * rhs[kk];
-    acc = warp_sum(acc);
-    if (lane == 0) sb[k] = acc;
-  }
+  rowdot(c.QtX + 1, E, c.r, nd, sm.v1, sm.s0);  // Qbar_r^T rhs
   __syncthreads();
-  const double* CC = a.CCb + static_cast<size_t>(i) * a.dmax * R;
-  for (int kk = warp; kk < nd; kk += nw) {
-    double acc = 0;
-    for (int k = lane; k < c.r; k += 32) acc += CC[static_cast<size_t>(kk) * R + k] * sb[k];
-    acc = warp_sum(acc);
-    if (lane == 0) a.tr[static_cast<size_t>(i) * a.dmax + kk] = acc;
+  double* tr = a.tr + static_cast<size_t>(i) * a.dmax;
+  if (a.coeff_space) {
+    // reference order (solvers.cpp:456): y = Kbar^+ rhs (M-vector), then Cdelta y
+    rowdot(a.C + static_cast<size_t>(a.N + i) * a.M * R, R, a.M, c.r, sm.s0, sm.cw);
+    __syncthreads();
+    coldot(a.Cd + static_cast<size_t>(i) * a.M * a.ldC, a.ldC, a.M, nd, sm.cw, tr, sm.red);
+  } else {
+    rowdot(a.CCb + static_cast<size_t>(i) * a.dmax * R, R, nd, c.r, sm.s0, tr);
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kBlk) nn2_kernel(CgArgs a, int guard) {
-  if (guard && cg_done(a)) return;
-  const int i = blockIdx.x;
+__device__ void dev_nn2(const CgArgs& a, int i) {
   const SubCtx c = sub_ctx(a, a.N + i, i);
   const int R = a.rmax, E = a.ext, nd = c.d.nd;
-  extern __shared__ double sm[];
-  double* px = sm;          // dmax
-  double* sb = px + a.dmax;  // rmax
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  Smem sm = carve(a);
   const int* nmap = a.ndelta_map + static_cast<size_t>(i) * a.dmax;
   for (int kk = threadIdx.x; kk < nd; kk += blockDim.x) {
     const int g = nmap[kk];
-    px[kk] = a.tr[a.own_nd[2 * g]] + a.tr[a.own_nd[2 * g + 1]];
+    sm.v1[kk] = a.tr[a.own_nd[2 * g]] + a.tr[a.own_nd[2 * g + 1]];  // (P x) at the local rows
   }
   __syncthreads();
-  const double* CC = a.CCb + static_cast<size_t>(i) * a.dmax * R;
-  for (int k = threadIdx.x; k < c.r; k += blockDim.x) {
-    double acc = 0;
-    for (int kk = 0; kk < nd; ++kk) acc += CC[static_cast<size_t>(kk) * R + k] * px[kk];
-    sb[k] = acc;
+  if (a.coeff_space) {
+    // reference order (solvers.cpp:469): x = Cdelta^T tl (M-vector), then (Kbar^+)^T x
+    rowdot(a.Cd + static_cast<size_t>(i) * a.M * a.ldC, a.ldC, a.M, nd, sm.v1, sm.cw);
+    __syncthreads();
+    coldot(a.C + static_cast<size_t>(a.N + i) * a.M * R, R, a.M, c.r, sm.cw, sm.s0, sm.red);
+  } else {
+    coldot(a.CCb + static_cast<size_t>(i) * a.dmax * R, R, nd, c.r, sm.v1, sm.s0, sm.red);
   }
-  __syncthreads();
-  for (int kk = threadIdx.x; kk < nd; kk += blockDim.x) {
-    double acc = 0;
-    for (int k = 0; k < c.r; ++k) acc += c.QtX[static_cast<size_t>(k) * E + 1 + kk] * sb[k];
-    a.zz[static_cast<size_t>(i) * a.dmax + kk] = acc;
-  }
+  coldot(c.QtX + 1, E, c.r, nd, sm.s0, a.zz + static_cast<size_t>(i) * a.dmax, sm.red);
 }
 
-// ---------------------------------------------------------------- op3: weight, u = FC^T a
-__global__ void __launch_bounds__(kBlk) op3_kernel(CgArgs a, int guard) {
-  if (guard && cg_done(a)) return;
-  const int i = blockIdx.x;
+// ---------------------------------------------------------------- op3: weight, u
+__device__ void dev_op3(const CgArgs& a, int i) {
   const SubCtx c = sub_ctx(a, i, i);
   const int R = a.rmax, E = a.ext;
-  extern __shared__ double sm[];
-  double* av = sm;          // fmax
-  double* u = av + a.fmax;  // rmax
+  Smem sm = carve(a);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int* fd = a.fluxrow_delta + static_cast<size_t>(i) * a.fmax;
   const double theta = a.theta;
@@ -291,54 +322,35 @@ __global__ void __launch_bounds__(kBlk) op3_kernel(CgArgs a, int guard) {
         w = x;
       }
     }
-    av[l] = w;
+    sm.v1[l] = w;  // apply_AT_delta: a(lrow) = w(grow) on the Delta flux rows
   }
   __syncthreads();
   if (a.coeff_space) {
-    // reference order: at = F^T a (M-vector, apply_AT), then (K^+)^T at -> Q_r (C^T at)
-    const double* Fi = a.F + static_cast<size_t>(i) * a.M * a.ldF;
-    double* cw = a.cwork + static_cast<size_t>(i) * a.M;
-    const int nw = blockDim.x >> 5;
-    for (int j = warp; j < a.M; j += nw) {
-      double acc = 0;
-      for (int l = lane; l < c.d.nF; l += 32) acc += Fi[static_cast<size_t>(j) * a.ldF + l] * av[l];
-      acc = warp_sum(acc);
-      if (lane == 0) cw[j] = acc;
-    }
+    // reference order: at = F^T a (M-vector, apply_AT), then (K^+)^T at -> C^T at
+    rowdot(a.F + static_cast<size_t>(i) * a.M * a.ldF, a.ldF, a.M, c.d.nF, sm.v1, sm.cw);
     __syncthreads();
-    const double* Ci = a.C + static_cast<size_t>(i) * a.M * R;
-    for (int k = threadIdx.x; k < c.r; k += blockDim.x) {
-      double acc = 0;
-      for (int j = 0; j < a.M; ++j) acc += Ci[static_cast<size_t>(j) * R + k] * cw[j];
-      u[k] = acc;
-      a.u[static_cast<size_t>(i) * R + k] = acc;
-    }
+    coldot(a.C + static_cast<size_t>(i) * a.M * R, R, a.M, c.r, sm.cw, sm.s0, sm.red);
   } else {
-    const double* FC = a.FC + static_cast<size_t>(i) * a.fmax * R;
-    for (int k = threadIdx.x; k < c.r; k += blockDim.x) {
-      double acc = 0;
-      for (int l = 0; l < c.d.nF; ++l) acc += FC[static_cast<size_t>(l) * R + k] * av[l];
-      u[k] = acc;
-      a.u[static_cast<size_t>(i) * R + k] = acc;
-    }
+    coldot(a.FC + static_cast<size_t>(i) * a.fmax * R, R, c.d.nF, c.r, sm.v1, sm.s0, sm.red);
   }
-  __syncthreads();
+  for (int k = threadIdx.x; k < c.r; k += blockDim.x) a.u[static_cast<size_t>(i) * R + k] = sm.s0[k];
   if (warp < 4) {
     const int g = a.corner_q[i * 4 + warp];
     double acc = 0;
     if (g >= 0)
-      for (int k = lane; k < c.r; k += 32) acc += c.QtX[static_cast<size_t>(k) * E + 1 + g] * u[k];
+      for (int k = lane; k < c.r; k += 32) acc += c.QtX[static_cast<size_t>(k) * E + 1 + g] * sm.s0[k];
     acc = warp_sum(acc);
-    if (lane == 0) a.tpart[i * 4 + warp] = acc;
+    if (lane == 0) a.tpart[i * 4 + warp] = acc;  // t(gp) += z(lr) at corners
   }
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(kBlk) coarse2_kernel(CgArgs a, int guard) {
-  if (guard && cg_done(a)) return;
-  extern __shared__ double sm[];
+__device__ void dev_coarse2(const CgArgs& a) {
+  Smem sm = carve(a);
   const int n = a.n_pi, npf = a.npf;
-  double* t = sm;
+  double* t = sm.cw;
   double* nu = t + n;
+  double* bot = nu + n;
   for (int gp = threadIdx.x; gp < n; gp += blockDim.x) {
     double acc = 0;
     for (int q = 0; q < 4; ++q) {
@@ -348,37 +360,29 @@ __global__ void __launch_bounds__(kBlk) coarse2_kernel(CgArgs a, int guard) {
     t[gp] = acc;
   }
   __syncthreads();
-  for (int gp = threadIdx.x; gp < n; gp += blockDim.x) {
-    double acc = 0;
-    for (int q = 0; q < n; ++q) acc += a.Sinv[static_cast<size_t>(gp) * n + q] * t[q];
-    nu[gp] = acc;
-    a.nu[gp] = acc;
-  }
+  rowdot(a.Sinv, n, n, n, t, nu);
   __syncthreads();
-  for (int rr = threadIdx.x; rr < npf; rr += blockDim.x) {
-    double acc = 0;
-    for (int gp = 0; gp < n; ++gp) acc += a.Dpp[static_cast<size_t>(rr) * n + gp] * nu[gp];
-    a.d2[rr] = a.d1[rr] - acc;
-  }
+  for (int gp = threadIdx.x; gp < n; gp += blockDim.x) a.nu[gp] = nu[gp];
+  rowdot(a.Dpp, n, npf, n, nu, bot);
+  __syncthreads();
+  for (int rr = threadIdx.x; rr < npf; rr += blockDim.x) a.d2[rr] = a.d1[rr] - bot[rr];
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- op4: local output rows
-__global__ void __launch_bounds__(kBlk) op4_kernel(CgArgs a, const double* v, int mode, int guard) {
-  if (guard && cg_done(a)) return;
-  const int i = blockIdx.x;
+__device__ void dev_op4(const CgArgs& a, int i, const double* v, int mode) {
   const SubCtx c = sub_ctx(a, i, i);
   const int R = a.rmax, E = a.ext;
-  extern __shared__ double sm[];
-  double* w = sm;  // rmax
+  Smem sm = carve(a);
   __shared__ double nuc[4];
   __shared__ int gq[4];
-  __shared__ double d2s[64];
+  double* d2s = sm.v1;
   if (threadIdx.x < 4) {
     const int g = a.corner_q[i * 4 + threadIdx.x];
     gq[threadIdx.x] = g;
     nuc[threadIdx.x] = g >= 0 ? a.nu[a.gamma_pi[static_cast<size_t>(i) * a.gmax + g]] : 0.0;
   }
-  for (int rho = threadIdx.x; rho < a.crmax && rho < 64; rho += blockDim.x) {
+  for (int rho = threadIdx.x; rho < a.crmax; rho += blockDim.x) {
     const int rr = a.cr_row[static_cast<size_t>(i) * a.crmax + rho];
     d2s[rho] = rr >= 0 ? a.d2[rr] : 0.0;
   }
@@ -387,45 +391,40 @@ __global__ void __launch_bounds__(kBlk) op4_kernel(CgArgs a, const double* v, in
     double uu = a.u[static_cast<size_t>(i) * R + k];
     for (int q = 0; q < 4; ++q)
       if (gq[q] >= 0) uu += c.QtX[static_cast<size_t>(k) * E + 1 + gq[q]] * nuc[q];
-    w[k] = a.s[static_cast<size_t>(i) * R + k] + uu;
+    sm.s0[k] = a.s[static_cast<size_t>(i) * R + k] + uu;  // s~ + u + Q_Pi^T nu
   }
   __syncthreads();
+  double* qs = sm.cw;
+  coldot(c.QtX + 1, E, c.r, c.d.n_gamma, sm.s0, qs, sm.red);
   const int* gd = a.gamma_delta + static_cast<size_t>(i) * a.gmax;
+  const double* Zc = a.Zc + static_cast<size_t>(i) * a.crmax * a.gmax;
   for (int g = threadIdx.x; g < c.d.n_gamma; g += blockDim.x) {
     const int dg = gd[g];
     if (dg < 0) continue;
-    double acc = (mode == 0) ? v[dg] : 0.0;  // -phi
-    double qs = 0;
-    for (int k = 0; k < c.r; ++k) qs += c.QtX[static_cast<size_t>(k) * E + 1 + g] * w[k];
     double zs = 0;
-    for (int rho = 0; rho < a.crmax; ++rho)
-      zs += a.Zc[(static_cast<size_t>(i) * a.crmax + rho) * a.gmax + g] * d2s[rho];
-    a.o[static_cast<size_t>(i) * a.gmax + g] = acc + qs + zs;
+    for (int rho = 0; rho < a.crmax; ++rho) zs += Zc[static_cast<size_t>(rho) * a.gmax + g] * d2s[rho];
+    const double mphi = (mode == 0) ? v[dg] : 0.0;  // -phi
+    a.o[static_cast<size_t>(i) * a.gmax + g] = mphi + qs[g] + zs;
   }
+  __syncthreads();
 }
 
-// ---------------------------------------------------------------- gather + CG update
-__global__ void __launch_bounds__(kBlk) gather_kernel(CgArgs a, double* out, int with_dot, int guard) {
-  if (guard && cg_done(a)) return;
-  __shared__ double red[32];
+__device__ __forceinline__ double gather_out(const CgArgs& a, int g) {
+  return a.o[a.own_gamma[2 * g]] + a.o[a.own_gamma[2 * g + 1]];
+}
+
+// ---------------------------------------------------------------- standalone kernels
+__global__ void __launch_bounds__(kBlk) op1_kernel(CgArgs a, const double* v, int mode) { dev_op1(a, blockIdx.x, v, mode); }
+__global__ void __launch_bounds__(kBlk) coarse1_kernel(CgArgs a, int mode) { dev_coarse1(a, mode); }
+__global__ void __launch_bounds__(kBlk) op2_kernel(CgArgs a, int mode) { dev_op2(a, blockIdx.x, mode); }
+__global__ void __launch_bounds__(kBlk) nn1_kernel(CgArgs a) { dev_nn1(a, blockIdx.x); }
+__global__ void __launch_bounds__(kBlk) nn2_kernel(CgArgs a) { dev_nn2(a, blockIdx.x); }
+__global__ void __launch_bounds__(kBlk) op3_kernel(CgArgs a) { dev_op3(a, blockIdx.x); }
+__global__ void __launch_bounds__(kBlk) coarse2_kernel(CgArgs a) { dev_coarse2(a); }
+__global__ void __launch_bounds__(kBlk) op4_kernel(CgArgs a, const double* v, int mode) { dev_op4(a, blockIdx.x, v, mode); }
+__global__ void __launch_bounds__(kBlk) gather_kernel(CgArgs a, double* out) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  double d = 0;
-  if (g < a.n_delta) {
-    const double val = a.o[a.own_gamma[2 * g]] + a.o[a.own_gamma[2 * g + 1]];
-    out[g] = val;
-    if (with_dot) d = a.p[g] * val;
-  }
-  if (with_dot) {
-    d = block_sum(d, red);
-    if (threadIdx.x == 0) a.partial[blockIdx.x] = d;
-  }
-}
-
-__device__ __forceinline__ double sum_partials(const double* p, int n) {
-  // identical order in every block -> identical scalars everywhere
-  double s = 0;
-  for (int k = 0; k < n; ++k) s += p[k];
-  return s;
+  if (g < a.n_delta) out[g] = gather_out(a, g);
 }
 
 __global__ void __launch_bounds__(kBlk) cg_init_kernel(CgArgs a) {
@@ -440,113 +439,131 @@ __global__ void __launch_bounds__(kBlk) cg_init_kernel(CgArgs a) {
     d = b * b;
   }
   d = block_sum(d, red);
-  if (threadIdx.x == 0) a.partial[gridDim.x + blockIdx.x] = d;
+  if (threadIdx.x == 0) a.partial[blockIdx.x] = d;
 }
 
 __global__ void cg_init2_kernel(CgArgs a, int nblk) {
   if (threadIdx.x != 0) return;
-  const double rr = sum_partials(a.partial + nblk, nblk);
+  double rr = 0;
+  for (int k = 0; k < nblk; ++k) rr += a.partial[k];
   a.scal[0] = rr;
   a.scal[1] = sqrt(rr);
-  a.state[0] = 1;
-  a.state[1] = (rr == 0.0) ? 1 : 0;
-  a.state[2] = (rr == 0.0) ? 1 : 0;
-  a.state[3] = 0;
-  a.state[4] = 0;
-  a.state[5] = 0;
+  for (int k = 0; k < 8; ++k) a.state[k] = 0;
+  if (rr == 0.0) {
+    a.state[1] = 1;  // bnorm == 0: converged with x = 0 (solvers.cpp:89-92)
+    a.state[2] = 1;
+  }
 }
 
-__global__ void __launch_bounds__(kBlk) cg_update1_kernel(CgArgs a, int guard) {
-  if (guard && cg_done(a)) return;
+// ---------------------------------------------------------------- persistent CG
+__device__ __forceinline__ double sum_partials(const double* p, int n) {
+  double s = 0;
+  for (int k = 0; k < n; ++k) s += p[k];
+  return s;
+}
+
+__global__ void __launch_bounds__(kPersistBlk) cg_persistent_kernel(CgArgs a) {
+  cgs::grid_group grid = cgs::this_grid();
+  const int G = gridDim.x, b = blockIdx.x;
   __shared__ double red[32];
-  const int nblk = gridDim.x;
-  const double pAp = sum_partials(a.partial, nblk);
-  if (pAp <= 0.0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      a.state[3] = pAp < 0.0 ? 1 : 0;
-      a.state[5] = a.state[0] - 1;
-      a.state[4] = 2;  // negative-curvature stop
+  double* partial = a.partial;          // G entries: p.Ap
+  double* partial2 = a.partial + G;     // G entries: r.r
+  double rr = a.scal[0];
+  const double bnorm = a.scal[1];
+  if (a.state[1]) return;  // rhs == 0
+  int it = 1;
+  for (;; ++it) {
+    for (int i = b; i < a.N; i += G) dev_op1(a, i, a.p, 0);
+    grid.sync();
+    if (b == 0) dev_coarse1(a, 0);
+    grid.sync();
+    for (int i = b; i < a.N; i += G) dev_op2(a, i, 0);
+    grid.sync();
+    if (a.use_neumann) {
+      for (int i = b; i < a.N; i += G) dev_nn1(a, i);
+      grid.sync();
+      for (int i = b; i < a.N; i += G) dev_nn2(a, i);
+      grid.sync();
     }
-    return;
-  }
-  const double alpha = a.scal[0] / pAp;
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  double d = 0;
-  if (g < a.n_delta) {
-    a.x[g] += alpha * a.p[g];
-    const double rg = a.r[g] - alpha * a.Ap[g];
-    a.r[g] = rg;
-    d = rg * rg;
-  }
-  d = block_sum(d, red);
-  if (threadIdx.x == 0) a.partial[nblk + blockIdx.x] = d;
-}
-
-__global__ void __launch_bounds__(kBlk) cg_update2_kernel(CgArgs a, int guard) {
-  if (guard && cg_done(a)) return;
-  if (a.state[4] == 2) return;  // negative curvature: x, p untouched
-  const int nblk = gridDim.x;
-  const double rr_new = sum_partials(a.partial + nblk, nblk);
-  const double rel = sqrt(rr_new) / a.scal[1];
-  const int it = a.state[0];
-  const bool conv = rel <= a.rel_tol;
-  const bool stop = conv || it >= a.max_iter;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.hist[it - 1] = rel;
-    a.state[5] = it;
-    a.scal[2] = rr_new;
-    a.state[4] = stop ? (conv ? 3 : 1) : 0;
-  }
-  if (stop) return;
-  const double beta = rr_new / a.scal[0];
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < a.n_delta) a.p[g] = a.r[g] + beta * a.p[g];
-}
-
-__global__ void cg_bookkeep_kernel(CgArgs a, unsigned long long handle, int use_cond) {
-  if (threadIdx.x != 0) return;
-  if (a.state[1] == 0) {
-    const int st = a.state[4];
-    if (st == 0) {
-      a.state[0] += 1;
-      a.scal[0] = a.scal[2];
-    } else {
-      a.state[1] = 1;
-      a.state[2] = (st == 3) ? 1 : 0;
+    for (int i = b; i < a.N; i += G) dev_op3(a, i);
+    grid.sync();
+    if (b == 0) dev_coarse2(a);
+    grid.sync();
+    for (int i = b; i < a.N; i += G) dev_op4(a, i, a.p, 0);
+    grid.sync();
+    // Ap = gathered output, pAp partials
+    double d = 0;
+    for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) {
+      const double val = gather_out(a, g);
+      a.Ap[g] = val;
+      d += a.p[g] * val;
     }
+    d = block_sum(d, red);
+    if (threadIdx.x == 0) partial[b] = d;
+    grid.sync();
+    const double pAp = sum_partials(partial, G);
+    if (pAp <= 0.0) {  // solvers.cpp:97-103
+      if (b == 0 && threadIdx.x == 0) {
+        a.state[3] = pAp < 0.0 ? 1 : 0;
+        a.state[5] = it - 1;
+        a.state[1] = 1;
+      }
+      return;
+    }
+    const double alpha = rr / pAp;
+    d = 0;
+    for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) {
+      a.x[g] += alpha * a.p[g];
+      const double rg = a.r[g] - alpha * a.Ap[g];
+      a.r[g] = rg;
+      d += rg * rg;
+    }
+    d = block_sum(d, red);
+    if (threadIdx.x == 0) partial2[b] = d;
+    grid.sync();
+    const double rr_new = sum_partials(partial2, G);
+    const double rel = sqrt(rr_new) / bnorm;
+    if (b == 0 && threadIdx.x == 0) {
+      a.hist[it - 1] = rel;
+      a.state[5] = it;
+    }
+    if (rel <= a.rel_tol || it >= a.max_iter) {
+      if (b == 0 && threadIdx.x == 0) {
+        a.state[1] = 1;
+        a.state[2] = rel <= a.rel_tol ? 1 : 0;
+      }
+      return;
+    }
+    const double beta = rr_new / rr;
+    for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) a.p[g] = a.r[g] + beta * a.p[g];
+    rr = rr_new;
+    grid.sync();
   }
-#if CUDART_VERSION >= 12040
-  if (use_cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(handle), a.state[1] ? 0u : 1u);
-#else
-  (void)handle;
-  (void)use_cond;
-#endif
 }
 
-size_t sub_smem(const CgArgs& a) {
+size_t smem_bytes(const CgArgs& a, int threads) {
   const int big = std::max(std::max(a.gmax, a.fmax), a.dmax);
-  return sizeof(double) * (big + a.rmax + 8);
+  const int cwsize = std::max(a.M, 3 * a.n_pi + 2 * a.npf);
+  return sizeof(double) * (static_cast<size_t>(big) + cwsize + 2 * a.rmax + threads);
 }
 
 }  // namespace
 
-int cg_kernels_per_step(const CgArgs& a) { return a.use_neumann ? 12 : 10; }
+int cg_kernels_per_step(const CgArgs& a) { return a.use_neumann ? 9 : 7; }
 
 void cg_launch_operator(const CgArgs& a, const double* v, double* out, int mode, cudaStream_t st) {
-  const size_t ssm = sub_smem(a);
-  const size_t csm = sizeof(double) * (3 * a.n_pi + a.npf + 8);
-  const int guard = (mode == 0) ? 1 : 0;
-  op1_kernel<<<a.N, kBlk, ssm, st>>>(a, v, mode, guard);
-  coarse1_kernel<<<1, kBlk, csm, st>>>(a, mode, guard);
-  op2_kernel<<<a.N, kBlk, ssm, st>>>(a, mode, guard);
+  const size_t sm = smem_bytes(a, kBlk);
+  op1_kernel<<<a.N, kBlk, sm, st>>>(a, v, mode);
+  coarse1_kernel<<<1, kBlk, sm, st>>>(a, mode);
+  op2_kernel<<<a.N, kBlk, sm, st>>>(a, mode);
   if (a.use_neumann) {
-    nn1_kernel<<<a.N, kBlk, ssm, st>>>(a, guard);
-    nn2_kernel<<<a.N, kBlk, ssm, st>>>(a, guard);
+    nn1_kernel<<<a.N, kBlk, sm, st>>>(a);
+    nn2_kernel<<<a.N, kBlk, sm, st>>>(a);
   }
-  op3_kernel<<<a.N, kBlk, ssm, st>>>(a, guard);
-  coarse2_kernel<<<1, kBlk, csm, st>>>(a, guard);
-  op4_kernel<<<a.N, kBlk, ssm, st>>>(a, v, mode, guard);
-  gather_kernel<<<ceil_div(a.n_delta, kBlk), kBlk, 0, st>>>(a, out, mode == 0 ? 1 : 0, guard);
+  op3_kernel<<<a.N, kBlk, sm, st>>>(a);
+  coarse2_kernel<<<1, kBlk, sm, st>>>(a);
+  op4_kernel<<<a.N, kBlk, sm, st>>>(a, v, mode);
+  gather_kernel<<<ceil_div(a.n_delta, kBlk), kBlk, 0, st>>>(a, out);
   DDG_LAUNCH_CHECK();
 }
 
@@ -557,21 +574,33 @@ void cg_launch_init(const CgArgs& a, cudaStream_t st) {
   DDG_LAUNCH_CHECK();
 }
 
-void cg_launch_step(const CgArgs& a, cudaStream_t st, unsigned long long cond_handle, bool use_cond) {
-  const int nblk = ceil_div(a.n_delta, kBlk);
-  cg_launch_operator(a, a.p, a.Ap, 0, st);
-  cg_update1_kernel<<<nblk, kBlk, 0, st>>>(a, 1);
-  cg_update2_kernel<<<nblk, kBlk, 0, st>>>(a, 1);
-  cg_bookkeep_kernel<<<1, 32, 0, st>>>(a, cond_handle, use_cond ? 1 : 0);
-  DDG_LAUNCH_CHECK();
+int cg_persistent_grid(const CgArgs& a) {
+  int dev = 0, sms = 0, per_sm = 0;
+  DDG_CUDA(cudaGetDevice(&dev));
+  DDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const size_t sm = smem_bytes(a, kPersistBlk);
+  DDG_CUDA(cudaFuncSetAttribute(cg_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sm)));
+  DDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_persistent_kernel, kPersistBlk, sm));
+  if (per_sm < 1) throw CudaError("cg_persistent_kernel cannot be resident (occupancy 0)");
+  // one CTA per SM is enough: the local phases have N (<= 256) work items
+  return std::max(1, std::min(sms * per_sm, std::max(sms, a.N)));
+}
+
+void cg_launch_persistent(const CgArgs& a, cudaStream_t st) {
+  const int G = cg_persistent_grid(a);
+  const size_t sm = smem_bytes(a, kPersistBlk);
+  CgArgs arg = a;
+  void* params[] = {&arg};
+  DDG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_persistent_kernel), dim3(G), dim3(kPersistBlk),
+                                       params, sm, st));
 }
 
 void cg_launch_reconstruct(const CgArgs& a, cudaStream_t st) {
-  const size_t ssm = sub_smem(a);
-  const size_t csm = sizeof(double) * (3 * a.n_pi + a.npf + 8);
-  op1_kernel<<<a.N, kBlk, ssm, st>>>(a, a.x, 2, 0);
-  coarse1_kernel<<<1, kBlk, csm, st>>>(a, 2, 0);
-  op2_kernel<<<a.N, kBlk, ssm, st>>>(a, 2, 0);
+  const size_t sm = smem_bytes(a, kBlk);
+  op1_kernel<<<a.N, kBlk, sm, st>>>(a, a.x, 2);
+  coarse1_kernel<<<1, kBlk, sm, st>>>(a, 2);
+  op2_kernel<<<a.N, kBlk, sm, st>>>(a, 2);
   DDG_LAUNCH_CHECK();
 }
 

@@ -23,6 +23,9 @@ namespace ddg {
 
 namespace {
 
+constexpr int kRecB = 8;  // flagged columns recomputed per register-blocked pass
+constexpr int kNPL = 32;  // register rows per lane in the finish kernel: M <= 32 * 32
+
 struct ArgMax {
   double v;
   int i;
@@ -56,7 +59,7 @@ __device__ ArgMax block_argmax(ArgMax x, ArgMax* sh) {
   return r;
 }
 
-__global__ void __launch_bounds__(1024) cod_pivqr_kernel(CodArgs a) {
+__global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
   const int t = blockIdx.x;
   const int M = a.M, K = a.kmax;
   const double mn = a.ratio[2 * t], mx = a.ratio[2 * t + 1];
@@ -83,6 +86,11 @@ __global__ void __launch_bounds__(1024) cod_pivqr_kernel(CodArgs a) {
   double* v = sm;            // M
   double* w = v + M;         // K
   double* vk = w + K;        // K  (row k of V)
+  double* Fs = vk + K;       // kRecB x K  (F rows of the columns being recomputed)
+  int* flist = reinterpret_cast<int*>(Fs + kRecB * K);  // M
+  __shared__ double redq[kRecB * 32];
+  __shared__ int wcnt[32], woff[32], cjs[kRecB];
+  __shared__ int s_nflag;
   __shared__ double red[32];
   __shared__ ArgMax ared[32];
   __shared__ double s_tau, s_maxpivot;
@@ -189,8 +197,17 @@ __global__ void __launch_bounds__(1024) cod_pivqr_kernel(CodArgs a) {
     for (int j = k + 1 + warp; j < M; j += nwarp) {
       const int cj = perm[j];
       const double* col = R0 + static_cast<size_t>(cj) * ld;
-      double g = 0;
-      for (int i = k + lane; i <= cj && i < M; i += 32) g += col[i] * v[i];
+      const int iend = min(cj, M - 1);
+      double g0 = 0, g1 = 0, g2 = 0, g3 = 0;
+      int i = k + lane;
+      for (; i + 96 <= iend; i += 128) {
+        g0 += col[i] * v[i];
+        g1 += col[i + 32] * v[i + 32];
+        g2 += col[i + 64] * v[i + 64];
+        g3 += col[i + 96] * v[i + 96];
+      }
+      for (; i <= iend; i += 32) g0 += col[i] * v[i];
+      double g = (g0 + g1) + (g2 + g3);
       double fw = 0;
       for (int u = lane; u < k; u += 32) fw += F1[static_cast<size_t>(j) * K + u] * w[u];
       g = warp_sum(g);
@@ -216,20 +233,66 @@ __global__ void __launch_bounds__(1024) cod_pivqr_kernel(CodArgs a) {
     }
     __syncthreads();
     // ---- exact recomputation of flagged norms: ||(A - V F^T)(k+1:M, j)||
-    for (int j = k + 1 + warp; j < M; j += nwarp) {
-      if (dir[j] != -1.0) continue;
-      const int cj = perm[j];
-      const double* col = R0 + static_cast<size_t>(cj) * ld;
-      double s = 0;
-      for (int i = k + 1 + lane; i < M; i += 32) {
-        double e = (i <= cj) ? col[i] : 0.0;
-        for (int u = 0; u <= k; ++u) e -= V1[static_cast<size_t>(u) * M + i] * F1[static_cast<size_t>(j) * K + u];
-        s += e * e;
-      }
-      s = warp_sum(s);
-      if (lane == 0) upd[j] = dir[j] = sqrt(s);
-    }
+    // compact the flagged columns (increasing j), then a register-blocked pass over rows that
+    // serves 8 columns per V1 read (a small GEMM instead of one warp per column)
+    if (threadIdx.x == 0) s_nflag = 0;
     __syncthreads();
+    for (int base = k + 1; base < M; base += blockDim.x) {
+      const int j = base + threadIdx.x;
+      const bool fl = j < M && dir[j] == -1.0;
+      const unsigned bal = __ballot_sync(0xffffffffu, fl);
+      if (lane == 0) wcnt[warp] = __popc(bal);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int s = s_nflag;
+        for (int w2 = 0; w2 < nwarp; ++w2) {
+          woff[w2] = s;
+          s += wcnt[w2];
+        }
+        s_nflag = s;
+      }
+      __syncthreads();
+      if (fl) flist[woff[warp] + __popc(bal & ((1u << lane) - 1u))] = j;
+      __syncthreads();
+    }
+    const int nflag = s_nflag;
+    for (int f0 = 0; f0 < nflag; f0 += kRecB) {
+      const int nb = min(kRecB, nflag - f0);
+      for (int idx = threadIdx.x; idx < kRecB * (k + 1); idx += blockDim.x) {
+        const int q = idx / (k + 1), u = idx % (k + 1);
+        Fs[q * K + u] = q < nb ? F1[static_cast<size_t>(flist[f0 + q]) * K + u] : 0.0;
+      }
+      if (threadIdx.x < kRecB) cjs[threadIdx.x] = threadIdx.x < nb ? perm[flist[f0 + threadIdx.x]] : -1;
+      __syncthreads();
+      double acc[kRecB];
+#pragma unroll
+      for (int q = 0; q < kRecB; ++q) acc[q] = 0.0;
+      for (int i = k + 1 + threadIdx.x; i < M; i += blockDim.x) {
+        double e[kRecB];
+#pragma unroll
+        for (int q = 0; q < kRecB; ++q) e[q] = (i <= cjs[q]) ? R0[static_cast<size_t>(cjs[q]) * ld + i] : 0.0;
+        for (int u = 0; u <= k; ++u) {
+          const double vv = V1[static_cast<size_t>(u) * M + i];
+#pragma unroll
+          for (int q = 0; q < kRecB; ++q) e[q] -= vv * Fs[q * K + u];
+        }
+#pragma unroll
+        for (int q = 0; q < kRecB; ++q) acc[q] += e[q] * e[q];
+      }
+#pragma unroll
+      for (int q = 0; q < kRecB; ++q) {
+        const double sq = warp_sum(acc[q]);
+        if (lane == 0) redq[q * 32 + warp] = sq;
+      }
+      __syncthreads();
+      if (threadIdx.x < nb) {
+        double sq = 0;
+        for (int w2 = 0; w2 < nwarp; ++w2) sq += redq[threadIdx.x * 32 + w2];
+        const int j = flist[f0 + threadIdx.x];
+        upd[j] = dir[j] = sqrt(sq);
+      }
+      __syncthreads();
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -337,73 +400,97 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
       __syncthreads();
     }
   }
-  // ---- Y = Z^T [I_r; 0]  (COD::solve's Z^* application, column by column)
-  for (int idx = threadIdx.x; idx < M * R; idx += blockDim.x) {
-    const int i = idx / R, c = idx % R;
-    Y[idx] = (i == c && i < r) ? 1.0 : 0.0;
+  // ---- Y = Z^T [I_r; 0] (COD::solve's Z^* application): one warp per column, the column held
+  // in registers (lane owns rows lane + 32 t), no block barriers between reflectors.
+  // Stored transposed, Yt(c, j) = Y[c*M + j], so every access is coalesced.
+  for (int c = warp; c < r; c += nwarp) {
+    double y[kNPL];
+#pragma unroll
+    for (int t2 = 0; t2 < kNPL; ++t2) y[t2] = (lane + 32 * t2 == c) ? 1.0 : 0.0;
+    if (r < M)
+      for (int k = 0; k < r; ++k) {
+        const double tau = zc[k];
+        if (tau == 0.0) continue;
+        const double* zr = Rr + static_cast<size_t>(k) * M;
+        // leading element at row k (COD's swap with row r-1 and back), tail rows r..M-1
+        double s = 0;
+#pragma unroll
+        for (int t2 = 0; t2 < kNPL; ++t2) {
+          const int j = lane + 32 * t2;
+          if (j >= r && j < M) s += zr[j] * y[t2];
+        }
+        s = warp_sum(s);
+        double yk = 0;
+#pragma unroll
+        for (int t2 = 0; t2 < kNPL; ++t2)
+          if (t2 == (k >> 5)) yk = y[t2];
+        yk = __shfl_sync(0xffffffffu, yk, k & 31);
+        s = (s + yk) * tau;
+#pragma unroll
+        for (int t2 = 0; t2 < kNPL; ++t2) {
+          const int j = lane + 32 * t2;
+          if (j == k) y[t2] -= s;
+          else if (j >= r && j < M) y[t2] -= s * zr[j];
+        }
+      }
+#pragma unroll
+    for (int t2 = 0; t2 < kNPL; ++t2) {
+      const int j = lane + 32 * t2;
+      if (j < M) Y[static_cast<size_t>(c) * M + j] = y[t2];
+    }
   }
   __syncthreads();
-  if (r < M) {
-    for (int k = 0; k < r; ++k) {
-      const double tau = zc[k];
-      if (tau == 0.0) continue;
-      const double* zr = Rr + static_cast<size_t>(k) * M;
-      for (int c = warp; c < r; c += nwarp) {
-        // rows {k} U {r..M-1}, with row k playing position r-1
-        const int lead = (k != r - 1) ? k : r - 1;
-        // swapping rows k and r-1 then operating on r-1 is equivalent to: leading element at
-        // row k, and row r-1 untouched (unless k == r-1)
-        double s = 0;
-        for (int j = r + lane; j < M; j += 32) s += zr[j] * Y[static_cast<size_t>(j) * R + c];
-        s = warp_sum(s);
-        const double yl = Y[static_cast<size_t>(lead) * R + c];
-        s = (s + yl) * tau;
-        __syncwarp();
-        if (lane == 0) Y[static_cast<size_t>(lead) * R + c] = yl - s;
-        for (int j = r + lane; j < M; j += 32) Y[static_cast<size_t>(j) * R + c] -= s * zr[j];
-        __syncwarp();
-      }
-      __syncthreads();
-    }
-  }
-  // ---- C(perm[i], :) = (Y T^{-1})(i, :), T = upper triangle of Rr(0:r, 0:r)
+  // ---- C(perm[i], :) = (Y T^{-1})(i, :), T = upper triangle of Rr(0:r, 0:r) (thread per row)
   for (int i = threadIdx.x; i < M; i += blockDim.x) {
-    double* yi = Y + static_cast<size_t>(i) * R;
-    for (int c = 0; c < r; ++c) {
-      double s = yi[c];
-      for (int u = 0; u < c; ++u) s -= yi[u] * Rr[static_cast<size_t>(u) * M + c];
-      yi[c] = s / Rr[static_cast<size_t>(c) * M + c];
-    }
     double* ci = C + static_cast<size_t>(perm[i]) * R;
-    for (int c = 0; c < R; ++c) ci[c] = c < r ? yi[c] : 0.0;
+    for (int c = 0; c < r; ++c) {
+      double s = Y[static_cast<size_t>(c) * M + i];
+      for (int u = 0; u < c; ++u) s -= ci[u] * Rr[static_cast<size_t>(u) * M + c];
+      ci[c] = s / Rr[static_cast<size_t>(c) * M + c];
+    }
+    for (int c = r; c < R; ++c) ci[c] = 0.0;
   }
-  // ---- Q1_r^T applied to the top M rows of Q0^T [f E] (in place), keep r rows
-  for (int u = 0; u < r; ++u) {
-    const double tau = tau1[u];
-    const double* vu = V1 + static_cast<size_t>(u) * M;
-    if (tau != 0.0)
-      for (int e = warp; e < E; e += nwarp) {
-        double* xe = X + static_cast<size_t>(e) * ld;
-        double s = 0;
-        for (int i = u + lane; i < M; i += 32) s += vu[i] * xe[i];
-        s = warp_sum(s) * tau;
-        __syncwarp();
-        for (int i = u + lane; i < M; i += 32) xe[i] -= s * vu[i];
-        __syncwarp();
+  // ---- Q1_r^T applied to the top M rows of Q0^T [f E]: one warp per column, in registers
+  for (int e = warp; e < E; e += nwarp) {
+    const double* xe = X + static_cast<size_t>(e) * ld;
+    double x[kNPL];
+#pragma unroll
+    for (int t2 = 0; t2 < kNPL; ++t2) {
+      const int i = lane + 32 * t2;
+      x[t2] = i < M ? xe[i] : 0.0;
+    }
+    for (int u = 0; u < r; ++u) {
+      const double tau = tau1[u];
+      if (tau == 0.0) continue;
+      const double* vu = V1 + static_cast<size_t>(u) * M;
+      double s = 0;
+#pragma unroll
+      for (int t2 = 0; t2 < kNPL; ++t2) {
+        const int i = lane + 32 * t2;
+        if (i >= u && i < M) s += vu[i] * x[t2];
       }
-    __syncthreads();
-  }
-  for (int idx = threadIdx.x; idx < R * E; idx += blockDim.x) {
-    const int c = idx / E, e = idx % E;
-    QtX[idx] = c < r ? X[static_cast<size_t>(e) * ld + c] : 0.0;
+      s = warp_sum(s) * tau;
+#pragma unroll
+      for (int t2 = 0; t2 < kNPL; ++t2) {
+        const int i = lane + 32 * t2;
+        if (i >= u && i < M) x[t2] -= s * vu[i];
+      }
+    }
+#pragma unroll
+    for (int t2 = 0; t2 < kNPL; ++t2) {
+      const int c = lane + 32 * t2;
+      if (c < R) QtX[static_cast<size_t>(c) * E + e] = c < r ? x[t2] : 0.0;
+    }
   }
 }
 
 }  // namespace
 
 void launch_cod_pivqr(const CodArgs& a, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (a.M + 2 * a.kmax);
-  cod_pivqr_kernel<<<a.nmat, 1024, smem, st>>>(a);
+  const size_t smem = sizeof(double) * (a.M + (2 + kRecB) * a.kmax) + sizeof(int) * a.M;
+  DDG_CUDA(cudaFuncSetAttribute(cod_pivqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  cod_pivqr_kernel<<<a.nmat, 512, smem, st>>>(a);
   DDG_LAUNCH_CHECK();
 }
 

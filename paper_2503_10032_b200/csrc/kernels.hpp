@@ -91,6 +91,7 @@ struct BlockArgs {
   double* Zc;            // N x crmax x gmax : (K^+)^T a restricted to gamma rows
   double* pd;            // N x crmax : flux data F K^+ f per cross row (before scatter)
   double* Gc;            // N x 4 x 4  : -(Q_Pi Q_Pi^T)
+  double* Ypi;           // N x M x 4  : -C Q_Pi^T = K^+ B_Pi (corner columns)
   int* corner_q;         // N x 4 gamma positions of the corners (-1 pad)
   double* Dpp;           // npf x n_pi
   double* dpi;           // npf
@@ -117,7 +118,10 @@ struct CgArgs {
   int coeff_space;
   const double* F;         // N x M x ldF (flux rows, j-major)
   int ldF;
+  const double* Cd;        // N x M x ldC (Neumann trace rows, j-major)
+  int ldC;
   double* cwork;           // N x M scratch (coefficients / F^T a)
+  const double* Ypi;       // N x M x 4 : K^+ B_Pi columns at the corners (assemble_coarse Ypi)
   double rel_tol;
   int max_iter;
   const int* rank;      // 2N
@@ -173,9 +177,9 @@ struct CgArgs {
 /// out = cs_reduced_apply(v) (mode 0) or the reduced right-hand side (mode 1, v unused)
 void cg_launch_operator(const CgArgs& a, const double* v, double* out, int mode, cudaStream_t st);
 void cg_launch_init(const CgArgs& a, cudaStream_t st);
-/// One CG iteration (solvers.cpp:95-117). With use_cond the last kernel drives the graph's
-/// while-conditional; every kernel is a no-op once the solve is done.
-void cg_launch_step(const CgArgs& a, cudaStream_t st, unsigned long long cond_handle, bool use_cond);
+/// The whole CG loop (solvers.cpp:95-117) as one persistent cooperative kernel.
+void cg_launch_persistent(const CgArgs& a, cudaStream_t st);
+int cg_persistent_grid(const CgArgs& a);
 void cg_launch_reconstruct(const CgArgs& a, cudaStream_t st);
 int cg_kernels_per_step(const CgArgs& a);
 

@@ -177,6 +177,7 @@ void Workspace::upload_plan() {
   d_Zc.alloc(static_cast<size_t>(N) * p.crmax * p.gmax);
   d_pd.alloc(static_cast<size_t>(N) * p.crmax);
   d_Gc.alloc(static_cast<size_t>(N) * 16);
+  d_Ypi.alloc(static_cast<size_t>(N) * p.M * 4);
   d_corner_q.alloc(static_cast<size_t>(N) * 4);
   const size_t npf = std::max(p.npf, 1), npi = std::max(p.n_pi, 1);
   d_Dpp.alloc(npf * npi);
@@ -206,29 +207,89 @@ void Workspace::upload_plan() {
 }
 
 void Workspace::init_layers() {
+  // seeded layers (features.cpp:9-35) drawn on the host into pinned staging, one H2D copy each
   const Plan& p = plan;
   const int N = p.N;
-  h_w0.resize(static_cast<size_t>(N) * p.M);
-  h_w1.resize(h_w0.size());
-  h_b.resize(h_w0.size());
+  const size_t nm = static_cast<size_t>(N) * p.M;
+  if (!h_layers_) DDG_CUDA(cudaMallocHost(&h_layers_, 3 * nm * sizeof(double)));
+  double* w0 = h_layers_;
+  double* w1 = h_layers_ + nm;
+  double* bb = h_layers_ + 2 * nm;
+  DDG_CUDA(cudaStreamSynchronize(st_));  // staging may still feed an earlier copy
   const int nth = std::max(1, std::min<int>(N, static_cast<int>(std::thread::hardware_concurrency())));
   std::vector<std::thread> th;
   for (int t = 0; t < nth; ++t)
     th.emplace_back([&, t] {
-      for (int i = t; i < N; i += nth)
-        init_layer(p, i, h_w0.data() + static_cast<size_t>(i) * p.M, h_w1.data() + static_cast<size_t>(i) * p.M,
-                   h_b.data() + static_cast<size_t>(i) * p.M);
+      for (int i = t; i < N; i += nth) {
+        const size_t o = static_cast<size_t>(i) * p.M;
+        init_layer(p, i, w0 + o, w1 + o, bb + o);
+      }
     });
   for (auto& x : th) x.join();
-  d_w0.upload(h_w0, st_);
-  d_w1.upload(h_w1, st_);
-  d_b.upload(h_b, st_);
+  DDG_CUDA(cudaMemcpyAsync(d_w0.ptr, w0, nm * sizeof(double), cudaMemcpyHostToDevice, st_));
+  DDG_CUDA(cudaMemcpyAsync(d_w1.ptr, w1, nm * sizeof(double), cudaMemcpyHostToDevice, st_));
+  DDG_CUDA(cudaMemcpyAsync(d_b.ptr, bb, nm * sizeof(double), cudaMemcpyHostToDevice, st_));
+  layers_valid_ = true;
 }
 
 void Workspace::reseed(uint64_t seed) {
   plan.seed = seed;
   for (size_t i = 0; i < plan.subs.size(); ++i) plan.subs[i].seed = seed + i;
   built_ = coarse_built_ = neumann_built_ = false;
+  layers_valid_ = false;
+}
+
+int Workspace::ktimer_begin() {
+  if (!profiling_) return -1;
+  if (ev_pool_.size() < 2 * (pending_.size() + 1)) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      DDG_CUDA(cudaEventCreate(&e));
+      ev_pool_.push_back(e);
+    }
+  }
+  const int slot = static_cast<int>(pending_.size());
+  PendingTimer t{ev_pool_[2 * slot], ev_pool_[2 * slot + 1], nullptr, 0, 0};
+  DDG_CUDA(cudaEventRecord(t.a, st_));
+  pending_.push_back(t);
+  return slot;
+}
+
+void Workspace::ktimer_end(int slot, const char* family, double flops, double bytes) {
+  if (slot < 0) return;
+  PendingTimer& t = pending_[slot];
+  t.family = family;
+  t.flops = flops;
+  t.bytes = bytes;
+  DDG_CUDA(cudaEventRecord(t.b, st_));
+}
+
+void Workspace::ktimer_collect() {
+  if (pending_.empty()) return;
+  DDG_CUDA(cudaStreamSynchronize(st_));
+  for (const PendingTimer& t : pending_) {
+    float ms = 0;
+    DDG_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+    auto it = std::find_if(stats_.begin(), stats_.end(), [&](const auto& s) { return s.first == t.family; });
+    if (it == stats_.end()) {
+      stats_.push_back({t.family, KernelStat{}});
+      it = stats_.end() - 1;
+    }
+    it->second.ms += ms;
+    it->second.flops += t.flops;
+    it->second.bytes += t.bytes;
+    it->second.launches += 1;
+  }
+  pending_.clear();
+}
+
+bool Workspace::kernel_stat(const std::string& name, KernelStat* out) const {
+  for (const auto& s : stats_)
+    if (s.first == name) {
+      *out = s.second;
+      return true;
+    }
+  return false;
 }
 
 FeatureArgs Workspace::feature_args() {
@@ -295,22 +356,35 @@ void Workspace::build() {
   const Plan& p = plan;
   launches_ = 0;
   const auto h0 = std::chrono::steady_clock::now();
-  init_layers();
+  if (!layers_valid_) init_layers();
   DDG_CUDA(cudaEventRecord(ev_[0], st_));
+  const double nmat_d = 2.0 * p.N;
+  int kt = ktimer_begin();
   launch_build_features(feature_args(), st_);
+  // algorithmic bytes: every generated matrix entry written once (SURVEY.md §8d B_feat)
+  ktimer_end(kt, "build_features", 0.0, 8.0 * p.N * static_cast<double>(p.M) * (2.0 * p.m + p.fmax + p.dmax));
   launches_ += 2;
   DDG_CUDA(cudaEventRecord(ev_[1], st_));
   QrArgs q{2 * p.N, p.m, ld_, ncol_, p.M, d_A.ptr, d_tau.ptr, d_T.ptr};
   for (int k0 = 0; k0 < p.M; k0 += kQrNB) {
+    const int nb = std::min(kQrNB, p.M - k0);
+    const double mrows = p.m - k0;
+    kt = ktimer_begin();
     launch_qr_panel(q, k0, st_);
+    ktimer_end(kt, "qr_panel", nmat_d * (4.0 * mrows * nb * nb / 2.0), 0.0);
+    kt = ktimer_begin();
     launch_qr_trailing(q, k0, st_);
+    // two GEMMs of the compact-WY update: W = V^T A and A -= V (T^T W)
+    ktimer_end(kt, "qr_trailing", nmat_d * 4.0 * mrows * nb * std::max(0, ncol_ - k0 - nb), 0.0);
     launches_ += (ncol_ - std::min(k0 + kQrNB, p.M) > 0) ? 2 : 1;
   }
   launch_qr_diag_ratio(q, d_ratio.ptr, st_);
   launches_ += 1;
   DDG_CUDA(cudaEventRecord(ev_[2], st_));
   CodArgs c = cod_args();
+  kt = ktimer_begin();
   launch_cod_pivqr(c, st_);
+  ktimer_end(kt, "cod_pivqr", 0.0, 0.0);
   launches_ += 1;
   // ranks decide the packed strides of everything downstream
   std::vector<int> rank(2 * p.N), status(2 * p.N);
@@ -334,7 +408,9 @@ void Workspace::build() {
   d_s.alloc(static_cast<size_t>(p.N) * rmax_);
   d_u.alloc(static_cast<size_t>(p.N) * rmax_);
   c = cod_args();
+  kt = ktimer_begin();
   launch_cod_finish(c, st_);
+  ktimer_end(kt, "cod_finish", 0.0, 0.0);
   launches_ += 1;
   DDG_CUDA(cudaEventRecord(ev_[3], st_));
   built_ = true;
@@ -375,6 +451,7 @@ BlockArgs Workspace::block_args() {
   b.Zc = d_Zc.ptr;
   b.pd = d_pd.ptr;
   b.Gc = d_Gc.ptr;
+  b.Ypi = d_Ypi.ptr;
   b.corner_q = d_corner_q.ptr;
   b.Dpp = d_Dpp.ptr;
   b.dpi = d_dpi.ptr;
@@ -439,12 +516,16 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.use_neumann = theta > 0.0 ? 1 : 0;
   {
     const char* op = std::getenv("DDELM_OPERATOR");
-    a.coeff_space = (op && std::strcmp(op, "coeff") == 0) ? 1 : 0;
+    // default: the reference's coefficient-space grouping (iteration-count parity)
+    a.coeff_space = (op && std::strcmp(op, "fused") == 0) ? 0 : 1;
   }
   a.F = d_F.ptr;
   a.ldF = p.fmax;
+  a.Cd = d_Cd.ptr;
+  a.ldC = p.dmax;
   d_cwork.alloc(static_cast<size_t>(p.N) * p.M);
   a.cwork = d_cwork.ptr;
+  a.Ypi = d_Ypi.ptr;
   a.rel_tol = tol;
   a.max_iter = max_iter;
   a.rank = d_rank.ptr;
@@ -497,47 +578,17 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   return a;
 }
 
-void Workspace::run_cg_graph(const CgArgs& a) {
-  const char* mode = std::getenv("DDELM_CG_MODE");
-  const bool use_cond = !(mode && std::strcmp(mode, "loop") == 0);
-  if (graph_exec_) {
-    cudaGraphExecDestroy(graph_exec_);
-    graph_exec_ = nullptr;
+void Workspace::run_cg(const CgArgs& a) {
+  // the whole iteration loop is one persistent cooperative kernel (k_cg.cu)
+  const size_t need = 2 * static_cast<size_t>(cg_persistent_grid(a)) + 2;
+  if (d_partial.count < need) {
+    d_partial.alloc(need);
+    CgArgs b = a;
+    b.partial = d_partial.ptr;
+    cg_launch_persistent(b, st_);
+    return;
   }
-  if (graph_) {
-    cudaGraphDestroy(graph_);
-    graph_ = nullptr;
-  }
-  if (use_cond) {
-    DDG_CUDA(cudaGraphCreate(&graph_, 0));
-    cudaGraphConditionalHandle h;
-    DDG_CUDA(cudaGraphConditionalHandleCreate(&h, graph_, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t node;
-    DDG_CUDA(cudaGraphAddNode(&node, graph_, nullptr, 0, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    DDG_CUDA(cudaStreamBeginCaptureToGraph(cap_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    cg_launch_step(a, cap_, static_cast<unsigned long long>(h), true);
-    DDG_CUDA(cudaStreamEndCapture(cap_, &body));
-    DDG_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
-    DDG_CUDA(cudaGraphLaunch(graph_exec_, st_));
-  } else {
-    // fallback: a graph of 16 iterations, relaunched until the device flags completion
-    DDG_CUDA(cudaStreamBeginCapture(cap_, cudaStreamCaptureModeThreadLocal));
-    for (int k = 0; k < 16; ++k) cg_launch_step(a, cap_, 0ull, false);
-    DDG_CUDA(cudaStreamEndCapture(cap_, &graph_));
-    DDG_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
-    for (;;) {
-      DDG_CUDA(cudaGraphLaunch(graph_exec_, st_));
-      DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
-      DDG_CUDA(cudaStreamSynchronize(st_));
-      if (pinned_state_[1]) break;
-    }
-  }
+  cg_launch_persistent(a, st_);
 }
 
 SolveResult Workspace::solve(int method, double theta, double tol, int max_iter) {
@@ -559,13 +610,22 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   if (max_iter <= 0) max_iter = 20 * p.n_delta;
   if (p.n_delta == 0) throw std::invalid_argument("s = 1 (local-only solve) is not on the device path");
   d_hist.alloc(static_cast<size_t>(max_iter));
+  {
+    // the persistent CG kernel needs 2 x grid partial slots
+    CgArgs probe = cg_args(theta, tol, max_iter);
+    const size_t need = std::max<size_t>(2 * static_cast<size_t>(cg_persistent_grid(probe)) + 2,
+                                         2 * static_cast<size_t>(ceil_div(p.n_delta, 256)) + 2);
+    if (d_partial.count < need) d_partial.alloc(need);
+  }
   CgArgs a = cg_args(theta, tol, max_iter);
   DDG_CUDA(cudaEventRecord(ev_[8], st_));
   cg_launch_operator(a, nullptr, d_rhs.ptr, 1, st_);
   cg_launch_init(a, st_);
-  launches_ += cg_kernels_per_step(a) - 3 + 2;
+  launches_ += cg_kernels_per_step(a) + 2;
   DDG_CUDA(cudaEventRecord(ev_[9], st_));
-  run_cg_graph(a);
+  const int kt_cg = ktimer_begin();
+  run_cg(a);
+  ktimer_end(kt_cg, "cg_iterations", 0.0, 0.0);
   DDG_CUDA(cudaEventRecord(ev_[10], st_));
   cg_launch_reconstruct(a, st_);
   launches_ += 3;
@@ -576,8 +636,7 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   res.iterations = state[5];
   res.converged = state[2] != 0;
   res.negative_curvature = state[3] != 0;
-  // every iteration runs the whole captured step (kernels no-op only after completion)
-  launches_ += static_cast<long long>(std::max(res.iterations, 1)) * cg_kernels_per_step(a);
+  launches_ += 1;  // the persistent CG kernel
   last_iterations_ = res.iterations;
   auto ms = [&](int e0, int e1) {
     float t = 0;
@@ -593,6 +652,29 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   phase_ms_[6] = ms(9, 10);  // cg
   phase_ms_[7] = ms(10, 11); // reconstruct
   res.phase_ms.assign(phase_ms_, phase_ms_ + 8);
+  device_span_ms_ = ms(0, 11);
+  if (kt_cg >= 0) {
+    // algorithmic bytes of one interface iteration: every operator block read as the kernels
+    // read it, times the iterations run
+    double per_it = 0;
+    const int N = p.N;
+    for (int i = 0; i < N; ++i) {
+      const ClassPlan& cp = p.classes[p.subs[i].cls];
+      const double r = h_rank[i], rb = h_rank[N + i];
+      const double M = p.M, ng = cp.n_gamma, nF = cp.nF, nd = cp.nd;
+      double b = 3.0 * r * ng + p.crmax * ng * 2.0;  // Q_G (op1, op4 + corners), Zc (op1, op4)
+      if (a.coeff_space) b += 2.0 * M * r + 2.0 * M * nF + 4.0 * M;  // C, F, Ypi
+      else b += 2.0 * nF * r;                                          // FC
+      if (method == 2) {
+        b += 2.0 * rb * nd;                                            // Qbar_flux
+        b += a.coeff_space ? 2.0 * M * rb + 2.0 * M * nd : 2.0 * nd * rb;  // Cbar, Cdelta | CCb
+      }
+      per_it += 8.0 * b;
+    }
+    per_it += 8.0 * (2.0 * p.n_pi * p.n_pi + 4.0 * p.npf * p.n_pi);  // S^{-1}, Dpp (coarse solves)
+    pending_[kt_cg].bytes = per_it * std::max(res.iterations, 1);
+  }
+  ktimer_collect();
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
   solve_launches_ = launches_ - l0;
   solved_ = true;
@@ -615,12 +697,14 @@ void Workspace::apply_operator(double theta, const double* v, double* out) {
 
 void Workspace::get_mu(double* mu) {
   const Plan& p = plan;
-  DDG_CUDA(cudaMemcpy(mu, d_x.ptr, sizeof(double) * p.n_delta, cudaMemcpyDeviceToHost));
-  if (p.n_pi) DDG_CUDA(cudaMemcpy(mu + p.n_delta, d_mu_pi_out.ptr, sizeof(double) * p.n_pi, cudaMemcpyDeviceToHost));
+  DDG_CUDA(cudaMemcpyAsync(mu, d_x.ptr, sizeof(double) * p.n_delta, cudaMemcpyDeviceToHost, st_));
+  if (p.n_pi) DDG_CUDA(cudaMemcpyAsync(mu + p.n_delta, d_mu_pi_out.ptr, sizeof(double) * p.n_pi, cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
 }
 
 void Workspace::get_coeffs(double* c) {
-  DDG_CUDA(cudaMemcpy(c, d_coeffs.ptr, sizeof(double) * plan.N * plan.M, cudaMemcpyDeviceToHost));
+  DDG_CUDA(cudaMemcpyAsync(c, d_coeffs.ptr, sizeof(double) * plan.N * plan.M, cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
 }
 
 int Workspace::get_residuals(double* h, int cap) {

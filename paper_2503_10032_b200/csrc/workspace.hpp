@@ -29,6 +29,12 @@ struct DevBuf {
   void upload(const std::vector<T>& v, cudaStream_t st);
 };
 
+/// Optional per-kernel-family CUDA-event timers (bench.py's live roofline numbers).
+struct KernelStat {
+  double ms = 0, flops = 0, bytes = 0;
+  long long launches = 0;
+};
+
 struct SolveResult {
   int iterations = 0;
   bool converged = false, negative_curvature = false;
@@ -48,7 +54,12 @@ class Workspace {
   void build_neumann();
   SolveResult solve(int method, double theta, double tol, int max_iter);
   void reseed(uint64_t seed);
+  /// drop every built layer but keep the uploaded feature layers (device-resident inputs)
+  void invalidate() { built_ = coarse_built_ = neumann_built_ = false; }
   void apply_operator(double theta, const double* v, double* out);
+  void set_profiling(bool on) { profiling_ = on; }
+  bool kernel_stat(const std::string& name, KernelStat* out) const;
+  double device_span_ms() const { return device_span_ms_; }
 
   void get_mu(double* mu);
   void get_coeffs(double* c);
@@ -72,7 +83,23 @@ class Workspace {
   CodArgs cod_args();
   BlockArgs block_args();
   CgArgs cg_args(double theta, double tol, int max_iter);
-  void run_cg_graph(const CgArgs& a);
+  void run_cg(const CgArgs& a);
+  // kernel timers: begin/end around a launch; collected after the stream syncs
+  int ktimer_begin();
+  void ktimer_end(int slot, const char* family, double flops, double bytes);
+  void ktimer_collect();
+  struct PendingTimer {
+    cudaEvent_t a, b;
+    const char* family;
+    double flops, bytes;
+  };
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<PendingTimer> pending_;
+  std::vector<std::pair<std::string, KernelStat>> stats_;
+  bool profiling_ = false;
+  double device_span_ms_ = 0;
+  double* h_layers_ = nullptr;  // pinned staging of w0 | w1 | b
+  bool layers_valid_ = false;
 
   int device_ = 0;
   cudaStream_t st_ = nullptr, cap_ = nullptr;
@@ -99,7 +126,7 @@ class Workspace {
   DevBuf<int> d_deficient, d_rank, d_status, d_perm, d_corner_q, d_spd_fail, d_state;
   DevBuf<double> d_V1, d_F1, d_Rr, d_tau1, d_zc, d_upd, d_dir, d_C, d_Y, d_QtX;
   // interface blocks / coarse
-  DevBuf<double> d_FC, d_CCb, d_Zc, d_pd, d_Gc, d_Dpp, d_dpi, d_S, d_Sinv;
+  DevBuf<double> d_FC, d_CCb, d_Zc, d_pd, d_Gc, d_Ypi, d_Dpp, d_dpi, d_S, d_Sinv;
   // CG
   DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu, d_nu, d_mu_pi_out, d_d1,
       d_d2, d_bot, d_tpart, d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_cwork;
