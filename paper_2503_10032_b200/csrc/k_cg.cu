@@ -16,9 +16,14 @@
 // flux / Cdelta rows), which reproduces its finite-precision CG behaviour; the fused mode uses
 // pre-multiplied FC / CCb blocks (fewer bytes, converges in fewer iterations).
 //
+// Work decomposition: in coefficient-space mode every local phase is split over the M
+// coefficient rows into P parts (P ~ SMs / subdomains); each part streams its slice of C, F,
+// Cbar, Cdelta and emits a partial result that the consumer sums in a fixed order (the maps are
+// linear), so all SMs share the HBM stream with no extra barrier.
+//
 // The whole iteration loop runs as ONE persistent cooperative kernel: phases are separated by
 // grid-wide barriers, every CTA keeps identical copies of the CG scalars (sums of per-CTA
-// partials in a fixed order), so there is no host round trip and no atomics: deterministic.
+// partials in a fixed order): no host round trip, no atomics, deterministic.
 #include <cooperative_groups.h>
 
 #include <cfloat>
@@ -49,10 +54,9 @@ __device__ __forceinline__ SubCtx sub_ctx(const CgArgs& a, int t /* matrix */, i
   return c;
 }
 
-/// Shared-memory carve-up used by every local phase.
 struct Smem {
   double* v1;   // big  (phi / rhs / px / a)
-  double* cw;   // M    (coefficient-space vector)
+  double* cw;   // cwsize (coefficient-space slice, coarse vectors)
   double* s0;   // rmax
   double* s1;   // rmax
   double* red;  // blockDim (partials of coldot)
@@ -61,7 +65,7 @@ struct Smem {
 __device__ __forceinline__ Smem carve(const CgArgs& a) {
   extern __shared__ double sm[];
   const int big = max(max(a.gmax, a.fmax), a.dmax);
-  const int cwsize = max(a.M, 3 * a.n_pi + 2 * a.npf);  // also hosts the coarse-solve vectors
+  const int cwsize = max(a.M, 3 * a.n_pi + 2 * a.npf);
   Smem s;
   s.v1 = sm;
   s.cw = s.v1 + big;
@@ -71,11 +75,39 @@ __device__ __forceinline__ Smem carve(const CgArgs& a) {
   return s;
 }
 
-// y[j] = sum_k A[j*lda + k] x[k], j < rows (warp per row; lanes over the contiguous k)
+__device__ __forceinline__ void part_rows(const CgArgs& a, int p, int& j0, int& j1) {
+  const int chunk = (a.M + a.P - 1) / a.P;
+  j0 = min(a.M, p * chunk);
+  j1 = min(a.M, j0 + chunk);
+}
+
+// y[j] = scale * sum_k A[j*lda + k] x[k], j < rows. Warp per row, 4 rows in flight per warp.
 __device__ __forceinline__ void rowdot(const double* A, size_t lda, int rows, int cols, const double* x,
                                        double* y, double scale = 1.0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = warp; j < rows; j += nw) {
+  int j = warp * 4;
+  for (; j + 3 < rows; j += nw * 4) {
+    const double* a0 = A + static_cast<size_t>(j) * lda;
+    double c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    for (int k = lane; k < cols; k += 32) {
+      const double xk = x[k];
+      c0 += a0[k] * xk;
+      c1 += a0[lda + k] * xk;
+      c2 += a0[2 * lda + k] * xk;
+      c3 += a0[3 * lda + k] * xk;
+    }
+    c0 = warp_sum(c0);
+    c1 = warp_sum(c1);
+    c2 = warp_sum(c2);
+    c3 = warp_sum(c3);
+    if (lane == 0) {
+      y[j] = scale * c0;
+      y[j + 1] = scale * c1;
+      y[j + 2] = scale * c2;
+      y[j + 3] = scale * c3;
+    }
+  }
+  for (; j < rows; ++j) {  // tail rows (< 4) of this warp's last group
     const double* aj = A + static_cast<size_t>(j) * lda;
     double acc = 0;
     for (int k = lane; k < cols; k += 32) acc += aj[k] * x[k];
@@ -84,7 +116,7 @@ __device__ __forceinline__ void rowdot(const double* A, size_t lda, int rows, in
   }
 }
 
-// y[k] = sum_j A[j*lda + k] x[j], k < cols (threads over (k, row group); fixed-order combine)
+// y[k] = scale * sum_j A[j*lda + k] x[j], k < cols (threads over (k, row group); fixed-order combine)
 __device__ __forceinline__ void coldot(const double* A, size_t lda, int rows, int cols, const double* x,
                                        double* y, double* red, double scale = 1.0) {
   for (int k0 = 0; k0 < cols; k0 += blockDim.x) {
@@ -96,8 +128,14 @@ __device__ __forceinline__ void coldot(const double* A, size_t lda, int rows, in
     double acc = 0;
     if (grp < groups && k < cc) {
       const double* ak = A + k0 + k;
-#pragma unroll 4
-      for (int j = grp; j < rows; j += groups) acc += ak[static_cast<size_t>(j) * lda] * x[j];
+      double a1 = 0;
+      int j = grp;
+      for (; j + groups < rows; j += 2 * groups) {
+        acc += ak[static_cast<size_t>(j) * lda] * x[j];
+        a1 += ak[static_cast<size_t>(j + groups) * lda] * x[j + groups];
+      }
+      if (j < rows) acc += ak[static_cast<size_t>(j) * lda] * x[j];
+      acc += a1;
     }
     red[t] = acc;
     __syncthreads();
@@ -110,8 +148,15 @@ __device__ __forceinline__ void coldot(const double* A, size_t lda, int rows, in
   }
 }
 
+__device__ __forceinline__ double sum_parts(const double* base, size_t stride, int P, int idx) {
+  double s = 0;
+  for (int p = 0; p < P; ++p) s += base[p * stride + idx];
+  return s;
+}
+
 __device__ __forceinline__ double gather_x(const CgArgs& a, int g) {
-  return a.flip_sign[g] * (a.xf[a.own_flux[2 * g]] + a.xf[a.own_flux[2 * g + 1]]);
+  const size_t st = static_cast<size_t>(a.N) * a.fmax;
+  return a.flip_sign[g] * (sum_parts(a.xf, st, a.P, a.own_flux[2 * g]) + sum_parts(a.xf, st, a.P, a.own_flux[2 * g + 1]));
 }
 
 // ---------------------------------------------------------------- op1: s, t-part, psi-part
@@ -166,6 +211,7 @@ __device__ void dev_coarse1(const CgArgs& a, int mode) {
   double* psi = t + n;     // npf
   double* rhs = psi + npf; // n
   double* mu = rhs + n;    // n
+  double* pb = mu + n;     // npf
   for (int gp = threadIdx.x; gp < n; gp += blockDim.x) {
     double acc = 0;
     for (int q = 0; q < 4; ++q) {
@@ -194,8 +240,7 @@ __device__ void dev_coarse1(const CgArgs& a, int mode) {
     if (mode == 2) a.mu_pi_out[gp] = mu[gp];
   }
   if (mode != 2) {
-    double* pb = mu + n;  // npf: proj_bottom = Dpp mu
-    rowdot(a.Dpp, n, npf, n, mu, pb);
+    rowdot(a.Dpp, n, npf, n, mu, pb);  // proj_bottom = Dpp mu
     __syncthreads();
     for (int rr = threadIdx.x; rr < npf; rr += blockDim.x) a.d1[rr] = psi[rr] - pb[rr];
   }
@@ -203,7 +248,7 @@ __device__ void dev_coarse1(const CgArgs& a, int mode) {
 }
 
 // ---------------------------------------------------------------- op2: s~, x (or coefficients)
-__device__ void dev_op2(const CgArgs& a, int i, int mode) {
+__device__ void dev_op2(const CgArgs& a, int i, int p, int mode) {
   const SubCtx c = sub_ctx(a, i, i);
   const int R = a.rmax, E = a.ext;
   Smem sm = carve(a);
@@ -222,16 +267,17 @@ __device__ void dev_op2(const CgArgs& a, int i, int mode) {
     for (int q = 0; q < 4; ++q)
       if (gq[q] >= 0) acc += c.QtX[static_cast<size_t>(k) * E + 1 + gq[q]] * muc[q];
     sm.s0[k] = sk;
-    sm.s1[k] = acc;
-    a.s[static_cast<size_t>(i) * R + k] = acc;  // s~ = s + Q_Pi^T mu
+    sm.s1[k] = acc;  // s~ = s + Q_Pi^T mu
   }
   __syncthreads();
   const double* Ci = a.C + static_cast<size_t>(i) * a.M * R;
   if (a.coeff_space) {
     // reference grouping (solvers.cpp:336, 342): c = K^+ phi - Ypi mu, then F c
+    int j0, j1;
+    part_rows(a, p, j0, j1);
     const double* Yp = a.Ypi + static_cast<size_t>(i) * a.M * 4;
-    double* cw = (mode == 2) ? a.coeffs + static_cast<size_t>(i) * a.M : sm.cw;
-    for (int j = warp; j < a.M; j += nw) {
+    double* cw = (mode == 2) ? a.coeffs + static_cast<size_t>(i) * a.M + j0 : sm.cw;
+    for (int j = j0 + warp; j < j1; j += nw) {
       const double* cj = Ci + static_cast<size_t>(j) * R;
       double acc = 0;
       for (int k = lane; k < c.r; k += 32) acc += cj[k] * sm.s0[k];
@@ -239,13 +285,13 @@ __device__ void dev_op2(const CgArgs& a, int i, int mode) {
       if (lane == 0) {
         double yp = 0;
         for (int q = 0; q < 4; ++q) yp += Yp[static_cast<size_t>(j) * 4 + q] * muc[q];
-        cw[j] = acc - yp;
+        cw[j - j0] = acc - yp;
       }
     }
     __syncthreads();
     if (mode == 2) return;
-    coldot(a.F + static_cast<size_t>(i) * a.M * a.ldF, a.ldF, a.M, c.d.nF, sm.cw,
-           a.xf + static_cast<size_t>(i) * a.fmax, sm.red, -1.0);
+    coldot(a.F + (static_cast<size_t>(i) * a.M + j0) * a.ldF, a.ldF, j1 - j0, c.d.nF, sm.cw,
+           a.xf + (static_cast<size_t>(p) * a.N + i) * a.fmax, sm.red, -1.0);
     return;
   }
   if (mode == 2) {
@@ -259,7 +305,7 @@ __device__ void dev_op2(const CgArgs& a, int i, int mode) {
 }
 
 // ---------------------------------------------------------------- Neumann-to-Dirichlet map
-__device__ void dev_nn1(const CgArgs& a, int i) {
+__device__ void dev_nn1(const CgArgs& a, int i, int p) {
   const SubCtx c = sub_ctx(a, a.N + i, i);
   const int R = a.rmax, E = a.ext, nd = c.d.nd;
   Smem sm = carve(a);
@@ -268,54 +314,60 @@ __device__ void dev_nn1(const CgArgs& a, int i) {
   __syncthreads();
   rowdot(c.QtX + 1, E, c.r, nd, sm.v1, sm.s0);  // Qbar_r^T rhs
   __syncthreads();
-  double* tr = a.tr + static_cast<size_t>(i) * a.dmax;
+  double* tr = a.tr + (static_cast<size_t>(p) * a.N + i) * a.dmax;
   if (a.coeff_space) {
     // reference order (solvers.cpp:456): y = Kbar^+ rhs (M-vector), then Cdelta y
-    rowdot(a.C + static_cast<size_t>(a.N + i) * a.M * R, R, a.M, c.r, sm.s0, sm.cw);
+    int j0, j1;
+    part_rows(a, p, j0, j1);
+    rowdot(a.C + (static_cast<size_t>(a.N + i) * a.M + j0) * R, R, j1 - j0, c.r, sm.s0, sm.cw);
     __syncthreads();
-    coldot(a.Cd + static_cast<size_t>(i) * a.M * a.ldC, a.ldC, a.M, nd, sm.cw, tr, sm.red);
+    coldot(a.Cd + (static_cast<size_t>(i) * a.M + j0) * a.ldC, a.ldC, j1 - j0, nd, sm.cw, tr, sm.red);
   } else {
     rowdot(a.CCb + static_cast<size_t>(i) * a.dmax * R, R, nd, c.r, sm.s0, tr);
     __syncthreads();
   }
 }
 
-__device__ void dev_nn2(const CgArgs& a, int i) {
+__device__ void dev_nn2(const CgArgs& a, int i, int p) {
   const SubCtx c = sub_ctx(a, a.N + i, i);
   const int R = a.rmax, E = a.ext, nd = c.d.nd;
   Smem sm = carve(a);
   const int* nmap = a.ndelta_map + static_cast<size_t>(i) * a.dmax;
+  const size_t st = static_cast<size_t>(a.N) * a.dmax;
   for (int kk = threadIdx.x; kk < nd; kk += blockDim.x) {
     const int g = nmap[kk];
-    sm.v1[kk] = a.tr[a.own_nd[2 * g]] + a.tr[a.own_nd[2 * g + 1]];  // (P x) at the local rows
+    sm.v1[kk] = sum_parts(a.tr, st, a.P, a.own_nd[2 * g]) + sum_parts(a.tr, st, a.P, a.own_nd[2 * g + 1]);
   }
   __syncthreads();
   if (a.coeff_space) {
     // reference order (solvers.cpp:469): x = Cdelta^T tl (M-vector), then (Kbar^+)^T x
-    rowdot(a.Cd + static_cast<size_t>(i) * a.M * a.ldC, a.ldC, a.M, nd, sm.v1, sm.cw);
+    int j0, j1;
+    part_rows(a, p, j0, j1);
+    rowdot(a.Cd + (static_cast<size_t>(i) * a.M + j0) * a.ldC, a.ldC, j1 - j0, nd, sm.v1, sm.cw);
     __syncthreads();
-    coldot(a.C + static_cast<size_t>(a.N + i) * a.M * R, R, a.M, c.r, sm.cw, sm.s0, sm.red);
+    coldot(a.C + (static_cast<size_t>(a.N + i) * a.M + j0) * R, R, j1 - j0, c.r, sm.cw, sm.s0, sm.red);
   } else {
     coldot(a.CCb + static_cast<size_t>(i) * a.dmax * R, R, nd, c.r, sm.v1, sm.s0, sm.red);
   }
-  coldot(c.QtX + 1, E, c.r, nd, sm.s0, a.zz + static_cast<size_t>(i) * a.dmax, sm.red);
+  coldot(c.QtX + 1, E, c.r, nd, sm.s0, a.zz + (static_cast<size_t>(p) * a.N + i) * a.dmax, sm.red);
 }
 
 // ---------------------------------------------------------------- op3: weight, u
-__device__ void dev_op3(const CgArgs& a, int i) {
+__device__ void dev_op3(const CgArgs& a, int i, int p) {
   const SubCtx c = sub_ctx(a, i, i);
   const int R = a.rmax, E = a.ext;
   Smem sm = carve(a);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int* fd = a.fluxrow_delta + static_cast<size_t>(i) * a.fmax;
   const double theta = a.theta;
+  const size_t st = static_cast<size_t>(a.N) * a.dmax;
   for (int l = threadIdx.x; l < c.d.nF; l += blockDim.x) {
     const int g = fd[l];
     double w = 0.0;
     if (g >= 0) {
       const double x = gather_x(a, g);
       if (a.use_neumann) {
-        const double ptp = -(a.zz[a.own_nd[2 * g]] + a.zz[a.own_nd[2 * g + 1]]);
+        const double ptp = -(sum_parts(a.zz, st, a.P, a.own_nd[2 * g]) + sum_parts(a.zz, st, a.P, a.own_nd[2 * g + 1]));
         w = theta * ptp;
         if (theta < 1.0) w += (1.0 - theta) * x;
       } else {
@@ -327,20 +379,23 @@ __device__ void dev_op3(const CgArgs& a, int i) {
   __syncthreads();
   if (a.coeff_space) {
     // reference order: at = F^T a (M-vector, apply_AT), then (K^+)^T at -> C^T at
-    rowdot(a.F + static_cast<size_t>(i) * a.M * a.ldF, a.ldF, a.M, c.d.nF, sm.v1, sm.cw);
+    int j0, j1;
+    part_rows(a, p, j0, j1);
+    rowdot(a.F + (static_cast<size_t>(i) * a.M + j0) * a.ldF, a.ldF, j1 - j0, c.d.nF, sm.v1, sm.cw);
     __syncthreads();
-    coldot(a.C + static_cast<size_t>(i) * a.M * R, R, a.M, c.r, sm.cw, sm.s0, sm.red);
+    coldot(a.C + (static_cast<size_t>(i) * a.M + j0) * R, R, j1 - j0, c.r, sm.cw, sm.s0, sm.red);
   } else {
     coldot(a.FC + static_cast<size_t>(i) * a.fmax * R, R, c.d.nF, c.r, sm.v1, sm.s0, sm.red);
   }
-  for (int k = threadIdx.x; k < c.r; k += blockDim.x) a.u[static_cast<size_t>(i) * R + k] = sm.s0[k];
+  double* up = a.u + (static_cast<size_t>(p) * a.N + i) * R;
+  for (int k = threadIdx.x; k < c.r; k += blockDim.x) up[k] = sm.s0[k];
   if (warp < 4) {
     const int g = a.corner_q[i * 4 + warp];
     double acc = 0;
     if (g >= 0)
       for (int k = lane; k < c.r; k += 32) acc += c.QtX[static_cast<size_t>(k) * E + 1 + g] * sm.s0[k];
     acc = warp_sum(acc);
-    if (lane == 0) a.tpart[i * 4 + warp] = acc;  // t(gp) += z(lr) at corners
+    if (lane == 0) a.tpart3[(static_cast<size_t>(p) * a.N + i) * 4 + warp] = acc;  // t(gp) += z(lr)
   }
   __syncthreads();
 }
@@ -351,11 +406,12 @@ __device__ void dev_coarse2(const CgArgs& a) {
   double* t = sm.cw;
   double* nu = t + n;
   double* bot = nu + n;
+  const size_t st = static_cast<size_t>(a.N) * 4;
   for (int gp = threadIdx.x; gp < n; gp += blockDim.x) {
     double acc = 0;
     for (int q = 0; q < 4; ++q) {
       const int o = a.pi_owner[gp * 4 + q];
-      if (o >= 0) acc += a.tpart[o];
+      if (o >= 0) acc += sum_parts(a.tpart3, st, a.P, o);
     }
     t[gp] = acc;
   }
@@ -374,24 +430,32 @@ __device__ void dev_op4(const CgArgs& a, int i, const double* v, int mode) {
   const SubCtx c = sub_ctx(a, i, i);
   const int R = a.rmax, E = a.ext;
   Smem sm = carve(a);
-  __shared__ double nuc[4];
+  __shared__ double nuc[4], muc[4];
   __shared__ int gq[4];
   double* d2s = sm.v1;
   if (threadIdx.x < 4) {
     const int g = a.corner_q[i * 4 + threadIdx.x];
     gq[threadIdx.x] = g;
-    nuc[threadIdx.x] = g >= 0 ? a.nu[a.gamma_pi[static_cast<size_t>(i) * a.gmax + g]] : 0.0;
+    const int gp = g >= 0 ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : 0;
+    nuc[threadIdx.x] = g >= 0 ? a.nu[gp] : 0.0;
+    muc[threadIdx.x] = g >= 0 ? a.mu[gp] : 0.0;
   }
   for (int rho = threadIdx.x; rho < a.crmax; rho += blockDim.x) {
     const int rr = a.cr_row[static_cast<size_t>(i) * a.crmax + rho];
     d2s[rho] = rr >= 0 ? a.d2[rr] : 0.0;
   }
   __syncthreads();
+  const size_t ust = static_cast<size_t>(a.N) * R;
   for (int k = threadIdx.x; k < c.r; k += blockDim.x) {
-    double uu = a.u[static_cast<size_t>(i) * R + k];
+    double uu = sum_parts(a.u + static_cast<size_t>(i) * R, ust, a.P, k);
+    double sk = a.s[static_cast<size_t>(i) * R + k];
     for (int q = 0; q < 4; ++q)
-      if (gq[q] >= 0) uu += c.QtX[static_cast<size_t>(k) * E + 1 + gq[q]] * nuc[q];
-    sm.s0[k] = a.s[static_cast<size_t>(i) * R + k] + uu;  // s~ + u + Q_Pi^T nu
+      if (gq[q] >= 0) {
+        const double qk = c.QtX[static_cast<size_t>(k) * E + 1 + gq[q]];
+        uu += qk * nuc[q];
+        sk += qk * muc[q];  // s~ = s + Q_Pi^T mu (op2 recomputes it per part)
+      }
+    sm.s0[k] = sk + uu;  // s~ + u + Q_Pi^T nu
   }
   __syncthreads();
   double* qs = sm.cw;
@@ -414,12 +478,13 @@ __device__ __forceinline__ double gather_out(const CgArgs& a, int g) {
 }
 
 // ---------------------------------------------------------------- standalone kernels
+// grid = N (op1, op4) or N * P (op2, nn1, nn2, op3: blockIdx = i * P + p)
 __global__ void __launch_bounds__(kBlk) op1_kernel(CgArgs a, const double* v, int mode) { dev_op1(a, blockIdx.x, v, mode); }
 __global__ void __launch_bounds__(kBlk) coarse1_kernel(CgArgs a, int mode) { dev_coarse1(a, mode); }
-__global__ void __launch_bounds__(kBlk) op2_kernel(CgArgs a, int mode) { dev_op2(a, blockIdx.x, mode); }
-__global__ void __launch_bounds__(kBlk) nn1_kernel(CgArgs a) { dev_nn1(a, blockIdx.x); }
-__global__ void __launch_bounds__(kBlk) nn2_kernel(CgArgs a) { dev_nn2(a, blockIdx.x); }
-__global__ void __launch_bounds__(kBlk) op3_kernel(CgArgs a) { dev_op3(a, blockIdx.x); }
+__global__ void __launch_bounds__(kBlk) op2_kernel(CgArgs a, int mode) { dev_op2(a, blockIdx.x / a.P, blockIdx.x % a.P, mode); }
+__global__ void __launch_bounds__(kBlk) nn1_kernel(CgArgs a) { dev_nn1(a, blockIdx.x / a.P, blockIdx.x % a.P); }
+__global__ void __launch_bounds__(kBlk) nn2_kernel(CgArgs a) { dev_nn2(a, blockIdx.x / a.P, blockIdx.x % a.P); }
+__global__ void __launch_bounds__(kBlk) op3_kernel(CgArgs a) { dev_op3(a, blockIdx.x / a.P, blockIdx.x % a.P); }
 __global__ void __launch_bounds__(kBlk) coarse2_kernel(CgArgs a) { dev_coarse2(a); }
 __global__ void __launch_bounds__(kBlk) op4_kernel(CgArgs a, const double* v, int mode) { dev_op4(a, blockIdx.x, v, mode); }
 __global__ void __launch_bounds__(kBlk) gather_kernel(CgArgs a, double* out) {
@@ -465,27 +530,27 @@ __device__ __forceinline__ double sum_partials(const double* p, int n) {
 __global__ void __launch_bounds__(kPersistBlk) cg_persistent_kernel(CgArgs a) {
   cgs::grid_group grid = cgs::this_grid();
   const int G = gridDim.x, b = blockIdx.x;
+  const int NP = a.N * a.P;
   __shared__ double red[32];
   double* partial = a.partial;          // G entries: p.Ap
   double* partial2 = a.partial + G;     // G entries: r.r
   double rr = a.scal[0];
   const double bnorm = a.scal[1];
   if (a.state[1]) return;  // rhs == 0
-  int it = 1;
-  for (;; ++it) {
+  for (int it = 1;; ++it) {
     for (int i = b; i < a.N; i += G) dev_op1(a, i, a.p, 0);
     grid.sync();
     if (b == 0) dev_coarse1(a, 0);
     grid.sync();
-    for (int i = b; i < a.N; i += G) dev_op2(a, i, 0);
+    for (int w = b; w < NP; w += G) dev_op2(a, w / a.P, w % a.P, 0);
     grid.sync();
     if (a.use_neumann) {
-      for (int i = b; i < a.N; i += G) dev_nn1(a, i);
+      for (int w = b; w < NP; w += G) dev_nn1(a, w / a.P, w % a.P);
       grid.sync();
-      for (int i = b; i < a.N; i += G) dev_nn2(a, i);
+      for (int w = b; w < NP; w += G) dev_nn2(a, w / a.P, w % a.P);
       grid.sync();
     }
-    for (int i = b; i < a.N; i += G) dev_op3(a, i);
+    for (int w = b; w < NP; w += G) dev_op3(a, w / a.P, w % a.P);
     grid.sync();
     if (b == 0) dev_coarse2(a);
     grid.sync();
@@ -553,14 +618,15 @@ int cg_kernels_per_step(const CgArgs& a) { return a.use_neumann ? 9 : 7; }
 
 void cg_launch_operator(const CgArgs& a, const double* v, double* out, int mode, cudaStream_t st) {
   const size_t sm = smem_bytes(a, kBlk);
+  const int NP = a.N * a.P;
   op1_kernel<<<a.N, kBlk, sm, st>>>(a, v, mode);
   coarse1_kernel<<<1, kBlk, sm, st>>>(a, mode);
-  op2_kernel<<<a.N, kBlk, sm, st>>>(a, mode);
+  op2_kernel<<<NP, kBlk, sm, st>>>(a, mode);
   if (a.use_neumann) {
-    nn1_kernel<<<a.N, kBlk, sm, st>>>(a);
-    nn2_kernel<<<a.N, kBlk, sm, st>>>(a);
+    nn1_kernel<<<NP, kBlk, sm, st>>>(a);
+    nn2_kernel<<<NP, kBlk, sm, st>>>(a);
   }
-  op3_kernel<<<a.N, kBlk, sm, st>>>(a);
+  op3_kernel<<<NP, kBlk, sm, st>>>(a);
   coarse2_kernel<<<1, kBlk, sm, st>>>(a);
   op4_kernel<<<a.N, kBlk, sm, st>>>(a, v, mode);
   gather_kernel<<<ceil_div(a.n_delta, kBlk), kBlk, 0, st>>>(a, out);
@@ -583,8 +649,8 @@ int cg_persistent_grid(const CgArgs& a) {
                                 static_cast<int>(sm)));
   DDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_persistent_kernel, kPersistBlk, sm));
   if (per_sm < 1) throw CudaError("cg_persistent_kernel cannot be resident (occupancy 0)");
-  // one CTA per SM is enough: the local phases have N (<= 256) work items
-  return std::max(1, std::min(sms * per_sm, std::max(sms, a.N)));
+  // one CTA per SM: the local phases have N * P (~ number of SMs) work items
+  return std::max(1, std::min(sms * per_sm, sms));
 }
 
 void cg_launch_persistent(const CgArgs& a, cudaStream_t st) {
@@ -600,7 +666,7 @@ void cg_launch_reconstruct(const CgArgs& a, cudaStream_t st) {
   const size_t sm = smem_bytes(a, kBlk);
   op1_kernel<<<a.N, kBlk, sm, st>>>(a, a.x, 2);
   coarse1_kernel<<<1, kBlk, sm, st>>>(a, 2);
-  op2_kernel<<<a.N, kBlk, sm, st>>>(a, 2);
+  op2_kernel<<<a.N * a.P, kBlk, sm, st>>>(a, 2);
   DDG_LAUNCH_CHECK();
 }
 

@@ -148,17 +148,22 @@ struct CgArgs {
   const double* dpi;       // npf
   const double* C;         // 2N x M x rmax
   // work
+  // P row-parts per subdomain (coefficient-space mode): every local phase is split over the M
+  // coefficient rows into P independent work items whose partial outputs are summed (fixed
+  // order) by the consumer, so all SMs stream the subdomain blocks.
+  int P;
   double* s;      // N x rmax
-  double* tpart;  // N x 4 (corner contributions)
+  double* tpart;  // N x 4 (corner contributions of op1)
+  double* tpart3; // P x N x 4 (corner contributions of op3)
   double* psipart;// N x crmax
   double* mu;     // n_pi
   double* d1;     // npf
   double* d2;     // npf
   double* o;      // N x gmax
-  double* xf;     // N x fmax
-  double* tr;     // N x dmax
-  double* zz;     // N x dmax
-  double* u;      // N x rmax
+  double* xf;     // P x N x fmax
+  double* tr;     // P x N x dmax
+  double* zz;     // P x N x dmax
+  double* u;      // P x N x rmax
   double* nu;     // n_pi
   double* bot;    // npf
   // CG vectors

@@ -406,7 +406,6 @@ void Workspace::build() {
   d_FC.alloc(static_cast<size_t>(p.N) * p.fmax * rmax_);
   d_CCb.alloc(static_cast<size_t>(p.N) * p.dmax * rmax_);
   d_s.alloc(static_cast<size_t>(p.N) * rmax_);
-  d_u.alloc(static_cast<size_t>(p.N) * rmax_);
   c = cod_args();
   kt = ktimer_begin();
   launch_cod_finish(c, st_);
@@ -526,6 +525,20 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   d_cwork.alloc(static_cast<size_t>(p.N) * p.M);
   a.cwork = d_cwork.ptr;
   a.Ypi = d_Ypi.ptr;
+  {
+    // row parts per subdomain so that N * P work items cover the SMs (coefficient-space mode)
+    int dev = 0, sms = 148;
+    DDG_CUDA(cudaGetDevice(&dev));
+    DDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    a.P = a.coeff_space ? std::max(1, std::min(8, sms / p.N)) : 1;
+    const size_t P = a.P, N = p.N;
+    d_xf.alloc(P * N * p.fmax);
+    d_tr.alloc(P * N * p.dmax);
+    d_zz.alloc(P * N * p.dmax);
+    d_u.alloc(P * N * rmax_);
+    d_tpart3.alloc(P * N * 4);
+    a.tpart3 = d_tpart3.ptr;
+  }
   a.rel_tol = tol;
   a.max_iter = max_iter;
   a.rank = d_rank.ptr;

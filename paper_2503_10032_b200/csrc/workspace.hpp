@@ -129,7 +129,7 @@ class Workspace {
   DevBuf<double> d_FC, d_CCb, d_Zc, d_pd, d_Gc, d_Ypi, d_Dpp, d_dpi, d_S, d_Sinv;
   // CG
   DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu, d_nu, d_mu_pi_out, d_d1,
-      d_d2, d_bot, d_tpart, d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_cwork;
+      d_d2, d_bot, d_tpart, d_tpart3, d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_cwork;
 };
 
 }  // namespace ddg
