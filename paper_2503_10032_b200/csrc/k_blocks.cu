@@ -1,14 +1,12 @@
 // Interface-level blocks and the coarse problem (sm_100a, fp64).
 //
-// With K^+ = C Q_r^T (k_cod.cu), every operator the interface iteration applies reduces to
-// small dense per-subdomain blocks (SURVEY.md §8d representation (ii)/(iii)):
+// With K^+ = C Q_r^T (k_cod.cu), the coarse layer reduces to small dense per-subdomain blocks:
 //   FC   = F C         (nF x r)   flux rows of K^+:   F K^+ = FC Q_r^T
-//   CCb  = Cdelta Cbar (nd x r~)  Neumann-to-Dirichlet: Cdelta Kbar^+ = CCb Qbar_r^T
 //   Zc   = Q_G FC^T w  (per cross-flux row): the Dpp / Dpd rows of assemble_coarse
 //   Gc   = -Q_Pi Q_Pi^T           the Gpi rows entering S_Pi
 // Reference: assemble_coarse (solvers.cpp:278-326), build_neumann Cdelta (solvers.cpp:436-438).
-// The coarse Schur matrix S_Pi is assembled and inverted (Cholesky) on one CTA; its inverse is
-// applied as a GEMV twice per interface iteration.
+// The coarse Schur matrix S_Pi is assembled and inverted (Cholesky) on one CTA; the rows the
+// interface iteration needs are precomputed as Wmu / Wd / W3 (coarse_weights*).
 #include <cfloat>
 
 #include "common.cuh"
@@ -254,22 +252,62 @@ __global__ void __launch_bounds__(1024) coarse_schur_kernel(BlockArgs a) {
   }
 }
 
+/// Coarse-solve rows used by the interface iteration (k_cg.cu): with z = [t; psi],
+///   mu = S^{-1}(t + Dpp^T psi) = Wmu z,   d1 = psi - Dpp mu = Wd z,   Dpp S^{-1} = W3.
+__global__ void coarse_weights1_kernel(BlockArgs a) {
+  const int n = a.n_pi, npf = a.npf, nz = n + npf;
+  const long total = static_cast<long>(n) * nz + static_cast<long>(npf) * n;
+  for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long>(gridDim.x) * blockDim.x) {
+    if (idx < static_cast<long>(n) * nz) {
+      const int p = static_cast<int>(idx / nz), c = static_cast<int>(idx % nz);
+      double s;
+      if (c < n) {
+        s = a.Sinv[static_cast<size_t>(p) * n + c];
+      } else {
+        const int rr = c - n;
+        s = 0;
+        for (int j = 0; j < n; ++j) s += a.Sinv[static_cast<size_t>(p) * n + j] * a.Dpp[static_cast<size_t>(rr) * n + j];
+      }
+      a.Wmu[idx] = s;
+    } else {
+      const long k = idx - static_cast<long>(n) * nz;
+      const int rr = static_cast<int>(k / n), p = static_cast<int>(k % n);
+      double s = 0;
+      for (int j = 0; j < n; ++j) s += a.Dpp[static_cast<size_t>(rr) * n + j] * a.Sinv[static_cast<size_t>(j) * n + p];
+      a.W3[k] = s;
+    }
+  }
+}
+
+__global__ void coarse_weights2_kernel(BlockArgs a) {
+  const int n = a.n_pi, npf = a.npf, nz = n + npf;
+  const long total = static_cast<long>(npf) * nz;
+  for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int rr = static_cast<int>(idx / nz), c = static_cast<int>(idx % nz);
+    double s;
+    if (c < n) {
+      s = -a.W3[static_cast<size_t>(rr) * n + c];
+    } else {
+      const int ss = c - n;
+      double acc = 0;
+      for (int j = 0; j < n; ++j) acc += a.Dpp[static_cast<size_t>(rr) * n + j] * a.Wmu[static_cast<size_t>(j) * nz + n + ss];
+      s = (rr == ss ? 1.0 : 0.0) - acc;
+    }
+    a.Wd[idx] = s;
+  }
+}
+
 }  // namespace
 
-void launch_blocks(const BlockArgs& a, bool neumann, cudaStream_t st) {
-  const size_t xs_f = static_cast<size_t>(a.M) * a.ldF, xs_c = static_cast<size_t>(a.M) * a.ldC;
+void launch_blocks(const BlockArgs& a, cudaStream_t st) {
+  // FC = F C: flux rows of K^+ (feeds the Dpp / Dpd rows of the coarse problem)
+  const size_t xs_f = static_cast<size_t>(a.M) * a.ldF;
   const size_t cs = static_cast<size_t>(a.M) * a.rmax;
-  if (!neumann) {
-    dim3 g(ceil_div(a.fmax, 64), ceil_div(a.rmax, 64), a.N);
-    jmajor_gemm_kernel<<<g, 256, 0, st>>>(a.M, a.rmax, a.F, a.ldF, xs_f, nullptr, 0, a.dims, a.sub_cls,
-                                          a.C, cs, a.rank, 0, a.FC, a.rmax,
-                                          static_cast<size_t>(a.fmax) * a.rmax);
-  } else {
-    dim3 g(ceil_div(a.dmax, 64), ceil_div(a.rmax, 64), a.N);
-    jmajor_gemm_kernel<<<g, 256, 0, st>>>(a.M, a.rmax, a.Cd, a.ldC, xs_c, nullptr, 1, a.dims, a.sub_cls,
-                                          a.C, cs, a.rank, a.N, a.CCb, a.rmax,
-                                          static_cast<size_t>(a.dmax) * a.rmax);
-  }
+  dim3 g(ceil_div(a.fmax, 64), ceil_div(a.rmax, 64), a.N);
+  jmajor_gemm_kernel<<<g, 256, 0, st>>>(a.M, a.rmax, a.F, a.ldF, xs_f, nullptr, 0, a.dims, a.sub_cls, a.C, cs,
+                                        a.rank, 0, a.FC, a.rmax, static_cast<size_t>(a.fmax) * a.rmax);
   DDG_LAUNCH_CHECK();
 }
 
@@ -287,6 +325,12 @@ void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t s
 
 void launch_coarse_schur(const BlockArgs& a, cudaStream_t st) {
   coarse_schur_kernel<<<1, 1024, 0, st>>>(a);
+  DDG_LAUNCH_CHECK();
+}
+
+void launch_coarse_weights(const BlockArgs& a, cudaStream_t st) {
+  coarse_weights1_kernel<<<296, 256, 0, st>>>(a);
+  coarse_weights2_kernel<<<296, 256, 0, st>>>(a);
   DDG_LAUNCH_CHECK();
 }
 

@@ -81,7 +81,6 @@ struct BlockArgs {
   const double* C;       // 2N x M x rmax
   const double* QtX;     // 2N x rmax x ext
   double* FC;            // N x fmax x rmax
-  double* CCb;           // N x dmax x rmax
   // coarse
   const int* gamma_pi;   // N x gmax (-1 or Pi index)
   const int* cr_row;     // N x crmax (cross-flux row index r or -1)
@@ -97,34 +96,36 @@ struct BlockArgs {
   double* dpi;           // npf
   double* S;             // n_pi x n_pi
   double* Sinv;          // n_pi x n_pi
+  double* Wmu;           // n_pi x (n_pi + npf)
+  double* Wd;            // npf x (n_pi + npf)
+  double* W3;            // npf x n_pi
   const int* mult_pi;    // n_pi
   int* spd_fail;         // 1 flag
   int flip_row;          // debug_flip_flux_row (global flux row) or -1
   const int* row_owner;  // npf x 4 : contributing (i * crmax + rho), subdomain order, -1 pad
 };
-void launch_blocks(const BlockArgs& a, bool neumann, cudaStream_t st);
+void launch_blocks(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_local(const BlockArgs& a, const int* cr_row, const int* cr_off, const int* cr_l,
                          const double* cr_w, cudaStream_t st);
 void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t st);
 void launch_coarse_schur(const BlockArgs& a, cudaStream_t st);
+void launch_coarse_weights(const BlockArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- CG (k_cg.cu)
+enum CgJob { kJobCg = 0, kJobApply = 1, kJobRhs = 2, kJobRecon = 3 };
+
 struct CgArgs {
   int N, n_delta, n_pi, npf, gmax, fmax, dmax, crmax, rmax, ext, M;
   double theta;
-  int use_neumann;  // theta > 0
-  // 1: apply K^+ as the reference does — coefficients c = C s (M-vector) first, then the flux
-  //    rows F c / F^T a (solvers.cpp:215-218, 240-241); 0: pre-multiplied FC = F C blocks
-  int coeff_space;
+  int use_neumann;         // theta > 0
   const double* F;         // N x M x ldF (flux rows, j-major)
   int ldF;
   const double* Cd;        // N x M x ldC (Neumann trace rows, j-major)
   int ldC;
-  double* cwork;           // N x M scratch (coefficients / F^T a)
   const double* Ypi;       // N x M x 4 : K^+ B_Pi columns at the corners (assemble_coarse Ypi)
   double rel_tol;
   int max_iter;
-  const int* rank;      // 2N
+  const int* rank;         // 2N
   const ClassDims* dims;
   const int* sub_cls;
   const int* gamma_delta;  // N x gmax
@@ -140,52 +141,46 @@ struct CgArgs {
   const int* row_owner;    // npf x 4 : (i * crmax + rho)
   const double* flip_sign; // n_delta (+1 / -1 debug hook)
   const double* QtX;       // 2N x rmax x ext (QGt = cols 1.., qf = col 0)
-  const double* FC;        // N x fmax x rmax
-  const double* CCb;       // N x dmax x rmax
   const double* Zc;        // N x crmax x gmax
-  const double* Dpp;       // npf x n_pi
   const double* Sinv;      // n_pi x n_pi
+  const double* Wmu;       // n_pi x (n_pi + npf) : [S^{-1} | S^{-1} Dpp^T]
+  const double* Wd;        // npf x (n_pi + npf)  : [-Dpp S^{-1} | I - Dpp S^{-1} Dpp^T]
+  const double* W3;        // npf x n_pi           : Dpp S^{-1}
   const double* dpi;       // npf
   const double* C;         // 2N x M x rmax
-  // work
-  // P row-parts per subdomain (coefficient-space mode): every local phase is split over the M
-  // coefficient rows into P independent work items whose partial outputs are summed (fixed
-  // order) by the consumer, so all SMs stream the subdomain blocks.
+  // P row-parts per subdomain: every streamed phase is split over the M coefficient rows into P
+  // independent work items whose partial outputs are summed (fixed order) by the consumer.
   int P;
+  int rpc_max;    // largest rows-per-chunk of the streaming pipeline
   double* s;      // N x rmax
-  double* tpart;  // N x 4 (corner contributions of op1)
-  double* tpart3; // P x N x 4 (corner contributions of op3)
+  double* tpart;  // N x 4 (corner contributions of OP1)
+  double* tpart3; // P x N x 4 (corner contributions of OP3)
   double* psipart;// N x crmax
-  double* mu;     // n_pi
-  double* d1;     // npf
-  double* d2;     // npf
   double* o;      // N x gmax
   double* xf;     // P x N x fmax
   double* tr;     // P x N x dmax
   double* zz;     // P x N x dmax
   double* u;      // P x N x rmax
-  double* nu;     // n_pi
-  double* bot;    // npf
+  double* pap;    // N : p . o_i
   // CG vectors
   double* x;
   double* r;
-  double* p;
-  double* Ap;
+  double* pbuf[2];  // double-buffered search direction
   double* rhs;
-  double* partial;  // reduction scratch
+  double* partial;  // reduction scratch (>= grid)
   double* hist;     // max_iter
-  int* state;       // [0] it, [1] done, [2] converged, [3] negcurv
-  double* scal;     // [0] rr, [1] bnorm, [2] alpha, [3] pAp
+  int* state;       // [1] done, [2] converged, [3] negcurv, [5] iterations
+  double* scal;     // [0] rr, [1] bnorm
   double* coeffs;   // N x M output
   double* mu_pi_out;  // n_pi
 };
-/// out = cs_reduced_apply(v) (mode 0) or the reduced right-hand side (mode 1, v unused)
-void cg_launch_operator(const CgArgs& a, const double* v, double* out, int mode, cudaStream_t st);
+/// One launch of the persistent cooperative kernel: kJobCg runs the whole CG loop
+/// (solvers.cpp:95-117); kJobApply writes vout = cs_reduced_apply(vin) (solvers.cpp:372-386);
+/// kJobRhs writes vout = the reduced right-hand side (solvers.cpp:542-551); kJobRecon writes the
+/// coefficients and mu_Pi for mu_Delta = vin (solvers.cpp:565-577).
+void cg_launch(const CgArgs& a, int job, const double* vin, double* vout, cudaStream_t st);
 void cg_launch_init(const CgArgs& a, cudaStream_t st);
-/// The whole CG loop (solvers.cpp:95-117) as one persistent cooperative kernel.
-void cg_launch_persistent(const CgArgs& a, cudaStream_t st);
-int cg_persistent_grid(const CgArgs& a);
-void cg_launch_reconstruct(const CgArgs& a, cudaStream_t st);
-int cg_kernels_per_step(const CgArgs& a);
+int cg_grid(const CgArgs& a);
+int cg_rows_per_chunk_max(const CgArgs& a);
 
 }  // namespace ddg

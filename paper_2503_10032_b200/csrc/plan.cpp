@@ -220,8 +220,9 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
     p.tmax = std::max(p.tmax, static_cast<int>(c.tasks.size()));
   }
   p.gmax = std::max(p.gmax, 1);
-  p.fmax = std::max(p.fmax, 1);
-  p.dmax = std::max(p.dmax, 1);
+  // flux / Cdelta row strides are even: 16-byte rows for the CG kernel's bulk copies
+  p.fmax = (std::max(p.fmax, 1) + 1) / 2 * 2;
+  p.dmax = (std::max(p.dmax, 1) + 1) / 2 * 2;
 
   // ---- global numbering per subdomain (geometry.cpp:148-179, assembly.cpp:89-133)
   auto edge_id = [s](int ix, int iy, int side) {

@@ -2,9 +2,11 @@
 //
 // Mirrors Workspace (solvers.hpp:78-160) and the drivers (solvers.cpp:535-605):
 //   build()          features -> batched QR (K_i and Kbar_i together) -> branch test -> COD
-//   build_coarse()   FC, Zc, Dpp, dpi, S_Pi and its inverse          (assemble_coarse)
-//   build_neumann()  CCb = Cdelta Cbar                                (build_neumann)
-//   solve()          reduced RHS, CG (one CUDA graph with a device-side while loop), reconstruct
+//   build_coarse()   FC, Zc, Dpp, dpi, S_Pi, its inverse and the coarse rows Wmu / Wd / W3
+//                    (assemble_coarse)
+//   build_neumann()  Kbar_i is factorised with K_i in build(); Cdelta is built by the feature
+//                    kernel (build_neumann, solvers.cpp:390-448)
+//   solve()          reduced RHS, CG (one persistent cooperative kernel), reconstruct
 #include <algorithm>
 #include <chrono>
 #include <cstring>
@@ -190,12 +192,13 @@ void Workspace::upload_plan() {
   d_partial.alloc(2 * static_cast<size_t>(ceil_div(static_cast<int>(nd), 256)) + 2);
   d_state.alloc(8);
   d_scal.alloc(8);
-  d_mu.alloc(npi);
-  d_nu.alloc(npi);
   d_mu_pi_out.alloc(npi);
-  d_d1.alloc(npf);
-  d_d2.alloc(npf);
-  d_bot.alloc(npf);
+  d_Wmu.alloc(npi * (npi + npf));
+  d_Wd.alloc(npf * (npi + npf));
+  d_W3.alloc(npf * npi);
+  d_pap.alloc(static_cast<size_t>(N));
+  d_vin.alloc(nd);
+  d_vout.alloc(nd);
   d_tpart.alloc(static_cast<size_t>(N) * 4);
   d_psipart.alloc(static_cast<size_t>(N) * p.crmax);
   d_o.alloc(static_cast<size_t>(N) * p.gmax);
@@ -354,7 +357,6 @@ CodArgs Workspace::cod_args() {
 void Workspace::build() {
   DDG_CUDA(cudaSetDevice(device_));
   const Plan& p = plan;
-  launches_ = 0;
   const auto h0 = std::chrono::steady_clock::now();
   if (!layers_valid_) init_layers();
   DDG_CUDA(cudaEventRecord(ev_[0], st_));
@@ -397,14 +399,13 @@ void Workspace::build() {
                           std::to_string(kmax_) + ")");
   int rmax = 1;
   for (int r : rank) rmax = std::max(rmax, r);
-  rmax_ = rmax;
+  rmax_ = (rmax + 1) / 2 * 2;  // even row stride: 16-byte rows for the CG bulk copies
   h_rank = rank;
   const size_t nmat = 2 * static_cast<size_t>(p.N);
   d_C.alloc(nmat * p.M * rmax_);
   d_Y.alloc(nmat * p.M * rmax_);
   d_QtX.alloc(nmat * rmax_ * ext_);
   d_FC.alloc(static_cast<size_t>(p.N) * p.fmax * rmax_);
-  d_CCb.alloc(static_cast<size_t>(p.N) * p.dmax * rmax_);
   d_s.alloc(static_cast<size_t>(p.N) * rmax_);
   c = cod_args();
   kt = ktimer_begin();
@@ -441,7 +442,9 @@ BlockArgs Workspace::block_args() {
   b.C = d_C.ptr;
   b.QtX = d_QtX.ptr;
   b.FC = d_FC.ptr;
-  b.CCb = d_CCb.ptr;
+  b.Wmu = d_Wmu.ptr;
+  b.Wd = d_Wd.ptr;
+  b.W3 = d_W3.ptr;
   b.gamma_pi = d_gamma_pi.ptr;
   b.cr_row = d_cr_row.ptr;
   b.cr_off = d_cr_off.ptr;
@@ -470,13 +473,14 @@ void Workspace::build_coarse() {
   DDG_CUDA(cudaEventRecord(ev_[4], st_));
   BlockArgs b = block_args();
   DDG_CUDA(cudaMemsetAsync(d_spd_fail.ptr, 0, sizeof(int), st_));
-  launch_blocks(b, false, st_);
+  launch_blocks(b, st_);
   launch_coarse_local(b, d_cr_row.ptr, d_cr_off.ptr, d_cr_l.ptr, d_cr_w.ptr, st_);
   launches_ += 2;
   if (plan.n_pi > 0) {
     launch_coarse_rows(b, d_row_owner.ptr, st_);
     launch_coarse_schur(b, st_);
-    launches_ += 2;
+    launch_coarse_weights(b, st_);
+    launches_ += 4;
   }
   DDG_CUDA(cudaEventRecord(ev_[5], st_));
   int fail = 0;
@@ -491,8 +495,8 @@ void Workspace::build_neumann() {
   if (neumann_built_) return;
   DDG_CUDA(cudaSetDevice(device_));
   DDG_CUDA(cudaEventRecord(ev_[6], st_));
-  launch_blocks(block_args(), true, st_);
-  launches_ += 1;
+  // Kbar_i = [interior; boundary; corner traces; Delta flux rows] and Cdelta come out of the
+  // feature kernel and are factorised together with K_i: nothing left to do on the device.
   DDG_CUDA(cudaEventRecord(ev_[7], st_));
   neumann_built_ = true;
 }
@@ -513,31 +517,25 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.M = p.M;
   a.theta = theta;
   a.use_neumann = theta > 0.0 ? 1 : 0;
-  {
-    const char* op = std::getenv("DDELM_OPERATOR");
-    // default: the reference's coefficient-space grouping (iteration-count parity)
-    a.coeff_space = (op && std::strcmp(op, "fused") == 0) ? 0 : 1;
-  }
   a.F = d_F.ptr;
   a.ldF = p.fmax;
   a.Cd = d_Cd.ptr;
   a.ldC = p.dmax;
-  d_cwork.alloc(static_cast<size_t>(p.N) * p.M);
-  a.cwork = d_cwork.ptr;
   a.Ypi = d_Ypi.ptr;
   {
-    // row parts per subdomain so that N * P work items cover the SMs (coefficient-space mode)
+    // row parts per subdomain so that N * P work items cover the SMs (DDELM_CG_PARTS overrides)
     int dev = 0, sms = 148;
     DDG_CUDA(cudaGetDevice(&dev));
     DDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    a.P = a.coeff_space ? std::max(1, std::min(8, sms / p.N)) : 1;
-    const size_t P = a.P, N = p.N;
-    d_xf.alloc(P * N * p.fmax);
-    d_tr.alloc(P * N * p.dmax);
-    d_zz.alloc(P * N * p.dmax);
-    d_u.alloc(P * N * rmax_);
-    d_tpart3.alloc(P * N * 4);
-    a.tpart3 = d_tpart3.ptr;
+    int P = std::max(1, std::min(8, sms / p.N));
+    if (const char* e = std::getenv("DDELM_CG_PARTS")) P = std::max(1, std::min(p.M, std::atoi(e)));
+    a.P = P;
+    const size_t PP = P, N = p.N;
+    d_xf.alloc(PP * N * p.fmax);
+    d_tr.alloc(PP * N * p.dmax);
+    d_zz.alloc(PP * N * p.dmax);
+    d_u.alloc(PP * N * rmax_);
+    d_tpart3.alloc(PP * N * 4);
   }
   a.rel_tol = tol;
   a.max_iter = max_iter;
@@ -557,30 +555,27 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.row_owner = d_row_owner.ptr;
   a.flip_sign = d_flip.ptr;
   a.QtX = d_QtX.ptr;
-  a.FC = d_FC.ptr;
-  a.CCb = d_CCb.ptr;
   a.Zc = d_Zc.ptr;
-  a.Dpp = d_Dpp.ptr;
   a.Sinv = d_Sinv.ptr;
+  a.Wmu = d_Wmu.ptr;
+  a.Wd = d_Wd.ptr;
+  a.W3 = d_W3.ptr;
   a.dpi = d_dpi.ptr;
   a.C = d_C.ptr;
   a.s = d_s.ptr;
   a.tpart = d_tpart.ptr;
+  a.tpart3 = d_tpart3.ptr;
   a.psipart = d_psipart.ptr;
-  a.mu = d_mu.ptr;
-  a.d1 = d_d1.ptr;
-  a.d2 = d_d2.ptr;
   a.o = d_o.ptr;
   a.xf = d_xf.ptr;
   a.tr = d_tr.ptr;
   a.zz = d_zz.ptr;
   a.u = d_u.ptr;
-  a.nu = d_nu.ptr;
-  a.bot = d_bot.ptr;
+  a.pap = d_pap.ptr;
   a.x = d_x.ptr;
   a.r = d_r.ptr;
-  a.p = d_p.ptr;
-  a.Ap = d_Ap.ptr;
+  a.pbuf[0] = d_p.ptr;
+  a.pbuf[1] = d_Ap.ptr;
   a.rhs = d_rhs.ptr;
   a.partial = d_partial.ptr;
   a.hist = d_hist.ptr;
@@ -588,20 +583,8 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.scal = d_scal.ptr;
   a.coeffs = d_coeffs.ptr;
   a.mu_pi_out = d_mu_pi_out.ptr;
+  a.rpc_max = cg_rows_per_chunk_max(a);
   return a;
-}
-
-void Workspace::run_cg(const CgArgs& a) {
-  // the whole iteration loop is one persistent cooperative kernel (k_cg.cu)
-  const size_t need = 2 * static_cast<size_t>(cg_persistent_grid(a)) + 2;
-  if (d_partial.count < need) {
-    d_partial.alloc(need);
-    CgArgs b = a;
-    b.partial = d_partial.ptr;
-    cg_launch_persistent(b, st_);
-    return;
-  }
-  cg_launch_persistent(a, st_);
 }
 
 SolveResult Workspace::solve(int method, double theta, double tol, int max_iter) {
@@ -624,24 +607,24 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   if (p.n_delta == 0) throw std::invalid_argument("s = 1 (local-only solve) is not on the device path");
   d_hist.alloc(static_cast<size_t>(max_iter));
   {
-    // the persistent CG kernel needs 2 x grid partial slots
+    // CG partial slots: one per CTA of the persistent kernel, one per block of cg_init
     CgArgs probe = cg_args(theta, tol, max_iter);
-    const size_t need = std::max<size_t>(2 * static_cast<size_t>(cg_persistent_grid(probe)) + 2,
-                                         2 * static_cast<size_t>(ceil_div(p.n_delta, 256)) + 2);
+    const size_t need = std::max<size_t>(static_cast<size_t>(cg_grid(probe)) + 2,
+                                         static_cast<size_t>(ceil_div(p.n_delta, 256)) + 2);
     if (d_partial.count < need) d_partial.alloc(need);
   }
   CgArgs a = cg_args(theta, tol, max_iter);
   DDG_CUDA(cudaEventRecord(ev_[8], st_));
-  cg_launch_operator(a, nullptr, d_rhs.ptr, 1, st_);
+  cg_launch(a, kJobRhs, nullptr, d_rhs.ptr, st_);
   cg_launch_init(a, st_);
-  launches_ += cg_kernels_per_step(a) + 2;
+  launches_ += 3;
   DDG_CUDA(cudaEventRecord(ev_[9], st_));
   const int kt_cg = ktimer_begin();
-  run_cg(a);
+  cg_launch(a, kJobCg, nullptr, nullptr, st_);
   ktimer_end(kt_cg, "cg_iterations", 0.0, 0.0);
   DDG_CUDA(cudaEventRecord(ev_[10], st_));
-  cg_launch_reconstruct(a, st_);
-  launches_ += 3;
+  cg_launch(a, kJobRecon, d_x.ptr, nullptr, st_);
+  launches_ += 1;
   DDG_CUDA(cudaEventRecord(ev_[11], st_));
   int state[8];
   DDG_CUDA(cudaMemcpyAsync(state, d_state.ptr, sizeof(state), cudaMemcpyDeviceToHost, st_));
@@ -675,16 +658,15 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
       const ClassPlan& cp = p.classes[p.subs[i].cls];
       const double r = h_rank[i], rb = h_rank[N + i];
       const double M = p.M, ng = cp.n_gamma, nF = cp.nF, nd = cp.nd;
-      double b = 3.0 * r * ng + p.crmax * ng * 2.0;  // Q_G (op1, op4 + corners), Zc (op1, op4)
-      if (a.coeff_space) b += 2.0 * M * r + 2.0 * M * nF + 4.0 * M;  // C, F, Ypi
-      else b += 2.0 * nF * r;                                          // FC
+      double b = 2.0 * r * ng + p.crmax * ng * 2.0;  // Q_G (OP1, OP4), Zc (OP1, OP4)
+      b += 2.0 * M * r + 2.0 * M * nF + 4.0 * M;      // C, F (OP2, OP3), Ypi (OP2)
       if (method == 2) {
-        b += 2.0 * rb * nd;                                            // Qbar_flux
-        b += a.coeff_space ? 2.0 * M * rb + 2.0 * M * nd : 2.0 * nd * rb;  // Cbar, Cdelta | CCb
+        b += 2.0 * rb * nd;                            // Qbar on the flux rows (NN1, NN2)
+        b += 2.0 * M * rb + 2.0 * M * nd;              // Cbar, Cdelta (NN1, NN2)
       }
       per_it += 8.0 * b;
     }
-    per_it += 8.0 * (2.0 * p.n_pi * p.n_pi + 4.0 * p.npf * p.n_pi);  // S^{-1}, Dpp (coarse solves)
+    // coarse rows (Wmu / Wd / W3 / S^{-1}) are L2-resident and not counted
     pending_[kt_cg].bytes = per_it * std::max(res.iterations, 1);
   }
   ktimer_collect();
@@ -701,10 +683,9 @@ void Workspace::apply_operator(double theta, const double* v, double* out) {
   if (theta > 0.0) build_neumann();
   CgArgs a = cg_args(theta, 1e-9, 1);
   const size_t nd = plan.n_delta;
-  DDG_CUDA(cudaMemsetAsync(d_state.ptr, 0, 8 * sizeof(int), st_));
-  DDG_CUDA(cudaMemcpyAsync(d_p.ptr, v, nd * sizeof(double), cudaMemcpyHostToDevice, st_));
-  cg_launch_operator(a, d_p.ptr, d_Ap.ptr, 0, st_);
-  DDG_CUDA(cudaMemcpyAsync(out, d_Ap.ptr, nd * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaMemcpyAsync(d_vin.ptr, v, nd * sizeof(double), cudaMemcpyHostToDevice, st_));
+  cg_launch(a, kJobApply, d_vin.ptr, d_vout.ptr, st_);
+  DDG_CUDA(cudaMemcpyAsync(out, d_vout.ptr, nd * sizeof(double), cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
 }
 

@@ -83,7 +83,6 @@ class Workspace {
   CodArgs cod_args();
   BlockArgs block_args();
   CgArgs cg_args(double theta, double tol, int max_iter);
-  void run_cg(const CgArgs& a);
   // kernel timers: begin/end around a launch; collected after the stream syncs
   int ktimer_begin();
   void ktimer_end(int slot, const char* family, double flops, double bytes);
@@ -126,10 +125,10 @@ class Workspace {
   DevBuf<int> d_deficient, d_rank, d_status, d_perm, d_corner_q, d_spd_fail, d_state;
   DevBuf<double> d_V1, d_F1, d_Rr, d_tau1, d_zc, d_upd, d_dir, d_C, d_Y, d_QtX;
   // interface blocks / coarse
-  DevBuf<double> d_FC, d_CCb, d_Zc, d_pd, d_Gc, d_Ypi, d_Dpp, d_dpi, d_S, d_Sinv;
+  DevBuf<double> d_FC, d_Zc, d_pd, d_Gc, d_Ypi, d_Dpp, d_dpi, d_S, d_Sinv, d_Wmu, d_Wd, d_W3;
   // CG
-  DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu, d_nu, d_mu_pi_out, d_d1,
-      d_d2, d_bot, d_tpart, d_tpart3, d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_cwork;
+  DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu_pi_out, d_tpart, d_tpart3,
+      d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_pap, d_vin, d_vout;
 };
 
 }  // namespace ddg
