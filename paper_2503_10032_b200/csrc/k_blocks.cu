@@ -7,6 +7,7 @@
 // Reference: assemble_coarse (solvers.cpp:278-326), build_neumann Cdelta (solvers.cpp:436-438).
 // The coarse Schur matrix S_Pi is assembled and inverted (Cholesky) on one CTA; the rows the
 // interface iteration needs are precomputed as Wmu / Wd / W3 (coarse_weights*).
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -325,6 +326,39 @@ void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t s
 
 void launch_coarse_schur(const BlockArgs& a, cudaStream_t st) {
   coarse_schur_kernel<<<1, 1024, 0, st>>>(a);
+  DDG_LAUNCH_CHECK();
+}
+
+namespace {
+__global__ void pack_streams_kernel(BlockArgs a, double* KF, int ldKF, double* KD, int ldKD) {
+  const int i = blockIdx.y;
+  const int R = a.rmax;
+  for (int j = blockIdx.x; j < a.M; j += gridDim.x) {
+    const size_t row = static_cast<size_t>(i) * a.M + j;
+    double* kf = KF + row * ldKF;
+    double* kd = KD + row * ldKD;
+    const double* c = a.C + row * R;
+    const double* cb = a.C + (static_cast<size_t>(a.N + i) * a.M + j) * R;
+    for (int k = threadIdx.x; k < ldKF; k += blockDim.x) {
+      double v = 0.0;
+      if (k < R) v = c[k];
+      else if (k < R + 4) v = a.Ypi[row * 4 + (k - R)];
+      else if (k - R - 4 < a.ldF) v = a.F[row * a.ldF + (k - R - 4)];
+      kf[k] = v;
+    }
+    for (int k = threadIdx.x; k < ldKD; k += blockDim.x) {
+      double v = 0.0;
+      if (k < R) v = cb[k];
+      else if (k - R < a.ldC) v = a.Cd[row * a.ldC + (k - R)];
+      kd[k] = v;
+    }
+  }
+}
+}  // namespace
+
+void launch_pack_streams(const BlockArgs& a, double* KF, int ldKF, double* KD, int ldKD, cudaStream_t st) {
+  dim3 g(std::min(a.M, 64), a.N);
+  pack_streams_kernel<<<g, 256, 0, st>>>(a, KF, ldKF, KD, ldKD);
   DDG_LAUNCH_CHECK();
 }
 

@@ -3,10 +3,10 @@
 // cs_reduced_apply (solvers.cpp:372-386) with the theta-mixed Neumann-Neumann weight
 // (solvers.cpp:599-603), in the reference's own grouping: K^+ is applied INTO coefficient space
 // (c = K^+ phi, an M-vector) and the flux / Cdelta rows act on c afterwards
-// (solvers.cpp:215-218, 240-241, 456, 469). With the factored pseudo-inverse K^+ = C Q_r^T
+// (solvers.cpp:215-218, 240-241, 455, 468). With the factored pseudo-inverse K^+ = C Q_r^T
 // (k_cod.cu) one operator application is, per subdomain i:
 //   OP1   s = Q_G^T phi (+ Q_r^T f), corner parts t_i, psi_i = Zc v            (per subdomain)
-//   OP2   mu|corners = Wmu [t; psi] ; c = C s - Ypi mu ; x_i = -F c            (streams C, F)
+//   OP2   mu|corners = Wmu [t; psi] ; c = C s - Ypi mu ; x_i = -F c            (streams C, F, Ypi)
 //   NN1   y = Cbar (Qbar^T (-x|flux)) ; tr_i = Cdelta y                        (streams Cbar, Cdelta)
 //   NN2   y = Cdelta^T tl ; zz_i = Qbar (Cbar^T y)                             (streams Cdelta, Cbar)
 //   OP3   w = theta P^T P x + (1-theta) x ; u_i = C^T (F^T w)                  (streams F, C)
@@ -17,13 +17,16 @@
 // (k_blocks.cu), so every work item evaluates the handful of coarse rows it needs from the
 // gathered [t; psi] vector itself: no single-CTA coarse phase, no extra grid barrier.
 //
-// HBM streaming: the four dense phases read contiguous row slices (rows j0..j1 of C, F, Cbar,
-// Cdelta — one work item = one subdomain part) through a 4-stage shared-memory ring filled by
-// the TMA engine (cp.async.bulk + mbarrier complete_tx). Each chunk is consumed by a row-dot
-// (t_j = A_j . x) followed by a column axpy (y += t_j B_j), both from shared memory. The first
-// chunks of the next phase are issued before the grid barrier (the matrices are constant during
-// the solve), and NN2 / OP3 walk their slices in reverse so they start on the lines NN1 / OP2
-// left in L2.
+// HBM streaming (warp-specialised): in the four dense phases one work item is a row slice
+// (rows j0..j1 of one subdomain's C, F, Cbar, Cdelta). Warp 15 is the producer: it walks the
+// CTA's chunks and fills a 4-stage shared-memory ring with bulk copies on the TMA engine
+// (cp.async.bulk, completion on a "full" mbarrier), refilling a stage once its "empty" mbarrier
+// says all consumer warps released it. Warps 0..14 consume: each takes whole rows — a row-dot
+// t_j = A_j . x against x held in registers, then the axpy y += t_j B_j into per-lane register
+// accumulators — so there is no block barrier per chunk; the 15 warp partials are summed in a
+// fixed order at the end of the item. The first chunks of the next phase are issued before the
+// grid barrier (the matrices are constant during the solve), and NN2 / OP3 walk their slices in
+// reverse so they start on the lines NN1 / OP2 left in L2.
 //
 // The whole CG loop (solvers.cpp:82-119) is ONE persistent cooperative kernel: 7 grid barriers per
 // iteration, the CG scalars are sums of per-CTA / per-subdomain partials in a fixed order (no
@@ -47,9 +50,12 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
+constexpr int kCWarps = kWarps - 1;  // consumer warps of a streamed phase
+constexpr int kCThreads = kCWarps * 32;
+constexpr int kProducerWarp = kWarps - 1;
 constexpr int kStages = 4;
 constexpr int kStageBytes = 32768;
-constexpr int kMaxColBlocks = 4;  // axpy width <= 4 * kThreads
+constexpr int kMaxW = 512;  // widest row-dot operand / axpy output (16 registers per lane)
 
 // ---------------------------------------------------------------- mbarrier + bulk copy (TMA)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -61,6 +67,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -80,55 +89,69 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+/// Thread team of a phase: the whole CTA (512) or the consumer warps of a streamed phase (480,
+/// named barrier 1 so the producer warp is never waited for).
+struct Team {
+  int n;
+  __device__ __forceinline__ void sync() const {
+    if (n == kThreads)
+      __syncthreads();
+    else
+      asm volatile("bar.sync 1, %0;" ::"r"(kCThreads) : "memory");
+  }
+};
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"r"(kCThreads) : "memory"); }
+
 // ---------------------------------------------------------------- shared state of one CTA
 struct Shared {
-  double* ring;    // kStages x kStageBytes
-  double* xa;      // row-dot operand (wamax)
-  double* tbuf;    // row-dot results of one chunk (rpc_max)
-  double* red;     // kThreads (axpy group partials)
+  double* ring;    // kStages x kStageBytes (also the Q_r^T staging area of OP1 / OP4)
+  double* xa;      // row-dot operand (wmax)
+  double* red;     // kCWarps x wred (warp partials of the axpy) / kThreads scratch
   double* z;       // [t; psi] (nz)
   double* t2;      // t' (n_pi)
-  double* v1;      // big per-subdomain vector (gmax / fmax / dmax)
+  double* v1;      // per-subdomain vector (wmax)
   double* s0;      // rmax
-  double* s1;      // rmax
-  uint64_t* full;  // kStages mbarriers
+  uint64_t* full;  // kStages
+  uint64_t* empty; // kStages
+  uint64_t* qbar;  // Q_r^T staging
 };
 
-__device__ __forceinline__ int wamax_of(const CgArgs& a) { return max(max(a.rmax, a.fmax), max(a.dmax, a.gmax)); }
+__device__ __forceinline__ int wmax_of(const CgArgs& a) { return max(max(a.rmax, a.fmax), max(a.dmax, a.gmax)); }
+__device__ __forceinline__ int wred_of(const CgArgs& a) {
+  return ((max(max(a.rmax, a.fmax), a.dmax) + 31) & ~31);
+}
 
 __device__ __forceinline__ Shared carve(const CgArgs& a, uint64_t* bars) {
   extern __shared__ __align__(128) double smem[];
   Shared s;
   s.ring = smem;
   double* q = smem + kStages * (kStageBytes / 8);
-  const int wa = wamax_of(a);
+  const int wm = wmax_of(a);
   s.xa = q;
-  q += wa;
-  s.tbuf = q;
-  q += a.rpc_max;
+  q += wm;
   s.red = q;
-  q += kThreads;
+  q += max(kCWarps * wred_of(a), kThreads);
   s.z = q;
   q += a.n_pi + a.npf;
   s.t2 = q;
   q += max(a.n_pi, 1);
   s.v1 = q;
-  q += wa;
+  q += wm;
   s.s0 = q;
-  q += a.rmax;
-  s.s1 = q;
   s.full = bars;
+  s.empty = bars + kStages;
+  s.qbar = bars + 2 * kStages;
   return s;
 }
 
 // ---------------------------------------------------------------- streamed phases
 enum StreamKind { kOp2 = 0, kNn1 = 1, kNn2 = 2, kOp3 = 3 };
 
-/// Geometry of one work item's streams: A rows and B rows j0..j1 of subdomain i.
+/// Geometry of one work item's stream: rows j0..j1 of a packed per-subdomain block (one bulk copy
+/// per chunk). Row j holds A_j at column aoff, B_j at boff and (OP2) the 4 Ypi entries at yoff.
 struct ItemGeo {
-  const double* A;  // row j0 of A
-  const double* B;  // row j0 of B (nullptr: row-dot only)
-  int lda, ldb, rows, wa, wb;
+  const double* base;  // row j0 of the packed block
+  int ld, aoff, boff, yoff, rows, wa, wb, rpc, nch;
   bool reverse;
 };
 
@@ -138,169 +161,166 @@ __device__ __forceinline__ void part_rows(const CgArgs& a, int p, int& j0, int& 
   j1 = min(a.M, j0 + chunk);
 }
 
+/// rows per chunk: a multiple of the consumer warp count when it fits a stage (one row per warp)
+__host__ __device__ __forceinline__ int rows_per_chunk(int ld) {
+  const int row = 8 * ld;
+  const int k = kStageBytes / (kCWarps * row);
+  return k > 0 ? min(k * kCWarps, 120) : max(1, kStageBytes / row);
+}
+
 __device__ __forceinline__ ItemGeo item_geo(const CgArgs& a, int kind, int i, int p, bool recon) {
   int j0, j1;
   part_rows(a, p, j0, j1);
   const ClassDims d = a.dims[a.sub_cls[i]];
-  const size_t R = a.rmax;
-  const double* Ck = a.C + (static_cast<size_t>(i) * a.M + j0) * R;
-  const double* Cb = a.C + (static_cast<size_t>(a.N + i) * a.M + j0) * R;
-  const double* Fi = a.F + (static_cast<size_t>(i) * a.M + j0) * a.ldF;
-  const double* Di = a.Cd + (static_cast<size_t>(i) * a.M + j0) * a.ldC;
+  const int R = a.rmax;
+  const double* KF = a.KF + (static_cast<size_t>(i) * a.M + j0) * a.ldKF;
+  const double* KD = a.KD + (static_cast<size_t>(i) * a.M + j0) * a.ldKD;
   ItemGeo g;
-  g.rows = j1 - j0;
   switch (kind) {
-    case kOp2:
-      g = {Ck, recon ? nullptr : Fi, a.rmax, a.ldF, j1 - j0, a.rank[i], d.nF, false};
+    case kOp2:  // A = C, Y = Ypi, B = F
+      g = {KF, a.ldKF, 0, recon ? -1 : R + 4, R, j1 - j0, a.rank[i], recon ? 0 : d.nF, 0, 0, false};
       break;
-    case kNn1:
-      g = {Cb, Di, a.rmax, a.ldC, j1 - j0, a.rank[a.N + i], d.nd, false};
+    case kNn1:  // A = Cbar, B = Cdelta
+      g = {KD, a.ldKD, 0, R, -1, j1 - j0, a.rank[a.N + i], d.nd, 0, 0, false};
       break;
-    case kNn2:
-      g = {Di, Cb, a.ldC, a.rmax, j1 - j0, d.nd, a.rank[a.N + i], true};
+    case kNn2:  // A = Cdelta, B = Cbar
+      g = {KD, a.ldKD, R, 0, -1, j1 - j0, d.nd, a.rank[a.N + i], 0, 0, true};
       break;
-    default:
-      g = {Fi, Ck, a.ldF, a.rmax, j1 - j0, d.nF, a.rank[i], true};
+    default:    // OP3: A = F, B = C
+      g = {KF, a.ldKF, R + 4, 0, -1, j1 - j0, d.nF, a.rank[i], 0, 0, true};
       break;
   }
+  g.rpc = rows_per_chunk(g.ld);
+  g.nch = (g.rows + g.rpc - 1) / g.rpc;
   return g;
 }
 
-__device__ __forceinline__ int rows_per_chunk(const ItemGeo& g) {
-  const int per_row = 8 * (g.lda + (g.B ? g.ldb : 0));
-  return max(1, min(kStageBytes / per_row, 128));
-}
-
-/// Producer cursor over the chunks of this CTA's work items in one streamed phase (thread 0).
-struct Producer {
-  int kind, item, nitems, chunk, nchunks, rpc, issued, consumed;
-  bool recon;
-};
-
-__device__ __forceinline__ int item_work(const CgArgs& a, int k, int nitems, bool reverse) {
-  // item k of this CTA in traversal order; reverse phases walk items (and chunks) backwards
-  const int kk = reverse ? nitems - 1 - k : k;
-  return blockIdx.x + kk * gridDim.x;
-}
-
-__device__ __forceinline__ int n_items(const CgArgs& a, int nwork) {
+__device__ __forceinline__ int n_items(int nwork) {
   const int b = blockIdx.x, G = gridDim.x;
   return b < nwork ? (nwork - 1 - b) / G + 1 : 0;
+}
+__device__ __forceinline__ bool reverse_kind(int kind) { return kind == kNn2 || kind == kOp3; }
+/// item k of this CTA in traversal order; reverse phases walk items (and chunks) backwards
+__device__ __forceinline__ int item_work(int k, int nitems, bool reverse) {
+  return blockIdx.x + (reverse ? nitems - 1 - k : k) * gridDim.x;
+}
+
+/// Producer (warp 15, lane 0): walks the chunks of this CTA's items of one streamed phase.
+/// `cnt` counts every chunk ever issued by this CTA: stage = cnt % kStages, use = cnt / kStages.
+struct Producer {
+  ItemGeo g;
+  int kind, item, nitems, chunk;
+  bool recon, active;
+  unsigned cnt;
+};
+
+__device__ void producer_load_item(const CgArgs& a, Producer& pr) {
+  if (pr.item < pr.nitems) {
+    const int w = item_work(pr.item, pr.nitems, reverse_kind(pr.kind));
+    pr.g = item_geo(a, pr.kind, w / a.P, w % a.P, pr.recon);
+  }
 }
 
 __device__ void producer_begin(const CgArgs& a, Producer& pr, int kind, bool recon) {
   pr.kind = kind;
   pr.recon = recon;
-  pr.nitems = n_items(a, a.N * a.P);
+  pr.nitems = n_items(a.N * a.P);
   pr.item = 0;
   pr.chunk = 0;
-  pr.nchunks = -1;
-  pr.issued = 0;
-  pr.consumed = 0;
+  pr.active = true;
+  producer_load_item(a, pr);
 }
 
-/// Issue the next chunk into stage (issued % kStages). Returns false when nothing is left.
-__device__ bool producer_issue(const CgArgs& a, Producer& pr, const Shared& sh) {
-  while (pr.item < pr.nitems) {
-    const bool rev = (pr.kind == kNn2 || pr.kind == kOp3);
-    const int w = item_work(a, pr.item, pr.nitems, rev);
-    const ItemGeo g = item_geo(a, pr.kind, w / a.P, w % a.P, pr.recon);
-    const int rpc = rows_per_chunk(g);
-    const int nch = (g.rows + rpc - 1) / rpc;
-    if (pr.chunk >= nch) {
+/// Issue up to `limit` chunks (limit < 0: all remaining) of the current phase.
+__device__ void producer_run(const CgArgs& a, Producer& pr, const Shared& sh, int limit) {
+  while (pr.active && limit != 0) {
+    while (pr.item < pr.nitems && pr.chunk >= pr.g.nch) {
       ++pr.item;
       pr.chunk = 0;
-      continue;
+      producer_load_item(a, pr);
     }
-    const int c = g.reverse ? nch - 1 - pr.chunk : pr.chunk;
-    const int ja = c * rpc, nr = min(rpc, g.rows - ja);
-    const int st = pr.issued % kStages;
+    if (pr.item >= pr.nitems) {
+      pr.active = false;
+      break;
+    }
+    const ItemGeo& g = pr.g;
+    const int c = g.reverse ? g.nch - 1 - pr.chunk : pr.chunk;
+    const int ja = c * g.rpc, nr = min(g.rpc, g.rows - ja);
+    const int st = pr.cnt % kStages;
+    const unsigned use = pr.cnt / kStages;
+    if (use > 0) mbar_wait(&sh.empty[st], (use - 1) & 1u);  // consumers released the stage
     double* dst = sh.ring + static_cast<size_t>(st) * (kStageBytes / 8);
-    const uint32_t ba = static_cast<uint32_t>(nr) * g.lda * 8;
-    const uint32_t bb = g.B ? static_cast<uint32_t>(nr) * g.ldb * 8 : 0;
-    mbar_expect_tx(&sh.full[st], ba + bb);
-    bulk_g2s(dst, g.A + static_cast<size_t>(ja) * g.lda, ba, &sh.full[st]);
-    if (g.B) bulk_g2s(dst + static_cast<size_t>(nr) * g.lda, g.B + static_cast<size_t>(ja) * g.ldb, bb, &sh.full[st]);
+    const uint32_t bytes = static_cast<uint32_t>(nr) * g.ld * 8;
+    mbar_expect_tx(&sh.full[st], bytes);
+    bulk_g2s(dst, g.base + static_cast<size_t>(ja) * g.ld, bytes, &sh.full[st]);
     ++pr.chunk;
-    ++pr.issued;
-    return true;
-  }
-  return false;
-}
-
-__device__ __forceinline__ void producer_fill(const CgArgs& a, Producer& pr, const Shared& sh) {
-  while (pr.issued - pr.consumed < kStages && producer_issue(a, pr, sh)) {
+    ++pr.cnt;
+    if (limit > 0) --limit;
   }
 }
 
-/// Consumer side of one work item: stream the rows of (A, B); per row j: t_j = A_j . xa, then
-/// hook(j, t_j) (returns the value used by the axpy), acc += t_j * B_j.  acc[] per thread column.
-/// `seq` / `phase` track the ring position and mbarrier parities (uniform over the CTA).
-template <class Hook>
-__device__ void stream_item(const CgArgs& a, const ItemGeo& g, const Shared& sh, Producer& pr, int& seq,
-                            uint32_t& phase, double* acc, Hook hook) {
+/// Consumer side of one work item (warps 0..14): per row j of each chunk, t_j = A_j . xa
+/// (xa in registers), u_j = hook(j, t_j, Ypi row) (lane-uniform), acc += u_j B_j (registers).
+/// `ccnt` counts the chunks consumed by this CTA (mirrors the producer's cnt).
+template <int W, class Hook>
+__device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt, double (&acc)[W], Hook hook) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rpc = rows_per_chunk(g);
-  const int nch = (g.rows + rpc - 1) / rpc;
-  const int ncb = g.B ? (g.wb + kThreads - 1) / kThreads : 0;
-  const int wbp = (ncb == 1) ? ((g.wb + 31) & ~31) : kThreads;
-  const int G = (ncb == 1) ? kThreads / wbp : 1;
-  const int col = threadIdx.x % wbp, grp = threadIdx.x / wbp;
-  for (int cc = 0; cc < nch; ++cc) {
-    const int c = g.reverse ? nch - 1 - cc : cc;
-    const int ja = c * rpc, nr = min(rpc, g.rows - ja);
-    const int st = seq % kStages;
-    const double* As = sh.ring + static_cast<size_t>(st) * (kStageBytes / 8);
-    const double* Bs = As + static_cast<size_t>(nr) * g.lda;
-    mbar_wait(&sh.full[st], (phase >> st) & 1u);
-    phase ^= 1u << st;
-    for (int rr = warp; rr < nr; rr += kWarps) {
-      const double* ar = As + static_cast<size_t>(rr) * g.lda;
+  double xr[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    const int k = lane + 32 * q;
+    xr[q] = k < g.wa ? sh.xa[k] : 0.0;
+    acc[q] = 0.0;
+  }
+  for (int cc = 0; cc < g.nch; ++cc) {
+    const int c = g.reverse ? g.nch - 1 - cc : cc;
+    const int ja = c * g.rpc, nr = min(g.rpc, g.rows - ja);
+    const int st = ccnt % kStages;
+    const double* S = sh.ring + static_cast<size_t>(st) * (kStageBytes / 8);
+    mbar_wait(&sh.full[st], (ccnt / kStages) & 1u);
+    for (int rr = warp; rr < nr; rr += kCWarps) {
+      const double* row = S + static_cast<size_t>(rr) * g.ld;
+      const double* ar = row + g.aoff;
       double s = 0;
-      for (int k = lane; k < g.wa; k += 32) s += ar[k] * sh.xa[k];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        const int k = lane + 32 * q;
+        if (k < g.wa) s += ar[k] * xr[q];
+      }
       s = warp_sum(s);
-      if (lane == 0) sh.tbuf[rr] = hook(ja + rr, s);
-    }
-    __syncthreads();
-    if (ncb > 0 && grp < G) {
-      for (int cb = 0; cb < ncb; ++cb) {
-        const int l = col + cb * kThreads;
-        if (l < g.wb) {
-          double s = acc[cb];
-          for (int rr = grp; rr < nr; rr += G) s += Bs[static_cast<size_t>(rr) * g.ldb + l] * sh.tbuf[rr];
-          acc[cb] = s;
+      const double t = hook(ja + rr, s, row + g.yoff, lane);
+      if (g.boff >= 0) {
+        const double* br = row + g.boff;
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          const int l = lane + 32 * q;
+          if (l < g.wb) acc[q] += br[l] * t;
         }
       }
     }
-    __syncthreads();  // stage st free, tbuf reusable
-    ++seq;
-    if (threadIdx.x == 0) {
-      ++pr.consumed;
-      producer_fill(a, pr, sh);
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.empty[st]);
+    ++ccnt;
   }
 }
 
-/// Reduce the axpy accumulators over the row groups (fixed order) and hand out column l values.
-template <class Out>
-__device__ void reduce_acc(const ItemGeo& g, const Shared& sh, double* acc, Out out) {
-  const int ncb = (g.wb + kThreads - 1) / kThreads;
-  const int wbp = (ncb == 1) ? ((g.wb + 31) & ~31) : kThreads;
-  const int G = (ncb == 1) ? kThreads / wbp : 1;
-  const int col = threadIdx.x % wbp, grp = threadIdx.x / wbp;
-  for (int cb = 0; cb < ncb; ++cb) {
-    sh.red[threadIdx.x] = (grp < G) ? acc[cb] : 0.0;
-    __syncthreads();
-    if (grp == 0) {
-      const int l = col + cb * kThreads;
-      if (l < g.wb) {
-        double s = 0;
-        for (int q = 0; q < G; ++q) s += sh.red[q * wbp + col];
-        out(l, s);
-      }
-    }
-    __syncthreads();
+/// Sum the consumer warps' accumulators (fixed warp order) and hand out column l values.
+template <int W, class Out>
+__device__ void reduce_warps(const CgArgs& a, const ItemGeo& g, const Shared& sh, const double (&acc)[W], Out out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wr = wred_of(a);
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    const int l = lane + 32 * q;
+    if (l < g.wb) sh.red[warp * wr + l] = acc[q];
   }
+  cons_sync();
+  for (int l = threadIdx.x; l < g.wb; l += kCThreads) {
+    double s = 0;
+    for (int w = 0; w < kCWarps; ++w) s += sh.red[w * wr + l];
+    out(l, s);
+  }
+  cons_sync();
 }
 
 // ---------------------------------------------------------------- small helpers
@@ -318,9 +338,9 @@ __device__ __forceinline__ double gather_x(const CgArgs& a, int g) {
 
 /// z = [t; psi]: corner contributions of OP1 summed over their owners (subdomain order) and the
 /// cross-flux data psi (mode 0: Dpd v; mode 1: dpi; mode 2: dpi - Dpd mu_Delta).
-__device__ void gather_z(const CgArgs& a, const Shared& sh, int mode) {
+__device__ void gather_z(const CgArgs& a, const Shared& sh, int mode, int nthr) {
   const int n = a.n_pi;
-  for (int gp = threadIdx.x; gp < n; gp += blockDim.x) {
+  for (int gp = threadIdx.x; gp < n; gp += nthr) {
     double acc = 0;
     for (int q = 0; q < 4; ++q) {
       const int o = a.pi_owner[gp * 4 + q];
@@ -328,7 +348,7 @@ __device__ void gather_z(const CgArgs& a, const Shared& sh, int mode) {
     }
     sh.z[gp] = acc;
   }
-  for (int rr = threadIdx.x; rr < a.npf; rr += blockDim.x) {
+  for (int rr = threadIdx.x; rr < a.npf; rr += nthr) {
     double acc = 0;
     if (mode != 1)
       for (int q = 0; q < 4; ++q) {
@@ -339,11 +359,11 @@ __device__ void gather_z(const CgArgs& a, const Shared& sh, int mode) {
   }
 }
 
-/// out[q] = W[row_q] . vec (len), one warp per row; rows < 0 give 0.
+/// out[q] = W[row_q] . vec (len), one warp per row (warps < nwarps); rows < 0 give 0.
 __device__ void rows_dot(const double* W, int ldw, const int* rows, int nrows, const double* vec, int len,
-                         double* out) {
+                         double* out, int nwarps) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int q = warp; q < nrows; q += kWarps) {
+  for (int q = warp; q < nrows; q += nwarps) {
     const int row = rows[q];
     double s = 0;
     if (row >= 0) {
@@ -355,19 +375,99 @@ __device__ void rows_dot(const double* W, int ldw, const int* rows, int nrows, c
   }
 }
 
-// ---------------------------------------------------------------- OP1 (per subdomain)
+/// Deterministic sum of n values: lanes stride the array, then the xor tree (bitwise identical in
+/// every lane, warp and CTA).
+__device__ __forceinline__ double det_sum(const double* p, int n) {
+  double s = 0;
+  for (int k = threadIdx.x & 31; k < n; k += 32) s += p[k];
+  return warp_sum(s);
+}
+
+/// y[k] = sum_e Q[k*ldq + e] x[e] for k < nk, e < ne: a warp per 4 rows (warps < nwarps).
+__device__ void rowdot4(const double* Q, int ldq, int nk, int ne, const double* x, double* y, int nwarps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k0 = 4 * warp; k0 < nk; k0 += 4 * nwarps) {
+    double c[4] = {0, 0, 0, 0};
+    for (int e = lane; e < ne; e += 32) {
+      const double xe = x[e];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u < nk) c[u] += Q[static_cast<size_t>(k0 + u) * ldq + e] * xe;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double v = warp_sum(c[u]);
+      if (lane == 0 && k0 + u < nk) y[k0 + u] = v;
+    }
+  }
+}
+
+/// y[c] = sum_k Q[k*ldq + c] x[k] for c < nc (<= team size), k < nk: threads over (c, k-group),
+/// the k-groups combined in a fixed order through red (>= team size doubles).
+template <class Out>
+__device__ void coldot_split(const double* Q, int ldq, int nk, int nc, const double* x, double* red, Team tm,
+                             Out out) {
+  const int ncp = max(32, (nc + 31) & ~31);
+  const int G = max(1, tm.n / ncp);
+  const int c = threadIdx.x % ncp, grp = threadIdx.x / ncp;
+  double s = 0;
+  if (grp < G && c < nc) {
+    const int k0 = (nk * grp) / G, k1 = (nk * (grp + 1)) / G;
+    double s1 = 0;
+    int k = k0;
+    for (; k + 1 < k1; k += 2) {
+      s += Q[static_cast<size_t>(k) * ldq + c] * x[k];
+      s1 += Q[static_cast<size_t>(k + 1) * ldq + c] * x[k + 1];
+    }
+    if (k < k1) s += Q[static_cast<size_t>(k) * ldq + c] * x[k];
+    s += s1;
+  }
+  if (threadIdx.x < tm.n) red[threadIdx.x] = s;
+  tm.sync();
+  if (grp == 0 && c < nc) {
+    double t = 0;
+    for (int q = 0; q < G; ++q) t += red[q * ncp + c];
+    out(c, t);
+  }
+  tm.sync();
+}
+
+/// Q_r^T [f E] rows (k < r) of local matrix t staged into the (idle) ring with one bulk copy;
+/// falls back to the global copy when it does not fit. `cached` remembers what the ring holds.
+struct QtxStage {
+  unsigned cnt;
+  int cached;
+};
+
+__device__ const double* stage_qtx(const CgArgs& a, const Shared& sh, QtxStage& q, int t, int r) {
+  const double* src = a.QtX + static_cast<size_t>(t) * a.rmax * a.ext;
+  const int rows = min(a.rmax, (r + 1) & ~1);
+  const size_t bytes = static_cast<size_t>(rows) * a.ext * 8;
+  if (rows == 0 || bytes > static_cast<size_t>(kStages) * kStageBytes) return src;
+  if (q.cached == t) return sh.ring;
+  __syncthreads();  // previous readers of the ring are done
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(sh.qbar, static_cast<uint32_t>(bytes));
+    bulk_g2s(sh.ring, src, static_cast<uint32_t>(bytes), sh.qbar);
+  }
+  mbar_wait(sh.qbar, q.cnt & 1u);
+  ++q.cnt;
+  q.cached = t;
+  return sh.ring;
+}
+
+// ---------------------------------------------------------------- OP1 (per subdomain, all warps)
 /// mode 0: operator on v (CG: v = r + beta p_cur, written to p_next by the first owner);
 /// mode 1: reduced right-hand side (phi = 0, + Q_r^T f); mode 2: reconstruction (phi = +v).
-__device__ void dev_op1(const CgArgs& a, const Shared& sh, int i, const double* v, int mode, bool cg,
-                        double beta, const double* pcur, double* pnext) {
+__device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, const double* v, int mode,
+                        bool cg, double beta, const double* pcur, double* pnext) {
   const ClassDims d = a.dims[a.sub_cls[i]];
   const int r = a.rank[i], R = a.rmax, E = a.ext;
-  const double* QtX = a.QtX + static_cast<size_t>(i) * R * E;
   double* vg = sh.v1;
   double* phi = sh.red;  // n_gamma <= kThreads (checked on the host)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int* gd = a.gamma_delta + static_cast<size_t>(i) * a.gmax;
-  for (int g = threadIdx.x; g < d.n_gamma; g += blockDim.x) {
+  for (int g = threadIdx.x; g < d.n_gamma; g += kThreads) {
     const int dg = gd[g];
     double vv = 0.0;
     if (dg >= 0 && mode != 1) {
@@ -381,18 +481,19 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, int i, const double* 
     vg[g] = vv;
     phi[g] = (mode == 0) ? -vv : vv;
   }
+  const double* QtX = stage_qtx(a, sh, qs, i, r);
   __syncthreads();
-  for (int k = warp; k < r; k += kWarps) {
-    const double* q = QtX + static_cast<size_t>(k) * E + 1;
-    double acc = 0;
-    if (mode != 1)
-      for (int g = lane; g < d.n_gamma; g += 32) acc += q[g] * phi[g];
-    acc = warp_sum(acc);
+  if (mode != 1) {
+    rowdot4(QtX + 1, E, r, d.n_gamma, phi, sh.s0, kWarps);
+  } else {
+    for (int k = threadIdx.x; k < r; k += kThreads) sh.s0[k] = 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < r; k += kThreads) {
+    double acc = sh.s0[k];
     if (mode >= 1) acc += QtX[static_cast<size_t>(k) * E];
-    if (lane == 0) {
-      sh.s0[k] = acc;
-      a.s[static_cast<size_t>(i) * R + k] = acc;
-    }
+    sh.s0[k] = acc;
+    a.s[static_cast<size_t>(i) * R + k] = acc;
   }
   __syncthreads();
   if (warp < 4) {
@@ -415,122 +516,109 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, int i, const double* 
   __syncthreads();
 }
 
-// ---------------------------------------------------------------- OP2 (streams C, F)
-__device__ void dev_op2(const CgArgs& a, const Shared& sh, Producer& pr, int& seq, uint32_t& phase, int mode) {
-  const int nitems = n_items(a, a.N * a.P);
+// ---------------------------------------------------------------- streamed phases (consumers)
+template <int W>
+__device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int mode) {
+  const int nitems = n_items(a.N * a.P);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ double muc[4];
   __shared__ int crow[4];
   for (int k = 0; k < nitems; ++k) {
-    const int w = item_work(a, k, nitems, false);
+    const int w = item_work(k, nitems, false);
     const int i = w / a.P, p = w % a.P;
-    gather_z(a, sh, mode);
+    gather_z(a, sh, mode, kCThreads);
     if (threadIdx.x < 4) {
       const int g = a.corner_q[i * 4 + threadIdx.x];
       crow[threadIdx.x] = g >= 0 ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
     }
     const int r = a.rank[i];
-    for (int kk = threadIdx.x; kk < r; kk += blockDim.x) sh.xa[kk] = a.s[static_cast<size_t>(i) * a.rmax + kk];
-    __syncthreads();
-    rows_dot(a.Wmu, a.n_pi + a.npf, crow, 4, sh.z, a.n_pi + a.npf, muc);  // mu = S^{-1}(t + Dpp^T psi)
+    for (int kk = threadIdx.x; kk < r; kk += kCThreads) sh.xa[kk] = a.s[static_cast<size_t>(i) * a.rmax + kk];
+    cons_sync();
+    const int nz = a.n_pi + a.npf;
+    rows_dot(a.Wmu, nz, crow, 4, sh.z, nz, muc, kCWarps);  // mu = S^{-1}(t + Dpp^T psi)
     if (mode == 2 && w == 0)  // mu_Pi of the solution (one CTA writes it)
-      for (int gp = threadIdx.x >> 5; gp < a.n_pi; gp += kWarps) {
+      for (int gp = warp; gp < a.n_pi; gp += kCWarps) {
         double s = 0;
-        const double* wr = a.Wmu + static_cast<size_t>(gp) * (a.n_pi + a.npf);
-        for (int kk = threadIdx.x & 31; kk < a.n_pi + a.npf; kk += 32) s += wr[kk] * sh.z[kk];
+        const double* wr = a.Wmu + static_cast<size_t>(gp) * nz;
+        for (int kk = lane; kk < nz; kk += 32) s += wr[kk] * sh.z[kk];
         s = warp_sum(s);
-        if ((threadIdx.x & 31) == 0) a.mu_pi_out[gp] = s;
+        if (lane == 0) a.mu_pi_out[gp] = s;
       }
-    __syncthreads();
+    cons_sync();
     const ItemGeo g = item_geo(a, kOp2, i, p, mode == 2);
     int j0, j1;
     part_rows(a, p, j0, j1);
-    const double* Yp = a.Ypi + static_cast<size_t>(i) * a.M * 4;
     double* coef = a.coeffs + static_cast<size_t>(i) * a.M;
-    double acc[kMaxColBlocks] = {0, 0, 0, 0};
+    const double m0 = muc[0], m1 = muc[1], m2 = muc[2], m3 = muc[3];
+    double acc[W];
     // reference grouping (solvers.cpp:336, 342): c = K^+ phi - Ypi mu, then F c
-    stream_item(a, g, sh, pr, seq, phase, acc, [&](int jr, double cs) {
-      const int j = j0 + jr;
-      double yp = 0;
-      for (int q = 0; q < 4; ++q) yp += Yp[static_cast<size_t>(j) * 4 + q] * muc[q];
-      const double cj = cs - yp;
-      if (mode == 2) coef[j] = cj;
+    consume_item<W>(g, sh, ccnt, acc, [&](int jr, double cs, const double* y, int ln) {
+      const double cj = cs - (((y[0] * m0 + y[1] * m1) + y[2] * m2) + y[3] * m3);
+      if (mode == 2 && ln == 0) coef[j0 + jr] = cj;
       return cj;
     });
     if (mode == 2) continue;
     double* xf = a.xf + (static_cast<size_t>(p) * a.N + i) * a.fmax;
-    reduce_acc(g, sh, acc, [&](int l, double s) { xf[l] = -s; });
+    reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { xf[l] = -s; });
   }
 }
 
-// ---------------------------------------------------------------- NN1 (streams Cbar, Cdelta)
-__device__ void dev_nn1(const CgArgs& a, const Shared& sh, Producer& pr, int& seq, uint32_t& phase) {
-  const int nitems = n_items(a, a.N * a.P);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <int W>
+__device__ void dev_nn1(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
+  const int nitems = n_items(a.N * a.P);
   for (int k = 0; k < nitems; ++k) {
-    const int w = item_work(a, k, nitems, false);
+    const int w = item_work(k, nitems, false);
     const int i = w / a.P, p = w % a.P;
     const ClassDims d = a.dims[a.sub_cls[i]];
     const int nd = d.nd, rb = a.rank[a.N + i], E = a.ext;
     const double* QtX = a.QtX + static_cast<size_t>(a.N + i) * a.rmax * E;
     const int* nmap = a.ndelta_map + static_cast<size_t>(i) * a.dmax;
-    for (int kk = threadIdx.x; kk < nd; kk += blockDim.x) sh.v1[kk] = -gather_x(a, nmap[kk]);
-    __syncthreads();
-    for (int kk = warp; kk < rb; kk += kWarps) {  // Qbar_r^T rhs (rhs nonzero on the flux rows only)
-      const double* q = QtX + static_cast<size_t>(kk) * E + 1;
-      double s = 0;
-      for (int e = lane; e < nd; e += 32) s += q[e] * sh.v1[e];
-      s = warp_sum(s);
-      if (lane == 0) sh.xa[kk] = s;
-    }
-    __syncthreads();
+    for (int kk = threadIdx.x; kk < nd; kk += kCThreads) sh.v1[kk] = -gather_x(a, nmap[kk]);
+    cons_sync();
+    rowdot4(QtX + 1, E, rb, nd, sh.v1, sh.xa, kCWarps);  // Qbar_r^T rhs (rhs nonzero on flux rows only)
+    cons_sync();
     const ItemGeo g = item_geo(a, kNn1, i, p, false);
-    double acc[kMaxColBlocks] = {0, 0, 0, 0};
+    double acc[W];
     // reference order (solvers.cpp:455): y = Kbar^+ rhs (M-vector), then Cdelta y
-    stream_item(a, g, sh, pr, seq, phase, acc, [](int, double cs) { return cs; });
+    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
     double* tr = a.tr + (static_cast<size_t>(p) * a.N + i) * a.dmax;
-    reduce_acc(g, sh, acc, [&](int l, double s) { tr[l] = s; });
+    reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { tr[l] = s; });
   }
 }
 
-// ---------------------------------------------------------------- NN2 (streams Cdelta, Cbar)
-__device__ void dev_nn2(const CgArgs& a, const Shared& sh, Producer& pr, int& seq, uint32_t& phase) {
-  const int nitems = n_items(a, a.N * a.P);
+template <int W>
+__device__ void dev_nn2(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
+  const int nitems = n_items(a.N * a.P);
   for (int k = 0; k < nitems; ++k) {
-    const int w = item_work(a, k, nitems, true);
+    const int w = item_work(k, nitems, true);
     const int i = w / a.P, p = w % a.P;
     const ClassDims d = a.dims[a.sub_cls[i]];
     const int nd = d.nd, rb = a.rank[a.N + i], E = a.ext;
     const double* QtX = a.QtX + static_cast<size_t>(a.N + i) * a.rmax * E;
     const int* nmap = a.ndelta_map + static_cast<size_t>(i) * a.dmax;
     const size_t st = static_cast<size_t>(a.N) * a.dmax;
-    for (int kk = threadIdx.x; kk < nd; kk += blockDim.x) {
+    for (int kk = threadIdx.x; kk < nd; kk += kCThreads) {
       const int gg = nmap[kk];
       sh.xa[kk] = sum_parts(a.tr, st, a.P, a.own_nd[2 * gg]) + sum_parts(a.tr, st, a.P, a.own_nd[2 * gg + 1]);
     }
-    __syncthreads();
+    cons_sync();
     const ItemGeo g = item_geo(a, kNn2, i, p, false);
-    double acc[kMaxColBlocks] = {0, 0, 0, 0};
+    double acc[W];
     // reference order (solvers.cpp:468): x = Cdelta^T tl (M-vector), then (Kbar^+)^T x
-    stream_item(a, g, sh, pr, seq, phase, acc, [](int, double cs) { return cs; });
-    reduce_acc(g, sh, acc, [&](int l, double s) { sh.s0[l] = s; });
-    __syncthreads();
+    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
+    reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { sh.s0[l] = s; });
     // zz = Qbar_r (Cbar^T x) on the flux rows (partial over the parts p; linear)
     double* zz = a.zz + (static_cast<size_t>(p) * a.N + i) * a.dmax;
-    for (int kk = threadIdx.x; kk < nd; kk += blockDim.x) {
-      double s = 0;
-      for (int q = 0; q < rb; ++q) s += QtX[static_cast<size_t>(q) * E + 1 + kk] * sh.s0[q];
-      zz[kk] = s;
-    }
-    __syncthreads();
+    coldot_split(QtX + 1, E, rb, nd, sh.s0, sh.red, Team{kCThreads}, [&](int kk, double v) { zz[kk] = v; });
   }
 }
 
-// ---------------------------------------------------------------- OP3 (streams F, C)
-__device__ void dev_op3(const CgArgs& a, const Shared& sh, Producer& pr, int& seq, uint32_t& phase) {
-  const int nitems = n_items(a, a.N * a.P);
+template <int W>
+__device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
+  const int nitems = n_items(a.N * a.P);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int k = 0; k < nitems; ++k) {
-    const int w = item_work(a, k, nitems, true);
+    const int w = item_work(k, nitems, true);
     const int i = w / a.P, p = w % a.P;
     const ClassDims d = a.dims[a.sub_cls[i]];
     const int r = a.rank[i], R = a.rmax, E = a.ext;
@@ -538,7 +626,7 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, Producer& pr, int& se
     const int* fd = a.fluxrow_delta + static_cast<size_t>(i) * a.fmax;
     const double theta = a.theta;
     const size_t st = static_cast<size_t>(a.N) * a.dmax;
-    for (int l = threadIdx.x; l < d.nF; l += blockDim.x) {
+    for (int l = threadIdx.x; l < d.nF; l += kCThreads) {
       const int gg = fd[l];
       double wv = 0.0;
       if (gg >= 0) {
@@ -554,17 +642,16 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, Producer& pr, int& se
       }
       sh.xa[l] = wv;  // apply_AT_delta: a(lrow) = w(grow) on the Delta flux rows
     }
-    __syncthreads();
+    cons_sync();
     const ItemGeo g = item_geo(a, kOp3, i, p, false);
-    double acc[kMaxColBlocks] = {0, 0, 0, 0};
+    double acc[W];
     // reference order: at = F^T a (M-vector, apply_AT), then (K^+)^T at = Q_r (C^T at)
-    stream_item(a, g, sh, pr, seq, phase, acc, [](int, double cs) { return cs; });
+    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
     double* up = a.u + (static_cast<size_t>(p) * a.N + i) * R;
-    reduce_acc(g, sh, acc, [&](int l, double s) {
+    reduce_warps<W>(a, g, sh, acc, [&](int l, double s) {
       up[l] = s;
       sh.s0[l] = s;
     });
-    __syncthreads();
     if (warp < 4) {
       const int gq = a.corner_q[i * 4 + warp];
       double acc2 = 0;
@@ -573,21 +660,20 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, Producer& pr, int& se
       acc2 = warp_sum(acc2);
       if (lane == 0) a.tpart3[(static_cast<size_t>(p) * a.N + i) * 4 + warp] = acc2;  // t(gp) += z(lr)
     }
-    __syncthreads();
+    cons_sync();
   }
 }
 
-// ---------------------------------------------------------------- OP4 (per subdomain)
+// ---------------------------------------------------------------- OP4 (per subdomain, all warps)
 /// o_i = -phi + Q_G (s~ + u + Q_Pi^T nu) + Zc^T d2 ; CG mode also returns p . o_i.
-__device__ double dev_op4(const CgArgs& a, const Shared& sh, int i, const double* v, int mode) {
+__device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int i, const double* v, int mode) {
   const ClassDims d = a.dims[a.sub_cls[i]];
   const int r = a.rank[i], R = a.rmax, E = a.ext, n = a.n_pi, nz = a.n_pi + a.npf;
-  const double* QtX = a.QtX + static_cast<size_t>(i) * R * E;
   __shared__ double cq_mu[4], cq_nu[4], d2s[64], w3t[64];
   __shared__ int crow[4], xrow[64];
-  gather_z(a, sh, mode);
+  gather_z(a, sh, mode, kThreads);
   const size_t st3 = static_cast<size_t>(a.N) * 4;
-  for (int gp = threadIdx.x; gp < n; gp += blockDim.x) {
+  for (int gp = threadIdx.x; gp < n; gp += kThreads) {
     double acc = 0;
     for (int q = 0; q < 4; ++q) {
       const int o = a.pi_owner[gp * 4 + q];
@@ -599,20 +685,20 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, int i, const double
     const int g = a.corner_q[i * 4 + threadIdx.x];
     crow[threadIdx.x] = g >= 0 ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
   }
-  for (int rho = threadIdx.x; rho < a.crmax; rho += blockDim.x)
-    xrow[rho] = a.cr_row[static_cast<size_t>(i) * a.crmax + rho];
+  for (int rho = threadIdx.x; rho < a.crmax; rho += kThreads) xrow[rho] = a.cr_row[static_cast<size_t>(i) * a.crmax + rho];
+  const double* QtX = stage_qtx(a, sh, qst, i, r);
   __syncthreads();
-  rows_dot(a.Wmu, nz, crow, 4, sh.z, nz, cq_mu);       // mu  = S^{-1}(t + Dpp^T psi)
-  rows_dot(a.Sinv, n, crow, 4, sh.t2, n, cq_nu);       // nu  = S^{-1} t'
-  rows_dot(a.Wd, nz, xrow, a.crmax, sh.z, nz, d2s);    // d1  = psi - Dpp mu
-  rows_dot(a.W3, n, xrow, a.crmax, sh.t2, n, w3t);     // Dpp nu
+  rows_dot(a.Wmu, nz, crow, 4, sh.z, nz, cq_mu, kWarps);       // mu  = S^{-1}(t + Dpp^T psi)
+  rows_dot(a.Sinv, n, crow, 4, sh.t2, n, cq_nu, kWarps);       // nu  = S^{-1} t'
+  rows_dot(a.Wd, nz, xrow, a.crmax, sh.z, nz, d2s, kWarps);    // d1  = psi - Dpp mu
+  rows_dot(a.W3, n, xrow, a.crmax, sh.t2, n, w3t, kWarps);     // Dpp nu
   __syncthreads();
-  for (int rho = threadIdx.x; rho < a.crmax; rho += blockDim.x) d2s[rho] = xrow[rho] >= 0 ? d2s[rho] - w3t[rho] : 0.0;
+  for (int rho = threadIdx.x; rho < a.crmax; rho += kThreads) d2s[rho] = xrow[rho] >= 0 ? d2s[rho] - w3t[rho] : 0.0;
   int gq[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) gq[q] = a.corner_q[i * 4 + q];
   const size_t ust = static_cast<size_t>(a.N) * R;
-  for (int k = threadIdx.x; k < r; k += blockDim.x) {
+  for (int k = threadIdx.x; k < r; k += kThreads) {
     double uu = sum_parts(a.u + static_cast<size_t>(i) * R, ust, a.P, k);
     double sk = a.s[static_cast<size_t>(i) * R + k];
     for (int q = 0; q < 4; ++q)
@@ -626,16 +712,17 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, int i, const double
   __syncthreads();
   const int* gd = a.gamma_delta + static_cast<size_t>(i) * a.gmax;
   const double* Zc = a.Zc + static_cast<size_t>(i) * a.crmax * a.gmax;
+  // o = -phi + Q_G s_tot + Zc^T d2 ; Q_G s_tot split over k-groups (coldot_split)
+  double* qsv = sh.v1;
+  coldot_split(QtX + 1, E, r, d.n_gamma, sh.s0, sh.red, Team{kThreads}, [&](int g, double s) { qsv[g] = s; });
   double dot = 0;
-  for (int g = threadIdx.x; g < d.n_gamma; g += blockDim.x) {
+  for (int g = threadIdx.x; g < d.n_gamma; g += kThreads) {
     const int dg = gd[g];
     if (dg < 0) continue;
-    double qs = 0;
-    for (int k = 0; k < r; ++k) qs += QtX[static_cast<size_t>(k) * E + 1 + g] * sh.s0[k];
     double zs = 0;
     for (int rho = 0; rho < a.crmax; ++rho) zs += Zc[static_cast<size_t>(rho) * a.gmax + g] * d2s[rho];
     const double mphi = (mode == 0) ? v[dg] : 0.0;  // -phi
-    const double o = mphi + qs + zs;
+    const double o = mphi + qsv[g] + zs;
     a.o[static_cast<size_t>(i) * a.gmax + g] = o;
     if (mode == 0) dot += v[dg] * o;
   }
@@ -648,112 +735,144 @@ __device__ __forceinline__ double gather_out(const CgArgs& a, int g) {
 }
 
 // ---------------------------------------------------------------- the persistent kernel
-__device__ void drain(Producer& pr, const Shared& sh, int& seq, uint32_t& phase) {
-  // wait for chunks issued ahead (next-phase prefetch) before leaving: no bulk copy may land in
-  // the shared memory of an exited CTA
-  __shared__ int s_pending;
-  if (threadIdx.x == 0) s_pending = pr.issued - pr.consumed;
-  __syncthreads();
-  for (int k = 0; k < s_pending; ++k) {
-    const int st = (seq + k) % kStages;
-    mbar_wait(&sh.full[st], (phase >> st) & 1u);
-    phase ^= 1u << st;
-  }
-  __syncthreads();
-}
-
+template <int W>
 __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, int job, const double* vin,
                                                                     double* vout) {
   cgs::grid_group grid = cgs::this_grid();
   const int G = gridDim.x, b = blockIdx.x;
-  __shared__ __align__(8) uint64_t bars[kStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp == kProducerWarp;
+  __shared__ __align__(8) uint64_t bars[2 * kStages + 1];
   __shared__ double bsum[32];
   const Shared sh = carve(a, bars);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sh.full[s], 1);
+      mbar_init(&sh.empty[s], kCWarps);
+    }
+    mbar_init(sh.qbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-  Producer pr;  // meaningful on thread 0 only
-  int seq = 0;
-  uint32_t phase = 0;
+  Producer pr;          // warp 15 lane 0
+  pr.cnt = 0;
+  pr.active = false;
+  unsigned ccnt = 0;    // chunks consumed (consumer warps, uniform)
+  QtxStage qst{0u, -1};
 
-  auto begin_stream = [&](int kind, bool recon) {
-    // issue the first chunks of the next streamed phase (ring is free here)
-    seq = 0;
-    if (threadIdx.x == 0) {
+  // Producer: issue the first chunks of `kind` (the ring is idle: the caller's last ring readers
+  // finished behind a block barrier) — they overlap the grid barrier that follows.
+  auto prefetch = [&](int kind, bool recon) {
+    qst.cached = -1;
+    if (producer && lane == 0) {
       producer_begin(a, pr, kind, recon);
-      producer_fill(a, pr, sh);
+      producer_run(a, pr, sh, kStages);
     }
+  };
+  // Streamed phase: warp 15 issues the remaining chunks, warps 0..14 consume.
+  auto finish_producer = [&]() {
+    if (lane == 0) producer_run(a, pr, sh, -1);
+    __syncwarp();
   };
 
   if (job == kJobRecon) {
-    begin_stream(kOp2, true);
-    for (int i = b; i < a.N; i += G) dev_op1(a, sh, i, vin, 2, false, 0.0, nullptr, nullptr);
+    for (int i = b; i < a.N; i += G) dev_op1(a, sh, qst, i, vin, 2, false, 0.0, nullptr, nullptr);
+    prefetch(kOp2, true);
     grid.sync();
-    dev_op2(a, sh, pr, seq, phase, 2);
-    drain(pr, sh, seq, phase);
+    if (producer) finish_producer(); else dev_op2<W>(a, sh, ccnt, 2);
+    __syncthreads();
     return;
   }
 
   if (job == kJobApply || job == kJobRhs) {
     const int mode = job == kJobApply ? 0 : 1;
-    begin_stream(kOp2, false);
-    for (int i = b; i < a.N; i += G) dev_op1(a, sh, i, vin, mode, false, 0.0, nullptr, nullptr);
+    for (int i = b; i < a.N; i += G) dev_op1(a, sh, qst, i, vin, mode, false, 0.0, nullptr, nullptr);
+    prefetch(kOp2, false);
     grid.sync();
-    dev_op2(a, sh, pr, seq, phase, mode);
+    if (producer) finish_producer(); else dev_op2<W>(a, sh, ccnt, mode);
+    __syncthreads();
     if (a.use_neumann) {
-      begin_stream(kNn1, false);
+      prefetch(kNn1, false);
       grid.sync();
-      dev_nn1(a, sh, pr, seq, phase);
-      begin_stream(kNn2, false);
+      if (producer) finish_producer(); else dev_nn1<W>(a, sh, ccnt);
+      __syncthreads();
+      prefetch(kNn2, false);
       grid.sync();
-      dev_nn2(a, sh, pr, seq, phase);
+      if (producer) finish_producer(); else dev_nn2<W>(a, sh, ccnt);
+      __syncthreads();
     }
-    begin_stream(kOp3, false);
+    prefetch(kOp3, false);
     grid.sync();
-    dev_op3(a, sh, pr, seq, phase);
+    if (producer) finish_producer(); else dev_op3<W>(a, sh, ccnt);
+    __syncthreads();
+    qst.cached = -1;
     grid.sync();
-    for (int i = b; i < a.N; i += G) dev_op4(a, sh, i, vin, mode);
+    for (int i = b; i < a.N; i += G) dev_op4(a, sh, qst, i, vin, mode);
     grid.sync();
     for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) vout[g] = gather_out(a, g);
     return;
   }
 
   // ---- CG (solvers.cpp:93-116): x0 = 0, r = p = b (cg_init), recursive residual
+  // optional per-phase device timers (a.trace: G x 16 ns counters; profiling runs only)
+  unsigned long long t_last = 0, t_acc[16] = {};
+  auto tr = [&](int k) {
+    if (a.trace != nullptr && threadIdx.x == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (k >= 0) t_acc[k] += now - t_last;
+      t_last = now;
+    }
+  };
+  tr(-1);
   double rr = a.scal[0];
   const double bnorm = a.scal[1];
   if (a.state[1]) return;  // rhs == 0
   double beta = 0.0;
-  begin_stream(kOp2, false);
   for (int it = 1;; ++it) {
     double* pcur = a.pbuf[(it - 1) & 1];
     double* pnext = a.pbuf[it & 1];
-    for (int i = b; i < a.N; i += G) dev_op1(a, sh, i, nullptr, 0, true, beta, pcur, pnext);
+    for (int i = b; i < a.N; i += G) dev_op1(a, sh, qst, i, nullptr, 0, true, beta, pcur, pnext);
+    prefetch(kOp2, false);
+    tr(0);
     grid.sync();
-    dev_op2(a, sh, pr, seq, phase, 0);
+    tr(1);
+    if (producer) finish_producer(); else dev_op2<W>(a, sh, ccnt, 0);
+    __syncthreads();
+    tr(2);
     if (a.use_neumann) {
-      begin_stream(kNn1, false);
+      prefetch(kNn1, false);
       grid.sync();
-      dev_nn1(a, sh, pr, seq, phase);
-      begin_stream(kNn2, false);
+      tr(3);
+      if (producer) finish_producer(); else dev_nn1<W>(a, sh, ccnt);
+      __syncthreads();
+      tr(4);
+      prefetch(kNn2, false);
       grid.sync();
-      dev_nn2(a, sh, pr, seq, phase);
+      tr(5);
+      if (producer) finish_producer(); else dev_nn2<W>(a, sh, ccnt);
+      __syncthreads();
+      tr(6);
     }
-    begin_stream(kOp3, false);
+    prefetch(kOp3, false);
     grid.sync();
-    dev_op3(a, sh, pr, seq, phase);
-    begin_stream(kOp2, false);  // next iteration's OP2 chunks, behind OP4 / XR / OP1
+    tr(7);
+    if (producer) finish_producer(); else dev_op3<W>(a, sh, ccnt);
+    __syncthreads();
+    tr(8);
+    qst.cached = -1;
     grid.sync();
+    tr(9);
     for (int i = b; i < a.N; i += G) {
-      const double dot = dev_op4(a, sh, i, pnext, 0);
+      const double dot = dev_op4(a, sh, qst, i, pnext, 0);
       if (threadIdx.x == 0) a.pap[i] = dot;
     }
+    tr(10);
     grid.sync();
+    tr(11);
     // pAp = sum over subdomains of p . o_i (fixed order), alpha, x / r update
-    double pAp = 0;
-    for (int i = 0; i < a.N; ++i) pAp += a.pap[i];
+    const double pAp = det_sum(a.pap, a.N);
     if (pAp <= 0.0) {  // solvers.cpp:97-103
       if (b == 0 && threadIdx.x == 0) {
         a.state[3] = pAp < 0.0 ? 1 : 0;
@@ -773,9 +892,10 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
     }
     dsum = block_sum(dsum, bsum);
     if (threadIdx.x == 0) a.partial[b] = dsum;
+    tr(12);
     grid.sync();
-    double rr_new = 0;
-    for (int k = 0; k < G; ++k) rr_new += a.partial[k];
+    tr(13);
+    const double rr_new = det_sum(a.partial, G);
     const double rel = sqrt(rr_new) / bnorm;
     if (b == 0 && threadIdx.x == 0) {
       a.hist[it - 1] = rel;
@@ -790,9 +910,11 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
     }
     beta = rr_new / rr;
     rr = rr_new;
-    // a.partial is rewritten only after two more grid barriers: no race with the reads above
+    tr(14);
+    // a.partial / a.pap are rewritten only after further grid barriers: no race with the reads
   }
-  drain(pr, sh, seq, phase);
+  if (a.trace != nullptr && threadIdx.x == 0)
+    for (int k = 0; k < 16; ++k) a.trace[b * 16 + k] = static_cast<double>(t_acc[k]);
 }
 
 __global__ void __launch_bounds__(256) cg_init_kernel(CgArgs a) {
@@ -823,11 +945,25 @@ __global__ void cg_init2_kernel(CgArgs a, int nblk) {
   }
 }
 
+int wmax_host(const CgArgs& a) { return std::max(std::max(a.rmax, a.fmax), std::max(a.dmax, a.gmax)); }
+
 size_t smem_bytes(const CgArgs& a) {
-  const int wa = std::max(std::max(a.rmax, a.fmax), std::max(a.dmax, a.gmax));
-  const size_t small = static_cast<size_t>(wa) + a.rpc_max + kThreads + a.n_pi + a.npf + std::max(a.n_pi, 1) + wa +
-                       2 * static_cast<size_t>(a.rmax);
+  const int wm = wmax_host(a);
+  const int wred = (std::max(std::max(a.rmax, a.fmax), a.dmax) + 31) & ~31;
+  const size_t small = static_cast<size_t>(wm) + std::max(kCWarps * wred, kThreads) + a.n_pi + a.npf +
+                       std::max(a.n_pi, 1) + wm + static_cast<size_t>(a.rmax);
   return static_cast<size_t>(kStages) * kStageBytes + sizeof(double) * small;
+}
+
+/// Register-blocking width of the streamed phases: widest row-dot operand / axpy output / 32.
+int width_regs(const CgArgs& a) {
+  const int w = std::max(std::max(a.rmax, a.fmax), a.dmax);
+  return w <= 256 ? 8 : 16;
+}
+
+const void* kernel_for(const CgArgs& a) {
+  return width_regs(a) == 8 ? reinterpret_cast<const void*>(cg_persistent_kernel<8>)
+                            : reinterpret_cast<const void*>(cg_persistent_kernel<16>);
 }
 
 }  // namespace
@@ -837,28 +973,25 @@ int cg_grid(const CgArgs& a) {
   DDG_CUDA(cudaGetDevice(&dev));
   DDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const size_t sm = smem_bytes(a);
-  DDG_CUDA(cudaFuncSetAttribute(cg_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(sm)));
-  DDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_persistent_kernel, kThreads, sm));
+  const void* k = kernel_for(a);
+  DDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  DDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, sm));
   if (per_sm < 1) throw CudaError("cg_persistent_kernel cannot be resident (occupancy 0)");
   return sms;  // one CTA per SM
 }
 
 void cg_check_capacity(const CgArgs& a) {
   // shapes the kernel's shared-memory carve-up and thread mapping assume
-  const int gmax = a.gmax, wb = std::max(std::max(a.rmax, a.fmax), a.dmax);
-  if (gmax > kThreads || a.crmax > 64 || wb > kMaxColBlocks * kThreads)
+  const int w = std::max(std::max(a.rmax, a.fmax), a.dmax);
+  if (a.gmax > kThreads || a.crmax > 64 || w > kMaxW)
     throw std::invalid_argument("interface block sizes exceed the CG kernel's capacity");
-  if ((a.rmax & 1) || (a.ldF & 1) || (a.ldC & 1))
-    throw std::logic_error("CG row strides must be even (16-byte bulk copies)");
-  if (8 * (a.rmax + std::max(a.ldF, a.ldC)) > kStageBytes)
+  if ((a.ldKF & 1) || (a.ldKD & 1)) throw std::logic_error("packed CG blocks need even row strides");
+  if (8 * std::max(a.ldKF, a.ldKD) > kStageBytes)
     throw std::invalid_argument("one coefficient row exceeds a CG pipeline stage");
+  if (smem_bytes(a) > 227 * 1024) throw std::invalid_argument("CG kernel shared memory exceeds 227 KB");
 }
 
-int cg_rows_per_chunk_max(const CgArgs& a) {
-  auto rpc = [](int lda, int ldb) { return std::max(1, std::min(kStageBytes / (8 * (lda + ldb)), 128)); };
-  return std::max({rpc(a.rmax, a.ldF), rpc(a.rmax, a.ldC), rpc(a.rmax, 0)});
-}
+int cg_rows_per_chunk_max(const CgArgs& a) { return std::max(rows_per_chunk(a.ldKF), rows_per_chunk(a.ldKD)); }
 
 void cg_launch(const CgArgs& a, int job, const double* vin, double* vout, cudaStream_t st) {
   cg_check_capacity(a);
@@ -866,8 +999,7 @@ void cg_launch(const CgArgs& a, int job, const double* vin, double* vout, cudaSt
   const size_t sm = smem_bytes(a);
   CgArgs arg = a;
   void* params[] = {&arg, &job, &vin, &vout};
-  DDG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_persistent_kernel), dim3(G), dim3(kThreads),
-                                       params, sm, st));
+  DDG_CUDA(cudaLaunchCooperativeKernel(kernel_for(a), dim3(G), dim3(kThreads), params, sm, st));
 }
 
 void cg_launch_init(const CgArgs& a, cudaStream_t st) {

@@ -110,6 +110,8 @@ void launch_coarse_local(const BlockArgs& a, const int* cr_row, const int* cr_of
 void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t st);
 void launch_coarse_schur(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_weights(const BlockArgs& a, cudaStream_t st);
+/// Pack the CG stream blocks KF = [C | Ypi | F] and KD = [Cbar | Cdelta] (row-interleaved).
+void launch_pack_streams(const BlockArgs& a, double* KF, int ldKF, double* KD, int ldKD, cudaStream_t st);
 
 // ---------------------------------------------------------------- CG (k_cg.cu)
 enum CgJob { kJobCg = 0, kJobApply = 1, kJobRhs = 2, kJobRecon = 3 };
@@ -118,11 +120,13 @@ struct CgArgs {
   int N, n_delta, n_pi, npf, gmax, fmax, dmax, crmax, rmax, ext, M;
   double theta;
   int use_neumann;         // theta > 0
-  const double* F;         // N x M x ldF (flux rows, j-major)
-  int ldF;
-  const double* Cd;        // N x M x ldC (Neumann trace rows, j-major)
-  int ldC;
-  const double* Ypi;       // N x M x 4 : K^+ B_Pi columns at the corners (assemble_coarse Ypi)
+  // packed per-subdomain stream blocks (one bulk copy per chunk of rows), row j:
+  //   KF : [ C_j (rmax) | Ypi_j (4) | F_j (fmax) ]        stride ldKF (even)
+  //   KD : [ Cbar_j (rmax) | Cdelta_j (dmax) ]             stride ldKD (even)
+  const double* KF;
+  int ldKF;
+  const double* KD;
+  int ldKD;
   double rel_tol;
   int max_iter;
   const int* rank;         // 2N
@@ -147,7 +151,6 @@ struct CgArgs {
   const double* Wd;        // npf x (n_pi + npf)  : [-Dpp S^{-1} | I - Dpp S^{-1} Dpp^T]
   const double* W3;        // npf x n_pi           : Dpp S^{-1}
   const double* dpi;       // npf
-  const double* C;         // 2N x M x rmax
   // P row-parts per subdomain: every streamed phase is split over the M coefficient rows into P
   // independent work items whose partial outputs are summed (fixed order) by the consumer.
   int P;
@@ -173,6 +176,7 @@ struct CgArgs {
   double* scal;     // [0] rr, [1] bnorm
   double* coeffs;   // N x M output
   double* mu_pi_out;  // n_pi
+  double* trace;      // optional G x 16 per-phase ns counters of the CG job (nullptr: off)
 };
 /// One launch of the persistent cooperative kernel: kJobCg runs the whole CG loop
 /// (solvers.cpp:95-117); kJobApply writes vout = cs_reduced_apply(vin) (solvers.cpp:372-386);

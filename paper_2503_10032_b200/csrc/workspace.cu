@@ -8,6 +8,7 @@
 //                    kernel (build_neumann, solvers.cpp:390-448)
 //   solve()          reduced RHS, CG (one persistent cooperative kernel), reconstruct
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -482,6 +483,13 @@ void Workspace::build_coarse() {
     launch_coarse_weights(b, st_);
     launches_ += 4;
   }
+  // row-interleaved stream blocks of the interface iteration (k_cg.cu)
+  ldKF_ = (rmax_ + 4 + plan.fmax + 1) / 2 * 2;
+  ldKD_ = (rmax_ + plan.dmax + 1) / 2 * 2;
+  d_KF.alloc(static_cast<size_t>(plan.N) * plan.M * ldKF_);
+  d_KD.alloc(static_cast<size_t>(plan.N) * plan.M * ldKD_);
+  launch_pack_streams(b, d_KF.ptr, ldKF_, d_KD.ptr, ldKD_, st_);
+  launches_ += 1;
   DDG_CUDA(cudaEventRecord(ev_[5], st_));
   int fail = 0;
   DDG_CUDA(cudaMemcpyAsync(&fail, d_spd_fail.ptr, sizeof(int), cudaMemcpyDeviceToHost, st_));
@@ -517,11 +525,10 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.M = p.M;
   a.theta = theta;
   a.use_neumann = theta > 0.0 ? 1 : 0;
-  a.F = d_F.ptr;
-  a.ldF = p.fmax;
-  a.Cd = d_Cd.ptr;
-  a.ldC = p.dmax;
-  a.Ypi = d_Ypi.ptr;
+  a.KF = d_KF.ptr;
+  a.ldKF = ldKF_;
+  a.KD = d_KD.ptr;
+  a.ldKD = ldKD_;
   {
     // row parts per subdomain so that N * P work items cover the SMs (DDELM_CG_PARTS overrides)
     int dev = 0, sms = 148;
@@ -561,7 +568,6 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.Wd = d_Wd.ptr;
   a.W3 = d_W3.ptr;
   a.dpi = d_dpi.ptr;
-  a.C = d_C.ptr;
   a.s = d_s.ptr;
   a.tpart = d_tpart.ptr;
   a.tpart3 = d_tpart3.ptr;
@@ -584,6 +590,11 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.coeffs = d_coeffs.ptr;
   a.mu_pi_out = d_mu_pi_out.ptr;
   a.rpc_max = cg_rows_per_chunk_max(a);
+  a.trace = nullptr;
+  if (std::getenv("DDELM_CG_TRACE")) {
+    d_trace.alloc(148 * 4 * 16);
+    a.trace = d_trace.ptr;
+  }
   return a;
 }
 
@@ -670,6 +681,25 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
     pending_[kt_cg].bytes = per_it * std::max(res.iterations, 1);
   }
   ktimer_collect();
+  if (a.trace) {
+    // per-phase device timers of the CG job: max and mean over CTAs, microseconds per iteration
+    const int G = cg_grid(a);
+    std::vector<double> t(static_cast<size_t>(G) * 16);
+    DDG_CUDA(cudaMemcpy(t.data(), d_trace.ptr, t.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    static const char* names[16] = {"op1",  "sync1", "op2", "sync2", "nn1", "sync3", "nn2", "sync4",
+                                    "op3",  "sync5", "op4", "sync6", "xr",  "sync7", "fin", "-"};
+    std::fprintf(stderr, "[cg trace] %d iterations, G=%d, P=%d (us/iteration: max / mean over CTAs)\n",
+                 res.iterations, G, a.P);
+    for (int k = 0; k < 15; ++k) {
+      double mx = 0, mean = 0;
+      for (int b = 0; b < G; ++b) {
+        mx = std::max(mx, t[b * 16 + k]);
+        mean += t[b * 16 + k] / G;
+      }
+      const double it = std::max(res.iterations, 1);
+      std::fprintf(stderr, "[cg trace] %-6s %8.2f %8.2f\n", names[k], mx / it / 1e3, mean / it / 1e3);
+    }
+  }
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
   solve_launches_ = launches_ - l0;
   solved_ = true;

@@ -128,7 +128,8 @@ class Workspace {
   DevBuf<double> d_FC, d_Zc, d_pd, d_Gc, d_Ypi, d_Dpp, d_dpi, d_S, d_Sinv, d_Wmu, d_Wd, d_W3;
   // CG
   DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu_pi_out, d_tpart, d_tpart3,
-      d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_pap, d_vin, d_vout;
+      d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_pap, d_vin, d_vout, d_trace, d_KF, d_KD;
+  int ldKF_ = 0, ldKD_ = 0;
 };
 
 }  // namespace ddg
