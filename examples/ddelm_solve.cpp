@@ -1,0 +1,56 @@
+// ddelm_solve — C++ host program over the drop-in façade (include/ddelm_b200/solvers.hpp).
+//
+// The device-path subset of `ddelm_cli solve` (tools/ddelm_cli.cpp:55-92, runner.cpp:126-155):
+//   ddelm_solve [key=value ...]   keys: problem s n_grid M l seed method theta flux_variant
+//                                 trace_basis cg_rel_tol cg_max_iter device
+// Prints one JSON object (iterations, converged, residual history, mu, timings) on stdout.
+// Exit codes follow the CLI: 0 ok, 2 non-convergence / solver error, 3 configuration error.
+#include <cstdio>
+#include <cstdlib>
+#include <exception>
+#include <map>
+#include <string>
+
+#include "ddelm_b200/solvers.hpp"
+
+int main(int argc, char** argv) {
+  std::map<std::string, std::string> kv = {
+      {"problem", "poisson_sinpi"}, {"s", "2"}, {"n_grid", "10"}, {"M", "64"}, {"l", "8"}, {"seed", "1"},
+      {"method", "ddelm-nn"}, {"theta", "0.999"}, {"flux_variant", "mean_edge"},
+      {"trace_basis", "change_of_variables"}, {"cg_rel_tol", "1e-9"}, {"cg_max_iter", "0"}, {"device", "0"}};
+  for (int k = 1; k < argc; ++k) {
+    const std::string a = argv[k];
+    const auto eq = a.find('=');
+    if (eq == std::string::npos || !kv.count(a.substr(0, eq))) {
+      std::fprintf(stderr, "config error: bad argument '%s'\n", a.c_str());
+      return 3;
+    }
+    kv[a.substr(0, eq)] = a.substr(eq + 1);
+  }
+  try {
+    ddelm::SolverOptions opts;
+    opts.flux_variant = kv["flux_variant"] == "mean_edge" ? ddelm::FluxVariant::MeanEdge : ddelm::FluxVariant::Pointwise;
+    opts.change_of_variables = kv["trace_basis"] == "change_of_variables";
+    opts.device = std::atoi(kv["device"].c_str());
+    ddelm::Workspace ws(ddelm::make_problem(kv["problem"]), std::atoi(kv["s"].c_str()), std::atoi(kv["n_grid"].c_str()),
+                        std::atoi(kv["M"].c_str()), std::atof(kv["l"].c_str()),
+                        std::strtoull(kv["seed"].c_str(), nullptr, 10), opts);
+    ddelm::CgOptions cg{std::atof(kv["cg_rel_tol"].c_str()), std::atoi(kv["cg_max_iter"].c_str())};
+    ddelm::SolveReport r = kv["method"] == "ddelm-cs" ? ddelm::ddelm_cs_solve(ws, cg)
+                                                      : ddelm::ddelm_nn_solve(ws, std::atof(kv["theta"].c_str()), cg);
+    std::printf("{\"iterations\": %d, \"converged\": %s, \"total_seconds\": %.9g, \"residual_history\": [", r.iterations,
+                r.converged ? "true" : "false", r.total_seconds);
+    for (size_t k = 0; k < r.residual_history.size(); ++k)
+      std::printf("%s%.17g", k ? ", " : "", r.residual_history[k]);
+    std::printf("], \"mu\": [");
+    for (size_t k = 0; k < r.mu.size(); ++k) std::printf("%s%.17g", k ? ", " : "", r.mu[k]);
+    std::printf("]}\n");
+    return r.converged ? 0 : 2;
+  } catch (const std::invalid_argument& e) {
+    std::fprintf(stderr, "config error: %s\n", e.what());
+    return 3;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "solver error: %s\n", e.what());
+    return 2;
+  }
+}

@@ -1,0 +1,169 @@
+// ddelm_b200/solvers.hpp — C++ drop-in façade of the reference solver API over the C-ABI.
+//
+// Mirrors proj/include/ddelm/solvers.hpp (namespace ddelm) for the north-star path:
+//   Workspace(problem, s, n_grid, M, l, seed, SolverOptions)     solvers.hpp:79-80
+//   ddelm_cs_solve(Workspace&, CgOptions)                          solvers.hpp:179
+//   ddelm_nn_solve(Workspace&, double theta, CgOptions)            solvers.hpp:181
+//   SolverOptions / CgOptions / SolveReport                        solvers.hpp:49-58,162-176
+//   ProblemSpec via make_problem(name)                             problems.hpp:38-62,
+//                                                                   problems.cpp:132-188
+// with the reference's error behaviour: std::invalid_argument for bad arguments (theta outside
+// [0,1], bad partition, unknown problem), std::runtime_error for a non-SPD coarse matrix and for
+// device failures. Non-convergence is SolveReport::converged == false, not an exception.
+//
+// Vectors are std::vector<double> instead of Eigen::VectorXd (Eigen is not a dependency of the
+// device path); layouts are the reference's (coefficients per subdomain; mu = [mu_Delta; mu_Pi]).
+// Everything heavy runs on the B200 behind include/ddelm_gpu.h; this header only marshals.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ddelm_gpu.h"
+
+namespace ddelm {
+
+enum class FluxVariant { Pointwise, MeanEdge };  // assembly.hpp FluxVariant
+
+struct ProblemSpec {
+  std::string name;
+  int id = DDELM_POISSON_SINPI;
+};
+
+/// make_problem (problems.cpp:132-188): the Poisson problems of the device path.
+inline ProblemSpec make_problem(const std::string& name) {
+  if (name == "poisson_sinpi") return {name, DDELM_POISSON_SINPI};
+  if (name == "poisson_sin2pi_exp") return {name, DDELM_POISSON_SIN2PI_EXP};
+  if (name == "poisson_sin2pi_cos3pi_x2y") return {name, DDELM_POISSON_SIN2PI_COS3PI_X2Y};
+  throw std::invalid_argument("make_problem: unknown problem '" + name + "'");
+}
+
+struct SolverOptions {  // solvers.hpp:49-58
+  FluxVariant flux_variant = FluxVariant::Pointwise;
+  bool change_of_variables = false;
+  double rank_tol = 1e-10;
+  int workers = 1;  // accepted for API parity; the device batches all subdomains
+  int debug_flip_flux_row = -1;
+  int device = 0;   // CUDA device ordinal (device-path addition)
+};
+
+struct CgOptions {  // solvers.hpp:173-176
+  double rel_tol = 1e-9;
+  int max_iter = 0;  // <= 0: 20x unknowns
+};
+
+struct SolveReport {  // solvers.hpp:162-171
+  std::vector<std::vector<double>> coeffs;  // per subdomain, M each
+  std::vector<double> mu, mu_delta, mu_pi;  // global ordering, Delta then Pi
+  int iterations = 0;
+  bool converged = true;
+  bool negative_curvature = false;
+  std::vector<double> residual_history;
+  double setup_seconds = 0, cg_seconds = 0, reconstruct_seconds = 0;
+  double assembly_seconds = 0, factorization_seconds = 0, total_seconds = 0;
+};
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == DDELM_OK) return;
+  const std::string msg = ddelm_gpu_last_error();
+  if (rc == DDELM_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+struct WsDeleter {
+  void operator()(ddelm_ws* w) const { ddelm_gpu_destroy(w); }
+};
+}  // namespace detail
+
+/// Device-resident Workspace (solvers.hpp:78-160): features, local factorisations, the coarse
+/// and Neumann layers live in HBM; the layers are built lazily like the reference's
+/// coarse_built / neumann_built flags. Not safe for concurrent solves (same as the reference).
+class Workspace {
+ public:
+  Workspace(const ProblemSpec& problem, int s, int n_grid, int M, double l, std::uint64_t seed,
+            const SolverOptions& opts = {})
+      : s_(s), n_grid_(n_grid), M_(M) {
+    ddelm_desc d{};
+    d.problem = problem.id;
+    d.s = s;
+    d.n_grid = n_grid;
+    d.M = M;
+    d.l = l;
+    d.seed = seed;
+    d.flux_variant = opts.flux_variant == FluxVariant::MeanEdge ? DDELM_FLUX_MEAN_EDGE : DDELM_FLUX_POINTWISE;
+    d.change_of_variables = opts.change_of_variables ? 1 : 0;
+    d.rank_tol = opts.rank_tol;
+    d.device = opts.device;
+    d.debug_flip_flux_row = opts.debug_flip_flux_row;
+    ddelm_ws* w = nullptr;
+    detail::check(ddelm_gpu_create(&d, &w));
+    ws_.reset(w);
+  }
+
+  int n_subs() const { return s_ * s_; }
+  int n_delta() const { return 2 * s_ * (s_ - 1) * (n_grid_ - 2); }
+  int n_pi() const { return (s_ - 1) * (s_ - 1); }
+  int M() const { return M_; }
+
+  void build() { detail::check(ddelm_gpu_build(ws_.get())); }
+  void assemble_coarse() { detail::check(ddelm_gpu_build_coarse(ws_.get())); }  // solvers.cpp:278
+  void build_neumann() { detail::check(ddelm_gpu_build_neumann(ws_.get())); }    // solvers.cpp:390
+
+  /// cs_reduced_apply with the NN weight (solvers.cpp:372-386, 599-603); theta = 0: coarse op.
+  std::vector<double> cs_reduced_apply(const std::vector<double>& v, double theta) {
+    std::vector<double> out(v.size());
+    detail::check(ddelm_gpu_apply_operator(ws_.get(), theta, v.data(), out.data()));
+    return out;
+  }
+
+  SolveReport solve(int method, double theta, const CgOptions& cg) {
+    ddelm_report r{};
+    detail::check(ddelm_gpu_solve(ws_.get(), method, theta, cg.rel_tol, cg.max_iter, &r));
+    SolveReport rep;
+    rep.iterations = r.iterations;
+    rep.converged = r.converged != 0;
+    rep.negative_curvature = r.negative_curvature != 0;
+    rep.mu.resize(r.n_mu);
+    detail::check(ddelm_gpu_get_mu(ws_.get(), rep.mu.data()));
+    rep.mu_delta.assign(rep.mu.begin(), rep.mu.begin() + r.n_delta);
+    rep.mu_pi.assign(rep.mu.begin() + r.n_delta, rep.mu.end());
+    std::vector<double> c(static_cast<size_t>(r.n_subdomains) * r.M);
+    detail::check(ddelm_gpu_get_coeffs(ws_.get(), c.data()));
+    rep.coeffs.resize(r.n_subdomains);
+    for (int i = 0; i < r.n_subdomains; ++i)
+      rep.coeffs[i].assign(c.begin() + static_cast<size_t>(i) * r.M, c.begin() + static_cast<size_t>(i + 1) * r.M);
+    rep.residual_history.resize(std::max(r.iterations, 0));
+    const int n = ddelm_gpu_get_residuals(ws_.get(), rep.residual_history.data(), r.iterations);
+    rep.residual_history.resize(std::max(n, 0));
+    rep.setup_seconds = r.setup_seconds;
+    rep.cg_seconds = r.cg_seconds;
+    rep.reconstruct_seconds = r.reconstruct_seconds;
+    rep.assembly_seconds = r.assembly_seconds;
+    rep.factorization_seconds = r.factorization_seconds;
+    rep.total_seconds = r.total_seconds;
+    return rep;
+  }
+
+  ddelm_ws* handle() { return ws_.get(); }
+
+ private:
+  int s_, n_grid_, M_;
+  std::unique_ptr<ddelm_ws, detail::WsDeleter> ws_;
+};
+
+/// ddelm_cs_solve (solvers.cpp:582-588).
+inline SolveReport ddelm_cs_solve(Workspace& ws, const CgOptions& cg_opts = {}) {
+  return ws.solve(DDELM_METHOD_CS, 0.0, cg_opts);
+}
+
+/// ddelm_nn_solve (solvers.cpp:590-605): theta in [0, 1]; theta = 0 is exactly ddelm_cs_solve.
+inline SolveReport ddelm_nn_solve(Workspace& ws, double theta, const CgOptions& cg_opts = {}) {
+  if (!(theta >= 0.0 && theta <= 1.0)) throw std::invalid_argument("ddelm_nn_solve: theta must lie in [0, 1]");
+  return ws.solve(DDELM_METHOD_NN, theta, cg_opts);
+}
+
+}  // namespace ddelm

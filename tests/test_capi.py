@@ -70,3 +70,23 @@ def test_invalid_arguments_mirror_reference():
     with pytest.raises(ValueError):
         P.SolverOptions(flux_variant="bogus") and P.Workspace("poisson_sinpi", 2, 10, 64, 8.0, 1,
                                                               P.SolverOptions(flux_variant="bogus"))
+
+
+FACADE_BIN = os.path.join(ROOT, "paper_2503_10032_b200", "ddelm_solve")
+
+
+def test_cpp_facade_builds_and_links():
+    """examples/ddelm_solve.cpp uses only include/ddelm_b200/solvers.hpp (the reference-shaped
+    C++ API) over the C-ABI; it is built by the package Makefile."""
+    import subprocess
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2503_10032_b200", "csrc")], check=True)
+    assert os.access(FACADE_BIN, os.X_OK)
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-device error path")
+def test_cpp_facade_fails_loudly_without_device():
+    import subprocess
+    out = subprocess.run([FACADE_BIN], capture_output=True, text=True)
+    assert out.returncode == 2 and "no CUDA device" in out.stderr
+    bad = subprocess.run([FACADE_BIN, "bogus=1"], capture_output=True, text=True)
+    assert bad.returncode == 3

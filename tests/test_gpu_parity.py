@@ -214,3 +214,19 @@ def test_reseed_changes_and_restores(P):
     ws.reseed(1)
     _, c = P.solve_config("T1", ws=ws)
     assert np.array_equal(a.mu, c.mu)
+
+
+def test_cpp_facade_matches_python_path(P):
+    """The C++ façade (include/ddelm_b200/solvers.hpp) drives the same device path: T1 through
+    examples/ddelm_solve reproduces the Python-mirror solve bit for bit."""
+    import json
+    import subprocess
+    exe = os.path.join(ROOT, "paper_2503_10032_b200", "ddelm_solve")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    d = json.loads(out.stdout)
+    _, rep = P.solve_config("T1")
+    assert d["iterations"] == rep.iterations
+    assert np.array_equal(np.array(d["mu"]), rep.mu)
+    bad = subprocess.run([exe, "theta=1.5"], capture_output=True, text=True, timeout=120)
+    assert bad.returncode == 3 and "theta" in bad.stderr
