@@ -21,77 +21,188 @@ namespace ddg {
 namespace {
 
 constexpr int NB = kQrNB;
-constexpr int TN = 64;  // trailing tile columns
-constexpr int RC = 32;  // row chunk
+constexpr int RC = 32;  // rows per chunk (panel Gram and trailing streams)
 
-__global__ void __launch_bounds__(1024) qr_panel_kernel(QrArgs a, int k0) {
+// ---------------------------------------------------------------- panel (BLAS-2, one CTA / matrix)
+// Column c of the panel costs ONE pass over the remaining panel rows: the pass applies the
+// previous reflector H_{c-1} (v scaled on the fly, pivot row set to beta) and, on the updated
+// values, accumulates ||x_c||^2 below the diagonal and s_j = x_c . y_j for the panel columns right
+// of c. One block reduction (warp reduce-scatter) then gives beta, tau and
+// d_j = v_c . y_j = y_cj + s_j / (alpha - beta) for the next pass. Each thread streams two rows
+// at a time (up to 64 independent loads in flight), so a column step is one L2 round trip + one
+// reduction instead of a chain of per-column dot products.
+constexpr int kPanelThreads = 512;
+constexpr int kPanelWarps = kPanelThreads / 32;
+
+/// lane l ends with the warp-wide sum of v[l] (31 shuffles for 32 values)
+__device__ __forceinline__ double reduce_scatter32(double (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int k = 0; k < s; ++k) {
+      const double send = upper ? v[k] : v[k + s];
+      const double keep = upper ? v[k + s] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
+
+/// One fused pass of the panel factorisation with NR = nb - jj columns left (compile-time, so
+/// every loop is fully unrolled with no per-element predicates): applies H_{c-1} to this warp's
+/// rows, stores them, and accumulates ||x_c||^2 and x_c . y_{c+k} (lane k of accS: column jj+k).
+template <int NR>
+__device__ __forceinline__ void panel_pass(double* P, size_t ld, int m, int rlo, int jj, int cp, int c,
+                                           double tau_p, double scale_p, double beta_p, bool triv_p,
+                                           const double* sd, double* srow, double& accS, double& n2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int rbase = rlo + warp * 32; rbase < m; rbase += kPanelThreads) {
+    const int r = rbase + lane;
+    const bool valid = r < m;
+    double y[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) y[k] = (k < NR && valid) ? P[static_cast<size_t>(jj + (k < NR ? k : 0)) * ld + r] : 0.0;
+    if (jj > 0) {  // apply H_{c-1}: v on this row, pivot row gets beta
+      double* pc = P + static_cast<size_t>(jj - 1) * ld + r;
+      const double xp = valid ? *pc : 0.0;
+      const double v = (r == cp) ? 1.0 : (triv_p ? 0.0 : xp * scale_p);
+      const double tv = tau_p * v;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) y[k] -= tv * sd[jj + k];
+      if (valid) {
+        *pc = (r == cp) ? beta_p : v;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) P[static_cast<size_t>(jj + k) * ld + r] = y[k];
+      }
+    }
+    if constexpr (NR > 0) {
+      const double x = y[0];
+      if (valid && r == c) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) srow[jj + k] = y[k];
+      }
+      const bool acc_row = valid && r > c;
+      // products in place; slot 0 carries ||x||^2 (column jj itself)
+#pragma unroll
+      for (int k = 0; k < 32; ++k) y[k] = (k < NR && acc_row) ? x * y[k] : 0.0;
+      accS += reduce_scatter32(y);
+    }
+  }
+  (void)n2;
+}
+
+__global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, int k0) {
   const int t = blockIdx.x;
   double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
-  const int m = a.m, ld = a.ld;
+  const int m = a.m;
+  const size_t ld = a.ld;
   const int nb = min(NB, a.M - k0);
-  __shared__ double red[32];
+  __shared__ double sred[kPanelWarps][NB + 1];
+  __shared__ double sfin[NB + 1];
+  __shared__ double srow[NB];
+  __shared__ double sd[NB];
+  __shared__ double stau[NB];
+  __shared__ double sbeta, sscale;
+  __shared__ int striv;
   __shared__ double Vs[RC][NB + 1];
   __shared__ double G[NB][NB + 1];
-  __shared__ double stau[NB];
   __shared__ double Tsh[NB][NB + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* P = A + static_cast<size_t>(k0) * ld;  // panel column j at P + j*ld
 
-  for (int jj = 0; jj < nb; ++jj) {
-    const int c = k0 + jj;
-    double* col = A + static_cast<size_t>(c) * ld;
-    double part = 0;
-    for (int i = c + 1 + threadIdx.x; i < m; i += blockDim.x) part += col[i] * col[i];
-    const double tail = block_sum(part, red);
-    const double alpha = col[c];
-    double tau = 0, beta = alpha, scale = 0;
-    const bool triv = !(tail > DBL_MIN);
-    if (!triv) {
-      beta = sqrt(alpha * alpha + tail);
-      if (alpha >= 0) beta = -beta;
-      scale = 1.0 / (alpha - beta);
-      tau = (beta - alpha) / beta;
+  for (int jj = 0; jj <= nb; ++jj) {
+    const int cp = k0 + jj - 1;  // previous pivot (row and column), jj > 0
+    const int c = k0 + jj;       // current pivot, jj < nb
+    const int jlo = jj > 0 ? jj - 1 : 0;
+    const int rlo = jj > 0 ? cp : c;
+    double tau_p = 0, scale_p = 0, beta_p = 0;
+    bool triv_p = true;
+    if (jj > 0) {
+      tau_p = stau[jj - 1];
+      scale_p = sscale;
+      beta_p = sbeta;
+      triv_p = striv != 0;
     }
-    for (int i = c + 1 + threadIdx.x; i < m; i += blockDim.x) col[i] = triv ? 0.0 : col[i] * scale;
+    // lane k accumulates x_c . y_{c+k} (k = 0: ||x_c||^2) over the rows this warp visits
+    double accS = 0, n2 = 0;
+    switch (nb - jj) {
+#define DDG_PANEL_CASE(n) \
+  case n:                 \
+    panel_pass<n>(P, ld, m, rlo, jj, cp, c, tau_p, scale_p, beta_p, triv_p, sd, srow, accS, n2); \
+    break;
+      DDG_PANEL_CASE(0) DDG_PANEL_CASE(1) DDG_PANEL_CASE(2) DDG_PANEL_CASE(3) DDG_PANEL_CASE(4)
+      DDG_PANEL_CASE(5) DDG_PANEL_CASE(6) DDG_PANEL_CASE(7) DDG_PANEL_CASE(8) DDG_PANEL_CASE(9)
+      DDG_PANEL_CASE(10) DDG_PANEL_CASE(11) DDG_PANEL_CASE(12) DDG_PANEL_CASE(13) DDG_PANEL_CASE(14)
+      DDG_PANEL_CASE(15) DDG_PANEL_CASE(16) DDG_PANEL_CASE(17) DDG_PANEL_CASE(18) DDG_PANEL_CASE(19)
+      DDG_PANEL_CASE(20) DDG_PANEL_CASE(21) DDG_PANEL_CASE(22) DDG_PANEL_CASE(23) DDG_PANEL_CASE(24)
+      DDG_PANEL_CASE(25) DDG_PANEL_CASE(26) DDG_PANEL_CASE(27) DDG_PANEL_CASE(28) DDG_PANEL_CASE(29)
+      DDG_PANEL_CASE(30) DDG_PANEL_CASE(31) DDG_PANEL_CASE(32)
+#undef DDG_PANEL_CASE
+      default:
+        break;
+    }
+    if (jj == nb) break;
+    // ---- block reduction of (n2, s_j)
+    sred[warp][lane] = accS;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      col[c] = beta;
-      stau[jj] = tau;
-      a.tau[static_cast<size_t>(t) * a.M + c] = tau;
+    if (threadIdx.x < NB) {
+      double s = 0;
+      for (int w = 0; w < kPanelWarps; ++w) s += sred[w][threadIdx.x];
+      sfin[threadIdx.x] = s;  // sfin[k]: column jj+k (k = 0: squared norm below the diagonal)
     }
-    // apply H_c to the remaining panel columns: one warp per column
-    for (int cc = c + 1 + warp; cc < k0 + nb; cc += 32) {
-      double* y = A + static_cast<size_t>(cc) * ld;
-      const double yc = y[c];
-      double d = 0;
-      for (int i = c + 1 + lane; i < m; i += 32) d += col[i] * y[i];
-      d = warp_sum(d);
-      d = (d + yc) * tau;
-      if (lane == 0) y[c] = yc - d;
-      for (int i = c + 1 + lane; i < m; i += 32) y[i] -= d * col[i];
+    __syncthreads();
+    {
+      const double alpha = srow[jj], tail = sfin[0];
+      double tau = 0, beta = alpha, scale = 0;
+      const bool triv = !(tail > DBL_MIN);
+      if (!triv) {
+        beta = sqrt(alpha * alpha + tail);
+        if (alpha >= 0) beta = -beta;
+        scale = 1.0 / (alpha - beta);
+        tau = (beta - alpha) / beta;
+      }
+      if (threadIdx.x < NB) {
+        const int j = threadIdx.x;
+        sd[j] = (j > jj && j < nb) ? srow[j] + sfin[j - jj] * scale : 0.0;
+      }
+      if (threadIdx.x == 0) {
+        stau[jj] = tau;
+        sbeta = beta;
+        sscale = scale;
+        striv = triv ? 1 : 0;
+        a.tau[static_cast<size_t>(t) * a.M + c] = tau;
+      }
     }
     __syncthreads();
   }
+  __syncthreads();
 
-  // G = V^T V over the panel (implicit unit diagonal, zeros above)
+  // G = V^T V over the panel (implicit unit diagonal, zeros above); thread -> (u, v), (u, v + 16)
   const int u = threadIdx.x & 31, v = threadIdx.x >> 5;
-  double g = 0;
+  double g0 = 0, g1 = 0;
   for (int r0 = k0; r0 < m; r0 += RC) {
-    {
-      const int rr = threadIdx.x & 31, uu = threadIdx.x >> 5;  // 32 x 32 chunk
+    for (int idx = threadIdx.x; idx < RC * NB; idx += blockDim.x) {
+      const int rr = idx & 31, uu = idx >> 5;
       const int row = r0 + rr;
       double val = 0;
       if (row < m && uu < nb) {
         if (row == k0 + uu) val = 1.0;
-        else if (row > k0 + uu) val = A[static_cast<size_t>(k0 + uu) * ld + row];
+        else if (row > k0 + uu) val = P[static_cast<size_t>(uu) * ld + row];
       }
       Vs[rr][uu] = val;
     }
     __syncthreads();
 #pragma unroll 8
-    for (int rr = 0; rr < RC; ++rr) g += Vs[rr][u] * Vs[rr][v];
+    for (int rr = 0; rr < RC; ++rr) {
+      g0 += Vs[rr][u] * Vs[rr][v];
+      g1 += Vs[rr][u] * Vs[rr][v + 16];
+    }
     __syncthreads();
   }
-  G[u][v] = g;
+  G[u][v] = g0;
+  G[u][v + 16] = g1;
   __syncthreads();
   // T: T(j,j) = tau_j, T(0:j, j) = -tau_j T(0:j,0:j) G(0:j, j)
   if (warp == 0) {
@@ -108,122 +219,217 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(QrArgs a, int k0) {
     }
   }
   __syncthreads();
-  double* T = a.T + static_cast<size_t>(t) * NB * NB;
-  T[threadIdx.x] = Tsh[threadIdx.x >> 5][threadIdx.x & 31];
+  double* T = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
+  for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x)
+    T[(idx >> 5) * kQrTmax + (idx & 31)] = Tsh[idx >> 5][idx & 31];
 }
 
-__global__ void __launch_bounds__(256) qr_trailing_kernel(QrArgs a, int k0) {
+// ---------------------------------------------------------------- trailing update (DMMA)
+// CTA = (matrix t, 64-column tile of the trailing matrix). The tile and the panel's reflectors V
+// stream through a 3-stage cp.async ring in 32-row chunks, twice:
+//   pass 1   W  = V^T A_tile          (NB x 64, DMMA m8n8k4, K = rows)
+//            W' = T^T W                (T upper triangular, from qr_panel)
+//   pass 2   A_tile -= V W'           (per chunk: accumulators initialised from the staged chunk,
+//                                      K = NB; result written back to smem, then coalesced stores)
+// Chunks are column-major in shared memory with a 36-double column stride: every m8n8k4 fragment
+// load (A: 4 k x 8 m, B: 4 k x 8 n) hits 16 distinct 8-byte banks per half-warp.
+constexpr int TN = 64;    // tile columns
+constexpr int RCP = 36;   // padded column stride of a staged chunk
+constexpr int TNP = 68;   // padded row stride of W / W'
+constexpr int kTrStages = 3;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 16 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int NB_>
+struct TrailSmem {
+  double V[kTrStages][NB_ * RCP];  // V chunk, column u at V[u*RCP + k]
+  double A[kTrStages][TN * RCP];   // A chunk, column c at A[c*RCP + k]
+  double W[NB_ * TNP];             // W, then W'
+  double T[NB_ * (NB_ + 1)];
+};
+
+template <int NB_>
+__global__ void __launch_bounds__(256, 2) qr_trailing_kernel(QrArgs a, int k0) {
+  static_assert(NB_ == 32 || NB_ == 64, "panel width");
+  constexpr int MT = NB_ / 8;  // m-tiles of W
+  extern __shared__ __align__(16) double smraw[];
+  TrailSmem<NB_>& S = *reinterpret_cast<TrailSmem<NB_>*>(smraw);
   const int t = blockIdx.y;
-  const int nb = min(NB, a.M - k0);
+  const int nb = min(NB_, a.M - k0);
   const int c0 = k0 + nb + blockIdx.x * TN;
   if (c0 >= a.ncol) return;
   const int ncols = min(TN, a.ncol - c0);
   double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
-  const int m = a.m, ld = a.ld;
-  __shared__ double Vs[RC][NB + 1];
-  __shared__ double Ts[NB][NB + 1];
-  // the A chunk (pass 1) and W / W' (after pass 1) share storage
-  __shared__ double AWbuf[RC * (TN + 1)];
-  double(*As)[TN + 1] = reinterpret_cast<double(*)[TN + 1]>(AWbuf);
-  double(*Ws)[TN + 1] = reinterpret_cast<double(*)[TN + 1]>(AWbuf);
-  static_assert(RC == NB, "A chunk and W share one buffer");
+  const size_t ld = a.ld;
+  const int nq = (a.m - k0 + RC - 1) / RC;  // chunks per pass
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lr = lane >> 2, lc = lane & 3;
 
-  auto load_v = [&](int r0) {
-    for (int idx = threadIdx.x; idx < RC * NB; idx += blockDim.x) {
-      const int rr = idx % RC, uu = idx / RC;
-      const int row = r0 + rr;
-      double val = 0;
-      if (row < m && uu < nb) {
-        if (row == k0 + uu) val = 1.0;
-        else if (row > k0 + uu) val = A[static_cast<size_t>(k0 + uu) * ld + row];
+  // issue chunk q of the unified stream (q < nq: pass 1, else pass 2) into stage q % 3
+  auto issue = [&](int q) {
+    if (q < 2 * nq) {
+      const int st = q % kTrStages;
+      const int r0 = k0 + (q % nq) * RC;
+      // V: nb columns x 32 rows = nb * 16 segments of 16 B; A: 64 columns
+      for (int idx = threadIdx.x; idx < (NB_ + TN) * 16; idx += blockDim.x) {
+        const int col = idx >> 4, seg = idx & 15;
+        const int row = r0 + 2 * seg;
+        if (col < NB_) {
+          const bool ok = col < nb && row < static_cast<int>(ld);
+          cp_async16(&S.V[st][col * RCP + 2 * seg], A + static_cast<size_t>(k0 + col) * ld + (ok ? row : 0), ok);
+        } else {
+          const int c = col - NB_;
+          const bool ok = c < ncols && row < static_cast<int>(ld);
+          cp_async16(&S.A[st][c * RCP + 2 * seg], A + static_cast<size_t>(c0 + (ok ? c : 0)) * ld + (ok ? row : 0), ok);
+        }
       }
-      Vs[rr][uu] = val;
+    }
+    cp_async_commit();
+  };
+  // unit lower-triangular structure of V inside the first NB rows of the stream
+  auto fix_v = [&](int st, int r0) {
+    if (r0 >= k0 + nb) return;
+    for (int idx = threadIdx.x; idx < NB_ * RC; idx += blockDim.x) {
+      const int u = idx / RC, k = idx % RC;
+      const int row = r0 + k;
+      if (row <= k0 + u) S.V[st][u * RCP + k] = (row == k0 + u && u < nb) ? 1.0 : 0.0;
     }
   };
 
-  // ---- pass 1: W = V^T A_tile   (32 x 64), warp w: t-block (w & 3), col blocks 4*(w>>2)..+3
-  const int tb = warp & 3, cb0 = (warp >> 2) * 4;
-  double acc[4][2];
+  issue(0);
+  issue(1);
+  // T (nb x nb upper triangular, zero padded)
+  const double* Tg = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
+  for (int idx = threadIdx.x; idx < NB_ * NB_; idx += blockDim.x) {
+    const int i = idx / NB_, j = idx % NB_;
+    S.T[i * (NB_ + 1) + j] = (i < nb && j < nb) ? Tg[i * kQrTmax + j] : 0.0;
+  }
+
+  // ---- pass 1: W = V^T A_tile. Warp tile: (MT/2) m-tiles x 2 n-tiles.
+  //      NB=32: warp -> m-tiles {2(w&1), +1}, n-tiles {2(w>>1), +1};  NB=64: m-tiles 4(w&1).., n-tiles 2(w>>1)..
+  constexpr int WM = MT / 2;
+  const int mt0 = (warp & 1) * WM, nt0 = (warp >> 1) * 2;
+  double acc[WM][2][2];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
-  for (int r0 = k0; r0 < m; r0 += RC) {
-    load_v(r0);
-    for (int idx = threadIdx.x; idx < RC * TN; idx += blockDim.x) {
-      const int rr = idx % RC, cc = idx / RC;
-      const int row = r0 + rr;
-      As[rr][cc] = (row < m && cc < ncols) ? A[static_cast<size_t>(c0 + cc) * ld + row] : 0.0;
-    }
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    cp_async_wait<1>();
     __syncthreads();
+    issue(q + 2);
+    const int st = q % kTrStages;
+    fix_v(st, k0 + q * RC);
+    __syncthreads();
+    const double* Vs = S.V[st];
+    const double* As = S.A[st];
 #pragma unroll
     for (int kk = 0; kk < RC / 4; ++kk) {
-      const double av = Vs[kk * 4 + lc][tb * 8 + lr];
+      const int k = kk * 4 + lc;
+      double av[WM], bv[2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double bv = As[kk * 4 + lc][(cb0 + q) * 8 + lr];
-        dmma_8x8x4(acc[q][0], acc[q][1], av, bv);
-      }
+      for (int i = 0; i < WM; ++i) av[i] = Vs[((mt0 + i) * 8 + lr) * RCP + k];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bv[j] = As[((nt0 + j) * 8 + lr) * RCP + k];
+#pragma unroll
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int r = (mt0 + i) * 8 + lr, c = (nt0 + j) * 8 + 2 * lc;
+      S.W[r * TNP + c] = acc[i][j][0];
+      S.W[r * TNP + c + 1] = acc[i][j][1];
+    }
+  __syncthreads();
+  // ---- W' = T^T W (T upper triangular): column c of W' = T^T W(:, c)
+  {
+    double wcol[NB_ * TN / 256];
+#pragma unroll
+    for (int e = 0; e < NB_ * TN / 256; ++e) {
+      const int idx = threadIdx.x + 256 * e;
+      const int u = idx / TN, c = idx % TN;
+      double s = 0;
+      for (int w = 0; w <= u; ++w) s += S.T[w * (NB_ + 1) + u] * S.W[w * TNP + c];
+      wcol[e] = s;
     }
     __syncthreads();
-  }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    Ws[tb * 8 + lr][(cb0 + q) * 8 + 2 * lc] = acc[q][0];
-    Ws[tb * 8 + lr][(cb0 + q) * 8 + 2 * lc + 1] = acc[q][1];
+    for (int e = 0; e < NB_ * TN / 256; ++e) {
+      const int idx = threadIdx.x + 256 * e;
+      S.W[(idx / TN) * TNP + idx % TN] = wcol[e];
+    }
   }
-  const double* T = a.T + static_cast<size_t>(t) * NB * NB;
-  for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x) Ts[idx / NB][idx % NB] = T[idx];
-  __syncthreads();
-  // ---- W' = T^T W  (T upper triangular)
-  double wv[NB * TN / 256];
-#pragma unroll
-  for (int e = 0; e < NB * TN / 256; ++e) {
-    const int idx = threadIdx.x + 256 * e;
-    const int uu = idx / TN, cc = idx % TN;
-    double s = 0;
-    for (int w = 0; w <= uu; ++w) s += Ts[w][uu] * Ws[w][cc];
-    wv[e] = s;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int e = 0; e < NB * TN / 256; ++e) {
-    const int idx = threadIdx.x + 256 * e;
-    Ws[idx / TN][idx % TN] = wv[e];
-  }
-  __syncthreads();
-  // ---- pass 2: A_tile -= V W'  (row chunk 32 x 64), warp w: row block (w & 3), col blocks 4*(w>>2)..
-  const int rb = warp & 3;
-  for (int r0 = k0; r0 < m; r0 += RC) {
-    load_v(r0);
+  // ---- pass 2: A_tile -= V W' per 32-row chunk. Warp tile: 2 row-tiles x 2 col-tiles.
+  const int rt0 = (warp & 1) * 2, ct0 = (warp >> 1) * 2;
+  for (int q = nq; q < 2 * nq; ++q) {
+    cp_async_wait<1>();
     __syncthreads();
-    double cfr[4][2];
-    const int row = r0 + rb * 8 + lr;
+    issue(q + 2);
+    const int st = q % kTrStages;
+    const int r0 = k0 + (q - nq) * RC;
+    fix_v(st, r0);
+    __syncthreads();
+    const double* Vs = S.V[st];
+    double* As = S.A[st];
+    double cf[2][2][2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int cc = (cb0 + q) * 8 + 2 * lc + e;
-        cfr[q][e] = (row < m && cc < ncols) ? A[static_cast<size_t>(c0 + cc) * ld + row] : 0.0;
+      for (int j = 0; j < 2; ++j) {
+        const int r = (rt0 + i) * 8 + lr, c = (ct0 + j) * 8 + 2 * lc;
+        cf[i][j][0] = As[c * RCP + r];
+        cf[i][j][1] = As[(c + 1) * RCP + r];
       }
 #pragma unroll
-    for (int kk = 0; kk < NB / 4; ++kk) {
-      const double av = -Vs[rb * 8 + lr][kk * 4 + lc];
+    for (int kk = 0; kk < NB_ / 4; ++kk) {
+      const int u = kk * 4 + lc;
+      double av[2], bv[2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double bv = Ws[kk * 4 + lc][(cb0 + q) * 8 + lr];
-        dmma_8x8x4(cfr[q][0], cfr[q][1], av, bv);
+      for (int i = 0; i < 2; ++i) av[i] = -Vs[u * RCP + (rt0 + i) * 8 + lr];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bv[j] = S.W[u * TNP + (ct0 + j) * 8 + lr];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(cf[i][j][0], cf[i][j][1], av[i], bv[j]);
+    }
+    __syncthreads();  // every warp read its accumulator init before the chunk is overwritten
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = (rt0 + i) * 8 + lr, c = (ct0 + j) * 8 + 2 * lc;
+        As[c * RCP + r] = cf[i][j][0];
+        As[(c + 1) * RCP + r] = cf[i][j][1];
+      }
+    __syncthreads();
+    // coalesced write-back: 64 columns x 16 two-row segments
+    for (int idx = threadIdx.x; idx < TN * 16; idx += blockDim.x) {
+      const int c = idx >> 4, seg = idx & 15;
+      const int row = r0 + 2 * seg;
+      if (c < ncols && row < static_cast<int>(ld)) {
+        double2 v;
+        v.x = As[c * RCP + 2 * seg];
+        v.y = As[c * RCP + 2 * seg + 1];
+        *reinterpret_cast<double2*>(A + static_cast<size_t>(c0 + c) * ld + row) = v;
       }
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int cc = (cb0 + q) * 8 + 2 * lc + e;
-        if (row < m && cc < ncols) A[static_cast<size_t>(c0 + cc) * ld + row] = cfr[q][e];
-      }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 }
 
 __global__ void qr_diag_ratio_kernel(QrArgs a, double* ratio) {
@@ -260,7 +466,7 @@ __global__ void qr_diag_ratio_kernel(QrArgs a, double* ratio) {
 }  // namespace
 
 void launch_qr_panel(const QrArgs& a, int k0, cudaStream_t st) {
-  qr_panel_kernel<<<a.nmat, 1024, 0, st>>>(a, k0);
+  qr_panel_kernel<<<a.nmat, kPanelThreads, 0, st>>>(a, k0);
   DDG_LAUNCH_CHECK();
 }
 
@@ -269,7 +475,14 @@ void launch_qr_trailing(const QrArgs& a, int k0, cudaStream_t st) {
   const int rest = a.ncol - (k0 + nb);
   if (rest <= 0) return;
   dim3 grid(ceil_div(rest, TN), a.nmat);
-  qr_trailing_kernel<<<grid, 256, 0, st>>>(a, k0);
+  const size_t smem = sizeof(TrailSmem<NB>);
+  static bool attr = false;
+  if (!attr) {
+    DDG_CUDA(cudaFuncSetAttribute(qr_trailing_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    attr = true;
+  }
+  qr_trailing_kernel<NB><<<grid, 256, smem, st>>>(a, k0);
   DDG_LAUNCH_CHECK();
 }
 

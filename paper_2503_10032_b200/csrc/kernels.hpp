@@ -36,9 +36,10 @@ struct QrArgs {
   int nmat, m, ld, ncol, M;
   double* A;    // nmat x ld x ncol
   double* tau;  // nmat x M
-  double* T;    // nmat x 32 x 32 (block reflector of the current panel)
+  double* T;    // nmat x kQrTmax x kQrTmax (block reflector of the current panel)
 };
 constexpr int kQrNB = 32;
+constexpr int kQrTmax = 64;
 void launch_qr_panel(const QrArgs& a, int k0, cudaStream_t st);
 void launch_qr_trailing(const QrArgs& a, int k0, cudaStream_t st);
 /// |R_ii| min / max per matrix -> ratio (branch test of LsFactor, solvers.cpp:27-32)

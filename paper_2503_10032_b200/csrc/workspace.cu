@@ -158,8 +158,10 @@ void Workspace::upload_plan() {
   kmax_ = std::min(p.M, 192);
   const size_t nmat = 2 * static_cast<size_t>(N);
   d_A.alloc(nmat * ld_ * ncol_);
+  // padding rows m..ld-1 stay zero for ever: the QR trailing update streams whole 32-row chunks
+  DDG_CUDA(cudaMemsetAsync(d_A.ptr, 0, d_A.count * sizeof(double), st_));
   d_tau.alloc(nmat * p.M);
-  d_T.alloc(nmat * kQrNB * kQrNB);
+  d_T.alloc(nmat * kQrTmax * kQrTmax);
   d_ratio.alloc(2 * nmat);
   d_deficient.alloc(nmat);
   d_rank.alloc(nmat);
