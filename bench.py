@@ -30,6 +30,17 @@ sys.path.insert(0, ROOT)
 FP64_PEAK_TFLOPS = 37.2  # measured DMMA loop on this pool's B200 (profiles/r01_fp64_peaks.json)
 
 
+def load_traffic(family):
+    """DRAM bytes per launch of `family` from the committed ncu capture (profiles/traffic.json,
+    written by tools/summarize_profiles.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(family)
+        return {"bytes": t["dram_bytes_per_launch"], "source": t["source"]} if t else None
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     hbm = 6554.2
@@ -284,15 +295,21 @@ def run_ours(args, cfg, world, rank, local, dist):
         s = fam[dominant]
         if s["flops"] > 0:
             ach = s["flops"] / (s["ms"] / 1e3) / 1e12
+            tr = load_traffic(dominant)
             roof = {"kernel": dominant, "bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS,
                     "peak_source": "measured FP64 DMMA loop (profiles/r01_fp64_peaks.json); "
                                    "MEASURED_PEAKS.json carries no FP64 entry",
-                    "traffic": None, "launches": s["launches"], "avg_launch_ms": s["ms"] / s["launches"]}
+                    "traffic": tr["bytes"] if tr else None, "traffic_source": tr["source"] if tr else None,
+                    "launches": s["launches"], "avg_launch_ms": s["ms"] / s["launches"]}
         else:
             ach = s["bytes"] / (s["ms"] / 1e3) / 1e9 if s["bytes"] > 0 else None
+            tr = load_traffic(dominant)
             roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": (ach / hbm) if ach else None, "traffic": None,
+                    "frac": (ach / hbm) if ach else None,
+                    "traffic": tr["bytes"] if tr else None,
+                    "traffic_source": tr["source"] if tr else None,
+                    "algorithmic_bytes_per_launch": s["bytes"] / s["launches"],
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs", "launches": s["launches"],
                     "avg_launch_ms": s["ms"] / s["launches"]}
     qr = fam.get("qr_trailing")

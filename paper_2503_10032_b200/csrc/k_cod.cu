@@ -193,26 +193,38 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
     }
     for (int u = threadIdx.x; u <= k; u += blockDim.x) vk[u] = V1[static_cast<size_t>(u) * M + k];
     __syncthreads();
-    // ---- F(:, k) = tau (A^T v - F V^T v) for positions j > k   (one warp per column)
-    for (int j = k + 1 + warp; j < M; j += nwarp) {
-      const int cj = perm[j];
-      const double* col = R0 + static_cast<size_t>(cj) * ld;
-      const int iend = min(cj, M - 1);
-      double g0 = 0, g1 = 0, g2 = 0, g3 = 0;
-      int i = k + lane;
-      for (; i + 96 <= iend; i += 128) {
-        g0 += col[i] * v[i];
-        g1 += col[i + 32] * v[i + 32];
-        g2 += col[i + 64] * v[i + 64];
-        g3 += col[i + 96] * v[i + 96];
+    // ---- F(:, k) = tau (A^T v - F V^T v) for positions j > k: a warp per 4 columns, lanes over
+    //      rows, 4 independent load streams (memory-level parallelism of the R0 / F1 reads)
+    for (int j0 = k + 1 + 4 * warp; j0 < M; j0 += 4 * nwarp) {
+      const double* col[4];
+      int iend[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = min(j0 + q, M - 1);
+        const int cj = perm[j];
+        col[q] = R0 + static_cast<size_t>(cj) * ld;
+        iend[q] = (j0 + q < M) ? min(cj, M - 1) : k - 1;
       }
-      for (; i <= iend; i += 32) g0 += col[i] * v[i];
-      double g = (g0 + g1) + (g2 + g3);
-      double fw = 0;
-      for (int u = lane; u < k; u += 32) fw += F1[static_cast<size_t>(j) * K + u] * w[u];
-      g = warp_sum(g);
-      fw = warp_sum(fw);
-      if (lane == 0) F1[static_cast<size_t>(j) * K + k] = s_tau * (g - fw);
+      const int imax = max(max(iend[0], iend[1]), max(iend[2], iend[3]));
+      double g[4] = {0, 0, 0, 0}, fw[4] = {0, 0, 0, 0};
+      for (int i = k + lane; i <= imax; i += 32) {
+        const double vi = v[i];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i <= iend[q]) g[q] += col[q][i] * vi;
+      }
+      for (int u = lane; u < k; u += 32) {
+        const double wu = w[u];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (j0 + q < M) fw[q] += F1[static_cast<size_t>(j0 + q) * K + u] * wu;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double gg = warp_sum(g[q]);
+        const double ff = warp_sum(fw[q]);
+        if (lane == 0 && j0 + q < M) F1[static_cast<size_t>(j0 + q) * K + k] = s_tau * (gg - ff);
+      }
     }
     __syncthreads();
     // ---- row k of R and norm downdating (thread per column)
