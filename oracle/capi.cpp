@@ -25,6 +25,7 @@ struct ddo_config {
   int cg_max_iter, cg_stop_after;
   int workers, cg_workers;
   int debug_flip_flux_row;
+  int layers_only;  // 1: partition + seeded layers only (field evaluation of given coefficients)
 };
 
 struct ddo_handle {
@@ -50,6 +51,7 @@ void* ddo_create(const ddo_config* c, char* err, int errlen) {
     o.workers = c->workers;
     o.cg_workers = c->cg_workers;
     o.debug_flip_flux_row = c->debug_flip_flux_row;
+    o.layers_only = c->layers_only != 0;
     const auto t0 = std::chrono::steady_clock::now();
     h->ws = std::make_unique<Workspace>(make_problem(c->problem), c->s, c->n_grid, c->M, c->l,
                                         c->seed, o);

@@ -278,6 +278,7 @@ struct SolverOptions {
   int workers = 1;     // setup-phase threads (reference knob)
   int cg_workers = 1;  // oracle-only: threads for per-subdomain CG work (1 = reference)
   int debug_flip_flux_row = -1;
+  bool layers_only = false;  // oracle-only: stop after the seeded layers (field evaluation)
 };
 
 struct CgResult {

@@ -139,11 +139,13 @@ struct CgArgs {
   const int* ndelta_map;   // N x dmax
   const int* cr_row;       // N x crmax
   const int* corner_q;     // N x 4
-  const int* own_gamma;    // 2 n_delta
-  const int* own_flux;
-  const int* own_nd;
-  const int* pi_owner;     // n_pi x 4 : (i * 4 + corner slot), subdomain order, -1 pad
-  const int* row_owner;    // npf x 4 : (i * crmax + rho)
+  // owner-slot destinations: every cross-subdomain sum is written by its producers into fixed
+  // slots and read back contiguously in a fixed (subdomain) order — one dependent load per gather
+  const int* gamma_dst;    // N x gmax : 2 g + s (slot s of Delta index g), -1 at corners
+  const int* flux_dst;     // N x fmax : 2 g + s for the weight-1 Delta flux rows, -1 otherwise
+  const int* nd_dst;       // N x dmax : 2 g + s for the Neumann Delta rows
+  const int* corner_dst;   // N x 4    : gp * 4 + slot, -1 pad
+  const int* cross_dst;    // N x crmax: rr * 4 + slot, -1 pad
   const double* flip_sign; // n_delta (+1 / -1 debug hook)
   const double* QtX;       // 2N x rmax x ext (QGt = cols 1.., qf = col 0)
   const double* Zc;        // N x crmax x gmax
@@ -157,13 +159,13 @@ struct CgArgs {
   int P;
   int rpc_max;    // largest rows-per-chunk of the streaming pipeline
   double* s;      // N x rmax
-  double* tpart;  // N x 4 (corner contributions of OP1)
-  double* tpart3; // P x N x 4 (corner contributions of OP3)
-  double* psipart;// N x crmax
-  double* o;      // N x gmax
-  double* xf;     // P x N x fmax
-  double* tr;     // P x N x dmax
-  double* zz;     // P x N x dmax
+  double* ttab;   // n_pi x 4    corner contributions of OP1 (owner slots)
+  double* ptab;   // npf x 4     cross-row contributions of OP1
+  double* t3tab;  // P x n_pi x 4 corner contributions of OP3
+  double* otab;   // 2 n_delta   OP4 outputs at the two owners of each Delta index
+  double* xtab;   // P x 2 n_delta  flux values x (OP2)
+  double* trtab;  // P x 2 n_delta  P x (NN1)
+  double* zztab;  // P x 2 n_delta  P^T P x (NN2)
   double* u;      // P x N x rmax
   double* pap;    // N : p . o_i
   // CG vectors

@@ -219,7 +219,7 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
     p.dmax = std::max(p.dmax, c.nd);
     p.tmax = std::max(p.tmax, static_cast<int>(c.tasks.size()));
   }
-  p.gmax = std::max(p.gmax, 1);
+  p.gmax = (std::max(p.gmax, 1) + 1) / 2 * 2;  // even: 16-byte aligned per-subdomain Zc blocks
   // flux / Cdelta row strides are even: 16-byte rows for the CG kernel's bulk copies
   p.fmax = (std::max(p.fmax, 1) + 1) / 2 * 2;
   p.dmax = (std::max(p.dmax, 1) + 1) / 2 * 2;

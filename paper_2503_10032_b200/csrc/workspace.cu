@@ -145,6 +145,30 @@ void Workspace::upload_plan() {
   d_own_gamma.upload(p.own_gamma, st_);
   d_own_flux.upload(p.own_flux, st_);
   d_own_nd.upload(p.own_nd, st_);
+  {
+    // owner-slot destinations (inverse of the owner lists): producers write their contribution
+    // to slot s of the quantity, readers sum the slots contiguously in the owner (subdomain) order
+    std::vector<int> gdst(static_cast<size_t>(N) * p.gmax, -1), fdst(static_cast<size_t>(N) * p.fmax, -1),
+        ndst(static_cast<size_t>(N) * p.dmax, -1), cdst(static_cast<size_t>(N) * 4, -1),
+        xdst(static_cast<size_t>(N) * p.crmax, -1);
+    for (int g = 0; g < p.n_delta; ++g)
+      for (int s = 0; s < 2; ++s) {
+        if (p.own_gamma[2 * g + s] >= 0) gdst[p.own_gamma[2 * g + s]] = 2 * g + s;
+        if (p.own_flux[2 * g + s] >= 0) fdst[p.own_flux[2 * g + s]] = 2 * g + s;
+        if (p.own_nd[2 * g + s] >= 0) ndst[p.own_nd[2 * g + s]] = 2 * g + s;
+      }
+    for (int gp = 0; gp < p.n_pi; ++gp)
+      for (int q = 0; q < 4; ++q)
+        if (pi_owner[static_cast<size_t>(gp) * 4 + q] >= 0) cdst[pi_owner[static_cast<size_t>(gp) * 4 + q]] = gp * 4 + q;
+    for (int rr = 0; rr < p.npf; ++rr)
+      for (int q = 0; q < 4; ++q)
+        if (row_owner[static_cast<size_t>(rr) * 4 + q] >= 0) xdst[row_owner[static_cast<size_t>(rr) * 4 + q]] = rr * 4 + q;
+    d_gamma_dst.upload(gdst, st_);
+    d_flux_dst.upload(fdst, st_);
+    d_nd_dst.upload(ndst, st_);
+    d_corner_dst.upload(cdst, st_);
+    d_cross_dst.upload(xdst, st_);
+  }
   d_mult_pi.upload(p.multiplicity_pi, st_);
   std::vector<double> flip(std::max(p.n_delta, 1), 1.0);
   if (p.debug_flip_flux_row >= 0 && p.debug_flip_flux_row < p.n_delta) flip[p.debug_flip_flux_row] = -1.0;
@@ -179,7 +203,7 @@ void Workspace::upload_plan() {
   d_b.alloc(static_cast<size_t>(N) * p.M);
   d_F.alloc(static_cast<size_t>(N) * p.M * p.fmax);
   d_Cd.alloc(static_cast<size_t>(N) * p.M * p.dmax);
-  d_Zc.alloc(static_cast<size_t>(N) * p.crmax * p.gmax);
+  d_Zc.alloc(static_cast<size_t>(N) * p.crmax * p.gmax + 2);  // +16 B: bulk-copy tail
   d_pd.alloc(static_cast<size_t>(N) * p.crmax);
   d_Gc.alloc(static_cast<size_t>(N) * 16);
   d_Ypi.alloc(static_cast<size_t>(N) * p.M * 4);
@@ -202,9 +226,12 @@ void Workspace::upload_plan() {
   d_pap.alloc(static_cast<size_t>(N));
   d_vin.alloc(nd);
   d_vout.alloc(nd);
-  d_tpart.alloc(static_cast<size_t>(N) * 4);
-  d_psipart.alloc(static_cast<size_t>(N) * p.crmax);
-  d_o.alloc(static_cast<size_t>(N) * p.gmax);
+  // owner-slot tables of the coarse gathers: unused slots stay zero
+  d_tpart.alloc(4 * npi);
+  d_psipart.alloc(4 * npf);
+  DDG_CUDA(cudaMemsetAsync(d_tpart.ptr, 0, d_tpart.count * sizeof(double), st_));
+  DDG_CUDA(cudaMemsetAsync(d_psipart.ptr, 0, d_psipart.count * sizeof(double), st_));
+  d_o.alloc(2 * nd);
   d_xf.alloc(static_cast<size_t>(N) * p.fmax);
   d_tr.alloc(static_cast<size_t>(N) * p.dmax);
   d_zz.alloc(static_cast<size_t>(N) * p.dmax);
@@ -539,12 +566,15 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
     int P = std::max(1, std::min(8, sms / p.N));
     if (const char* e = std::getenv("DDELM_CG_PARTS")) P = std::max(1, std::min(p.M, std::atoi(e)));
     a.P = P;
-    const size_t PP = P, N = p.N;
-    d_xf.alloc(PP * N * p.fmax);
-    d_tr.alloc(PP * N * p.dmax);
-    d_zz.alloc(PP * N * p.dmax);
+    const size_t PP = P, N = p.N, nd2 = 2 * static_cast<size_t>(std::max(p.n_delta, 1));
+    d_xf.alloc(PP * nd2);
+    d_tr.alloc(PP * nd2);
+    d_zz.alloc(PP * nd2);
     d_u.alloc(PP * N * rmax_);
-    d_tpart3.alloc(PP * N * 4);
+    if (d_tpart3.count != PP * 4 * std::max(p.n_pi, 1)) {
+      d_tpart3.alloc(PP * 4 * std::max(p.n_pi, 1));  // unused owner slots must read as zero
+      DDG_CUDA(cudaMemsetAsync(d_tpart3.ptr, 0, d_tpart3.count * sizeof(double), st_));
+    }
   }
   a.rel_tol = tol;
   a.max_iter = max_iter;
@@ -557,11 +587,11 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.ndelta_map = d_ndelta_map.ptr;
   a.cr_row = d_cr_row.ptr;
   a.corner_q = d_corner_q.ptr;
-  a.own_gamma = d_own_gamma.ptr;
-  a.own_flux = d_own_flux.ptr;
-  a.own_nd = d_own_nd.ptr;
-  a.pi_owner = d_pi_owner.ptr;
-  a.row_owner = d_row_owner.ptr;
+  a.gamma_dst = d_gamma_dst.ptr;
+  a.flux_dst = d_flux_dst.ptr;
+  a.nd_dst = d_nd_dst.ptr;
+  a.corner_dst = d_corner_dst.ptr;
+  a.cross_dst = d_cross_dst.ptr;
   a.flip_sign = d_flip.ptr;
   a.QtX = d_QtX.ptr;
   a.Zc = d_Zc.ptr;
@@ -571,13 +601,13 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.W3 = d_W3.ptr;
   a.dpi = d_dpi.ptr;
   a.s = d_s.ptr;
-  a.tpart = d_tpart.ptr;
-  a.tpart3 = d_tpart3.ptr;
-  a.psipart = d_psipart.ptr;
-  a.o = d_o.ptr;
-  a.xf = d_xf.ptr;
-  a.tr = d_tr.ptr;
-  a.zz = d_zz.ptr;
+  a.ttab = d_tpart.ptr;
+  a.t3tab = d_tpart3.ptr;
+  a.ptab = d_psipart.ptr;
+  a.otab = d_o.ptr;
+  a.xtab = d_xf.ptr;
+  a.trtab = d_tr.ptr;
+  a.zztab = d_zz.ptr;
   a.u = d_u.ptr;
   a.pap = d_pap.ptr;
   a.x = d_x.ptr;
@@ -594,7 +624,7 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.rpc_max = cg_rows_per_chunk_max(a);
   a.trace = nullptr;
   if (std::getenv("DDELM_CG_TRACE")) {
-    d_trace.alloc(148 * 4 * 16);
+    d_trace.alloc(148 * 4 * 32);
     a.trace = d_trace.ptr;
   }
   return a;
@@ -686,17 +716,20 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   if (a.trace) {
     // per-phase device timers of the CG job: max and mean over CTAs, microseconds per iteration
     const int G = cg_grid(a);
-    std::vector<double> t(static_cast<size_t>(G) * 16);
+    std::vector<double> t(static_cast<size_t>(G) * 32);
     DDG_CUDA(cudaMemcpy(t.data(), d_trace.ptr, t.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    static const char* names[16] = {"op1",  "sync1", "op2", "sync2", "nn1", "sync3", "nn2", "sync4",
-                                    "op3",  "sync5", "op4", "sync6", "xr",  "sync7", "fin", "-"};
+    static const char* names[32] = {"op1",     "sync1",   "op2",      "sync2",  "nn1",    "sync3",   "nn2", "sync4",
+                                    "op3",     "sync5",   "op4",      "sync6",  "xr",     "sync7",   "fin", "-",
+                                    "op4.gat", "op4.qtx", "op4.rows", "op4.s0", "op4.qs", "op4.out", "-",   "-",
+                                    "-",       "-",       "-",        "-",      "-",      "-",       "-",   "-"};
     std::fprintf(stderr, "[cg trace] %d iterations, G=%d, P=%d (us/iteration: max / mean over CTAs)\n",
                  res.iterations, G, a.P);
-    for (int k = 0; k < 15; ++k) {
+    for (int k = 0; k < 22; ++k) {
+      if (k == 15) continue;
       double mx = 0, mean = 0;
       for (int b = 0; b < G; ++b) {
-        mx = std::max(mx, t[b * 16 + k]);
-        mean += t[b * 16 + k] / G;
+        mx = std::max(mx, t[b * 32 + k]);
+        mean += t[b * 32 + k] / G;
       }
       const double it = std::max(res.iterations, 1);
       std::fprintf(stderr, "[cg trace] %-6s %8.2f %8.2f\n", names[k], mx / it / 1e3, mean / it / 1e3);

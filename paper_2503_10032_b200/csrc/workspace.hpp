@@ -117,7 +117,7 @@ class Workspace {
   DevBuf<Task> d_tasks;
   DevBuf<int> d_task_off, d_task_cnt, d_cls, d_ix, d_iy, d_gamma_delta, d_gamma_pi, d_fluxrow_delta,
       d_ndelta_map, d_cr_row, d_cr_off, d_cr_l, d_row_owner, d_pi_owner, d_own_gamma, d_own_flux,
-      d_own_nd, d_mult_pi;
+      d_own_nd, d_mult_pi, d_gamma_dst, d_flux_dst, d_nd_dst, d_corner_dst, d_cross_dst;
   DevBuf<ClassDims> d_dims;
   DevBuf<double> d_cr_w, d_flip, d_f;
   // layers and matrices

@@ -50,7 +50,9 @@ def check(name, detail=True, dump=None):
     ws, rep = P.solve_config(name, ws=ws)
     t2 = time.time()
     rk, rkb, ratio = ws.ranks()
-    u = oracle_ws(cfg).field(257, rep.coeffs)[0]
+    u = OracleWorkspace(problem=cfg["problem"], s=cfg["s"], n_grid=cfg["n_grid"], M=cfg["M"], l=cfg["l"],
+                        seed=cfg["seed"], flux_variant=cfg["flux_variant"], trace_basis=cfg["trace_basis"],
+                        layers_only=True).field(257, rep.coeffs)[0]
     out.update(iters=rep.iterations, golden_iters=int(g["iterations"]),
                spread_it=int(g["spread_iterations"]), converged=rep.converged,
                field_diff=field_rel_l2(u, g["field_u"], 257), spread_field=float(g["spread_field"]),
