@@ -22,19 +22,37 @@
 
 namespace ddg {
 
+thread_local Arena* g_arena = nullptr;
+
+/// Scope in which small DevBuf allocations come from the workspace arena.
+struct ArenaScope {
+  Arena* prev;
+  explicit ArenaScope(Arena* a) : prev(g_arena) { g_arena = a; }
+  ~ArenaScope() { g_arena = prev; }
+};
+
 template <typename T>
 void DevBuf<T>::alloc(size_t n) {
   if (n == count && ptr) return;
   free();
   count = n;
-  if (n) DDG_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+  if (!n) return;
+  if (g_arena != nullptr && n * sizeof(T) <= kArenaSmallBytes) {
+    if (void* p = g_arena->take(n * sizeof(T))) {
+      ptr = static_cast<T*>(p);
+      in_arena = true;
+      return;
+    }
+  }
+  DDG_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
 }
 
 template <typename T>
 void DevBuf<T>::free() {
-  if (ptr) cudaFree(ptr);
+  if (ptr && !in_arena) cudaFree(ptr);
   ptr = nullptr;
   count = 0;
+  in_arena = false;
 }
 
 template <typename T>
@@ -54,11 +72,41 @@ Workspace::Workspace(const Plan& p, int device) : plan(p), device_(device) {
   DDG_CUDA(cudaStreamCreateWithFlags(&cap_, cudaStreamNonBlocking));
   for (auto& e : ev_) DDG_CUDA(cudaEventCreate(&e));
   DDG_CUDA(cudaMallocHost(&pinned_state_, 64));
+  arena_.cap = size_t(64) << 20;
+  DDG_CUDA(cudaMalloc(reinterpret_cast<void**>(&arena_.base), arena_.cap));
   upload_plan();
+}
+
+void Workspace::apply_l2_policy() {
+  // persisting L2 window over the arena (index tables, coarse rows, CG vectors); skipped when
+  // the device offers no persisting carve-out (DDELM_NO_L2_PERSIST=1 disables it)
+  if (arena_.used == l2_window_bytes_ || std::getenv("DDELM_NO_L2_PERSIST")) return;
+  int max_persist = 0, max_window = 0;
+  DDG_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device_));
+  DDG_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device_));
+  if (max_persist <= 0 || max_window <= 0) return;
+  const size_t bytes = std::min<size_t>(arena_.used, static_cast<size_t>(max_window));
+  const size_t carve = std::min<size_t>(bytes, static_cast<size_t>(max_persist));
+  DDG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = arena_.base;
+  v.accessPolicyWindow.num_bytes = bytes;
+  v.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(carve) / static_cast<double>(bytes)));
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  DDG_CUDA(cudaStreamSetAttribute(st_, cudaStreamAttributeAccessPolicyWindow, &v));
+  l2_window_bytes_ = arena_.used;
 }
 
 Workspace::~Workspace() {
   cudaSetDevice(device_);
+  if (arena_.base) {
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st_, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+  }
+  // arena-backed DevBufs never free their pointers; release the arena itself last
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   for (auto& e : ev_) cudaEventDestroy(e);
@@ -83,6 +131,7 @@ void Workspace::upload_plan() {
   d_tasks.upload(tasks, st_);
   d_task_off.upload(off, st_);
   d_task_cnt.upload(cnt, st_);
+  ArenaScope hot(&arena_);  // index tables read by the interface iteration
   d_dims.upload(dims, st_);
   std::vector<int> cls(N), ix(N), iy(N);
   std::vector<int> gdel(static_cast<size_t>(N) * p.gmax, -1), gpi(static_cast<size_t>(N) * p.gmax, -1);
@@ -173,6 +222,7 @@ void Workspace::upload_plan() {
   std::vector<double> flip(std::max(p.n_delta, 1), 1.0);
   if (p.debug_flip_flux_row >= 0 && p.debug_flip_flux_row < p.n_delta) flip[p.debug_flip_flux_row] = -1.0;
   d_flip.upload(flip, st_);
+  g_arena = nullptr;  // setup-only / large buffers below
   d_f.upload(p.f, st_);
 
   // fixed-size device storage
@@ -188,7 +238,9 @@ void Workspace::upload_plan() {
   d_T.alloc(nmat * kQrTmax * kQrTmax);
   d_ratio.alloc(2 * nmat);
   d_deficient.alloc(nmat);
+  g_arena = &arena_;
   d_rank.alloc(nmat);
+  g_arena = nullptr;
   d_status.alloc(nmat);
   d_V1.alloc(nmat * kmax_ * p.M);
   d_F1.alloc(nmat * p.M * kmax_);
@@ -203,10 +255,13 @@ void Workspace::upload_plan() {
   d_b.alloc(static_cast<size_t>(N) * p.M);
   d_F.alloc(static_cast<size_t>(N) * p.M * p.fmax);
   d_Cd.alloc(static_cast<size_t>(N) * p.M * p.dmax);
+  g_arena = &arena_;
   d_Zc.alloc(static_cast<size_t>(N) * p.crmax * p.gmax + 2);  // +16 B: bulk-copy tail
+  g_arena = nullptr;
   d_pd.alloc(static_cast<size_t>(N) * p.crmax);
   d_Gc.alloc(static_cast<size_t>(N) * 16);
   d_Ypi.alloc(static_cast<size_t>(N) * p.M * 4);
+  g_arena = &arena_;  // coarse rows and CG vectors: hot
   d_corner_q.alloc(static_cast<size_t>(N) * 4);
   const size_t npf = std::max(p.npf, 1), npi = std::max(p.n_pi, 1);
   d_Dpp.alloc(npf * npi);
@@ -235,6 +290,7 @@ void Workspace::upload_plan() {
   d_xf.alloc(static_cast<size_t>(N) * p.fmax);
   d_tr.alloc(static_cast<size_t>(N) * p.dmax);
   d_zz.alloc(static_cast<size_t>(N) * p.dmax);
+  g_arena = nullptr;
   d_coeffs.alloc(static_cast<size_t>(N) * p.M);
   DDG_CUDA(cudaStreamSynchronize(st_));
 }
@@ -566,6 +622,7 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
     int P = std::max(1, std::min(8, sms / p.N));
     if (const char* e = std::getenv("DDELM_CG_PARTS")) P = std::max(1, std::min(p.M, std::atoi(e)));
     a.P = P;
+    ArenaScope hot(&arena_);
     const size_t PP = P, N = p.N, nd2 = 2 * static_cast<size_t>(std::max(p.n_delta, 1));
     d_xf.alloc(PP * nd2);
     d_tr.alloc(PP * nd2);
@@ -648,6 +705,7 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   SolveResult res;
   if (max_iter <= 0) max_iter = 20 * p.n_delta;
   if (p.n_delta == 0) throw std::invalid_argument("s = 1 (local-only solve) is not on the device path");
+  ArenaScope hot(&arena_);
   d_hist.alloc(static_cast<size_t>(max_iter));
   {
     // CG partial slots: one per CTA of the persistent kernel, one per block of cg_init
@@ -657,6 +715,7 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
     if (d_partial.count < need) d_partial.alloc(need);
   }
   CgArgs a = cg_args(theta, tol, max_iter);
+  apply_l2_policy();
   DDG_CUDA(cudaEventRecord(ev_[8], st_));
   cg_launch(a, kJobRhs, nullptr, d_rhs.ptr, st_);
   cg_launch_init(a, st_);
@@ -747,6 +806,7 @@ void Workspace::apply_operator(double theta, const double* v, double* out) {
   build_coarse();
   if (theta > 0.0) build_neumann();
   CgArgs a = cg_args(theta, 1e-9, 1);
+  apply_l2_policy();
   const size_t nd = plan.n_delta;
   DDG_CUDA(cudaMemcpyAsync(d_vin.ptr, v, nd * sizeof(double), cudaMemcpyHostToDevice, st_));
   cg_launch(a, kJobApply, d_vin.ptr, d_vout.ptr, st_);

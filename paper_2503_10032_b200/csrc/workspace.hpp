@@ -16,10 +16,31 @@ struct CapacityError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+/// Device arena for the small, hot buffers of the interface iteration (index tables, coarse
+/// rows, CG vectors): one contiguous range that an L2 access-policy window marks persisting, so
+/// the ~0.4 GB of coefficient blocks streamed per CG iteration cannot evict them.
+struct Arena {
+  ~Arena() {
+    if (base) cudaFree(base);
+  }
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+  void* take(size_t bytes) {
+    const size_t off = (used + 255) / 256 * 256;
+    if (base == nullptr || off + bytes > cap) return nullptr;
+    used = off + bytes;
+    return base + off;
+  }
+};
+/// Arena that DevBuf::alloc draws small requests from while set (Workspace scopes it).
+extern thread_local Arena* g_arena;
+constexpr size_t kArenaSmallBytes = size_t(8) << 20;
+
 template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t count = 0;
+  bool in_arena = false;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -101,6 +122,9 @@ class Workspace {
   bool layers_valid_ = false;
 
   int device_ = 0;
+  Arena arena_;
+  size_t l2_window_bytes_ = 0;
+  void apply_l2_policy();
   cudaStream_t st_ = nullptr, cap_ = nullptr;
   cudaEvent_t ev_[12] = {};
   cudaGraph_t graph_ = nullptr;
