@@ -202,6 +202,32 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def lsq_microbench(P, nblocks, device, reps=3):
+    """BASELINE config C5: nblocks fp64 blocks [K (3000 x 1000) | B (3000 x 200)] of tanh features,
+    batched Householder QR (B carried as appended columns: Q^T B) + Schur block S = B^T B -
+    (Q^T B)^T (Q^T B) on DMMA. Device-resident inputs (generated on the GPU), CUDA-event timed."""
+    m, n, k = 3000, 1000, 200
+    L = P.LsqBatch(nblocks, m, n, k, device)
+    L.generate(1, "tanh")
+    L.factor()  # warm-up
+    qr = sc = 0.0
+    for _ in range(reps):
+        L.generate(1, "tanh")
+        a, b = L.factor()
+        qr += a
+        sc += b
+    qr, sc = qr / reps, sc / reps
+    fl = L.flops_per_block() * nblocks
+    t = (qr + sc) / 1e3
+    tf = fl / t / 1e12
+    del L
+    return {"config": f"C5: {nblocks} blocks, K {m}x{n} + B {m}x{k}, tanh(w.x+b), fp64",
+            "blocks_per_s": nblocks / t, "ms_per_step": qr + sc, "qr_ms": qr, "schur_ms": sc,
+            "tflops": tf, "peak_tflops": FP64_PEAK_TFLOPS, "frac_fp64_peak": tf / FP64_PEAK_TFLOPS,
+            "flops_per_block": fl / nblocks,
+            "flop_model": "geqrf 2mn^2-2n^3/3 + Q^T B 4mnk-2n^2k + S 2(m-n)k^2 (SURVEY.md §8d)"}
+
+
 def workload_config(args, cfg):
     return {"workload": f"{args.config}: DDELM-NN (theta {cfg['theta']}) {cfg['s']}x{cfg['s']} subdomains, "
                         f"M={cfg['M']}, n_grid={cfg['n_grid']}, l={cfg['l']}, {cfg['problem']}, "
@@ -318,6 +344,9 @@ def run_ours(args, cfg, world, rank, local, dist):
                     "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["bytes"] else None}
                 for k, v in fam.items()}
 
+    lsq = None
+    if not args.no_lsq:
+        lsq = lsq_microbench(P, args.lsq_blocks, local)
     if rank != 0:
         return
     cpu = None
@@ -337,6 +366,7 @@ def run_ours(args, cfg, world, rank, local, dist):
             "roofline": roof, "kernel_families": families,
             "phase_ms": {k: round(v, 3) for k, v in rep.phase_ms.items()},
             "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
+            "fp64_lsq_microbench": lsq,
             "fp64_trailing_tflops": (qr["flops"] / (qr["ms"] / 1e3) / 1e12) if qr else None}
     print(json.dumps(line), flush=True)
 
@@ -350,6 +380,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--cpu-cg-iters", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-lsq", action="store_true", help="skip the C5 local-solve microbenchmark")
+    ap.add_argument("--lsq-blocks", type=int, default=1024)
     args = ap.parse_args()
     from paper_2503_10032_b200.configs import CONFIGS
 

@@ -128,6 +128,23 @@ int ddelm_gpu_get_phase_ms(ddelm_ws* ws, double* ms, int cap);
 /* Kernel launches issued by the last ddelm_gpu_build..solve sequence (own kernels only). */
 long long ddelm_gpu_get_launch_count(ddelm_ws* ws);
 
+/* ---- C5: batched local least-squares microbenchmark (BASELINE.json config 5).
+ * nblocks independent [K | B] blocks (m x n and m x k, column-major, ld = ddelm_gpu_lsq_ld),
+ * generated on the device (kind 0: tanh(w.x + b), w, b ~ U[-1,1], x ~ U[0,1]^2; kind 1: N(0,1)
+ * control) from a counter-based hash of (seed, block, index); factored with the batched
+ * Householder QR of LsFactor (solvers.cpp:24-45): R and the reflectors in place of K, Q^T B in
+ * place of B; then S = (Q^T B)_bot^T (Q^T B)_bot = B^T B - (Q^T B)_top^T (Q^T B)_top (k x k), the
+ * interface Schur block of assemble_coarse's products (solvers.cpp:286-321), on FP64 tensor cores.
+ * n must be even. */
+typedef struct ddelm_lsq ddelm_lsq;
+int ddelm_gpu_lsq_create(int nblocks, int m, int n, int k, int device, ddelm_lsq** out);
+int ddelm_gpu_lsq_generate(ddelm_lsq* lsq, uint64_t seed, int kind);
+int ddelm_gpu_lsq_factor(ddelm_lsq* lsq, double* qr_ms, double* schur_ms);
+/* A: ld x (n + k) factored block, tau: n Householder scalars, S: k x k (any may be NULL) */
+int ddelm_gpu_lsq_get_block(ddelm_lsq* lsq, int block, double* A, double* tau, double* S);
+int ddelm_gpu_lsq_ld(ddelm_lsq* lsq);
+void ddelm_gpu_lsq_destroy(ddelm_lsq* lsq);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,9 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_get_residuals", "ddelm_gpu_get_ranks", "ddelm_gpu_get_layer",
            "ddelm_gpu_get_local", "ddelm_gpu_apply_operator", "ddelm_gpu_invalidate",
            "ddelm_gpu_stream", "ddelm_gpu_set_profiling", "ddelm_gpu_get_kernel_stats",
-           "ddelm_gpu_get_device_span_ms", "ddelm_gpu_get_phase_ms", "ddelm_gpu_get_launch_count")
+           "ddelm_gpu_get_device_span_ms", "ddelm_gpu_get_phase_ms", "ddelm_gpu_get_launch_count",
+           "ddelm_gpu_lsq_create", "ddelm_gpu_lsq_generate", "ddelm_gpu_lsq_factor",
+           "ddelm_gpu_lsq_get_block", "ddelm_gpu_lsq_ld", "ddelm_gpu_lsq_destroy")
 
 
 class _Desc(C.Structure):
@@ -95,6 +97,12 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_get_phase_ms.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
     L.ddelm_gpu_get_launch_count.argtypes = [C.c_void_p]
     L.ddelm_gpu_get_launch_count.restype = C.c_longlong
+    L.ddelm_gpu_lsq_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+    L.ddelm_gpu_lsq_generate.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
+    L.ddelm_gpu_lsq_factor.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.ddelm_gpu_lsq_get_block.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_lsq_ld.argtypes = [C.c_void_p]
+    L.ddelm_gpu_lsq_destroy.argtypes = [C.c_void_p]
     _lib = L
     return L
 
@@ -301,6 +309,45 @@ def ddelm_nn_solve(ws: Workspace, theta: float, cg: CgOptions | None = None) -> 
 def ddelm_solve(ws: Workspace, cg: CgOptions | None = None) -> SolveReport:
     """One-level DDELM (solvers.cpp:493-531) — SURVEY.md §8f 'next'; not on the device path yet."""
     raise NotImplementedError("ddelm (one-level) is a §8f 'next' row; use ddelm_cs_solve / ddelm_nn_solve")
+
+
+class LsqBatch:
+    """C5 microbenchmark: batched local least squares (QR of [K | B]) + interface Schur block S
+    (include/ddelm_gpu.h, ddelm_gpu_lsq_*). Flops per block follow SURVEY.md §8d."""
+
+    def __init__(self, nblocks: int, m: int, n: int, k: int, device: int = 0):
+        L = load_library()
+        h = C.c_void_p()
+        _check(L.ddelm_gpu_lsq_create(nblocks, m, n, k, device, C.byref(h)))
+        self._h = h
+        self.nblocks, self.m, self.n, self.k = nblocks, m, n, k
+        self.ld = int(L.ddelm_gpu_lsq_ld(h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            load_library().ddelm_gpu_lsq_destroy(h)
+            self._h = None
+
+    def generate(self, seed: int = 1, kind: str = "tanh"):
+        _check(load_library().ddelm_gpu_lsq_generate(self._h, seed, {"tanh": 0, "gaussian": 1}[kind]))
+
+    def factor(self) -> tuple[float, float]:
+        qr, sc = C.c_double(), C.c_double()
+        _check(load_library().ddelm_gpu_lsq_factor(self._h, C.byref(qr), C.byref(sc)))
+        return qr.value, sc.value
+
+    def block(self, b: int):
+        """(A (ld x (n+k)) column-major as an (n+k, ld) array transposed, tau (n), S (k x k))."""
+        A = np.zeros((self.n + self.k, self.ld))
+        tau = np.zeros(self.n)
+        S = np.zeros((self.k, self.k))
+        _check(load_library().ddelm_gpu_lsq_get_block(self._h, b, _ptr(A), _ptr(tau), _ptr(S)))
+        return A.T[: self.m].copy(), tau, S
+
+    def flops_per_block(self) -> float:
+        m, n, k = self.m, self.n, self.k
+        return (2.0 * m * n * n - 2.0 * n ** 3 / 3.0) + (4.0 * m * n * k - 2.0 * n * n * k) + 2.0 * (m - n) * k * k
 
 
 def workspace_from_config(name_or_cfg, device: int = 0) -> Workspace:

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 
@@ -14,6 +15,25 @@
 struct ddelm_ws {
   ddg::Workspace* w = nullptr;
   ddelm_report last{};
+};
+
+/// C5 batched least-squares microbenchmark state (k_lsq.cu + k_qr.cu).
+struct ddelm_lsq {
+  int device = 0;
+  ddg::LsqArgs a{};
+  double *tau = nullptr, *T = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[3] = {};
+  ~ddelm_lsq() {
+    cudaSetDevice(device);
+    cudaFree(a.A);
+    cudaFree(a.S);
+    cudaFree(tau);
+    cudaFree(T);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  }
 };
 
 namespace {
@@ -180,5 +200,85 @@ int ddelm_gpu_get_phase_ms(ddelm_ws* ws, double* ms, int cap) {
   return n;
 }
 long long ddelm_gpu_get_launch_count(ddelm_ws* ws) { return ws->w->launches(); }
+
+
+int ddelm_gpu_lsq_create(int nblocks, int m, int n, int k, int device, ddelm_lsq** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("ddelm_gpu_lsq_create: null argument");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw ddg::CudaError("ddelm_gpu_lsq_create: no CUDA device available (no CPU fallback)");
+    if (nblocks < 1 || n < 1 || k < 1 || m < n || (n % 2) || device < 0 || device >= ndev)
+      throw std::invalid_argument("ddelm_gpu_lsq_create: need nblocks >= 1, m >= n >= 1 (n even), k >= 1");
+    auto* L = new ddelm_lsq;
+    std::unique_ptr<ddelm_lsq> guard(L);
+    L->device = device;
+    DDG_CUDA(cudaSetDevice(device));
+    DDG_CUDA(cudaStreamCreateWithFlags(&L->st, cudaStreamNonBlocking));
+    for (auto& e : L->ev) DDG_CUDA(cudaEventCreate(&e));
+    L->a = ddg::LsqArgs{nblocks, m, n, k, (m + 3) / 4 * 4, n + k, nullptr, nullptr};
+    const size_t nA = static_cast<size_t>(nblocks) * L->a.ld * L->a.ncol;
+    DDG_CUDA(cudaMalloc(&L->a.A, nA * sizeof(double)));
+    DDG_CUDA(cudaMemsetAsync(L->a.A, 0, nA * sizeof(double), L->st));
+    DDG_CUDA(cudaMalloc(&L->a.S, static_cast<size_t>(nblocks) * k * k * sizeof(double)));
+    DDG_CUDA(cudaMalloc(&L->tau, static_cast<size_t>(nblocks) * n * sizeof(double)));
+    DDG_CUDA(cudaMalloc(&L->T, static_cast<size_t>(nblocks) * ddg::kQrTmax * ddg::kQrTmax * sizeof(double)));
+    DDG_CUDA(cudaStreamSynchronize(L->st));
+    *out = guard.release();
+  });
+}
+
+int ddelm_gpu_lsq_generate(ddelm_lsq* L, uint64_t seed, int kind) {
+  return guarded([&] {
+    if (!L || kind < 0 || kind > 1) throw std::invalid_argument("ddelm_gpu_lsq_generate: bad argument");
+    DDG_CUDA(cudaSetDevice(L->device));
+    ddg::launch_lsq_generate(L->a, seed, kind, L->st);
+    DDG_CUDA(cudaStreamSynchronize(L->st));
+  });
+}
+
+int ddelm_gpu_lsq_factor(ddelm_lsq* L, double* qr_ms, double* schur_ms) {
+  return guarded([&] {
+    if (!L) throw std::invalid_argument("ddelm_gpu_lsq_factor: null handle");
+    DDG_CUDA(cudaSetDevice(L->device));
+    const ddg::LsqArgs& a = L->a;
+    ddg::QrArgs q{a.nb, a.m, a.ld, a.ncol, a.n, a.A, L->tau, L->T};
+    DDG_CUDA(cudaEventRecord(L->ev[0], L->st));
+    for (int k0 = 0; k0 < a.n; k0 += ddg::kQrNB) {
+      ddg::launch_qr_panel(q, k0, L->st);
+      ddg::launch_qr_trailing(q, k0, L->st);
+    }
+    DDG_CUDA(cudaEventRecord(L->ev[1], L->st));
+    ddg::launch_lsq_gram(a, L->st);
+    DDG_CUDA(cudaEventRecord(L->ev[2], L->st));
+    DDG_CUDA(cudaStreamSynchronize(L->st));
+    float t0 = 0, t1 = 0;
+    DDG_CUDA(cudaEventElapsedTime(&t0, L->ev[0], L->ev[1]));
+    DDG_CUDA(cudaEventElapsedTime(&t1, L->ev[1], L->ev[2]));
+    if (qr_ms) *qr_ms = t0;
+    if (schur_ms) *schur_ms = t1;
+  });
+}
+
+int ddelm_gpu_lsq_get_block(ddelm_lsq* L, int b, double* A, double* tau, double* S) {
+  return guarded([&] {
+    if (!L || b < 0 || b >= L->a.nb) throw std::invalid_argument("ddelm_gpu_lsq_get_block: bad block");
+    DDG_CUDA(cudaSetDevice(L->device));
+    const ddg::LsqArgs& a = L->a;
+    if (A)
+      DDG_CUDA(cudaMemcpy(A, a.A + static_cast<size_t>(b) * a.ld * a.ncol,
+                          static_cast<size_t>(a.ld) * a.ncol * sizeof(double), cudaMemcpyDeviceToHost));
+    if (tau)
+      DDG_CUDA(cudaMemcpy(tau, L->tau + static_cast<size_t>(b) * a.n, a.n * sizeof(double), cudaMemcpyDeviceToHost));
+    if (S)
+      DDG_CUDA(cudaMemcpy(S, a.S + static_cast<size_t>(b) * a.k * a.k, static_cast<size_t>(a.k) * a.k * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+  });
+}
+
+int ddelm_gpu_lsq_ld(ddelm_lsq* L) { return L ? L->a.ld : 0; }
+
+void ddelm_gpu_lsq_destroy(ddelm_lsq* L) { delete L; }
 
 }  // extern "C"

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include "plan.hpp"
 
 namespace ddg {
@@ -113,6 +115,15 @@ void launch_coarse_schur(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_weights(const BlockArgs& a, cudaStream_t st);
 /// Pack the CG stream blocks KF = [C | Ypi | F] and KD = [Cbar | Cdelta] (row-interleaved).
 void launch_pack_streams(const BlockArgs& a, double* KF, int ldKF, double* KD, int ldKD, cudaStream_t st);
+
+// ---------------------------------------------------------------- C5 microbenchmark (k_lsq.cu)
+struct LsqArgs {
+  int nb, m, n, k, ld, ncol;  // ncol = n + k
+  double* A;                  // nb x ld x ncol column-major: [K | B], factored in place
+  double* S;                  // nb x k x k
+};
+void launch_lsq_generate(const LsqArgs& a, uint64_t seed, int kind, cudaStream_t st);  // kind 0 tanh, 1 N(0,1)
+void launch_lsq_gram(const LsqArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- CG (k_cg.cu)
 enum CgJob { kJobCg = 0, kJobApply = 1, kJobRhs = 2, kJobRecon = 3 };
