@@ -245,10 +245,7 @@ int ddelm_gpu_lsq_factor(ddelm_lsq* L, double* qr_ms, double* schur_ms) {
     const ddg::LsqArgs& a = L->a;
     ddg::QrArgs q{a.nb, a.m, a.ld, a.ncol, a.n, a.A, L->tau, L->T};
     DDG_CUDA(cudaEventRecord(L->ev[0], L->st));
-    for (int k0 = 0; k0 < a.n; k0 += ddg::kQrNB) {
-      ddg::launch_qr_panel(q, k0, L->st);
-      ddg::launch_qr_trailing(q, k0, L->st);
-    }
+    for (const ddg::QrOp& op : ddg::qr_schedule(a.n, a.ncol)) ddg::launch_qr_op(q, op, L->st);
     DDG_CUDA(cudaEventRecord(L->ev[1], L->st));
     ddg::launch_lsq_gram(a, L->st);
     DDG_CUDA(cudaEventRecord(L->ev[2], L->st));

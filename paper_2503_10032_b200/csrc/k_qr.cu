@@ -11,7 +11,10 @@
 //                 tcgen05.mma has no f64 kind on sm_100a.
 // The appended columns [f | E] ride along in the trailing updates, so the factorisation also
 // produces Q0^T [f | E] (the interface rows of Q and Q^T f) with no extra pass.
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -93,7 +96,7 @@ __device__ __forceinline__ void panel_pass(double* P, size_t ld, int m, int rlo,
   (void)n2;
 }
 
-__global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, int k0) {
+__global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, int k0, int toff) {
   const int t = blockIdx.x;
   double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
   const int m = a.m;
@@ -221,7 +224,61 @@ __global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, in
   __syncthreads();
   double* T = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
   for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x)
-    T[(idx >> 5) * kQrTmax + (idx & 31)] = Tsh[idx >> 5][idx & 31];
+    T[(toff + (idx >> 5)) * kQrTmax + toff + (idx & 31)] = Tsh[idx >> 5][idx & 31];
+  if (toff == 0) return;
+  // ---- second half of a 64-wide block: T12 = -T1 (V1^T V2) T2, V1 = the 32 reflectors left of k0
+  //      (rows >= k0 only: V2 is zero above its diagonal)
+  const double* V1 = A + static_cast<size_t>(k0 - NB) * ld;
+  g0 = g1 = 0;
+  for (int r0 = k0; r0 < m; r0 += RC) {
+    for (int idx = threadIdx.x; idx < RC * NB; idx += blockDim.x) {
+      const int rr = idx & 31, uu = idx >> 5;
+      const int row = r0 + rr;
+      double v2 = 0;
+      if (row < m && uu < nb) {
+        if (row == k0 + uu) v2 = 1.0;
+        else if (row > k0 + uu) v2 = P[static_cast<size_t>(uu) * ld + row];
+      }
+      Vs[rr][uu] = v2;
+      G[rr][uu] = row < m ? V1[static_cast<size_t>(uu) * ld + row] : 0.0;  // V1 rows >= k0 (below its diagonal)
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < RC; ++rr) {
+      g0 += G[rr][u] * Vs[rr][v];       // (V1^T V2)(u, v)
+      g1 += G[rr][u] * Vs[rr][v + 16];
+    }
+    __syncthreads();
+  }
+  // Tsh <- G12 ; then T12 = -T1 G12 T2 (T1 from global, T2 = this panel's T in Tsh -> keep a copy)
+  __shared__ double T2s[NB][NB + 1];
+  for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x) T2s[idx >> 5][idx & 31] = Tsh[idx >> 5][idx & 31];
+  __syncthreads();
+  Vs[u][v] = g0;  // reuse Vs as G12
+  Vs[u][v + 16] = g1;
+  for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x)
+    G[idx >> 5][idx & 31] = T[(idx >> 5) * kQrTmax + (idx & 31)];  // T1 (rows/cols 0..31)
+  __syncthreads();
+  // X = G12 T2 (thread -> two entries)
+  double x0 = 0, x1 = 0;
+  for (int w = 0; w < NB; ++w) {
+    x0 += Vs[u][w] * T2s[w][v];
+    x1 += Vs[u][w] * T2s[w][v + 16];
+  }
+  __syncthreads();
+  Tsh[u][v] = x0;
+  Tsh[u][v + 16] = x1;
+  __syncthreads();
+  double y0 = 0, y1 = 0;
+  for (int w = 0; w < NB; ++w) {
+    y0 += G[u][w] * Tsh[w][v];
+    y1 += G[u][w] * Tsh[w][v + 16];
+  }
+  T[u * kQrTmax + NB + v] = -y0;
+  T[u * kQrTmax + NB + v + 16] = -y1;
+  // T21 block (lower left) is zero: T is upper triangular
+  T[(NB + u) * kQrTmax + v] = 0.0;
+  T[(NB + u) * kQrTmax + v + 16] = 0.0;
 }
 
 // ---------------------------------------------------------------- trailing update (DMMA)
@@ -258,16 +315,16 @@ struct TrailSmem {
 };
 
 template <int NB_>
-__global__ void __launch_bounds__(256, 2) qr_trailing_kernel(QrArgs a, int k0) {
+__global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrArgs a, int k0, int nbw, int cb, int ce) {
   static_assert(NB_ == 32 || NB_ == 64, "panel width");
   constexpr int MT = NB_ / 8;  // m-tiles of W
   extern __shared__ __align__(16) double smraw[];
   TrailSmem<NB_>& S = *reinterpret_cast<TrailSmem<NB_>*>(smraw);
   const int t = blockIdx.y;
-  const int nb = min(NB_, a.M - k0);
-  const int c0 = k0 + nb + blockIdx.x * TN;
-  if (c0 >= a.ncol) return;
-  const int ncols = min(TN, a.ncol - c0);
+  const int nb = nbw;  // reflectors k0 .. k0 + nb - 1 (nb <= NB_)
+  const int c0 = cb + blockIdx.x * TN;
+  if (c0 >= ce) return;
+  const int ncols = min(TN, ce - c0);
   double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
   const size_t ld = a.ld;
   const int nq = (a.m - k0 + RC - 1) / RC;  // chunks per pass
@@ -465,25 +522,67 @@ __global__ void qr_diag_ratio_kernel(QrArgs a, double* ratio) {
 
 }  // namespace
 
-void launch_qr_panel(const QrArgs& a, int k0, cudaStream_t st) {
-  qr_panel_kernel<<<a.nmat, kPanelThreads, 0, st>>>(a, k0);
+std::vector<QrOp> qr_schedule(int M, int ncol) {
+  // 64-wide blocks: panel (32) -> update the right 32 panel columns -> panel (32, + T12) ->
+  // 64-wide trailing update of the rest; a block of at most 32 columns is a plain 32 step
+  std::vector<QrOp> ops;
+  const char* e = std::getenv("DDELM_QR_NB");
+  // 32-wide blocking by default: measured faster than the recursive 64-wide blocks on B200 (the
+  // 64-wide DMMA tile needs 180 KB of staging -> 1 CTA / SM); DDELM_QR_NB=64 selects them
+  const int bw = (e && std::atoi(e) == 64) ? 64 : NB;
+  for (int k0 = 0; k0 < M; k0 += bw) {
+    const int w = std::min(bw, M - k0);
+    if (w <= NB) {
+      ops.push_back({QrOp::kPanel, k0, 0, 0, 0, 0});
+      ops.push_back({QrOp::kTrail32, k0, w, k0 + w, ncol, 0});
+      continue;
+    }
+    ops.push_back({QrOp::kPanel, k0, 0, 0, 0, 0});
+    ops.push_back({QrOp::kTrail32, k0, NB, k0 + NB, k0 + w, 0});
+    ops.push_back({QrOp::kPanel, k0 + NB, 0, 0, 0, NB});
+    ops.push_back({QrOp::kTrail64, k0, w, k0 + w, ncol, 0});
+  }
+  return ops;
+}
+
+void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
+  if (op.kind == QrOp::kPanel) {
+    qr_panel_kernel<<<a.nmat, kPanelThreads, 0, st>>>(a, op.k0, op.toff);
+    DDG_LAUNCH_CHECK();
+    return;
+  }
+  const int rest = op.ce - op.cb;
+  if (rest <= 0) return;
+  dim3 grid(ceil_div(rest, TN), a.nmat);
+  if (op.kind == QrOp::kTrail32) {
+    const size_t smem = sizeof(TrailSmem<32>);
+    static bool attr = false;
+    if (!attr) {
+      DDG_CUDA(cudaFuncSetAttribute(qr_trailing_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      attr = true;
+    }
+    qr_trailing_kernel<32><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce);
+  } else {
+    const size_t smem = sizeof(TrailSmem<64>);
+    static bool attr = false;
+    if (!attr) {
+      DDG_CUDA(cudaFuncSetAttribute(qr_trailing_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      attr = true;
+    }
+    qr_trailing_kernel<64><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce);
+  }
   DDG_LAUNCH_CHECK();
 }
 
-void launch_qr_trailing(const QrArgs& a, int k0, cudaStream_t st) {
-  const int nb = std::min(NB, a.M - k0);
-  const int rest = a.ncol - (k0 + nb);
-  if (rest <= 0) return;
-  dim3 grid(ceil_div(rest, TN), a.nmat);
-  const size_t smem = sizeof(TrailSmem<NB>);
-  static bool attr = false;
-  if (!attr) {
-    DDG_CUDA(cudaFuncSetAttribute(qr_trailing_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    attr = true;
+double qr_op_flops(const QrArgs& a, const QrOp& op) {
+  const double mrows = a.m - op.k0;
+  if (op.kind == QrOp::kPanel) {
+    const double nb = std::min(NB, a.M - op.k0);
+    return a.nmat * 2.0 * mrows * nb * nb;
   }
-  qr_trailing_kernel<NB><<<grid, 256, smem, st>>>(a, k0);
-  DDG_LAUNCH_CHECK();
+  return a.nmat * 4.0 * mrows * op.nbw * std::max(0, op.ce - op.cb);  // W = V^T A, A -= V (T^T W)
 }
 
 void launch_qr_diag_ratio(const QrArgs& a, double* ratio, cudaStream_t st) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "plan.hpp"
 
@@ -42,8 +43,16 @@ struct QrArgs {
 };
 constexpr int kQrNB = 32;
 constexpr int kQrTmax = 64;
-void launch_qr_panel(const QrArgs& a, int k0, cudaStream_t st);
-void launch_qr_trailing(const QrArgs& a, int k0, cudaStream_t st);
+/// One step of the blocked factorisation: a 32-column panel (toff = 32: second half of a 64-wide
+/// block, also forms the coupling block of the 64 x 64 T), or a DMMA trailing update with the
+/// nbw reflectors starting at k0 applied to columns [cb, ce).
+struct QrOp {
+  enum Kind { kPanel, kTrail32, kTrail64 } kind;
+  int k0, nbw, cb, ce, toff;
+};
+std::vector<QrOp> qr_schedule(int M, int ncol);
+void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st);
+double qr_op_flops(const QrArgs& a, const QrOp& op);
 /// |R_ii| min / max per matrix -> ratio (branch test of LsFactor, solvers.cpp:27-32)
 void launch_qr_diag_ratio(const QrArgs& a, double* ratio, cudaStream_t st);
 

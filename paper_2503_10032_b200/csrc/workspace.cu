@@ -446,7 +446,6 @@ void Workspace::build() {
   const auto h0 = std::chrono::steady_clock::now();
   if (!layers_valid_) init_layers();
   DDG_CUDA(cudaEventRecord(ev_[0], st_));
-  const double nmat_d = 2.0 * p.N;
   int kt = ktimer_begin();
   launch_build_features(feature_args(), st_);
   // algorithmic bytes: every generated matrix entry written once (SURVEY.md §8d B_feat)
@@ -454,17 +453,11 @@ void Workspace::build() {
   launches_ += 2;
   DDG_CUDA(cudaEventRecord(ev_[1], st_));
   QrArgs q{2 * p.N, p.m, ld_, ncol_, p.M, d_A.ptr, d_tau.ptr, d_T.ptr};
-  for (int k0 = 0; k0 < p.M; k0 += kQrNB) {
-    const int nb = std::min(kQrNB, p.M - k0);
-    const double mrows = p.m - k0;
+  for (const QrOp& op : qr_schedule(p.M, ncol_)) {
     kt = ktimer_begin();
-    launch_qr_panel(q, k0, st_);
-    ktimer_end(kt, "qr_panel", nmat_d * (4.0 * mrows * nb * nb / 2.0), 0.0);
-    kt = ktimer_begin();
-    launch_qr_trailing(q, k0, st_);
-    // two GEMMs of the compact-WY update: W = V^T A and A -= V (T^T W)
-    ktimer_end(kt, "qr_trailing", nmat_d * 4.0 * mrows * nb * std::max(0, ncol_ - k0 - nb), 0.0);
-    launches_ += (ncol_ - std::min(k0 + kQrNB, p.M) > 0) ? 2 : 1;
+    launch_qr_op(q, op, st_);
+    ktimer_end(kt, op.kind == QrOp::kPanel ? "qr_panel" : "qr_trailing", qr_op_flops(q, op), 0.0);
+    launches_ += (op.kind == QrOp::kPanel || op.ce > op.cb) ? 1 : 0;
   }
   launch_qr_diag_ratio(q, d_ratio.ptr, st_);
   launches_ += 1;
