@@ -85,6 +85,21 @@ const char* ddelm_gpu_last_error(void);
 const char* ddelm_gpu_version(void);
 
 int ddelm_gpu_create(const ddelm_desc* desc, ddelm_ws** out);
+/* Sharded workspace (one process per GPU): rank `rank` of `world` owns the contiguous strip of
+ * subdomains ddelm_gpu_get_shard reports and factorises only those; the coarse problem and the
+ * interface vectors are replicated; the owner-slot tables of every cross-subdomain sum are
+ * all-reduced over NCCL (nccl_id: 128 bytes from ddelm_gpu_nccl_unique_id on rank 0, broadcast
+ * by the caller). world = 1 runs the same phase-by-phase path on one device (nccl_id unused).
+ * Coefficients / ranks / layers returned by the getters are those of the local strip. */
+int ddelm_gpu_nccl_unique_id(unsigned char* nccl_id /* 128 bytes */);
+int ddelm_gpu_create_sharded(const ddelm_desc* desc, int rank, int world, const unsigned char* nccl_id,
+                             ddelm_ws** out);
+int ddelm_gpu_get_shard(ddelm_ws* ws, int* sub_lo, int* sub_count, int* n_global);
+/* Host-only view of a shard's owner-slot tables (no device needed): which = 0 gamma, 1 flux,
+ * 2 Neumann, 3 corner, 4 cross-row destinations of the local strip, 5 = {sub_lo, N_local,
+ * N_global, n_delta, n_pi, npf, gmax, fmax, dmax, crmax}. Returns the table length (copies at
+ * most cap entries into out), or -error. */
+int ddelm_gpu_plan_tables(const ddelm_desc* desc, int rank, int world, int which, int* out, int cap);
 int ddelm_gpu_build(ddelm_ws* ws);
 int ddelm_gpu_build_coarse(ddelm_ws* ws);
 int ddelm_gpu_build_neumann(ddelm_ws* ws);

@@ -38,7 +38,9 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_stream", "ddelm_gpu_set_profiling", "ddelm_gpu_get_kernel_stats",
            "ddelm_gpu_get_device_span_ms", "ddelm_gpu_get_phase_ms", "ddelm_gpu_get_launch_count",
            "ddelm_gpu_lsq_create", "ddelm_gpu_lsq_generate", "ddelm_gpu_lsq_factor",
-           "ddelm_gpu_lsq_get_block", "ddelm_gpu_lsq_ld", "ddelm_gpu_lsq_destroy")
+           "ddelm_gpu_lsq_get_block", "ddelm_gpu_lsq_ld", "ddelm_gpu_lsq_destroy",
+           "ddelm_gpu_nccl_unique_id", "ddelm_gpu_create_sharded", "ddelm_gpu_get_shard",
+           "ddelm_gpu_plan_tables")
 
 
 class _Desc(C.Structure):
@@ -103,6 +105,10 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_lsq_get_block.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_lsq_ld.argtypes = [C.c_void_p]
     L.ddelm_gpu_lsq_destroy.argtypes = [C.c_void_p]
+    L.ddelm_gpu_nccl_unique_id.argtypes = [C.c_void_p]
+    L.ddelm_gpu_create_sharded.argtypes = [C.POINTER(_Desc), C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+    L.ddelm_gpu_get_shard.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.ddelm_gpu_plan_tables.argtypes = [C.POINTER(_Desc), C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int]
     _lib = L
     return L
 
@@ -172,11 +178,46 @@ class SolveReport:
     launches: int = 0
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for a sharded workspace (rank 0 creates it, the caller broadcasts it)."""
+    buf = (C.c_ubyte * 128)()
+    _check(load_library().ddelm_gpu_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def plan_tables(cfg, rank: int, world: int) -> dict:
+    """Host-side owner-slot tables of one shard (no GPU needed): the sharding logic under test."""
+    L = load_library()
+    d = _Desc(PROBLEMS[cfg["problem"]], cfg["s"], cfg["n_grid"], cfg["M"], float(cfg["l"]), cfg["seed"],
+              1 if cfg["flux_variant"] == "mean_edge" else 0,
+              1 if cfg["trace_basis"] == "change_of_variables" else 0, 1e-10, 0, -1)
+    out = {}
+    for which, name in enumerate(["gamma_dst", "flux_dst", "nd_dst", "corner_dst", "cross_dst", "meta"]):
+        n = L.ddelm_gpu_plan_tables(C.byref(d), rank, world, which, None, 0)
+        if n < 0:
+            _check(-n)
+        a = np.zeros(max(n, 1), dtype=np.int32)
+        L.ddelm_gpu_plan_tables(C.byref(d), rank, world, which, _ptr(a), n)
+        out[name] = a[:n]
+    keys = ["sub_lo", "n_local", "n_global", "n_delta", "n_pi", "npf", "gmax", "fmax", "dmax", "crmax"]
+    out.update({k: int(v) for k, v in zip(keys, out.pop("meta"))})
+    return out
+
+
+def shard_range(n_subs: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous strip [lo, hi) of subdomains owned by `rank` (plan.cpp shard_range)."""
+    return n_subs * rank // world, n_subs * (rank + 1) // world
+
+
 class Workspace:
-    """Device-resident Workspace (solvers.hpp:78-160) on one B200."""
+    """Device-resident Workspace (solvers.hpp:78-160) on one B200.
+
+    shard=(rank, world, nccl_id) builds a sharded workspace: this process/GPU owns the strip
+    shard_range(s*s, rank, world) of subdomains; interface vectors and the coarse problem are
+    replicated and every cross-subdomain sum is an NCCL all-reduce of owner-slot tables."""
 
     def __init__(self, problem: ProblemSpec | str, s: int, n_grid: int, M: int, l: float, seed: int,
-                 opts: SolverOptions | None = None, device: int = 0):
+                 opts: SolverOptions | None = None, device: int = 0, shard: tuple | None = None):
         L = load_library()
         if isinstance(problem, str):
             problem = make_problem(problem)
@@ -187,11 +228,19 @@ class Workspace:
                   1 if opts.flux_variant == "mean_edge" else 0, 1 if opts.change_of_variables else 0,
                   float(opts.rank_tol), device, int(opts.debug_flip_flux_row))
         h = C.c_void_p()
-        _check(L.ddelm_gpu_create(C.byref(d), C.byref(h)))
+        if shard is None:
+            _check(L.ddelm_gpu_create(C.byref(d), C.byref(h)))
+        else:
+            rank, world, nid = shard
+            idbuf = (C.c_ubyte * 128).from_buffer_copy(nid) if nid is not None else None
+            _check(L.ddelm_gpu_create_sharded(C.byref(d), int(rank), int(world), idbuf, C.byref(h)))
         self._h = h
         self.problem, self.s, self.n_grid, self.M, self.l, self.seed = problem, s, n_grid, M, l, seed
         self.opts = opts
-        self.n_subs = s * s
+        lo, cnt, ng = C.c_int(), C.c_int(), C.c_int()
+        _check(L.ddelm_gpu_get_shard(h, C.byref(lo), C.byref(cnt), C.byref(ng)))
+        self.sub_lo, self.n_local, self.n_global = lo.value, cnt.value, ng.value
+        self.n_subs = cnt.value
         self.n_delta = 2 * s * (s - 1) * (n_grid - 2)
         self.n_pi = (s - 1) * (s - 1)
 
@@ -350,11 +399,12 @@ class LsqBatch:
         return (2.0 * m * n * n - 2.0 * n ** 3 / 3.0) + (4.0 * m * n * k - 2.0 * n * n * k) + 2.0 * (m - n) * k * k
 
 
-def workspace_from_config(name_or_cfg, device: int = 0) -> Workspace:
+def workspace_from_config(name_or_cfg, device: int = 0, shard: tuple | None = None) -> Workspace:
     cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
     opts = SolverOptions(flux_variant=cfg["flux_variant"],
                          change_of_variables=cfg["trace_basis"] == "change_of_variables")
-    return Workspace(cfg["problem"], cfg["s"], cfg["n_grid"], cfg["M"], cfg["l"], cfg["seed"], opts, device)
+    return Workspace(cfg["problem"], cfg["s"], cfg["n_grid"], cfg["M"], cfg["l"], cfg["seed"], opts, device,
+                     shard)
 
 
 def solve_config(name_or_cfg, device: int = 0, ws: Workspace | None = None) -> tuple[Workspace, SolveReport]:

@@ -2,6 +2,7 @@
 // point fails with DDELM_ERR_CUDA when no CUDA device is usable.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -81,12 +82,83 @@ int ddelm_gpu_create(const ddelm_desc* d, ddelm_ws** out) {
                                   d->debug_flip_flux_row);
     auto* h = new ddelm_ws;
     try {
-      h->w = new ddg::Workspace(p, d->device);
+      h->w = new ddg::Workspace(ddg::shard_plan(p, 0, p.N), d->device);
     } catch (...) {
       delete h;
       throw;
     }
     *out = h;
+  });
+}
+
+int ddelm_gpu_nccl_unique_id(unsigned char* id) {
+  return guarded([&] {
+    if (!id) throw std::invalid_argument("ddelm_gpu_nccl_unique_id: null argument");
+    ddg::Exchange::unique_id(id);
+  });
+}
+
+int ddelm_gpu_create_sharded(const ddelm_desc* d, int rank, int world, const unsigned char* nccl_id, ddelm_ws** out) {
+  return guarded([&] {
+    if (!d || !out || (world > 1 && !nccl_id)) throw std::invalid_argument("ddelm_gpu_create_sharded: null argument");
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("ddelm_gpu_create_sharded: bad rank / world");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw ddg::CudaError("ddelm_gpu_create_sharded: no CUDA device available (no CPU fallback)");
+    if (d->device < 0 || d->device >= ndev) throw std::invalid_argument("ddelm_gpu_create_sharded: bad device ordinal");
+    ddg::Plan g = ddg::build_plan(d->problem, d->s, d->n_grid, d->M, d->l, d->seed, d->flux_variant,
+                                  d->change_of_variables != 0, d->rank_tol > 0 ? d->rank_tol : 1e-10,
+                                  d->debug_flip_flux_row);
+    if (world > g.N) throw std::invalid_argument("ddelm_gpu_create_sharded: more ranks than subdomains");
+    int lo = 0, hi = 0;
+    ddg::shard_range(g.N, rank, world, &lo, &hi);
+    std::unique_ptr<ddg::Exchange> ex = world > 1 ? std::make_unique<ddg::Exchange>(rank, world, nccl_id, d->device)
+                                                  : std::make_unique<ddg::Exchange>();
+    auto* h = new ddelm_ws;
+    try {
+      h->w = new ddg::Workspace(ddg::shard_plan(g, lo, hi), d->device, std::move(ex));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int ddelm_gpu_plan_tables(const ddelm_desc* d, int rank, int world, int which, int* out, int cap) {
+  int n = 0;
+  const int rc = guarded([&] {
+    if (!d || world < 1 || rank < 0 || rank >= world || which < 0 || which > 5)
+      throw std::invalid_argument("ddelm_gpu_plan_tables: bad argument");
+    ddg::Plan g = ddg::build_plan(d->problem, d->s, d->n_grid, d->M, d->l, d->seed, d->flux_variant,
+                                  d->change_of_variables != 0, d->rank_tol > 0 ? d->rank_tol : 1e-10,
+                                  d->debug_flip_flux_row);
+    int lo = 0, hi = 0;
+    ddg::shard_range(g.N, rank, world, &lo, &hi);
+    const ddg::Plan p = ddg::shard_plan(g, lo, hi);
+    const std::vector<int>* v = nullptr;
+    std::vector<int> meta = {p.sub_lo, p.N, p.N_global, p.n_delta, p.n_pi, p.npf, p.gmax, p.fmax, p.dmax, p.crmax};
+    switch (which) {
+      case 0: v = &p.gamma_dst; break;
+      case 1: v = &p.flux_dst; break;
+      case 2: v = &p.nd_dst; break;
+      case 3: v = &p.corner_dst; break;
+      case 4: v = &p.cross_dst; break;
+      default: v = &meta; break;
+    }
+    n = static_cast<int>(v->size());
+    if (out) std::memcpy(out, v->data(), sizeof(int) * std::min<size_t>(v->size(), static_cast<size_t>(std::max(cap, 0))));
+  });
+  return rc == DDELM_OK ? n : -rc;
+}
+
+int ddelm_gpu_get_shard(ddelm_ws* ws, int* sub_lo, int* sub_count, int* n_global) {
+  return guarded([&] {
+    if (!ws) throw std::invalid_argument("ddelm_gpu_get_shard: null handle");
+    if (sub_lo) *sub_lo = ws->w->plan.sub_lo;
+    if (sub_count) *sub_count = ws->w->plan.N;
+    if (n_global) *n_global = ws->w->plan.N_global;
   });
 }
 

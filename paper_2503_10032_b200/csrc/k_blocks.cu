@@ -177,7 +177,29 @@ __global__ void coarse_rows_kernel(BlockArgs a, const int* row_owner /* npf x 4 
   }
 }
 
-/// S = diag(mult) + Dpp^T Dpp + sum_i Gpi rows; symmetrise; Cholesky; S^{-1}. One CTA.
+/// Gsum = sum over this workspace's subdomains of the corner Grams -(Q_Pi Q_Pi^T), scattered to
+/// (Pi, Pi), in subdomain order. One CTA.
+__global__ void __launch_bounds__(256) coarse_gsum_kernel(BlockArgs a) {
+  const int n = a.n_pi;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) a.Gsum[idx] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.N; ++i)
+      for (int p = 0; p < 4; ++p) {
+        const int gp_ = a.corner_q[i * 4 + p];
+        if (gp_ < 0) continue;
+        const int rp = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gp_];
+        for (int q = 0; q < 4; ++q) {
+          const int gq_ = a.corner_q[i * 4 + q];
+          if (gq_ < 0) continue;
+          const int rq = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gq_];
+          a.Gsum[static_cast<size_t>(rp) * n + rq] += a.Gc[static_cast<size_t>(i) * 16 + p * 4 + q];
+        }
+      }
+  }
+}
+
+/// S = diag(mult) + Dpp^T Dpp + Gsum; symmetrise; Cholesky; S^{-1}. One CTA.
 __global__ void __launch_bounds__(1024) coarse_schur_kernel(BlockArgs a) {
   const int n = a.n_pi, npf = a.npf;
   double* S = a.S;
@@ -191,20 +213,9 @@ __global__ void __launch_bounds__(1024) coarse_schur_kernel(BlockArgs a) {
     S[idx] = (p == q ? static_cast<double>(a.mult_pi[p]) : 0.0) + s;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < a.N; ++i)
-      for (int p = 0; p < 4; ++p) {
-        const int gp_ = a.corner_q[i * 4 + p];
-        if (gp_ < 0) continue;
-        const int rp = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gp_];
-        for (int q = 0; q < 4; ++q) {
-          const int gq_ = a.corner_q[i * 4 + q];
-          if (gq_ < 0) continue;
-          const int rq = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gq_];
-          S[static_cast<size_t>(rp) * n + rq] += a.Gc[static_cast<size_t>(i) * 16 + p * 4 + q];
-        }
-      }
-  }
+  // + sum_i Gpi rows (the corner Grams of every subdomain, summed by coarse_gsum_kernel and, when
+  //   sharded, all-reduced over the ranks)
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) S[idx] += a.Gsum[idx];
   __syncthreads();
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
     const int p = idx / n, q = idx % n;
@@ -321,6 +332,11 @@ void launch_coarse_local(const BlockArgs& a, const int* cr_row, const int* cr_of
 
 void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t st) {
   coarse_rows_kernel<<<a.npf, 128, 0, st>>>(a, row_owner);
+  DDG_LAUNCH_CHECK();
+}
+
+void launch_coarse_gsum(const BlockArgs& a, cudaStream_t st) {
+  coarse_gsum_kernel<<<1, 256, 0, st>>>(a);
   DDG_LAUNCH_CHECK();
 }
 

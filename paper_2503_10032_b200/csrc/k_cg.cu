@@ -28,12 +28,15 @@
 // grid barrier (the matrices are constant during the solve), and NN2 / OP3 walk their slices in
 // reverse so they start on the lines NN1 / OP2 left in L2.
 //
-// The whole CG loop (solvers.cpp:82-119) is ONE persistent cooperative kernel: 7 grid barriers per
-// iteration, the CG scalars are sums of per-CTA / per-subdomain partials in a fixed order (no
-// atomics: bitwise deterministic), the search direction is double-buffered so the p-update is
-// fused into OP1. The same kernel, with a job code, applies the operator once (tests), forms the
-// reduced right-hand side (solvers.cpp:542-551) and reconstructs the coefficients
-// (solvers.cpp:565-577).
+// Two drivers share these phases. Default: one kernel launch per phase, the whole CG loop
+// (solvers.cpp:82-119) captured as ONE CUDA graph with a device-side while node (the XR2 phase sets
+// the loop condition) — on a sharded workspace the owner-slot all-reduces sit between the phases
+// inside the same graph. Alternative (DDELM_CG_MODE=persistent, one device): one persistent
+// cooperative kernel with 7 grid barriers per iteration. In both, the CG scalars are sums of
+// per-CTA / per-subdomain partials in a fixed order (no atomics: bitwise deterministic, and the two
+// drivers agree bit for bit), the search direction is double-buffered so the p-update is fused
+// into OP1, and the same phases apply the operator once (tests), form the reduced right-hand side
+// (solvers.cpp:542-551) and reconstruct the coefficients (solvers.cpp:565-577).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -532,7 +535,7 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, 
       for (int k = lane; k < r; k += 32) acc += QtX[static_cast<size_t>(k) * E + 1 + g] * sh.s0[k];
     acc = warp_sum(acc);
     const int dst = a.corner_dst[i * 4 + warp];
-    if (lane == 0 && dst >= 0) a.ttab[dst] = acc;  // t(gp) -= phi - Ky at the corners (phi = 0 there)
+    if (lane == 0 && dst >= 0) a.ttab_w[dst] = acc;  // t(gp) -= phi - Ky at the corners (phi = 0 there)
   } else if (mode != 1) {
     // psi_i = Zc v (Dpd rows restricted to this subdomain), warps 4..
     const double* Zc = stg.zc;
@@ -541,7 +544,7 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, 
       for (int g = lane; g < d.n_gamma; g += 32) acc += Zc[static_cast<size_t>(rho) * a.gmax + g] * vg[g];
       acc = warp_sum(acc);
       const int dst = a.cross_dst[static_cast<size_t>(i) * a.crmax + rho];
-      if (lane == 0 && dst >= 0) a.ptab[dst] = acc;
+      if (lane == 0 && dst >= 0) a.ptab_w[dst] = acc;
     }
   }
   __syncthreads();
@@ -589,7 +592,7 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
       return cj;
     });
     if (mode == 2) continue;
-    double* xt = a.xtab + static_cast<size_t>(p) * 2 * a.n_delta;
+    double* xt = a.xtab_w + static_cast<size_t>(p) * 2 * a.n_delta;
     const int* fdst = a.flux_dst + static_cast<size_t>(i) * a.fmax;
     reduce_warps<W>(a, g, sh, acc, [&](int l, double s) {
       const int dst = fdst[l];
@@ -616,7 +619,7 @@ __device__ void dev_nn1(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
     double acc[W];
     // reference order (solvers.cpp:455): y = Kbar^+ rhs (M-vector), then Cdelta y
     consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
-    double* trt = a.trtab + static_cast<size_t>(p) * 2 * a.n_delta;
+    double* trt = a.trtab_w + static_cast<size_t>(p) * 2 * a.n_delta;
     const int* ndst = a.nd_dst + static_cast<size_t>(i) * a.dmax;
     reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { trt[ndst[l]] = s; });
   }
@@ -644,7 +647,7 @@ __device__ void dev_nn2(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
     consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
     reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { sh.s0[l] = s; });
     // zz = Qbar_r (Cbar^T x) on the flux rows (partial over the parts p; linear)
-    double* zzt = a.zztab + static_cast<size_t>(p) * 2 * a.n_delta;
+    double* zzt = a.zztab_w + static_cast<size_t>(p) * 2 * a.n_delta;
     const int* ndst = a.nd_dst + static_cast<size_t>(i) * a.dmax;
     coldot_split(QtX + 1, E, rb, nd, sh.s0, sh.red, Team{kCThreads}, [&](int kk, double v) { zzt[ndst[kk]] = v; });
   }
@@ -695,7 +698,7 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
         for (int kk = lane; kk < r; kk += 32) acc2 += QtX[static_cast<size_t>(kk) * E + 1 + gq] * sh.s0[kk];
       acc2 = warp_sum(acc2);
       const int dst = a.corner_dst[i * 4 + warp];
-      if (lane == 0 && dst >= 0) a.t3tab[static_cast<size_t>(p) * 4 * a.n_pi + dst] = acc2;  // t(gp) += z(lr)
+      if (lane == 0 && dst >= 0) a.t3tab_w[static_cast<size_t>(p) * 4 * a.n_pi + dst] = acc2;  // t(gp) += z(lr)
     }
     cons_sync();
   }
@@ -786,7 +789,7 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
     for (int rho = 0; rho < a.crmax; ++rho) zs += Zc[static_cast<size_t>(rho) * a.gmax + g] * d2s[rho];
     const double mphi = (mode == 0) ? v[dg] : 0.0;  // -phi
     const double o = mphi + qsv[g] + zs;
-    a.otab[a.gamma_dst[static_cast<size_t>(i) * a.gmax + g]] = o;
+    a.otab_w[a.gamma_dst[static_cast<size_t>(i) * a.gmax + g]] = o;
     if (mode == 0) dot += v[dg] * o;
   }
   dot = block_sum(dot, sh.red);
@@ -931,13 +934,13 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
     for (int i = b; i < a.N; i += G) {
       if (a.trace != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_op4[15]));
       const double dot = dev_op4(a, sh, qst, i, pnext, 0, a.trace != nullptr ? t_op4 : nullptr);
-      if (threadIdx.x == 0) a.pap[i] = dot;
+      if (threadIdx.x == 0) a.pap_w[a.sub_lo + i] = dot;
     }
     tr(10);
     grid.sync();
     tr(11);
     // pAp = sum over subdomains of p . o_i (fixed order), alpha, x / r update
-    const double pAp = det_sum(a.pap, a.N);
+    const double pAp = det_sum(a.pap, a.N_global);
     if (pAp <= 0.0) {  // solvers.cpp:97-103
       if (b == 0 && threadIdx.x == 0) {
         a.state[3] = pAp < 0.0 ? 1 : 0;
@@ -985,6 +988,127 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
     }
 }
 
+// ---------------------------------------------------------------- phase-by-phase execution
+// The same phases as the persistent kernel, one launch each, for the sharded path: the host
+// enqueues an all-reduce of the owner-slot tables between launches (comm.hpp). With one device
+// the sequence is bitwise identical to the persistent kernel (same work split, same sums).
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int phase, int mode, int it,
+                                                               const double* vin, double* vout) {
+  const int G = gridDim.x, b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp == kProducerWarp;
+  __shared__ __align__(8) uint64_t bars[2 * kStages + 1];
+  __shared__ double bsum[32];
+  const Shared sh = carve(a, bars);
+  if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < kStages; ++s2) {
+      mbar_init(&sh.full[s2], 1);
+      mbar_init(&sh.empty[s2], kCWarps);
+    }
+    mbar_init(sh.qbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  Producer pr;
+  pr.cnt = 0;
+  pr.active = false;
+  unsigned ccnt = 0;
+  QtxStage qst{0u, -1};
+  const bool cg = (mode == 0 && vin == nullptr);  // CG iteration: v = r + beta p_cur
+  if (cg) it = a.state[6];  // the iteration counter lives on the device (graph replays)
+  double* pcur = a.pbuf[(it + 1) & 1];
+  double* pnext = a.pbuf[it & 1];
+  if (cg && a.state[1]) {  // converged / aborted earlier
+    if (phase == kPhXr2 && b == 0 && threadIdx.x == 0 && a.cond != 0) cudaGraphSetConditional(a.cond, 0);
+    return;
+  }
+  switch (phase) {
+    case kPhOp1: {
+      const double beta = cg ? a.scal[2] : 0.0;
+      for (int i = b; i < a.N; i += G) dev_op1(a, sh, qst, i, cg ? nullptr : vin, mode, cg, beta, pcur, pnext);
+      return;
+    }
+    case kPhOp2:
+    case kPhNn1:
+    case kPhNn2:
+    case kPhOp3: {
+      const int kind = phase == kPhOp2 ? kOp2 : phase == kPhNn1 ? kNn1 : phase == kPhNn2 ? kNn2 : kOp3;
+      if (producer) {
+        if (lane == 0) {
+          producer_begin(a, pr, kind, mode == 2);
+          producer_run(a, pr, sh, -1);
+        }
+        __syncwarp();
+      } else if (phase == kPhOp2) {
+        dev_op2<W>(a, sh, ccnt, mode);
+      } else if (phase == kPhNn1) {
+        dev_nn1<W>(a, sh, ccnt);
+      } else if (phase == kPhNn2) {
+        dev_nn2<W>(a, sh, ccnt);
+      } else {
+        dev_op3<W>(a, sh, ccnt);
+      }
+      __syncthreads();
+      return;
+    }
+    case kPhOp4:
+      for (int i = b; i < a.N; i += G) {
+        const double dot = dev_op4(a, sh, qst, i, cg ? pnext : vin, mode);
+        if (cg && threadIdx.x == 0) a.pap_w[a.sub_lo + i] = dot;
+      }
+      return;
+    case kPhXr1: {  // alpha, x / r update, r.r partials (solvers.cpp:96-107)
+      const double pAp = det_sum(a.pap, a.N_global);
+      if (pAp <= 0.0) {
+        if (b == 0 && threadIdx.x == 0) {
+          a.state[3] = pAp < 0.0 ? 1 : 0;
+          a.state[5] = it - 1;
+          a.state[1] = 1;
+        }
+        return;
+      }
+      const double alpha = a.scal[0] / pAp;
+      double dsum = 0;
+      for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) {
+        const double ap = gather_out(a, g);
+        a.x[g] += alpha * pnext[g];
+        const double rg = a.r[g] - alpha * ap;
+        a.r[g] = rg;
+        dsum += rg * rg;
+      }
+      dsum = block_sum(dsum, bsum);
+      if (threadIdx.x == 0) a.partial[b] = dsum;
+      return;
+    }
+    case kPhXr2: {  // one CTA: ||r||, history, stopping test, beta (solvers.cpp:108-116)
+      if (b != 0) return;
+      const double rr_new = det_sum(a.partial, a.xr_parts);
+      const double rel = sqrt(rr_new) / a.scal[1];
+      const bool stop = rel <= a.rel_tol || it >= a.max_iter;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        a.hist[it - 1] = rel;
+        a.state[5] = it;
+        if (stop) {
+          a.state[1] = 1;
+          a.state[2] = rel <= a.rel_tol ? 1 : 0;
+        } else {
+          a.scal[2] = rr_new / a.scal[0];
+          a.scal[0] = rr_new;
+          a.state[6] = it + 1;
+        }
+        if (a.cond != 0) cudaGraphSetConditional(a.cond, stop ? 0 : 1);  // CUDA-graph while loop
+      }
+      return;
+    }
+    default:  // kPhGather
+      for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) vout[g] = gather_out(a, g);
+      return;
+  }
+}
+
 __global__ void __launch_bounds__(256) cg_init_kernel(CgArgs a) {
   __shared__ double red[32];
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1006,7 +1130,9 @@ __global__ void cg_init2_kernel(CgArgs a, int nblk) {
   for (int k = 0; k < nblk; ++k) rr += a.partial[k];
   a.scal[0] = rr;
   a.scal[1] = sqrt(rr);
+  a.scal[2] = 0.0;  // beta of "iteration 0" (phase-by-phase CG)
   for (int k = 0; k < 8; ++k) a.state[k] = 0;
+  a.state[6] = 1;  // phase-by-phase CG: current iteration
   if (rr == 0.0) {
     a.state[1] = 1;  // bnorm == 0: converged with x = 0 (solvers.cpp:89-92)
     a.state[2] = 1;
@@ -1068,6 +1194,22 @@ void cg_launch(const CgArgs& a, int job, const double* vin, double* vout, cudaSt
   CgArgs arg = a;
   void* params[] = {&arg, &job, &vin, &vout};
   DDG_CUDA(cudaLaunchCooperativeKernel(kernel_for(a), dim3(G), dim3(kThreads), params, sm, st));
+}
+
+void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double* vin, double* vout,
+                     cudaStream_t st) {
+  cg_check_capacity(a);
+  const int G = cg_grid(a);
+  const size_t sm = smem_bytes(a);
+  const bool wide = width_regs(a) != 8;
+  const void* k = wide ? reinterpret_cast<const void*>(cg_phase_kernel<16>) : reinterpret_cast<const void*>(cg_phase_kernel<8>);
+  DDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  const int grid = (phase == kPhXr2) ? 1 : G;
+  if (wide)
+    cg_phase_kernel<16><<<grid, kThreads, sm, st>>>(a, phase, mode, it, vin, vout);
+  else
+    cg_phase_kernel<8><<<grid, kThreads, sm, st>>>(a, phase, mode, it, vin, vout);
+  DDG_LAUNCH_CHECK();
 }
 
 void cg_launch_init(const CgArgs& a, cudaStream_t st) {

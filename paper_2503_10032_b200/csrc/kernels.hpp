@@ -107,6 +107,7 @@ struct BlockArgs {
   double* Dpp;           // npf x n_pi
   double* dpi;           // npf
   double* S;             // n_pi x n_pi
+  double* Gsum;          // n_pi x n_pi : sum of the subdomain corner Grams (all-reduced when sharded)
   double* Sinv;          // n_pi x n_pi
   double* Wmu;           // n_pi x (n_pi + npf)
   double* Wd;            // npf x (n_pi + npf)
@@ -120,6 +121,7 @@ void launch_blocks(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_local(const BlockArgs& a, const int* cr_row, const int* cr_off, const int* cr_l,
                          const double* cr_w, cudaStream_t st);
 void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t st);
+void launch_coarse_gsum(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_schur(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_weights(const BlockArgs& a, cudaStream_t st);
 /// Pack the CG stream blocks KF = [C | Ypi | F] and KD = [Cbar | Cdelta] (row-interleaved).
@@ -179,15 +181,20 @@ struct CgArgs {
   int P;
   int rpc_max;    // largest rows-per-chunk of the streaming pipeline
   double* s;      // N x rmax
-  double* ttab;   // n_pi x 4    corner contributions of OP1 (owner slots)
-  double* ptab;   // npf x 4     cross-row contributions of OP1
-  double* t3tab;  // P x n_pi x 4 corner contributions of OP3
-  double* otab;   // 2 n_delta   OP4 outputs at the two owners of each Delta index
-  double* xtab;   // P x 2 n_delta  flux values x (OP2)
-  double* trtab;  // P x 2 n_delta  P x (NN1)
-  double* zztab;  // P x 2 n_delta  P^T P x (NN2)
+  // owner-slot tables: producers write the *_w copy (their own slots), consumers read the plain
+  // copy; identical pointers on one device, send / receive buffers of an all-reduce when sharded
+  double *ttab, *ttab_w;    // n_pi x 4    corner contributions of OP1
+  double *ptab, *ptab_w;    // npf x 4     cross-row contributions of OP1
+  double *t3tab, *t3tab_w;  // P x n_pi x 4 corner contributions of OP3
+  double *otab, *otab_w;    // 2 n_delta   OP4 outputs at the two owners of each Delta index
+  double *xtab, *xtab_w;    // P x 2 n_delta  flux values x (OP2)
+  double *trtab, *trtab_w;  // P x 2 n_delta  P x (NN1)
+  double *zztab, *zztab_w;  // P x 2 n_delta  P^T P x (NN2)
+  int N_global, sub_lo;     // sharding: this device holds subdomains [sub_lo, sub_lo + N)
+  int xr_parts;             // r.r partials written by the XR phase (= its grid size)
+  unsigned long long cond;  // cudaGraphConditionalHandle of the CG while-loop graph (0: none)
   double* u;      // P x N x rmax
-  double* pap;    // N : p . o_i
+  double *pap, *pap_w;  // N_global : p . o_i (indexed by global subdomain)
   // CG vectors
   double* x;
   double* r;
@@ -195,8 +202,8 @@ struct CgArgs {
   double* rhs;
   double* partial;  // reduction scratch (>= grid)
   double* hist;     // max_iter
-  int* state;       // [1] done, [2] converged, [3] negcurv, [5] iterations
-  double* scal;     // [0] rr, [1] bnorm
+  int* state;       // [1] done, [2] converged, [3] negcurv, [5] iterations, [6] current iteration
+  double* scal;     // [0] rr, [1] bnorm, [2] beta (phase-by-phase CG)
   double* coeffs;   // N x M output
   double* mu_pi_out;  // n_pi
   double* trace;      // optional G x 16 per-phase ns counters of the CG job (nullptr: off)
@@ -206,6 +213,11 @@ struct CgArgs {
 /// kJobRhs writes vout = the reduced right-hand side (solvers.cpp:542-551); kJobRecon writes the
 /// coefficients and mu_Pi for mu_Delta = vin (solvers.cpp:565-577).
 void cg_launch(const CgArgs& a, int job, const double* vin, double* vout, cudaStream_t st);
+/// Phase-by-phase execution (sharded mode: an all-reduce of the owner-slot tables between phases)
+enum CgPhase { kPhOp1 = 0, kPhOp2, kPhNn1, kPhNn2, kPhOp3, kPhOp4, kPhXr1, kPhXr2, kPhGather };
+/// mode: 0 operator / CG, 1 reduced rhs, 2 reconstruction; it: CG iteration (1-based, CG only)
+void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double* vin, double* vout,
+                     cudaStream_t st);
 void cg_launch_init(const CgArgs& a, cudaStream_t st);
 int cg_grid(const CgArgs& a);
 int cg_rows_per_chunk_max(const CgArgs& a);

@@ -212,6 +212,7 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
       sp.iy = iy;
       sp.cls = it->second;
       sp.seed = seed + static_cast<uint64_t>(i);
+      sp.gid = i;
     }
   for (const ClassPlan& c : p.classes) {
     p.gmax = std::max(p.gmax, c.n_gamma);
@@ -329,12 +330,75 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
   return p;
 }
 
+void shard_range(int N, int rank, int world, int* lo, int* hi) {
+  *lo = static_cast<int>(static_cast<long long>(N) * rank / world);
+  *hi = static_cast<int>(static_cast<long long>(N) * (rank + 1) / world);
+}
+
+Plan shard_plan(const Plan& g, int lo, int hi) {
+  if (lo < 0 || hi > g.N || lo >= hi) throw std::invalid_argument("shard_plan: empty or out-of-range strip");
+  // global owner-slot destinations, built on the global plan
+  const int N = g.N;
+  std::vector<int> gdst(static_cast<size_t>(N) * g.gmax, -1), fdst(static_cast<size_t>(N) * g.fmax, -1),
+      ndst(static_cast<size_t>(N) * g.dmax, -1), cdst(static_cast<size_t>(N) * 4, -1),
+      xdst(static_cast<size_t>(N) * g.crmax, -1);
+  for (int d = 0; d < g.n_delta; ++d)
+    for (int s = 0; s < 2; ++s) {
+      if (g.own_gamma[2 * d + s] >= 0) gdst[g.own_gamma[2 * d + s]] = 2 * d + s;
+      if (g.own_flux[2 * d + s] >= 0) fdst[g.own_flux[2 * d + s]] = 2 * d + s;
+      if (g.own_nd[2 * d + s] >= 0) ndst[g.own_nd[2 * d + s]] = 2 * d + s;
+    }
+  // corner / cross-row owners in subdomain order (the order the single-device sums use)
+  std::vector<int> pi_n(std::max(g.n_pi, 1), 0), row_n(std::max(g.npf, 1), 0);
+  for (int i = 0; i < N; ++i) {
+    const SubPlan& sp = g.subs[i];
+    int slot = 0;
+    for (size_t q = 0; q < sp.gamma_pi.size(); ++q)
+      if (sp.gamma_pi[q] >= 0) {
+        const int gp = sp.gamma_pi[q];
+        if (pi_n[gp] >= 4) throw std::logic_error("shard_plan: corner owner overflow");
+        cdst[static_cast<size_t>(i) * 4 + slot++] = gp * 4 + pi_n[gp]++;
+      }
+    for (size_t rho = 0; rho < sp.cross_rows.size(); ++rho) {
+      const int r = sp.cross_rows[rho].r;
+      if (row_n[r] >= 4) throw std::logic_error("shard_plan: cross-row owner overflow");
+      xdst[static_cast<size_t>(i) * g.crmax + rho] = r * 4 + row_n[r]++;
+    }
+  }
+  Plan p = g;
+  p.N = hi - lo;
+  p.sub_lo = lo;
+  p.N_global = g.N;
+  p.subs.assign(g.subs.begin() + lo, g.subs.begin() + hi);
+  p.f.assign(g.f.begin() + static_cast<size_t>(lo) * g.m, g.f.begin() + static_cast<size_t>(hi) * g.m);
+  auto slice = [&](const std::vector<int>& v, int w) {
+    return std::vector<int>(v.begin() + static_cast<size_t>(lo) * w, v.begin() + static_cast<size_t>(hi) * w);
+  };
+  p.gamma_dst = slice(gdst, g.gmax);
+  p.flux_dst = slice(fdst, g.fmax);
+  p.nd_dst = slice(ndst, g.dmax);
+  p.corner_dst = slice(cdst, 4);
+  p.cross_dst = slice(xdst, g.crmax);
+  // owner tables restricted to this strip (local subdomain numbering; -1 = owned by another rank)
+  auto remap = [&](std::vector<int>& own, int w) {
+    for (int& v : own)
+      if (v >= 0) {
+        const int i = v / w, pos = v % w;
+        v = (i >= lo && i < hi) ? (i - lo) * w + pos : -1;
+      }
+  };
+  remap(p.own_gamma, g.gmax);
+  remap(p.own_flux, g.fmax);
+  remap(p.own_nd, g.dmax);
+  return p;
+}
+
 void init_layer(const Plan& p, int i, double* w0, double* w1, double* b) {
   const SubPlan& sp = p.subs[i];
   const double h = 1.0 / p.s;
   const double x0 = sp.ix * h, y0 = sp.iy * h, x1 = (sp.ix + 1) * h, y1 = (sp.iy + 1) * h;
   const double r = std::hypot(x1 - x0, y1 - y0) / 2.0;
-  std::mt19937_64 gen(p.seed + static_cast<uint64_t>(i));
+  std::mt19937_64 gen(p.seed + static_cast<uint64_t>(sp.gid));
   std::uniform_real_distribution<double> uw(-p.l, p.l);
   std::uniform_real_distribution<double> ux(x0 - r, x1 + r);
   std::uniform_real_distribution<double> uy(y0 - r, y1 + r);

@@ -76,6 +76,7 @@ struct SubPlan {
   std::vector<CrossRow> cross_rows;
   std::vector<int> ndelta_map;   // per Neumann Delta row k: Delta index
   uint64_t seed = 0;
+  int gid = 0;                   // global subdomain index (seed + gid, solvers.cpp:136)
 };
 
 struct Plan {
@@ -99,7 +100,19 @@ struct Plan {
   std::vector<int> own_nd;     // 2 * n_delta: i * dmax + k
 
   std::vector<double> f;  // N x m right-hand sides (problem data, assembly.cpp:21-33)
+
+  // ---- sharding: this plan holds subdomains [sub_lo, sub_lo + N) of N_global (one rank's
+  // contiguous strip); the interface numbering (n_delta, n_pi, npf) stays global
+  int sub_lo = 0, N_global = 1;
+  // owner-slot destinations (global slot numbering, so that every slot has exactly one writer
+  // across all ranks): gamma/flux/nd -> 2 g + s, corner -> gp * 4 + slot, cross -> rr * 4 + slot
+  std::vector<int> gamma_dst, flux_dst, nd_dst, corner_dst, cross_dst;
 };
+
+/// The strip of subdomains [lo, hi) of a global plan, with global owner slots (see Plan).
+Plan shard_plan(const Plan& g, int lo, int hi);
+/// Contiguous balanced partition of N subdomains over `world` ranks: [lo, hi) of `rank`.
+void shard_range(int N, int rank, int world, int* lo, int* hi);
 
 /// Builds the plan; throws std::invalid_argument like the reference (geometry.cpp:21-22).
 Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, int flux_variant,

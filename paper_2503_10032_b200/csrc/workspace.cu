@@ -66,12 +66,19 @@ template struct DevBuf<int>;
 template struct DevBuf<Task>;
 template struct DevBuf<ClassDims>;
 
-Workspace::Workspace(const Plan& p, int device) : plan(p), device_(device) {
+Workspace::Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex)
+    : plan(p), ex_(std::move(ex)), device_(device) {
+  // default: phase-by-phase kernels in one CUDA graph (a device-side while loop) — measured faster
+  // than the single persistent cooperative kernel (C3 CG 31 vs 43 ms, C4 143 vs 207 ms);
+  // DDELM_CG_MODE=persistent selects the persistent kernel (single device only)
+  phased_ = true;
+  if (const char* m = std::getenv("DDELM_CG_MODE")) phased_ = std::strcmp(m, "persistent") != 0;
   DDG_CUDA(cudaSetDevice(device_));
   DDG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   DDG_CUDA(cudaStreamCreateWithFlags(&cap_, cudaStreamNonBlocking));
   for (auto& e : ev_) DDG_CUDA(cudaEventCreate(&e));
   DDG_CUDA(cudaMallocHost(&pinned_state_, 64));
+  if (sharded()) phased_ = true;
   arena_.cap = size_t(64) << 20;
   DDG_CUDA(cudaMalloc(reinterpret_cast<void**>(&arena_.base), arena_.cap));
   upload_plan();
@@ -191,33 +198,14 @@ void Workspace::upload_plan() {
   d_cr_w.upload(crw, st_);
   d_row_owner.upload(row_owner, st_);
   d_pi_owner.upload(pi_owner, st_);
-  d_own_gamma.upload(p.own_gamma, st_);
-  d_own_flux.upload(p.own_flux, st_);
-  d_own_nd.upload(p.own_nd, st_);
-  {
-    // owner-slot destinations (inverse of the owner lists): producers write their contribution
-    // to slot s of the quantity, readers sum the slots contiguously in the owner (subdomain) order
-    std::vector<int> gdst(static_cast<size_t>(N) * p.gmax, -1), fdst(static_cast<size_t>(N) * p.fmax, -1),
-        ndst(static_cast<size_t>(N) * p.dmax, -1), cdst(static_cast<size_t>(N) * 4, -1),
-        xdst(static_cast<size_t>(N) * p.crmax, -1);
-    for (int g = 0; g < p.n_delta; ++g)
-      for (int s = 0; s < 2; ++s) {
-        if (p.own_gamma[2 * g + s] >= 0) gdst[p.own_gamma[2 * g + s]] = 2 * g + s;
-        if (p.own_flux[2 * g + s] >= 0) fdst[p.own_flux[2 * g + s]] = 2 * g + s;
-        if (p.own_nd[2 * g + s] >= 0) ndst[p.own_nd[2 * g + s]] = 2 * g + s;
-      }
-    for (int gp = 0; gp < p.n_pi; ++gp)
-      for (int q = 0; q < 4; ++q)
-        if (pi_owner[static_cast<size_t>(gp) * 4 + q] >= 0) cdst[pi_owner[static_cast<size_t>(gp) * 4 + q]] = gp * 4 + q;
-    for (int rr = 0; rr < p.npf; ++rr)
-      for (int q = 0; q < 4; ++q)
-        if (row_owner[static_cast<size_t>(rr) * 4 + q] >= 0) xdst[row_owner[static_cast<size_t>(rr) * 4 + q]] = rr * 4 + q;
-    d_gamma_dst.upload(gdst, st_);
-    d_flux_dst.upload(fdst, st_);
-    d_nd_dst.upload(ndst, st_);
-    d_corner_dst.upload(cdst, st_);
-    d_cross_dst.upload(xdst, st_);
-  }
+  // owner-slot destinations (global slot numbering from shard_plan): producers write their
+  // contribution to slot s of the quantity, readers sum the slots contiguously in owner order
+  if (p.gamma_dst.empty()) throw std::logic_error("plan without owner slots (use shard_plan)");
+  d_gamma_dst.upload(p.gamma_dst, st_);
+  d_flux_dst.upload(p.flux_dst, st_);
+  d_nd_dst.upload(p.nd_dst, st_);
+  d_corner_dst.upload(p.corner_dst, st_);
+  d_cross_dst.upload(p.cross_dst, st_);
   d_mult_pi.upload(p.multiplicity_pi, st_);
   std::vector<double> flip(std::max(p.n_delta, 1), 1.0);
   if (p.debug_flip_flux_row >= 0 && p.debug_flip_flux_row < p.n_delta) flip[p.debug_flip_flux_row] = -1.0;
@@ -267,6 +255,7 @@ void Workspace::upload_plan() {
   d_Dpp.alloc(npf * npi);
   d_dpi.alloc(npf);
   d_S.alloc(npi * npi);
+  d_Gsum.alloc(npi * npi);
   d_Sinv.alloc(npi * npi);
   d_spd_fail.alloc(1);
   const size_t nd = std::max(p.n_delta, 1);
@@ -278,7 +267,7 @@ void Workspace::upload_plan() {
   d_Wmu.alloc(npi * (npi + npf));
   d_Wd.alloc(npf * (npi + npf));
   d_W3.alloc(npf * npi);
-  d_pap.alloc(static_cast<size_t>(N));
+  d_pap.alloc(static_cast<size_t>(p.N_global));
   d_vin.alloc(nd);
   d_vout.alloc(nd);
   // owner-slot tables of the coarse gathers: unused slots stay zero
@@ -537,6 +526,7 @@ BlockArgs Workspace::block_args() {
   b.Dpp = d_Dpp.ptr;
   b.dpi = d_dpi.ptr;
   b.S = d_S.ptr;
+  b.Gsum = d_Gsum.ptr;
   b.Sinv = d_Sinv.ptr;
   b.mult_pi = d_mult_pi.ptr;
   b.spd_fail = d_spd_fail.ptr;
@@ -557,9 +547,14 @@ void Workspace::build_coarse() {
   launches_ += 2;
   if (plan.n_pi > 0) {
     launch_coarse_rows(b, d_row_owner.ptr, st_);
+    launch_coarse_gsum(b, st_);
+    // sharded: this device holds only its strip's contributions to Dpp, dpi and the corner Grams
+    xchg(d_Dpp.ptr, d_Dpp.ptr, static_cast<size_t>(plan.npf) * plan.n_pi);
+    xchg(d_dpi.ptr, d_dpi.ptr, static_cast<size_t>(plan.npf));
+    xchg(d_Gsum.ptr, d_Gsum.ptr, static_cast<size_t>(plan.n_pi) * plan.n_pi);
     launch_coarse_schur(b, st_);
     launch_coarse_weights(b, st_);
-    launches_ += 4;
+    launches_ += 5;
   }
   // row-interleaved stream blocks of the interface iteration (k_cg.cu)
   ldKF_ = (rmax_ + 4 + plan.fmax + 1) / 2 * 2;
@@ -612,7 +607,10 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
     int dev = 0, sms = 148;
     DDG_CUDA(cudaGetDevice(&dev));
     DDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    int P = std::max(1, std::min(8, sms / p.N));
+    // the same P on every rank (table layouts must agree): from the largest strip size
+    const int world = ex_ ? ex_->world() : 1;
+    const int nstrip = (p.N_global + world - 1) / world;
+    int P = std::max(1, std::min(8, sms / nstrip));
     if (const char* e = std::getenv("DDELM_CG_PARTS")) P = std::max(1, std::min(p.M, std::atoi(e)));
     a.P = P;
     ArenaScope hot(&arena_);
@@ -624,6 +622,19 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
     if (d_tpart3.count != PP * 4 * std::max(p.n_pi, 1)) {
       d_tpart3.alloc(PP * 4 * std::max(p.n_pi, 1));  // unused owner slots must read as zero
       DDG_CUDA(cudaMemsetAsync(d_tpart3.ptr, 0, d_tpart3.count * sizeof(double), st_));
+    }
+    if (sharded()) {
+      // send tables: slots owned by other ranks stay zero; receive twins hold the all-reduced sums
+      for (DevBuf<double>* bsend : {&d_xf, &d_tr, &d_zz, &d_o, &d_pap})
+        DDG_CUDA(cudaMemsetAsync(bsend->ptr, 0, bsend->count * sizeof(double), st_));
+      r_tpart.alloc(d_tpart.count);
+      r_psipart.alloc(d_psipart.count);
+      r_tpart3.alloc(d_tpart3.count);
+      r_o.alloc(d_o.count);
+      r_xf.alloc(d_xf.count);
+      r_tr.alloc(d_tr.count);
+      r_zz.alloc(d_zz.count);
+      r_pap.alloc(d_pap.count);
     }
   }
   a.rel_tol = tol;
@@ -651,15 +662,26 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.W3 = d_W3.ptr;
   a.dpi = d_dpi.ptr;
   a.s = d_s.ptr;
-  a.ttab = d_tpart.ptr;
-  a.t3tab = d_tpart3.ptr;
-  a.ptab = d_psipart.ptr;
-  a.otab = d_o.ptr;
-  a.xtab = d_xf.ptr;
-  a.trtab = d_tr.ptr;
-  a.zztab = d_zz.ptr;
+  a.ttab_w = d_tpart.ptr;
+  a.t3tab_w = d_tpart3.ptr;
+  a.ptab_w = d_psipart.ptr;
+  a.otab_w = d_o.ptr;
+  a.xtab_w = d_xf.ptr;
+  a.trtab_w = d_tr.ptr;
+  a.zztab_w = d_zz.ptr;
+  a.pap_w = d_pap.ptr;
+  const bool sh = sharded();
+  a.ttab = sh ? r_tpart.ptr : d_tpart.ptr;
+  a.t3tab = sh ? r_tpart3.ptr : d_tpart3.ptr;
+  a.ptab = sh ? r_psipart.ptr : d_psipart.ptr;
+  a.otab = sh ? r_o.ptr : d_o.ptr;
+  a.xtab = sh ? r_xf.ptr : d_xf.ptr;
+  a.trtab = sh ? r_tr.ptr : d_tr.ptr;
+  a.zztab = sh ? r_zz.ptr : d_zz.ptr;
+  a.pap = sh ? r_pap.ptr : d_pap.ptr;
+  a.N_global = p.N_global;
+  a.sub_lo = p.sub_lo;
   a.u = d_u.ptr;
-  a.pap = d_pap.ptr;
   a.x = d_x.ptr;
   a.r = d_r.ptr;
   a.pbuf[0] = d_p.ptr;
@@ -672,6 +694,8 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.coeffs = d_coeffs.ptr;
   a.mu_pi_out = d_mu_pi_out.ptr;
   a.rpc_max = cg_rows_per_chunk_max(a);
+  a.xr_parts = cg_grid(a);
+  a.cond = 0;
   a.trace = nullptr;
   if (std::getenv("DDELM_CG_TRACE")) {
     d_trace.alloc(148 * 4 * 32);
@@ -710,21 +734,25 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   CgArgs a = cg_args(theta, tol, max_iter);
   apply_l2_policy();
   DDG_CUDA(cudaEventRecord(ev_[8], st_));
-  cg_launch(a, kJobRhs, nullptr, d_rhs.ptr, st_);
+  if (phased_) run_phases(a, 1, nullptr, d_rhs.ptr);
+  else cg_launch(a, kJobRhs, nullptr, d_rhs.ptr, st_);
   cg_launch_init(a, st_);
   launches_ += 3;
   DDG_CUDA(cudaEventRecord(ev_[9], st_));
   const int kt_cg = ktimer_begin();
-  cg_launch(a, kJobCg, nullptr, nullptr, st_);
+  if (phased_) run_cg_phased(a);
+  else cg_launch(a, kJobCg, nullptr, nullptr, st_);
   ktimer_end(kt_cg, "cg_iterations", 0.0, 0.0);
   DDG_CUDA(cudaEventRecord(ev_[10], st_));
-  cg_launch(a, kJobRecon, d_x.ptr, nullptr, st_);
+  if (phased_) run_phases(a, 2, d_x.ptr, nullptr);
+  else cg_launch(a, kJobRecon, d_x.ptr, nullptr, st_);
   launches_ += 1;
   DDG_CUDA(cudaEventRecord(ev_[11], st_));
   int state[8];
   DDG_CUDA(cudaMemcpyAsync(state, d_state.ptr, sizeof(state), cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
   res.iterations = state[5];
+  if (phased_) launches_ += 10 * std::max(0, res.iterations - 1);  // graph replays of the iteration
   res.converged = state[2] != 0;
   res.negative_curvature = state[3] != 0;
   launches_ += 1;  // the persistent CG kernel
@@ -802,9 +830,106 @@ void Workspace::apply_operator(double theta, const double* v, double* out) {
   apply_l2_policy();
   const size_t nd = plan.n_delta;
   DDG_CUDA(cudaMemcpyAsync(d_vin.ptr, v, nd * sizeof(double), cudaMemcpyHostToDevice, st_));
-  cg_launch(a, kJobApply, d_vin.ptr, d_vout.ptr, st_);
+  if (phased_) run_phases(a, 0, d_vin.ptr, d_vout.ptr);
+  else cg_launch(a, kJobApply, d_vin.ptr, d_vout.ptr, st_);
   DDG_CUDA(cudaMemcpyAsync(out, d_vout.ptr, nd * sizeof(double), cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Workspace::xchg(double* send, double* recv, size_t n) {
+  if (ex_ && n) ex_->allreduce(send, recv, n, st_);
+}
+
+void Workspace::run_phases(const CgArgs& a, int mode, const double* vin, double* vout) {
+  // one operator application (mode 0), the reduced rhs (1) or the reconstruction (2), phase by
+  // phase, all-reducing each owner-slot table between its producer and its consumers
+  const size_t npi4 = 4 * static_cast<size_t>(plan.n_pi), npf4 = 4 * static_cast<size_t>(plan.npf);
+  const size_t tab = static_cast<size_t>(a.P) * 2 * plan.n_delta;
+  cg_launch_phase(a, kPhOp1, mode, 0, vin, vout, st_);
+  xchg(a.ttab_w, a.ttab, npi4);
+  xchg(a.ptab_w, a.ptab, npf4);
+  cg_launch_phase(a, kPhOp2, mode, 0, vin, vout, st_);
+  if (mode == 2) return;
+  xchg(a.xtab_w, a.xtab, tab);
+  if (a.use_neumann) {
+    cg_launch_phase(a, kPhNn1, mode, 0, vin, vout, st_);
+    xchg(a.trtab_w, a.trtab, tab);
+    cg_launch_phase(a, kPhNn2, mode, 0, vin, vout, st_);
+    xchg(a.zztab_w, a.zztab, tab);
+  }
+  cg_launch_phase(a, kPhOp3, mode, 0, vin, vout, st_);
+  xchg(a.t3tab_w, a.t3tab, static_cast<size_t>(a.P) * npi4);
+  cg_launch_phase(a, kPhOp4, mode, 0, vin, vout, st_);
+  xchg(a.otab_w, a.otab, 2 * static_cast<size_t>(plan.n_delta));
+  cg_launch_phase(a, kPhGather, mode, 0, vin, vout, st_);
+}
+
+void Workspace::run_cg_phased(const CgArgs& a_in) {
+  // The CG loop as ONE CUDA graph: a conditional while node whose body is one iteration (the
+  // phase kernels and, when sharded, the owner-slot all-reduces, captured from this stream); the
+  // XR2 kernel sets the loop condition on the device, so there is no host round trip per
+  // iteration. DDELM_CG_GRAPH=0 falls back to a host loop with one stopping-test read-back per
+  // iteration.
+  const size_t npi4 = 4 * static_cast<size_t>(plan.n_pi), npf4 = 4 * static_cast<size_t>(plan.npf);
+  const size_t tab = static_cast<size_t>(a_in.P) * 2 * plan.n_delta;
+  auto iteration = [&](const CgArgs& a) {
+    cg_launch_phase(a, kPhOp1, 0, 0, nullptr, nullptr, st_);
+    xchg(a.ttab_w, a.ttab, npi4);
+    xchg(a.ptab_w, a.ptab, npf4);
+    cg_launch_phase(a, kPhOp2, 0, 0, nullptr, nullptr, st_);
+    xchg(a.xtab_w, a.xtab, tab);
+    if (a.use_neumann) {
+      cg_launch_phase(a, kPhNn1, 0, 0, nullptr, nullptr, st_);
+      xchg(a.trtab_w, a.trtab, tab);
+      cg_launch_phase(a, kPhNn2, 0, 0, nullptr, nullptr, st_);
+      xchg(a.zztab_w, a.zztab, tab);
+    }
+    cg_launch_phase(a, kPhOp3, 0, 0, nullptr, nullptr, st_);
+    xchg(a.t3tab_w, a.t3tab, static_cast<size_t>(a.P) * npi4);
+    cg_launch_phase(a, kPhOp4, 0, 0, nullptr, nullptr, st_);
+    xchg(a.otab_w, a.otab, 2 * static_cast<size_t>(plan.n_delta));
+    xchg(a.pap_w, a.pap, static_cast<size_t>(plan.N_global));
+    cg_launch_phase(a, kPhXr1, 0, 0, nullptr, nullptr, st_);
+    cg_launch_phase(a, kPhXr2, 0, 0, nullptr, nullptr, st_);
+  };
+  const char* ge = std::getenv("DDELM_CG_GRAPH");
+  if (ge && std::strcmp(ge, "0") == 0) {
+    CgArgs a = a_in;
+    a.cond = 0;
+    for (int it = 1; it <= a.max_iter; ++it) {
+      iteration(a);
+      DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+      DDG_CUDA(cudaStreamSynchronize(st_));
+      launches_ += 10;
+      if (pinned_state_[1]) break;
+    }
+    return;
+  }
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge_exec = nullptr;
+  DDG_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h = 0;
+  DDG_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  DDG_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CgArgs a = a_in;
+  a.cond = static_cast<unsigned long long>(h);
+  DDG_CUDA(cudaStreamBeginCaptureToGraph(st_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  iteration(a);
+  cudaGraph_t captured = nullptr;
+  DDG_CUDA(cudaStreamEndCapture(st_, &captured));
+  DDG_CUDA(cudaGraphInstantiate(&ge_exec, g, 0));
+  DDG_CUDA(cudaGraphLaunch(ge_exec, st_));
+  launches_ += 10;  // per iteration (the graph replays them)
+  DDG_CUDA(cudaStreamSynchronize(st_));
+  DDG_CUDA(cudaGraphExecDestroy(ge_exec));
+  DDG_CUDA(cudaGraphDestroy(g));
 }
 
 void Workspace::get_mu(double* mu) {

@@ -7,6 +7,9 @@
 #include <string>
 #include <vector>
 
+#include <memory>
+
+#include "comm.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
 
@@ -65,7 +68,9 @@ struct SolveResult {
 
 class Workspace {
  public:
-  Workspace(const Plan& p, int device);
+  /// p: the (possibly sharded, see shard_plan) plan of this device; ex: the cross-GPU exchange
+  /// (nullptr: single device)
+  Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex = nullptr);
   ~Workspace();
   Workspace(const Workspace&) = delete;
   Workspace& operator=(const Workspace&) = delete;
@@ -104,6 +109,14 @@ class Workspace {
   CodArgs cod_args();
   BlockArgs block_args();
   CgArgs cg_args(double theta, double tol, int max_iter);
+  bool sharded() const { return ex_ && ex_->world() > 1; }
+  /// phase-by-phase launches with owner-slot all-reduces (sharded path; DDELM_CG_MODE=phased
+  /// selects it on one device too)
+  void run_phases(const CgArgs& a, int mode, const double* vin, double* vout);
+  void run_cg_phased(const CgArgs& a);
+  void xchg(double* send, double* recv, size_t n);
+  std::unique_ptr<Exchange> ex_;
+  bool phased_ = false;
   // kernel timers: begin/end around a launch; collected after the stream syncs
   int ktimer_begin();
   void ktimer_end(int slot, const char* family, double flops, double bytes);
@@ -153,6 +166,8 @@ class Workspace {
   // CG
   DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu_pi_out, d_tpart, d_tpart3,
       d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_pap, d_vin, d_vout, d_trace, d_KF, d_KD;
+  // receive side of the owner-slot all-reduces (sharded only)
+  DevBuf<double> r_tpart, r_psipart, r_tpart3, r_o, r_xf, r_tr, r_zz, r_pap, d_Gsum;
   int ldKF_ = 0, ldKD_ = 0;
 };
 

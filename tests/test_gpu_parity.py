@@ -231,3 +231,22 @@ def test_cpp_facade_matches_python_path(P):
     assert np.array_equal(np.array(d["mu"]), rep.mu)
     bad = subprocess.run([exe, "theta=1.5"], capture_output=True, text=True, timeout=120)
     assert bad.returncode == 3 and "theta" in bad.stderr
+
+
+@pytest.mark.parametrize("name", ["T2", "C2"])
+def test_sharded_path_world1_matches_persistent(P, name):
+    """The sharded path (phase-by-phase launches + owner-slot all-reduces, ddelm_gpu_create_sharded)
+    run with world = 1 reproduces the persistent single-device kernel bit for bit: the same work
+    split and the same fixed-order sums. (With world > 1 the exchanged tables carry exact zeros in
+    non-owned slots; tests/test_sharding.py checks that partition over real gloo ranks.)"""
+    ws_a = P.workspace_from_config(name)
+    ws_b = P.workspace_from_config(name, shard=(0, 1, None))
+    assert (ws_b.sub_lo, ws_b.n_local, ws_b.n_global) == (0, ws_a.n_subs, ws_a.n_subs)
+    _, ra = P.solve_config(name, ws=ws_a)
+    _, rb = P.solve_config(name, ws=ws_b)
+    assert ra.iterations == rb.iterations
+    assert np.array_equal(ra.mu, rb.mu)
+    assert np.array_equal(ra.coeffs, rb.coeffs)
+    assert np.array_equal(ra.residual_history, rb.residual_history)
+    v = np.random.default_rng(3).standard_normal(ws_a.n_delta)
+    assert np.array_equal(ws_a.apply_operator(v), ws_b.apply_operator(v))
