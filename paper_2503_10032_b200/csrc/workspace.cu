@@ -752,7 +752,7 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   DDG_CUDA(cudaMemcpyAsync(state, d_state.ptr, sizeof(state), cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
   res.iterations = state[5];
-  if (phased_) launches_ += 10 * std::max(0, res.iterations - 1);  // graph replays of the iteration
+  if (phased_) launches_ += 8 * std::max(0, res.iterations - 1);  // graph replays of the iteration
   res.converged = state[2] != 0;
   res.negative_curvature = state[3] != 0;
   launches_ += 1;  // the persistent CG kernel
@@ -900,7 +900,7 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
       iteration(a);
       DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
       DDG_CUDA(cudaStreamSynchronize(st_));
-      launches_ += 10;
+      launches_ += 8;
       if (pinned_state_[1]) break;
     }
     return;
@@ -926,7 +926,7 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
   DDG_CUDA(cudaStreamEndCapture(st_, &captured));
   DDG_CUDA(cudaGraphInstantiate(&ge_exec, g, 0));
   DDG_CUDA(cudaGraphLaunch(ge_exec, st_));
-  launches_ += 10;  // per iteration (the graph replays them)
+  launches_ += 8;  // one iteration's phase kernels (the graph replays them; see solve())
   DDG_CUDA(cudaStreamSynchronize(st_));
   DDG_CUDA(cudaGraphExecDestroy(ge_exec));
   DDG_CUDA(cudaGraphDestroy(g));

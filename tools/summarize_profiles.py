@@ -91,11 +91,50 @@ def report(name, rep, tag):
     return None
 
 
+def report_multi(name, rep, tag, scale_to=1, skip=0, count=None):
+    """A report holding several kernels (e.g. the 10 phase kernels of one CG iteration): per-kernel
+    duration and DRAM bytes, summed; traffic = sum x scale_to (iterations per solve)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(out.splitlines()))
+    h, units = r[0], r[1]
+    idx = {k: i for i, k in enumerate(h)}
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
+
+    def val(row, k):
+        try:
+            return float(row[idx[k]].replace(",", "")) * mult.get(units[idx[k]], 1)
+        except (KeyError, ValueError):
+            return 0.0
+
+    lines = [f"# ncu --set full --clock-control none: {os.path.basename(rep)} ({name}, kernels {skip}.."
+             f"{skip + (count if count is not None else len(r) - 2 - skip) - 1} of {len(r) - 2}; caches flushed"
+             " between kernels by ncu, so cross-kernel L2 reuse is not credited)"]
+    tot_t = tot_b = 0.0
+    rows = r[2 + skip:]
+    if count is not None:
+        rows = rows[:count]
+    for row in rows:
+        t = val(row, "gpu__time_duration.sum")
+        b = val(row, "dram__bytes_read.sum") + val(row, "dram__bytes_write.sum")
+        dm = row[idx.get("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", 0)]
+        kname = row[idx["Kernel Name"]].split("(")[0].split("::")[-1] if "Kernel Name" in idx else "?"
+        lines.append(f"  {kname:40s} {t * 1e6:9.2f} us  dram {b / 1e6:9.2f} MB  {b / max(t, 1e-12) / 1e9:8.1f} GB/s")
+        tot_t += t
+        tot_b += b
+    lines.append(f"# sum: {tot_t * 1e6:.2f} us, dram {tot_b / 1e6:.2f} MB ({tot_b / max(tot_t, 1e-12) / 1e9:.1f} GB/s); "
+                 f"x{scale_to} -> {tot_b * scale_to:.4g} bytes per solve")
+    open(os.path.join(PROF, f"{tag}_ncu_{name}.txt"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    return tot_b * scale_to
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("tag")
     ap.add_argument("--launches", default=None)
     ap.add_argument("--rep", action="append", default=[])
+    ap.add_argument("--multi", action="append", default=[],
+                    help="name=rep=scale[=skip[=count]] (sum over the selected kernels x scale)")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
@@ -107,6 +146,13 @@ def main():
         b = report(name, rep, a.tag)
         if b is not None:
             traffic[name] = {"dram_bytes_per_launch": b, "source": f"profiles/{a.tag}_ncu_{name}.txt"}
+    for spec in a.multi:
+        parts = spec.split("=")
+        name, rep, scale = parts[0], parts[1], int(parts[2])
+        skip = int(parts[3]) if len(parts) > 3 else 0
+        count = int(parts[4]) if len(parts) > 4 else None
+        b = report_multi(name, rep, a.tag, scale, skip, count)
+        traffic[name] = {"dram_bytes_per_launch": b, "source": f"profiles/{a.tag}_ncu_{name}.txt"}
     json.dump(traffic, open(tpath, "w"), indent=1)
 
 
