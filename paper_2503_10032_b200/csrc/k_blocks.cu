@@ -346,13 +346,15 @@ void launch_coarse_schur(const BlockArgs& a, cudaStream_t st) {
 }
 
 namespace {
-__global__ void pack_streams_kernel(BlockArgs a, double* KF, int ldKF, double* KD, int ldKD) {
+__global__ void pack_streams_kernel(BlockArgs a, double* KF, const int* kf_ld, const long long* kf_off, double* KD,
+                                    const int* kd_ld, const long long* kd_off) {
   const int i = blockIdx.y;
   const int R = a.rmax;
+  const int ldKF = kf_ld[i], ldKD = kd_ld[i];  // per-subdomain strides: no padding to the widest class
   for (int j = blockIdx.x; j < a.M; j += gridDim.x) {
     const size_t row = static_cast<size_t>(i) * a.M + j;
-    double* kf = KF + row * ldKF;
-    double* kd = KD + row * ldKD;
+    double* kf = KF + kf_off[i] + static_cast<size_t>(j) * ldKF;
+    double* kd = KD + kd_off[i] + static_cast<size_t>(j) * ldKD;
     const double* c = a.C + row * R;
     const double* cb = a.C + (static_cast<size_t>(a.N + i) * a.M + j) * R;
     for (int k = threadIdx.x; k < ldKF; k += blockDim.x) {
@@ -372,9 +374,10 @@ __global__ void pack_streams_kernel(BlockArgs a, double* KF, int ldKF, double* K
 }
 }  // namespace
 
-void launch_pack_streams(const BlockArgs& a, double* KF, int ldKF, double* KD, int ldKD, cudaStream_t st) {
+void launch_pack_streams(const BlockArgs& a, double* KF, const int* kf_ld, const long long* kf_off, double* KD,
+                         const int* kd_ld, const long long* kd_off, cudaStream_t st) {
   dim3 g(std::min(a.M, 64), a.N);
-  pack_streams_kernel<<<g, 256, 0, st>>>(a, KF, ldKF, KD, ldKD);
+  pack_streams_kernel<<<g, 256, 0, st>>>(a, KF, kf_ld, kf_off, KD, kd_ld, kd_off);
   DDG_LAUNCH_CHECK();
 }
 

@@ -176,21 +176,22 @@ __device__ __forceinline__ ItemGeo item_geo(const CgArgs& a, int kind, int i, in
   part_rows(a, p, j0, j1);
   const ClassDims d = a.dims[a.sub_cls[i]];
   const int R = a.rmax;
-  const double* KF = a.KF + (static_cast<size_t>(i) * a.M + j0) * a.ldKF;
-  const double* KD = a.KD + (static_cast<size_t>(i) * a.M + j0) * a.ldKD;
+  const int ldf = a.kf_ld[i], ldd = a.kd_ld[i];
+  const double* KF = a.KF + a.kf_off[i] + static_cast<size_t>(j0) * ldf;
+  const double* KD = a.KD + a.kd_off[i] + static_cast<size_t>(j0) * ldd;
   ItemGeo g;
   switch (kind) {
     case kOp2:  // A = C, Y = Ypi, B = F
-      g = {KF, a.ldKF, 0, recon ? -1 : R + 4, R, j1 - j0, a.rank[i], recon ? 0 : d.nF, 0, 0, false};
+      g = {KF, ldf, 0, recon ? -1 : R + 4, R, j1 - j0, a.rank[i], recon ? 0 : d.nF, 0, 0, false};
       break;
     case kNn1:  // A = Cbar, B = Cdelta
-      g = {KD, a.ldKD, 0, R, -1, j1 - j0, a.rank[a.N + i], d.nd, 0, 0, false};
+      g = {KD, ldd, 0, R, -1, j1 - j0, a.rank[a.N + i], d.nd, 0, 0, false};
       break;
     case kNn2:  // A = Cdelta, B = Cbar
-      g = {KD, a.ldKD, R, 0, -1, j1 - j0, d.nd, a.rank[a.N + i], 0, 0, true};
+      g = {KD, ldd, R, 0, -1, j1 - j0, d.nd, a.rank[a.N + i], 0, 0, true};
       break;
     default:    // OP3: A = F, B = C
-      g = {KF, a.ldKF, R + 4, 0, -1, j1 - j0, d.nF, a.rank[i], 0, 0, true};
+      g = {KF, ldf, R + 4, 0, -1, j1 - j0, d.nF, a.rank[i], 0, 0, true};
       break;
   }
   g.rpc = rows_per_chunk(g.ld);
@@ -1021,7 +1022,8 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
   double* pcur = a.pbuf[(it + 1) & 1];
   double* pnext = a.pbuf[it & 1];
   if (cg && a.state[1]) {  // converged / aborted earlier
-    if (phase == kPhXr2 && b == 0 && threadIdx.x == 0 && a.cond != 0) cudaGraphSetConditional(a.cond, 0);
+    if ((phase == kPhXr1 || phase == kPhXr2) && b == 0 && threadIdx.x == 0 && a.cond != 0)
+      cudaGraphSetConditional(a.cond, 0);
     return;
   }
   switch (phase) {
@@ -1059,36 +1061,47 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
         if (cg && threadIdx.x == 0) a.pap_w[a.sub_lo + i] = dot;
       }
       return;
-    case kPhXr1: {  // alpha, x / r update, r.r partials (solvers.cpp:96-107)
-      const double pAp = det_sum(a.pap, a.N_global);
-      if (pAp <= 0.0) {
-        if (b == 0 && threadIdx.x == 0) {
-          a.state[3] = pAp < 0.0 ? 1 : 0;
-          a.state[5] = it - 1;
-          a.state[1] = 1;
+    case kPhXr1:    // alpha, x / r update, r.r partials (solvers.cpp:96-107); the last CTA to finish
+    case kPhXr2: {  // also takes the stopping decision (solvers.cpp:108-116) — one launch per iteration
+      __shared__ int s_last;
+      if (phase == kPhXr1) {
+        const double pAp = det_sum(a.pap, a.N_global);
+        if (pAp <= 0.0) {
+          if (b == 0 && threadIdx.x == 0) {
+            a.state[3] = pAp < 0.0 ? 1 : 0;
+            a.state[5] = it - 1;
+            a.state[1] = 1;
+            if (a.cond != 0) cudaGraphSetConditional(a.cond, 0);
+          }
+          return;
         }
+        const double alpha = a.scal[0] / pAp;
+        double dsum = 0;
+        for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) {
+          const double ap = gather_out(a, g);
+          a.x[g] += alpha * pnext[g];
+          const double rg = a.r[g] - alpha * ap;
+          a.r[g] = rg;
+          dsum += rg * rg;
+        }
+        dsum = block_sum(dsum, bsum);
+        if (threadIdx.x == 0) {
+          a.partial[b] = dsum;
+          __threadfence();
+          s_last = atomicAdd(&a.state[7], 1) == G - 1;  // arrival counter (reset by cg_init / below)
+        }
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+      } else if (b != 0) {
         return;
       }
-      const double alpha = a.scal[0] / pAp;
-      double dsum = 0;
-      for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) {
-        const double ap = gather_out(a, g);
-        a.x[g] += alpha * pnext[g];
-        const double rg = a.r[g] - alpha * ap;
-        a.r[g] = rg;
-        dsum += rg * rg;
-      }
-      dsum = block_sum(dsum, bsum);
-      if (threadIdx.x == 0) a.partial[b] = dsum;
-      return;
-    }
-    case kPhXr2: {  // one CTA: ||r||, history, stopping test, beta (solvers.cpp:108-116)
-      if (b != 0) return;
       const double rr_new = det_sum(a.partial, a.xr_parts);
       const double rel = sqrt(rr_new) / a.scal[1];
       const bool stop = rel <= a.rel_tol || it >= a.max_iter;
       __syncthreads();
       if (threadIdx.x == 0) {
+        a.state[7] = 0;
         a.hist[it - 1] = rel;
         a.state[5] = it;
         if (stop) {

@@ -125,7 +125,8 @@ void launch_coarse_gsum(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_schur(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_weights(const BlockArgs& a, cudaStream_t st);
 /// Pack the CG stream blocks KF = [C | Ypi | F] and KD = [Cbar | Cdelta] (row-interleaved).
-void launch_pack_streams(const BlockArgs& a, double* KF, int ldKF, double* KD, int ldKD, cudaStream_t st);
+void launch_pack_streams(const BlockArgs& a, double* KF, const int* kf_ld, const long long* kf_off, double* KD,
+                         const int* kd_ld, const long long* kd_off, cudaStream_t st);
 
 // ---------------------------------------------------------------- C5 microbenchmark (k_lsq.cu)
 struct LsqArgs {
@@ -147,9 +148,13 @@ struct CgArgs {
   //   KF : [ C_j (rmax) | Ypi_j (4) | F_j (fmax) ]        stride ldKF (even)
   //   KD : [ Cbar_j (rmax) | Cdelta_j (dmax) ]             stride ldKD (even)
   const double* KF;
-  int ldKF;
+  int ldKF;                 // widest row (capacity); per subdomain: kf_ld[i], block at KF + kf_off[i]
   const double* KD;
   int ldKD;
+  const int* kf_ld;
+  const int* kd_ld;
+  const long long* kf_off;
+  const long long* kd_off;
   double rel_tol;
   int max_iter;
   const int* rank;         // 2N

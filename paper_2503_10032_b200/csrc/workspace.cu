@@ -65,6 +65,7 @@ template struct DevBuf<double>;
 template struct DevBuf<int>;
 template struct DevBuf<Task>;
 template struct DevBuf<ClassDims>;
+template struct DevBuf<long long>;
 
 Workspace::Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex)
     : plan(p), ex_(std::move(ex)), device_(device) {
@@ -557,11 +558,35 @@ void Workspace::build_coarse() {
     launches_ += 5;
   }
   // row-interleaved stream blocks of the interface iteration (k_cg.cu)
-  ldKF_ = (rmax_ + 4 + plan.fmax + 1) / 2 * 2;
-  ldKD_ = (rmax_ + plan.dmax + 1) / 2 * 2;
-  d_KF.alloc(static_cast<size_t>(plan.N) * plan.M * ldKF_);
-  d_KD.alloc(static_cast<size_t>(plan.N) * plan.M * ldKD_);
-  launch_pack_streams(b, d_KF.ptr, ldKF_, d_KD.ptr, ldKD_, st_);
+  // per-subdomain row strides (boundary subdomains have fewer flux / Neumann rows: no padding
+  // to the widest class is streamed); even strides keep every row 16-byte aligned
+  {
+    std::vector<int> kfl(plan.N), kdl(plan.N);
+    std::vector<long long> kfo(plan.N), kdo(plan.N);
+    long long of = 0, od = 0;
+    ldKF_ = ldKD_ = 2;
+    for (int i = 0; i < plan.N; ++i) {
+      const ClassPlan& c = plan.classes[plan.subs[i].cls];
+      kfl[i] = (rmax_ + 4 + c.nF + 1) / 2 * 2;
+      kdl[i] = (rmax_ + c.nd + 1) / 2 * 2;
+      kfo[i] = of;
+      kdo[i] = od;
+      of += static_cast<long long>(plan.M) * kfl[i];
+      od += static_cast<long long>(plan.M) * kdl[i];
+      ldKF_ = std::max(ldKF_, kfl[i]);
+      ldKD_ = std::max(ldKD_, kdl[i]);
+    }
+    {
+      ArenaScope hot(&arena_);
+      d_kf_ld.upload(kfl, st_);
+      d_kd_ld.upload(kdl, st_);
+      d_kf_off.upload(kfo, st_);
+      d_kd_off.upload(kdo, st_);
+    }
+    d_KF.alloc(static_cast<size_t>(of));
+    d_KD.alloc(static_cast<size_t>(od));
+  }
+  launch_pack_streams(b, d_KF.ptr, d_kf_ld.ptr, d_kf_off.ptr, d_KD.ptr, d_kd_ld.ptr, d_kd_off.ptr, st_);
   launches_ += 1;
   DDG_CUDA(cudaEventRecord(ev_[5], st_));
   int fail = 0;
@@ -602,6 +627,10 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.ldKF = ldKF_;
   a.KD = d_KD.ptr;
   a.ldKD = ldKD_;
+  a.kf_ld = d_kf_ld.ptr;
+  a.kd_ld = d_kd_ld.ptr;
+  a.kf_off = d_kf_off.ptr;
+  a.kd_off = d_kd_off.ptr;
   {
     // row parts per subdomain so that N * P work items cover the SMs (DDELM_CG_PARTS overrides)
     int dev = 0, sms = 148;
@@ -752,7 +781,7 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   DDG_CUDA(cudaMemcpyAsync(state, d_state.ptr, sizeof(state), cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
   res.iterations = state[5];
-  if (phased_) launches_ += 8 * std::max(0, res.iterations - 1);  // graph replays of the iteration
+  if (phased_) launches_ += 7 * std::max(0, res.iterations - 1);  // graph replays of the iteration
   res.converged = state[2] != 0;
   res.negative_curvature = state[3] != 0;
   launches_ += 1;  // the persistent CG kernel
@@ -889,8 +918,7 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
     cg_launch_phase(a, kPhOp4, 0, 0, nullptr, nullptr, st_);
     xchg(a.otab_w, a.otab, 2 * static_cast<size_t>(plan.n_delta));
     xchg(a.pap_w, a.pap, static_cast<size_t>(plan.N_global));
-    cg_launch_phase(a, kPhXr1, 0, 0, nullptr, nullptr, st_);
-    cg_launch_phase(a, kPhXr2, 0, 0, nullptr, nullptr, st_);
+    cg_launch_phase(a, kPhXr1, 0, 0, nullptr, nullptr, st_);  // its last CTA also runs XR2
   };
   const char* ge = std::getenv("DDELM_CG_GRAPH");
   if (ge && std::strcmp(ge, "0") == 0) {
@@ -900,7 +928,7 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
       iteration(a);
       DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
       DDG_CUDA(cudaStreamSynchronize(st_));
-      launches_ += 8;
+      launches_ += 7;
       if (pinned_state_[1]) break;
     }
     return;
@@ -926,7 +954,7 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
   DDG_CUDA(cudaStreamEndCapture(st_, &captured));
   DDG_CUDA(cudaGraphInstantiate(&ge_exec, g, 0));
   DDG_CUDA(cudaGraphLaunch(ge_exec, st_));
-  launches_ += 8;  // one iteration's phase kernels (the graph replays them; see solve())
+  launches_ += 7;  // one iteration's phase kernels (the graph replays them; see solve())
   DDG_CUDA(cudaStreamSynchronize(st_));
   DDG_CUDA(cudaGraphExecDestroy(ge_exec));
   DDG_CUDA(cudaGraphDestroy(g));

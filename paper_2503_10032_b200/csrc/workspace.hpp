@@ -162,6 +162,8 @@ class Workspace {
   DevBuf<int> d_deficient, d_rank, d_status, d_perm, d_corner_q, d_spd_fail, d_state;
   DevBuf<double> d_V1, d_F1, d_Rr, d_tau1, d_zc, d_upd, d_dir, d_C, d_Y, d_QtX;
   // interface blocks / coarse
+  DevBuf<int> d_kf_ld, d_kd_ld;
+  DevBuf<long long> d_kf_off, d_kd_off;
   DevBuf<double> d_FC, d_Zc, d_pd, d_Gc, d_Ypi, d_Dpp, d_dpi, d_S, d_Sinv, d_Wmu, d_Wd, d_W3;
   // CG
   DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu_pi_out, d_tpart, d_tpart3,
