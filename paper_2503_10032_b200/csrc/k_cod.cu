@@ -24,6 +24,7 @@ namespace ddg {
 namespace {
 
 constexpr int kRecB = 8;  // flagged columns recomputed per register-blocked pass
+constexpr double kRowTruncation = 1e-14;  // R0 rows with tail energy below this x ||R0||_F are dropped
 constexpr int kNPL = 32;  // register rows per lane in the finish kernel: M <= 32 * 32
 
 struct ArgMax {
@@ -99,10 +100,43 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
   const double eps = DBL_EPSILON;
   const double downdate_thr = sqrt(eps);
 
+  // ---- effective row count of R0: rows whose tail energy ||R0(i:, i:)||_F is below
+  //      kRowTruncation * ||R0||_F carry only round-off (the numerical rank is ~70 of M = 800), so
+  //      the pivoted factorisation reads rows < Reff only — a perturbation of the column norms far
+  //      below the rank threshold (1e-10 |R_00|), the regime of the oracle's own 1-ulp spread
+  __shared__ int s_reff;
+  {
+    double* rowsq = v;  // scratch (M)
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+      double s = 0;
+      for (int j = i; j < M; ++j) {
+        const double e = R0[static_cast<size_t>(j) * ld + i];
+        s += e * e;
+      }
+      rowsq[i] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0;
+      for (int i = 0; i < M; ++i) tot += rowsq[i];
+      const double lim = kRowTruncation * kRowTruncation * tot;
+      double tail = 0;
+      int reff = M;
+      for (int i = M - 1; i >= 1; --i) {
+        tail += rowsq[i];
+        if (tail > lim) break;
+        reff = i;
+      }
+      s_reff = reff;
+      a.reff[t] = reff;
+    }
+    __syncthreads();
+  }
+  const int Reff = s_reff;
   // initial column norms (of R0 = of K up to rounding)
   for (int j = warp; j < M; j += nwarp) {
     double s = 0;
-    for (int i = lane; i <= j; i += 32) {
+    for (int i = lane; i <= min(j, Reff - 1); i += 32) {
       const double e = R0[static_cast<size_t>(j) * ld + i];
       s += e * e;
     }
@@ -151,14 +185,17 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
     for (int u = threadIdx.x; u < k; u += blockDim.x) w[u] = F1[static_cast<size_t>(k) * K + u];
     __syncthreads();
     for (int i = k + threadIdx.x; i < M; i += blockDim.x) {
-      double s = (i <= ck) ? R0[static_cast<size_t>(ck) * ld + i] : 0.0;
-      for (int u = 0; u < k; ++u) s -= V1[static_cast<size_t>(u) * M + i] * w[u];
+      double s = 0.0;
+      if (i < Reff) {
+        s = (i <= ck) ? R0[static_cast<size_t>(ck) * ld + i] : 0.0;
+        for (int u = 0; u < k; ++u) s -= V1[static_cast<size_t>(u) * M + i] * w[u];
+      }
       v[i] = s;
     }
     __syncthreads();
     // ---- Householder (makeHouseholderInPlace)
     double part = 0;
-    for (int i = k + 1 + threadIdx.x; i < M; i += blockDim.x) part += v[i] * v[i];
+    for (int i = k + 1 + threadIdx.x; i < Reff; i += blockDim.x) part += v[i] * v[i];
     const double tail = block_sum(part, red);
     const double alpha = v[k];
     double tau = 0, beta = alpha, scale = 0;
@@ -187,7 +224,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
     // ---- w = V(:, 0:k)^T v ; vk = V(k, 0:k]
     for (int u = warp; u < k; u += nwarp) {
       double s = 0;
-      for (int i = k + lane; i < M; i += 32) s += V1[static_cast<size_t>(u) * M + i] * v[i];
+      for (int i = k + lane; i < Reff; i += 32) s += V1[static_cast<size_t>(u) * M + i] * v[i];
       s = warp_sum(s);
       if (lane == 0) w[u] = s;
     }
@@ -203,7 +240,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
         const int j = min(j0 + q, M - 1);
         const int cj = perm[j];
         col[q] = R0 + static_cast<size_t>(cj) * ld;
-        iend[q] = (j0 + q < M) ? min(cj, M - 1) : k - 1;
+        iend[q] = (j0 + q < M) ? min(cj, Reff - 1) : k - 1;
       }
       const int imax = max(max(iend[0], iend[1]), max(iend[2], iend[3]));
       double g[4] = {0, 0, 0, 0}, fw[4] = {0, 0, 0, 0};
@@ -279,7 +316,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
       double acc[kRecB];
 #pragma unroll
       for (int q = 0; q < kRecB; ++q) acc[q] = 0.0;
-      for (int i = k + 1 + threadIdx.x; i < M; i += blockDim.x) {
+      for (int i = k + 1 + threadIdx.x; i < Reff; i += blockDim.x) {
         double e[kRecB];
 #pragma unroll
         for (int q = 0; q < kRecB; ++q) e[q] = (i <= cjs[q]) ? R0[static_cast<size_t>(cjs[q]) * ld + i] : 0.0;

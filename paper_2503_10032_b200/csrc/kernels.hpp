@@ -73,6 +73,7 @@ struct CodArgs {
   int* perm;     // M
   int* rank;     // per matrix
   int* status;   // per matrix: 0 ok, 1 capacity exceeded
+  int* reff;     // per matrix: rows of R0 kept by the pivoted factorisation (diagnostic)
   double* zc;    // kmax RZ reflector coefficients
   // outputs (rmax-strided, allocated after ranks are known)
   double* C;     // nmat x M x rmax   : K^+ = C Q_r^T (C row i = original column i)

@@ -231,6 +231,7 @@ void Workspace::upload_plan() {
   d_rank.alloc(nmat);
   g_arena = nullptr;
   d_status.alloc(nmat);
+  d_reff.alloc(nmat);
   d_V1.alloc(nmat * kmax_ * p.M);
   d_F1.alloc(nmat * p.M * kmax_);
   d_Rr.alloc(nmat * kmax_ * p.M);
@@ -423,6 +424,7 @@ CodArgs Workspace::cod_args() {
   c.perm = d_perm.ptr;
   c.rank = d_rank.ptr;
   c.status = d_status.ptr;
+  c.reff = d_reff.ptr;
   c.zc = d_zc.ptr;
   c.C = d_C.ptr;
   c.QtX = d_QtX.ptr;

@@ -159,7 +159,7 @@ class Workspace {
   DevBuf<double> d_cr_w, d_flip, d_f;
   // layers and matrices
   DevBuf<double> d_w0, d_w1, d_b, d_A, d_tau, d_T, d_ratio, d_F, d_Cd;
-  DevBuf<int> d_deficient, d_rank, d_status, d_perm, d_corner_q, d_spd_fail, d_state;
+  DevBuf<int> d_deficient, d_rank, d_status, d_reff, d_perm, d_corner_q, d_spd_fail, d_state;
   DevBuf<double> d_V1, d_F1, d_Rr, d_tau1, d_zc, d_upd, d_dir, d_C, d_Y, d_QtX;
   // interface blocks / coarse
   DevBuf<int> d_kf_ld, d_kd_ld;
