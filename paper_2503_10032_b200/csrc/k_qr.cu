@@ -182,8 +182,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, in
   }
   __syncthreads();
 
-  // G = V^T V over the panel (implicit unit diagonal, zeros above); thread -> (u, v), (u, v + 16)
+  // G = V^T V over the panel (implicit unit diagonal, zeros above) on DMMA: 16 warps = the 4 x 4
+  // grid of 8 x 8 tiles of G, 32-row chunks staged in shared memory
   const int u = threadIdx.x & 31, v = threadIdx.x >> 5;
+  const int tu = warp >> 2, tv = warp & 3, lr = lane >> 2, lc = lane & 3;
   double g0 = 0, g1 = 0;
   for (int r0 = k0; r0 < m; r0 += RC) {
     for (int idx = threadIdx.x; idx < RC * NB; idx += blockDim.x) {
@@ -197,15 +199,13 @@ __global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, in
       Vs[rr][uu] = val;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int rr = 0; rr < RC; ++rr) {
-      g0 += Vs[rr][u] * Vs[rr][v];
-      g1 += Vs[rr][u] * Vs[rr][v + 16];
-    }
+#pragma unroll
+    for (int kk = 0; kk < RC / 4; ++kk)
+      dmma_8x8x4(g0, g1, Vs[kk * 4 + lc][tu * 8 + lr], Vs[kk * 4 + lc][tv * 8 + lr]);
     __syncthreads();
   }
-  G[u][v] = g0;
-  G[u][v + 16] = g1;
+  G[tu * 8 + lr][tv * 8 + 2 * lc] = g0;
+  G[tu * 8 + lr][tv * 8 + 2 * lc + 1] = g1;
   __syncthreads();
   // T: T(j,j) = tau_j, T(0:j, j) = -tau_j T(0:j,0:j) G(0:j, j)
   if (warp == 0) {
