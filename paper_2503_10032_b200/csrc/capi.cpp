@@ -7,6 +7,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/ddelm_gpu.h"
 #include "common.cuh"
@@ -23,7 +24,8 @@ struct ddelm_lsq {
   int device = 0;
   ddg::LsqArgs a{};
   double *tau = nullptr, *T = nullptr;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr, side = nullptr;
+  std::vector<cudaEvent_t> qr_ev;
   cudaEvent_t ev[3] = {};
   ~ddelm_lsq() {
     cudaSetDevice(device);
@@ -33,6 +35,8 @@ struct ddelm_lsq {
     cudaFree(T);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : qr_ev) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -287,7 +291,12 @@ int ddelm_gpu_lsq_create(int nblocks, int m, int n, int k, int device, ddelm_lsq
     std::unique_ptr<ddelm_lsq> guard(L);
     L->device = device;
     DDG_CUDA(cudaSetDevice(device));
-    DDG_CUDA(cudaStreamCreateWithFlags(&L->st, cudaStreamNonBlocking));
+    {
+      int lo = 0, hi = 0;
+      DDG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      DDG_CUDA(cudaStreamCreateWithPriority(&L->st, cudaStreamNonBlocking, hi));
+      DDG_CUDA(cudaStreamCreateWithPriority(&L->side, cudaStreamNonBlocking, lo));
+    }
     for (auto& e : L->ev) DDG_CUDA(cudaEventCreate(&e));
     L->a = ddg::LsqArgs{nblocks, m, n, k, (m + 3) / 4 * 4, n + k, nullptr, nullptr};
     const size_t nA = static_cast<size_t>(nblocks) * L->a.ld * L->a.ncol;
@@ -317,7 +326,7 @@ int ddelm_gpu_lsq_factor(ddelm_lsq* L, double* qr_ms, double* schur_ms) {
     const ddg::LsqArgs& a = L->a;
     ddg::QrArgs q{a.nb, a.m, a.ld, a.ncol, a.n, a.A, L->tau, L->T};
     DDG_CUDA(cudaEventRecord(L->ev[0], L->st));
-    for (const ddg::QrOp& op : ddg::qr_schedule(a.n, a.ncol)) ddg::launch_qr_op(q, op, L->st);
+    ddg::qr_factor(q, L->st, L->side, L->qr_ev);
     DDG_CUDA(cudaEventRecord(L->ev[1], L->st));
     ddg::launch_lsq_gram(a, L->st);
     DDG_CUDA(cudaEventRecord(L->ev[2], L->st));

@@ -96,7 +96,7 @@ __device__ __forceinline__ void panel_pass(double* P, size_t ld, int m, int rlo,
   (void)n2;
 }
 
-__global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, int k0, int toff) {
+__global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, int k0, int toff, int combine) {
   const int t = blockIdx.x;
   double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
   const int m = a.m;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, in
   double* T = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
   for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x)
     T[(toff + (idx >> 5)) * kQrTmax + toff + (idx & 31)] = Tsh[idx >> 5][idx & 31];
-  if (toff == 0) return;
+  if (!combine) return;
   // ---- second half of a 64-wide block: T12 = -T1 (V1^T V2) T2, V1 = the 32 reflectors left of k0
   //      (rows >= k0 only: V2 is zero above its diagonal)
   const double* V1 = A + static_cast<size_t>(k0 - NB) * ld;
@@ -315,7 +315,7 @@ struct TrailSmem {
 };
 
 template <int NB_>
-__global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrArgs a, int k0, int nbw, int cb, int ce) {
+__global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrArgs a, int k0, int nbw, int cb, int ce, int tq) {
   static_assert(NB_ == 32 || NB_ == 64, "panel width");
   constexpr int MT = NB_ / 8;  // m-tiles of W
   extern __shared__ __align__(16) double smraw[];
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
   const double* Tg = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
   for (int idx = threadIdx.x; idx < NB_ * NB_; idx += blockDim.x) {
     const int i = idx / NB_, j = idx % NB_;
-    S.T[i * (NB_ + 1) + j] = (i < nb && j < nb) ? Tg[i * kQrTmax + j] : 0.0;
+    S.T[i * (NB_ + 1) + j] = (i < nb && j < nb) ? Tg[(tq + i) * kQrTmax + tq + j] : 0.0;
   }
 
   // ---- pass 1: W = V^T A_tile. Warp tile: (MT/2) m-tiles x 2 n-tiles.
@@ -533,21 +533,22 @@ std::vector<QrOp> qr_schedule(int M, int ncol) {
   for (int k0 = 0; k0 < M; k0 += bw) {
     const int w = std::min(bw, M - k0);
     if (w <= NB) {
-      ops.push_back({QrOp::kPanel, k0, 0, 0, 0, 0});
-      ops.push_back({QrOp::kTrail32, k0, w, k0 + w, ncol, 0});
+      const int tq = (k0 / NB) % 2 * NB;  // alternate T quadrants (look-ahead overlaps panels)
+      ops.push_back({QrOp::kPanel, k0, 0, 0, 0, tq, 0});
+      ops.push_back({QrOp::kTrail32, k0, w, k0 + w, ncol, tq, 0});
       continue;
     }
-    ops.push_back({QrOp::kPanel, k0, 0, 0, 0, 0});
-    ops.push_back({QrOp::kTrail32, k0, NB, k0 + NB, k0 + w, 0});
-    ops.push_back({QrOp::kPanel, k0 + NB, 0, 0, 0, NB});
-    ops.push_back({QrOp::kTrail64, k0, w, k0 + w, ncol, 0});
+    ops.push_back({QrOp::kPanel, k0, 0, 0, 0, 0, 0});
+    ops.push_back({QrOp::kTrail32, k0, NB, k0 + NB, k0 + w, 0, 0});
+    ops.push_back({QrOp::kPanel, k0 + NB, 0, 0, 0, NB, 1});
+    ops.push_back({QrOp::kTrail64, k0, w, k0 + w, ncol, 0, 0});
   }
   return ops;
 }
 
 void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
   if (op.kind == QrOp::kPanel) {
-    qr_panel_kernel<<<a.nmat, kPanelThreads, 0, st>>>(a, op.k0, op.toff);
+    qr_panel_kernel<<<a.nmat, kPanelThreads, 0, st>>>(a, op.k0, op.toff, op.combine);
     DDG_LAUNCH_CHECK();
     return;
   }
@@ -562,7 +563,7 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
                                     static_cast<int>(smem)));
       attr = true;
     }
-    qr_trailing_kernel<32><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce);
+    qr_trailing_kernel<32><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, op.toff);
   } else {
     const size_t smem = sizeof(TrailSmem<64>);
     static bool attr = false;
@@ -571,9 +572,50 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
                                     static_cast<int>(smem)));
       attr = true;
     }
-    qr_trailing_kernel<64><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce);
+    qr_trailing_kernel<64><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, 0);
   }
   DDG_LAUNCH_CHECK();
+}
+
+void qr_factor(const QrArgs& a, cudaStream_t main, cudaStream_t side, std::vector<cudaEvent_t>& ev) {
+  // Look-ahead blocked QR on two streams: after panel p, the next panel's 32 columns are updated
+  // first (main stream), so panel p+1 can start while the rest of the trailing update of panel p
+  // runs on the side stream. Dependencies (events): T_rest(p) needs panel p; the next-panel update
+  // T_next(p+1) needs T_rest(p) (same columns, reflectors applied in order).
+  // Off by default: measured no overlap on B200 (a 512-thread panel CTA needs a whole SM's
+  // registers, so it cannot co-reside with trailing CTAs) and ~2% slower; DDELM_QR_LOOKAHEAD=1.
+  const char* e = std::getenv("DDELM_QR_LOOKAHEAD");
+  const bool off = !(e && std::atoi(e) == 1) || side == nullptr;
+  const char* nbe = std::getenv("DDELM_QR_NB");
+  if (off || (nbe && std::atoi(nbe) == 64)) {
+    for (const QrOp& op : qr_schedule(a.M, a.ncol)) launch_qr_op(a, op, main);
+    return;
+  }
+  const int np = (a.M + NB - 1) / NB;
+  while (static_cast<int>(ev.size()) < 2 * np + 1) {
+    cudaEvent_t x;
+    DDG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    ev.push_back(x);
+  }
+  cudaEvent_t start = ev[2 * np];
+  DDG_CUDA(cudaEventRecord(start, main));
+  DDG_CUDA(cudaStreamWaitEvent(side, start, 0));
+  for (int p = 0; p < np; ++p) {
+    const int k0 = p * NB, nb = std::min(NB, a.M - k0);
+    const int nbn = std::min(NB, std::max(0, a.M - (k0 + nb)));  // next panel width
+    // T factors alternate between two quadrants: panel p+1 writes its T while T_rest(p), still
+    // running on the side stream, reads panel p's
+    const int tq = (p % 2) * NB;
+    if (p > 1) DDG_CUDA(cudaStreamWaitEvent(main, ev[2 * p - 3], 0));  // T_rest(p-2) read quadrant tq
+    launch_qr_op(a, QrOp{QrOp::kPanel, k0, 0, 0, 0, tq, 0}, main);
+    DDG_CUDA(cudaEventRecord(ev[2 * p], main));
+    if (p > 0) DDG_CUDA(cudaStreamWaitEvent(main, ev[2 * p - 1], 0));  // T_rest(p-1) done
+    if (nbn > 0) launch_qr_op(a, QrOp{QrOp::kTrail32, k0, nb, k0 + nb, k0 + nb + nbn, tq, 0}, main);
+    DDG_CUDA(cudaStreamWaitEvent(side, ev[2 * p], 0));
+    launch_qr_op(a, QrOp{QrOp::kTrail32, k0, nb, k0 + nb + nbn, a.ncol, tq, 0}, side);
+    DDG_CUDA(cudaEventRecord(ev[2 * p + 1], side));
+  }
+  DDG_CUDA(cudaStreamWaitEvent(main, ev[2 * np - 1], 0));
 }
 
 double qr_op_flops(const QrArgs& a, const QrOp& op) {

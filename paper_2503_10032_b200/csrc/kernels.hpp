@@ -43,16 +43,20 @@ struct QrArgs {
 };
 constexpr int kQrNB = 32;
 constexpr int kQrTmax = 64;
-/// One step of the blocked factorisation: a 32-column panel (toff = 32: second half of a 64-wide
-/// block, also forms the coupling block of the 64 x 64 T), or a DMMA trailing update with the
-/// nbw reflectors starting at k0 applied to columns [cb, ce).
+/// One step of the blocked factorisation: a 32-column panel writing its T factor to quadrant
+/// (toff, toff) of the per-matrix 64 x 64 T (combine = 1: second half of a 64-wide block, also
+/// forms the coupling block T12), or a DMMA trailing update with the nbw reflectors starting at k0
+/// (T read at quadrant toff) applied to columns [cb, ce).
 struct QrOp {
   enum Kind { kPanel, kTrail32, kTrail64 } kind;
-  int k0, nbw, cb, ce, toff;
+  int k0, nbw, cb, ce, toff, combine;
 };
 std::vector<QrOp> qr_schedule(int M, int ncol);
 void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st);
 double qr_op_flops(const QrArgs& a, const QrOp& op);
+/// The whole factorisation with look-ahead on two streams (DDELM_QR_LOOKAHEAD=0: the plain op
+/// schedule on `main`); `ev` is a reusable event pool.
+void qr_factor(const QrArgs& a, cudaStream_t main, cudaStream_t side, std::vector<cudaEvent_t>& ev);
 /// |R_ii| min / max per matrix -> ratio (branch test of LsFactor, solvers.cpp:27-32)
 void launch_qr_diag_ratio(const QrArgs& a, double* ratio, cudaStream_t st);
 

@@ -75,7 +75,14 @@ Workspace::Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex)
   phased_ = true;
   if (const char* m = std::getenv("DDELM_CG_MODE")) phased_ = std::strcmp(m, "persistent") != 0;
   DDG_CUDA(cudaSetDevice(device_));
-  DDG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  {
+    // main stream at the highest priority (QR panels are on the critical path), the look-ahead
+    // trailing updates on a default-priority side stream
+    int lo = 0, hi = 0;
+    DDG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    DDG_CUDA(cudaStreamCreateWithPriority(&st_, cudaStreamNonBlocking, hi));
+    DDG_CUDA(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, lo));
+  }
   DDG_CUDA(cudaStreamCreateWithFlags(&cap_, cudaStreamNonBlocking));
   for (auto& e : ev_) DDG_CUDA(cudaEventCreate(&e));
   DDG_CUDA(cudaMallocHost(&pinned_state_, 64));
@@ -119,6 +126,8 @@ Workspace::~Workspace() {
   if (graph_) cudaGraphDestroy(graph_);
   for (auto& e : ev_) cudaEventDestroy(e);
   if (pinned_state_) cudaFreeHost(pinned_state_);
+  for (cudaEvent_t e : qr_events_) cudaEventDestroy(e);
+  cudaStreamDestroy(side_);
   cudaStreamDestroy(cap_);
   cudaStreamDestroy(st_);
 }
@@ -445,11 +454,15 @@ void Workspace::build() {
   launches_ += 2;
   DDG_CUDA(cudaEventRecord(ev_[1], st_));
   QrArgs q{2 * p.N, p.m, ld_, ncol_, p.M, d_A.ptr, d_tau.ptr, d_T.ptr};
-  for (const QrOp& op : qr_schedule(p.M, ncol_)) {
+  {
+    // one timer over the look-ahead factorisation (panels overlap the trailing updates, so the
+    // two families cannot be timed separately); flops = panel + trailing work of the schedule
+    double fl = 0;
+    for (const QrOp& op : qr_schedule(p.M, ncol_)) fl += qr_op_flops(q, op);
     kt = ktimer_begin();
-    launch_qr_op(q, op, st_);
-    ktimer_end(kt, op.kind == QrOp::kPanel ? "qr_panel" : "qr_trailing", qr_op_flops(q, op), 0.0);
-    launches_ += (op.kind == QrOp::kPanel || op.ce > op.cb) ? 1 : 0;
+    qr_factor(q, st_, side_, qr_events_);
+    ktimer_end(kt, "qr_factor", fl, 0.0);
+    launches_ += 2 * ((p.M + kQrNB - 1) / kQrNB);
   }
   launch_qr_diag_ratio(q, d_ratio.ptr, st_);
   launches_ += 1;

@@ -138,7 +138,8 @@ class Workspace {
   Arena arena_;
   size_t l2_window_bytes_ = 0;
   void apply_l2_policy();
-  cudaStream_t st_ = nullptr, cap_ = nullptr;
+  cudaStream_t st_ = nullptr, cap_ = nullptr, side_ = nullptr;
+  std::vector<cudaEvent_t> qr_events_;
   cudaEvent_t ev_[12] = {};
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;

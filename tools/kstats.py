@@ -12,7 +12,7 @@ for name in sys.argv[1:]:
     ws.set_profiling(True)
     ws, rep = P.solve_config(name, ws=ws)
     out = []
-    for f in ("build_features", "qr_panel", "qr_trailing", "cod_pivqr", "cod_finish", "cg_iterations"):
+    for f in ("build_features", "qr_factor", "qr_panel", "qr_trailing", "cod_pivqr", "cod_finish", "cg_iterations"):
         try:
             s = ws.kernel_stats(f)
             out.append(f"{f}={s['ms']:.2f}ms/{s['launches']}")
