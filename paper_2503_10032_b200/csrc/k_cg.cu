@@ -41,6 +41,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -438,6 +439,7 @@ __device__ void coldot_split(const double* Q, int ldq, int nk, int nc, const dou
 struct QtxStage {
   unsigned cnt;
   int cached;
+  bool pending;  // a bulk copy into the ring is in flight for `cached`
 };
 
 /// Staged per-subdomain blocks of OP1 / OP4: Q_r^T [f | E] rows k < r (ldq = ext) and Zc.
@@ -446,23 +448,41 @@ struct Staged {
   const double* zc;
 };
 
-__device__ Staged stage_qtx(const CgArgs& a, const Shared& sh, QtxStage& q, int i, int r) {
+/// Issue the bulk copies of subdomain i's Q_r^T / Zc into the (idle) ring; false if they do not fit.
+__device__ bool stage_issue(const CgArgs& a, const Shared& sh, QtxStage& q, int i, int r, size_t* qbytes) {
   const double* src = a.QtX + static_cast<size_t>(i) * a.rmax * a.ext;
   const double* zsrc = a.Zc + static_cast<size_t>(i) * a.crmax * a.gmax;
   const int rows = min(a.rmax, (r + 1) & ~1);
   const size_t bytes = static_cast<size_t>(rows) * a.ext * 8;
   const size_t zbytes = (static_cast<size_t>(a.crmax) * a.gmax * 8 + 15) / 16 * 16;  // Zc has 16 B of tail padding
-  if (rows == 0 || bytes + zbytes > static_cast<size_t>(kStages) * kStageBytes) return {src, zsrc};
-  if (q.cached == i) return {sh.ring, sh.ring + bytes / 8};
-  __syncthreads();  // previous readers of the ring are done
+  *qbytes = bytes;
+  if (rows == 0 || bytes + zbytes > static_cast<size_t>(kStages) * kStageBytes) return false;
   if (threadIdx.x == 0) {
     mbar_expect_tx(sh.qbar, static_cast<uint32_t>(bytes + zbytes));
     bulk_g2s(sh.ring, src, static_cast<uint32_t>(bytes), sh.qbar);
     bulk_g2s(sh.ring + bytes / 8, zsrc, static_cast<uint32_t>(zbytes), sh.qbar);
   }
-  mbar_wait(sh.qbar, q.cnt & 1u);
-  ++q.cnt;
   q.cached = i;
+  q.pending = true;
+  return true;
+}
+
+__device__ Staged stage_qtx(const CgArgs& a, const Shared& sh, QtxStage& q, int i, int r) {
+  const double* src = a.QtX + static_cast<size_t>(i) * a.rmax * a.ext;
+  const double* zsrc = a.Zc + static_cast<size_t>(i) * a.crmax * a.gmax;
+  size_t bytes = 0;
+  if (q.cached != i) {
+    __syncthreads();  // previous readers of the ring are done
+    if (!stage_issue(a, sh, q, i, r, &bytes)) return {src, zsrc};
+  } else {
+    const int rows = min(a.rmax, (r + 1) & ~1);
+    bytes = static_cast<size_t>(rows) * a.ext * 8;
+  }
+  if (q.pending) {
+    mbar_wait(sh.qbar, q.cnt & 1u);
+    ++q.cnt;
+    q.pending = false;
+  }
   return {sh.ring, sh.ring + bytes / 8};
 }
 
@@ -827,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
   pr.cnt = 0;
   pr.active = false;
   unsigned ccnt = 0;    // chunks consumed (consumer warps, uniform)
-  QtxStage qst{0u, -1};
+  QtxStage qst{0u, -1, false};
 
   // Producer: issue the first chunks of `kind` (the ring is idle: the caller's last ring readers
   // finished behind a block barrier) — they overlap the grid barrier that follows.
@@ -1016,14 +1036,38 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
   pr.cnt = 0;
   pr.active = false;
   unsigned ccnt = 0;
-  QtxStage qst{0u, -1};
+  QtxStage qst{0u, -1, false};
   const bool cg = (mode == 0 && vin == nullptr);  // CG iteration: v = r + beta p_cur
+  // Programmatic dependent launch: let the next phase's CTAs start as SMs free up, and issue this
+  // phase's static-data bulk copies (coefficient blocks, Q_r^T / Zc) before waiting for the
+  // previous phase to complete — the in-kernel analogue of prefetching across a grid barrier.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const bool streamed = phase == kPhOp2 || phase == kPhNn1 || phase == kPhNn2 || phase == kPhOp3;
+  if (streamed) {
+    const int kind = phase == kPhOp2 ? kOp2 : phase == kPhNn1 ? kNn1 : phase == kPhNn2 ? kNn2 : kOp3;
+    if (producer && lane == 0) {
+      producer_begin(a, pr, kind, mode == 2);
+      producer_run(a, pr, sh, kStages);
+    }
+  } else if ((phase == kPhOp1 || phase == kPhOp4) && b < a.N) {
+    size_t qb;
+    stage_issue(a, sh, qst, b, a.rank[b], &qb);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (cg) it = a.state[6];  // the iteration counter lives on the device (graph replays)
   double* pcur = a.pbuf[(it + 1) & 1];
   double* pnext = a.pbuf[it & 1];
-  if (cg && a.state[1]) {  // converged / aborted earlier
+  if (cg && a.state[1]) {  // converged / aborted earlier: drain the prefetched copies, then leave
     if ((phase == kPhXr1 || phase == kPhXr2) && b == 0 && threadIdx.x == 0 && a.cond != 0)
       cudaGraphSetConditional(a.cond, 0);
+    __shared__ int s_issued;
+    if (threadIdx.x == 0) s_issued = (producer && lane == 0) ? 0 : 0;
+    __syncthreads();
+    if (producer && lane == 0) s_issued = static_cast<int>(pr.cnt);
+    __syncthreads();
+    for (int c = 0; c < s_issued; ++c) mbar_wait(&sh.full[c % kStages], (c / kStages) & 1u);
+    if (qst.pending) mbar_wait(sh.qbar, 0u);
+    __syncthreads();
     return;
   }
   switch (phase) {
@@ -1036,12 +1080,8 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
     case kPhNn1:
     case kPhNn2:
     case kPhOp3: {
-      const int kind = phase == kPhOp2 ? kOp2 : phase == kPhNn1 ? kNn1 : phase == kPhNn2 ? kNn2 : kOp3;
       if (producer) {
-        if (lane == 0) {
-          producer_begin(a, pr, kind, mode == 2);
-          producer_run(a, pr, sh, -1);
-        }
+        if (lane == 0) producer_run(a, pr, sh, -1);  // the first kStages chunks went out before the wait
         __syncwarp();
       } else if (phase == kPhOp2) {
         dev_op2<W>(a, sh, ccnt, mode);
@@ -1218,11 +1258,26 @@ void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double*
   const void* k = wide ? reinterpret_cast<const void*>(cg_phase_kernel<16>) : reinterpret_cast<const void*>(cg_phase_kernel<8>);
   DDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   const int grid = (phase == kPhXr2) ? 1 : G;
+  // programmatic dependent launch (the kernel overlaps its static prologue with the previous
+  // phase; griddepcontrol.wait orders every dependent read); DDELM_CG_PDL=0 disables it
+  static const bool pdl = [] {
+    const char* e = std::getenv("DDELM_CG_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
   if (wide)
-    cg_phase_kernel<16><<<grid, kThreads, sm, st>>>(a, phase, mode, it, vin, vout);
+    DDG_CUDA(cudaLaunchKernelEx(&cfg, cg_phase_kernel<16>, a, phase, mode, it, vin, vout));
   else
-    cg_phase_kernel<8><<<grid, kThreads, sm, st>>>(a, phase, mode, it, vin, vout);
-  DDG_LAUNCH_CHECK();
+    DDG_CUDA(cudaLaunchKernelEx(&cfg, cg_phase_kernel<8>, a, phase, mode, it, vin, vout));
 }
 
 void cg_launch_init(const CgArgs& a, cudaStream_t st) {

@@ -939,12 +939,46 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
   if (ge && std::strcmp(ge, "0") == 0) {
     CgArgs a = a_in;
     a.cond = 0;
+    // DDELM_CG_PHASE_TIMES=1: per-phase CUDA-event times (host loop only; diagnostics)
+    const bool ptimes = std::getenv("DDELM_CG_PHASE_TIMES") != nullptr;
+    std::vector<cudaEvent_t> pev;
+    std::vector<double> pms(8, 0.0);
+    if (ptimes) {
+      pev.resize(9);
+      for (auto& e : pev) DDG_CUDA(cudaEventCreate(&e));
+    }
+    int nit = 0;
     for (int it = 1; it <= a.max_iter; ++it) {
-      iteration(a);
+      if (ptimes) {
+        const int phases[7] = {kPhOp1, kPhOp2, kPhNn1, kPhNn2, kPhOp3, kPhOp4, kPhXr1};
+        DDG_CUDA(cudaEventRecord(pev[0], st_));
+        for (int q = 0; q < 7; ++q) {
+          if (!a.use_neumann && (phases[q] == kPhNn1 || phases[q] == kPhNn2)) {
+            DDG_CUDA(cudaEventRecord(pev[q + 1], st_));
+            continue;
+          }
+          cg_launch_phase(a, phases[q], 0, 0, nullptr, nullptr, st_);
+          DDG_CUDA(cudaEventRecord(pev[q + 1], st_));
+        }
+      } else {
+        iteration(a);
+      }
       DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
       DDG_CUDA(cudaStreamSynchronize(st_));
+      if (ptimes)
+        for (int q = 0; q < 7; ++q) {
+          float t = 0;
+          DDG_CUDA(cudaEventElapsedTime(&t, pev[q], pev[q + 1]));
+          pms[q] += t;
+        }
+      ++nit;
       launches_ += 7;
       if (pinned_state_[1]) break;
+    }
+    if (ptimes) {
+      static const char* nm[7] = {"op1", "op2", "nn1", "nn2", "op3", "op4", "xr"};
+      for (int q = 0; q < 7; ++q) std::fprintf(stderr, "[cg phase] %-4s %8.2f us\n", nm[q], 1e3 * pms[q] / std::max(nit, 1));
+      for (auto& e : pev) cudaEventDestroy(e);
     }
     return;
   }
