@@ -332,22 +332,39 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
   const int lr = lane >> 2, lc = lane & 3;
 
   // issue chunk q of the unified stream (q < nq: pass 1, else pass 2) into stage q % 3
+  // Each thread copies the same two-row segment (rows 2 seg, 2 seg + 1 of every chunk) of a fixed
+  // set of columns: the column pointers and shared-memory offsets are computed once, so issuing a
+  // chunk is one add and one cp.async per segment (no per-chunk index arithmetic).
+  constexpr int kSegs = (NB_ + TN) * 16 / 256;
+  const int seg = threadIdx.x & 15;
+  const double* gcol[kSegs];
+  int soff[kSegs];
+  bool isv[kSegs], cok[kSegs];
+#pragma unroll
+  for (int j = 0; j < kSegs; ++j) {
+    const int col = (threadIdx.x >> 4) + 16 * j;
+    isv[j] = col < NB_;
+    if (isv[j]) {
+      cok[j] = col < nb;
+      gcol[j] = A + static_cast<size_t>(k0 + (cok[j] ? col : 0)) * ld;
+      soff[j] = col * RCP + 2 * seg;
+    } else {
+      const int c = col - NB_;
+      cok[j] = c < ncols;
+      gcol[j] = A + static_cast<size_t>(c0 + (cok[j] ? c : 0)) * ld;
+      soff[j] = c * RCP + 2 * seg;
+    }
+  }
   auto issue = [&](int q) {
     if (q < 2 * nq) {
       const int st = q % kTrStages;
-      const int r0 = k0 + (q % nq) * RC;
-      // V: nb columns x 32 rows = nb * 16 segments of 16 B; A: 64 columns
-      for (int idx = threadIdx.x; idx < (NB_ + TN) * 16; idx += blockDim.x) {
-        const int col = idx >> 4, seg = idx & 15;
-        const int row = r0 + 2 * seg;
-        if (col < NB_) {
-          const bool ok = col < nb && row < static_cast<int>(ld);
-          cp_async16(&S.V[st][col * RCP + 2 * seg], A + static_cast<size_t>(k0 + col) * ld + (ok ? row : 0), ok);
-        } else {
-          const int c = col - NB_;
-          const bool ok = c < ncols && row < static_cast<int>(ld);
-          cp_async16(&S.A[st][c * RCP + 2 * seg], A + static_cast<size_t>(c0 + (ok ? c : 0)) * ld + (ok ? row : 0), ok);
-        }
+      const int row = k0 + (q % nq) * RC + 2 * seg;
+      const bool rok = row < static_cast<int>(ld);
+#pragma unroll
+      for (int j = 0; j < kSegs; ++j) {
+        const bool ok = cok[j] && rok;
+        double* dst = (isv[j] ? S.V[st] : S.A[st]) + soff[j];
+        cp_async16(dst, gcol[j] + (ok ? row : 0), ok);
       }
     }
     cp_async_commit();
@@ -464,27 +481,18 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
 #pragma unroll
         for (int j = 0; j < 2; ++j) dmma_8x8x4(cf[i][j][0], cf[i][j][1], av[i], bv[j]);
     }
-    __syncthreads();  // every warp read its accumulator init before the chunk is overwritten
+    // write the updated tile straight from the accumulators: per column, 8 consecutive rows
+    // (64 B) per instruction; rows m..ld-1 stay zero (zero V and A rows there)
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int r = (rt0 + i) * 8 + lr, c = (ct0 + j) * 8 + 2 * lc;
-        As[c * RCP + r] = cf[i][j][0];
-        As[(c + 1) * RCP + r] = cf[i][j][1];
+        const int r = r0 + (rt0 + i) * 8 + lr, c = (ct0 + j) * 8 + 2 * lc;
+        if (r < static_cast<int>(ld)) {
+          if (c < ncols) A[static_cast<size_t>(c0 + c) * ld + r] = cf[i][j][0];
+          if (c + 1 < ncols) A[static_cast<size_t>(c0 + c + 1) * ld + r] = cf[i][j][1];
+        }
       }
-    __syncthreads();
-    // coalesced write-back: 64 columns x 16 two-row segments
-    for (int idx = threadIdx.x; idx < TN * 16; idx += blockDim.x) {
-      const int c = idx >> 4, seg = idx & 15;
-      const int row = r0 + 2 * seg;
-      if (c < ncols && row < static_cast<int>(ld)) {
-        double2 v;
-        v.x = As[c * RCP + 2 * seg];
-        v.y = As[c * RCP + 2 * seg + 1];
-        *reinterpret_cast<double2*>(A + static_cast<size_t>(c0 + c) * ld + row) = v;
-      }
-    }
   }
   cp_async_wait<0>();
 }
