@@ -183,26 +183,46 @@ __global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, in
   __syncthreads();
 
   // G = V^T V over the panel (implicit unit diagonal, zeros above) on DMMA: 16 warps = the 4 x 4
-  // grid of 8 x 8 tiles of G, 32-row chunks staged in shared memory
+  // grid of 8 x 8 tiles of G; 32-row chunks double-buffered with cp.async (column-major, padded)
   const int u = threadIdx.x & 31, v = threadIdx.x >> 5;
   const int tu = warp >> 2, tv = warp & 3, lr = lane >> 2, lc = lane & 3;
   double g0 = 0, g1 = 0;
-  for (int r0 = k0; r0 < m; r0 += RC) {
-    for (int idx = threadIdx.x; idx < RC * NB; idx += blockDim.x) {
-      const int rr = idx & 31, uu = idx >> 5;
-      const int row = r0 + rr;
-      double val = 0;
-      if (row < m && uu < nb) {
-        if (row == k0 + uu) val = 1.0;
-        else if (row > k0 + uu) val = P[static_cast<size_t>(uu) * ld + row];
+  {
+    extern __shared__ __align__(16) double pdyn[];  // [2][NB][RCP]
+    constexpr int kRCP = 36;
+    const int gcolu = threadIdx.x >> 4, gseg = threadIdx.x & 15;  // one 16-B segment per thread
+    const bool cok = gcolu < nb;
+    const double* gsrc = P + static_cast<size_t>(cok ? gcolu : 0) * ld;
+    const int nq = (m - k0 + RC - 1) / RC;
+    auto issue = [&](int q) {
+      if (q < nq) {
+        const int row = k0 + q * RC + 2 * gseg;
+        const bool ok = cok && row < static_cast<int>(ld);
+        const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(pdyn + (q & 1) * NB * kRCP + gcolu * kRCP + 2 * gseg));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gsrc + (ok ? row : 0)), "r"(ok ? 16 : 0) : "memory");
       }
-      Vs[rr][uu] = val;
-    }
-    __syncthreads();
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(0);
+    for (int q = 0; q < nq; ++q) {
+      issue(q + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncthreads();
+      double* Vc = pdyn + (q & 1) * NB * kRCP;
+      const int r0 = k0 + q * RC;
+      if (r0 < k0 + nb) {  // unit diagonal, zeros above it
+        for (int idx = threadIdx.x; idx < NB * RC; idx += blockDim.x) {
+          const int uu = idx >> 5, rr = idx & 31;
+          const int row = r0 + rr;
+          if (row <= k0 + uu) Vc[uu * kRCP + rr] = (row == k0 + uu && uu < nb) ? 1.0 : 0.0;
+        }
+        __syncthreads();
+      }
 #pragma unroll
-    for (int kk = 0; kk < RC / 4; ++kk)
-      dmma_8x8x4(g0, g1, Vs[kk * 4 + lc][tu * 8 + lr], Vs[kk * 4 + lc][tv * 8 + lr]);
-    __syncthreads();
+      for (int kk = 0; kk < RC / 4; ++kk)
+        dmma_8x8x4(g0, g1, Vc[(tu * 8 + lr) * kRCP + kk * 4 + lc], Vc[(tv * 8 + lr) * kRCP + kk * 4 + lc]);
+      __syncthreads();
+    }
   }
   G[tu * 8 + lr][tv * 8 + 2 * lc] = g0;
   G[tu * 8 + lr][tv * 8 + 2 * lc + 1] = g1;
@@ -556,7 +576,14 @@ std::vector<QrOp> qr_schedule(int M, int ncol) {
 
 void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
   if (op.kind == QrOp::kPanel) {
-    qr_panel_kernel<<<a.nmat, kPanelThreads, 0, st>>>(a, op.k0, op.toff, op.combine);
+    const size_t smem = 2 * NB * 36 * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      DDG_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      attr = true;
+    }
+    qr_panel_kernel<<<a.nmat, kPanelThreads, smem, st>>>(a, op.k0, op.toff, op.combine);
     DDG_LAUNCH_CHECK();
     return;
   }
