@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -96,99 +97,29 @@ __device__ __forceinline__ void panel_pass(double* P, size_t ld, int m, int rlo,
   (void)n2;
 }
 
-__global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, int k0, int toff, int combine) {
-  const int t = blockIdx.x;
+/// Block reflector of a factored panel (both panel kernels): G = V^T V from the stored panel,
+/// T by the dlarft recurrence, written to quadrant (toff, toff) of the per-matrix T; combine = 1
+/// also forms the coupling block T12 of a 64-wide block. `dyn`: kFinishDoubles of shared memory.
+constexpr int kFinishDoubles = 2 * NB * 36 + 4 * NB * (NB + 1);
+
+__device__ __forceinline__ void panel_finish(const QrArgs& a, int t, int k0, int nb, int toff, int combine,
+                                             const double* stau, double* dyn) {
   double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
   const int m = a.m;
   const size_t ld = a.ld;
-  const int nb = min(NB, a.M - k0);
-  __shared__ double sred[kPanelWarps][NB + 1];
-  __shared__ double sfin[NB + 1];
-  __shared__ double srow[NB];
-  __shared__ double sd[NB];
-  __shared__ double stau[NB];
-  __shared__ double sbeta, sscale;
-  __shared__ int striv;
-  __shared__ double Vs[RC][NB + 1];
-  __shared__ double G[NB][NB + 1];
-  __shared__ double Tsh[NB][NB + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* P = A + static_cast<size_t>(k0) * ld;  // panel column j at P + j*ld
-
-  for (int jj = 0; jj <= nb; ++jj) {
-    const int cp = k0 + jj - 1;  // previous pivot (row and column), jj > 0
-    const int c = k0 + jj;       // current pivot, jj < nb
-    const int jlo = jj > 0 ? jj - 1 : 0;
-    const int rlo = jj > 0 ? cp : c;
-    double tau_p = 0, scale_p = 0, beta_p = 0;
-    bool triv_p = true;
-    if (jj > 0) {
-      tau_p = stau[jj - 1];
-      scale_p = sscale;
-      beta_p = sbeta;
-      triv_p = striv != 0;
-    }
-    // lane k accumulates x_c . y_{c+k} (k = 0: ||x_c||^2) over the rows this warp visits
-    double accS = 0, n2 = 0;
-    switch (nb - jj) {
-#define DDG_PANEL_CASE(n) \
-  case n:                 \
-    panel_pass<n>(P, ld, m, rlo, jj, cp, c, tau_p, scale_p, beta_p, triv_p, sd, srow, accS, n2); \
-    break;
-      DDG_PANEL_CASE(0) DDG_PANEL_CASE(1) DDG_PANEL_CASE(2) DDG_PANEL_CASE(3) DDG_PANEL_CASE(4)
-      DDG_PANEL_CASE(5) DDG_PANEL_CASE(6) DDG_PANEL_CASE(7) DDG_PANEL_CASE(8) DDG_PANEL_CASE(9)
-      DDG_PANEL_CASE(10) DDG_PANEL_CASE(11) DDG_PANEL_CASE(12) DDG_PANEL_CASE(13) DDG_PANEL_CASE(14)
-      DDG_PANEL_CASE(15) DDG_PANEL_CASE(16) DDG_PANEL_CASE(17) DDG_PANEL_CASE(18) DDG_PANEL_CASE(19)
-      DDG_PANEL_CASE(20) DDG_PANEL_CASE(21) DDG_PANEL_CASE(22) DDG_PANEL_CASE(23) DDG_PANEL_CASE(24)
-      DDG_PANEL_CASE(25) DDG_PANEL_CASE(26) DDG_PANEL_CASE(27) DDG_PANEL_CASE(28) DDG_PANEL_CASE(29)
-      DDG_PANEL_CASE(30) DDG_PANEL_CASE(31) DDG_PANEL_CASE(32)
-#undef DDG_PANEL_CASE
-      default:
-        break;
-    }
-    if (jj == nb) break;
-    // ---- block reduction of (n2, s_j)
-    sred[warp][lane] = accS;
-    __syncthreads();
-    if (threadIdx.x < NB) {
-      double s = 0;
-      for (int w = 0; w < kPanelWarps; ++w) s += sred[w][threadIdx.x];
-      sfin[threadIdx.x] = s;  // sfin[k]: column jj+k (k = 0: squared norm below the diagonal)
-    }
-    __syncthreads();
-    {
-      const double alpha = srow[jj], tail = sfin[0];
-      double tau = 0, beta = alpha, scale = 0;
-      const bool triv = !(tail > DBL_MIN);
-      if (!triv) {
-        beta = sqrt(alpha * alpha + tail);
-        if (alpha >= 0) beta = -beta;
-        scale = 1.0 / (alpha - beta);
-        tau = (beta - alpha) / beta;
-      }
-      if (threadIdx.x < NB) {
-        const int j = threadIdx.x;
-        sd[j] = (j > jj && j < nb) ? srow[j] + sfin[j - jj] * scale : 0.0;
-      }
-      if (threadIdx.x == 0) {
-        stau[jj] = tau;
-        sbeta = beta;
-        sscale = scale;
-        striv = triv ? 1 : 0;
-        a.tau[static_cast<size_t>(t) * a.M + c] = tau;
-      }
-    }
-    __syncthreads();
-  }
-  __syncthreads();
-
+  const double* P = A + static_cast<size_t>(k0) * ld;
+  double(*G)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dyn + 2 * NB * 36);
+  double(*Tsh)[NB + 1] = G + NB;
+  double(*Vs)[NB + 1] = G + 2 * NB;
+  double(*T2s)[NB + 1] = G + 3 * NB;
   // G = V^T V over the panel (implicit unit diagonal, zeros above) on DMMA: 16 warps = the 4 x 4
   // grid of 8 x 8 tiles of G; 32-row chunks double-buffered with cp.async (column-major, padded)
   const int u = threadIdx.x & 31, v = threadIdx.x >> 5;
   const int tu = warp >> 2, tv = warp & 3, lr = lane >> 2, lc = lane & 3;
   double g0 = 0, g1 = 0;
   {
-    extern __shared__ __align__(16) double pdyn[];  // [2][NB][RCP]
+    double* pdyn = dyn;  // [2][NB][RCP]
     constexpr int kRCP = 36;
     const int gcolu = threadIdx.x >> 4, gseg = threadIdx.x & 15;  // one 16-B segment per thread
     const bool cok = gcolu < nb;
@@ -271,7 +202,6 @@ __global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, in
     __syncthreads();
   }
   // Tsh <- G12 ; then T12 = -T1 G12 T2 (T1 from global, T2 = this panel's T in Tsh -> keep a copy)
-  __shared__ double T2s[NB][NB + 1];
   for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x) T2s[idx >> 5][idx & 31] = Tsh[idx >> 5][idx & 31];
   __syncthreads();
   Vs[u][v] = g0;  // reuse Vs as G12
@@ -299,6 +229,365 @@ __global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, in
   // T21 block (lower left) is zero: T is upper triangular
   T[(NB + u) * kQrTmax + v] = 0.0;
   T[(NB + u) * kQrTmax + v + 16] = 0.0;
+}
+
+__global__ void __launch_bounds__(kPanelThreads, 1) qr_panel_kernel(QrArgs a, int k0, int toff, int combine) {
+  const int t = blockIdx.x;
+  double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
+  const int m = a.m;
+  const size_t ld = a.ld;
+  const int nb = min(NB, a.M - k0);
+  __shared__ double sred[kPanelWarps][NB + 1];
+  __shared__ double sfin[NB + 1];
+  __shared__ double srow[NB];
+  __shared__ double sd[NB];
+  __shared__ double stau[NB];
+  __shared__ double sbeta, sscale;
+  __shared__ int striv;
+  extern __shared__ __align__(16) double dyn[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* P = A + static_cast<size_t>(k0) * ld;  // panel column j at P + j*ld
+
+  for (int jj = 0; jj <= nb; ++jj) {
+    const int cp = k0 + jj - 1;  // previous pivot (row and column), jj > 0
+    const int c = k0 + jj;       // current pivot, jj < nb
+    const int jlo = jj > 0 ? jj - 1 : 0;
+    const int rlo = jj > 0 ? cp : c;
+    double tau_p = 0, scale_p = 0, beta_p = 0;
+    bool triv_p = true;
+    if (jj > 0) {
+      tau_p = stau[jj - 1];
+      scale_p = sscale;
+      beta_p = sbeta;
+      triv_p = striv != 0;
+    }
+    // lane k accumulates x_c . y_{c+k} (k = 0: ||x_c||^2) over the rows this warp visits
+    double accS = 0, n2 = 0;
+    switch (nb - jj) {
+#define DDG_PANEL_CASE(n) \
+  case n:                 \
+    panel_pass<n>(P, ld, m, rlo, jj, cp, c, tau_p, scale_p, beta_p, triv_p, sd, srow, accS, n2); \
+    break;
+      DDG_PANEL_CASE(0) DDG_PANEL_CASE(1) DDG_PANEL_CASE(2) DDG_PANEL_CASE(3) DDG_PANEL_CASE(4)
+      DDG_PANEL_CASE(5) DDG_PANEL_CASE(6) DDG_PANEL_CASE(7) DDG_PANEL_CASE(8) DDG_PANEL_CASE(9)
+      DDG_PANEL_CASE(10) DDG_PANEL_CASE(11) DDG_PANEL_CASE(12) DDG_PANEL_CASE(13) DDG_PANEL_CASE(14)
+      DDG_PANEL_CASE(15) DDG_PANEL_CASE(16) DDG_PANEL_CASE(17) DDG_PANEL_CASE(18) DDG_PANEL_CASE(19)
+      DDG_PANEL_CASE(20) DDG_PANEL_CASE(21) DDG_PANEL_CASE(22) DDG_PANEL_CASE(23) DDG_PANEL_CASE(24)
+      DDG_PANEL_CASE(25) DDG_PANEL_CASE(26) DDG_PANEL_CASE(27) DDG_PANEL_CASE(28) DDG_PANEL_CASE(29)
+      DDG_PANEL_CASE(30) DDG_PANEL_CASE(31) DDG_PANEL_CASE(32)
+#undef DDG_PANEL_CASE
+      default:
+        break;
+    }
+    if (jj == nb) break;
+    // ---- block reduction of (n2, s_j)
+    sred[warp][lane] = accS;
+    __syncthreads();
+    if (threadIdx.x < NB) {
+      double s = 0;
+      for (int w = 0; w < kPanelWarps; ++w) s += sred[w][threadIdx.x];
+      sfin[threadIdx.x] = s;  // sfin[k]: column jj+k (k = 0: squared norm below the diagonal)
+    }
+    __syncthreads();
+    {
+      const double alpha = srow[jj], tail = sfin[0];
+      double tau = 0, beta = alpha, scale = 0;
+      const bool triv = !(tail > DBL_MIN);
+      if (!triv) {
+        beta = sqrt(alpha * alpha + tail);
+        if (alpha >= 0) beta = -beta;
+        scale = 1.0 / (alpha - beta);
+        tau = (beta - alpha) / beta;
+      }
+      if (threadIdx.x < NB) {
+        const int j = threadIdx.x;
+        sd[j] = (j > jj && j < nb) ? srow[j] + sfin[j - jj] * scale : 0.0;
+      }
+      if (threadIdx.x == 0) {
+        stau[jj] = tau;
+        sbeta = beta;
+        sscale = scale;
+        striv = triv ? 1 : 0;
+        a.tau[static_cast<size_t>(t) * a.M + c] = tau;
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  panel_finish(a, t, k0, nb, toff, combine, stau, dyn);
+}
+
+// ---------------------------------------------------------------- panel, shared-memory resident
+// For panels of up to ~3300 rows the 32 columns are factored as four 8-column sub-panels, each
+// staged once into shared memory (cp.async) and factored there with the same fused column passes
+// (no L2/HBM round trip per column: the streaming kernel above re-reads and re-writes the rest of
+// the panel on every column, ~16x the panel's bytes). Between sub-panels, the 8 reflectors are
+// applied to the panel columns on their right as one small blocked update on DMMA
+// (W = V8^T Y, W' = T8^T W, Y -= V8 W'), reading Y from global memory twice.
+constexpr int kSub = 8;
+
+/// lane l ends with the warp-wide sum of v[l & 7] (7 + 2 shuffles for 8 values)
+__device__ __forceinline__ double reduce_scatter8(double (&v)[kSub]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int k = 0; k < s; ++k) {
+      const double send = upper ? v[k] : v[k + s];
+      const double keep = upper ? v[k + s] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  double r = v[0];
+  r += __shfl_xor_sync(0xffffffffu, r, 8);
+  r += __shfl_xor_sync(0xffffffffu, r, 16);
+  return r;
+}
+
+/// Pass jj over a staged sub-panel (column j at S + j*lds, row 0 = the sub-panel's first pivot
+/// row, R rows): apply H_{jj-1} to columns jj.., then accumulate ||x_jj||^2 below the diagonal and
+/// x_jj . y_{jj+k} into acc[k] (this thread's rows only).
+template <int NR>
+__device__ __forceinline__ void sub_pass(double* S, int lds, int R, int jj, double tau_p, double scale_p, double beta_p,
+                                         bool triv_p, const double* sdl, double* srowl, double (&acc)[kSub]) {
+  const int rlo = jj > 0 ? jj - 1 : 0;
+  for (int i = rlo + threadIdx.x; i < R; i += kPanelThreads) {
+    double y[NR > 0 ? NR : 1];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) y[k] = S[(jj + k) * lds + i];
+    if (jj > 0) {
+      double* pc = S + (jj - 1) * lds + i;
+      const double v = (i == jj - 1) ? 1.0 : (triv_p ? 0.0 : *pc * scale_p);
+      const double tv = tau_p * v;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) {
+        y[k] -= tv * sdl[jj + k];
+        S[(jj + k) * lds + i] = y[k];
+      }
+      *pc = (i == jj - 1) ? beta_p : v;
+    }
+    if constexpr (NR > 0) {
+      if (i == jj) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) srowl[jj + k] = y[k];
+      }
+      if (i > jj) {
+        const double x = y[0];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) acc[k] += x * y[k];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPanelThreads, 1)
+    qr_panel_smem_kernel(QrArgs a, int k0, int toff, int combine, int lds) {
+  const int t = blockIdx.x;
+  double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
+  const int m = a.m;
+  const size_t ld = a.ld;
+  const int nb = min(NB, a.M - k0);
+  extern __shared__ __align__(16) double dyn[];  // sub-panel [kSub][lds]; later panel_finish scratch
+  __shared__ double sred[kPanelWarps][kSub];
+  __shared__ double sfin[kSub], srow[kSub], sd[kSub];
+  __shared__ double stau[NB];
+  __shared__ double sbeta, sscale;
+  __shared__ int striv;
+  __shared__ double sGp[kPanelWarps][kSub * kSub];  // V8^T V8 partials (per warp)
+  __shared__ double sT8[kSub][kSub + 1];
+  __shared__ double sWp[kPanelWarps * kSub * kSub];  // V8^T Y partials (per row group)
+  __shared__ double sW[kSub][NB + 1];               // W' = T8^T W
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  double* P = A + static_cast<size_t>(k0) * ld;
+
+  for (int s0 = 0; s0 < nb; s0 += kSub) {
+    const int w = min(kSub, nb - s0);
+    const int c0 = k0 + s0;  // first pivot (row and column) of the sub-panel
+    const int R = m - c0;
+    double* Pc = P + static_cast<size_t>(s0) * ld + c0;  // column j at Pc + j*ld, from row c0
+    {
+      const int nseg = (R + 1) >> 1;
+      for (int idx = threadIdx.x; idx < w * nseg; idx += kPanelThreads) {
+        const int j = idx / nseg, sg = idx - j * nseg;
+        const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dyn + j * lds + 2 * sg));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(Pc + static_cast<size_t>(j) * ld + 2 * sg),
+                     "r"(R - 2 * sg >= 2 ? 16 : 8)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    for (int jj = 0; jj <= w; ++jj) {
+      double tau_p = 0, scale_p = 0, beta_p = 0;
+      bool triv_p = true;
+      if (jj > 0) {
+        tau_p = stau[s0 + jj - 1];
+        scale_p = sscale;
+        beta_p = sbeta;
+        triv_p = striv != 0;
+      }
+      double acc[kSub];
+#pragma unroll
+      for (int k = 0; k < kSub; ++k) acc[k] = 0.0;
+      switch (w - jj) {
+#define DDG_SUB_CASE(n) \
+  case n:               \
+    sub_pass<n>(dyn, lds, R, jj, tau_p, scale_p, beta_p, triv_p, sd, srow, acc); \
+    break;
+        DDG_SUB_CASE(0) DDG_SUB_CASE(1) DDG_SUB_CASE(2) DDG_SUB_CASE(3) DDG_SUB_CASE(4)
+        DDG_SUB_CASE(5) DDG_SUB_CASE(6) DDG_SUB_CASE(7) DDG_SUB_CASE(8)
+#undef DDG_SUB_CASE
+        default:
+          break;
+      }
+      if (jj == w) break;
+      const double red = reduce_scatter8(acc);
+      if (lane < kSub) sred[warp][lane] = red;
+      __syncthreads();
+      if (threadIdx.x < kSub) {
+        double s = 0;
+        for (int q = 0; q < kPanelWarps; ++q) s += sred[q][threadIdx.x];
+        sfin[threadIdx.x] = s;  // sfin[k]: column jj+k (k = 0: squared norm below the diagonal)
+      }
+      __syncthreads();
+      {
+        const double alpha = srow[jj], tail = sfin[0];
+        double tau = 0, beta = alpha, scale = 0;
+        const bool triv = !(tail > DBL_MIN);
+        if (!triv) {
+          beta = sqrt(alpha * alpha + tail);
+          if (alpha >= 0) beta = -beta;
+          scale = 1.0 / (alpha - beta);
+          tau = (beta - alpha) / beta;
+        }
+        if (threadIdx.x < kSub) {
+          const int j = threadIdx.x;
+          sd[j] = (j > jj && j < w) ? srow[j] + sfin[j - jj] * scale : 0.0;
+        }
+        if (threadIdx.x == 0) {
+          stau[s0 + jj] = tau;
+          sbeta = beta;
+          sscale = scale;
+          striv = triv ? 1 : 0;
+          a.tau[static_cast<size_t>(t) * a.M + c0 + jj] = tau;
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    // write the factored sub-panel back (R entries above the diagonal, beta, v below)
+    for (int j = 0; j < w; ++j)
+      for (int i = threadIdx.x; i < R; i += kPanelThreads) Pc[static_cast<size_t>(j) * ld + i] = dyn[j * lds + i];
+    const int nrem = nb - s0 - w;  // panel columns right of the sub-panel
+    if (nrem <= 0) break;
+    // ---- apply the sub-panel's reflectors to the panel columns on its right
+    double* Yc = P + static_cast<size_t>(s0 + w) * ld + c0;  // column q at Yc + q*ld, from row c0
+    auto vval = [&](int j, int i) -> double {  // V(i, j): unit diagonal, zeros above
+      return (j < w && i < R) ? (i > j ? dyn[j * lds + i] : (i == j ? 1.0 : 0.0)) : 0.0;
+    };
+    const int nk = (R + 3) >> 2;  // 4-row k-steps
+    const int ntiles = (nrem + 7) >> 3;
+    const int ngroups = kPanelWarps / ntiles;
+    const int nt = warp % ntiles, g = warp / ntiles;
+    {  // G8 = V8^T V8 (all warps) and W = V8^T Y partials (warps of the first ngroups groups)
+      double g0 = 0, g1 = 0;
+      for (int q = warp; q < nk; q += kPanelWarps) {
+        const double x = vval(lr, 4 * q + lc);
+        dmma_8x8x4(g0, g1, x, x);
+      }
+      sGp[warp][lr * kSub + 2 * lc] = g0;
+      sGp[warp][lr * kSub + 2 * lc + 1] = g1;
+      if (g < ngroups) {
+        const int col = nt * 8 + lr;
+        const bool cok = col < nrem;
+        const double* yc = Yc + static_cast<size_t>(cok ? col : 0) * ld;
+        double w0 = 0, w1 = 0;
+        constexpr int U = 8;
+        for (int q0 = g * U; q0 < nk; q0 += ngroups * U) {
+          double av[U], bv[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = 4 * (q0 + u) + lc;
+            av[u] = vval(lr, i);
+            bv[u] = (cok && i < R) ? yc[i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) dmma_8x8x4(w0, w1, av[u], bv[u]);
+        }
+        const int wc = ntiles * 8;
+        sWp[(g * kSub + lr) * wc + nt * 8 + 2 * lc] = w0;
+        sWp[(g * kSub + lr) * wc + nt * 8 + 2 * lc + 1] = w1;
+      }
+    }
+    __syncthreads();
+    const int wc = ntiles * 8;
+    if (threadIdx.x < kSub * kSub) {
+      double s = 0;
+      for (int q = 0; q < kPanelWarps; ++q) s += sGp[q][threadIdx.x];
+      sGp[0][threadIdx.x] = s;
+    }
+    for (int e = threadIdx.x; e < kSub * wc; e += kPanelThreads) {
+      double s = 0;
+      for (int q = 0; q < ngroups; ++q) s += sWp[q * kSub * wc + e];
+      sWp[e] = s;  // W(j, c) at sWp[j*wc + c]
+    }
+    __syncthreads();
+    if (warp == 0) {  // T8 by the dlarft recurrence
+      if (lane < kSub)
+        for (int j = 0; j < kSub; ++j) sT8[lane][j] = 0.0;
+      __syncwarp();
+      for (int j = 0; j < w; ++j) {
+        double s = 0;
+        if (lane < j)
+          for (int q = lane; q < j; ++q) s += sT8[lane][q] * sGp[0][q * kSub + j];
+        __syncwarp();
+        if (lane < j) sT8[lane][j] = -stau[s0 + j] * s;
+        if (lane == j) sT8[j][j] = stau[s0 + j];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kSub * wc; e += kPanelThreads) {  // W' = T8^T W
+      const int j = e / wc, c = e - j * wc;
+      double s = 0;
+      for (int q = 0; q <= j; ++q) s += sT8[q][j] * sWp[q * wc + c];
+      sW[j][c] = s;
+    }
+    __syncthreads();
+    // Y -= V8 W': 8-row x 8-column tiles, the Y tile loaded into the DMMA accumulators
+    if (g < ngroups) {
+      const double b0 = -sW[lc][nt * 8 + lr], b1 = -sW[4 + lc][nt * 8 + lr];
+      const int colA = nt * 8 + 2 * lc;
+      const bool ok0 = colA < nrem, ok1 = colA + 1 < nrem;
+      double* y0 = Yc + static_cast<size_t>(ok0 ? colA : 0) * ld;
+      double* y1 = Yc + static_cast<size_t>(ok1 ? colA + 1 : 0) * ld;
+      const int nrt = (R + 7) >> 3;
+      constexpr int U = 4;
+      for (int r0 = g * U; r0 < nrt; r0 += ngroups * U) {
+        double c[U][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = 8 * (r0 + u) + lr;
+          c[u][0] = (ok0 && i < R) ? y0[i] : 0.0;
+          c[u][1] = (ok1 && i < R) ? y1[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = 8 * (r0 + u) + lr;
+          dmma_8x8x4(c[u][0], c[u][1], vval(lc, i), b0);
+          dmma_8x8x4(c[u][0], c[u][1], vval(4 + lc, i), b1);
+          if (ok0 && i < R) y0[i] = c[u][0];
+          if (ok1 && i < R) y1[i] = c[u][1];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  panel_finish(a, t, k0, nb, toff, combine, stau, dyn);
 }
 
 // ---------------------------------------------------------------- trailing update (DMMA)
@@ -576,14 +865,31 @@ std::vector<QrOp> qr_schedule(int M, int ncol) {
 
 void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
   if (op.kind == QrOp::kPanel) {
-    const size_t smem = 2 * NB * 36 * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    // shared-memory resident panel when an 8-column sub-panel of all m - k0 rows fits
+    static int smem_static = -1, smem_optin = 0;
+    static bool use_smem = true;
+    if (smem_static < 0) {
+      cudaFuncAttributes fa{};
+      DDG_CUDA(cudaFuncGetAttributes(&fa, qr_panel_smem_kernel));
+      smem_static = static_cast<int>(fa.sharedSizeBytes);
+      int dev = 0;
+      DDG_CUDA(cudaGetDevice(&dev));
+      DDG_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      DDG_CUDA(cudaFuncSetAttribute(qr_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem_optin - smem_static));
       DDG_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-      attr = true;
+                                    static_cast<int>(kFinishDoubles * sizeof(double))));
+      const char* e = std::getenv("DDELM_QR_PANEL");
+      use_smem = !(e && std::string(e) == "stream");
     }
-    qr_panel_kernel<<<a.nmat, kPanelThreads, smem, st>>>(a, op.k0, op.toff, op.combine);
+    const int rows = a.m - op.k0;
+    const int lds = ((rows + 27) / 32) * 32 + 4;  // >= rows, = 4 (mod 32): conflict-free DMMA fragments
+    const size_t smem = std::max<size_t>(static_cast<size_t>(kSub) * lds, kFinishDoubles) * sizeof(double);
+    if (use_smem && smem + smem_static <= static_cast<size_t>(smem_optin)) {
+      qr_panel_smem_kernel<<<a.nmat, kPanelThreads, smem, st>>>(a, op.k0, op.toff, op.combine, lds);
+    } else {
+      qr_panel_kernel<<<a.nmat, kPanelThreads, kFinishDoubles * sizeof(double), st>>>(a, op.k0, op.toff, op.combine);
+    }
     DDG_LAUNCH_CHECK();
     return;
   }
