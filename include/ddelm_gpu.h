@@ -116,6 +116,19 @@ void ddelm_gpu_destroy(ddelm_ws* ws);
 int ddelm_gpu_get_mu(ddelm_ws* ws, double* mu /* n_mu: Delta then Pi */);
 int ddelm_gpu_get_coeffs(ddelm_ws* ws, double* coeffs /* n_subdomains x M */);
 int ddelm_gpu_get_residuals(ddelm_ws* ws, double* hist, int cap);
+
+/* Field of the last solve on the uniform n x n grid of [0,1]^2 (point (a,b) = (a,b)/(n-1)),
+ * evaluated on the device by the owning subdomain's ELM (sample_field, metrics.cpp:18-57).
+ * u, gx, gy: n*n host buffers, index b*n + a, each may be NULL. On a sharded workspace only the
+ * points of this rank's subdomains are filled (the rest are 0). */
+int ddelm_gpu_sample_field(ddelm_ws* ws, int n, double* u, double* gx, double* gy);
+/* Relative L2 and H1 errors (trapezoid rule on the n x n grid) against the problem's exact
+ * solution: relative_errors (metrics.cpp:112-128). n < 64 -> DDELM_ERR_INVALID_ARGUMENT, as the
+ * reference. Sharded: the sums are all-reduced, every rank gets the global errors. */
+int ddelm_gpu_relative_errors(ddelm_ws* ws, int n, double* l2, double* h1);
+/* The same errors against the ELM field of ref_coeffs (n_subdomains x M, this workspace's
+ * layers): oracle_check's field_diff (runner.cpp:269-281). */
+int ddelm_gpu_field_diff(ddelm_ws* ws, int n, const double* ref_coeffs, double* l2, double* h1);
 /* Per-subdomain numerical ranks of K_i and Kbar_i (-1 when the layer is not built) and the
  * unpivoted-QR diagonal ratio min|R_ii|/max|R_ii| used by the branch test (solvers.cpp:27-32). */
 int ddelm_gpu_get_ranks(ddelm_ws* ws, int* rank_k, int* rank_kbar, double* qr_ratio /* 2N */);

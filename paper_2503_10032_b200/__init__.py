@@ -40,7 +40,8 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_lsq_create", "ddelm_gpu_lsq_generate", "ddelm_gpu_lsq_factor",
            "ddelm_gpu_lsq_get_block", "ddelm_gpu_lsq_ld", "ddelm_gpu_lsq_destroy",
            "ddelm_gpu_nccl_unique_id", "ddelm_gpu_create_sharded", "ddelm_gpu_get_shard",
-           "ddelm_gpu_plan_tables")
+           "ddelm_gpu_plan_tables", "ddelm_gpu_sample_field", "ddelm_gpu_relative_errors",
+           "ddelm_gpu_field_diff")
 
 
 class _Desc(C.Structure):
@@ -83,6 +84,9 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_get_mu.argtypes = [C.c_void_p, C.c_void_p]
     L.ddelm_gpu_get_coeffs.argtypes = [C.c_void_p, C.c_void_p]
     L.ddelm_gpu_get_residuals.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+    L.ddelm_gpu_sample_field.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_relative_errors.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_field_diff.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_get_ranks.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_get_layer.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_get_local.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int)]
@@ -310,6 +314,27 @@ class Workspace:
         out = np.zeros_like(v)
         _check(load_library().ddelm_gpu_apply_operator(self._h, float(theta), _ptr(v), _ptr(out)))
         return out
+
+    def sample_field(self, n: int = 257):
+        """Field and gradient of the last solve on the n x n grid, flat b*n + a (sample_field,
+        metrics.cpp:18-57), evaluated on the device."""
+        u, gx, gy = np.zeros(n * n), np.zeros(n * n), np.zeros(n * n)
+        _check(load_library().ddelm_gpu_sample_field(self._h, int(n), _ptr(u), _ptr(gx), _ptr(gy)))
+        return u, gx, gy
+
+    def relative_errors(self, n: int = 257) -> tuple[float, float]:
+        """(L2, H1) relative errors against the exact solution (metrics.cpp:112-128)."""
+        l2, h1 = C.c_double(), C.c_double()
+        _check(load_library().ddelm_gpu_relative_errors(self._h, int(n), C.byref(l2), C.byref(h1)))
+        return l2.value, h1.value
+
+    def field_diff(self, ref_coeffs: np.ndarray, n: int = 257) -> tuple[float, float]:
+        """(L2, H1) relative difference against the ELM field of ref_coeffs on the same layers
+        (oracle_check's field_diff, runner.cpp:269-281)."""
+        c = np.ascontiguousarray(ref_coeffs, dtype=np.float64)
+        l2, h1 = C.c_double(), C.c_double()
+        _check(load_library().ddelm_gpu_field_diff(self._h, int(n), _ptr(c), C.byref(l2), C.byref(h1)))
+        return l2.value, h1.value
 
     def _solve(self, method: str, theta: float, cg: CgOptions | None, fetch: bool = True) -> SolveReport:
         """fetch=False leaves mu / coefficients / history on the device (device-resident timing)."""

@@ -1,5 +1,6 @@
 // C-ABI boundary (include/ddelm_gpu.h) over the device workspace. No CPU fallback: every entry
 // point fails with DDELM_ERR_CUDA when no CUDA device is usable.
+#include <cmath>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -216,6 +217,37 @@ int ddelm_gpu_get_mu(ddelm_ws* ws, double* mu) {
 }
 int ddelm_gpu_get_coeffs(ddelm_ws* ws, double* c) {
   return guarded([&] { ws->w->get_coeffs(c); });
+}
+int ddelm_gpu_sample_field(ddelm_ws* ws, int n, double* u, double* gx, double* gy) {
+  return guarded([&] {
+    double sums[4];
+    ws->w->field(n, nullptr, u, gx, gy, sums);
+  });
+}
+namespace {
+/// relative L2 / H1 from the trapezoid sums (metrics.cpp:79-87)
+void errors_from_sums(const double* s, double* l2, double* h1) {
+  if (l2) *l2 = s[1] > 0 ? std::sqrt(s[0] / s[1]) : std::sqrt(s[0]);
+  const double den = s[1] + s[3];
+  if (h1) *h1 = den > 0 ? std::sqrt((s[0] + s[2]) / den) : std::sqrt(s[0] + s[2]);
+}
+}  // namespace
+int ddelm_gpu_relative_errors(ddelm_ws* ws, int n, double* l2, double* h1) {
+  return guarded([&] {
+    if (n < 64) throw std::invalid_argument("relative_errors: evaluation grid too coarse");
+    double sums[4];
+    ws->w->field(n, nullptr, nullptr, nullptr, nullptr, sums);
+    errors_from_sums(sums, l2, h1);
+  });
+}
+int ddelm_gpu_field_diff(ddelm_ws* ws, int n, const double* ref_coeffs, double* l2, double* h1) {
+  return guarded([&] {
+    if (n < 64) throw std::invalid_argument("relative_errors: evaluation grid too coarse");
+    if (ref_coeffs == nullptr) throw std::invalid_argument("field_diff: reference coefficients required");
+    double sums[4];
+    ws->w->field(n, ref_coeffs, nullptr, nullptr, nullptr, sums);
+    errors_from_sums(sums, l2, h1);
+  });
 }
 int ddelm_gpu_get_residuals(ddelm_ws* ws, double* h, int cap) {
   int n = 0;

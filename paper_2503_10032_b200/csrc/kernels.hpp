@@ -232,4 +232,26 @@ void cg_launch_init(const CgArgs& a, cudaStream_t st);
 int cg_grid(const CgArgs& a);
 int cg_rows_per_chunk_max(const CgArgs& a);
 
+
+// ---------------------------------------------------------------- field evaluation (k_field.cu)
+/// Field samples and trapezoid error sums on the n x n grid (metrics.cpp:18-88).
+struct FieldArgs {
+  int n, N, M, problem;
+  const int* sub_ix;
+  const int* sub_iy;
+  const int* lo;          // s + 1 boundaries: grid index a in [lo[k], lo[k+1]) lies in column k
+  const double* w0;       // N x M layers
+  const double* w1;
+  const double* b;
+  const double* coef;     // N x M coefficients of the field
+  const double* coef_ref; // N x M reference coefficients (nullptr: the problem's exact solution)
+  double* u;              // n x n samples, index b*n + a (nullable)
+  double* gx;
+  double* gy;
+  double* part;           // field_parts() x 4 partial sums
+};
+int field_parts(const FieldArgs& f, int max_pts);
+/// sums = {sum w du^2, sum w u_ref^2, sum w |d grad|^2, sum w |grad_ref|^2}
+void launch_field(const FieldArgs& f, int max_pts, double* sums, cudaStream_t st);
+
 }  // namespace ddg

@@ -8,6 +8,7 @@
 //                    kernel (build_neumann, solvers.cpp:390-448)
 //   solve()          reduced RHS, CG (one persistent cooperative kernel), reconstruct
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <chrono>
 #include <cstring>
@@ -1013,6 +1014,62 @@ void Workspace::get_mu(double* mu) {
   const Plan& p = plan;
   DDG_CUDA(cudaMemcpyAsync(mu, d_x.ptr, sizeof(double) * p.n_delta, cudaMemcpyDeviceToHost, st_));
   if (p.n_pi) DDG_CUDA(cudaMemcpyAsync(mu + p.n_delta, d_mu_pi_out.ptr, sizeof(double) * p.n_pi, cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Workspace::field(int n, const double* ref, double* u, double* gx, double* gy, double* sums) {
+  if (n < 2) throw std::invalid_argument("sample_field: grid must have at least 2 points per side");
+  if (!solved_) throw std::runtime_error("sample_field: no solution (call solve first)");
+  const int s = plan.s, N = plan.N, M = plan.M;
+  // column (row) ranges of the grid indices, subdomain_of (geometry.cpp:12-18) in the same arithmetic
+  const double h = 1.0 / (n - 1);
+  std::vector<int> lo(s + 1, n);
+  for (int a = n - 1; a >= 0; --a) {
+    const int k = std::clamp(static_cast<int>(std::floor(a * h * s)), 0, s - 1);
+    lo[k] = a;
+  }
+  lo[s] = n;
+  for (int k = s - 1; k >= 0; --k) lo[k] = std::min(lo[k], lo[k + 1]);
+  int max_pts = 0;
+  for (int i = 0; i < N; ++i) {
+    const SubPlan& sp = plan.subs[i];
+    max_pts = std::max(max_pts, (lo[sp.ix + 1] - lo[sp.ix]) * (lo[sp.iy + 1] - lo[sp.iy]));
+  }
+  d_flo.upload(lo, st_);
+  const size_t nn = static_cast<size_t>(n) * n;
+  const bool want = u || gx || gy;
+  if (want && d_field.count < 3 * nn) d_field.alloc(3 * nn);
+  if (want) DDG_CUDA(cudaMemsetAsync(d_field.ptr, 0, 3 * nn * sizeof(double), st_));
+  if (ref) {
+    if (d_fref.count < static_cast<size_t>(N) * M) d_fref.alloc(static_cast<size_t>(N) * M);
+    DDG_CUDA(cudaMemcpyAsync(d_fref.ptr, ref, sizeof(double) * N * M, cudaMemcpyHostToDevice, st_));
+  }
+  FieldArgs f{};
+  f.n = n;
+  f.N = N;
+  f.M = M;
+  f.problem = plan.problem;
+  f.sub_ix = d_ix.ptr;
+  f.sub_iy = d_iy.ptr;
+  f.lo = d_flo.ptr;
+  f.w0 = d_w0.ptr;
+  f.w1 = d_w1.ptr;
+  f.b = d_b.ptr;
+  f.coef = d_coeffs.ptr;
+  f.coef_ref = ref ? d_fref.ptr : nullptr;
+  f.u = want ? d_field.ptr : nullptr;
+  f.gx = want ? d_field.ptr + nn : nullptr;
+  f.gy = want ? d_field.ptr + 2 * nn : nullptr;
+  const int parts = field_parts(f, std::max(max_pts, 1));
+  if (d_fpart.count < static_cast<size_t>(parts) * 4) d_fpart.alloc(static_cast<size_t>(parts) * 4);
+  if (d_fsums.count < 8) d_fsums.alloc(8);
+  f.part = d_fpart.ptr;
+  launch_field(f, std::max(max_pts, 1), d_fsums.ptr, st_);
+  if (sharded()) xchg(d_fsums.ptr, d_fsums.ptr + 4, 4);
+  DDG_CUDA(cudaMemcpyAsync(sums, d_fsums.ptr + (sharded() ? 4 : 0), 4 * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  if (u) DDG_CUDA(cudaMemcpyAsync(u, d_field.ptr, nn * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  if (gx) DDG_CUDA(cudaMemcpyAsync(gx, d_field.ptr + nn, nn * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  if (gy) DDG_CUDA(cudaMemcpyAsync(gy, d_field.ptr + 2 * nn, nn * sizeof(double), cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
 }
 

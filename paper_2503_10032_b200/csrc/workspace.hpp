@@ -87,6 +87,11 @@ class Workspace {
   bool kernel_stat(const std::string& name, KernelStat* out) const;
   double device_span_ms() const { return device_span_ms_; }
 
+  /// Field of the last solve on the n x n grid (sample_field, metrics.cpp:18-57): samples to the
+  /// host buffers (each nullable, n*n), and sums[4] of the trapezoid error terms against the
+  /// exact solution (ref = nullptr) or the ELM field of ref (N x M, same layers). Sharded: the
+  /// strip's points only; the sums are all-reduced over the ranks.
+  void field(int n, const double* ref, double* u, double* gx, double* gy, double* sums);
   void get_mu(double* mu);
   void get_coeffs(double* c);
   int get_residuals(double* h, int cap);
@@ -170,6 +175,8 @@ class Workspace {
   DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu_pi_out, d_tpart, d_tpart3,
       d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_pap, d_vin, d_vout, d_trace, d_KF, d_KD;
   // receive side of the owner-slot all-reduces (sharded only)
+  DevBuf<double> d_field, d_fpart, d_fref, d_fsums;
+  DevBuf<int> d_flo;
   DevBuf<double> r_tpart, r_psipart, r_tpart3, r_o, r_xf, r_tr, r_zz, r_pap, d_Gsum;
   int ldKF_ = 0, ldKD_ = 0;
 };
