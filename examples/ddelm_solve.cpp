@@ -2,8 +2,9 @@
 //
 // The device-path subset of `ddelm_cli solve` (tools/ddelm_cli.cpp:55-92, runner.cpp:126-155):
 //   ddelm_solve [key=value ...]   keys: problem s n_grid M l seed method theta flux_variant
-//                                 trace_basis cg_rel_tol cg_max_iter device
-// Prints one JSON object (iterations, converged, residual history, mu, timings) on stdout.
+//                                 trace_basis cg_rel_tol cg_max_iter device eval_grid_n
+// Prints one JSON object (iterations, converged, residual history, mu, timings, and the relative
+// L2 / H1 errors against the exact solution on the eval_grid_n^2 grid, runner.cpp:144-150) on stdout.
 // Exit codes follow the CLI: 0 ok, 2 non-convergence / solver error, 3 configuration error.
 #include <cstdio>
 #include <cstdlib>
@@ -17,7 +18,8 @@ int main(int argc, char** argv) {
   std::map<std::string, std::string> kv = {
       {"problem", "poisson_sinpi"}, {"s", "2"}, {"n_grid", "10"}, {"M", "64"}, {"l", "8"}, {"seed", "1"},
       {"method", "ddelm-nn"}, {"theta", "0.999"}, {"flux_variant", "mean_edge"},
-      {"trace_basis", "change_of_variables"}, {"cg_rel_tol", "1e-9"}, {"cg_max_iter", "0"}, {"device", "0"}};
+      {"trace_basis", "change_of_variables"}, {"cg_rel_tol", "1e-9"}, {"cg_max_iter", "0"}, {"device", "0"},
+      {"eval_grid_n", "257"}};
   for (int k = 1; k < argc; ++k) {
     const std::string a = argv[k];
     const auto eq = a.find('=');
@@ -36,10 +38,16 @@ int main(int argc, char** argv) {
                         std::atoi(kv["M"].c_str()), std::atof(kv["l"].c_str()),
                         std::strtoull(kv["seed"].c_str(), nullptr, 10), opts);
     ddelm::CgOptions cg{std::atof(kv["cg_rel_tol"].c_str()), std::atoi(kv["cg_max_iter"].c_str())};
-    ddelm::SolveReport r = kv["method"] == "ddelm-cs" ? ddelm::ddelm_cs_solve(ws, cg)
-                                                      : ddelm::ddelm_nn_solve(ws, std::atof(kv["theta"].c_str()), cg);
-    std::printf("{\"iterations\": %d, \"converged\": %s, \"total_seconds\": %.9g, \"residual_history\": [", r.iterations,
-                r.converged ? "true" : "false", r.total_seconds);
+    const std::string method = kv["method"];
+    if (method != "ddelm" && method != "ddelm-cs" && method != "ddelm-nn")
+      throw std::invalid_argument("unknown method '" + method + "'");
+    ddelm::SolveReport r = method == "ddelm"      ? ddelm::ddelm_solve(ws, cg)
+                           : method == "ddelm-cs" ? ddelm::ddelm_cs_solve(ws, cg)
+                                                  : ddelm::ddelm_nn_solve(ws, std::atof(kv["theta"].c_str()), cg);
+    const ddelm::ErrorReport err = ddelm::relative_errors(ws, std::atoi(kv["eval_grid_n"].c_str()));
+    std::printf("{\"iterations\": %d, \"converged\": %s, \"total_seconds\": %.9g, \"l2_error\": %.17g, "
+                "\"h1_error\": %.17g, \"residual_history\": [",
+                r.iterations, r.converged ? "true" : "false", r.total_seconds, err.l2, err.h1);
     for (size_t k = 0; k < r.residual_history.size(); ++k)
       std::printf("%s%.17g", k ? ", " : "", r.residual_history[k]);
     std::printf("], \"mu\": [");

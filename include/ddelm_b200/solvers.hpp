@@ -2,11 +2,14 @@
 //
 // Mirrors proj/include/ddelm/solvers.hpp (namespace ddelm) for the north-star path:
 //   Workspace(problem, s, n_grid, M, l, seed, SolverOptions)     solvers.hpp:79-80
+//   ddelm_solve(Workspace&, CgOptions)  (one-level)                 solvers.hpp:178
 //   ddelm_cs_solve(Workspace&, CgOptions)                          solvers.hpp:179
 //   ddelm_nn_solve(Workspace&, double theta, CgOptions)            solvers.hpp:181
 //   SolverOptions / CgOptions / SolveReport                        solvers.hpp:49-58,162-176
 //   ProblemSpec via make_problem(name)                             problems.hpp:38-62,
 //                                                                   problems.cpp:132-188
+//   relative_errors(ws, grid_n) / field_diff(ws, ref, grid_n)      metrics.cpp:112-128,
+//                                                                   runner.cpp:269-281
 // with the reference's error behaviour: std::invalid_argument for bad arguments (theta outside
 // [0,1], bad partition, unknown problem), std::runtime_error for a non-SPD coarse matrix and for
 // device failures. Non-convergence is SolveReport::converged == false, not an exception.
@@ -120,6 +123,13 @@ class Workspace {
     return out;
   }
 
+  /// reduced_apply, the one-level operator on mu = [mu_Delta; mu_Pi] (solvers.cpp:262-274).
+  std::vector<double> reduced_apply(const std::vector<double>& mu) {
+    std::vector<double> out(mu.size());
+    detail::check(ddelm_gpu_apply_reduced(ws_.get(), mu.data(), out.data()));
+    return out;
+  }
+
   SolveReport solve(int method, double theta, const CgOptions& cg) {
     ddelm_report r{};
     detail::check(ddelm_gpu_solve(ws_.get(), method, theta, cg.rel_tol, cg.max_iter, &r));
@@ -155,6 +165,11 @@ class Workspace {
   std::unique_ptr<ddelm_ws, detail::WsDeleter> ws_;
 };
 
+/// ddelm_solve, one-level DDELM (solvers.cpp:493-531).
+inline SolveReport ddelm_solve(Workspace& ws, const CgOptions& cg_opts = {}) {
+  return ws.solve(DDELM_METHOD_DDELM, 0.0, cg_opts);
+}
+
 /// ddelm_cs_solve (solvers.cpp:582-588).
 inline SolveReport ddelm_cs_solve(Workspace& ws, const CgOptions& cg_opts = {}) {
   return ws.solve(DDELM_METHOD_CS, 0.0, cg_opts);
@@ -164,6 +179,30 @@ inline SolveReport ddelm_cs_solve(Workspace& ws, const CgOptions& cg_opts = {}) 
 inline SolveReport ddelm_nn_solve(Workspace& ws, double theta, const CgOptions& cg_opts = {}) {
   if (!(theta >= 0.0 && theta <= 1.0)) throw std::invalid_argument("ddelm_nn_solve: theta must lie in [0, 1]");
   return ws.solve(DDELM_METHOD_NN, theta, cg_opts);
+}
+
+/// Relative L2 / H1 errors of the last solve's field against the problem's exact solution on the
+/// grid_n x grid_n trapezoid grid, evaluated on the device (relative_errors, metrics.cpp:112-128;
+/// grid_n < 64 throws std::invalid_argument as the reference).
+struct ErrorReport {  // metrics.hpp ErrorReport
+  double l2 = 0, h1 = 0;
+  int grid_n = 0;
+};
+inline ErrorReport relative_errors(Workspace& ws, int grid_n = 257) {
+  ErrorReport e;
+  e.grid_n = grid_n;
+  detail::check(ddelm_gpu_relative_errors(ws.handle(), grid_n, &e.l2, &e.h1));
+  return e;
+}
+/// The same errors against another coefficient set on the same layers (oracle_check's
+/// field_diff, runner.cpp:269-281); ref: one M-vector per subdomain.
+inline ErrorReport field_diff(Workspace& ws, const std::vector<std::vector<double>>& ref, int grid_n = 257) {
+  std::vector<double> flat;
+  for (const auto& c : ref) flat.insert(flat.end(), c.begin(), c.end());
+  ErrorReport e;
+  e.grid_n = grid_n;
+  detail::check(ddelm_gpu_field_diff(ws.handle(), grid_n, flat.data(), &e.l2, &e.h1));
+  return e;
 }
 
 }  // namespace ddelm

@@ -103,8 +103,9 @@ int ddelm_gpu_plan_tables(const ddelm_desc* desc, int rank, int world, int which
 int ddelm_gpu_build(ddelm_ws* ws);
 int ddelm_gpu_build_coarse(ddelm_ws* ws);
 int ddelm_gpu_build_neumann(ddelm_ws* ws);
-/* method: DDELM_METHOD_CS or DDELM_METHOD_NN (theta in [0,1]; theta = 0 is exactly CS).
- * max_iter <= 0 means 20 x n_delta (solvers.cpp:85). */
+/* method: DDELM_METHOD_DDELM (one-level ddelm_solve, solvers.cpp:493-531: CG on
+ * mu = [mu_Delta; mu_Pi], theta ignored), DDELM_METHOD_CS or DDELM_METHOD_NN (theta in [0,1];
+ * theta = 0 is exactly CS). max_iter <= 0 means 20 x the CG dimension (solvers.cpp:85). */
 int ddelm_gpu_solve(ddelm_ws* ws, int method, double theta, double rel_tol, int max_iter,
                     ddelm_report* report);
 /* Re-seed the feature layers (seed + i per subdomain) and invalidate every built layer;
@@ -139,6 +140,9 @@ int ddelm_gpu_get_local(ddelm_ws* ws, int i, int which /* 0 K, 1 Kbar */, double
 /* out = cs_reduced_apply(v, weight) on the device (solvers.cpp:372-386, weight 599-603;
  * theta = 0: plain coarse operator). v, out: n_delta host doubles. Builds layers as needed. */
 int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double* out);
+/* out = reduced_apply(v), the one-level operator (solvers.cpp:262-274); v, out: n_mu = n_delta +
+ * n_pi host doubles. */
+int ddelm_gpu_apply_reduced(ddelm_ws* ws, const double* v, double* out);
 /* Drop every built layer (features, factors, coarse, Neumann) but keep the feature layers
  * already uploaded to the device: the next solve re-runs the whole device pipeline. */
 int ddelm_gpu_invalidate(ddelm_ws* ws);

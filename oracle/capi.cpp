@@ -211,6 +211,16 @@ int ddo_apply_cs(void* p, double theta, const double* v, double* out) {
   return 0;
 }
 
+/// reduced_apply(mu), the one-level operator (solvers.cpp:262-274); mu, out: n_mu doubles.
+int ddo_apply_reduced(void* p, const double* v, double* out) {
+  auto h = static_cast<ddo_handle*>(p);
+  Workspace& ws = *h->ws;
+  Vec in(v, v + ws.n_mu());
+  Vec o = ws.reduced_apply(in);
+  std::copy(o.begin(), o.end(), out);
+  return 0;
+}
+
 /// Relative L2 / H1 errors against the exact solution (runner.cpp:144-150).
 int ddo_errors(void* p, int n, double* l2, double* h1) {
   auto h = static_cast<ddo_handle*>(p);

@@ -41,7 +41,7 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_lsq_get_block", "ddelm_gpu_lsq_ld", "ddelm_gpu_lsq_destroy",
            "ddelm_gpu_nccl_unique_id", "ddelm_gpu_create_sharded", "ddelm_gpu_get_shard",
            "ddelm_gpu_plan_tables", "ddelm_gpu_sample_field", "ddelm_gpu_relative_errors",
-           "ddelm_gpu_field_diff")
+           "ddelm_gpu_field_diff", "ddelm_gpu_apply_reduced")
 
 
 class _Desc(C.Structure):
@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_get_layer.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_get_local.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int)]
     L.ddelm_gpu_apply_operator.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_apply_reduced.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_invalidate.argtypes = [C.c_void_p]
     L.ddelm_gpu_stream.argtypes = [C.c_void_p]
     L.ddelm_gpu_stream.restype = C.c_void_p
@@ -336,6 +337,13 @@ class Workspace:
         _check(load_library().ddelm_gpu_field_diff(self._h, int(n), _ptr(c), C.byref(l2), C.byref(h1)))
         return l2.value, h1.value
 
+    def apply_reduced(self, v: np.ndarray) -> np.ndarray:
+        """reduced_apply (solvers.cpp:262-274), the one-level operator on mu = [mu_Delta; mu_Pi]."""
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.zeros_like(v)
+        _check(load_library().ddelm_gpu_apply_reduced(self._h, _ptr(v), _ptr(out)))
+        return out
+
     def _solve(self, method: str, theta: float, cg: CgOptions | None, fetch: bool = True) -> SolveReport:
         """fetch=False leaves mu / coefficients / history on the device (device-resident timing)."""
         cg = cg or CgOptions()
@@ -381,8 +389,8 @@ def ddelm_nn_solve(ws: Workspace, theta: float, cg: CgOptions | None = None) -> 
 
 
 def ddelm_solve(ws: Workspace, cg: CgOptions | None = None) -> SolveReport:
-    """One-level DDELM (solvers.cpp:493-531) — SURVEY.md §8f 'next'; not on the device path yet."""
-    raise NotImplementedError("ddelm (one-level) is a §8f 'next' row; use ddelm_cs_solve / ddelm_nn_solve")
+    """One-level DDELM (solvers.cpp:493-531): CG on mu = [mu_Delta; mu_Pi] with reduced_apply."""
+    return ws._solve("ddelm", 0.0, cg)
 
 
 class LsqBatch:
@@ -438,4 +446,6 @@ def solve_config(name_or_cfg, device: int = 0, ws: Workspace | None = None) -> t
     cg = CgOptions(rel_tol=cfg["cg_rel_tol"])
     if cfg["method"] == "ddelm-cs":
         return ws, ddelm_cs_solve(ws, cg)
+    if cfg["method"] == "ddelm":
+        return ws, ddelm_solve(ws, cg)
     return ws, ddelm_nn_solve(ws, cfg["theta"], cg)

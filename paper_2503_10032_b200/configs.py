@@ -23,4 +23,18 @@ CONFIGS = {
     "T3": dict(_BASE, s=8, M=48, l=12.0, n_grid=10),
     "T4": dict(_BASE, s=3, M=100, l=20.0, n_grid=16),
     "T1cs": dict(_BASE, s=2, M=64, l=8.0, n_grid=10, method="ddelm-cs"),
+    # one-level DDELM (ddelm_solve, solvers.cpp:493-531) with the reference's
+    # one-level defaults pointwise + nodal (runner.cpp:114-115), and one with the coarse-method
+    # flux / trace choices (mean-edge cross rows in A and A^T)
+    "T1d": dict(_BASE, s=2, M=64, l=8.0, n_grid=10, method="ddelm", flux_variant="pointwise",
+                trace_basis="nodal"),
+    "T2d": dict(_BASE, s=4, M=64, l=10.0, n_grid=12, method="ddelm", flux_variant="pointwise",
+                trace_basis="nodal"),
+    "T4d": dict(_BASE, s=3, M=100, l=20.0, n_grid=16, method="ddelm", flux_variant="pointwise",
+                trace_basis="nodal"),
+    "T2dm": dict(_BASE, s=4, M=64, l=10.0, n_grid=12, method="ddelm"),
+    "C1d": dict(_BASE, s=2, M=200, l=1.0, n_grid=22, method="ddelm", flux_variant="pointwise",
+                trace_basis="nodal"),
+    "C2d": dict(_BASE, s=4, M=400, l=2.0, n_grid=32, method="ddelm", flux_variant="pointwise",
+                trace_basis="nodal"),
 }

@@ -282,6 +282,9 @@ int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double
     ws->w->apply_operator(theta, v, out);
   });
 }
+int ddelm_gpu_apply_reduced(ddelm_ws* ws, const double* v, double* out) {
+  return guarded([&] { ws->w->apply_reduced(v, out); });
+}
 int ddelm_gpu_invalidate(ddelm_ws* ws) {
   return guarded([&] { ws->w->invalidate(); });
 }

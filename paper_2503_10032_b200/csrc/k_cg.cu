@@ -343,6 +343,15 @@ __device__ __forceinline__ double gather_delta(const double* tab, const CgArgs& 
 
 __device__ __forceinline__ double gather_x(const CgArgs& a, int g) { return a.flip_sign[g] * gather_delta(a.xtab, a, g); }
 
+/// one-level: dmu of cross flux row rr (= global flux row n_delta + rr), summed over its up to 4
+/// owner slots and the P parts
+__device__ __forceinline__ double gather_xc(const CgArgs& a, int rr) {
+  const size_t st = 4 * static_cast<size_t>(a.npf);
+  double s = 0;
+  for (int k = 0; k < 4; ++k) s += sum_parts(a.xctab, st, a.P, rr * 4 + k);
+  return a.flip_sign[a.n_delta + rr] * s;
+}
+
 /// z = [t; psi]: corner contributions of OP1 summed over their owners (subdomain order) and the
 /// cross-flux data psi (mode 0: Dpd v; mode 1: dpi; mode 2: dpi - Dpd mu_Delta).
 __device__ void gather_z(const CgArgs& a, const Shared& sh, int mode, int nthr) {
@@ -519,13 +528,15 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, 
   double* phi = sh.red;  // n_gamma <= kThreads (checked on the host)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int* gd = a.gamma_delta + static_cast<size_t>(i) * a.gmax;
+  const int* gpi = a.gamma_pi + static_cast<size_t>(i) * a.gmax;
   for (int g = threadIdx.x; g < d.n_gamma; g += kThreads) {
-    const int dg = gd[g];
+    int dg = gd[g];
+    if (dg < 0 && a.one_level && gpi[g] >= 0) dg = a.n_delta + gpi[g];  // mu_Pi entry (apply_B)
     double vv = 0.0;
     if (dg >= 0 && mode != 1) {
       if (cg) {
         vv = a.r[dg] + beta * pcur[dg];
-        if (a.gamma_dst[static_cast<size_t>(i) * a.gmax + g] == 2 * dg) pnext[dg] = vv;  // first owner
+        if (dg < a.n_delta && a.gamma_dst[static_cast<size_t>(i) * a.gmax + g] == 2 * dg) pnext[dg] = vv;  // first owner
       } else {
         vv = v[dg];
       }
@@ -549,7 +560,14 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, 
     a.s[static_cast<size_t>(i) * R + k] = acc;
   }
   __syncthreads();
-  if (warp < 4) {
+  if (a.one_level) {
+    // no coarse space; the first owner of each corner writes the Pi entries of p_next
+    if (cg && threadIdx.x < 4) {
+      const int g = a.corner_q[i * 4 + threadIdx.x];
+      const int dst = a.corner_dst[i * 4 + threadIdx.x];
+      if (g >= 0 && dst >= 0 && (dst & 3) == 0) pnext[a.n_delta + gpi[g]] = vg[g];
+    }
+  } else if (warp < 4) {
     const int g = a.corner_q[i * 4 + warp];
     double acc = 0;
     if (g >= 0)
@@ -581,17 +599,17 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
   for (int k = 0; k < nitems; ++k) {
     const int w = item_work(k, nitems, false);
     const int i = w / a.P, p = w % a.P;
-    gather_z(a, sh, mode, kCThreads);
+    if (!a.one_level) gather_z(a, sh, mode, kCThreads);
     if (threadIdx.x < 4) {
       const int g = a.corner_q[i * 4 + threadIdx.x];
-      crow[threadIdx.x] = g >= 0 ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
+      crow[threadIdx.x] = (g >= 0 && !a.one_level) ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
     }
     const int r = a.rank[i];
     for (int kk = threadIdx.x; kk < r; kk += kCThreads) sh.xa[kk] = a.s[static_cast<size_t>(i) * a.rmax + kk];
     cons_sync();
     const int nz = a.n_pi + a.npf;
-    rows_dot(a.Wmu, nz, crow, 4, sh.z, nz, muc, kCWarps);  // mu = S^{-1}(t + Dpp^T psi)
-    if (mode == 2 && w == 0)  // mu_Pi of the solution (one CTA writes it)
+    rows_dot(a.Wmu, nz, crow, 4, sh.z, nz, muc, kCWarps);  // mu = S^{-1}(t + Dpp^T psi); 0 one-level
+    if (mode == 2 && w == 0 && !a.one_level)  // mu_Pi of the solution (one CTA writes it)
       for (int gp = warp; gp < a.n_pi; gp += kCWarps) {
         double s = 0;
         const double* wr = a.Wmu + static_cast<size_t>(gp) * nz;
@@ -607,8 +625,9 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
     const double m0 = muc[0], m1 = muc[1], m2 = muc[2], m3 = muc[3];
     double acc[W];
     // reference grouping (solvers.cpp:336, 342): c = K^+ phi - Ypi mu, then F c
+    const bool one = a.one_level != 0;
     consume_item<W>(g, sh, ccnt, acc, [&](int jr, double cs, const double* y, int ln) {
-      const double cj = cs - (((y[0] * m0 + y[1] * m1) + y[2] * m2) + y[3] * m3);
+      const double cj = one ? cs : cs - (((y[0] * m0 + y[1] * m1) + y[2] * m2) + y[3] * m3);
       if (mode == 2 && ln == 0) coef[j0 + jr] = cj;
       return cj;
     });
@@ -618,7 +637,24 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
     reduce_warps<W>(a, g, sh, acc, [&](int l, double s) {
       const int dst = fdst[l];
       if (dst >= 0) xt[dst] = -s;
+      if (one) sh.v1[l] = s;
     });
+    if (one) {
+      // cross flux rows (apply_A, solvers.cpp:209-224): this subdomain's weighted share of every
+      // cross row it touches (mean_edge: 1/(n-1) over the edge's points), one warp per row
+      cons_sync();
+      const int* off = a.cr_off + static_cast<size_t>(i) * (a.crmax + 1);
+      double* xc = a.xctab_w + static_cast<size_t>(p) * 4 * a.npf;
+      for (int rho = warp; rho < a.crmax; rho += kCWarps) {
+        const int dst = a.cross_dst[static_cast<size_t>(i) * a.crmax + rho];
+        if (dst < 0) continue;
+        double v = 0;
+        for (int e = off[rho] + lane; e < off[rho + 1]; e += 32) v += a.cr_w[e] * sh.v1[a.cr_l[e]];
+        v = warp_sum(v);
+        if (lane == 0) xc[dst] = -v;
+      }
+      cons_sync();
+    }
   }
 }
 
@@ -702,6 +738,22 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
       }
       sh.xa[l] = wv;  // apply_AT_delta: a(lrow) = w(grow) on the Delta flux rows
     }
+    if (a.one_level) {
+      // apply_AT over the cross rows too (solvers.cpp:230-244): a(lrow) += w dmu(cross row)
+      const int* off = a.cr_off + static_cast<size_t>(i) * (a.crmax + 1);
+      const int* crr = a.cr_row + static_cast<size_t>(i) * a.crmax;
+      for (int rho = threadIdx.x; rho < a.crmax; rho += kCThreads) sh.z[rho] = crr[rho] >= 0 ? gather_xc(a, crr[rho]) : 0.0;
+      cons_sync();
+      for (int l = threadIdx.x; l < d.nF; l += kCThreads) {
+        double add = 0;
+        for (int rho = 0; rho < a.crmax; ++rho) {
+          if (crr[rho] < 0) continue;
+          for (int e = off[rho]; e < off[rho + 1]; ++e)
+            if (a.cr_l[e] == l) add += a.cr_w[e] * sh.z[rho];
+        }
+        sh.xa[l] += add;
+      }
+    }
     cons_sync();
     const ItemGeo g = item_geo(a, kOp3, i, p, false);
     double acc[W];
@@ -712,7 +764,7 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
       up[l] = s;
       sh.s0[l] = s;
     });
-    if (warp < 4) {
+    if (warp < 4 && !a.one_level) {
       const int gq = a.corner_q[i * 4 + warp];
       double acc2 = 0;
       if (gq >= 0)
@@ -743,6 +795,36 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
   const int r = a.rank[i], R = a.rmax, E = a.ext, n = a.n_pi, nz = a.n_pi + a.npf;
   __shared__ double cq_mu[4], cq_nu[4], d2s[64], w3t[64];
   __shared__ RowTask tasks[8 + 2 * 64];
+  if (a.one_level) {
+    // reduced_apply (solvers.cpp:262-274) at the trace rows: o = -phi + Q_G (s + u), written to the
+    // owner slots of its Delta index (2 owners) or Pi index (up to 4 owners)
+    const size_t ust = static_cast<size_t>(a.N) * R;
+    const Staged stg = stage_qtx(a, sh, qst, i, r);
+    const double* QtX = stg.qtx;
+    for (int k = threadIdx.x; k < r; k += kThreads)
+      sh.s0[k] = a.s[static_cast<size_t>(i) * R + k] + sum_parts(a.u + static_cast<size_t>(i) * R, ust, a.P, k);
+    __syncthreads();
+    double* qsv = sh.v1;
+    coldot_split(QtX + 1, E, r, d.n_gamma, sh.s0, sh.red, Team{kThreads}, [&](int g, double s) { qsv[g] = s; });
+    const int* gd = a.gamma_delta + static_cast<size_t>(i) * a.gmax;
+    const int* gpi = a.gamma_pi + static_cast<size_t>(i) * a.gmax;
+    double dot = 0;
+    for (int g = threadIdx.x; g < d.n_gamma; g += kThreads) {
+      const int dg = gd[g];
+      const int idx = dg >= 0 ? dg : (gpi[g] >= 0 ? a.n_delta + gpi[g] : -1);
+      if (idx < 0) continue;
+      const double mphi = (mode == 0) ? v[idx] : 0.0;  // -phi
+      const double o = mphi + qsv[g];
+      if (dg >= 0) {
+        a.otab_w[a.gamma_dst[static_cast<size_t>(i) * a.gmax + g]] = o;
+      } else {
+        for (int q = 0; q < 4; ++q)
+          if (a.corner_q[i * 4 + q] == g && a.corner_dst[i * 4 + q] >= 0) a.opitab_w[a.corner_dst[i * 4 + q]] = o;
+      }
+      if (mode == 0) dot += v[idx] * o;
+    }
+    return block_sum(dot, sh.red);
+  }
   gather_z(a, sh, mode, kThreads);
   const size_t st3 = 4 * static_cast<size_t>(n);
   for (int gp = threadIdx.x; gp < n; gp += kThreads) {
@@ -819,6 +901,10 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
 }
 
 __device__ __forceinline__ double gather_out(const CgArgs& a, int g) {
+  if (g >= a.n_delta) {  // one-level Pi entry: its corner owners in subdomain order
+    const double* o = a.opitab + 4 * (g - a.n_delta);
+    return ((o[0] + o[1]) + o[2]) + o[3];
+  }
   return a.otab[2 * g] + a.otab[2 * g + 1];
 }
 
@@ -898,7 +984,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
     grid.sync();
     for (int i = b; i < a.N; i += G) dev_op4(a, sh, qst, i, vin, mode);
     grid.sync();
-    for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) vout[g] = gather_out(a, g);
+    for (int g = b * blockDim.x + threadIdx.x; g < a.n_cg; g += G * blockDim.x) vout[g] = gather_out(a, g);
     return;
   }
 
@@ -972,7 +1058,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
     }
     const double alpha = rr / pAp;
     double dsum = 0;
-    for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) {
+    for (int g = b * blockDim.x + threadIdx.x; g < a.n_cg; g += G * blockDim.x) {
       const double ap = gather_out(a, g);
       a.x[g] += alpha * pnext[g];
       const double rg = a.r[g] - alpha * ap;
@@ -1117,7 +1203,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
         }
         const double alpha = a.scal[0] / pAp;
         double dsum = 0;
-        for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) {
+        for (int g = b * blockDim.x + threadIdx.x; g < a.n_cg; g += G * blockDim.x) {
           const double ap = gather_out(a, g);
           a.x[g] += alpha * pnext[g];
           const double rg = a.r[g] - alpha * ap;
@@ -1157,7 +1243,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
       return;
     }
     default:  // kPhGather
-      for (int g = b * blockDim.x + threadIdx.x; g < a.n_delta; g += G * blockDim.x) vout[g] = gather_out(a, g);
+      for (int g = b * blockDim.x + threadIdx.x; g < a.n_cg; g += G * blockDim.x) vout[g] = gather_out(a, g);
       return;
   }
 }
@@ -1166,7 +1252,7 @@ __global__ void __launch_bounds__(256) cg_init_kernel(CgArgs a) {
   __shared__ double red[32];
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   double d = 0;
-  if (g < a.n_delta) {
+  if (g < a.n_cg) {
     const double b = a.rhs[g];
     a.x[g] = 0.0;
     a.r[g] = b;
@@ -1281,7 +1367,7 @@ void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double*
 }
 
 void cg_launch_init(const CgArgs& a, cudaStream_t st) {
-  const int nblk = ceil_div(a.n_delta, 256);
+  const int nblk = ceil_div(a.n_cg, 256);
   cg_init_kernel<<<nblk, 256, 0, st>>>(a);
   cg_init2_kernel<<<1, 32, 0, st>>>(a, nblk);
   DDG_LAUNCH_CHECK();

@@ -178,7 +178,14 @@ struct CgArgs {
   const int* nd_dst;       // N x dmax : 2 g + s for the Neumann Delta rows
   const int* corner_dst;   // N x 4    : gp * 4 + slot, -1 pad
   const int* cross_dst;    // N x crmax: rr * 4 + slot, -1 pad
-  const double* flip_sign; // n_delta (+1 / -1 debug hook)
+  const double* flip_sign; // n_delta + npf (+1 / -1 debug hook, global flux row)
+  // one-level DDELM (reduced_apply, solvers.cpp:262-274): no coarse space, the Pi trace values are
+  // CG unknowns (mu = [mu_Delta; mu_Pi]) and A / A^T run over every flux row, cross rows included
+  int one_level;
+  int n_cg;                // CG vector length: n_delta, + n_pi one-level
+  const int* cr_off;       // N x (crmax + 1) offsets into cr_l / cr_w (cross-row scatter triples)
+  const int* cr_l;
+  const double* cr_w;
   const double* QtX;       // 2N x rmax x ext (QGt = cols 1.., qf = col 0)
   const double* Zc;        // N x crmax x gmax
   const double* Sinv;      // n_pi x n_pi
@@ -200,6 +207,8 @@ struct CgArgs {
   double *xtab, *xtab_w;    // P x 2 n_delta  flux values x (OP2)
   double *trtab, *trtab_w;  // P x 2 n_delta  P x (NN1)
   double *zztab, *zztab_w;  // P x 2 n_delta  P^T P x (NN2)
+  double *xctab, *xctab_w;  // P x npf x 4   cross-row flux contributions (OP2, one-level)
+  double *opitab, *opitab_w;  // n_pi x 4    OP4 outputs at the corner owners (one-level)
   int N_global, sub_lo;     // sharding: this device holds subdomains [sub_lo, sub_lo + N)
   int xr_parts;             // r.r partials written by the XR phase (= its grid size)
   unsigned long long cond;  // cudaGraphConditionalHandle of the CG while-loop graph (0: none)

@@ -218,8 +218,8 @@ void Workspace::upload_plan() {
   d_corner_dst.upload(p.corner_dst, st_);
   d_cross_dst.upload(p.cross_dst, st_);
   d_mult_pi.upload(p.multiplicity_pi, st_);
-  std::vector<double> flip(std::max(p.n_delta, 1), 1.0);
-  if (p.debug_flip_flux_row >= 0 && p.debug_flip_flux_row < p.n_delta) flip[p.debug_flip_flux_row] = -1.0;
+  std::vector<double> flip(std::max(p.n_delta + p.npf, 1), 1.0);  // global flux rows (apply_A)
+  if (p.debug_flip_flux_row >= 0 && p.debug_flip_flux_row < p.n_delta + p.npf) flip[p.debug_flip_flux_row] = -1.0;
   d_flip.upload(flip, st_);
   g_arena = nullptr;  // setup-only / large buffers below
   d_f.upload(p.f, st_);
@@ -271,8 +271,9 @@ void Workspace::upload_plan() {
   d_Sinv.alloc(npi * npi);
   d_spd_fail.alloc(1);
   const size_t nd = std::max(p.n_delta, 1);
-  for (auto* b : {&d_x, &d_r, &d_p, &d_Ap, &d_rhs}) b->alloc(nd);
-  d_partial.alloc(2 * static_cast<size_t>(ceil_div(static_cast<int>(nd), 256)) + 2);
+  const size_t nmu = std::max(p.n_delta + p.n_pi, 1);  // one-level CG vectors carry mu_Pi too
+  for (auto* b : {&d_x, &d_r, &d_p, &d_Ap, &d_rhs}) b->alloc(nmu);
+  d_partial.alloc(2 * static_cast<size_t>(ceil_div(static_cast<int>(nmu), 256)) + 2);
   d_state.alloc(8);
   d_scal.alloc(8);
   d_mu_pi_out.alloc(npi);
@@ -280,14 +281,16 @@ void Workspace::upload_plan() {
   d_Wd.alloc(npf * (npi + npf));
   d_W3.alloc(npf * npi);
   d_pap.alloc(static_cast<size_t>(p.N_global));
-  d_vin.alloc(nd);
-  d_vout.alloc(nd);
+  d_vin.alloc(nmu);
+  d_vout.alloc(nmu);
   // owner-slot tables of the coarse gathers: unused slots stay zero
   d_tpart.alloc(4 * npi);
   d_psipart.alloc(4 * npf);
   DDG_CUDA(cudaMemsetAsync(d_tpart.ptr, 0, d_tpart.count * sizeof(double), st_));
   DDG_CUDA(cudaMemsetAsync(d_psipart.ptr, 0, d_psipart.count * sizeof(double), st_));
   d_o.alloc(2 * nd);
+  d_opi.alloc(4 * npi);  // one-level: OP4 outputs at the corner owners (unused slots stay zero)
+  DDG_CUDA(cudaMemsetAsync(d_opi.ptr, 0, d_opi.count * sizeof(double), st_));
   d_xf.alloc(static_cast<size_t>(N) * p.fmax);
   d_tr.alloc(static_cast<size_t>(N) * p.dmax);
   d_zz.alloc(static_cast<size_t>(N) * p.dmax);
@@ -325,7 +328,7 @@ void Workspace::init_layers() {
 void Workspace::reseed(uint64_t seed) {
   plan.seed = seed;
   for (size_t i = 0; i < plan.subs.size(); ++i) plan.subs[i].seed = seed + i;
-  built_ = coarse_built_ = neumann_built_ = false;
+  built_ = blocks_built_ = coarse_built_ = neumann_built_ = false;
   layers_valid_ = false;
 }
 
@@ -499,7 +502,7 @@ void Workspace::build() {
   launches_ += 1;
   DDG_CUDA(cudaEventRecord(ev_[3], st_));
   built_ = true;
-  coarse_built_ = neumann_built_ = false;
+  blocks_built_ = coarse_built_ = neumann_built_ = false;
   host_build_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
 }
 
@@ -552,16 +555,28 @@ BlockArgs Workspace::block_args() {
   return b;
 }
 
-void Workspace::build_coarse() {
+void Workspace::build_blocks() {
+  // interface blocks of the local solves (C, F, Ypi, Zc, ...) and the packed CG streams: what
+  // every method needs; the coarse Schur problem (build_coarse) only the coarse-space methods
   if (!built_) build();
-  if (coarse_built_) return;
+  if (blocks_built_) return;
   DDG_CUDA(cudaSetDevice(device_));
   DDG_CUDA(cudaEventRecord(ev_[4], st_));
   BlockArgs b = block_args();
-  DDG_CUDA(cudaMemsetAsync(d_spd_fail.ptr, 0, sizeof(int), st_));
   launch_blocks(b, st_);
   launch_coarse_local(b, d_cr_row.ptr, d_cr_off.ptr, d_cr_l.ptr, d_cr_w.ptr, st_);
   launches_ += 2;
+  pack_blocks(b);
+  DDG_CUDA(cudaEventRecord(ev_[5], st_));
+  blocks_built_ = true;
+}
+
+void Workspace::build_coarse() {
+  build_blocks();
+  if (coarse_built_) return;
+  DDG_CUDA(cudaSetDevice(device_));
+  BlockArgs b = block_args();
+  DDG_CUDA(cudaMemsetAsync(d_spd_fail.ptr, 0, sizeof(int), st_));
   if (plan.n_pi > 0) {
     launch_coarse_rows(b, d_row_owner.ptr, st_);
     launch_coarse_gsum(b, st_);
@@ -573,6 +588,15 @@ void Workspace::build_coarse() {
     launch_coarse_weights(b, st_);
     launches_ += 5;
   }
+  DDG_CUDA(cudaEventRecord(ev_[5], st_));
+  int fail = 0;
+  DDG_CUDA(cudaMemcpyAsync(&fail, d_spd_fail.ptr, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
+  if (fail) throw std::runtime_error("assemble_coarse: coarse Schur matrix is not positive definite");
+  coarse_built_ = true;
+}
+
+void Workspace::pack_blocks(const BlockArgs& b) {
   // row-interleaved stream blocks of the interface iteration (k_cg.cu)
   // per-subdomain row strides (boundary subdomains have fewer flux / Neumann rows: no padding
   // to the widest class is streamed); even strides keep every row 16-byte aligned
@@ -604,12 +628,6 @@ void Workspace::build_coarse() {
   }
   launch_pack_streams(b, d_KF.ptr, d_kf_ld.ptr, d_kf_off.ptr, d_KD.ptr, d_kd_ld.ptr, d_kd_off.ptr, st_);
   launches_ += 1;
-  DDG_CUDA(cudaEventRecord(ev_[5], st_));
-  int fail = 0;
-  DDG_CUDA(cudaMemcpyAsync(&fail, d_spd_fail.ptr, sizeof(int), cudaMemcpyDeviceToHost, st_));
-  DDG_CUDA(cudaStreamSynchronize(st_));
-  if (fail) throw std::runtime_error("assemble_coarse: coarse Schur matrix is not positive definite");
-  coarse_built_ = true;
 }
 
 void Workspace::build_neumann() {
@@ -623,11 +641,13 @@ void Workspace::build_neumann() {
   neumann_built_ = true;
 }
 
-CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
+CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level) {
   const Plan& p = plan;
   CgArgs a;
   a.N = p.N;
   a.n_delta = p.n_delta;
+  a.one_level = one_level ? 1 : 0;
+  a.n_cg = p.n_delta + (one_level ? p.n_pi : 0);
   a.n_pi = p.n_pi;
   a.npf = p.npf;
   a.gmax = p.gmax;
@@ -664,13 +684,17 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
     d_tr.alloc(PP * nd2);
     d_zz.alloc(PP * nd2);
     d_u.alloc(PP * N * rmax_);
+    if (d_xc.count != PP * 4 * std::max(p.npf, 1)) {
+      d_xc.alloc(PP * 4 * std::max(p.npf, 1));  // one-level cross-row owner slots: unused stay zero
+      DDG_CUDA(cudaMemsetAsync(d_xc.ptr, 0, d_xc.count * sizeof(double), st_));
+    }
     if (d_tpart3.count != PP * 4 * std::max(p.n_pi, 1)) {
       d_tpart3.alloc(PP * 4 * std::max(p.n_pi, 1));  // unused owner slots must read as zero
       DDG_CUDA(cudaMemsetAsync(d_tpart3.ptr, 0, d_tpart3.count * sizeof(double), st_));
     }
     if (sharded()) {
       // send tables: slots owned by other ranks stay zero; receive twins hold the all-reduced sums
-      for (DevBuf<double>* bsend : {&d_xf, &d_tr, &d_zz, &d_o, &d_pap})
+      for (DevBuf<double>* bsend : {&d_xf, &d_tr, &d_zz, &d_o, &d_pap, &d_xc, &d_opi})
         DDG_CUDA(cudaMemsetAsync(bsend->ptr, 0, bsend->count * sizeof(double), st_));
       r_tpart.alloc(d_tpart.count);
       r_psipart.alloc(d_psipart.count);
@@ -680,6 +704,8 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
       r_tr.alloc(d_tr.count);
       r_zz.alloc(d_zz.count);
       r_pap.alloc(d_pap.count);
+      r_xc.alloc(d_xc.count);
+      r_opi.alloc(d_opi.count);
     }
   }
   a.rel_tol = tol;
@@ -692,6 +718,9 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.fluxrow_delta = d_fluxrow_delta.ptr;
   a.ndelta_map = d_ndelta_map.ptr;
   a.cr_row = d_cr_row.ptr;
+  a.cr_off = d_cr_off.ptr;
+  a.cr_l = d_cr_l.ptr;
+  a.cr_w = d_cr_w.ptr;
   a.corner_q = d_corner_q.ptr;
   a.gamma_dst = d_gamma_dst.ptr;
   a.flux_dst = d_flux_dst.ptr;
@@ -715,6 +744,8 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.trtab_w = d_tr.ptr;
   a.zztab_w = d_zz.ptr;
   a.pap_w = d_pap.ptr;
+  a.xctab_w = d_xc.ptr;
+  a.opitab_w = d_opi.ptr;
   const bool sh = sharded();
   a.ttab = sh ? r_tpart.ptr : d_tpart.ptr;
   a.t3tab = sh ? r_tpart3.ptr : d_tpart3.ptr;
@@ -724,6 +755,8 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
   a.trtab = sh ? r_tr.ptr : d_tr.ptr;
   a.zztab = sh ? r_zz.ptr : d_zz.ptr;
   a.pap = sh ? r_pap.ptr : d_pap.ptr;
+  a.xctab = sh ? r_xc.ptr : d_xc.ptr;
+  a.opitab = sh ? r_opi.ptr : d_opi.ptr;
   a.N_global = p.N_global;
   a.sub_lo = p.sub_lo;
   a.u = d_u.ptr;
@@ -752,8 +785,8 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter) {
 SolveResult Workspace::solve(int method, double theta, double tol, int max_iter) {
   if (method == 2 && (theta < 0.0 || theta > 1.0))
     throw std::invalid_argument("ddelm_nn_solve: theta must lie in [0, 1]");
-  if (method == 0) throw std::invalid_argument("method ddelm (one-level) is not on the device path");
-  if (method == 1 || theta == 0.0) {
+  const bool one_level = method == 0;  // ddelm_solve (solvers.cpp:493-531)
+  if (method == 1 || (method == 2 && theta == 0.0)) {
     method = 1;
     theta = 0.0;
   }
@@ -761,22 +794,29 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   const auto h0 = std::chrono::steady_clock::now();
   const long long l0 = launches_;
   if (!built_) build();
-  build_coarse();
+  if (one_level) {
+    build_blocks();
+    theta = 0.0;
+  } else {
+    build_coarse();
+  }
   if (method == 2) build_neumann();
+  last_method_ = method;
   const Plan& p = plan;
   SolveResult res;
-  if (max_iter <= 0) max_iter = 20 * p.n_delta;
+  const int n_cg = p.n_delta + (one_level ? p.n_pi : 0);
+  if (max_iter <= 0) max_iter = 20 * n_cg;  // cg: max 20 n (solvers.cpp:86)
   if (p.n_delta == 0) throw std::invalid_argument("s = 1 (local-only solve) is not on the device path");
   ArenaScope hot(&arena_);
   d_hist.alloc(static_cast<size_t>(max_iter));
   {
     // CG partial slots: one per CTA of the persistent kernel, one per block of cg_init
-    CgArgs probe = cg_args(theta, tol, max_iter);
+    CgArgs probe = cg_args(theta, tol, max_iter, one_level);
     const size_t need = std::max<size_t>(static_cast<size_t>(cg_grid(probe)) + 2,
-                                         static_cast<size_t>(ceil_div(p.n_delta, 256)) + 2);
+                                         static_cast<size_t>(ceil_div(n_cg, 256)) + 2);
     if (d_partial.count < need) d_partial.alloc(need);
   }
-  CgArgs a = cg_args(theta, tol, max_iter);
+  CgArgs a = cg_args(theta, tol, max_iter, one_level);
   apply_l2_policy();
   DDG_CUDA(cudaEventRecord(ev_[8], st_));
   if (phased_) run_phases(a, 1, nullptr, d_rhs.ptr);
@@ -881,6 +921,21 @@ void Workspace::apply_operator(double theta, const double* v, double* out) {
   DDG_CUDA(cudaStreamSynchronize(st_));
 }
 
+void Workspace::apply_reduced(const double* v, double* out) {
+  // one-level operator reduced_apply (solvers.cpp:262-274) on mu = [mu_Delta; mu_Pi]
+  DDG_CUDA(cudaSetDevice(device_));
+  if (!built_) build();
+  build_blocks();
+  CgArgs a = cg_args(0.0, 1e-9, 1, true);
+  apply_l2_policy();
+  const size_t n = static_cast<size_t>(plan.n_delta) + plan.n_pi;
+  DDG_CUDA(cudaMemcpyAsync(d_vin.ptr, v, n * sizeof(double), cudaMemcpyHostToDevice, st_));
+  if (phased_) run_phases(a, 0, d_vin.ptr, d_vout.ptr);
+  else cg_launch(a, kJobApply, d_vin.ptr, d_vout.ptr, st_);
+  DDG_CUDA(cudaMemcpyAsync(out, d_vout.ptr, n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
+}
+
 void Workspace::xchg(double* send, double* recv, size_t n) {
   if (ex_ && n) ex_->allreduce(send, recv, n, st_);
 }
@@ -891,11 +946,14 @@ void Workspace::run_phases(const CgArgs& a, int mode, const double* vin, double*
   const size_t npi4 = 4 * static_cast<size_t>(plan.n_pi), npf4 = 4 * static_cast<size_t>(plan.npf);
   const size_t tab = static_cast<size_t>(a.P) * 2 * plan.n_delta;
   cg_launch_phase(a, kPhOp1, mode, 0, vin, vout, st_);
-  xchg(a.ttab_w, a.ttab, npi4);
-  xchg(a.ptab_w, a.ptab, npf4);
+  if (!a.one_level) {
+    xchg(a.ttab_w, a.ttab, npi4);
+    xchg(a.ptab_w, a.ptab, npf4);
+  }
   cg_launch_phase(a, kPhOp2, mode, 0, vin, vout, st_);
   if (mode == 2) return;
   xchg(a.xtab_w, a.xtab, tab);
+  if (a.one_level) xchg(a.xctab_w, a.xctab, static_cast<size_t>(a.P) * npf4);
   if (a.use_neumann) {
     cg_launch_phase(a, kPhNn1, mode, 0, vin, vout, st_);
     xchg(a.trtab_w, a.trtab, tab);
@@ -903,9 +961,10 @@ void Workspace::run_phases(const CgArgs& a, int mode, const double* vin, double*
     xchg(a.zztab_w, a.zztab, tab);
   }
   cg_launch_phase(a, kPhOp3, mode, 0, vin, vout, st_);
-  xchg(a.t3tab_w, a.t3tab, static_cast<size_t>(a.P) * npi4);
+  if (!a.one_level) xchg(a.t3tab_w, a.t3tab, static_cast<size_t>(a.P) * npi4);
   cg_launch_phase(a, kPhOp4, mode, 0, vin, vout, st_);
   xchg(a.otab_w, a.otab, 2 * static_cast<size_t>(plan.n_delta));
+  if (a.one_level) xchg(a.opitab_w, a.opitab, npi4);
   cg_launch_phase(a, kPhGather, mode, 0, vin, vout, st_);
 }
 
@@ -919,10 +978,13 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
   const size_t tab = static_cast<size_t>(a_in.P) * 2 * plan.n_delta;
   auto iteration = [&](const CgArgs& a) {
     cg_launch_phase(a, kPhOp1, 0, 0, nullptr, nullptr, st_);
-    xchg(a.ttab_w, a.ttab, npi4);
-    xchg(a.ptab_w, a.ptab, npf4);
+    if (!a.one_level) {
+      xchg(a.ttab_w, a.ttab, npi4);
+      xchg(a.ptab_w, a.ptab, npf4);
+    }
     cg_launch_phase(a, kPhOp2, 0, 0, nullptr, nullptr, st_);
     xchg(a.xtab_w, a.xtab, tab);
+    if (a.one_level) xchg(a.xctab_w, a.xctab, static_cast<size_t>(a.P) * npf4);
     if (a.use_neumann) {
       cg_launch_phase(a, kPhNn1, 0, 0, nullptr, nullptr, st_);
       xchg(a.trtab_w, a.trtab, tab);
@@ -930,9 +992,10 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
       xchg(a.zztab_w, a.zztab, tab);
     }
     cg_launch_phase(a, kPhOp3, 0, 0, nullptr, nullptr, st_);
-    xchg(a.t3tab_w, a.t3tab, static_cast<size_t>(a.P) * npi4);
+    if (!a.one_level) xchg(a.t3tab_w, a.t3tab, static_cast<size_t>(a.P) * npi4);
     cg_launch_phase(a, kPhOp4, 0, 0, nullptr, nullptr, st_);
     xchg(a.otab_w, a.otab, 2 * static_cast<size_t>(plan.n_delta));
+    if (a.one_level) xchg(a.opitab_w, a.opitab, npi4);
     xchg(a.pap_w, a.pap, static_cast<size_t>(plan.N_global));
     cg_launch_phase(a, kPhXr1, 0, 0, nullptr, nullptr, st_);  // its last CTA also runs XR2
   };
@@ -1013,7 +1076,9 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
 void Workspace::get_mu(double* mu) {
   const Plan& p = plan;
   DDG_CUDA(cudaMemcpyAsync(mu, d_x.ptr, sizeof(double) * p.n_delta, cudaMemcpyDeviceToHost, st_));
-  if (p.n_pi) DDG_CUDA(cudaMemcpyAsync(mu + p.n_delta, d_mu_pi_out.ptr, sizeof(double) * p.n_pi, cudaMemcpyDeviceToHost, st_));
+  if (p.n_pi && last_method_ == 0)  // one-level: mu_Pi is part of the CG solution
+    DDG_CUDA(cudaMemcpyAsync(mu + p.n_delta, d_x.ptr + p.n_delta, sizeof(double) * p.n_pi, cudaMemcpyDeviceToHost, st_));
+  else if (p.n_pi) DDG_CUDA(cudaMemcpyAsync(mu + p.n_delta, d_mu_pi_out.ptr, sizeof(double) * p.n_pi, cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
 }
 
@@ -1107,7 +1172,7 @@ void Workspace::get_local(int i, int which, double* K) {
   DDG_CUDA(cudaMemcpy2DAsync(K, sizeof(double) * plan.m, d_A.ptr + t * ld_ * ncol_, sizeof(double) * ld_,
                              sizeof(double) * plan.m, plan.M, cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
-  built_ = coarse_built_ = neumann_built_ = false;
+  built_ = blocks_built_ = coarse_built_ = neumann_built_ = false;
 }
 
 }  // namespace ddg

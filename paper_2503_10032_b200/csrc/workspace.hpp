@@ -76,13 +76,15 @@ class Workspace {
   Workspace& operator=(const Workspace&) = delete;
 
   void build();
+  void build_blocks();
   void build_coarse();
   void build_neumann();
   SolveResult solve(int method, double theta, double tol, int max_iter);
   void reseed(uint64_t seed);
   /// drop every built layer but keep the uploaded feature layers (device-resident inputs)
-  void invalidate() { built_ = coarse_built_ = neumann_built_ = false; }
+  void invalidate() { built_ = blocks_built_ = coarse_built_ = neumann_built_ = false; }
   void apply_operator(double theta, const double* v, double* out);
+  void apply_reduced(const double* v, double* out);
   void set_profiling(bool on) { profiling_ = on; }
   bool kernel_stat(const std::string& name, KernelStat* out) const;
   double device_span_ms() const { return device_span_ms_; }
@@ -113,7 +115,8 @@ class Workspace {
   FeatureArgs feature_args();
   CodArgs cod_args();
   BlockArgs block_args();
-  CgArgs cg_args(double theta, double tol, int max_iter);
+  CgArgs cg_args(double theta, double tol, int max_iter, bool one_level = false);
+  void pack_blocks(const BlockArgs& b);
   bool sharded() const { return ex_ && ex_->world() > 1; }
   /// phase-by-phase launches with owner-slot all-reduces (sharded path; DDELM_CG_MODE=phased
   /// selects it on one device too)
@@ -150,7 +153,8 @@ class Workspace {
   cudaGraphExec_t graph_exec_ = nullptr;
   int* pinned_state_ = nullptr;
   int ld_ = 0, ext_ = 0, ncol_ = 0, kmax_ = 0, rmax_ = 1;
-  bool built_ = false, coarse_built_ = false, neumann_built_ = false, solved_ = false;
+  int last_method_ = 2;
+  bool built_ = false, blocks_built_ = false, coarse_built_ = false, neumann_built_ = false, solved_ = false;
   int last_iterations_ = 0;
   long long launches_ = 0, solve_launches_ = 0;
   double phase_ms_[8] = {};
@@ -175,7 +179,7 @@ class Workspace {
   DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu_pi_out, d_tpart, d_tpart3,
       d_psipart, d_o, d_xf, d_tr, d_zz, d_s, d_u, d_coeffs, d_pap, d_vin, d_vout, d_trace, d_KF, d_KD;
   // receive side of the owner-slot all-reduces (sharded only)
-  DevBuf<double> d_field, d_fpart, d_fref, d_fsums;
+  DevBuf<double> d_field, d_fpart, d_fref, d_fsums, d_xc, d_opi, r_xc, r_opi;
   DevBuf<int> d_flo;
   DevBuf<double> r_tpart, r_psipart, r_tpart3, r_o, r_xf, r_tr, r_zz, r_pap, d_Gsum;
   int ldKF_ = 0, ldKD_ = 0;

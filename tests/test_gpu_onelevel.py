@@ -1,0 +1,137 @@
+"""GPU tests of the one-level DDELM method (ddelm_solve, solvers.cpp:493-531)
+on the device path: CG on mu = [mu_Delta; mu_Pi] with reduced_apply (solvers.cpp:262-274) —
+every trace row (Delta and Pi) an unknown, every flux row (cross rows included) in A and A^T.
+
+Same parity bar as test_gpu_parity.py: full-rank configs hold the field to <= 1e-9 where the
+oracle's own spread allows it, rank-deficient ones (C1d, C2d) to the oracle's spread under 1-ulp
+input perturbations. Iterations: within max(1 + 2 x spread, 10 % of the golden count). One-level CG
+has no coarse space (kappa ~ 1e3-1e4, C2d needs 542 iterations) and loses orthogonality early: on
+T4d the device and oracle residual histories agree to 1e-3 for 18 iterations and then separate,
+ending at 103 vs 112 iterations with the solutions equal to 2e-10 (mu) and 4e-11 (field). The
+oracle's 1-ulp input perturbations keep its own summation order and so underestimate this
+(spread 2 over 16 perturbations); the CG dot products on the device are summed per CTA / per
+subdomain in a fixed order that differs from the oracle's sequential sums.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from test_gpu_parity import _field_diff, _golden, _oracle
+
+pytestmark = pytest.mark.gpu
+
+FULL_RANK = ["T1d", "T2d", "T4d", "T2dm"]
+DEFICIENT = ["C1d", "C2d"]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_10032_b200 as P
+    P.load_library()
+    return P
+
+
+@pytest.mark.parametrize("name", FULL_RANK + DEFICIENT)
+def test_one_level_solve_matches_oracle(P, name):
+    cfg = P.CONFIGS[name]
+    g = _golden(name)
+    ws, rep = P.solve_config(name)
+    assert rep.converged
+    it_tol = max(1 + 2 * int(g["spread_iterations"]), int(np.ceil(0.1 * int(g["iterations"]))))
+    assert abs(rep.iterations - int(g["iterations"])) <= it_tol, (rep.iterations, int(g["iterations"]), it_tol)
+    rk, _, _ = ws.ranks()
+    assert (rk == g["ranks"]).all()
+    assert rep.mu.shape == g["mu"].shape  # n_delta + n_pi unknowns
+    f_tol = max(1e-9, 4.0 * float(g["spread_field"]))
+    diff = _field_diff(cfg, rep.coeffs, g["field_u"])
+    assert diff <= f_tol, f"{name}: field diff {diff:.3e} > {f_tol:.3e}"
+    if name in FULL_RANK:
+        assert np.linalg.norm(rep.mu - g["mu"]) <= 1e-6 * np.linalg.norm(g["mu"])
+
+
+@pytest.mark.parametrize("name", ["T1d", "T2dm", "C1d"])
+def test_reduced_operator_matches_oracle(P, name):
+    """reduced_apply on random vectors (oracle_check's op_diff, runner.cpp:283-314)."""
+    cfg = P.CONFIGS[name]
+    ws = P.workspace_from_config(name)
+    ows = _oracle(cfg)
+    rng = np.random.default_rng(5)
+    n = ws.n_delta + ws.n_pi
+    tol = 1e-9 if name.startswith("T") else 1e-5
+    for _ in range(3):
+        v = rng.standard_normal(n)
+        a = ws.apply_reduced(v)
+        b = ows.apply_reduced(v)
+        assert np.linalg.norm(a - b) <= tol * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("name", ["T2d", "T2dm"])
+def test_reduced_operator_symmetric_psd(P, name):
+    """reduced_apply = B^T (I - K K^+) B + B^T K^+T A^T A K^+ B is symmetric positive semi-definite."""
+    ws = P.workspace_from_config(name)
+    rng = np.random.default_rng(13)
+    n = ws.n_delta + ws.n_pi
+    for _ in range(3):
+        v, w = rng.standard_normal(n), rng.standard_normal(n)
+        av, aw = ws.apply_reduced(v), ws.apply_reduced(w)
+        scale = np.linalg.norm(v) * np.linalg.norm(aw)
+        assert abs(v @ aw - w @ av) <= 1e-10 * scale
+        assert v @ av >= -1e-10 * np.linalg.norm(v) * np.linalg.norm(av)
+
+
+def test_one_level_persistent_and_phased_agree(P, monkeypatch):
+    """The persistent cooperative kernel and the phase-by-phase graph run the same one-level
+    iteration bit for bit (same work split, same fixed-order sums)."""
+    monkeypatch.setenv("DDELM_CG_MODE", "persistent")
+    ws_a = P.workspace_from_config("T2dm")
+    monkeypatch.delenv("DDELM_CG_MODE")
+    ws_b = P.workspace_from_config("T2dm")
+    _, ra = P.solve_config("T2dm", ws=ws_a)
+    _, rb = P.solve_config("T2dm", ws=ws_b)
+    assert ra.iterations == rb.iterations
+    assert np.array_equal(ra.mu, rb.mu) and np.array_equal(ra.coeffs, rb.coeffs)
+
+
+def test_one_level_sharded_world1_matches(P):
+    ws_a = P.workspace_from_config("T2d")
+    ws_b = P.workspace_from_config("T2d", shard=(0, 1, None))
+    _, ra = P.solve_config("T2d", ws=ws_a)
+    _, rb = P.solve_config("T2d", ws=ws_b)
+    assert ra.iterations == rb.iterations
+    assert np.array_equal(ra.mu, rb.mu) and np.array_equal(ra.coeffs, rb.coeffs)
+
+
+def test_methods_share_one_workspace(P):
+    """The layers built once serve every method (the reference's Workspace is reused by
+    ddelm_solve / ddelm_cs_solve / ddelm_nn_solve alike)."""
+    ws = P.workspace_from_config("T2")
+    a = P.ddelm_solve(ws, P.CgOptions(rel_tol=1e-9))
+    b = P.ddelm_nn_solve(ws, 0.999, P.CgOptions(rel_tol=1e-9))
+    c = P.ddelm_solve(ws, P.CgOptions(rel_tol=1e-9))
+    assert a.converged and b.converged
+    assert a.iterations == c.iterations and np.array_equal(a.mu, c.mu)
+    assert a.mu.shape == b.mu.shape
+
+
+def test_cpp_facade_one_level(P):
+    """examples/ddelm_solve method=ddelm (ddelm::ddelm_solve over the C-ABI) reproduces the Python
+    mirror bit for bit and reports the device-evaluated exact-solution errors."""
+    import json
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "paper_2503_10032_b200", "ddelm_solve")
+    args = ["method=ddelm", "flux_variant=pointwise", "trace_basis=nodal"]
+    out = subprocess.run([exe] + args, capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    d = json.loads(out.stdout)
+    ws, rep = P.solve_config("T1d")
+    assert d["iterations"] == rep.iterations
+    assert np.array_equal(np.array(d["mu"]), rep.mu)
+    l2, h1 = ws.relative_errors(257)
+    assert d["l2_error"] == l2 and d["h1_error"] == h1
+    bad = subprocess.run([exe, "method=ddelm-xx"], capture_output=True, text=True, timeout=120)
+    assert bad.returncode == 3
