@@ -210,6 +210,19 @@ __device__ __forceinline__ int item_work(int k, int nitems, bool reverse) {
   return blockIdx.x + (reverse ? nitems - 1 - k : k) * gridDim.x;
 }
 
+/// Per-CTA timestamps of the streamed-phase trace (DDELM_CG_TRACE, phase-by-phase driver):
+/// [0] kernel entry, [1] after griddepcontrol.wait, [2] first chunk consumed, [3] last chunk done,
+/// [4] prologue done (consumers enter the stream).
+__device__ __forceinline__ unsigned long long* phase_stamps() {
+  __shared__ unsigned long long t[5];
+  return t;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  return now;
+}
+
 /// Producer (warp 15, lane 0): walks the chunks of this CTA's items of one streamed phase.
 /// `cnt` counts every chunk ever issued by this CTA: stage = cnt % kStages, use = cnt / kStages.
 struct Producer {
@@ -271,6 +284,7 @@ template <int W, class Hook>
 __device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt, double (&acc)[W], Hook hook) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double xr[W];
+  if (threadIdx.x == 0 && phase_stamps()[4] == 0) phase_stamps()[4] = gtimer();
 #pragma unroll
   for (int q = 0; q < W; ++q) {
     const int k = lane + 32 * q;
@@ -283,6 +297,7 @@ __device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt,
     const int st = ccnt % kStages;
     const double* S = sh.ring + static_cast<size_t>(st) * (kStageBytes / 8);
     mbar_wait(&sh.full[st], (ccnt / kStages) & 1u);
+    if (threadIdx.x == 0 && phase_stamps()[2] == 0) phase_stamps()[2] = gtimer();
     for (int rr = warp; rr < nr; rr += kCWarps) {
       const double* row = S + static_cast<size_t>(rr) * g.ld;
       const double* ar = row + g.aoff;
@@ -307,6 +322,7 @@ __device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt,
     if (lane == 0) mbar_arrive(&sh.empty[st]);
     ++ccnt;
   }
+  if (threadIdx.x == 0) phase_stamps()[3] = gtimer();
 }
 
 /// Sum the consumer warps' accumulators (fixed warp order) and hand out column l values.
@@ -330,6 +346,18 @@ __device__ void reduce_warps(const CgArgs& a, const ItemGeo& g, const Shared& sh
 
 // ---------------------------------------------------------------- small helpers
 __device__ __forceinline__ double sum_parts(const double* base, size_t stride, int P, int idx) {
+  // every part's load in flight before the (fixed-order) sum: the prologues are latency chains
+  constexpr int kMaxP = 8;
+  if (P <= kMaxP) {
+    double v[kMaxP];
+#pragma unroll
+    for (int p = 0; p < kMaxP; ++p) v[p] = p < P ? base[p * stride + idx] : 0.0;
+    double s = 0;
+#pragma unroll
+    for (int p = 0; p < kMaxP; ++p)
+      if (p < P) s += v[p];
+    return s;
+  }
   double s = 0;
   for (int p = 0; p < P; ++p) s += base[p * stride + idx];
   return s;
@@ -379,7 +407,15 @@ __device__ void rows_dot(const double* W, int ldw, const int* rows, int nrows, c
     double s = 0;
     if (row >= 0) {
       const double* w = W + static_cast<size_t>(row) * ldw;
-      for (int k = lane; k < len; k += 32) s += w[k] * vec[k];
+      int k = lane;
+      for (; k + 96 < len; k += 128) {  // four loads in flight per lane
+        const double w0 = w[k], w1 = w[k + 32], w2 = w[k + 64], w3 = w[k + 96];
+        s += w0 * vec[k];
+        s += w1 * vec[k + 32];
+        s += w2 * vec[k + 64];
+        s += w3 * vec[k + 96];
+      }
+      for (; k < len; k += 32) s += w[k] * vec[k];
     }
     s = warp_sum(s);
     if (lane == 0) out[q] = s;
@@ -399,7 +435,23 @@ __device__ void rowdot4(const double* Q, int ldq, int nk, int ne, const double* 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int k0 = 4 * warp; k0 < nk; k0 += 4 * nwarps) {
     double c[4] = {0, 0, 0, 0};
-    for (int e = lane; e < ne; e += 32) {
+    int e = lane;
+    for (; e + 32 < ne; e += 64) {  // 8 loads in flight per lane (latency-bound prologues)
+      double q0[4], q1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* qr = Q + static_cast<size_t>(k0 + u < nk ? k0 + u : k0) * ldq;
+        q0[u] = qr[e];
+        q1[u] = qr[e + 32];
+      }
+      const double x0 = x[e], x1 = x[e + 32];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c[u] += q0[u] * x0;
+        c[u] += q1[u] * x1;
+      }
+    }
+    for (; e < ne; e += 32) {
       const double xe = x[e];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -426,6 +478,14 @@ __device__ void coldot_split(const double* Q, int ldq, int nk, int nc, const dou
     const int k0 = (nk * grp) / G, k1 = (nk * (grp + 1)) / G;
     double s1 = 0;
     int k = k0;
+    for (; k + 3 < k1; k += 4) {  // four loads in flight
+      const double q0 = Q[static_cast<size_t>(k) * ldq + c], q1 = Q[static_cast<size_t>(k + 1) * ldq + c];
+      const double q2 = Q[static_cast<size_t>(k + 2) * ldq + c], q3 = Q[static_cast<size_t>(k + 3) * ldq + c];
+      s += q0 * x[k];
+      s1 += q1 * x[k + 1];
+      s += q2 * x[k + 2];
+      s1 += q3 * x[k + 3];
+    }
     for (; k + 1 < k1; k += 2) {
       s += Q[static_cast<size_t>(k) * ldq + c] * x[k];
       s1 += Q[static_cast<size_t>(k + 1) * ldq + c] * x[k + 1];
@@ -1109,6 +1169,8 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
   __shared__ double bsum[32];
   const Shared sh = carve(a, bars);
   if (threadIdx.x == 0) {
+    phase_stamps()[0] = a.trace ? gtimer() : 0;
+    phase_stamps()[2] = phase_stamps()[3] = phase_stamps()[4] = 0;
     for (int s2 = 0; s2 < kStages; ++s2) {
       mbar_init(&sh.full[s2], 1);
       mbar_init(&sh.empty[s2], kCWarps);
@@ -1140,6 +1202,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
     stage_issue(a, sh, qst, b, a.rank[b], &qb);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (a.trace && threadIdx.x == 0) phase_stamps()[1] = gtimer();
   if (cg) it = a.state[6];  // the iteration counter lives on the device (graph replays)
   double* pcur = a.pbuf[(it + 1) & 1];
   double* pnext = a.pbuf[it & 1];
@@ -1179,6 +1242,17 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
         dev_op3<W>(a, sh, ccnt);
       }
       __syncthreads();
+      if (a.trace && threadIdx.x == 0 && phase_stamps()[2] != 0) {
+        // streamed-phase trace: slots 16 + 4 (phase - kPhOp2) + {entry->wait, wait->first chunk,
+        // first chunk->last chunk, last chunk->exit}, ns summed over the launches
+        const unsigned long long* t = phase_stamps();
+        const unsigned long long end = gtimer();
+        double* tr = a.trace + b * 32 + 16 + 4 * (phase - kPhOp2);
+        tr[0] += static_cast<double>(t[4] - t[1]);  // prologue (after the wait)
+        tr[1] += static_cast<double>(t[2] - t[4]);  // first chunk's data wait
+        tr[2] += static_cast<double>(t[3] - t[2]);
+        tr[3] += static_cast<double>(end - t[3]);
+      }
       return;
     }
     case kPhOp4:

@@ -14,7 +14,9 @@
 //   C      = P Z^T [I_r; 0] T^{-1}   (M x r)      so that  K^+ = C Q_r^T
 //   QtX    = Q_r^T [f | E]           (r x ext)    (Q_r = Q0 Q1[:, :r])
 // The full-rank branch (solvers.cpp:43-44) is the same contract with r = M, C = R0^{-1}.
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -60,8 +62,8 @@ __device__ ArgMax block_argmax(ArgMax x, ArgMax* sh) {
   return r;
 }
 
-__global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
-  const int t = blockIdx.x;
+__global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
+  const int t = t0 + blockIdx.x;
   const int M = a.M, K = a.kmax;
   const double mn = a.ratio[2 * t], mx = a.ratio[2 * t + 1];
   const bool deficient = !(mx > 0) || mn < a.rank_tol * mx;  // solvers.cpp:32
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
       double s = 0.0;
       if (i < Reff) {
         s = (i <= ck) ? R0[static_cast<size_t>(ck) * ld + i] : 0.0;
+#pragma unroll 8
         for (int u = 0; u < k; ++u) s -= V1[static_cast<size_t>(u) * M + i] * w[u];
       }
       v[i] = s;
@@ -224,6 +227,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
     // ---- w = V(:, 0:k)^T v ; vk = V(k, 0:k]
     for (int u = warp; u < k; u += nwarp) {
       double s = 0;
+#pragma unroll 8
       for (int i = k + lane; i < Reff; i += 32) s += V1[static_cast<size_t>(u) * M + i] * v[i];
       s = warp_sum(s);
       if (lane == 0) w[u] = s;
@@ -244,12 +248,14 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
       }
       const int imax = max(max(iend[0], iend[1]), max(iend[2], iend[3]));
       double g[4] = {0, 0, 0, 0}, fw[4] = {0, 0, 0, 0};
+#pragma unroll 8
       for (int i = k + lane; i <= imax; i += 32) {
         const double vi = v[i];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (i <= iend[q]) g[q] += col[q][i] * vi;
       }
+#pragma unroll 4
       for (int u = lane; u < k; u += 32) {
         const double wu = w[u];
 #pragma unroll
@@ -268,6 +274,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
     for (int j = k + 1 + threadIdx.x; j < M; j += blockDim.x) {
       const int cj = perm[j];
       double rkj = (k <= cj) ? R0[static_cast<size_t>(cj) * ld + k] : 0.0;
+#pragma unroll 8
       for (int u = 0; u <= k; ++u) rkj -= vk[u] * F1[static_cast<size_t>(j) * K + u];
       Rr[static_cast<size_t>(k) * M + j] = rkj;
       if (upd[j] != 0.0) {
@@ -320,6 +327,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
         double e[kRecB];
 #pragma unroll
         for (int q = 0; q < kRecB; ++q) e[q] = (i <= cjs[q]) ? R0[static_cast<size_t>(cjs[q]) * ld + i] : 0.0;
+#pragma unroll 4
         for (int u = 0; u <= k; ++u) {
           const double vv = V1[static_cast<size_t>(u) * M + i];
 #pragma unroll
@@ -350,6 +358,166 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a) {
     for (int u = 0; u < k; ++u) r += fabs(Rr[static_cast<size_t>(u) * M + u]) > pre ? 1 : 0;
     a.rank[t] = r;
   }
+}
+
+// ---------------------------------------------------------------- blocked finish (r <= kFinR)
+// The three reflector applications of the finish — Y = Z^T [I_r; 0] (RZ), C = Y T11^{-1} and
+// Q_r^T X = Q1^T X (pivoted-QR reflectors) — as compact-WY products on the FP64 tensor cores
+// instead of one reflector at a time: G = V^T V, T by the dlarft recurrence, then
+// (I - V T^T V^T) as two small GEMMs. The sequential form (below, kept for r > kFinR) spent
+// ~5 us per reflector on dependent global loads.
+constexpr int kFinR = 96;
+constexpr int kFinEB = 64;  // X columns per block of the Q1^T application
+
+/// out(m, n, sum_k A(k, m) B(k, n)) for m < Mo, n < No, k < Ko, with A(k, m) = A[k*sak + m*sam]
+/// and B(k, n) = B[k*sbk + n*sbn]: 8 x 8 output tiles over the CTA's warps, DMMA m8n8k4.
+template <class Out>
+__device__ void tile_gemm_tn(int Mo, int No, int Ko, const double* A, long sak, long sam, const double* B,
+                             long sbk, long sbn, Out out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int tm = (Mo + 7) >> 3, tn = (No + 7) >> 3;
+  for (int tile = warp; tile < tm * tn; tile += nw) {
+    const int m0 = (tile / tn) * 8, n0 = (tile % tn) * 8;
+    const bool mok = m0 + lr < Mo, nok = n0 + lr < No;
+    const double* Ap = A + (mok ? m0 + lr : 0) * sam;
+    const double* Bp = B + (nok ? n0 + lr : 0) * sbn;
+    double c0 = 0, c1 = 0;
+    int k = 0;
+    for (; k + 16 <= Ko; k += 16) {  // 8 loads in flight per lane
+      double av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long kk = k + 4 * u + lc;
+        av[u] = mok ? Ap[kk * sak] : 0.0;
+        bv[u] = nok ? Bp[kk * sbk] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma_8x8x4(c0, c1, av[u], bv[u]);
+    }
+    for (; k < Ko; k += 4) {
+      const int kk = k + lc;
+      const double av = (mok && kk < Ko) ? Ap[static_cast<long>(kk) * sak] : 0.0;
+      const double bv = (nok && kk < Ko) ? Bp[static_cast<long>(kk) * sbk] : 0.0;
+      dmma_8x8x4(c0, c1, av, bv);
+    }
+    const int om = m0 + lr, on = n0 + 2 * lc;
+    if (om < Mo) {
+      if (on < No) out(om, on, c0);
+      if (on + 1 < No) out(om, on + 1, c1);
+    }
+  }
+}
+
+/// dlarft (forward, columnwise) from the Gram matrix: T(j,j) = tau_j,
+/// T(0:j, j) = -tau_j T(0:j, 0:j) G(0:j, j); T upper triangular, zero below.
+__device__ void larft_from_gram(const double* G, int ldg, const double* tau, int r, double* T, int ldt) {
+  for (int idx = threadIdx.x; idx < r * ldt; idx += blockDim.x) T[idx] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < r; ++j) {
+    double s = 0;
+    const int i = threadIdx.x;
+    if (i < j)
+      for (int w = i; w < j; ++w) s += T[i * ldt + w] * G[w * ldg + j];
+    __syncthreads();
+    if (i < j) T[i * ldt + j] = -tau[j] * s;
+    if (i == j) T[j * ldt + j] = tau[j];
+    __syncthreads();
+  }
+}
+
+/// Y, C and Q_r^T X of a deficient matrix with numerical rank r <= kFinR (after the RZ pass).
+__device__ void finish_wy(const CodArgs& a, int t, int r, const double* X, const double* Rr, const double* V1,
+                          const double* tau1, const int* perm, const double* zc, double* Y, double* C,
+                          double* QtX) {
+  extern __shared__ __align__(16) double fsm[];
+  const int M = a.M, R = a.rmax, E = a.ext;
+  const long ld = a.ld;
+  const int reff = a.reff[t];  // V1 rows >= reff are zero
+  const int ldt = r + 1;       // odd stride: conflict-free row access
+  double* T = fsm;             // r x ldt
+  double* G = T + r * ldt;     // r x ldt
+  // ---- Y = Z^T [I_r; 0]: z_k = e_k + tail Rr(k, r:M) (COD's RZ reflectors, applied k = 0..r-1),
+  //      so Y = [I_r; 0] - Z T^T Z^T [I_r; 0] = [I_r - T^T; -Z_tail T^T]
+  if (r < M) {
+    tile_gemm_tn(r, r, M - r, Rr + r, 1, M, Rr + r, 1, M,
+                 [&](int m, int n, double v) { G[m * ldt + n] = v + (m == n ? 1.0 : 0.0); });
+    __syncthreads();
+    larft_from_gram(G, ldt, zc, r, T, ldt);
+    for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
+      const int c = idx / r, j = idx % r;
+      Y[static_cast<size_t>(c) * M + j] = (j == c ? 1.0 : 0.0) - T[c * ldt + j];
+    }
+    tile_gemm_tn(M - r, r, r, Rr + r, M, 1, T, 1, ldt,
+                 [&](int m, int n, double v) { Y[static_cast<size_t>(n) * M + r + m] = -v; });
+  } else {
+    for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
+      const int c = idx / r, j = idx % r;
+      Y[static_cast<size_t>(c) * M + j] = (j == c ? 1.0 : 0.0);
+    }
+  }
+  __syncthreads();
+  // ---- C(perm[i], :) = Y(i, :) T11^{-1}, T11 = upper triangle of Rr(0:r, 0:r): the triangular
+  //      inverse by columns (thread per column), then one GEMM
+  double* T11 = fsm;            // r x ldt
+  double* U = T11 + r * ldt;    // r x ldt : T11^{-1}
+  for (int idx = threadIdx.x; idx < r * ldt; idx += blockDim.x) {
+    const int u = idx / ldt, c = idx % ldt;
+    T11[idx] = (c < r && u <= c) ? Rr[static_cast<size_t>(u) * M + c] : 0.0;
+    U[idx] = 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < r) {
+    const int c = threadIdx.x;
+    U[c * ldt + c] = 1.0 / T11[c * ldt + c];
+    for (int i = c - 1; i >= 0; --i) {
+      double s = 0;
+      for (int u = i + 1; u <= c; ++u) s += T11[i * ldt + u] * U[u * ldt + c];
+      U[i * ldt + c] = -s / T11[i * ldt + i];
+    }
+  }
+  __syncthreads();
+  tile_gemm_tn(M, r, r, Y, M, 1, U, ldt, 1,
+               [&](int m, int n, double v) { C[static_cast<size_t>(perm[m]) * R + n] = v; });
+  for (int idx = threadIdx.x; idx < M * (R - r); idx += blockDim.x) {
+    const int i = idx / (R - r), c = r + idx % (R - r);
+    C[static_cast<size_t>(perm[i]) * R + c] = 0.0;
+  }
+  __syncthreads();
+  // ---- Q_r^T X = top r rows of Q1^T X, Q1^T = I - V T^T V^T (V = V1, rows < reff)
+  tile_gemm_tn(r, r, reff, V1, 1, M, V1, 1, M, [&](int m, int n, double v) { G[m * ldt + n] = v; });
+  __syncthreads();
+  larft_from_gram(G, ldt, tau1, r, T, ldt);
+  const int ldw = kFinEB + 1;
+  double* Wb = G;                           // r x ldw : V^T X(:, block)   (G is free again)
+  double* Wt = G + r * max(ldt, ldw);       // r x ldw : T^T W
+  for (int e0 = 0; e0 < E; e0 += kFinEB) {
+    const int eb = min(kFinEB, E - e0);
+    const double* Xb = X + static_cast<size_t>(e0) * ld;
+    tile_gemm_tn(r, eb, reff, V1, 1, M, Xb, 1, ld, [&](int m, int n, double v) { Wb[m * ldw + n] = v; });
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < r * eb; idx += blockDim.x) {
+      const int u = idx / eb, e = idx % eb;
+      double s = 0;
+      for (int w = 0; w <= u; ++w) s += T[w * ldt + u] * Wb[w * ldw + e];
+      Wt[u * ldw + e] = s;
+    }
+    __syncthreads();
+    tile_gemm_tn(r, eb, r, V1, M, 1, Wt, ldw, 1, [&](int m, int n, double v) {
+      QtX[static_cast<size_t>(m) * E + e0 + n] = Xb[static_cast<size_t>(n) * ld + m] - v;
+    });
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < (R - r) * E; idx += blockDim.x)
+    QtX[static_cast<size_t>(r) * E + idx] = 0.0;
+}
+
+size_t finish_smem_bytes(int rmax) {
+  // T (r x (r+1)), G / W-block (r x max(r+1, kFinEB+1)), T^T W block (r x (kFinEB+1))
+  const int r = min(rmax, kFinR);
+  const size_t ldt = r + 1, ldw = kFinEB + 1;
+  return (static_cast<size_t>(r) * ldt + static_cast<size_t>(r) * std::max(ldt, ldw) + static_cast<size_t>(r) * ldw) *
+         sizeof(double);
 }
 
 /// RZ + C + Q^T X for a deficient matrix; C = R0^{-1}, Q^T X = X for a full-rank one.
@@ -449,6 +617,11 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
       __syncthreads();
     }
   }
+  if (r <= kFinR) {
+    __syncthreads();
+    finish_wy(a, t, r, X, Rr, V1, tau1, perm, zc, Y, C, QtX);
+    return;
+  }
   // ---- Y = Z^T [I_r; 0] (COD::solve's Z^* application): one warp per column, the column held
   // in registers (lane owns rows lane + 32 t), no block barriers between reflectors.
   // Stored transposed, Yt(c, j) = Y[c*M + j], so every access is coalesced.
@@ -539,12 +712,14 @@ void launch_cod_pivqr(const CodArgs& a, cudaStream_t st) {
   const size_t smem = sizeof(double) * (a.M + (2 + kRecB) * a.kmax) + sizeof(int) * a.M;
   DDG_CUDA(cudaFuncSetAttribute(cod_pivqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  cod_pivqr_kernel<<<a.nmat, 512, smem, st>>>(a);
+  cod_pivqr_kernel<<<a.nmat, 512, smem, st>>>(a, 0);
   DDG_LAUNCH_CHECK();
 }
 
 void launch_cod_finish(const CodArgs& a, cudaStream_t st) {
-  cod_finish_kernel<<<a.nmat, 512, 0, st>>>(a);
+  const size_t smem = finish_smem_bytes(a.rmax);
+  DDG_CUDA(cudaFuncSetAttribute(cod_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  cod_finish_kernel<<<a.nmat, 512, smem, st>>>(a);
   DDG_LAUNCH_CHECK();
 }
 

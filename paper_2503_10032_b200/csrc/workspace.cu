@@ -777,6 +777,7 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.trace = nullptr;
   if (std::getenv("DDELM_CG_TRACE")) {
     d_trace.alloc(148 * 4 * 32);
+    DDG_CUDA(cudaMemsetAsync(d_trace.ptr, 0, d_trace.count * sizeof(double), st_));
     a.trace = d_trace.ptr;
   }
   return a;
@@ -889,6 +890,20 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
                                     "-",       "-",       "-",        "-",      "-",      "-",       "-",   "-"};
     std::fprintf(stderr, "[cg trace] %d iterations, G=%d, P=%d (us/iteration: max / mean over CTAs)\n",
                  res.iterations, G, a.P);
+    if (phased_) {
+      static const char* ph[4] = {"op2", "nn1", "nn2", "op3"};
+      static const char* part[4] = {"prologue", "1st chunk wait", "streaming", "epilogue"};
+      for (int q = 0; q < 4; ++q)
+        for (int k = 0; k < 4; ++k) {
+          double mx = 0, mean = 0;
+          for (int b = 0; b < G; ++b) {
+            mx = std::max(mx, t[b * 32 + 16 + 4 * q + k]);
+            mean += t[b * 32 + 16 + 4 * q + k] / G;
+          }
+          const double it = std::max(res.iterations, 1);
+          std::fprintf(stderr, "[cg trace] %s %-16s %8.2f %8.2f\n", ph[q], part[k], mx / it / 1e3, mean / it / 1e3);
+        }
+    }
     for (int k = 0; k < 22; ++k) {
       if (k == 15) continue;
       double mx = 0, mean = 0;
