@@ -81,16 +81,18 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
   double* F1 = a.F1 + static_cast<size_t>(t) * M * K;
   double* Rr = a.Rr + static_cast<size_t>(t) * K * M;
   double* tau1 = a.tau1 + static_cast<size_t>(t) * K;
-  double* upd = a.upd + static_cast<size_t>(t) * M;
-  double* dir = a.dir + static_cast<size_t>(t) * M;
-  int* perm = a.perm + static_cast<size_t>(t) * M;
 
   extern __shared__ double sm[];
-  double* v = sm;            // M
+  double* v = sm;            // M  (pivot column, then the reflector)
   double* w = v + M;         // K
   double* vk = w + K;        // K  (row k of V)
   double* Fs = vk + K;       // kRecB x K  (F rows of the columns being recomputed)
-  int* flist = reinterpret_cast<int*>(Fs + kRecB * K);  // M
+  double* upd = Fs + kRecB * K;  // M  updated column norms (by position)
+  double* dir = upd + M;         // M  norms at the last exact computation (-1: recompute)
+  double* gs = dir + M;          // M  A(k:, j)^T v of the current step
+  int* flist = reinterpret_cast<int*>(gs + M);  // M
+  int* perm = flist + M;                        // M
+  int* permg = a.perm + static_cast<size_t>(t) * M;
   __shared__ double redq[kRecB * 32];
   __shared__ int wcnt[32], woff[32], cjs[kRecB];
   __shared__ int s_nflag;
@@ -101,6 +103,8 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const double eps = DBL_EPSILON;
   const double downdate_thr = sqrt(eps);
+  // F is stored transposed, F1[u*M + j] (reflector u, column position j): every per-column pass
+  // below reads it coalesced across threads
 
   // ---- effective row count of R0: rows whose tail energy ||R0(i:, i:)||_F is below
   //      kRowTruncation * ||R0||_F carry only round-off (the numerical rank is ~70 of M = 800), so
@@ -173,9 +177,9 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
         const int ti = perm[k]; perm[k] = perm[p]; perm[p] = ti;
       }
       for (int u = threadIdx.x; u < k; u += blockDim.x) {
-        double tmp = F1[static_cast<size_t>(k) * K + u];
-        F1[static_cast<size_t>(k) * K + u] = F1[static_cast<size_t>(p) * K + u];
-        F1[static_cast<size_t>(p) * K + u] = tmp;
+        double tmp = F1[static_cast<size_t>(u) * M + k];
+        F1[static_cast<size_t>(u) * M + k] = F1[static_cast<size_t>(u) * M + p];
+        F1[static_cast<size_t>(u) * M + p] = tmp;
         tmp = Rr[static_cast<size_t>(u) * M + k];
         Rr[static_cast<size_t>(u) * M + k] = Rr[static_cast<size_t>(u) * M + p];
         Rr[static_cast<size_t>(u) * M + p] = tmp;
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
     __syncthreads();
     // ---- updated pivot column (rows k..M-1): R0(:, perm[k]) - V F(k, :)^T
     const int ck = perm[k];
-    for (int u = threadIdx.x; u < k; u += blockDim.x) w[u] = F1[static_cast<size_t>(k) * K + u];
+    for (int u = threadIdx.x; u < k; u += blockDim.x) w[u] = F1[static_cast<size_t>(u) * M + k];
     __syncthreads();
     for (int i = k + threadIdx.x; i < M; i += blockDim.x) {
       double s = 0.0;
@@ -233,9 +237,8 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       if (lane == 0) w[u] = s;
     }
     for (int u = threadIdx.x; u <= k; u += blockDim.x) vk[u] = V1[static_cast<size_t>(u) * M + k];
-    __syncthreads();
-    // ---- F(:, k) = tau (A^T v - F V^T v) for positions j > k: a warp per 4 columns, lanes over
-    //      rows, 4 independent load streams (memory-level parallelism of the R0 / F1 reads)
+    // ---- g_j = A(k:, j)^T v for positions j > k (the original R0 columns: the dlaqps GEMV, the
+    //      only pass over R0 per step): a warp per 4 columns, lanes over rows
     for (int j0 = k + 1 + 4 * warp; j0 < M; j0 += 4 * nwarp) {
       const double* col[4];
       int iend[4];
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
         iend[q] = (j0 + q < M) ? min(cj, Reff - 1) : k - 1;
       }
       const int imax = max(max(iend[0], iend[1]), max(iend[2], iend[3]));
-      double g[4] = {0, 0, 0, 0}, fw[4] = {0, 0, 0, 0};
+      double g[4] = {0, 0, 0, 0};
 #pragma unroll 8
       for (int i = k + lane; i <= imax; i += 32) {
         const double vi = v[i];
@@ -255,27 +258,29 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
         for (int q = 0; q < 4; ++q)
           if (i <= iend[q]) g[q] += col[q][i] * vi;
       }
-#pragma unroll 4
-      for (int u = lane; u < k; u += 32) {
-        const double wu = w[u];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (j0 + q < M) fw[q] += F1[static_cast<size_t>(j0 + q) * K + u] * wu;
-      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const double gg = warp_sum(g[q]);
-        const double ff = warp_sum(fw[q]);
-        if (lane == 0 && j0 + q < M) F1[static_cast<size_t>(j0 + q) * K + k] = s_tau * (gg - ff);
+        if (lane == 0 && j0 + q < M) gs[j0 + q] = gg;
       }
     }
     __syncthreads();
-    // ---- row k of R and norm downdating (thread per column)
+    // ---- per column position j > k (thread per j, coalesced over F1[u*M + j]):
+    //      F(j, k) = tau (g_j - F(j, 0:k) w), row k of R: R(k, j) = R0(k, cj) - F(j, 0:k] . V(k, 0:k],
+    //      and the LAPACK norm downdate (flag for exact recomputation below sqrt(eps))
+    int any_flag = 0;
     for (int j = k + 1 + threadIdx.x; j < M; j += blockDim.x) {
       const int cj = perm[j];
-      double rkj = (k <= cj) ? R0[static_cast<size_t>(cj) * ld + k] : 0.0;
+      double fw = 0, fv = 0;
 #pragma unroll 8
-      for (int u = 0; u <= k; ++u) rkj -= vk[u] * F1[static_cast<size_t>(j) * K + u];
+      for (int u = 0; u < k; ++u) {
+        const double f = F1[static_cast<size_t>(u) * M + j];
+        fw += f * w[u];
+        fv += f * vk[u];
+      }
+      const double fk = s_tau * (gs[j] - fw);
+      F1[static_cast<size_t>(k) * M + j] = fk;
+      const double rkj = ((k <= cj) ? R0[static_cast<size_t>(cj) * ld + k] : 0.0) - fv - vk[k] * fk;
       Rr[static_cast<size_t>(k) * M + j] = rkj;
       if (upd[j] != 0.0) {
         double tmp = fabs(rkj) / upd[j];
@@ -283,11 +288,15 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
         if (tmp < 0) tmp = 0;
         const double ratio = upd[j] / dir[j];
         const double tmp2 = tmp * ratio * ratio;
-        if (tmp2 <= downdate_thr) dir[j] = -1.0;  // flag: recompute exactly below
-        else upd[j] *= sqrt(tmp);
+        if (tmp2 <= downdate_thr) {
+          dir[j] = -1.0;  // flag: recompute exactly below
+          any_flag = 1;
+        } else {
+          upd[j] *= sqrt(tmp);
+        }
       }
     }
-    __syncthreads();
+    if (!__syncthreads_or(any_flag)) continue;
     // ---- exact recomputation of flagged norms: ||(A - V F^T)(k+1:M, j)||
     // compact the flagged columns (increasing j), then a register-blocked pass over rows that
     // serves 8 columns per V1 read (a small GEMM instead of one warp per column)
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       const int nb = min(kRecB, nflag - f0);
       for (int idx = threadIdx.x; idx < kRecB * (k + 1); idx += blockDim.x) {
         const int q = idx / (k + 1), u = idx % (k + 1);
-        Fs[q * K + u] = q < nb ? F1[static_cast<size_t>(flist[f0 + q]) * K + u] : 0.0;
+        Fs[q * K + u] = q < nb ? F1[static_cast<size_t>(u) * M + flist[f0 + q]] : 0.0;
       }
       if (threadIdx.x < kRecB) cjs[threadIdx.x] = threadIdx.x < nb ? perm[flist[f0 + threadIdx.x]] : -1;
       __syncthreads();
@@ -352,6 +361,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
     }
   }
   __syncthreads();
+  for (int j = threadIdx.x; j < M; j += blockDim.x) permg[j] = perm[j];
   if (threadIdx.x == 0) {
     const double pre = s_maxpivot * a.rank_tol;
     int r = 0;
@@ -709,7 +719,7 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
 }  // namespace
 
 void launch_cod_pivqr(const CodArgs& a, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (a.M + (2 + kRecB) * a.kmax) + sizeof(int) * a.M;
+  const size_t smem = sizeof(double) * (4 * a.M + (2 + kRecB) * a.kmax) + sizeof(int) * 2 * a.M;
   DDG_CUDA(cudaFuncSetAttribute(cod_pivqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   cod_pivqr_kernel<<<a.nmat, 512, smem, st>>>(a, 0);

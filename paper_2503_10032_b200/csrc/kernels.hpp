@@ -69,7 +69,7 @@ struct CodArgs {
   int* deficient;        // per matrix: branch taken (1 = COD)
   // pivoted-QR state (per matrix)
   double* V1;    // kmax x M  (reflector t at V1[t*M + i])
-  double* F1;    // M x kmax  (F1[j*kmax + t])
+  double* F1;    // kmax x M  (F1[t*M + j]: reflector t, column position j)
   double* Rr;    // kmax x M  (R rows by column position)
   double* tau1;  // kmax
   double* upd;   // M
