@@ -251,12 +251,20 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       }
       const int imax = max(max(iend[0], iend[1]), max(iend[2], iend[3]));
       double g[4] = {0, 0, 0, 0};
-#pragma unroll 8
-      for (int i = k + lane; i <= imax; i += 32) {
-        const double vi = v[i];
+      constexpr int kU = 6;  // rows per lane per batch: 24 independent loads in flight
+      for (int i0 = k + lane; i0 <= imax; i0 += 32 * kU) {
+        double x[kU][4], vv[kU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (i <= iend[q]) g[q] += col[q][i] * vi;
+        for (int u = 0; u < kU; ++u) {
+          const int i = i0 + 32 * u;
+          vv[u] = i <= imax ? v[i] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[u][q] = i <= iend[q] ? col[q][i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) g[q] += x[u][q] * vv[u];
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
