@@ -25,7 +25,6 @@ namespace ddg {
 
 namespace {
 
-constexpr int kRecB = 8;  // flagged columns recomputed per register-blocked pass
 constexpr double kRowTruncation = 1e-14;  // R0 rows with tail energy below this x ||R0||_F are dropped
 constexpr int kNPL = 32;  // register rows per lane in the finish kernel: M <= 32 * 32
 
@@ -86,15 +85,13 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
   double* v = sm;            // M  (pivot column, then the reflector)
   double* w = v + M;         // K
   double* vk = w + K;        // K  (row k of V)
-  double* Fs = vk + K;       // kRecB x K  (F rows of the columns being recomputed)
-  double* upd = Fs + kRecB * K;  // M  updated column norms (by position)
+  double* upd = vk + K;          // M  updated column norms (by position)
   double* dir = upd + M;         // M  norms at the last exact computation (-1: recompute)
   double* gs = dir + M;          // M  A(k:, j)^T v of the current step
   int* flist = reinterpret_cast<int*>(gs + M);  // M
   int* perm = flist + M;                        // M
   int* permg = a.perm + static_cast<size_t>(t) * M;
-  __shared__ double redq[kRecB * 32];
-  __shared__ int wcnt[32], woff[32], cjs[kRecB];
+  __shared__ int wcnt[32], woff[32];
   __shared__ int s_nflag;
   __shared__ double red[32];
   __shared__ ArgMax ared[32];
@@ -280,8 +277,18 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
     for (int j = k + 1 + threadIdx.x; j < M; j += blockDim.x) {
       const int cj = perm[j];
       double fw = 0, fv = 0;
-#pragma unroll 8
-      for (int u = 0; u < k; ++u) {
+      int u = 0;
+      for (; u + 8 <= k; u += 8) {  // 8 loads in flight
+        double f[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[q] = F1[static_cast<size_t>(u + q) * M + j];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          fw += f[q] * w[u + q];
+          fv += f[q] * vk[u + q];
+        }
+      }
+      for (; u < k; ++u) {
         const double f = F1[static_cast<size_t>(u) * M + j];
         fw += f * w[u];
         fv += f * vk[u];
@@ -306,8 +313,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
     }
     if (!__syncthreads_or(any_flag)) continue;
     // ---- exact recomputation of flagged norms: ||(A - V F^T)(k+1:M, j)||
-    // compact the flagged columns (increasing j), then a register-blocked pass over rows that
-    // serves 8 columns per V1 read (a small GEMM instead of one warp per column)
+    // compact the flagged columns (increasing j)
     if (threadIdx.x == 0) s_nflag = 0;
     __syncthreads();
     for (int base = k + 1; base < M; base += blockDim.x) {
@@ -329,44 +335,60 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       __syncthreads();
     }
     const int nflag = s_nflag;
-    for (int f0 = 0; f0 < nflag; f0 += kRecB) {
-      const int nb = min(kRecB, nflag - f0);
-      for (int idx = threadIdx.x; idx < kRecB * (k + 1); idx += blockDim.x) {
-        const int q = idx / (k + 1), u = idx % (k + 1);
-        Fs[q * K + u] = q < nb ? F1[static_cast<size_t>(u) * M + flist[f0 + q]] : 0.0;
-      }
-      if (threadIdx.x < kRecB) cjs[threadIdx.x] = threadIdx.x < nb ? perm[flist[f0 + threadIdx.x]] : -1;
-      __syncthreads();
-      double acc[kRecB];
-#pragma unroll
-      for (int q = 0; q < kRecB; ++q) acc[q] = 0.0;
-      for (int i = k + 1 + threadIdx.x; i < Reff; i += blockDim.x) {
-        double e[kRecB];
-#pragma unroll
-        for (int q = 0; q < kRecB; ++q) e[q] = (i <= cjs[q]) ? R0[static_cast<size_t>(cjs[q]) * ld + i] : 0.0;
-#pragma unroll 4
-        for (int u = 0; u <= k; ++u) {
-          const double vv = V1[static_cast<size_t>(u) * M + i];
-#pragma unroll
-          for (int q = 0; q < kRecB; ++q) e[q] -= vv * Fs[q * K + u];
+    // E = R0(k+1:Reff, flagged) - V(k+1:Reff, 0:k] F(flagged, 0:k]^T on DMMA, 8 x 8 tiles
+    // (rows x flagged columns): the warps split the column groups and, when there are fewer
+    // than 16 groups, the row tiles too; per-warp partial squares are combined in a fixed order
+    const int ncg = (nflag + 7) >> 3;
+    const int rg = max(1, min(ncg >= nwarp ? 1 : nwarp / ncg, M / nflag));  // row groups per column group
+    const int nrt = (Reff - (k + 1) + 7) >> 3;
+    for (int wt = warp; wt < ncg * rg; wt += nwarp) {
+      const int g = wt / rg, q = wt % rg;  // column group, row group
+      const int f0 = 8 * g;
+      const int lr = lane >> 2, lc = lane & 3;
+      const int cb = f0 + lr;
+      const int jb = cb < nflag ? flist[cb] : -1;
+      const int c0 = f0 + 2 * lc;
+      const int cjo0 = c0 < nflag ? perm[flist[c0]] : -1, cjo1 = c0 + 1 < nflag ? perm[flist[c0 + 1]] : -1;
+      double sq0 = 0.0, sq1 = 0.0;
+      for (int rt = q; rt < nrt; rt += rg) {
+        const int i0 = k + 1 + 8 * rt;
+        double o0 = 0, o1 = 0;
+        const int ia = i0 + lr;
+        for (int u0 = 0; u0 <= k; u0 += 8) {  // two DMMAs per iteration, loads first
+          const int ua = u0 + lc, ub = u0 + 4 + lc;
+          const double a0 = (ua <= k && ia < Reff) ? V1[static_cast<size_t>(ua) * M + ia] : 0.0;
+          const double b0 = (ua <= k && jb >= 0) ? F1[static_cast<size_t>(ua) * M + jb] : 0.0;
+          const double a1 = (ub <= k && ia < Reff) ? V1[static_cast<size_t>(ub) * M + ia] : 0.0;
+          const double b1 = (ub <= k && jb >= 0) ? F1[static_cast<size_t>(ub) * M + jb] : 0.0;
+          dmma_8x8x4(o0, o1, a0, b0);
+          dmma_8x8x4(o0, o1, a1, b1);
         }
-#pragma unroll
-        for (int q = 0; q < kRecB; ++q) acc[q] += e[q] * e[q];
+        const int i = i0 + lr;
+        if (i < Reff) {
+          const double e0 = (cjo0 >= 0 && i <= cjo0 ? R0[static_cast<size_t>(cjo0) * ld + i] : 0.0) - o0;
+          const double e1 = (cjo1 >= 0 && i <= cjo1 ? R0[static_cast<size_t>(cjo1) * ld + i] : 0.0) - o1;
+          sq0 += e0 * e0;
+          sq1 += e1 * e1;
+        }
       }
-#pragma unroll
-      for (int q = 0; q < kRecB; ++q) {
-        const double sq = warp_sum(acc[q]);
-        if (lane == 0) redq[q * 32 + warp] = sq;
+      sq0 += __shfl_xor_sync(0xffffffffu, sq0, 4);
+      sq0 += __shfl_xor_sync(0xffffffffu, sq0, 8);
+      sq0 += __shfl_xor_sync(0xffffffffu, sq0, 16);
+      sq1 += __shfl_xor_sync(0xffffffffu, sq1, 4);
+      sq1 += __shfl_xor_sync(0xffffffffu, sq1, 8);
+      sq1 += __shfl_xor_sync(0xffffffffu, sq1, 16);
+      if (lr == 0) {  // partial of row group q for columns c0, c0 + 1 (rg * nflag <= M entries)
+        if (c0 < nflag) gs[q * nflag + c0] = sq0;
+        if (c0 + 1 < nflag) gs[q * nflag + c0 + 1] = sq1;
       }
-      __syncthreads();
-      if (threadIdx.x < nb) {
-        double sq = 0;
-        for (int w2 = 0; w2 < nwarp; ++w2) sq += redq[threadIdx.x * 32 + w2];
-        const int j = flist[f0 + threadIdx.x];
-        upd[j] = dir[j] = sqrt(sq);
-      }
-      __syncthreads();
     }
+    __syncthreads();
+    for (int c = threadIdx.x; c < nflag; c += blockDim.x) {
+      double t2 = 0;
+      for (int q = 0; q < rg; ++q) t2 += gs[q * nflag + c];
+      upd[flist[c]] = dir[flist[c]] = sqrt(t2);
+    }
+    __syncthreads();
   }
   __syncthreads();
   for (int j = threadIdx.x; j < M; j += blockDim.x) permg[j] = perm[j];
@@ -727,7 +749,7 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
 }  // namespace
 
 void launch_cod_pivqr(const CodArgs& a, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (4 * a.M + (2 + kRecB) * a.kmax) + sizeof(int) * 2 * a.M;
+  const size_t smem = sizeof(double) * (4 * a.M + 2 * a.kmax) + sizeof(int) * 2 * a.M;
   DDG_CUDA(cudaFuncSetAttribute(cod_pivqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   cod_pivqr_kernel<<<a.nmat, 512, smem, st>>>(a, 0);
