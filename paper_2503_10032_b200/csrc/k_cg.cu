@@ -175,24 +175,24 @@ __host__ __device__ __forceinline__ int rows_per_chunk(int ld) {
 __device__ __forceinline__ ItemGeo item_geo(const CgArgs& a, int kind, int i, int p, bool recon) {
   int j0, j1;
   part_rows(a, p, j0, j1);
-  const ClassDims d = a.dims[a.sub_cls[i]];
+  const SubGeo d = a.geo[i];
   const int R = a.rmax;
-  const int ldf = a.kf_ld[i], ldd = a.kd_ld[i];
-  const double* KF = a.KF + a.kf_off[i] + static_cast<size_t>(j0) * ldf;
-  const double* KD = a.KD + a.kd_off[i] + static_cast<size_t>(j0) * ldd;
+  const int ldf = d.kf_ld, ldd = d.kd_ld;
+  const double* KF = a.KF + d.kf_off + static_cast<size_t>(j0) * ldf;
+  const double* KD = a.KD + d.kd_off + static_cast<size_t>(j0) * ldd;
   ItemGeo g;
   switch (kind) {
     case kOp2:  // A = C, Y = Ypi, B = F
-      g = {KF, ldf, 0, recon ? -1 : R + 4, R, j1 - j0, a.rank[i], recon ? 0 : d.nF, 0, 0, false};
+      g = {KF, ldf, 0, recon ? -1 : R + 4, R, j1 - j0, d.r, recon ? 0 : d.nF, 0, 0, false};
       break;
     case kNn1:  // A = Cbar, B = Cdelta
-      g = {KD, ldd, 0, R, -1, j1 - j0, a.rank[a.N + i], d.nd, 0, 0, false};
+      g = {KD, ldd, 0, R, -1, j1 - j0, d.rb, d.nd, 0, 0, false};
       break;
     case kNn2:  // A = Cdelta, B = Cbar
-      g = {KD, ldd, R, 0, -1, j1 - j0, d.nd, a.rank[a.N + i], 0, 0, true};
+      g = {KD, ldd, R, 0, -1, j1 - j0, d.nd, d.rb, 0, 0, true};
       break;
     default:    // OP3: A = F, B = C
-      g = {KF, ldf, R + 4, 0, -1, j1 - j0, d.nF, a.rank[i], 0, 0, true};
+      g = {KF, ldf, R + 4, 0, -1, j1 - j0, d.nF, d.r, 0, 0, true};
       break;
   }
   g.rpc = rows_per_chunk(g.ld);
@@ -208,6 +208,50 @@ __device__ __forceinline__ bool reverse_kind(int kind) { return kind == kNn2 || 
 /// item k of this CTA in traversal order; reverse phases walk items (and chunks) backwards
 __device__ __forceinline__ int item_work(int k, int nitems, bool reverse) {
   return blockIdx.x + (reverse ? nitems - 1 - k : k) * gridDim.x;
+}
+
+/// Static data of a CTA's first work item of a streamed phase, loaded BEFORE griddepcontrol.wait
+/// (it does not depend on the previous phase): the subdomain geometry, this thread's entry of the
+/// phase's index table and (OP2) the coarse row of its corner. The prologue after the wait is
+/// then one dependent load of fresh data instead of three.
+struct StreamPre {
+  int i;     // subdomain of the first item, -1: none
+  int idx;   // OP3: fluxrow_delta, NN1 / NN2: ndelta_map, of row threadIdx.x (-1 beyond)
+  int crow;  // OP2: Wmu row of corner threadIdx.x (threads < 4), -1 none
+};
+__device__ constexpr StreamPre kNoPre{-1, -1, -1};
+/// the first item's geometry, shared by the CTA (kept out of registers across the wait)
+__device__ __forceinline__ SubGeo& pre_geo() {
+  __shared__ SubGeo g;
+  return g;
+}
+
+__device__ __forceinline__ StreamPre stream_pre(const CgArgs& a, int kind) {
+  StreamPre pre{-1, -1, -1};
+  const int nitems = n_items(a.N * a.P);
+  if (nitems == 0) return pre;
+  const int w = item_work(0, nitems, kind == kNn2 || kind == kOp3);
+  const int i = w / a.P;
+  pre.i = i;
+  if (threadIdx.x == 0) pre_geo() = a.geo[i];
+  const int l = threadIdx.x;
+  if (kind == kOp3) {
+    if (l < a.fmax) pre.idx = a.fluxrow_delta[static_cast<size_t>(i) * a.fmax + l];
+  } else if (kind == kNn1 || kind == kNn2) {
+    if (l < a.dmax) pre.idx = a.ndelta_map[static_cast<size_t>(i) * a.dmax + l];
+    // the Qbar_r^T rows of the prologue (NN1) / epilogue (NN2) GEMV: into L2 ahead of the wait
+    const int E = a.ext;
+    if (l < a.rmax) {
+      const double* row = a.QtX + static_cast<size_t>(a.N + i) * a.rmax * E + static_cast<size_t>(l) * E;
+      const unsigned long long lo = reinterpret_cast<unsigned long long>(row) & ~15ull;
+      const unsigned long long hi = (reinterpret_cast<unsigned long long>(row + 1 + a.dmax) + 15ull) & ~15ull;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(static_cast<unsigned>(hi - lo)) : "memory");
+    }
+  } else if (kind == kOp2 && l < 4 && !a.one_level) {
+    const int g = a.corner_q[i * 4 + l];
+    pre.crow = g >= 0 ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
+  }
+  return pre;
 }
 
 /// Per-CTA timestamps of the streamed-phase trace (DDELM_CG_TRACE, phase-by-phase driver):
@@ -465,6 +509,41 @@ __device__ void rowdot4(const double* Q, int ldq, int nk, int ne, const double* 
   }
 }
 
+/// y[k] = sum_e Q[k*ldq + e] x[e] for k < nk (<= 8 nwarps), e < ne: each warp takes up to 8
+/// consecutive rows and issues all of a batch's loads (8 rows x 6 columns per lane) before its FMAs
+/// — one memory latency per 192 columns instead of one per 32 (latency-bound prologues).
+__device__ void rowdot_wide(const double* Q, int ldq, int nk, int ne, const double* x, double* y, int nwarps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp >= nwarps) return;
+  const int rpw = min(8, (nk + nwarps - 1) / nwarps);
+  const int k0 = warp * rpw;
+  if (k0 >= nk) return;
+  constexpr int kE = 4;
+  double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int e0 = lane; e0 < ne; e0 += 32 * kE) {
+    double q[8][kE];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int t = 0; t < kE; ++t) {
+        const int e = e0 + 32 * t;
+        q[u][t] = (u < rpw && k0 + u < nk && e < ne) ? Q[static_cast<size_t>(k0 + u) * ldq + e] : 0.0;
+      }
+#pragma unroll
+    for (int t = 0; t < kE; ++t) {
+      const int e = e0 + 32 * t;
+      const double xe = e < ne ? x[e] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u] += q[u][t] * xe;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double v = warp_sum(c[u]);
+    if (lane == 0 && u < rpw && k0 + u < nk) y[k0 + u] = v;
+  }
+}
+
 /// y[c] = sum_k Q[k*ldq + c] x[k] for c < nc (<= team size), k < nk: threads over (c, k-group),
 /// the k-groups combined in a fixed order through red (>= team size doubles).
 template <class Out>
@@ -478,6 +557,16 @@ __device__ void coldot_split(const double* Q, int ldq, int nk, int nc, const dou
     const int k0 = (nk * grp) / G, k1 = (nk * (grp + 1)) / G;
     double s1 = 0;
     int k = k0;
+    for (; k + 11 < k1; k += 12) {  // twelve loads in flight
+      double q[12];
+#pragma unroll
+      for (int u = 0; u < 12; ++u) q[u] = Q[static_cast<size_t>(k + u) * ldq + c];
+#pragma unroll
+      for (int u = 0; u < 12; u += 2) {
+        s += q[u] * x[k + u];
+        s1 += q[u + 1] * x[k + u + 1];
+      }
+    }
     for (; k + 3 < k1; k += 4) {  // four loads in flight
       const double q0 = Q[static_cast<size_t>(k) * ldq + c], q1 = Q[static_cast<size_t>(k + 1) * ldq + c];
       const double q2 = Q[static_cast<size_t>(k + 2) * ldq + c], q3 = Q[static_cast<size_t>(k + 3) * ldq + c];
@@ -582,8 +671,8 @@ __device__ void row_tasks(const RowTask* tk, int ntask, int nwarps) {
 /// mode 1: reduced right-hand side (phi = 0, + Q_r^T f); mode 2: reconstruction (phi = +v).
 __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, const double* v, int mode,
                         bool cg, double beta, const double* pcur, double* pnext) {
-  const ClassDims d = a.dims[a.sub_cls[i]];
-  const int r = a.rank[i], R = a.rmax, E = a.ext;
+  const SubGeo d = a.geo[i];
+  const int r = d.r, R = a.rmax, E = a.ext;
   double* vg = sh.v1;
   double* phi = sh.red;  // n_gamma <= kThreads (checked on the host)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -651,7 +740,7 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, 
 
 // ---------------------------------------------------------------- streamed phases (consumers)
 template <int W>
-__device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int mode) {
+__device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int mode, const StreamPre& pre) {
   const int nitems = n_items(a.N * a.P);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ double muc[4];
@@ -660,11 +749,16 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
     const int w = item_work(k, nitems, false);
     const int i = w / a.P, p = w % a.P;
     if (!a.one_level) gather_z(a, sh, mode, kCThreads);
+    const bool first = (k == 0 && pre.i == i);
     if (threadIdx.x < 4) {
-      const int g = a.corner_q[i * 4 + threadIdx.x];
-      crow[threadIdx.x] = (g >= 0 && !a.one_level) ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
+      if (first) {
+        crow[threadIdx.x] = pre.crow;
+      } else {
+        const int g = a.corner_q[i * 4 + threadIdx.x];
+        crow[threadIdx.x] = (g >= 0 && !a.one_level) ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
+      }
     }
-    const int r = a.rank[i];
+    const int r = first ? pre_geo().r : a.geo[i].r;
     for (int kk = threadIdx.x; kk < r; kk += kCThreads) sh.xa[kk] = a.s[static_cast<size_t>(i) * a.rmax + kk];
     cons_sync();
     const int nz = a.n_pi + a.npf;
@@ -719,18 +813,20 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
 }
 
 template <int W>
-__device__ void dev_nn1(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
+__device__ void dev_nn1(const CgArgs& a, const Shared& sh, unsigned& ccnt, const StreamPre& pre) {
   const int nitems = n_items(a.N * a.P);
   for (int k = 0; k < nitems; ++k) {
     const int w = item_work(k, nitems, false);
     const int i = w / a.P, p = w % a.P;
-    const ClassDims d = a.dims[a.sub_cls[i]];
-    const int nd = d.nd, rb = a.rank[a.N + i], E = a.ext;
+    const bool first = (k == 0 && pre.i == i);
+    const SubGeo d = first ? pre_geo() : a.geo[i];
+    const int nd = d.nd, rb = d.rb, E = a.ext;
     const double* QtX = a.QtX + static_cast<size_t>(a.N + i) * a.rmax * E;
     const int* nmap = a.ndelta_map + static_cast<size_t>(i) * a.dmax;
-    for (int kk = threadIdx.x; kk < nd; kk += kCThreads) sh.v1[kk] = -gather_x(a, nmap[kk]);
+    for (int kk = threadIdx.x; kk < nd; kk += kCThreads)
+      sh.v1[kk] = -gather_x(a, (first && kk == threadIdx.x) ? pre.idx : nmap[kk]);
     cons_sync();
-    rowdot4(QtX + 1, E, rb, nd, sh.v1, sh.xa, kCWarps);  // Qbar_r^T rhs (rhs nonzero on flux rows only)
+    rowdot_wide(QtX + 1, E, rb, nd, sh.v1, sh.xa, kCWarps);  // Qbar_r^T rhs (rhs nonzero on flux rows only)
     cons_sync();
     const ItemGeo g = item_geo(a, kNn1, i, p, false);
     double acc[W];
@@ -743,18 +839,19 @@ __device__ void dev_nn1(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
 }
 
 template <int W>
-__device__ void dev_nn2(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
+__device__ void dev_nn2(const CgArgs& a, const Shared& sh, unsigned& ccnt, const StreamPre& pre) {
   const int nitems = n_items(a.N * a.P);
   for (int k = 0; k < nitems; ++k) {
     const int w = item_work(k, nitems, true);
     const int i = w / a.P, p = w % a.P;
-    const ClassDims d = a.dims[a.sub_cls[i]];
-    const int nd = d.nd, rb = a.rank[a.N + i], E = a.ext;
+    const bool first = (k == 0 && pre.i == i);
+    const SubGeo d = first ? pre_geo() : a.geo[i];
+    const int nd = d.nd, rb = d.rb, E = a.ext;
     const double* QtX = a.QtX + static_cast<size_t>(a.N + i) * a.rmax * E;
     const int* nmap = a.ndelta_map + static_cast<size_t>(i) * a.dmax;
     const size_t st = static_cast<size_t>(a.N) * a.dmax;
     for (int kk = threadIdx.x; kk < nd; kk += kCThreads) {
-      const int gg = nmap[kk];
+      const int gg = (first && kk == threadIdx.x) ? pre.idx : nmap[kk];
       sh.xa[kk] = gather_delta(a.trtab, a, gg);
     }
     cons_sync();
@@ -771,25 +868,29 @@ __device__ void dev_nn2(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
 }
 
 template <int W>
-__device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt) {
+__device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt, const StreamPre& pre) {
   const int nitems = n_items(a.N * a.P);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int k = 0; k < nitems; ++k) {
     const int w = item_work(k, nitems, true);
     const int i = w / a.P, p = w % a.P;
-    const ClassDims d = a.dims[a.sub_cls[i]];
-    const int r = a.rank[i], R = a.rmax, E = a.ext;
+    const bool first = (k == 0 && pre.i == i);
+    const SubGeo d = first ? pre_geo() : a.geo[i];
+    const int r = d.r, R = a.rmax, E = a.ext;
     const double* QtX = a.QtX + static_cast<size_t>(i) * R * E;
     const int* fd = a.fluxrow_delta + static_cast<size_t>(i) * a.fmax;
     const double theta = a.theta;
     const size_t st = static_cast<size_t>(a.N) * a.dmax;
     for (int l = threadIdx.x; l < d.nF; l += kCThreads) {
-      const int gg = fd[l];
+      const int gg = (first && l == threadIdx.x) ? pre.idx : fd[l];
       double wv = 0.0;
       if (gg >= 0) {
+        // every load of both gathers in flight before the sums
+        double zz = 0.0;
+        if (a.use_neumann) zz = gather_delta(a.zztab, a, gg);
         const double x = gather_x(a, gg);
         if (a.use_neumann) {
-          const double ptp = -gather_delta(a.zztab, a, gg);
+          const double ptp = -zz;
           wv = theta * ptp;
           if (theta < 1.0) wv += (1.0 - theta) * x;
         } else {
@@ -851,8 +952,8 @@ __device__ __forceinline__ void mark(unsigned long long* tm, int k) {
 
 __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int i, const double* v, int mode,
                           unsigned long long* tm = nullptr) {
-  const ClassDims d = a.dims[a.sub_cls[i]];
-  const int r = a.rank[i], R = a.rmax, E = a.ext, n = a.n_pi, nz = a.n_pi + a.npf;
+  const SubGeo d = a.geo[i];
+  const int r = d.r, R = a.rmax, E = a.ext, n = a.n_pi, nz = a.n_pi + a.npf;
   __shared__ double cq_mu[4], cq_nu[4], d2s[64], w3t[64];
   __shared__ RowTask tasks[8 + 2 * 64];
   if (a.one_level) {
@@ -1014,7 +1115,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
     for (int i = b; i < a.N; i += G) dev_op1(a, sh, qst, i, vin, 2, false, 0.0, nullptr, nullptr);
     prefetch(kOp2, true);
     grid.sync();
-    if (producer) finish_producer(); else dev_op2<W>(a, sh, ccnt, 2);
+    if (producer) finish_producer(); else dev_op2<W>(a, sh, ccnt, 2, kNoPre);
     __syncthreads();
     return;
   }
@@ -1024,21 +1125,21 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
     for (int i = b; i < a.N; i += G) dev_op1(a, sh, qst, i, vin, mode, false, 0.0, nullptr, nullptr);
     prefetch(kOp2, false);
     grid.sync();
-    if (producer) finish_producer(); else dev_op2<W>(a, sh, ccnt, mode);
+    if (producer) finish_producer(); else dev_op2<W>(a, sh, ccnt, mode, kNoPre);
     __syncthreads();
     if (a.use_neumann) {
       prefetch(kNn1, false);
       grid.sync();
-      if (producer) finish_producer(); else dev_nn1<W>(a, sh, ccnt);
+      if (producer) finish_producer(); else dev_nn1<W>(a, sh, ccnt, kNoPre);
       __syncthreads();
       prefetch(kNn2, false);
       grid.sync();
-      if (producer) finish_producer(); else dev_nn2<W>(a, sh, ccnt);
+      if (producer) finish_producer(); else dev_nn2<W>(a, sh, ccnt, kNoPre);
       __syncthreads();
     }
     prefetch(kOp3, false);
     grid.sync();
-    if (producer) finish_producer(); else dev_op3<W>(a, sh, ccnt);
+    if (producer) finish_producer(); else dev_op3<W>(a, sh, ccnt, kNoPre);
     __syncthreads();
     qst.cached = -1;
     grid.sync();
@@ -1072,27 +1173,27 @@ __global__ void __launch_bounds__(kThreads, 1) cg_persistent_kernel(CgArgs a, in
     tr(0);
     grid.sync();
     tr(1);
-    if (producer) finish_producer(); else dev_op2<W>(a, sh, ccnt, 0);
+    if (producer) finish_producer(); else dev_op2<W>(a, sh, ccnt, 0, kNoPre);
     __syncthreads();
     tr(2);
     if (a.use_neumann) {
       prefetch(kNn1, false);
       grid.sync();
       tr(3);
-      if (producer) finish_producer(); else dev_nn1<W>(a, sh, ccnt);
+      if (producer) finish_producer(); else dev_nn1<W>(a, sh, ccnt, kNoPre);
       __syncthreads();
       tr(4);
       prefetch(kNn2, false);
       grid.sync();
       tr(5);
-      if (producer) finish_producer(); else dev_nn2<W>(a, sh, ccnt);
+      if (producer) finish_producer(); else dev_nn2<W>(a, sh, ccnt, kNoPre);
       __syncthreads();
       tr(6);
     }
     prefetch(kOp3, false);
     grid.sync();
     tr(7);
-    if (producer) finish_producer(); else dev_op3<W>(a, sh, ccnt);
+    if (producer) finish_producer(); else dev_op3<W>(a, sh, ccnt, kNoPre);
     __syncthreads();
     tr(8);
     qst.cached = -1;
@@ -1191,22 +1292,27 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
   // previous phase to complete — the in-kernel analogue of prefetching across a grid barrier.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const bool streamed = phase == kPhOp2 || phase == kPhNn1 || phase == kPhNn2 || phase == kPhOp3;
+  StreamPre pre{-1, -1, -1};
   if (streamed) {
     const int kind = phase == kPhOp2 ? kOp2 : phase == kPhNn1 ? kNn1 : phase == kPhNn2 ? kNn2 : kOp3;
     if (producer && lane == 0) {
       producer_begin(a, pr, kind, mode == 2);
       producer_run(a, pr, sh, kStages);
     }
+    if (!producer) pre = stream_pre(a, kind);
   } else if ((phase == kPhOp1 || phase == kPhOp4) && b < a.N) {
     size_t qb;
-    stage_issue(a, sh, qst, b, a.rank[b], &qb);
+    stage_issue(a, sh, qst, b, a.geo[b].r, &qb);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (streamed) __syncthreads();  // pre_geo() written by thread 0 before the wait
   if (a.trace && threadIdx.x == 0) phase_stamps()[1] = gtimer();
-  if (cg) it = a.state[6];  // the iteration counter lives on the device (graph replays)
+  // the streamed phases only write intermediate tables: they need neither the iteration counter
+  // nor the stop flag (XR1 checks it), so their prologue starts with fresh data, not state
+  if (cg && !streamed) it = a.state[6];  // the iteration counter lives on the device (graph replays)
   double* pcur = a.pbuf[(it + 1) & 1];
   double* pnext = a.pbuf[it & 1];
-  if (cg && a.state[1]) {  // converged / aborted earlier: drain the prefetched copies, then leave
+  if (cg && !streamed && a.state[1]) {  // converged / aborted earlier: drain prefetched copies, leave
     if ((phase == kPhXr1 || phase == kPhXr2) && b == 0 && threadIdx.x == 0 && a.cond != 0)
       cudaGraphSetConditional(a.cond, 0);
     __shared__ int s_issued;
@@ -1233,13 +1339,13 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
         if (lane == 0) producer_run(a, pr, sh, -1);  // the first kStages chunks went out before the wait
         __syncwarp();
       } else if (phase == kPhOp2) {
-        dev_op2<W>(a, sh, ccnt, mode);
+        dev_op2<W>(a, sh, ccnt, mode, pre);
       } else if (phase == kPhNn1) {
-        dev_nn1<W>(a, sh, ccnt);
+        dev_nn1<W>(a, sh, ccnt, pre);
       } else if (phase == kPhNn2) {
-        dev_nn2<W>(a, sh, ccnt);
+        dev_nn2<W>(a, sh, ccnt, pre);
       } else {
-        dev_op3<W>(a, sh, ccnt);
+        dev_op3<W>(a, sh, ccnt, pre);
       }
       __syncthreads();
       if (a.trace && threadIdx.x == 0 && phase_stamps()[2] != 0) {

@@ -143,6 +143,12 @@ void launch_lsq_generate(const LsqArgs& a, uint64_t seed, int kind, cudaStream_t
 void launch_lsq_gram(const LsqArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- CG (k_cg.cu)
+/// Per-subdomain geometry of the interface iteration in one 48-byte record (one dependent load
+/// instead of class -> dims, rank, strides, offsets).
+struct SubGeo {
+  int n_gamma, nF, nd, r, rb, kf_ld, kd_ld, pad;
+  long long kf_off, kd_off;
+};
 enum CgJob { kJobCg = 0, kJobApply = 1, kJobRhs = 2, kJobRecon = 3 };
 
 struct CgArgs {
@@ -165,6 +171,7 @@ struct CgArgs {
   const int* rank;         // 2N
   const ClassDims* dims;
   const int* sub_cls;
+  const SubGeo* geo;       // N
   const int* gamma_delta;  // N x gmax
   const int* gamma_pi;     // N x gmax
   const int* fluxrow_delta;  // N x fmax

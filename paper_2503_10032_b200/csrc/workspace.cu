@@ -66,6 +66,7 @@ template struct DevBuf<double>;
 template struct DevBuf<int>;
 template struct DevBuf<Task>;
 template struct DevBuf<ClassDims>;
+template struct DevBuf<SubGeo>;
 template struct DevBuf<long long>;
 
 Workspace::Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex)
@@ -616,6 +617,10 @@ void Workspace::pack_blocks(const BlockArgs& b) {
       ldKF_ = std::max(ldKF_, kfl[i]);
       ldKD_ = std::max(ldKD_, kdl[i]);
     }
+    h_kf_ld_ = kfl;
+    h_kd_ld_ = kdl;
+    h_kf_off_ = kfo;
+    h_kd_off_ = kdo;
     {
       ArenaScope hot(&arena_);
       d_kf_ld.upload(kfl, st_);
@@ -713,6 +718,17 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.rank = d_rank.ptr;
   a.dims = d_dims.ptr;
   a.sub_cls = d_cls.ptr;
+  {
+    std::vector<SubGeo> geo(p.N);
+    for (int i = 0; i < p.N; ++i) {
+      const ClassPlan& c = p.classes[p.subs[i].cls];
+      geo[i] = SubGeo{c.n_gamma, c.nF, c.nd, h_rank[i], h_rank[p.N + i], h_kf_ld_[i], h_kd_ld_[i], 0,
+                      h_kf_off_[i], h_kd_off_[i]};
+    }
+    ArenaScope hot(&arena_);
+    d_geo.upload(geo, st_);
+  }
+  a.geo = d_geo.ptr;
   a.gamma_delta = d_gamma_delta.ptr;
   a.gamma_pi = d_gamma_pi.ptr;
   a.fluxrow_delta = d_fluxrow_delta.ptr;

@@ -166,6 +166,9 @@ class Workspace {
       d_ndelta_map, d_cr_row, d_cr_off, d_cr_l, d_row_owner, d_pi_owner, d_own_gamma, d_own_flux,
       d_own_nd, d_mult_pi, d_gamma_dst, d_flux_dst, d_nd_dst, d_corner_dst, d_cross_dst;
   DevBuf<ClassDims> d_dims;
+  DevBuf<SubGeo> d_geo;
+  std::vector<int> h_kf_ld_, h_kd_ld_;
+  std::vector<long long> h_kf_off_, h_kd_off_;
   DevBuf<double> d_cr_w, d_flip, d_f;
   // layers and matrices
   DevBuf<double> d_w0, d_w1, d_b, d_A, d_tau, d_T, d_ratio, d_F, d_Cd;
