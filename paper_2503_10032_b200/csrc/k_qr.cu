@@ -667,7 +667,10 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
   auto issue = [&](int q) {
     if (q < 2 * nq) {
       const int st = q % kTrStages;
-      const int row = k0 + (q % nq) * RC + 2 * seg;
+      // pass 2 walks the row chunks backwards: its first chunks are the ones pass 1 read last,
+      // still in L2 (the concurrent A tiles far exceed L2, so a forward pass 2 re-reads HBM)
+      const int cq = q < nq ? q : 2 * nq - 1 - q;
+      const int row = k0 + cq * RC + 2 * seg;
       const bool rok = row < static_cast<int>(ld);
 #pragma unroll
       for (int j = 0; j < kSegs; ++j) {
@@ -763,7 +766,7 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
     __syncthreads();
     issue(q + 2);
     const int st = q % kTrStages;
-    const int r0 = k0 + (q - nq) * RC;
+    const int r0 = k0 + (2 * nq - 1 - q) * RC;
     fix_v(st, r0);
     __syncthreads();
     const double* Vs = S.V[st];
