@@ -266,6 +266,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
   return now;
 }
+/// trace of a per-subdomain phase (OP1 / OP4): slots s, s+1 = launch->wait, wait->end (CTAs with work)
+__device__ __forceinline__ void trace_small(const CgArgs& a, int slot) {
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < a.N) {
+    const unsigned long long* t = phase_stamps();
+    double* tr = a.trace + blockIdx.x * 32 + slot;
+    tr[0] += static_cast<double>(t[1] - t[0]);
+    tr[1] += static_cast<double>(gtimer() - t[1]);
+  }
+}
 
 /// Producer (warp 15, lane 0): walks the chunks of this CTA's items of one streamed phase.
 /// `cnt` counts every chunk ever issued by this CTA: stage = cnt % kStages, use = cnt / kStages.
@@ -659,7 +668,15 @@ __device__ void row_tasks(const RowTask* tk, int ntask, int nwarps) {
     double s = 0;
     if (t.row >= 0) {
       const double* w = t.W + static_cast<size_t>(t.row) * t.ld;
-      for (int k = lane; k < t.len; k += 32) s += w[k] * t.vec[k];
+      int k = lane;
+      for (; k + 160 < t.len; k += 192) {  // six loads in flight per lane
+        double wv[6];
+#pragma unroll
+        for (int u = 0; u < 6; ++u) wv[u] = w[k + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 6; ++u) s += wv[u] * t.vec[k + 32 * u];
+      }
+      for (; k < t.len; k += 32) s += w[k] * t.vec[k];
     }
     s = warp_sum(s);
     if (lane == 0) *t.out = s;
@@ -986,6 +1003,18 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
     }
     return block_sum(dot, sh.red);
   }
+  // this thread's output row (gamma point threadIdx.x): index, slot and -phi loaded up front, off the
+  // critical path of the coarse row dots
+  int pdg = -1, pdst = -1, pcr = -1;
+  double pv = 0.0;
+  if (threadIdx.x < d.n_gamma) {
+    pdg = a.gamma_delta[static_cast<size_t>(i) * a.gmax + threadIdx.x];
+    if (pdg >= 0) {
+      pdst = a.gamma_dst[static_cast<size_t>(i) * a.gmax + threadIdx.x];
+      if (mode == 0) pv = v[pdg];
+    }
+  }
+  if (threadIdx.x < a.crmax) pcr = a.cr_row[static_cast<size_t>(i) * a.crmax + threadIdx.x];
   gather_z(a, sh, mode, kThreads);
   const size_t st3 = 4 * static_cast<size_t>(n);
   for (int gp = threadIdx.x; gp < n; gp += kThreads) {
@@ -1021,8 +1050,7 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
   row_tasks(tasks, 8 + 2 * a.crmax, kWarps);
   __syncthreads();
   mark(tm, 2);
-  for (int rho = threadIdx.x; rho < a.crmax; rho += kThreads)
-    d2s[rho] = a.cr_row[static_cast<size_t>(i) * a.crmax + rho] >= 0 ? d2s[rho] - w3t[rho] : 0.0;
+  if (threadIdx.x < a.crmax) d2s[threadIdx.x] = pcr >= 0 ? d2s[threadIdx.x] - w3t[threadIdx.x] : 0.0;
   int gq[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) gq[q] = a.corner_q[i * 4 + q];
@@ -1046,15 +1074,14 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
   coldot_split(QtX + 1, E, r, d.n_gamma, sh.s0, sh.red, Team{kThreads}, [&](int g, double s) { qsv[g] = s; });
   mark(tm, 4);
   double dot = 0;
-  for (int g = threadIdx.x; g < d.n_gamma; g += kThreads) {
-    const int dg = gd[g];
-    if (dg < 0) continue;
+  (void)gd;
+  if (pdg >= 0) {  // n_gamma <= kThreads (cg_check_capacity): one gamma point per thread
+    const int g = threadIdx.x;
     double zs = 0;
     for (int rho = 0; rho < a.crmax; ++rho) zs += Zc[static_cast<size_t>(rho) * a.gmax + g] * d2s[rho];
-    const double mphi = (mode == 0) ? v[dg] : 0.0;  // -phi
-    const double o = mphi + qsv[g] + zs;
-    a.otab_w[a.gamma_dst[static_cast<size_t>(i) * a.gmax + g]] = o;
-    if (mode == 0) dot += v[dg] * o;
+    const double o = pv + qsv[g] + zs;  // -phi + Q_G s_tot + Zc^T d2
+    a.otab_w[pdst] = o;
+    if (mode == 0) dot += pv * o;
   }
   dot = block_sum(dot, sh.red);
   mark(tm, 5);
@@ -1329,6 +1356,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
     case kPhOp1: {
       const double beta = cg ? a.scal[2] : 0.0;
       for (int i = b; i < a.N; i += G) dev_op1(a, sh, qst, i, cg ? nullptr : vin, mode, cg, beta, pcur, pnext);
+      trace_small(a, 0);
       return;
     }
     case kPhOp2:
@@ -1366,6 +1394,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
         const double dot = dev_op4(a, sh, qst, i, cg ? pnext : vin, mode);
         if (cg && threadIdx.x == 0) a.pap_w[a.sub_lo + i] = dot;
       }
+      trace_small(a, 2);
       return;
     case kPhXr1:    // alpha, x / r update, r.r partials (solvers.cpp:96-107); the last CTA to finish
     case kPhXr2: {  // also takes the stopping decision (solvers.cpp:108-116) — one launch per iteration

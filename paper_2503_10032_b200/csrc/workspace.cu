@@ -907,6 +907,17 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
     std::fprintf(stderr, "[cg trace] %d iterations, G=%d, P=%d (us/iteration: max / mean over CTAs)\n",
                  res.iterations, G, a.P);
     if (phased_) {
+      static const char* sm[4] = {"op1 launch->wait", "op1 work", "op4 launch->wait", "op4 work"};
+      for (int k = 0; k < 4; ++k) {
+        double mx = 0, mean = 0;
+        const int nb = std::min(G, plan.N);
+        for (int b = 0; b < nb; ++b) {
+          mx = std::max(mx, t[b * 32 + k]);
+          mean += t[b * 32 + k] / nb;
+        }
+        const double it = std::max(res.iterations, 1);
+        std::fprintf(stderr, "[cg trace] %-20s %8.2f %8.2f\n", sm[k], mx / it / 1e3, mean / it / 1e3);
+      }
       static const char* ph[4] = {"op2", "nn1", "nn2", "op3"};
       static const char* part[4] = {"prologue", "1st chunk wait", "streaming", "epilogue"};
       for (int q = 0; q < 4; ++q)
