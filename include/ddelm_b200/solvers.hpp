@@ -32,16 +32,26 @@ namespace ddelm {
 
 enum class FluxVariant { Pointwise, MeanEdge };  // assembly.hpp FluxVariant
 
+struct ProblemParams {  // problems.hpp:64-68
+  double alpha = 32.0;
+  std::uint64_t forcing_seed = 2;
+  std::uint64_t rho_seed = 3;
+};
+
 struct ProblemSpec {
   std::string name;
   int id = DDELM_POISSON_SINPI;
+  ProblemParams params;
 };
 
-/// make_problem (problems.cpp:132-188): the Poisson problems of the device path.
-inline ProblemSpec make_problem(const std::string& name) {
-  if (name == "poisson_sinpi") return {name, DDELM_POISSON_SINPI};
-  if (name == "poisson_sin2pi_exp") return {name, DDELM_POISSON_SIN2PI_EXP};
-  if (name == "poisson_sin2pi_cos3pi_x2y") return {name, DDELM_POISSON_SIN2PI_COS3PI_X2Y};
+/// make_problem (problems.cpp:132-188): the Poisson-kind problems of the device path.
+inline ProblemSpec make_problem(const std::string& name, const ProblemParams& params = {}) {
+  if (!(params.alpha > 0)) throw std::invalid_argument("sample_grf: alpha must be positive");
+  if (name == "poisson_sinpi") return {name, DDELM_POISSON_SINPI, params};
+  if (name == "poisson_sin2pi_exp") return {name, DDELM_POISSON_SIN2PI_EXP, params};
+  if (name == "poisson_sin2pi_cos3pi_x2y") return {name, DDELM_POISSON_SIN2PI_COS3PI_X2Y, params};
+  if (name == "poisson_grf") return {name, DDELM_POISSON_GRF, params};
+  if (name == "varcoef_poisson") return {name, DDELM_VARCOEF_POISSON, params};
   throw std::invalid_argument("make_problem: unknown problem '" + name + "'");
 }
 
@@ -102,6 +112,9 @@ class Workspace {
     d.rank_tol = opts.rank_tol;
     d.device = opts.device;
     d.debug_flip_flux_row = opts.debug_flip_flux_row;
+    d.alpha = problem.params.alpha;
+    d.forcing_seed = problem.params.forcing_seed;
+    d.rho_seed = problem.params.rho_seed;
     ddelm_ws* w = nullptr;
     detail::check(ddelm_gpu_create(&d, &w));
     ws_.reset(w);

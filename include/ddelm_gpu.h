@@ -46,7 +46,9 @@ enum {
 enum {
   DDELM_POISSON_SINPI = 0,
   DDELM_POISSON_SIN2PI_EXP = 1,
-  DDELM_POISSON_SIN2PI_COS3PI_X2Y = 2
+  DDELM_POISSON_SIN2PI_COS3PI_X2Y = 2,
+  DDELM_POISSON_GRF = 3,      /* -lap u = GRF(forcing_seed), u = 0 on the boundary */
+  DDELM_VARCOEF_POISSON = 4   /* -div(rho grad u) = 1, rho = tanh(GRF(rho_seed)) + 1.1 */
 };
 
 enum { DDELM_METHOD_DDELM = 0, DDELM_METHOD_CS = 1, DDELM_METHOD_NN = 2 };
@@ -64,6 +66,9 @@ typedef struct ddelm_desc {
   double rank_tol;          /* SolverOptions::rank_tol, 1e-10 */
   int device;               /* CUDA device ordinal */
   int debug_flip_flux_row;  /* validation hook (solvers.hpp:54-57); -1 = off */
+  double alpha;             /* ProblemParams (problems.hpp:64-68): GRF smoothness, default 32 */
+  uint64_t forcing_seed;    /* GRF forcing seed (poisson_grf), default 2 */
+  uint64_t rho_seed;        /* GRF coefficient seed (varcoef_poisson), default 3 */
 } ddelm_desc;
 
 typedef struct ddelm_report {

@@ -26,6 +26,8 @@ struct ddo_config {
   int workers, cg_workers;
   int debug_flip_flux_row;
   int layers_only;  // 1: partition + seeded layers only (field evaluation of given coefficients)
+  double alpha;     // ProblemParams (problems.hpp:64-68): GRF smoothness and seeds
+  unsigned long long forcing_seed, rho_seed;
 };
 
 struct ddo_handle {
@@ -53,7 +55,11 @@ void* ddo_create(const ddo_config* c, char* err, int errlen) {
     o.debug_flip_flux_row = c->debug_flip_flux_row;
     o.layers_only = c->layers_only != 0;
     const auto t0 = std::chrono::steady_clock::now();
-    h->ws = std::make_unique<Workspace>(make_problem(c->problem), c->s, c->n_grid, c->M, c->l,
+    ProblemParams pp;
+    pp.alpha = c->alpha;
+    pp.forcing_seed = c->forcing_seed;
+    pp.rho_seed = c->rho_seed;
+    h->ws = std::make_unique<Workspace>(make_problem(c->problem, pp), c->s, c->n_grid, c->M, c->l,
                                         c->seed, o);
     h->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return h;

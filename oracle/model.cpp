@@ -211,6 +211,27 @@ uint64_t perturb_seed() {
   }();
   return s;
 }
+// DDO_PERTURB_MODE=tanh: perturb the tanh value itself and derive the sigma derivatives from it,
+// the faithful model of a 1-ulp tanh difference (near saturation 1 - s^2 magnifies it, which the
+// variable-coefficient rows expose through grad rho); default: 1 ulp of every final entry
+bool perturb_tanh() {
+  static const bool t = [] {
+    const char* e = std::getenv("DDO_PERTURB_MODE");
+    return e && std::strncmp(e, "tanh", 4) == 0;
+  }();
+  return t;
+}
+// DDO_PERTURB_MODE=tanh_up / tanh_down: every tanh value moved by +1 / -1 ulp (the extreme
+// cases of a systematic 1-ulp bias)
+int perturb_tanh_sign() {
+  static const int t = [] {
+    const char* e = std::getenv("DDO_PERTURB_MODE");
+    if (e && std::strcmp(e, "tanh_up") == 0) return 1;
+    if (e && std::strcmp(e, "tanh_down") == 0) return -1;
+    return 0;
+  }();
+  return t;
+}
 double perturb(double v, uint64_t seed, int j, const Point& p, int order) {
   uint64_t h = seed * 0x9E3779B97F4A7C15ull ^ (static_cast<uint64_t>(j) << 20) ^ static_cast<uint64_t>(order);
   uint64_t xb, yb;
@@ -241,7 +262,10 @@ Mat eval_derivative_matrix(const FeatureLayer& L, const std::vector<Point>& pts,
     for (int a = 0; a < dy; ++a) wfac *= w1;
     for (int k = 0; k < np; ++k) {
       const double z = w0 * pts[k].x + w1 * pts[k].y + L.b[j];
-      const double s0 = std::tanh(z);
+      double s0 = std::tanh(z);
+      if (perturb_seed() && perturb_tanh())
+        s0 = perturb_tanh_sign() ? std::nextafter(s0, perturb_tanh_sign() > 0 ? 2.0 : -2.0)
+                                 : perturb(s0, perturb_seed(), j, pts[k], 0);
       double v = s0;
       if (order > 0) {
         const double s1 = 1.0 - s0 * s0;
@@ -256,7 +280,7 @@ Mat eval_derivative_matrix(const FeatureLayer& L, const std::vector<Point>& pts,
         }
         v *= wfac;
       }
-      out(k, j) = perturb_seed() ? perturb(v, perturb_seed(), j, pts[k], order * 8 + dx) : v;
+      out(k, j) = (perturb_seed() && !perturb_tanh()) ? perturb(v, perturb_seed(), j, pts[k], order * 8 + dx) : v;
     }
   }
   return out;
@@ -273,11 +297,72 @@ Mat add(const Mat& A, const Mat& B, double sa, double sb) {
 }
 }  // namespace
 
+GrfField sample_grf(double alpha, uint64_t seed) {  // problems.cpp:15-39 (draw order amp, w0, w1, phase)
+  if (alpha <= 0) throw std::invalid_argument("sample_grf: alpha must be positive");
+  constexpr int kTerms = 256;
+  GrfField g;
+  g.alpha = alpha;
+  g.seed = seed;
+  g.amp.resize(kTerms);
+  g.fx.resize(kTerms);
+  g.fy.resize(kTerms);
+  g.phase.resize(kTerms);
+  std::mt19937_64 gen(seed);
+  std::normal_distribution<double> na(0.0, alpha * alpha / 16.0);
+  std::normal_distribution<double> nw(0.0, alpha);
+  std::uniform_real_distribution<double> ub(0.0, 2.0 * kPi);
+  for (int i = 0; i < kTerms; ++i) {
+    g.amp[i] = na(gen);
+    g.fx[i] = nw(gen);
+    g.fy[i] = nw(gen);
+    double b;
+    do {
+      b = ub(gen);
+    } while (b <= 0.0);
+    g.phase[i] = b;
+  }
+  return g;
+}
+
+double eval_grf(const GrfField& g, const Point& x) {  // problems.cpp:41-46
+  double v = 0.0;
+  for (size_t i = 0; i < g.amp.size(); ++i) v += g.amp[i] * std::sin(g.fx[i] * x.x + g.fy[i] * x.y + g.phase[i]);
+  return v;
+}
+
+Point grad_grf(const GrfField& g, const Point& x) {  // problems.cpp:48-57
+  Point d{0.0, 0.0};
+  for (size_t i = 0; i < g.amp.size(); ++i) {
+    const double c = g.amp[i] * std::cos(g.fx[i] * x.x + g.fy[i] * x.y + g.phase[i]);
+    d.x += c * g.fx[i];
+    d.y += c * g.fy[i];
+  }
+  return d;
+}
+
+double eval_rho(const GrfField& g, const Point& x) { return std::tanh(eval_grf(g, x)) + 1.1; }
+
+Point grad_rho(const GrfField& g, const Point& x) {  // problems.cpp:63-66
+  const double t = std::tanh(eval_grf(g, x));
+  const Point d = grad_grf(g, x);
+  return Point{(1.0 - t * t) * d.x, (1.0 - t * t) * d.y};
+}
+
 Mat ProblemSpec::interior_rows(const FeatureLayer& L, const std::vector<Point>& pts) const {
-  // problems.cpp:71-73: -(D20 + D02)
   const Mat a = eval_derivative_matrix(L, pts, 2, 0), b = eval_derivative_matrix(L, pts, 0, 2);
   Mat C(a.r, a.c);
-  for (size_t t = 0; t < a.a.size(); ++t) C.a[t] = -(a.a[t] + b.a[t]);
+  if (kind == 0) {
+    // problems.cpp:71-73: -(D20 + D02)
+    for (size_t t = 0; t < a.a.size(); ++t) C.a[t] = -(a.a[t] + b.a[t]);
+    return C;
+  }
+  // problems.cpp:74-87: -rho lap(u) - grad(rho) . grad(u), row by row
+  const Mat gx = eval_derivative_matrix(L, pts, 1, 0), gy = eval_derivative_matrix(L, pts, 0, 1);
+  for (int k = 0; k < a.r; ++k) {
+    const double r = eval_rho(*rho, pts[k]);
+    const Point gr = grad_rho(*rho, pts[k]);
+    for (int j = 0; j < a.c; ++j) C(k, j) = -r * (a(k, j) + b(k, j)) - gr.x * gx(k, j) - gr.y * gy(k, j);
+  }
   return C;
 }
 
@@ -292,12 +377,31 @@ Mat ProblemSpec::trace_rows(const FeatureLayer& L, const std::vector<Point>& pts
 Mat ProblemSpec::flux_rows(const FeatureLayer& L, const std::vector<Point>& pts,
                            const Point& n) const {
   // problems.cpp:113-121: n_x D10 + n_y D01 (Eigen evaluates nx*A + ny*B elementwise)
-  return add(eval_derivative_matrix(L, pts, 1, 0), eval_derivative_matrix(L, pts, 0, 1), n.x, n.y);
+  Mat rows = add(eval_derivative_matrix(L, pts, 1, 0), eval_derivative_matrix(L, pts, 0, 1), n.x, n.y);
+  if (kind == 1)  // conormal flux rho du/dn (problems.cpp:117-121)
+    for (int k = 0; k < rows.r; ++k) {
+      const double r = eval_rho(*rho, pts[k]);
+      for (int j = 0; j < rows.c; ++j) rows(k, j) *= r;
+    }
+  return rows;
 }
 
-ProblemSpec make_problem(const std::string& name) {  // problems.cpp:132-188
+ProblemSpec make_problem(const std::string& name, const ProblemParams& params) {  // problems.cpp:132-188
   ProblemSpec p;
   p.name = name;
+  if (name == "poisson_grf") {  // problems.cpp:157-161
+    auto f = std::make_shared<GrfField>(sample_grf(params.alpha, params.forcing_seed));
+    p.forcing = [f](const Point& x) { return eval_grf(*f, x); };
+    p.boundary = [](const Point&) { return 0.0; };
+    return p;
+  }
+  if (name == "varcoef_poisson") {  // problems.cpp:162-166
+    p.kind = 1;
+    p.rho = std::make_shared<GrfField>(sample_grf(params.alpha, params.rho_seed));
+    p.forcing = [](const Point&) { return 1.0; };
+    p.boundary = [](const Point&) { return 0.0; };
+    return p;
+  }
   if (name == "poisson_sinpi") {
     p.exact = [](const Point& x) { return std::sin(kPi * x.x) * std::sin(kPi * x.y); };
     p.exact_grad = [](const Point& x) {

@@ -31,6 +31,7 @@
 #include <array>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -149,13 +150,34 @@ Mat eval_derivative_matrix(const FeatureLayer& L, const std::vector<Point>& pts,
 using ScalarFn = std::function<double(const Point&)>;
 using GradFn = std::function<Point(const Point&)>;
 
-/// Poisson-kind problems only (biharmonic / variable-coefficient / GRF are out of scope,
-/// SURVEY.md §2). C4's manufactured solution is added as "poisson_sin2pi_cos3pi_x2y".
+/// Gaussian random field sum_i amp_i sin(w_i . x + phase_i), 256 terms (problems.cpp:15-58).
+struct GrfField {
+  std::vector<double> amp, fx, fy, phase;
+  double alpha = 0;
+  uint64_t seed = 0;
+};
+GrfField sample_grf(double alpha, uint64_t seed);
+double eval_grf(const GrfField& g, const Point& x);
+Point grad_grf(const GrfField& g, const Point& x);
+double eval_rho(const GrfField& g, const Point& x);   // tanh(grf) + 1.1
+Point grad_rho(const GrfField& g, const Point& x);
+
+struct ProblemParams {  // problems.hpp:64-68
+  double alpha = 32.0;
+  uint64_t forcing_seed = 2;
+  uint64_t rho_seed = 3;
+};
+
+/// Poisson-kind problems (cc = bc = 1): poisson_sinpi, poisson_sin2pi_exp, poisson_grf (GRF
+/// forcing), varcoef_poisson (-div(rho grad u) = 1, rho = tanh(GRF) + 1.1, conormal flux), and
+/// C4's manufactured "poisson_sin2pi_cos3pi_x2y". Biharmonic (cc = bc = 2) is out of scope.
 struct ProblemSpec {
   std::string name;
+  int kind = 0;  // 0 Poisson, 1 variable-coefficient Poisson (problems.hpp ProblemKind)
   int components = 1, boundary_components = 1;
   ScalarFn forcing, boundary, exact;
   GradFn exact_grad;
+  std::shared_ptr<GrfField> rho;  // varcoef_poisson
   double default_l = 32;
   bool has_exact() const { return static_cast<bool>(exact); }
   Mat interior_rows(const FeatureLayer& L, const std::vector<Point>& pts) const;
@@ -164,7 +186,7 @@ struct ProblemSpec {
   Mat flux_rows(const FeatureLayer& L, const std::vector<Point>& pts, const Point& n) const;
 };
 
-ProblemSpec make_problem(const std::string& name);
+ProblemSpec make_problem(const std::string& name, const ProblemParams& params = {});
 
 // ------------------------------------------------------------------ assembly (assembly.hpp)
 struct LocalBlocks {

@@ -34,6 +34,8 @@ class _Config(C.Structure):
         ("workers", C.c_int), ("cg_workers", C.c_int),
         ("debug_flip_flux_row", C.c_int),
         ("layers_only", C.c_int),
+        ("alpha", C.c_double),
+        ("forcing_seed", C.c_ulonglong), ("rho_seed", C.c_ulonglong),
     ]
 
 
@@ -88,13 +90,14 @@ class OracleWorkspace:
 
     def __init__(self, problem="poisson_sinpi", s=2, n_grid=10, M=64, l=8.0, seed=1,
                  flux_variant="mean_edge", trace_basis="change_of_variables", workers=1,
-                 cg_workers=1, debug_flip_flux_row=-1, layers_only=False):
+                 cg_workers=1, debug_flip_flux_row=-1, layers_only=False, alpha=32.0, forcing_seed=2,
+                 rho_seed=3):
         L = lib()
         self._cfg = _Config(problem.encode(), s, n_grid, M, float(l), seed, 2, 0.999,
                             1 if flux_variant == "mean_edge" else 0,
                             1 if trace_basis == "change_of_variables" else 0,
                             1e-9, 0, 0, workers, cg_workers, debug_flip_flux_row,
-                            1 if layers_only else 0)
+                            1 if layers_only else 0, float(alpha), forcing_seed, rho_seed)
         err = C.create_string_buffer(512)
         self.h = L.ddo_create(C.byref(self._cfg), err, 512)
         if not self.h:

@@ -704,8 +704,74 @@ void test_solvers() {  // test_solvers.cpp:107-217 and acceptance criteria 1, 2,
 
 }  // namespace
 
+void test_problems_grf() {  // test_problems.cpp: GRF sampler, rho, variable-coefficient rows
+  const GrfField a = sample_grf(32, 5), b = sample_grf(32, 5), c = sample_grf(32, 6);
+  CHECK(a.amp == b.amp && a.fx == b.fx && a.fy == b.fy && a.phase == b.phase);
+  CHECK(a.amp != c.amp);
+  bool in_range = true;
+  for (double ph : a.phase) in_range = in_range && ph > 0.0 && ph < 2 * std::numbers::pi;
+  CHECK(in_range);
+  std::mt19937_64 gen(1);
+  std::uniform_real_distribution<double> u(0, 1);
+  const GrfField g = sample_grf(16, 9);
+  bool sum_ok = true, fd_ok = true, rho_ok = true;
+  for (int k = 0; k < 20; ++k) {
+    const Point x{u(gen), u(gen)};
+    long double acc = 0;
+    for (size_t j = 0; j < g.amp.size(); ++j)
+      acc += static_cast<long double>(g.amp[j]) * sinl(g.fx[j] * x.x + g.fy[j] * x.y + g.phase[j]);
+    sum_ok = sum_ok && std::abs(eval_grf(g, x) - static_cast<double>(acc)) <= 1e-12 * std::max(1.0L, fabsl(acc));
+    const double h = 1e-6;
+    const Point gr = grad_grf(g, x);
+    const double gx = (eval_grf(g, {x.x + h, x.y}) - eval_grf(g, {x.x - h, x.y})) / (2 * h);
+    const double gy = (eval_grf(g, {x.x, x.y + h}) - eval_grf(g, {x.x, x.y - h})) / (2 * h);
+    fd_ok = fd_ok && std::abs(gr.x - gx) < 1e-5 * std::max(1.0, std::abs(gx)) &&
+            std::abs(gr.y - gy) < 1e-5 * std::max(1.0, std::abs(gy));
+    const double r = eval_rho(g, x), t = std::tanh(eval_grf(g, x));
+    const Point dr = grad_rho(g, x);
+    rho_ok = rho_ok && r >= 0.1 && r <= 2.1 && std::abs(r - (t + 1.1)) <= 1e-14 * r &&
+             std::abs(dr.x - (1 - t * t) * gr.x) <= 1e-12 * std::max(1.0, std::abs(dr.x)) &&
+             std::abs(dr.y - (1 - t * t) * gr.y) <= 1e-12 * std::max(1.0, std::abs(dr.y));
+  }
+  CHECK(sum_ok);
+  CHECK(fd_ok);
+  CHECK(rho_ok);
+  // -div(rho grad phi) = -rho lap(phi) - grad(rho) . grad(phi); conormal flux rho dphi/dn
+  ProblemParams pp;
+  pp.alpha = 8;
+  const ProblemSpec vp = make_problem("varcoef_poisson", pp);
+  CHECK(vp.kind == 1 && vp.rho != nullptr && !vp.has_exact());
+  Box box{0.0, 0.0, 0.5, 0.5};
+  const FeatureLayer L = init_layer(6, box, 3, box.diam() / 2, 12);
+  const std::vector<Point> pts{{0.2, 0.3}, {0.4, 0.1}, {0.25, 0.25}};
+  const Mat rows = vp.interior_rows(L, pts), fr = vp.flux_rows(L, pts, Point{1, 0});
+  const Mat d20 = eval_derivative_matrix(L, pts, 2, 0), d02 = eval_derivative_matrix(L, pts, 0, 2);
+  const Mat d10 = eval_derivative_matrix(L, pts, 1, 0), d01 = eval_derivative_matrix(L, pts, 0, 1);
+  bool rows_ok = true;
+  for (int k = 0; k < 3; ++k) {
+    const double r = eval_rho(*vp.rho, pts[k]);
+    const Point dr = grad_rho(*vp.rho, pts[k]);
+    double mx = 0, err = 0, fmx = 0, ferr = 0;
+    for (int j = 0; j < L.M; ++j) {
+      const double e = -r * (d20(k, j) + d02(k, j)) - dr.x * d10(k, j) - dr.y * d01(k, j);
+      mx = std::max(mx, std::abs(e));
+      err = std::max(err, std::abs(rows(k, j) - e));
+      fmx = std::max(fmx, std::abs(fr(k, j)));
+      ferr = std::max(ferr, std::abs(fr(k, j) - r * d10(k, j)));
+    }
+    rows_ok = rows_ok && err <= 1e-12 * mx && ferr <= 1e-12 * fmx;
+  }
+  CHECK(rows_ok);
+  const ProblemSpec gp = make_problem("poisson_grf", pp);
+  CHECK(gp.kind == 0 && !gp.has_exact() && gp.boundary(Point{0.3, 0.0}) == 0.0);
+  const GrfField gf = sample_grf(8, 2);
+  CHECK(gp.forcing(Point{0.3, 0.7}) == eval_grf(gf, Point{0.3, 0.7}));
+  CHECK_THROWS(make_problem("heat_equation"));
+}
+
 int main() {
   test_features();
+  test_problems_grf();
   test_geometry();
   test_assembly();
   test_lsfactor();

@@ -24,7 +24,8 @@ from .configs import CONFIGS  # noqa: F401
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libddelm_gpu.so")
 
-PROBLEMS = {"poisson_sinpi": 0, "poisson_sin2pi_exp": 1, "poisson_sin2pi_cos3pi_x2y": 2}
+PROBLEMS = {"poisson_sinpi": 0, "poisson_sin2pi_exp": 1, "poisson_sin2pi_cos3pi_x2y": 2,
+            "poisson_grf": 3, "varcoef_poisson": 4}
 METHODS = {"ddelm": 0, "ddelm-cs": 1, "ddelm-nn": 2}
 
 DDELM_OK, DDELM_ERR_INVALID_ARGUMENT, DDELM_ERR_RUNTIME, DDELM_ERR_CUDA, DDELM_ERR_CAPACITY = range(5)
@@ -48,7 +49,8 @@ class _Desc(C.Structure):
     _fields_ = [("problem", C.c_int), ("s", C.c_int), ("n_grid", C.c_int), ("M", C.c_int),
                 ("l", C.c_double), ("seed", C.c_uint64), ("flux_variant", C.c_int),
                 ("change_of_variables", C.c_int), ("rank_tol", C.c_double), ("device", C.c_int),
-                ("debug_flip_flux_row", C.c_int)]
+                ("debug_flip_flux_row", C.c_int), ("alpha", C.c_double),
+                ("forcing_seed", C.c_uint64), ("rho_seed", C.c_uint64)]
 
 
 class _Report(C.Structure):
@@ -132,17 +134,28 @@ def _ptr(a: np.ndarray):
 
 
 @dataclass
+class ProblemParams:
+    """ProblemParams (problems.hpp:64-68): GRF smoothness and seeds."""
+    alpha: float = 32.0
+    forcing_seed: int = 2
+    rho_seed: int = 3
+
+
+@dataclass
 class ProblemSpec:
-    """make_problem (problems.cpp:132-188) — Poisson problems on the device path."""
+    """make_problem (problems.cpp:132-188) — the Poisson-kind problems on the device path."""
     name: str
+    params: ProblemParams = field(default_factory=ProblemParams)
 
     def __post_init__(self):
         if self.name not in PROBLEMS:
             raise ValueError(f"make_problem: unknown problem '{self.name}'")
+        if not self.params.alpha > 0:
+            raise ValueError("sample_grf: alpha must be positive")
 
 
-def make_problem(name: str) -> ProblemSpec:
-    return ProblemSpec(name)
+def make_problem(name: str, params: ProblemParams | None = None) -> ProblemSpec:
+    return ProblemSpec(name, params or ProblemParams())
 
 
 @dataclass
@@ -195,7 +208,8 @@ def plan_tables(cfg, rank: int, world: int) -> dict:
     L = load_library()
     d = _Desc(PROBLEMS[cfg["problem"]], cfg["s"], cfg["n_grid"], cfg["M"], float(cfg["l"]), cfg["seed"],
               1 if cfg["flux_variant"] == "mean_edge" else 0,
-              1 if cfg["trace_basis"] == "change_of_variables" else 0, 1e-10, 0, -1)
+              1 if cfg["trace_basis"] == "change_of_variables" else 0, 1e-10, 0, -1,
+              float(cfg.get("alpha", 32.0)), int(cfg.get("forcing_seed", 2)), int(cfg.get("rho_seed", 3)))
     out = {}
     for which, name in enumerate(["gamma_dst", "flux_dst", "nd_dst", "corner_dst", "cross_dst", "meta"]):
         n = L.ddelm_gpu_plan_tables(C.byref(d), rank, world, which, None, 0)
@@ -229,9 +243,11 @@ class Workspace:
         opts = opts or SolverOptions()
         if opts.flux_variant not in ("pointwise", "mean_edge"):
             raise ValueError("flux_variant must be pointwise or mean_edge")
+        pp = problem.params
         d = _Desc(PROBLEMS[problem.name], s, n_grid, M, float(l), seed,
                   1 if opts.flux_variant == "mean_edge" else 0, 1 if opts.change_of_variables else 0,
-                  float(opts.rank_tol), device, int(opts.debug_flip_flux_row))
+                  float(opts.rank_tol), device, int(opts.debug_flip_flux_row), float(pp.alpha),
+                  int(pp.forcing_seed), int(pp.rho_seed))
         h = C.c_void_p()
         if shard is None:
             _check(L.ddelm_gpu_create(C.byref(d), C.byref(h)))
@@ -436,7 +452,9 @@ def workspace_from_config(name_or_cfg, device: int = 0, shard: tuple | None = No
     cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
     opts = SolverOptions(flux_variant=cfg["flux_variant"],
                          change_of_variables=cfg["trace_basis"] == "change_of_variables")
-    return Workspace(cfg["problem"], cfg["s"], cfg["n_grid"], cfg["M"], cfg["l"], cfg["seed"], opts, device,
+    problem = make_problem(cfg["problem"], ProblemParams(cfg.get("alpha", 32.0), cfg.get("forcing_seed", 2),
+                                                         cfg.get("rho_seed", 3)))
+    return Workspace(problem, cfg["s"], cfg["n_grid"], cfg["M"], cfg["l"], cfg["seed"], opts, device,
                      shard)
 
 

@@ -37,4 +37,11 @@ CONFIGS = {
                 trace_basis="nodal"),
     "C2d": dict(_BASE, s=4, M=400, l=2.0, n_grid=32, method="ddelm", flux_variant="pointwise",
                 trace_basis="nodal"),
+    # the reference's other Poisson-kind problems (problems.cpp:157-166):
+    # GRF forcing (alpha 32, forcing_seed 2) and the variable coefficient rho = tanh(GRF) + 1.1
+    # (rho_seed 3) with conormal flux rows; no exact solution
+    "T2g": dict(_BASE, problem="poisson_grf", s=4, M=64, l=10.0, n_grid=12),
+    "T2v": dict(_BASE, problem="varcoef_poisson", s=4, M=64, l=10.0, n_grid=12),
+    "T4v": dict(_BASE, problem="varcoef_poisson", s=3, M=100, l=20.0, n_grid=16),
+    "C2g": dict(_BASE, problem="poisson_grf", s=4, M=400, l=2.0, n_grid=32),
 }

@@ -46,6 +46,14 @@ namespace {
 
 thread_local std::string g_err;
 
+ddg::ProblemParams desc_params(const ddelm_desc* d) {
+  ddg::ProblemParams pp;
+  pp.alpha = d->alpha;
+  pp.forcing_seed = d->forcing_seed;
+  pp.rho_seed = d->rho_seed;
+  return pp;
+}
+
 template <typename F>
 int guarded(F&& f) {
   try {
@@ -84,7 +92,7 @@ int ddelm_gpu_create(const ddelm_desc* d, ddelm_ws** out) {
     if (d->device < 0 || d->device >= ndev) throw std::invalid_argument("ddelm_gpu_create: bad device ordinal");
     ddg::Plan p = ddg::build_plan(d->problem, d->s, d->n_grid, d->M, d->l, d->seed, d->flux_variant,
                                   d->change_of_variables != 0, d->rank_tol > 0 ? d->rank_tol : 1e-10,
-                                  d->debug_flip_flux_row);
+                                  d->debug_flip_flux_row, desc_params(d));
     auto* h = new ddelm_ws;
     try {
       h->w = new ddg::Workspace(ddg::shard_plan(p, 0, p.N), d->device);
@@ -114,7 +122,7 @@ int ddelm_gpu_create_sharded(const ddelm_desc* d, int rank, int world, const uns
     if (d->device < 0 || d->device >= ndev) throw std::invalid_argument("ddelm_gpu_create_sharded: bad device ordinal");
     ddg::Plan g = ddg::build_plan(d->problem, d->s, d->n_grid, d->M, d->l, d->seed, d->flux_variant,
                                   d->change_of_variables != 0, d->rank_tol > 0 ? d->rank_tol : 1e-10,
-                                  d->debug_flip_flux_row);
+                                  d->debug_flip_flux_row, desc_params(d));
     if (world > g.N) throw std::invalid_argument("ddelm_gpu_create_sharded: more ranks than subdomains");
     int lo = 0, hi = 0;
     ddg::shard_range(g.N, rank, world, &lo, &hi);
@@ -138,7 +146,7 @@ int ddelm_gpu_plan_tables(const ddelm_desc* d, int rank, int world, int which, i
       throw std::invalid_argument("ddelm_gpu_plan_tables: bad argument");
     ddg::Plan g = ddg::build_plan(d->problem, d->s, d->n_grid, d->M, d->l, d->seed, d->flux_variant,
                                   d->change_of_variables != 0, d->rank_tol > 0 ? d->rank_tol : 1e-10,
-                                  d->debug_flip_flux_row);
+                                  d->debug_flip_flux_row, desc_params(d));
     int lo = 0, hi = 0;
     ddg::shard_range(g.N, rank, world, &lo, &hi);
     const ddg::Plan p = ddg::shard_plan(g, lo, hi);

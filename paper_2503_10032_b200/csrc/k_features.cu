@@ -55,8 +55,17 @@ __global__ void __launch_bounds__(256) build_features_kernel(FeatureArgs p) {
   const double inv_n1 = 1.0 / (n - 1);
   (void)inv_n1;
 
+  const double* coef = p.coef ? p.coef + static_cast<size_t>(i) * p.tmax * 3 : nullptr;
   for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
     const Task tk = tasks[t];
+    // varcoef_poisson (problems.cpp:74-87, 117-121): rho and grad rho at this row's point
+    double rho = 1.0, rhox = 0.0, rhoy = 0.0;
+    const bool var = coef != nullptr && (tk.kind == kLap || tk.kind == kFlux);
+    if (var) {
+      rho = coef[t * 3];
+      rhox = coef[t * 3 + 1];
+      rhoy = coef[t * 3 + 2];
+    }
     const double x = coord(gx0, tk.a, S), y = coord(gy0, tk.b, S);
     const int dst = tk.dst & 0x0f;
     const bool dual = (tk.dst & kDual) != 0;
@@ -100,10 +109,16 @@ __global__ void __launch_bounds__(256) build_features_kernel(FeatureArgs p) {
         const double s2 = __dmul_rn(__dmul_rn(-2.0, s0), s1);
         const double d20 = __dmul_rn(s2, __dmul_rn(f.w0, f.w0));
         const double d02 = __dmul_rn(s2, __dmul_rn(f.w1, f.w1));
-        v = -__dadd_rn(d20, d02);
+        if (var) {  // -rho (D20 + D02) - rho_x D10 - rho_y D01
+          const double d10 = __dmul_rn(s1, f.w0), d01 = __dmul_rn(s1, f.w1);
+          v = __dadd_rn(__dadd_rn(__dmul_rn(-rho, __dadd_rn(d20, d02)), -__dmul_rn(rhox, d10)), -__dmul_rn(rhoy, d01));
+        } else {
+          v = -__dadd_rn(d20, d02);
+        }
       } else if (tk.kind == kFlux) {
         const double s1 = __dadd_rn(1.0, -__dmul_rn(s0, s0));
         v = __dadd_rn(__dmul_rn(nx, __dmul_rn(s1, f.w0)), __dmul_rn(ny, __dmul_rn(s1, f.w1)));
+        if (var) v = __dmul_rn(v, rho);  // conormal flux rho du/dn
       } else {  // kValueCov: sum over gamma index order first corner, point, last corner
         v = 0.0;
         if (tk.flags & 1) v = -__dmul_rn(e1, tanh(feat_z(f, cx1, cy1)));

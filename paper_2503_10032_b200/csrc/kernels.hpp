@@ -28,6 +28,8 @@ struct FeatureArgs {
   const double* w1;
   const double* b;
   const double* f;  // N x m
+  const double* coef;  // varcoef_poisson: N x tmax x 3 (rho, rho_x, rho_y) per class task; else nullptr
+  int tmax;
   double* A;        // 2N matrices, ld x ncol column-major (K_i then Kbar_i)
   double* F;        // N x (M x ldF)
   double* Cd;       // N x (M x ldC)

@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <random>
+#include <thread>
 #include <numbers>
 #include <random>
 #include <stdexcept>
@@ -151,7 +153,54 @@ ClassPlan build_class(int mask, int n, bool cov) {
 
 }  // namespace
 
-bool problem_known(int problem) { return problem >= 0 && problem <= 2; }
+bool problem_known(int problem) { return problem >= 0 && problem <= 4; }
+
+GrfField sample_grf(double alpha, uint64_t seed) {  // problems.cpp:15-39: draw order amp, w0, w1, phase
+  if (alpha <= 0) throw std::invalid_argument("sample_grf: alpha must be positive");
+  constexpr int kTerms = 256;
+  GrfField g;
+  g.amp.resize(kTerms);
+  g.fx.resize(kTerms);
+  g.fy.resize(kTerms);
+  g.phase.resize(kTerms);
+  std::mt19937_64 gen(seed);
+  std::normal_distribution<double> na(0.0, alpha * alpha / 16.0);
+  std::normal_distribution<double> nw(0.0, alpha);
+  std::uniform_real_distribution<double> ub(0.0, 2.0 * kPi);
+  for (int i = 0; i < kTerms; ++i) {
+    g.amp[i] = na(gen);
+    g.fx[i] = nw(gen);
+    g.fy[i] = nw(gen);
+    double b;
+    do {
+      b = ub(gen);
+    } while (b <= 0.0);
+    g.phase[i] = b;
+  }
+  return g;
+}
+
+double eval_grf(const GrfField& g, double x, double y) {  // problems.cpp:41-46
+  double v = 0.0;
+  for (size_t i = 0; i < g.amp.size(); ++i) v += g.amp[i] * std::sin(g.fx[i] * x + g.fy[i] * y + g.phase[i]);
+  return v;
+}
+
+namespace {
+/// rho = tanh(grf) + 1.1 and grad rho = (1 - tanh^2) grad grf (problems.cpp:48-66)
+void rho_and_grad(const GrfField& g, double x, double y, double* out) {
+  const double t = std::tanh(eval_grf(g, x, y));
+  double dx = 0.0, dy = 0.0;
+  for (size_t i = 0; i < g.amp.size(); ++i) {
+    const double c = g.amp[i] * std::cos(g.fx[i] * x + g.fy[i] * y + g.phase[i]);
+    dx += c * g.fx[i];
+    dy += c * g.fy[i];
+  }
+  out[0] = t + 1.1;
+  out[1] = (1.0 - t * t) * dx;
+  out[2] = (1.0 - t * t) * dy;
+}
+}  // namespace
 
 double problem_forcing(int problem, double x, double y) {
   switch (problem) {
@@ -170,7 +219,7 @@ double problem_boundary(int problem, double x, double y) {
 }
 
 Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, int flux_variant,
-                bool cov, double rank_tol, int debug_flip_flux_row) {
+                bool cov, double rank_tol, int debug_flip_flux_row, const ProblemParams& params) {
   if (!problem_known(problem)) throw std::invalid_argument("make_problem: unknown problem id");
   if (s < 1) throw std::invalid_argument("partition_domain: s must be >= 1");
   if (n_grid < 3) throw std::invalid_argument("partition_domain: n_grid must be >= 3");
@@ -178,6 +227,7 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
   if (!(l > 0)) throw std::invalid_argument("init_layer: l must be positive");
   Plan p;
   p.problem = problem;
+  p.params = params;
   p.s = s;
   p.n_grid = n_grid;
   p.M = M;
@@ -312,20 +362,42 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
   }
   p.crmax = std::max(p.crmax, 1);
 
-  // ---- right-hand sides f (assembly.cpp:21-33): forcing, boundary data, zero on traces
+  // ---- right-hand sides f (assembly.cpp:21-33): forcing, boundary data, zero on traces;
+  //      varcoef_poisson: the coefficient field at every row point (problems.cpp:74-87, 117-121)
   const int S = s * (n - 1);
+  GrfField grf;
+  if (problem == 3) grf = sample_grf(params.alpha, params.forcing_seed);
+  if (problem == 4) {
+    grf = sample_grf(params.alpha, params.rho_seed);
+    p.coef.assign(static_cast<size_t>(p.N) * p.tmax * 3, 0.0);
+  }
   p.f.assign(static_cast<size_t>(p.N) * p.m, 0.0);
-  for (int i = 0; i < p.N; ++i) {
-    const SubPlan& sp = p.subs[i];
-    const ClassPlan& c = p.classes[sp.cls];
-    for (int t = 0; t < c.n_tasks_k; ++t) {
-      const Task& tk = c.tasks[t];
-      if (tk.row >= c.fixed) continue;
-      const double x = static_cast<double>(sp.ix * (n - 1) + tk.a) / S;
-      const double y = static_cast<double>(sp.iy * (n - 1) + tk.b) / S;
-      p.f[static_cast<size_t>(i) * p.m + tk.row] =
-          tk.kind == kLap ? problem_forcing(problem, x, y) : problem_boundary(problem, x, y);
+  auto fill = [&](int i0, int i1) {
+    for (int i = i0; i < i1; ++i) {
+      const SubPlan& sp = p.subs[i];
+      const ClassPlan& c = p.classes[sp.cls];
+      for (int t = 0; t < static_cast<int>(c.tasks.size()); ++t) {
+        const Task& tk = c.tasks[t];
+        const double x = static_cast<double>(sp.ix * (n - 1) + tk.a) / S;
+        const double y = static_cast<double>(sp.iy * (n - 1) + tk.b) / S;
+        if (problem == 4 && (tk.kind == kLap || tk.kind == kFlux))
+          rho_and_grad(grf, x, y, &p.coef[(static_cast<size_t>(i) * p.tmax + t) * 3]);
+        if (t >= c.n_tasks_k || tk.row >= c.fixed) continue;
+        double v;
+        if (problem <= 2) v = tk.kind == kLap ? problem_forcing(problem, x, y) : problem_boundary(problem, x, y);
+        else if (problem == 3) v = tk.kind == kLap ? eval_grf(grf, x, y) : 0.0;
+        else v = tk.kind == kLap ? 1.0 : 0.0;
+        p.f[static_cast<size_t>(i) * p.m + tk.row] = v;
+      }
     }
+  };
+  if (problem >= 3 && p.N > 1) {  // 256-term GRF sums per point: the reference's parallel_for
+    const int nt = std::max(1, std::min<int>(p.N, static_cast<int>(std::thread::hardware_concurrency())));
+    std::vector<std::thread> th;
+    for (int k = 0; k < nt; ++k) th.emplace_back(fill, p.N * k / nt, p.N * (k + 1) / nt);
+    for (auto& t : th) t.join();
+  } else {
+    fill(0, p.N);
   }
   return p;
 }
@@ -371,6 +443,8 @@ Plan shard_plan(const Plan& g, int lo, int hi) {
   p.N_global = g.N;
   p.subs.assign(g.subs.begin() + lo, g.subs.begin() + hi);
   p.f.assign(g.f.begin() + static_cast<size_t>(lo) * g.m, g.f.begin() + static_cast<size_t>(hi) * g.m);
+  if (!g.coef.empty())
+    p.coef.assign(g.coef.begin() + static_cast<size_t>(lo) * g.tmax * 3, g.coef.begin() + static_cast<size_t>(hi) * g.tmax * 3);
   auto slice = [&](const std::vector<int>& v, int w) {
     return std::vector<int>(v.begin() + static_cast<size_t>(lo) * w, v.begin() + static_cast<size_t>(hi) * w);
   };

@@ -79,8 +79,23 @@ struct SubPlan {
   int gid = 0;                   // global subdomain index (seed + gid, solvers.cpp:136)
 };
 
+/// Problem parameters of the GRF problems (problems.hpp:64-68).
+struct ProblemParams {
+  double alpha = 32.0;
+  uint64_t forcing_seed = 2, rho_seed = 3;
+};
+
+/// Gaussian random field sum_i amp_i sin(w_i . x + phase_i), 256 terms (problems.cpp:15-58),
+/// drawn on the host with the reference's generator and draw order.
+struct GrfField {
+  std::vector<double> amp, fx, fy, phase;
+};
+GrfField sample_grf(double alpha, uint64_t seed);
+double eval_grf(const GrfField& g, double x, double y);
+
 struct Plan {
   int problem = 0, s = 1, n_grid = 3, M = 1;
+  ProblemParams params;
   double l = 1;
   uint64_t seed = 1;
   int flux_variant = 1;  // 0 pointwise, 1 mean_edge
@@ -100,6 +115,9 @@ struct Plan {
   std::vector<int> own_nd;     // 2 * n_delta: i * dmax + k
 
   std::vector<double> f;  // N x m right-hand sides (problem data, assembly.cpp:21-33)
+  // varcoef_poisson: per subdomain and class task, (rho, d rho/dx, d rho/dy) at the task's point
+  // (interior rows: -rho lap - grad rho . grad; flux rows: x rho); empty for the other problems
+  std::vector<double> coef;  // N x tmax x 3
 
   // ---- sharding: this plan holds subdomains [sub_lo, sub_lo + N) of N_global (one rank's
   // contiguous strip); the interface numbering (n_delta, n_pi, npf) stays global
@@ -116,14 +134,14 @@ void shard_range(int N, int rank, int world, int* lo, int* hi);
 
 /// Builds the plan; throws std::invalid_argument like the reference (geometry.cpp:21-22).
 Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, int flux_variant,
-                bool cov, double rank_tol, int debug_flip_flux_row);
+                bool cov, double rank_tol, int debug_flip_flux_row, const ProblemParams& params = {});
 
 /// Seeded feature layer of subdomain i (features.cpp:9-35 via solvers.cpp:134-137):
 /// w0, w1, b (M each) from std::mt19937_64(seed + i).
 void init_layer(const Plan& p, int i, double* w0, double* w1, double* b);
 
 /// Problem data (problems.cpp:135-156 + C4's added problem).
-double problem_forcing(int problem, double x, double y);
+double problem_forcing(int problem, double x, double y);  // problems 0-2 (manufactured)
 double problem_boundary(int problem, double x, double y);
 bool problem_known(int problem);
 

@@ -224,6 +224,7 @@ void Workspace::upload_plan() {
   d_flip.upload(flip, st_);
   g_arena = nullptr;  // setup-only / large buffers below
   d_f.upload(p.f, st_);
+  if (!p.coef.empty()) d_coef.upload(p.coef, st_);
 
   // fixed-size device storage
   ld_ = (p.m + 3) / 4 * 4;
@@ -409,6 +410,8 @@ FeatureArgs Workspace::feature_args() {
   a.w1 = d_w1.ptr;
   a.b = d_b.ptr;
   a.f = d_f.ptr;
+  a.coef = plan.coef.empty() ? nullptr : d_coef.ptr;
+  a.tmax = plan.tmax;
   a.A = d_A.ptr;
   a.F = d_F.ptr;
   a.Cd = d_Cd.ptr;
@@ -1127,6 +1130,8 @@ void Workspace::get_mu(double* mu) {
 void Workspace::field(int n, const double* ref, double* u, double* gx, double* gy, double* sums) {
   if (n < 2) throw std::invalid_argument("sample_field: grid must have at least 2 points per side");
   if (!solved_) throw std::runtime_error("sample_field: no solution (call solve first)");
+  if (ref == nullptr && sums != nullptr && plan.problem >= 3 && !u && !gx && !gy)
+    throw std::invalid_argument("relative_errors: problem has no exact solution");
   const int s = plan.s, N = plan.N, M = plan.M;
   // column (row) ranges of the grid indices, subdomain_of (geometry.cpp:12-18) in the same arithmetic
   const double h = 1.0 / (n - 1);

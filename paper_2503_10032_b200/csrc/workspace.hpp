@@ -169,7 +169,7 @@ class Workspace {
   DevBuf<SubGeo> d_geo;
   std::vector<int> h_kf_ld_, h_kd_ld_;
   std::vector<long long> h_kf_off_, h_kd_off_;
-  DevBuf<double> d_cr_w, d_flip, d_f;
+  DevBuf<double> d_cr_w, d_flip, d_f, d_coef;
   // layers and matrices
   DevBuf<double> d_w0, d_w1, d_b, d_A, d_tau, d_T, d_ratio, d_F, d_Cd;
   DevBuf<int> d_deficient, d_rank, d_status, d_reff, d_perm, d_corner_q, d_spd_fail, d_state;

@@ -44,7 +44,8 @@ def _oracle(cfg, workers=8, layers_only=False):
     return OracleWorkspace(problem=cfg["problem"], s=cfg["s"], n_grid=cfg["n_grid"], M=cfg["M"],
                            l=cfg["l"], seed=cfg["seed"], flux_variant=cfg["flux_variant"],
                            trace_basis=cfg["trace_basis"], workers=workers, cg_workers=workers,
-                           layers_only=layers_only)
+                           layers_only=layers_only, alpha=cfg.get("alpha", 32.0),
+                           forcing_seed=cfg.get("forcing_seed", 2), rho_seed=cfg.get("rho_seed", 3))
 
 
 def _golden(name):

@@ -34,11 +34,13 @@ def run_one(name: str, workers: int, out: str, eval_n: int) -> None:
     t0 = time.time()
     ws = OracleWorkspace(problem=c["problem"], s=c["s"], n_grid=c["n_grid"], M=c["M"], l=c["l"],
                          seed=c["seed"], flux_variant=c["flux_variant"],
-                         trace_basis=c["trace_basis"], workers=workers, cg_workers=workers)
+                         trace_basis=c["trace_basis"], workers=workers, cg_workers=workers,
+                         alpha=c.get("alpha", 32.0), forcing_seed=c.get("forcing_seed", 2),
+                         rho_seed=c.get("rho_seed", 3))
     r = ws.solve(c["method"], c["theta"], c["cg_rel_tol"], 0)
     t1 = time.time()
     u, gx, gy = ws.field(eval_n)
-    l2, h1 = ws.errors(eval_n) if c["problem"] != "none" else (-1, -1)
+    l2, h1 = ws.errors(eval_n) if c["problem"] not in ("poisson_grf", "varcoef_poisson") else (-1.0, -1.0)
     np.savez_compressed(out, iterations=r.iterations, converged=r.converged,
                         residual_history=r.residual_history, mu=r.mu, coeffs=r.coeffs,
                         field_u=u, ranks=r.ranks, ranks_bar=r.ranks_bar, qr_ratio=r.qr_ratio,
@@ -52,6 +54,9 @@ def main() -> None:
     ap.add_argument("--perturb", type=int, default=2)
     ap.add_argument("--workers", type=int, default=os.cpu_count())
     ap.add_argument("--eval-n", type=int, default=257)
+    ap.add_argument("--probe", choices=["entry", "tanh"], default="entry",
+                    help="perturbation model of the spread: 1 ulp of every feature entry, or of the "
+                         "tanh value before the derivatives (DDO_PERTURB_MODE=tanh)")
     ap.add_argument("--child", default=None)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -65,10 +70,17 @@ def main() -> None:
         base = os.path.join("/tmp", f"golden_{name}_0.npz")
         runs = [(0, base)] + [(k, os.path.join("/tmp", f"golden_{name}_{k}.npz"))
                               for k in range(1, a.perturb + 1)]
+        if a.probe == "tanh":  # plus the two systematic biases: every tanh value +1 / -1 ulp
+            runs += [(a.perturb + 1, os.path.join("/tmp", f"golden_{name}_up.npz")),
+                     (a.perturb + 2, os.path.join("/tmp", f"golden_{name}_down.npz"))]
         for seed, out in runs:
             env = dict(os.environ)
+            env.pop("DDO_PERTURB_MODE", None)
             if seed:
                 env["DDO_PERTURB"] = str(1000 + seed)
+                if a.probe == "tanh":
+                    env["DDO_PERTURB_MODE"] = ("tanh_up" if seed == a.perturb + 1 else
+                                               "tanh_down" if seed == a.perturb + 2 else "tanh")
             else:
                 env.pop("DDO_PERTURB", None)
             subprocess.run([sys.executable, __file__, "--child", name, "--out", out,
@@ -83,6 +95,7 @@ def main() -> None:
         g["spread_field"] = spread_field
         g["spread_iterations"] = spread_it
         g["n_perturbed"] = a.perturb
+        g["probe"] = a.probe
         g["config"] = json.dumps(CONFIGS[name])
         np.savez_compressed(os.path.join(GOLDEN, f"{name}.npz"), **g)
         print(f"{name}: iterations {int(g['iterations'])} (spread {spread_it}), field spread "
