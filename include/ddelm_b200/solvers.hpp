@@ -52,6 +52,7 @@ inline ProblemSpec make_problem(const std::string& name, const ProblemParams& pa
   if (name == "poisson_sin2pi_cos3pi_x2y") return {name, DDELM_POISSON_SIN2PI_COS3PI_X2Y, params};
   if (name == "poisson_grf") return {name, DDELM_POISSON_GRF, params};
   if (name == "varcoef_poisson") return {name, DDELM_VARCOEF_POISSON, params};
+  if (name == "biharmonic_sinpi") return {name, DDELM_BIHARMONIC_SINPI, params};
   throw std::invalid_argument("make_problem: unknown problem '" + name + "'");
 }
 
@@ -99,7 +100,7 @@ class Workspace {
  public:
   Workspace(const ProblemSpec& problem, int s, int n_grid, int M, double l, std::uint64_t seed,
             const SolverOptions& opts = {})
-      : s_(s), n_grid_(n_grid), M_(M) {
+      : s_(s), n_grid_(n_grid), M_(M), cc_(problem.id == DDELM_BIHARMONIC_SINPI ? 2 : 1) {
     ddelm_desc d{};
     d.problem = problem.id;
     d.s = s;
@@ -121,8 +122,8 @@ class Workspace {
   }
 
   int n_subs() const { return s_ * s_; }
-  int n_delta() const { return 2 * s_ * (s_ - 1) * (n_grid_ - 2); }
-  int n_pi() const { return (s_ - 1) * (s_ - 1); }
+  int n_delta() const { return 2 * s_ * (s_ - 1) * (n_grid_ - 2) * cc_; }  // geometry.cpp:155-157
+  int n_pi() const { return (s_ - 1) * (s_ - 1) * cc_; }
   int M() const { return M_; }
 
   void build() { detail::check(ddelm_gpu_build(ws_.get())); }
@@ -174,7 +175,7 @@ class Workspace {
   ddelm_ws* handle() { return ws_.get(); }
 
  private:
-  int s_, n_grid_, M_;
+  int s_, n_grid_, M_, cc_;
   std::unique_ptr<ddelm_ws, detail::WsDeleter> ws_;
 };
 

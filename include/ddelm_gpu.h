@@ -48,7 +48,8 @@ enum {
   DDELM_POISSON_SIN2PI_EXP = 1,
   DDELM_POISSON_SIN2PI_COS3PI_X2Y = 2,
   DDELM_POISSON_GRF = 3,      /* -lap u = GRF(forcing_seed), u = 0 on the boundary */
-  DDELM_VARCOEF_POISSON = 4   /* -div(rho grad u) = 1, rho = tanh(GRF(rho_seed)) + 1.1 */
+  DDELM_VARCOEF_POISSON = 4,  /* -div(rho grad u) = 1, rho = tanh(GRF(rho_seed)) + 1.1 */
+  DDELM_BIHARMONIC_SINPI = 5  /* lap^2 u = 4 pi^4 sin sin: cc = bc = 2 (value + Laplacian) */
 };
 
 enum { DDELM_METHOD_DDELM = 0, DDELM_METHOD_CS = 1, DDELM_METHOD_NN = 2 };

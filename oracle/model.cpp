@@ -349,6 +349,13 @@ Point grad_rho(const GrfField& g, const Point& x) {  // problems.cpp:63-66
 }
 
 Mat ProblemSpec::interior_rows(const FeatureLayer& L, const std::vector<Point>& pts) const {
+  if (kind == 2) {  // problems.cpp:88-91: D40 + 2 D22 + D04
+    const Mat d40 = eval_derivative_matrix(L, pts, 4, 0), d22 = eval_derivative_matrix(L, pts, 2, 2),
+              d04 = eval_derivative_matrix(L, pts, 0, 4);
+    Mat C(d40.r, d40.c);
+    for (size_t t = 0; t < C.a.size(); ++t) C.a[t] = (d40.a[t] + 2.0 * d22.a[t]) + d04.a[t];
+    return C;
+  }
   const Mat a = eval_derivative_matrix(L, pts, 2, 0), b = eval_derivative_matrix(L, pts, 0, 2);
   Mat C(a.r, a.c);
   if (kind == 0) {
@@ -366,16 +373,25 @@ Mat ProblemSpec::interior_rows(const FeatureLayer& L, const std::vector<Point>& 
   return C;
 }
 
-Mat ProblemSpec::boundary_rows(const FeatureLayer& L, const std::vector<Point>& pts) const {
-  return trace_rows(L, pts);  // problems.cpp:96-100
+Mat ProblemSpec::boundary_rows(const FeatureLayer& L, const std::vector<Point>& pts, int comp) const {
+  return trace_rows(L, pts, comp);  // problems.cpp:96-100
 }
 
-Mat ProblemSpec::trace_rows(const FeatureLayer& L, const std::vector<Point>& pts) const {
-  return eval_derivative_matrix(L, pts, 0, 0);  // problems.cpp:102-108 (comp 0)
+Mat ProblemSpec::trace_rows(const FeatureLayer& L, const std::vector<Point>& pts, int comp) const {
+  // problems.cpp:102-108: comp 0 the value, comp 1 (biharmonic) the Laplacian
+  if (comp == 0) return eval_derivative_matrix(L, pts, 0, 0);
+  if (comp == 1 && kind == 2) return add(eval_derivative_matrix(L, pts, 2, 0), eval_derivative_matrix(L, pts, 0, 2), 1.0, 1.0);
+  throw std::invalid_argument("trace_rows: invalid component");
 }
 
 Mat ProblemSpec::flux_rows(const FeatureLayer& L, const std::vector<Point>& pts,
-                           const Point& n) const {
+                           const Point& n, int comp) const {
+  if (comp == 1 && kind == 2) {  // problems.cpp:123-128: n . grad(lap u)
+    const Mat gx = add(eval_derivative_matrix(L, pts, 3, 0), eval_derivative_matrix(L, pts, 1, 2), 1.0, 1.0);
+    const Mat gy = add(eval_derivative_matrix(L, pts, 2, 1), eval_derivative_matrix(L, pts, 0, 3), 1.0, 1.0);
+    return add(gx, gy, n.x, n.y);
+  }
+  if (comp != 0) throw std::invalid_argument("flux_rows: invalid component");
   // problems.cpp:113-121: n_x D10 + n_y D01 (Eigen evaluates nx*A + ny*B elementwise)
   Mat rows = add(eval_derivative_matrix(L, pts, 1, 0), eval_derivative_matrix(L, pts, 0, 1), n.x, n.y);
   if (kind == 1)  // conormal flux rho du/dn (problems.cpp:117-121)
@@ -393,6 +409,20 @@ ProblemSpec make_problem(const std::string& name, const ProblemParams& params) {
     auto f = std::make_shared<GrfField>(sample_grf(params.alpha, params.forcing_seed));
     p.forcing = [f](const Point& x) { return eval_grf(*f, x); };
     p.boundary = [](const Point&) { return 0.0; };
+    return p;
+  }
+  if (name == "biharmonic_sinpi") {  // problems.cpp:167-181
+    p.kind = 2;
+    p.components = 2;
+    p.boundary_components = 2;
+    p.default_l = 64;
+    p.exact = [](const Point& x) { return std::sin(kPi * x.x) * std::sin(kPi * x.y); };
+    p.exact_grad = [](const Point& x) {
+      return Point{kPi * std::cos(kPi * x.x) * std::sin(kPi * x.y), kPi * std::sin(kPi * x.x) * std::cos(kPi * x.y)};
+    };
+    p.forcing = [](const Point& x) { return 4.0 * kPi * kPi * kPi * kPi * std::sin(kPi * x.x) * std::sin(kPi * x.y); };
+    p.boundary = p.exact;
+    p.boundary2 = [](const Point& x) { return -2.0 * kPi * kPi * std::sin(kPi * x.x) * std::sin(kPi * x.y); };
     return p;
   }
   if (name == "varcoef_poisson") {  // problems.cpp:162-166
@@ -461,14 +491,27 @@ LocalBlocks assemble_local(const ProblemSpec& problem, const FeatureLayer& L, co
   put(problem.interior_rows(L, ps.interior[i]), 0);
   for (int k = 0; k < b.n_int; ++k) b.f[k] = problem.forcing(ps.interior[i][k]);
   int row = b.n_int;
-  put(problem.boundary_rows(L, ps.boundary[i]), row);
-  for (int k = 0; k < b.n_bnd; ++k) b.f[row + k] = problem.boundary(ps.boundary[i][k]);
-  row += b.n_bnd;
-  put(problem.trace_rows(L, ps.interface[i]), row);
-  for (const LocalEdge& le : ps.local_edges[i]) {
+  for (int c = 0; c < b.bc; ++c) {  // assembly.cpp:23-28: one block per boundary component
+    put(problem.boundary_rows(L, ps.boundary[i], c), row);
+    const ScalarFn& g = c == 0 ? problem.boundary : problem.boundary2;
+    for (int k = 0; k < b.n_bnd; ++k) b.f[row + k] = g(ps.boundary[i][k]);
+    row += b.n_bnd;
+  }
+  for (int c = 0; c < b.cc; ++c) {  // assembly.cpp:29-32: one trace block per component
+    put(problem.trace_rows(L, ps.interface[i], c), row);
+    row += b.n_gamma;
+  }
+  for (const LocalEdge& le : ps.local_edges[i]) {  // assembly.cpp:34-44: F = [comp 0; comp 1]
     std::vector<Point> pts;
     for (int q : le.pts) pts.push_back(ps.interface[i][q]);
-    b.F_edges.push_back(problem.flux_rows(L, pts, le.normal));
+    const int np = static_cast<int>(pts.size());
+    Mat F(b.cc * np, L.M);
+    for (int c = 0; c < b.cc; ++c) {
+      const Mat Fc = problem.flux_rows(L, pts, le.normal, c);
+      for (int j = 0; j < L.M; ++j)
+        for (int k = 0; k < np; ++k) F(c * np + k, j) = Fc(k, j);
+    }
+    b.F_edges.push_back(std::move(F));
   }
   return b;
 }
@@ -513,17 +556,20 @@ Transition build_subdomain_transition(const std::vector<LocalEdge>& edges, int n
 void apply_change_of_variables(LocalBlocks& blocks, const Transition& t) {  // assembly.cpp:80-87
   if (t.T.r != blocks.n_gamma)
     throw std::invalid_argument("apply_change_of_variables: transition size mismatch");
-  const int r0 = blocks.trace_row(0, 0), ng = blocks.n_gamma;
-  for (int j = 0; j < blocks.K.c; ++j) {
-    std::vector<double> old(ng);
-    for (int q = 0; q < ng; ++q) old[q] = blocks.K(r0 + q, j);
-    for (int q = 0; q < ng; ++q) {
-      double s = 0;
-      for (int k = 0; k < ng; ++k) {
-        const double tq = t.Tinv(q, k);
-        if (tq != 0.0) s += tq * old[k];
+  const int ng = blocks.n_gamma;
+  for (int c = 0; c < blocks.cc; ++c) {  // every trace component (assembly.cpp:83-86)
+    const int r0 = blocks.trace_row(c, 0);
+    for (int j = 0; j < blocks.K.c; ++j) {
+      std::vector<double> old(ng);
+      for (int q = 0; q < ng; ++q) old[q] = blocks.K(r0 + q, j);
+      for (int q = 0; q < ng; ++q) {
+        double s = 0;
+        for (int k = 0; k < ng; ++k) {
+          const double tq = t.Tinv(q, k);
+          if (tq != 0.0) s += tq * old[k];
+        }
+        blocks.K(r0 + q, j) = s;
       }
-      blocks.K(r0 + q, j) = s;
     }
   }
 }

@@ -168,22 +168,24 @@ struct ProblemParams {  // problems.hpp:64-68
   uint64_t rho_seed = 3;
 };
 
-/// Poisson-kind problems (cc = bc = 1): poisson_sinpi, poisson_sin2pi_exp, poisson_grf (GRF
-/// forcing), varcoef_poisson (-div(rho grad u) = 1, rho = tanh(GRF) + 1.1, conormal flux), and
-/// C4's manufactured "poisson_sin2pi_cos3pi_x2y". Biharmonic (cc = bc = 2) is out of scope.
+/// The reference catalogue (problems.cpp:132-188): poisson_sinpi, poisson_sin2pi_exp,
+/// poisson_grf (GRF forcing), varcoef_poisson (-div(rho grad u) = 1, rho = tanh(GRF) + 1.1,
+/// conormal flux), biharmonic_sinpi (lap^2 u = f, cc = bc = 2: value and Laplacian traces, normal
+/// derivative and normal derivative of the Laplacian as fluxes), and C4's manufactured
+/// "poisson_sin2pi_cos3pi_x2y".
 struct ProblemSpec {
   std::string name;
-  int kind = 0;  // 0 Poisson, 1 variable-coefficient Poisson (problems.hpp ProblemKind)
+  int kind = 0;  // 0 Poisson, 1 variable-coefficient Poisson, 2 biharmonic (ProblemKind)
   int components = 1, boundary_components = 1;
-  ScalarFn forcing, boundary, exact;
+  ScalarFn forcing, boundary, boundary2, exact;  // boundary2: boundary data of component 1
   GradFn exact_grad;
   std::shared_ptr<GrfField> rho;  // varcoef_poisson
   double default_l = 32;
   bool has_exact() const { return static_cast<bool>(exact); }
   Mat interior_rows(const FeatureLayer& L, const std::vector<Point>& pts) const;
-  Mat boundary_rows(const FeatureLayer& L, const std::vector<Point>& pts) const;
-  Mat trace_rows(const FeatureLayer& L, const std::vector<Point>& pts) const;
-  Mat flux_rows(const FeatureLayer& L, const std::vector<Point>& pts, const Point& n) const;
+  Mat boundary_rows(const FeatureLayer& L, const std::vector<Point>& pts, int comp = 0) const;
+  Mat trace_rows(const FeatureLayer& L, const std::vector<Point>& pts, int comp = 0) const;
+  Mat flux_rows(const FeatureLayer& L, const std::vector<Point>& pts, const Point& n, int comp = 0) const;
 };
 
 ProblemSpec make_problem(const std::string& name, const ProblemParams& params = {});

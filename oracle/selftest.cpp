@@ -769,8 +769,49 @@ void test_problems_grf() {  // test_problems.cpp: GRF sampler, rho, variable-coe
   CHECK_THROWS(make_problem("heat_equation"));
 }
 
+void test_biharmonic_blocks() {  // test_assembly.cpp:70-84, test_problems.cpp:104-116
+  const ProblemSpec p = make_problem("biharmonic_sinpi");
+  CHECK(p.components == 2 && p.boundary_components == 2 && p.kind == 2);
+  const Point x{0.3, 0.7};
+  const double uu = std::sin(std::numbers::pi * x.x) * std::sin(std::numbers::pi * x.y);
+  CHECK(approx(p.exact(x), uu));
+  CHECK(std::abs(p.forcing(x) - 4 * std::pow(std::numbers::pi, 4) * uu) <= 1e-12 * std::abs(p.forcing(x)));
+  CHECK(std::abs(p.boundary2(x) + 2 * std::numbers::pi * std::numbers::pi * uu) <= 1e-13 * std::abs(p.boundary2(x)));
+  const DomainPartition part = partition_domain(2, 5);
+  const PointSets ps = classify_points(part);
+  const FeatureLayer L = init_layer(12, part.boxes[0], 4.0, part.boxes[0].diam() / 2, 3);
+  const LocalBlocks b = assemble_local(p, L, ps, 0);
+  CHECK(b.bc == 2 && b.cc == 2);
+  CHECK(b.rows() == b.n_int + 2 * b.n_bnd + 2 * b.n_gamma);
+  // second trace component = Laplacian trace; second flux component = n . grad(lap)
+  const Mat d20 = eval_derivative_matrix(L, ps.interface[0], 2, 0), d02 = eval_derivative_matrix(L, ps.interface[0], 0, 2);
+  double err = 0, mx = 0;
+  for (int k = 0; k < b.n_gamma; ++k)
+    for (int j = 0; j < L.M; ++j) {
+      const double e = d20(k, j) + d02(k, j);
+      mx = std::max(mx, std::abs(e));
+      err = std::max(err, std::abs(b.K(b.trace_row(1, k), j) - e));
+    }
+  CHECK(err < 1e-13 * mx);
+  bool fstack = true;
+  for (const Mat& F : b.F_edges) fstack = fstack && F.r % 2 == 0;
+  CHECK(fstack);
+  // interior rows: the biharmonic operator of a single feature against finite differences
+  const std::vector<Point> q{{0.2, 0.3}};
+  const Mat rows = p.interior_rows(L, q);
+  const double h = 1e-3;
+  auto lap = [&](double xx, double yy) {
+    const Mat a = eval_derivative_matrix(L, {Point{xx, yy}}, 2, 0), c = eval_derivative_matrix(L, {Point{xx, yy}}, 0, 2);
+    return a(0, 0) + c(0, 0);
+  };
+  const double fd = (lap(q[0].x + h, q[0].y) + lap(q[0].x - h, q[0].y) + lap(q[0].x, q[0].y + h) +
+                     lap(q[0].x, q[0].y - h) - 4 * lap(q[0].x, q[0].y)) / (h * h);
+  CHECK(std::abs(rows(0, 0) - fd) <= 1e-4 * std::max(1.0, std::abs(fd)));
+}
+
 int main() {
   test_features();
+  test_biharmonic_blocks();
   test_problems_grf();
   test_geometry();
   test_assembly();

@@ -25,7 +25,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libddelm_gpu.so")
 
 PROBLEMS = {"poisson_sinpi": 0, "poisson_sin2pi_exp": 1, "poisson_sin2pi_cos3pi_x2y": 2,
-            "poisson_grf": 3, "varcoef_poisson": 4}
+            "poisson_grf": 3, "varcoef_poisson": 4, "biharmonic_sinpi": 5}
 METHODS = {"ddelm": 0, "ddelm-cs": 1, "ddelm-nn": 2}
 
 DDELM_OK, DDELM_ERR_INVALID_ARGUMENT, DDELM_ERR_RUNTIME, DDELM_ERR_CUDA, DDELM_ERR_CAPACITY = range(5)
@@ -262,8 +262,9 @@ class Workspace:
         _check(L.ddelm_gpu_get_shard(h, C.byref(lo), C.byref(cnt), C.byref(ng)))
         self.sub_lo, self.n_local, self.n_global = lo.value, cnt.value, ng.value
         self.n_subs = cnt.value
-        self.n_delta = 2 * s * (s - 1) * (n_grid - 2)
-        self.n_pi = (s - 1) * (s - 1)
+        cc = 2 if problem.name == "biharmonic_sinpi" else 1  # trace components (geometry.cpp:155-157)
+        self.n_delta = 2 * s * (s - 1) * (n_grid - 2) * cc
+        self.n_pi = (s - 1) * (s - 1) * cc
 
     def __del__(self):
         h = getattr(self, "_h", None)

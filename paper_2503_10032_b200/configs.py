@@ -44,4 +44,12 @@ CONFIGS = {
     "T2v": dict(_BASE, problem="varcoef_poisson", s=4, M=64, l=10.0, n_grid=12),
     "T4v": dict(_BASE, problem="varcoef_poisson", s=3, M=100, l=20.0, n_grid=16),
     "C2g": dict(_BASE, problem="poisson_grf", s=4, M=400, l=2.0, n_grid=32),
+    # biharmonic_sinpi (cc = bc = 2; problems.cpp:167-181): full-rank, and the reference's
+    # acceptance criterion 8 (acceptance.cpp:310-328: s = 2, n_grid = 40, M = 1024, l = 16)
+    # scaled to M = 256, n_grid = 20 (pivoted ranks ~245 of 256: the COD branch)
+    "T1b": dict(_BASE, problem="biharmonic_sinpi", s=2, M=64, l=8.0, n_grid=12),
+    "T3b": dict(_BASE, problem="biharmonic_sinpi", s=3, M=144, l=12.0, n_grid=16),
+    "T3bd": dict(_BASE, problem="biharmonic_sinpi", s=3, M=144, l=12.0, n_grid=16, method="ddelm",
+                 flux_variant="pointwise", trace_basis="nodal"),
+    "C8b": dict(_BASE, problem="biharmonic_sinpi", s=2, M=256, l=16.0, n_grid=20),
 }

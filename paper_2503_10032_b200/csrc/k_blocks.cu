@@ -83,13 +83,14 @@ __global__ void __launch_bounds__(256) coarse_local_kernel(BlockArgs a, const in
   extern __shared__ double sm[];
   double* u = sm;                  // r
   double* vals = u + R;            // nF: FC qf
-  __shared__ int cq[4];
+  __shared__ int cq[kMaxCq];
+  const int ncq = a.ncq;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // corner rows in trace-row order (component 0 corners, then component 1)
     int n = 0;
     for (int g = 0; g < d.n_gamma; ++g)
-      if (a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] >= 0 && n < 4) cq[n++] = g;
-    for (; n < 4; ++n) cq[n] = -1;
+      if (a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] >= 0 && n < ncq) cq[n++] = g;
+    for (; n < kMaxCq; ++n) cq[n] = -1;
   }
   // vals = FC qf  (F K^+ f, the data of the flux rows)
   for (int l = warp; l < d.nF; l += nwarp) {
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(256) coarse_local_kernel(BlockArgs a, const in
     if (lane == 0) vals[l] = s;
   }
   __syncthreads();
-  if (threadIdx.x < 4) a.corner_q[i * 4 + threadIdx.x] = cq[threadIdx.x];
+  if (threadIdx.x < ncq) a.corner_q[i * ncq + threadIdx.x] = cq[threadIdx.x];
   const int* off = cr_off + static_cast<size_t>(i) * (a.crmax + 1);
   for (int rho = 0; rho < a.crmax; ++rho) {
     const int row = cr_row[static_cast<size_t>(i) * a.crmax + rho];
@@ -131,22 +132,22 @@ __global__ void __launch_bounds__(256) coarse_local_kernel(BlockArgs a, const in
     __syncthreads();
   }
   // Gc = -(Q_Pi Q_Pi^T) over the corners
-  if (threadIdx.x < 16) {
-    const int p = threadIdx.x / 4, q = threadIdx.x % 4;
+  if (threadIdx.x < ncq * ncq) {
+    const int p = threadIdx.x / ncq, q = threadIdx.x % ncq;
     double s = 0;
     if (cq[p] >= 0 && cq[q] >= 0)
       for (int k = 0; k < r; ++k)
         s += QtX[static_cast<size_t>(k) * E + 1 + cq[p]] * QtX[static_cast<size_t>(k) * E + 1 + cq[q]];
-    a.Gc[static_cast<size_t>(i) * 16 + threadIdx.x] = -s;
+    a.Gc[static_cast<size_t>(i) * ncq * ncq + threadIdx.x] = -s;
   }
   // Ypi = K^+ B_Pi = -C Q_Pi^T (the corner columns; solvers.cpp:287-289)
   const double* Ci = a.C + static_cast<size_t>(i) * a.M * R;
   for (int j = threadIdx.x; j < a.M; j += blockDim.x)
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < ncq; ++q) {
       double s = 0;
       if (cq[q] >= 0)
         for (int k = 0; k < r; ++k) s += Ci[static_cast<size_t>(j) * R + k] * QtX[static_cast<size_t>(k) * E + 1 + cq[q]];
-      a.Ypi[(static_cast<size_t>(i) * a.M + j) * 4 + q] = -s;
+      a.Ypi[(static_cast<size_t>(i) * a.M + j) * ncq + q] = -s;
     }
 }
 
@@ -164,8 +165,8 @@ __global__ void coarse_rows_kernel(BlockArgs a, const int* row_owner /* npf x 4 
       const int i = own / a.crmax, rho = own % a.crmax;
       s += a.pd[own];
       const double* z = a.Zc + (static_cast<size_t>(i) * a.crmax + rho) * a.gmax;
-      for (int p = 0; p < 4; ++p) {
-        const int g = a.corner_q[i * 4 + p];
+      for (int p = 0; p < a.ncq; ++p) {
+        const int g = a.corner_q[i * a.ncq + p];
         if (g < 0) continue;
         const int gp = a.gamma_pi[static_cast<size_t>(i) * a.gmax + g];
         drow[gp] += z[g];
@@ -185,15 +186,15 @@ __global__ void __launch_bounds__(256) coarse_gsum_kernel(BlockArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.N; ++i)
-      for (int p = 0; p < 4; ++p) {
-        const int gp_ = a.corner_q[i * 4 + p];
+      for (int p = 0; p < a.ncq; ++p) {
+        const int gp_ = a.corner_q[i * a.ncq + p];
         if (gp_ < 0) continue;
         const int rp = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gp_];
-        for (int q = 0; q < 4; ++q) {
-          const int gq_ = a.corner_q[i * 4 + q];
+        for (int q = 0; q < a.ncq; ++q) {
+          const int gq_ = a.corner_q[i * a.ncq + q];
           if (gq_ < 0) continue;
           const int rq = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gq_];
-          a.Gsum[static_cast<size_t>(rp) * n + rq] += a.Gc[static_cast<size_t>(i) * 16 + p * 4 + q];
+          a.Gsum[static_cast<size_t>(rp) * n + rq] += a.Gc[(static_cast<size_t>(i) * a.ncq + p) * a.ncq + q];
         }
       }
   }
@@ -360,8 +361,8 @@ __global__ void pack_streams_kernel(BlockArgs a, double* KF, const int* kf_ld, c
     for (int k = threadIdx.x; k < ldKF; k += blockDim.x) {
       double v = 0.0;
       if (k < R) v = c[k];
-      else if (k < R + 4) v = a.Ypi[row * 4 + (k - R)];
-      else if (k - R - 4 < a.ldF) v = a.F[row * a.ldF + (k - R - 4)];
+      else if (k < R + a.ncq) v = a.Ypi[row * a.ncq + (k - R)];
+      else if (k - R - a.ncq < a.ldF) v = a.F[row * a.ldF + (k - R - a.ncq)];
       kf[k] = v;
     }
     for (int k = threadIdx.x; k < ldKD; k += blockDim.x) {

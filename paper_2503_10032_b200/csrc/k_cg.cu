@@ -183,7 +183,7 @@ __device__ __forceinline__ ItemGeo item_geo(const CgArgs& a, int kind, int i, in
   ItemGeo g;
   switch (kind) {
     case kOp2:  // A = C, Y = Ypi, B = F
-      g = {KF, ldf, 0, recon ? -1 : R + 4, R, j1 - j0, d.r, recon ? 0 : d.nF, 0, 0, false};
+      g = {KF, ldf, 0, recon ? -1 : R + a.ncq, R, j1 - j0, d.r, recon ? 0 : d.nF, 0, 0, false};
       break;
     case kNn1:  // A = Cbar, B = Cdelta
       g = {KD, ldd, 0, R, -1, j1 - j0, d.rb, d.nd, 0, 0, false};
@@ -192,7 +192,7 @@ __device__ __forceinline__ ItemGeo item_geo(const CgArgs& a, int kind, int i, in
       g = {KD, ldd, R, 0, -1, j1 - j0, d.nd, d.rb, 0, 0, true};
       break;
     default:    // OP3: A = F, B = C
-      g = {KF, ldf, R + 4, 0, -1, j1 - j0, d.nF, d.r, 0, 0, true};
+      g = {KF, ldf, R + a.ncq, 0, -1, j1 - j0, d.nF, d.r, 0, 0, true};
       break;
   }
   g.rpc = rows_per_chunk(g.ld);
@@ -247,8 +247,8 @@ __device__ __forceinline__ StreamPre stream_pre(const CgArgs& a, int kind) {
       const unsigned long long hi = (reinterpret_cast<unsigned long long>(row + 1 + a.dmax) + 15ull) & ~15ull;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(static_cast<unsigned>(hi - lo)) : "memory");
     }
-  } else if (kind == kOp2 && l < 4 && !a.one_level) {
-    const int g = a.corner_q[i * 4 + l];
+  } else if (kind == kOp2 && l < a.ncq && !a.one_level) {
+    const int g = a.corner_q[i * a.ncq + l];
     pre.crow = g >= 0 ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
   }
   return pre;
@@ -518,38 +518,39 @@ __device__ void rowdot4(const double* Q, int ldq, int nk, int ne, const double* 
   }
 }
 
-/// y[k] = sum_e Q[k*ldq + e] x[e] for k < nk (<= 8 nwarps), e < ne: each warp takes up to 8
-/// consecutive rows and issues all of a batch's loads (8 rows x 6 columns per lane) before its FMAs
-/// — one memory latency per 192 columns instead of one per 32 (latency-bound prologues).
+/// y[k] = sum_e Q[k*ldq + e] x[e] for k < nk, e < ne: each warp takes blocks of up to 8
+/// consecutive rows (ceil(nk / nwarps) <= 8: one block per warp) and issues all of a batch's
+/// loads (8 rows x 4 columns per lane) before its FMAs — one memory latency per 128 columns
+/// instead of one per 32 (latency-bound prologues).
 __device__ void rowdot_wide(const double* Q, int ldq, int nk, int ne, const double* x, double* y, int nwarps) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp >= nwarps) return;
   const int rpw = min(8, (nk + nwarps - 1) / nwarps);
-  const int k0 = warp * rpw;
-  if (k0 >= nk) return;
   constexpr int kE = 4;
-  double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int e0 = lane; e0 < ne; e0 += 32 * kE) {
-    double q[8][kE];
+  for (int k0 = warp * rpw; k0 < nk; k0 += nwarps * rpw) {
+    double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int e0 = lane; e0 < ne; e0 += 32 * kE) {
+      double q[8][kE];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int t = 0; t < kE; ++t) {
+          const int e = e0 + 32 * t;
+          q[u][t] = (u < rpw && k0 + u < nk && e < ne) ? Q[static_cast<size_t>(k0 + u) * ldq + e] : 0.0;
+        }
 #pragma unroll
       for (int t = 0; t < kE; ++t) {
         const int e = e0 + 32 * t;
-        q[u][t] = (u < rpw && k0 + u < nk && e < ne) ? Q[static_cast<size_t>(k0 + u) * ldq + e] : 0.0;
+        const double xe = e < ne ? x[e] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] += q[u][t] * xe;
       }
-#pragma unroll
-    for (int t = 0; t < kE; ++t) {
-      const int e = e0 + 32 * t;
-      const double xe = e < ne ? x[e] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] += q[u][t] * xe;
     }
-  }
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const double v = warp_sum(c[u]);
-    if (lane == 0 && u < rpw && k0 + u < nk) y[k0 + u] = v;
+    for (int u = 0; u < 8; ++u) {
+      const double v = warp_sum(c[u]);
+      if (lane == 0 && u < rpw && k0 + u < nk) y[k0 + u] = v;
+    }
   }
 }
 
@@ -728,23 +729,23 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, 
   __syncthreads();
   if (a.one_level) {
     // no coarse space; the first owner of each corner writes the Pi entries of p_next
-    if (cg && threadIdx.x < 4) {
-      const int g = a.corner_q[i * 4 + threadIdx.x];
-      const int dst = a.corner_dst[i * 4 + threadIdx.x];
+    if (cg && threadIdx.x < a.ncq) {
+      const int g = a.corner_q[i * a.ncq + threadIdx.x];
+      const int dst = a.corner_dst[i * a.ncq + threadIdx.x];
       if (g >= 0 && dst >= 0 && (dst & 3) == 0) pnext[a.n_delta + gpi[g]] = vg[g];
     }
-  } else if (warp < 4) {
-    const int g = a.corner_q[i * 4 + warp];
+  } else if (warp < a.ncq) {
+    const int g = a.corner_q[i * a.ncq + warp];
     double acc = 0;
     if (g >= 0)
       for (int k = lane; k < r; k += 32) acc += QtX[static_cast<size_t>(k) * E + 1 + g] * sh.s0[k];
     acc = warp_sum(acc);
-    const int dst = a.corner_dst[i * 4 + warp];
+    const int dst = a.corner_dst[i * a.ncq + warp];
     if (lane == 0 && dst >= 0) a.ttab_w[dst] = acc;  // t(gp) -= phi - Ky at the corners (phi = 0 there)
   } else if (mode != 1) {
-    // psi_i = Zc v (Dpd rows restricted to this subdomain), warps 4..
+    // psi_i = Zc v (Dpd rows restricted to this subdomain), warps ncq..
     const double* Zc = stg.zc;
-    for (int rho = warp - 4; rho < a.crmax; rho += kWarps - 4) {
+    for (int rho = warp - a.ncq; rho < a.crmax; rho += kWarps - a.ncq) {
       double acc = 0;
       for (int g = lane; g < d.n_gamma; g += 32) acc += Zc[static_cast<size_t>(rho) * a.gmax + g] * vg[g];
       acc = warp_sum(acc);
@@ -760,18 +761,18 @@ template <int W>
 __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int mode, const StreamPre& pre) {
   const int nitems = n_items(a.N * a.P);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ double muc[4];
-  __shared__ int crow[4];
+  __shared__ double muc[kMaxCq];
+  __shared__ int crow[kMaxCq];
   for (int k = 0; k < nitems; ++k) {
     const int w = item_work(k, nitems, false);
     const int i = w / a.P, p = w % a.P;
     if (!a.one_level) gather_z(a, sh, mode, kCThreads);
     const bool first = (k == 0 && pre.i == i);
-    if (threadIdx.x < 4) {
+    if (threadIdx.x < a.ncq) {
       if (first) {
         crow[threadIdx.x] = pre.crow;
       } else {
-        const int g = a.corner_q[i * 4 + threadIdx.x];
+        const int g = a.corner_q[i * a.ncq + threadIdx.x];
         crow[threadIdx.x] = (g >= 0 && !a.one_level) ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
       }
     }
@@ -779,7 +780,7 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
     for (int kk = threadIdx.x; kk < r; kk += kCThreads) sh.xa[kk] = a.s[static_cast<size_t>(i) * a.rmax + kk];
     cons_sync();
     const int nz = a.n_pi + a.npf;
-    rows_dot(a.Wmu, nz, crow, 4, sh.z, nz, muc, kCWarps);  // mu = S^{-1}(t + Dpp^T psi); 0 one-level
+    rows_dot(a.Wmu, nz, crow, a.ncq, sh.z, nz, muc, kCWarps);  // mu = S^{-1}(t + Dpp^T psi); 0 one-level
     if (mode == 2 && w == 0 && !a.one_level)  // mu_Pi of the solution (one CTA writes it)
       for (int gp = warp; gp < a.n_pi; gp += kCWarps) {
         double s = 0;
@@ -794,11 +795,14 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
     part_rows(a, p, j0, j1);
     double* coef = a.coeffs + static_cast<size_t>(i) * a.M;
     const double m0 = muc[0], m1 = muc[1], m2 = muc[2], m3 = muc[3];
+    const int ncq = a.ncq;
     double acc[W];
     // reference grouping (solvers.cpp:336, 342): c = K^+ phi - Ypi mu, then F c
     const bool one = a.one_level != 0;
     consume_item<W>(g, sh, ccnt, acc, [&](int jr, double cs, const double* y, int ln) {
-      const double cj = one ? cs : cs - (((y[0] * m0 + y[1] * m1) + y[2] * m2) + y[3] * m3);
+      double ym = ((y[0] * m0 + y[1] * m1) + y[2] * m2) + y[3] * m3;
+      for (int q = 4; q < ncq; ++q) ym += y[q] * muc[q];  // biharmonic: second-component corners
+      const double cj = one ? cs : cs - ym;
       if (mode == 2 && ln == 0) coef[j0 + jr] = cj;
       return cj;
     });
@@ -942,13 +946,13 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
       up[l] = s;
       sh.s0[l] = s;
     });
-    if (warp < 4 && !a.one_level) {
-      const int gq = a.corner_q[i * 4 + warp];
+    if (warp < a.ncq && !a.one_level) {
+      const int gq = a.corner_q[i * a.ncq + warp];
       double acc2 = 0;
       if (gq >= 0)
         for (int kk = lane; kk < r; kk += 32) acc2 += QtX[static_cast<size_t>(kk) * E + 1 + gq] * sh.s0[kk];
       acc2 = warp_sum(acc2);
-      const int dst = a.corner_dst[i * 4 + warp];
+      const int dst = a.corner_dst[i * a.ncq + warp];
       if (lane == 0 && dst >= 0) a.t3tab_w[static_cast<size_t>(p) * 4 * a.n_pi + dst] = acc2;  // t(gp) += z(lr)
     }
     cons_sync();
@@ -971,8 +975,9 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
                           unsigned long long* tm = nullptr) {
   const SubGeo d = a.geo[i];
   const int r = d.r, R = a.rmax, E = a.ext, n = a.n_pi, nz = a.n_pi + a.npf;
-  __shared__ double cq_mu[4], cq_nu[4], d2s[64], w3t[64];
-  __shared__ RowTask tasks[8 + 2 * 64];
+  __shared__ double cq_mu[kMaxCq], cq_nu[kMaxCq], d2s[64], w3t[64];
+  __shared__ RowTask tasks[2 * kMaxCq + 2 * 64];
+  const int ncq = a.ncq;
   if (a.one_level) {
     // reduced_apply (solvers.cpp:262-274) at the trace rows: o = -phi + Q_G (s + u), written to the
     // owner slots of its Delta index (2 owners) or Pi index (up to 4 owners)
@@ -996,8 +1001,8 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
       if (dg >= 0) {
         a.otab_w[a.gamma_dst[static_cast<size_t>(i) * a.gmax + g]] = o;
       } else {
-        for (int q = 0; q < 4; ++q)
-          if (a.corner_q[i * 4 + q] == g && a.corner_dst[i * 4 + q] >= 0) a.opitab_w[a.corner_dst[i * 4 + q]] = o;
+        for (int q = 0; q < ncq; ++q)
+          if (a.corner_q[i * ncq + q] == g && a.corner_dst[i * ncq + q] >= 0) a.opitab_w[a.corner_dst[i * ncq + q]] = o;
       }
       if (mode == 0) dot += v[idx] * o;
     }
@@ -1023,16 +1028,16 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
     sh.t2[gp] = acc;
   }
   // the four coarse row-dot families run concurrently (one warp per row)
-  if (threadIdx.x < 4) {
-    const int g = a.corner_q[i * 4 + threadIdx.x];
+  if (threadIdx.x < ncq) {
+    const int g = a.corner_q[i * ncq + threadIdx.x];
     const int row = g >= 0 ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
-    tasks[threadIdx.x] = RowTask{a.Wmu, sh.z, &cq_mu[threadIdx.x], nz, row, nz};        // mu = S^-1 (t + Dpp^T psi)
-    tasks[4 + threadIdx.x] = RowTask{a.Sinv, sh.t2, &cq_nu[threadIdx.x], n, row, n};    // nu = S^-1 t'
+    tasks[threadIdx.x] = RowTask{a.Wmu, sh.z, &cq_mu[threadIdx.x], nz, row, nz};          // mu = S^-1 (t + Dpp^T psi)
+    tasks[ncq + threadIdx.x] = RowTask{a.Sinv, sh.t2, &cq_nu[threadIdx.x], n, row, n};    // nu = S^-1 t'
   }
   for (int rho = threadIdx.x; rho < a.crmax; rho += kThreads) {
     const int row = a.cr_row[static_cast<size_t>(i) * a.crmax + rho];
-    tasks[8 + rho] = RowTask{a.Wd, sh.z, &d2s[rho], nz, row, nz};                        // d1 = psi - Dpp mu
-    tasks[8 + a.crmax + rho] = RowTask{a.W3, sh.t2, &w3t[rho], n, row, n};               // Dpp nu
+    tasks[2 * ncq + rho] = RowTask{a.Wd, sh.z, &d2s[rho], nz, row, nz};                   // d1 = psi - Dpp mu
+    tasks[2 * ncq + a.crmax + rho] = RowTask{a.W3, sh.t2, &w3t[rho], n, row, n};          // Dpp nu
   }
   // this thread's u parts and s (independent of the coarse rows: issued early)
   const size_t ust = static_cast<size_t>(a.N) * R;
@@ -1047,17 +1052,17 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
   const double* QtX = stg.qtx;
   __syncthreads();
   mark(tm, 1);
-  row_tasks(tasks, 8 + 2 * a.crmax, kWarps);
+  row_tasks(tasks, 2 * ncq + 2 * a.crmax, kWarps);
   __syncthreads();
   mark(tm, 2);
   if (threadIdx.x < a.crmax) d2s[threadIdx.x] = pcr >= 0 ? d2s[threadIdx.x] - w3t[threadIdx.x] : 0.0;
-  int gq[4];
+  int gq[kMaxCq];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) gq[q] = a.corner_q[i * 4 + q];
+  for (int q = 0; q < kMaxCq; ++q) gq[q] = q < ncq ? a.corner_q[i * ncq + q] : -1;
   for (int k = threadIdx.x; k < r; k += kThreads) {
     double uu = (k == threadIdx.x) ? uu0 : sum_parts(a.u + static_cast<size_t>(i) * R, ust, a.P, k);
     double sk = (k == threadIdx.x) ? sk0 : a.s[static_cast<size_t>(i) * R + k];
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < ncq; ++q)
       if (gq[q] >= 0) {
         const double qk = QtX[static_cast<size_t>(k) * E + 1 + gq[q]];
         uu += qk * cq_nu[q];

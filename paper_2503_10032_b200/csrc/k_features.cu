@@ -26,6 +26,15 @@ __device__ __forceinline__ double feat_z(const Feat& f, double x, double y) {
   return __dadd_rn(__dadd_rn(__dmul_rn(f.w0, x), __dmul_rn(f.w1, y)), f.b);
 }
 
+/// Laplacian of feature f at (x, y): s2 (w0^2) + s2 (w1^2), s2 = -2 s0 (1 - s0^2)
+/// (features.cpp:42-76 order; problems.cpp:105-108 trace / boundary component 1)
+__device__ __forceinline__ double feat_lap(const Feat& f, double x, double y) {
+  const double s0 = tanh(feat_z(f, x, y));
+  const double s1 = __dadd_rn(1.0, -__dmul_rn(s0, s0));
+  const double s2 = __dmul_rn(__dmul_rn(-2.0, s0), s1);
+  return __dadd_rn(__dmul_rn(s2, __dmul_rn(f.w0, f.w0)), __dmul_rn(s2, __dmul_rn(f.w1, f.w1)));
+}
+
 __device__ __forceinline__ double coord(int i0, int a, int S) {
   return static_cast<double>(i0 + a) / static_cast<double>(S);
 }
@@ -78,7 +87,7 @@ __global__ void __launch_bounds__(256) build_features_kernel(FeatureArgs p) {
     // change-of-variables corner points (assembly.cpp:59-75)
     double cx1 = 0, cy1 = 0, cx2 = 0, cy2 = 0, e1 = 0, e2 = 0;
     double nx = 0, ny = 0;
-    if (tk.kind == kValueCov) {
+    if (tk.kind == kValueCov || tk.kind == kLapCov) {
       const bool vert = tk.side < 2;
       const int jj = vert ? tk.b : tk.a;  // geom_j along the edge
       const int ae = vert ? (tk.side == 0 ? 0 : n - 1) : 0;
@@ -93,7 +102,7 @@ __global__ void __launch_bounds__(256) build_features_kernel(FeatureArgs p) {
       // Tinv entries: -(1 - j/(n-1)) for the first corner, -(j/(n-1)) for the last
       e1 = 1.0 - static_cast<double>(jj) / (n - 1);
       e2 = static_cast<double>(jj) / (n - 1);
-    } else if (tk.kind == kFlux) {
+    } else if (tk.kind == kFlux || tk.kind == kFlux3) {
       const double nxs[4] = {-1.0, 1.0, 0.0, 0.0}, nys[4] = {0.0, 0.0, -1.0, 1.0};
       nx = nxs[tk.side];
       ny = nys[tk.side];
@@ -119,6 +128,33 @@ __global__ void __launch_bounds__(256) build_features_kernel(FeatureArgs p) {
         const double s1 = __dadd_rn(1.0, -__dmul_rn(s0, s0));
         v = __dadd_rn(__dmul_rn(nx, __dmul_rn(s1, f.w0)), __dmul_rn(ny, __dmul_rn(s1, f.w1)));
         if (var) v = __dmul_rn(v, rho);  // conormal flux rho du/dn
+      } else if (tk.kind == kLapP) {
+        v = feat_lap(f, x, y);
+      } else if (tk.kind == kBih || tk.kind == kFlux3) {
+        // sigma''' = -2 s1^2 - 2 s0 s2, sigma'''' = -6 s1 s2 - 2 s0 s3 (features.cpp:60-66)
+        const double s1 = __dadd_rn(1.0, -__dmul_rn(s0, s0));
+        const double s2 = __dmul_rn(__dmul_rn(-2.0, s0), s1);
+        const double s3 = __dadd_rn(__dmul_rn(__dmul_rn(-2.0, s1), s1), -__dmul_rn(__dmul_rn(2.0, s0), s2));
+        const double w00 = __dmul_rn(f.w0, f.w0), w11 = __dmul_rn(f.w1, f.w1);
+        if (tk.kind == kBih) {  // D40 + 2 D22 + D04 (problems.cpp:88-91)
+          const double s4 = __dadd_rn(__dmul_rn(__dmul_rn(-6.0, s1), s2), -__dmul_rn(__dmul_rn(2.0, s0), s3));
+          const double d40 = __dmul_rn(s4, __dmul_rn(__dmul_rn(w00, f.w0), f.w0));
+          const double d22 = __dmul_rn(s4, __dmul_rn(__dmul_rn(w00, f.w1), f.w1));
+          const double d04 = __dmul_rn(s4, __dmul_rn(__dmul_rn(w11, f.w1), f.w1));
+          v = __dadd_rn(__dadd_rn(d40, __dmul_rn(2.0, d22)), d04);
+        } else {  // n . grad(lap): nx (D30 + D12) + ny (D21 + D03) (problems.cpp:123-128)
+          const double d30 = __dmul_rn(s3, __dmul_rn(w00, f.w0));
+          const double d12 = __dmul_rn(s3, __dmul_rn(__dmul_rn(f.w0, f.w1), f.w1));
+          const double d21 = __dmul_rn(s3, __dmul_rn(w00, f.w1));
+          const double d03 = __dmul_rn(s3, __dmul_rn(w11, f.w1));
+          v = __dadd_rn(__dmul_rn(nx, __dadd_rn(d30, d12)), __dmul_rn(ny, __dadd_rn(d21, d03)));
+        }
+      } else if (tk.kind == kLapCov) {  // kLapP with the change of variables (as kValueCov)
+        const double lp = feat_lap(f, x, y);
+        v = 0.0;
+        if (tk.flags & 1) v = -__dmul_rn(e1, feat_lap(f, cx1, cy1));
+        v = (tk.flags & 1) ? __dadd_rn(v, lp) : lp;
+        if (tk.flags & 2) v = __dadd_rn(v, -__dmul_rn(e2, feat_lap(f, cx2, cy2)));
       } else {  // kValueCov: sum over gamma index order first corner, point, last corner
         v = 0.0;
         if (tk.flags & 1) v = -__dmul_rn(e1, tanh(feat_z(f, cx1, cy1)));

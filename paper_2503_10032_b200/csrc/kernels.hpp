@@ -90,8 +90,12 @@ void launch_cod_pivqr(const CodArgs& a, cudaStream_t st);
 void launch_cod_finish(const CodArgs& a, cudaStream_t st);  // RZ, C, Q^T X (both branches)
 
 // ---------------------------------------------------------------- interface blocks (k_blocks.cu)
+/// Corner (Pi) rows per subdomain: 4 corners x cc components (cc = 2: biharmonic).
+constexpr int kMaxCq = 8;
+
 struct BlockArgs {
   int N, M, rmax, ext, gmax, fmax, dmax, crmax, ldF, ldC, n_pi, npf, n_delta;
+  int ncq;               // corner rows per subdomain (4 cc)
   const int* rank;       // 2N
   const ClassDims* dims;
   const int* sub_cls;
@@ -108,9 +112,9 @@ struct BlockArgs {
   const double* cr_w;
   double* Zc;            // N x crmax x gmax : (K^+)^T a restricted to gamma rows
   double* pd;            // N x crmax : flux data F K^+ f per cross row (before scatter)
-  double* Gc;            // N x 4 x 4  : -(Q_Pi Q_Pi^T)
-  double* Ypi;           // N x M x 4  : -C Q_Pi^T = K^+ B_Pi (corner columns)
-  int* corner_q;         // N x 4 gamma positions of the corners (-1 pad)
+  double* Gc;            // N x ncq x ncq : -(Q_Pi Q_Pi^T)
+  double* Ypi;           // N x M x ncq  : -C Q_Pi^T = K^+ B_Pi (corner columns)
+  int* corner_q;         // N x ncq gamma rows of the corners (-1 pad)
   double* Dpp;           // npf x n_pi
   double* dpi;           // npf
   double* S;             // n_pi x n_pi
@@ -155,6 +159,7 @@ enum CgJob { kJobCg = 0, kJobApply = 1, kJobRhs = 2, kJobRecon = 3 };
 
 struct CgArgs {
   int N, n_delta, n_pi, npf, gmax, fmax, dmax, crmax, rmax, ext, M;
+  int ncq;                 // corner rows per subdomain (4 cc); KF rows carry ncq Ypi entries
   double theta;
   int use_neumann;         // theta > 0
   // packed per-subdomain stream blocks (one bulk copy per chunk of rows), row j:

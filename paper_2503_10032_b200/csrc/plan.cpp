@@ -25,10 +25,14 @@ int class_mask(int s, int ix, int iy) {
   return m;
 }
 
-/// Point classes of one side class (geometry.cpp:80-142 restricted to one subdomain).
-ClassPlan build_class(int mask, int n, bool cov) {
+/// Point classes of one side class (geometry.cpp:80-142 restricted to one subdomain), with its
+/// row-generation tasks for cc trace / flux components and bc boundary components
+/// (assembly.cpp:9-46, solvers.cpp:418-438); `bih`: biharmonic row kinds.
+ClassPlan build_class(int mask, int n, bool cov, int cc, int bc, bool bih) {
   ClassPlan c;
   c.mask = mask;
+  c.cc = cc;
+  c.bc = bc;
   const bool outer[4] = {(mask & 1) != 0, (mask & 2) != 0, (mask & 4) != 0, (mask & 8) != 0};
   std::vector<std::pair<int, int>> interior, boundary;
   std::map<std::pair<int, int>, int> gamma_of;
@@ -59,9 +63,10 @@ ClassPlan build_class(int mask, int n, bool cov) {
     }
   c.n_int = static_cast<int>(interior.size());
   c.n_bnd = static_cast<int>(boundary.size());
-  c.n_gamma = static_cast<int>(c.gamma.size());
-  c.m = c.n_int + c.n_bnd + c.n_gamma;
-  c.fixed = c.n_int + c.n_bnd;
+  c.n_gpts = static_cast<int>(c.gamma.size());
+  c.n_gamma = cc * c.n_gpts;
+  c.fixed = c.n_int + bc * c.n_bnd;
+  c.m = c.fixed + c.n_gamma;
   for (int side = 0; side < 4; ++side) {
     if (outer[side]) continue;
     LocalEdgeC le;
@@ -79,27 +84,27 @@ ClassPlan build_class(int mask, int n, bool cov) {
     }
     c.edges.push_back(le);
   }
-  // Edge-local position of each non-corner gamma point (solvers.cpp:408-413).
-  std::vector<std::pair<int, int>> where(c.n_gamma, {-1, -1});
+  // flux rows per edge [component 0 points; component 1 points] (assembly.cpp:34-44); edge-local
+  // position of each non-corner interface point (solvers.cpp:408-413)
+  std::vector<std::pair<int, int>> where(c.n_gpts, {-1, -1});
   std::vector<int> edge_row0;
   int off = 0;
   for (int e = 0; e < static_cast<int>(c.edges.size()); ++e) {
     edge_row0.push_back(off);
     const LocalEdgeC& le = c.edges[e];
-    for (int pos = 0; pos < static_cast<int>(le.pts.size()); ++pos) {
-      c.flux_rows.push_back({e, pos});
+    const int np = static_cast<int>(le.pts.size());
+    for (int comp = 0; comp < cc; ++comp)
+      for (int pos = 0; pos < np; ++pos) c.flux_rows.push_back({e, pos, comp});
+    for (int pos = 0; pos < np; ++pos)
       if (!c.gamma[le.pts[pos]].is_cross) where[le.pts[pos]] = {e, pos};
-    }
-    off += static_cast<int>(le.pts.size());
+    off += cc * np;
   }
   c.nF = off;
-  for (int q = 0; q < c.n_gamma; ++q) (c.gamma[q].is_cross ? c.corner_idx : c.delta_idx).push_back(q);
-  c.nc = static_cast<int>(c.corner_idx.size());
-  c.nd = static_cast<int>(c.delta_idx.size());
-  for (int k = 0; k < c.nd; ++k) {
-    auto [e, pos] = where[c.delta_idx[k]];
-    c.flux_row_of_delta.push_back(edge_row0[e] + pos);
-  }
+  for (int q = 0; q < c.n_gpts; ++q) (c.gamma[q].is_cross ? c.corner_idx : c.delta_idx).push_back(q);
+  c.nc_pts = static_cast<int>(c.corner_idx.size());
+  c.nd_pts = static_cast<int>(c.delta_idx.size());
+  c.nc = cc * c.nc_pts;
+  c.nd = cc * c.nd_pts;
 
   // ---- row-generation tasks
   auto task = [](int a, int b, uint8_t kind, uint8_t dst, uint8_t side, uint8_t flags, int row) {
@@ -114,46 +119,54 @@ ClassPlan build_class(int mask, int n, bool cov) {
     t.pad = 0;
     return t;
   };
+  const uint8_t kTrace[2] = {kValue, kLapP}, kTraceCov[2] = {kValueCov, kLapCov}, kFl[2] = {kFlux, kFlux3};
   int row = 0;
-  for (auto [a, b] : interior) c.tasks.push_back(task(a, b, kLap, kDstK | kDual, 0, 0, row++));
-  for (auto [a, b] : boundary) c.tasks.push_back(task(a, b, kValue, kDstK | kDual, 0, 0, row++));
-  for (int q = 0; q < c.n_gamma; ++q) {
-    const GammaPt& g = c.gamma[q];
-    if (!cov || g.is_cross) {
-      c.tasks.push_back(task(g.a, g.b, kValue, kDstK, 0, 0, row++));
-      continue;
+  for (auto [a, b] : interior) c.tasks.push_back(task(a, b, bih ? kBih : kLap, kDstK | kDual, 0, 0, row++));
+  for (int comp = 0; comp < bc; ++comp)
+    for (auto [a, b] : boundary) c.tasks.push_back(task(a, b, kTrace[comp], kDstK | kDual, 0, 0, row++));
+  for (int comp = 0; comp < cc; ++comp)
+    for (int q = 0; q < c.n_gpts; ++q) {
+      const GammaPt& g = c.gamma[q];
+      if (!cov || g.is_cross) {
+        c.tasks.push_back(task(g.a, g.b, kTrace[comp], kDstK, 0, 0, row++));
+        continue;
+      }
+      uint8_t flags = 0;
+      for (const LocalEdgeC& le : c.edges)
+        if (le.side == g.side) flags = (le.first_corner ? 1 : 0) | (le.last_corner ? 2 : 0);
+      c.tasks.push_back(task(g.a, g.b, flags ? kTraceCov[comp] : kTrace[comp], kDstK, static_cast<uint8_t>(g.side),
+                             flags, row++));
     }
-    uint8_t flags = 0;
-    for (const LocalEdgeC& le : c.edges)
-      if (le.side == g.side) flags = (le.first_corner ? 1 : 0) | (le.last_corner ? 2 : 0);
-    c.tasks.push_back(task(g.a, g.b, flags ? kValueCov : kValue, kDstK, static_cast<uint8_t>(g.side), flags, row++));
-  }
   c.n_tasks_k = row;
-  // Kbar tail: corner trace rows (nodal basis), then Delta flux rows (solvers.cpp:418-431)
+  // Kbar tail: corner trace rows (nodal basis), then Delta flux rows, per component
+  // (solvers.cpp:418-431)
   int rb = c.fixed;
-  for (int q : c.corner_idx) c.tasks.push_back(task(c.gamma[q].a, c.gamma[q].b, kValue, kDstKbar, 0, 0, rb++));
-  for (int k = 0; k < c.nd; ++k) {
-    const GammaPt& g = c.gamma[c.delta_idx[k]];
-    c.tasks.push_back(task(g.a, g.b, kFlux, kDstKbar, static_cast<uint8_t>(g.side), 0, rb++));
-  }
+  for (int comp = 0; comp < cc; ++comp)
+    for (int q : c.corner_idx) c.tasks.push_back(task(c.gamma[q].a, c.gamma[q].b, kTrace[comp], kDstKbar, 0, 0, rb++));
+  for (int comp = 0; comp < cc; ++comp)
+    for (int k = 0; k < c.nd_pts; ++k) {
+      const GammaPt& g = c.gamma[c.delta_idx[k]];
+      c.tasks.push_back(task(g.a, g.b, kFl[comp], kDstKbar, static_cast<uint8_t>(g.side), 0, rb++));
+    }
   c.n_tasks_kbar = rb - c.fixed;
   for (int l = 0; l < c.nF; ++l) {
-    auto [e, pos] = c.flux_rows[l];
-    const GammaPt& g = c.gamma[c.edges[e].pts[pos]];
-    c.tasks.push_back(task(g.a, g.b, kFlux, kDstF, static_cast<uint8_t>(c.edges[e].side), 0, l));
+    const ClassPlan::FluxRow& fr = c.flux_rows[l];
+    const GammaPt& g = c.gamma[c.edges[fr.e].pts[fr.pos]];
+    c.tasks.push_back(task(g.a, g.b, kFl[fr.comp], kDstF, static_cast<uint8_t>(c.edges[fr.e].side), 0, l));
   }
   c.n_tasks_f = c.nF;
-  for (int k = 0; k < c.nd; ++k) {
-    const GammaPt& g = c.gamma[c.delta_idx[k]];
-    c.tasks.push_back(task(g.a, g.b, kValue, kDstCd, 0, 0, k));
-  }
+  for (int comp = 0; comp < cc; ++comp)
+    for (int k = 0; k < c.nd_pts; ++k) {
+      const GammaPt& g = c.gamma[c.delta_idx[k]];
+      c.tasks.push_back(task(g.a, g.b, kTrace[comp], kDstCd, 0, 0, comp * c.nd_pts + k));
+    }
   c.n_tasks_cd = c.nd;
   return c;
 }
 
 }  // namespace
 
-bool problem_known(int problem) { return problem >= 0 && problem <= 4; }
+bool problem_known(int problem) { return problem >= 0 && problem <= 5; }
 
 GrfField sample_grf(double alpha, uint64_t seed) {  // problems.cpp:15-39: draw order amp, w0, w1, phase
   if (alpha <= 0) throw std::invalid_argument("sample_grf: alpha must be positive");
@@ -239,10 +252,13 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
   p.debug_flip_flux_row = debug_flip_flux_row;
   const int n = n_grid;
   p.N = s * s;
-  p.m = n * n;
-  if (p.m < M) throw std::invalid_argument("LsFactor: matrix must be square or tall");
-  p.n_delta = 2 * s * (s - 1) * (n - 2);
-  p.n_pi = (s - 1) * (s - 1);
+  p.m = n * n;  // rows of K for cc = 1 (every grid point once); the classes raise it for cc = 2
+  // biharmonic_sinpi (problems.cpp:167-181): two trace / flux / boundary components
+  const int cc = problem == 5 ? 2 : 1, bc = cc;
+  p.cc = cc;
+  p.ncq = 4 * cc;
+  p.n_delta = 2 * s * (s - 1) * (n - 2) * cc;  // geometry.cpp:155-157
+  p.n_pi = (s - 1) * (s - 1) * cc;
   p.npf = 2 * p.n_pi;
   p.multiplicity_pi.assign(p.n_pi, 0);
 
@@ -255,7 +271,7 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
       auto it = cls_of_mask.find(mask);
       if (it == cls_of_mask.end()) {
         it = cls_of_mask.emplace(mask, static_cast<int>(p.classes.size())).first;
-        p.classes.push_back(build_class(mask, n, cov));
+        p.classes.push_back(build_class(mask, n, cov, cc, bc, problem == 5));
       }
       SubPlan& sp = p.subs[i];
       sp.ix = ix;
@@ -265,6 +281,9 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
       sp.gid = i;
     }
   for (const ClassPlan& c : p.classes) {
+    // K = [interior; bc x boundary; cc x trace] rows (assembly.cpp:9-32); LsFactor needs K tall
+    if (c.m < M) throw std::invalid_argument("LsFactor: matrix must be square or tall");
+    p.m = std::max(p.m, c.m);
     p.gmax = std::max(p.gmax, c.n_gamma);
     p.fmax = std::max(p.fmax, c.nF);
     p.dmax = std::max(p.dmax, c.nd);
@@ -295,19 +314,25 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
     if (v[2 * g] < 0) v[2 * g] = val;
     else v[2 * g + 1] = val;
   };
+  // global indices (geometry.cpp:148-179): Delta (edge, comp, t) -> (edge cc + comp)(n-2) + t-1,
+  // Pi (cross, comp) -> cross cc + comp; trace rows q = comp * points + point
+  auto delta_of = [&](int ix, int iy, int side, int comp, int t) {
+    return (edge_id(ix, iy, side) * cc + comp) * (n - 2) + (t - 1);
+  };
   for (int i = 0; i < p.N; ++i) {
     SubPlan& sp = p.subs[i];
     const ClassPlan& c = p.classes[sp.cls];
     sp.gamma_delta.assign(c.n_gamma, -1);
     sp.gamma_pi.assign(c.n_gamma, -1);
     for (int q = 0; q < c.n_gamma; ++q) {
-      const GammaPt& g = c.gamma[q];
+      const int comp = q / c.n_gpts;
+      const GammaPt& g = c.gamma[q % c.n_gpts];
       if (g.is_cross) {
-        const int cid = cross_of(sp.ix, sp.iy, g.a, g.b);
+        const int cid = cross_of(sp.ix, sp.iy, g.a, g.b) * cc + comp;
         sp.gamma_pi[q] = cid;
         p.multiplicity_pi[cid] += 1;
       } else {
-        const int d = edge_id(sp.ix, sp.iy, g.side) * (n - 2) + (g.t - 1);
+        const int d = delta_of(sp.ix, sp.iy, g.side, comp, g.t);
         sp.gamma_delta[q] = d;
         own(p.own_gamma, d, i * p.gmax + q);
       }
@@ -319,33 +344,34 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
     for (const LocalEdgeC& le : c.edges) {
       const int np = static_cast<int>(le.pts.size());
       const int dir = le.side < 2 ? 0 : 1;
-      for (int q = 0; q < np; ++q) {
-        const int j = le.geom_j[q];
-        const int lrow = off + q;
-        if (j > 0 && j < n - 1) {
-          const int d = edge_id(sp.ix, sp.iy, le.side) * (n - 2) + (j - 1);
-          sp.fluxrow_delta[lrow] = d;
-          own(p.own_flux, d, i * p.fmax + lrow);
-          continue;
+      for (int comp = 0; comp < cc; ++comp)
+        for (int q = 0; q < np; ++q) {
+          const int j = le.geom_j[q];
+          const int lrow = off + comp * np + q;
+          if (j > 0 && j < n - 1) {
+            const int d = delta_of(sp.ix, sp.iy, le.side, comp, j);
+            sp.fluxrow_delta[lrow] = d;
+            own(p.own_flux, d, i * p.fmax + lrow);
+            continue;
+          }
+          const GammaPt& g = c.gamma[le.pts[q]];
+          const int r = (cross_of(sp.ix, sp.iy, g.a, g.b) * cc + comp) * 2 + dir;  // assembly.cpp:116
+          auto it = cross_slot.find(r);
+          if (it == cross_slot.end()) {
+            it = cross_slot.emplace(r, static_cast<int>(sp.cross_rows.size())).first;
+            sp.cross_rows.push_back(CrossRow{r, {}});
+          }
+          CrossRow& cr = sp.cross_rows[it->second];
+          if (flux_variant == 0) {
+            cr.e.push_back({lrow, 1.0});
+          } else {
+            const int opposing = (j == 0) ? n - 1 : 0;
+            const double w = 1.0 / (n - 1);
+            for (int q2 = 0; q2 < np; ++q2)
+              if (le.geom_j[q2] != opposing) cr.e.push_back({off + comp * np + q2, w});
+          }
         }
-        const GammaPt& g = c.gamma[le.pts[q]];
-        const int r = cross_of(sp.ix, sp.iy, g.a, g.b) * 2 + dir;
-        auto it = cross_slot.find(r);
-        if (it == cross_slot.end()) {
-          it = cross_slot.emplace(r, static_cast<int>(sp.cross_rows.size())).first;
-          sp.cross_rows.push_back(CrossRow{r, {}});
-        }
-        CrossRow& cr = sp.cross_rows[it->second];
-        if (flux_variant == 0) {
-          cr.e.push_back({lrow, 1.0});
-        } else {
-          const int opposing = (j == 0) ? n - 1 : 0;
-          const double w = 1.0 / (n - 1);
-          for (int q2 = 0; q2 < np; ++q2)
-            if (le.geom_j[q2] != opposing) cr.e.push_back({off + q2, w});
-        }
-      }
-      off += np;
+      off += cc * np;
     }
     // the reference groups cross entries with std::map<grow,...> (solvers.cpp:302-304):
     // rows in increasing global order, entries in scatter order
@@ -353,9 +379,9 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
               [](const CrossRow& x, const CrossRow& y) { return x.r < y.r; });
     p.crmax = std::max(p.crmax, static_cast<int>(sp.cross_rows.size()));
     sp.ndelta_map.assign(c.nd, -1);
-    for (int k = 0; k < c.nd; ++k) {
-      const GammaPt& g = c.gamma[c.delta_idx[k]];
-      const int d = edge_id(sp.ix, sp.iy, g.side) * (n - 2) + (g.t - 1);
+    for (int k = 0; k < c.nd; ++k) {  // Neumann Delta rows comp * points + k (solvers.cpp:439-444)
+      const GammaPt& g = c.gamma[c.delta_idx[k % c.nd_pts]];
+      const int d = delta_of(sp.ix, sp.iy, g.side, k / c.nd_pts, g.t);
       sp.ndelta_map[k] = d;
       own(p.own_nd, d, i * p.dmax + k);
     }
@@ -386,7 +412,11 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
         double v;
         if (problem <= 2) v = tk.kind == kLap ? problem_forcing(problem, x, y) : problem_boundary(problem, x, y);
         else if (problem == 3) v = tk.kind == kLap ? eval_grf(grf, x, y) : 0.0;
-        else v = tk.kind == kLap ? 1.0 : 0.0;
+        else if (problem == 4) v = tk.kind == kLap ? 1.0 : 0.0;
+        else  // biharmonic_sinpi: lap^2 u = 4 pi^4 sin sin, u = sin sin, lap u = -2 pi^2 sin sin
+          v = tk.kind == kBih   ? 4.0 * kPi * kPi * kPi * kPi * std::sin(kPi * x) * std::sin(kPi * y)
+              : tk.kind == kLapP ? -2.0 * kPi * kPi * std::sin(kPi * x) * std::sin(kPi * y)
+                                 : std::sin(kPi * x) * std::sin(kPi * y);
         p.f[static_cast<size_t>(i) * p.m + tk.row] = v;
       }
     }
@@ -412,7 +442,7 @@ Plan shard_plan(const Plan& g, int lo, int hi) {
   // global owner-slot destinations, built on the global plan
   const int N = g.N;
   std::vector<int> gdst(static_cast<size_t>(N) * g.gmax, -1), fdst(static_cast<size_t>(N) * g.fmax, -1),
-      ndst(static_cast<size_t>(N) * g.dmax, -1), cdst(static_cast<size_t>(N) * 4, -1),
+      ndst(static_cast<size_t>(N) * g.dmax, -1), cdst(static_cast<size_t>(N) * g.ncq, -1),
       xdst(static_cast<size_t>(N) * g.crmax, -1);
   for (int d = 0; d < g.n_delta; ++d)
     for (int s = 0; s < 2; ++s) {
@@ -429,7 +459,7 @@ Plan shard_plan(const Plan& g, int lo, int hi) {
       if (sp.gamma_pi[q] >= 0) {
         const int gp = sp.gamma_pi[q];
         if (pi_n[gp] >= 4) throw std::logic_error("shard_plan: corner owner overflow");
-        cdst[static_cast<size_t>(i) * 4 + slot++] = gp * 4 + pi_n[gp]++;
+        cdst[static_cast<size_t>(i) * g.ncq + slot++] = gp * 4 + pi_n[gp]++;
       }
     for (size_t rho = 0; rho < sp.cross_rows.size(); ++rho) {
       const int r = sp.cross_rows[rho].r;
@@ -451,7 +481,7 @@ Plan shard_plan(const Plan& g, int lo, int hi) {
   p.gamma_dst = slice(gdst, g.gmax);
   p.flux_dst = slice(fdst, g.fmax);
   p.nd_dst = slice(ndst, g.dmax);
-  p.corner_dst = slice(cdst, 4);
+  p.corner_dst = slice(cdst, g.ncq);
   p.cross_dst = slice(xdst, g.crmax);
   // owner tables restricted to this strip (local subdomain numbering; -1 = owned by another rank)
   auto remap = [&](std::vector<int>& own, int w) {

@@ -21,7 +21,11 @@
 
 namespace ddg {
 
-enum RowKind : uint8_t { kLap = 0, kValue = 1, kValueCov = 2, kFlux = 3 };
+/// kLap: -(D20 + D02) (Poisson interior; variable coefficient with per-row rho); kValue: D00;
+/// kValueCov: D00 with the change of variables; kFlux: n . grad; biharmonic (cc = bc = 2):
+/// kBih: D40 + 2 D22 + D04, kLapP: D20 + D02 (second trace / boundary component), kLapCov: kLapP
+/// with the change of variables, kFlux3: n . grad(lap) (second flux component)
+enum RowKind : uint8_t { kLap = 0, kValue = 1, kValueCov = 2, kFlux = 3, kBih = 4, kLapP = 5, kLapCov = 6, kFlux3 = 7 };
 enum RowDst : uint8_t { kDstK = 0, kDstKbar = 1, kDstF = 2, kDstCd = 3, kDual = 0x10 };
 
 /// One matrix row to generate (16 bytes). Coordinates come from the local grid (a, b).
@@ -51,14 +55,20 @@ struct LocalEdgeC {
 };
 
 /// Rows and points of one side class (mask bit k set = side k lies on the outer boundary).
+/// Row counts carry the components: n_gamma = cc x interface points (the trace rows, component
+/// blocks), nc / nd = cc x corner / Delta points (Neumann rows), nF = cc x edge points (flux rows,
+/// per edge [component 0; component 1]), fixed = n_int + bc x n_bnd.
 struct ClassPlan {
   int mask = 0;
   int n_int = 0, n_bnd = 0, n_gamma = 0, m = 0, fixed = 0, nc = 0, nd = 0, nF = 0;
-  std::vector<GammaPt> gamma;
+  int cc = 1, bc = 1, n_gpts = 0, nc_pts = 0, nd_pts = 0;  // components and point counts
+  std::vector<GammaPt> gamma;                        // interface points (n_gpts)
   std::vector<LocalEdgeC> edges;
-  std::vector<int> corner_idx, delta_idx;            // gamma indices
-  std::vector<std::pair<int, int>> flux_rows;        // (edge, pos) per concatenated F row
-  std::vector<int> flux_row_of_delta;                // per delta point k: its F row
+  std::vector<int> corner_idx, delta_idx;            // interface point indices
+  struct FluxRow {
+    int e, pos, comp;
+  };
+  std::vector<FluxRow> flux_rows;                    // per concatenated F row
   std::vector<Task> tasks;                           // K (m), Kbar tail (m-fixed), F (nF), Cd (nd)
   int n_tasks_k = 0, n_tasks_kbar = 0, n_tasks_f = 0, n_tasks_cd = 0;
 };
@@ -95,6 +105,8 @@ double eval_grf(const GrfField& g, double x, double y);
 
 struct Plan {
   int problem = 0, s = 1, n_grid = 3, M = 1;
+  int cc = 1;   // trace / flux components per interface point (2: biharmonic)
+  int ncq = 4;  // corner (Pi) rows per subdomain: 4 corners x cc
   ProblemParams params;
   double l = 1;
   uint64_t seed = 1;

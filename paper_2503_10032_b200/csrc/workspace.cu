@@ -179,7 +179,7 @@ void Workspace::upload_plan() {
     }
     int slot = 0;
     for (size_t q = 0; q < sp.gamma_pi.size(); ++q)
-      if (sp.gamma_pi[q] >= 0) push_owner(pi_owner, sp.gamma_pi[q], i * 4 + slot++);
+      if (sp.gamma_pi[q] >= 0) push_owner(pi_owner, sp.gamma_pi[q], i * p.ncq + slot++);
     for (size_t l = 0; l < sp.fluxrow_delta.size(); ++l) fdel[static_cast<size_t>(i) * p.fmax + l] = sp.fluxrow_delta[l];
     for (size_t k = 0; k < sp.ndelta_map.size(); ++k) nmap[static_cast<size_t>(i) * p.dmax + k] = sp.ndelta_map[k];
     int* o = croff.data() + static_cast<size_t>(i) * (p.crmax + 1);
@@ -230,8 +230,15 @@ void Workspace::upload_plan() {
   ld_ = (p.m + 3) / 4 * 4;
   ext_ = 1 + p.gmax;
   ncol_ = p.M + ext_;
-  kmax_ = std::min(p.M, 192);
   const size_t nmat = 2 * static_cast<size_t>(N);
+  // COD rank capacity: the pivoted-QR state (V1, F1, Rr: 3 x kmax x M per matrix) within a
+  // 24 GB budget, at least 192 (the Poisson configs' ranks are 50-90; the biharmonic ones reach
+  // ~750 of M = 1024)
+  {
+    const double per = 24.0 * static_cast<double>(nmat) * p.M;  // bytes per unit of kmax
+    const int fit = static_cast<int>(std::min(1e9, 24e9 / per));
+    kmax_ = std::min(p.M, std::max(192, fit));
+  }
   d_A.alloc(nmat * ld_ * ncol_);
   // padding rows m..ld-1 stay zero for ever: the QR trailing update streams whole 32-row chunks
   DDG_CUDA(cudaMemsetAsync(d_A.ptr, 0, d_A.count * sizeof(double), st_));
@@ -261,10 +268,10 @@ void Workspace::upload_plan() {
   d_Zc.alloc(static_cast<size_t>(N) * p.crmax * p.gmax + 2);  // +16 B: bulk-copy tail
   g_arena = nullptr;
   d_pd.alloc(static_cast<size_t>(N) * p.crmax);
-  d_Gc.alloc(static_cast<size_t>(N) * 16);
-  d_Ypi.alloc(static_cast<size_t>(N) * p.M * 4);
+  d_Gc.alloc(static_cast<size_t>(N) * p.ncq * p.ncq);
+  d_Ypi.alloc(static_cast<size_t>(N) * p.M * p.ncq);
   g_arena = &arena_;  // coarse rows and CG vectors: hot
-  d_corner_q.alloc(static_cast<size_t>(N) * 4);
+  d_corner_q.alloc(static_cast<size_t>(N) * p.ncq);
   const size_t npf = std::max(p.npf, 1), npi = std::max(p.n_pi, 1);
   d_Dpp.alloc(npf * npi);
   d_dpi.alloc(npf);
@@ -518,6 +525,7 @@ BlockArgs Workspace::block_args() {
   b.rmax = rmax_;
   b.ext = ext_;
   b.gmax = p.gmax;
+  b.ncq = p.ncq;
   b.fmax = p.fmax;
   b.dmax = p.dmax;
   b.crmax = p.crmax;
@@ -611,7 +619,7 @@ void Workspace::pack_blocks(const BlockArgs& b) {
     ldKF_ = ldKD_ = 2;
     for (int i = 0; i < plan.N; ++i) {
       const ClassPlan& c = plan.classes[plan.subs[i].cls];
-      kfl[i] = (rmax_ + 4 + c.nF + 1) / 2 * 2;
+      kfl[i] = (rmax_ + plan.ncq + c.nF + 1) / 2 * 2;
       kdl[i] = (rmax_ + c.nd + 1) / 2 * 2;
       kfo[i] = of;
       kdo[i] = od;
@@ -659,6 +667,7 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.n_pi = p.n_pi;
   a.npf = p.npf;
   a.gmax = p.gmax;
+  a.ncq = p.ncq;
   a.fmax = p.fmax;
   a.dmax = p.dmax;
   a.crmax = p.crmax;
@@ -1130,7 +1139,7 @@ void Workspace::get_mu(double* mu) {
 void Workspace::field(int n, const double* ref, double* u, double* gx, double* gy, double* sums) {
   if (n < 2) throw std::invalid_argument("sample_field: grid must have at least 2 points per side");
   if (!solved_) throw std::runtime_error("sample_field: no solution (call solve first)");
-  if (ref == nullptr && sums != nullptr && plan.problem >= 3 && !u && !gx && !gy)
+  if (ref == nullptr && sums != nullptr && (plan.problem == 3 || plan.problem == 4) && !u && !gx && !gy)
     throw std::invalid_argument("relative_errors: problem has no exact solution");
   const int s = plan.s, N = plan.N, M = plan.M;
   // column (row) ranges of the grid indices, subdomain_of (geometry.cpp:12-18) in the same arithmetic
@@ -1216,8 +1225,9 @@ void Workspace::get_local(int i, int which, double* K) {
   init_layers();
   launch_build_features(feature_args(), st_);
   const size_t t = static_cast<size_t>(which ? plan.N + i : i);
-  DDG_CUDA(cudaMemcpy2DAsync(K, sizeof(double) * plan.m, d_A.ptr + t * ld_ * ncol_, sizeof(double) * ld_,
-                             sizeof(double) * plan.m, plan.M, cudaMemcpyDeviceToHost, st_));
+  const size_t rows = plan.classes[plan.subs[i].cls].m;
+  DDG_CUDA(cudaMemcpy2DAsync(K, sizeof(double) * rows, d_A.ptr + t * ld_ * ncol_, sizeof(double) * ld_,
+                             sizeof(double) * rows, plan.M, cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
   built_ = blocks_built_ = coarse_built_ = neumann_built_ = false;
 }

@@ -90,3 +90,54 @@ def test_problem_parameters_reach_the_device(P):
         P.make_problem("varcoef_poisson", P.ProblemParams(alpha=0.0))
     with pytest.raises(ValueError):
         P.make_problem("heat_equation")
+
+
+# ---------------------------------------------------------------- biharmonic (cc = bc = 2)
+BIH = ["T1b", "T3b", "T3bd", "C8b"]
+
+
+@pytest.mark.parametrize("name", ["T1b", "T3b"])
+def test_biharmonic_matrices_match_oracle(P, name):
+    """Two boundary / trace components (value, Laplacian; problems.cpp:96-108), flux components
+    n . grad u and n . grad(lap u) (problems.cpp:113-128), interior D40 + 2 D22 + D04, and the
+    Neumann matrices with both components (solvers.cpp:418-438). Fourth derivatives carry the
+    tanh ulp through 1 - tanh^2 four times: row-relative 1e-11."""
+    cfg = P.CONFIGS[name]
+    ws = P.workspace_from_config(name)
+    ows = _oracle(cfg)
+    ows.solve(cfg["method"], cfg["theta"], cfg["cg_rel_tol"])
+    for i in range(ws.n_subs):
+        for Kg, Ko in ((ws.local_matrix(i, 0), ows.local(i)[0]), (ws.local_matrix(i, 1), ows.kbar(i))):
+            assert Kg.shape == Ko.shape
+            row_scale = np.maximum(np.abs(Ko).max(axis=1, keepdims=True), 1e-300)
+            assert np.max(np.abs(Kg - Ko) / row_scale) <= 1e-11
+
+
+@pytest.mark.parametrize("name", BIH)
+def test_biharmonic_solves_match_oracle(P, name):
+    cfg = P.CONFIGS[name]
+    g = _golden(name)
+    ws, rep = P.solve_config(name)
+    assert rep.converged
+    it_tol = max(1 + 2 * int(g["spread_iterations"]),
+                 int(np.ceil(0.1 * int(g["iterations"]))) if cfg["method"] == "ddelm" else 0)
+    assert abs(rep.iterations - int(g["iterations"])) <= it_tol, (rep.iterations, int(g["iterations"]))
+    rk, rkb, _ = ws.ranks()
+    assert (rk == g["ranks"]).all()
+    assert rep.mu.shape == g["mu"].shape  # Delta and Pi unknowns of both components
+    f_tol = max(1e-9, 4.0 * float(g["spread_field"]))
+    diff = _field_diff(cfg, rep.coeffs, g["field_u"])
+    assert diff <= f_tol, f"{name}: field diff {diff:.3e} > {f_tol:.3e}"
+    # the device's exact-solution metric against the oracle's (same field to f_tol)
+    l2, _ = ws.relative_errors(257)
+    assert abs(l2 - float(g["l2"])) <= 1e-3 * float(g["l2"]) + 10 * f_tol
+
+
+def test_biharmonic_iteration_trend(P):
+    """acceptance.cpp:310-328 (criterion 8, scaled): NN < CS < one-level iterations."""
+    cfg = dict(P.CONFIGS["T3b"])
+    _, nn = P.solve_config(cfg)
+    ws = P.workspace_from_config(cfg)
+    cs = P.ddelm_cs_solve(ws, P.CgOptions(rel_tol=1e-9))
+    _, one = P.solve_config("T3bd")
+    assert nn.iterations < cs.iterations < one.iterations
