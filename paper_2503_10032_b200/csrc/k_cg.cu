@@ -59,7 +59,8 @@ constexpr int kCThreads = kCWarps * 32;
 constexpr int kProducerWarp = kWarps - 1;
 constexpr int kStages = 4;
 constexpr int kStageBytes = 32768;
-constexpr int kMaxW = 512;  // widest row-dot operand / axpy output (16 registers per lane)
+constexpr int kMaxW = 1024;  // widest row-dot operand / axpy output (32 accumulators per lane)
+constexpr int kRedW = 512;   // column chunk of the cross-warp accumulator reduction
 
 // ---------------------------------------------------------------- mbarrier + bulk copy (TMA)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -122,7 +123,7 @@ struct Shared {
 
 __device__ __forceinline__ int wmax_of(const CgArgs& a) { return max(max(a.rmax, a.fmax), max(a.dmax, a.gmax)); }
 __device__ __forceinline__ int wred_of(const CgArgs& a) {
-  return ((max(max(a.rmax, a.fmax), a.dmax) + 31) & ~31);
+  return min(kRedW, (max(max(a.rmax, a.fmax), a.dmax) + 31) & ~31);
 }
 
 __device__ __forceinline__ Shared carve(const CgArgs& a, uint64_t* bars) {
@@ -336,12 +337,15 @@ __device__ void producer_run(const CgArgs& a, Producer& pr, const Shared& sh, in
 template <int W, class Hook>
 __device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt, double (&acc)[W], Hook hook) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double xr[W];
+  // W <= 16: the row-dot operand lives in registers; W = 32 (rows up to 1024 wide): it is read
+  // from shared memory, the registers hold the 32 axpy accumulators
+  constexpr bool kXs = W > 16;
+  double xr[kXs ? 1 : W];
   if (threadIdx.x == 0 && phase_stamps()[4] == 0) phase_stamps()[4] = gtimer();
 #pragma unroll
   for (int q = 0; q < W; ++q) {
     const int k = lane + 32 * q;
-    xr[q] = k < g.wa ? sh.xa[k] : 0.0;
+    if constexpr (!kXs) xr[q] = k < g.wa ? sh.xa[k] : 0.0;
     acc[q] = 0.0;
   }
   for (int cc = 0; cc < g.nch; ++cc) {
@@ -358,7 +362,11 @@ __device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt,
 #pragma unroll
       for (int q = 0; q < W; ++q) {
         const int k = lane + 32 * q;
-        if (k < g.wa) s += ar[k] * xr[q];
+        if constexpr (kXs) {
+          if (k < g.wa) s += ar[k] * sh.xa[k];
+        } else {
+          if (k < g.wa) s += ar[k] * xr[q];
+        }
       }
       s = warp_sum(s);
       const double t = hook(ja + rr, s, row + g.yoff, lane);
@@ -383,18 +391,21 @@ template <int W, class Out>
 __device__ void reduce_warps(const CgArgs& a, const ItemGeo& g, const Shared& sh, const double (&acc)[W], Out out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wr = wred_of(a);
+  for (int c0 = 0; c0 < g.wb; c0 += wr) {  // one chunk unless the rows are wider than kRedW
 #pragma unroll
-  for (int q = 0; q < W; ++q) {
-    const int l = lane + 32 * q;
-    if (l < g.wb) sh.red[warp * wr + l] = acc[q];
+    for (int q = 0; q < W; ++q) {
+      const int l = lane + 32 * q;
+      if (l >= c0 && l < c0 + wr && l < g.wb) sh.red[warp * wr + (l - c0)] = acc[q];
+    }
+    cons_sync();
+    const int nl = min(wr, g.wb - c0);
+    for (int l = threadIdx.x; l < nl; l += kCThreads) {
+      double s = 0;
+      for (int w = 0; w < kCWarps; ++w) s += sh.red[w * wr + l];
+      out(c0 + l, s);
+    }
+    cons_sync();
   }
-  cons_sync();
-  for (int l = threadIdx.x; l < g.wb; l += kCThreads) {
-    double s = 0;
-    for (int w = 0; w < kCWarps; ++w) s += sh.red[w * wr + l];
-    out(l, s);
-  }
-  cons_sync();
 }
 
 // ---------------------------------------------------------------- small helpers
@@ -1496,7 +1507,7 @@ int wmax_host(const CgArgs& a) { return std::max(std::max(a.rmax, a.fmax), std::
 
 size_t smem_bytes(const CgArgs& a) {
   const int wm = wmax_host(a);
-  const int wred = (std::max(std::max(a.rmax, a.fmax), a.dmax) + 31) & ~31;
+  const int wred = std::min(kRedW, (std::max(std::max(a.rmax, a.fmax), a.dmax) + 31) & ~31);
   const size_t small = static_cast<size_t>(wm) + std::max(kCWarps * wred, kThreads) + a.n_pi + a.npf +
                        std::max(a.n_pi, 1) + wm + static_cast<size_t>(a.rmax);
   return static_cast<size_t>(kStages) * kStageBytes + sizeof(double) * small;
@@ -1505,12 +1516,14 @@ size_t smem_bytes(const CgArgs& a) {
 /// Register-blocking width of the streamed phases: widest row-dot operand / axpy output / 32.
 int width_regs(const CgArgs& a) {
   const int w = std::max(std::max(a.rmax, a.fmax), a.dmax);
-  return w <= 256 ? 8 : 16;
+  return w <= 256 ? 8 : w <= 512 ? 16 : 32;
 }
 
 const void* kernel_for(const CgArgs& a) {
-  return width_regs(a) == 8 ? reinterpret_cast<const void*>(cg_persistent_kernel<8>)
-                            : reinterpret_cast<const void*>(cg_persistent_kernel<16>);
+  const int w = width_regs(a);
+  return w == 8    ? reinterpret_cast<const void*>(cg_persistent_kernel<8>)
+         : w == 16 ? reinterpret_cast<const void*>(cg_persistent_kernel<16>)
+                   : reinterpret_cast<const void*>(cg_persistent_kernel<32>);
 }
 
 }  // namespace
@@ -1554,8 +1567,10 @@ void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double*
   cg_check_capacity(a);
   const int G = cg_grid(a);
   const size_t sm = smem_bytes(a);
-  const bool wide = width_regs(a) != 8;
-  const void* k = wide ? reinterpret_cast<const void*>(cg_phase_kernel<16>) : reinterpret_cast<const void*>(cg_phase_kernel<8>);
+  const int wreg = width_regs(a);
+  const void* k = wreg == 8    ? reinterpret_cast<const void*>(cg_phase_kernel<8>)
+                  : wreg == 16 ? reinterpret_cast<const void*>(cg_phase_kernel<16>)
+                               : reinterpret_cast<const void*>(cg_phase_kernel<32>);
   DDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   const int grid = (phase == kPhXr2) ? 1 : G;
   // programmatic dependent launch (the kernel overlaps its static prologue with the previous
@@ -1574,10 +1589,12 @@ void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double*
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (wide)
+  if (wreg == 8)
+    DDG_CUDA(cudaLaunchKernelEx(&cfg, cg_phase_kernel<8>, a, phase, mode, it, vin, vout));
+  else if (wreg == 16)
     DDG_CUDA(cudaLaunchKernelEx(&cfg, cg_phase_kernel<16>, a, phase, mode, it, vin, vout));
   else
-    DDG_CUDA(cudaLaunchKernelEx(&cfg, cg_phase_kernel<8>, a, phase, mode, it, vin, vout));
+    DDG_CUDA(cudaLaunchKernelEx(&cfg, cg_phase_kernel<32>, a, phase, mode, it, vin, vout));
 }
 
 void cg_launch_init(const CgArgs& a, cudaStream_t st) {

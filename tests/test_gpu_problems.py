@@ -141,3 +141,20 @@ def test_biharmonic_iteration_trend(P):
     cs = P.ddelm_cs_solve(ws, P.CgOptions(rel_tol=1e-9))
     _, one = P.solve_config("T3bd")
     assert nn.iterations < cs.iterations < one.iterations
+
+
+def test_acceptance_criterion_8_full_size(P):
+    """The reference's acceptance criterion 8 (acceptance.cpp:310-328) at its own size: biharmonic,
+    s = 2, n_grid = 40, M = 1024, l = 16 — local ranks ~750, the 1024-wide rows of the interface
+    iteration. All three methods converge with H1 error < 1e-3 and NN < CS < one-level iterations."""
+    base = dict(P.CONFIGS["C8b"], s=2, M=1024, n_grid=40, l=16.0)
+    runs = {}
+    for meth, fv, tb, th in [("ddelm", "pointwise", "nodal", 0.0),
+                             ("ddelm-cs", "mean_edge", "change_of_variables", 0.0),
+                             ("ddelm-nn", "mean_edge", "change_of_variables", 0.999)]:
+        cfg = dict(base, method=meth, flux_variant=fv, trace_basis=tb, theta=th)
+        ws, rep = P.solve_config(cfg)
+        assert rep.converged, meth
+        runs[meth] = (rep.iterations, ws.relative_errors(257)[1])
+    assert all(h1 < 1e-3 for _, h1 in runs.values()), runs
+    assert runs["ddelm-nn"][0] < runs["ddelm-cs"][0] < runs["ddelm"][0], runs
