@@ -103,7 +103,7 @@ int ddelm_gpu_create_sharded(const ddelm_desc* desc, int rank, int world, const 
 int ddelm_gpu_get_shard(ddelm_ws* ws, int* sub_lo, int* sub_count, int* n_global);
 /* Host-only view of a shard's owner-slot tables (no device needed): which = 0 gamma, 1 flux,
  * 2 Neumann, 3 corner, 4 cross-row destinations of the local strip, 5 = {sub_lo, N_local,
- * N_global, n_delta, n_pi, npf, gmax, fmax, dmax, crmax}. Returns the table length (copies at
+ * N_global, n_delta, n_pi, npf, gmax, fmax, dmax, crmax, ncq}. Returns the table length (copies at
  * most cap entries into out), or -error. */
 int ddelm_gpu_plan_tables(const ddelm_desc* desc, int rank, int world, int which, int* out, int cap);
 int ddelm_gpu_build(ddelm_ws* ws);

@@ -218,7 +218,7 @@ def plan_tables(cfg, rank: int, world: int) -> dict:
         a = np.zeros(max(n, 1), dtype=np.int32)
         L.ddelm_gpu_plan_tables(C.byref(d), rank, world, which, _ptr(a), n)
         out[name] = a[:n]
-    keys = ["sub_lo", "n_local", "n_global", "n_delta", "n_pi", "npf", "gmax", "fmax", "dmax", "crmax"]
+    keys = ["sub_lo", "n_local", "n_global", "n_delta", "n_pi", "npf", "gmax", "fmax", "dmax", "crmax", "ncq"]
     out.update({k: int(v) for k, v in zip(keys, out.pop("meta"))})
     return out
 

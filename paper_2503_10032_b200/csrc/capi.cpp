@@ -151,7 +151,7 @@ int ddelm_gpu_plan_tables(const ddelm_desc* d, int rank, int world, int which, i
     ddg::shard_range(g.N, rank, world, &lo, &hi);
     const ddg::Plan p = ddg::shard_plan(g, lo, hi);
     const std::vector<int>* v = nullptr;
-    std::vector<int> meta = {p.sub_lo, p.N, p.N_global, p.n_delta, p.n_pi, p.npf, p.gmax, p.fmax, p.dmax, p.crmax};
+    std::vector<int> meta = {p.sub_lo, p.N, p.N_global, p.n_delta, p.n_pi, p.npf, p.gmax, p.fmax, p.dmax, p.crmax, p.ncq};
     switch (which) {
       case 0: v = &p.gamma_dst; break;
       case 1: v = &p.flux_dst; break;

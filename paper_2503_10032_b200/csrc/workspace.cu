@@ -1053,8 +1053,12 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
     xchg(a.pap_w, a.pap, static_cast<size_t>(plan.N_global));
     cg_launch_phase(a, kPhXr1, 0, 0, nullptr, nullptr, st_);  // its last CTA also runs XR2
   };
+  // Sharded (world > 1): the host loop by default — the NCCL all-reduces are then plain stream
+  // operations rather than nodes inside a conditional graph body (whose node types CUDA
+  // restricts); DDELM_CG_GRAPH=1 captures them into the graph anyway.
   const char* ge = std::getenv("DDELM_CG_GRAPH");
-  if (ge && std::strcmp(ge, "0") == 0) {
+  const bool host_loop = ge ? std::strcmp(ge, "0") == 0 : sharded();
+  if (host_loop) {
     CgArgs a = a_in;
     a.cond = 0;
     // DDELM_CG_PHASE_TIMES=1: per-phase CUDA-event times (host loop only; diagnostics)

@@ -22,7 +22,7 @@ import torch.multiprocessing as mp
 
 import paper_2503_10032_b200 as P
 
-CFGS = ["T2", "C2", "C3"]
+CFGS = ["T2", "C2", "C3", "T3b"]  # T3b: biharmonic, two components per interface point
 
 
 def _free_port():
@@ -40,7 +40,7 @@ def _tables_as_writers(cfg, rank, world):
     out = {}
     sizes = {"gamma_dst": 2 * t["n_delta"], "flux_dst": 2 * t["n_delta"], "nd_dst": 2 * t["n_delta"],
              "corner_dst": 4 * t["n_pi"], "cross_dst": 4 * t["npf"]}
-    widths = {"gamma_dst": t["gmax"], "flux_dst": t["fmax"], "nd_dst": t["dmax"], "corner_dst": 4,
+    widths = {"gamma_dst": t["gmax"], "flux_dst": t["fmax"], "nd_dst": t["dmax"], "corner_dst": t["ncq"],
               "cross_dst": t["crmax"]}
     for name, size in sizes.items():
         w = np.zeros(max(size, 1), dtype=np.int64)
