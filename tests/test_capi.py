@@ -90,3 +90,25 @@ def test_cpp_facade_fails_loudly_without_device():
     assert out.returncode == 2 and "no CUDA device" in out.stderr
     bad = subprocess.run([FACADE_BIN, "bogus=1"], capture_output=True, text=True)
     assert bad.returncode == 3
+
+
+def test_problem_catalogue_matches_header():
+    """make_problem's names (problems.cpp:132-188 + C4's addition) map onto the C enumerants."""
+    import re
+    import paper_2503_10032_b200 as P
+    h = open(os.path.join(ROOT, "include", "ddelm_gpu.h")).read()
+    enums = {m.group(1).lower(): int(m.group(2)) for m in re.finditer(r"DDELM_([A-Z0-9_]+) = (\d+)", h)
+             if not m.group(1).startswith(("METHOD", "FLUX", "OK", "ERR"))}
+    assert enums == P.PROBLEMS
+    with pytest.raises(ValueError):
+        P.make_problem("heat_equation")
+    with pytest.raises(ValueError):
+        P.make_problem("poisson_grf", P.ProblemParams(alpha=-1.0))
+    assert P.make_problem("varcoef_poisson").params.rho_seed == 3  # problems.hpp:64-68 defaults
+
+
+def test_every_config_has_a_golden():
+    """Every named workload is pinned by an oracle fixture (tools/make_goldens.py)."""
+    import paper_2503_10032_b200 as P
+    missing = [n for n in P.CONFIGS if not os.path.exists(os.path.join(ROOT, "tests", "golden", f"{n}.npz"))]
+    assert not missing, missing
