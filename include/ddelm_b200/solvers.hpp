@@ -19,6 +19,7 @@
 // Everything heavy runs on the B200 behind include/ddelm_gpu.h; this header only marshals.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -217,6 +218,75 @@ inline ErrorReport field_diff(Workspace& ws, const std::vector<std::vector<doubl
   e.grid_n = grid_n;
   detail::check(ddelm_gpu_field_diff(ws.handle(), grid_n, flat.data(), &e.l2, &e.h1));
   return e;
+}
+
+/// Method selector of dense_oracle_solve (solvers.hpp Method).
+enum class Method { Ddelm = DDELM_METHOD_DDELM, DdelmCs = DDELM_METHOD_CS, DdelmNn = DDELM_METHOD_NN };
+
+/// dense_oracle_solve (solvers.hpp DenseOracle, solvers.cpp:609-709) on the device: the global
+/// block system assembled densely, every pseudo-inverse through the device QR / COD kernels.
+struct DenseOracle {
+  std::vector<double> reduced_op;  // dim x dim, column-major
+  std::vector<double> reduced_rhs, mu_reduced, mu_full;
+  std::vector<std::vector<double>> coeffs;
+  int dim = 0;
+};
+inline DenseOracle dense_oracle_solve(Workspace& ws, Method method, double theta = 0.999) {
+  const int m = static_cast<int>(method);
+  const int dim = method == Method::Ddelm ? ws.n_delta() + ws.n_pi() : ws.n_delta();
+  DenseOracle o;
+  o.reduced_op.resize(static_cast<size_t>(dim) * dim);
+  o.reduced_rhs.resize(dim);
+  o.mu_full.resize(ws.n_delta() + ws.n_pi());
+  std::vector<double> c(static_cast<size_t>(ws.n_subs()) * ws.M());
+  detail::check(ddelm_gpu_dense_oracle(ws.handle(), m, theta, &o.dim, o.reduced_op.data(), o.reduced_rhs.data(),
+                                       o.mu_full.data(), c.data()));
+  o.mu_reduced.assign(o.mu_full.begin(), o.mu_full.begin() + dim);
+  o.coeffs.resize(ws.n_subs());
+  for (int i = 0; i < ws.n_subs(); ++i)
+    o.coeffs[i].assign(c.begin() + static_cast<size_t>(i) * ws.M(), c.begin() + static_cast<size_t>(i + 1) * ws.M());
+  return o;
+}
+
+/// oracle_check (runner.cpp:252-316) on a constructed workspace: solve to 1e-12, the dense
+/// oracle, then the relative mu difference, the field difference on the 65 x 65 grid and the
+/// largest entry of (iterative operator - dense reduced operator) over the unit vectors.
+struct OracleCheckReport {  // runner.hpp OracleCheckReport
+  double mu_diff = 0, field_diff = 0, op_diff = 0;
+  int op_row = -1, op_col = -1;
+  bool pass = false;
+};
+inline OracleCheckReport oracle_check(Workspace& ws, Method method, double theta = 0.999) {
+  const DenseOracle oracle = dense_oracle_solve(ws, method, theta);
+  const CgOptions tight{1e-12, 0};
+  const SolveReport rep = method == Method::Ddelm     ? ddelm_solve(ws, tight)
+                          : method == Method::DdelmCs ? ddelm_cs_solve(ws, tight)
+                                                      : ddelm_nn_solve(ws, theta, tight);
+  OracleCheckReport r;
+  double dn = 0, on = 0;
+  for (size_t k = 0; k < rep.mu.size(); ++k) {
+    dn += (rep.mu[k] - oracle.mu_full[k]) * (rep.mu[k] - oracle.mu_full[k]);
+    on += oracle.mu_full[k] * oracle.mu_full[k];
+  }
+  r.mu_diff = on > 0 ? std::sqrt(dn / on) : std::sqrt(dn);
+  r.field_diff = field_diff(ws, oracle.coeffs, 65).l2;
+  const int dim = oracle.dim;
+  for (int j = 0; j < dim; ++j) {
+    std::vector<double> e(dim, 0.0);
+    e[j] = 1.0;
+    const std::vector<double> col = method == Method::Ddelm ? ws.reduced_apply(e)
+                                    : ws.cs_reduced_apply(e, method == Method::DdelmNn ? theta : 0.0);
+    for (int i = 0; i < dim; ++i) {
+      const double d = std::abs(col[i] - oracle.reduced_op[static_cast<size_t>(j) * dim + i]);
+      if (d > r.op_diff) {
+        r.op_diff = d;
+        r.op_row = i;
+        r.op_col = j;
+      }
+    }
+  }
+  r.pass = r.mu_diff < 1e-6 && r.field_diff < 1e-6 && r.op_diff < 1e-6;
+  return r;
 }
 
 }  // namespace ddelm

@@ -11,6 +11,8 @@
  *   ddelm_gpu_solve         ddelm_cs_solve / ddelm_nn_solve (solvers.cpp:582-605, 535-578)
  *   ddelm_gpu_get_*         SolveReport fields               (solvers.hpp:162-171)
  *   ddelm_gpu_destroy       ~Workspace
+ *   ddelm_gpu_dense_oracle  dense_oracle_solve (solvers.cpp:609-709), behind oracle_check
+ *                           (runner.cpp:252-316)
  *
  * Error convention (mirrors the reference's exceptions, solvers.hpp / SURVEY.md §8b):
  *   DDELM_OK = 0
@@ -149,6 +151,15 @@ int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double
 /* out = reduced_apply(v), the one-level operator (solvers.cpp:262-274); v, out: n_mu = n_delta +
  * n_pi host doubles. */
 int ddelm_gpu_apply_reduced(ddelm_ws* ws, const double* v, double* out);
+/* dense_oracle_solve (solvers.cpp:609-709) on the device: the global block matrices K, B, A (and
+ * Kbar, Bbar, Abar for NN) assembled densely, every pseudo-inverse through the device QR / COD
+ * kernels with Eigen's default threshold eps * min(rows, cols). method: DDELM_METHOD_*; the
+ * reduced system has dim = n_mu (one-level) or n_delta (CS / NN). Outputs (each may be NULL):
+ * reduced_op dim x dim column-major, reduced_rhs dim, mu_full n_mu, coeffs n_subdomains x M.
+ * sum(M) + n_mu > 3000 -> DDELM_ERR_INVALID_ARGUMENT (solvers.cpp:619-620), as is a sharded
+ * workspace. Regenerates the local matrices: the next solve rebuilds the factorisations. */
+int ddelm_gpu_dense_oracle(ddelm_ws* ws, int method, double theta, int* dim, double* reduced_op,
+                           double* reduced_rhs, double* mu_full, double* coeffs);
 /* Drop every built layer (features, factors, coarse, Neumann) but keep the feature layers
  * already uploaded to the device: the next solve re-runs the whole device pipeline. */
 int ddelm_gpu_invalidate(ddelm_ws* ws);

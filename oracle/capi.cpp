@@ -227,6 +227,26 @@ int ddo_apply_reduced(void* p, const double* v, double* out) {
   return 0;
 }
 
+/// dense_oracle_solve (solvers.cpp:609-709): dim = n_mu (one-level) or n_delta; op dim x dim
+/// column-major, rhs dim, mu_full n_mu, coeffs N x M. Returns 0, or 2 on invalid_argument.
+int ddo_dense(void* p, int method, double theta, int* dim, double* op, double* rhs, double* mu_full,
+              double* coeffs) {
+  auto h = static_cast<ddo_handle*>(p);
+  Workspace& ws = *h->ws;
+  try {
+    const Method m = method == 0 ? Method::Ddelm : method == 1 ? Method::DdelmCs : Method::DdelmNn;
+    DenseOracle d = dense_oracle_solve(ws, m, theta);
+    *dim = d.reduced_op.c;
+    std::copy(d.reduced_op.a.begin(), d.reduced_op.a.end(), op);
+    std::copy(d.reduced_rhs.begin(), d.reduced_rhs.end(), rhs);
+    std::copy(d.mu_full.begin(), d.mu_full.end(), mu_full);
+    for (size_t i = 0; i < d.coeffs.size(); ++i) std::copy(d.coeffs[i].begin(), d.coeffs[i].end(), coeffs + i * d.coeffs[i].size());
+  } catch (const std::invalid_argument&) {
+    return 2;
+  }
+  return 0;
+}
+
 /// Relative L2 / H1 errors against the exact solution (runner.cpp:144-150).
 int ddo_errors(void* p, int n, double* l2, double* h1) {
   auto h = static_cast<ddo_handle*>(p);

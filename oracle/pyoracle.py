@@ -59,7 +59,7 @@ def lib():
                                 C.c_char_p, C.c_int]
         for name in ("ddo_info", "ddo_timings", "ddo_residuals", "ddo_mu", "ddo_coeffs",
                      "ddo_ranks", "ddo_layer", "ddo_local", "ddo_kbar", "ddo_field",
-                     "ddo_field_of", "ddo_errors", "ddo_apply_cs", "ddo_apply_reduced"):
+                     "ddo_field_of", "ddo_errors", "ddo_apply_cs", "ddo_apply_reduced", "ddo_dense"):
             getattr(L, name).argtypes = None  # variadic pointer args, set per call
         _lib = L
     return _lib
@@ -186,6 +186,19 @@ class OracleWorkspace:
         out = np.zeros_like(v)
         lib().ddo_apply_reduced(C.c_void_p(self.h), _p(v), _p(out))
         return out
+
+    def dense(self, method="ddelm-nn", theta=0.999):
+        """dense_oracle_solve (solvers.cpp:609-709): (reduced_op, reduced_rhs, mu_full, coeffs)."""
+        info = self.info()
+        N, nd, npi, nmu, M = (int(x) for x in info[:5])
+        dim = nmu if method == "ddelm" else nd
+        op, rhs, mu, co = np.zeros(dim * dim), np.zeros(dim), np.zeros(nmu), np.zeros((N, M))
+        d = C.c_int()
+        rc = lib().ddo_dense(C.c_void_p(self.h), METHODS[method], C.c_double(theta), C.byref(d), _p(op),
+                             _p(rhs), _p(mu), _p(co))
+        if rc:
+            raise ValueError("dense_oracle_solve: system too large for the dense path")
+        return op.reshape(dim, dim).T.copy(), rhs, mu, co
 
     def errors(self, n=257):
         l2, h1 = C.c_double(), C.c_double()

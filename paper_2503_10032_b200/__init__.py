@@ -42,7 +42,7 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_lsq_get_block", "ddelm_gpu_lsq_ld", "ddelm_gpu_lsq_destroy",
            "ddelm_gpu_nccl_unique_id", "ddelm_gpu_create_sharded", "ddelm_gpu_get_shard",
            "ddelm_gpu_plan_tables", "ddelm_gpu_sample_field", "ddelm_gpu_relative_errors",
-           "ddelm_gpu_field_diff", "ddelm_gpu_apply_reduced")
+           "ddelm_gpu_field_diff", "ddelm_gpu_apply_reduced", "ddelm_gpu_dense_oracle")
 
 
 class _Desc(C.Structure):
@@ -95,6 +95,8 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_apply_operator.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_apply_reduced.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_invalidate.argtypes = [C.c_void_p]
+    L.ddelm_gpu_dense_oracle.argtypes = [C.c_void_p, C.c_int, C.c_double, C.POINTER(C.c_int), C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_stream.argtypes = [C.c_void_p]
     L.ddelm_gpu_stream.restype = C.c_void_p
     L.ddelm_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
@@ -410,6 +412,72 @@ def ddelm_solve(ws: Workspace, cg: CgOptions | None = None) -> SolveReport:
     return ws._solve("ddelm", 0.0, cg)
 
 
+@dataclass
+class DenseOracle:
+    """solvers.hpp DenseOracle: the brute-force dense solve of the same discrete system."""
+    reduced_op: np.ndarray   # (dim, dim)
+    reduced_rhs: np.ndarray
+    mu_reduced: np.ndarray
+    mu_full: np.ndarray
+    coeffs: np.ndarray       # (n_subs, M)
+
+
+def dense_oracle_solve(ws: Workspace, method: str = "ddelm-nn", theta: float = 0.999) -> DenseOracle:
+    """dense_oracle_solve (solvers.cpp:609-709) on the device: K, B, A (and Kbar, Bbar, Abar for NN)
+    assembled densely, every pseudo-inverse through the device QR / COD kernels with Eigen's default
+    threshold; the reduced system solved by a device COD. sum(M) + n_mu <= 3000 (ValueError above,
+    as the reference). Regenerates the local matrices: the next solve rebuilds the factorisations."""
+    nmu = ws.n_delta + ws.n_pi
+    dim = nmu if method == "ddelm" else ws.n_delta
+    op = np.zeros((dim, dim))
+    rhs, mu, co = np.zeros(dim), np.zeros(nmu), np.zeros((ws.n_subs, ws.M))
+    d = C.c_int()
+    _check(load_library().ddelm_gpu_dense_oracle(ws._h, METHODS[method], float(theta), C.byref(d), _ptr(op),
+                                                 _ptr(rhs), _ptr(mu), _ptr(co)))
+    op = op.T.copy()  # column-major -> (row, col)
+    return DenseOracle(op, rhs, mu[:dim].copy(), mu, co)
+
+
+@dataclass
+class OracleCheckReport:
+    """runner.hpp OracleCheckReport."""
+    mu_diff: float
+    field_diff: float
+    op_diff: float
+    op_row: int
+    op_col: int
+    passed: bool
+
+
+def oracle_check(name_or_cfg, device: int = 0) -> OracleCheckReport:
+    """oracle_check (runner.cpp:252-316): the iterative solve to 1e-12 against the dense oracle —
+    relative mu difference, field difference on the 65 x 65 grid, and the largest entry of
+    (iterative operator - dense reduced operator) over the unit vectors; pass below 1e-6 each."""
+    cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
+    method, theta = cfg["method"], float(cfg.get("theta", 0.999))
+    ws = workspace_from_config(cfg, device)
+    dense = dense_oracle_solve(ws, method, theta)
+    tight = CgOptions(rel_tol=1e-12, max_iter=0)
+    rep = (ddelm_solve(ws, tight) if method == "ddelm" else ddelm_cs_solve(ws, tight)
+           if method == "ddelm-cs" else ddelm_nn_solve(ws, theta, tight))
+    mn = np.linalg.norm(dense.mu_full)
+    mu_diff = float(np.linalg.norm(rep.mu - dense.mu_full) / (mn if mn > 0 else 1.0))
+    field = ws.field_diff(dense.coeffs, 65)[0]
+    dim = dense.reduced_op.shape[0]
+    op_diff, op_row, op_col = 0.0, -1, -1
+    for j in range(dim):
+        e = np.zeros(dim)
+        e[j] = 1.0
+        col = ws.apply_reduced(e) if method == "ddelm" else \
+            ws.apply_operator(e, theta if method == "ddelm-nn" else 0.0)
+        d = np.abs(col - dense.reduced_op[:, j])
+        i = int(np.argmax(d))
+        if d[i] > op_diff:
+            op_diff, op_row, op_col = float(d[i]), i, j
+    return OracleCheckReport(mu_diff, field, op_diff, op_row, op_col,
+                             mu_diff < 1e-6 and field < 1e-6 and op_diff < 1e-6)
+
+
 class LsqBatch:
     """C5 microbenchmark: batched local least squares (QR of [K | B]) + interface Schur block S
     (include/ddelm_gpu.h, ddelm_gpu_lsq_*). Flops per block follow SURVEY.md §8d."""
@@ -452,7 +520,8 @@ class LsqBatch:
 def workspace_from_config(name_or_cfg, device: int = 0, shard: tuple | None = None) -> Workspace:
     cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
     opts = SolverOptions(flux_variant=cfg["flux_variant"],
-                         change_of_variables=cfg["trace_basis"] == "change_of_variables")
+                         change_of_variables=cfg["trace_basis"] == "change_of_variables",
+                         debug_flip_flux_row=int(cfg.get("debug_flip_flux_row", -1)))
     problem = make_problem(cfg["problem"], ProblemParams(cfg.get("alpha", 32.0), cfg.get("forcing_seed", 2),
                                                          cfg.get("rho_seed", 3)))
     return Workspace(problem, cfg["s"], cfg["n_grid"], cfg["M"], cfg["l"], cfg["seed"], opts, device,

@@ -293,6 +293,18 @@ int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double
 int ddelm_gpu_apply_reduced(ddelm_ws* ws, const double* v, double* out) {
   return guarded([&] { ws->w->apply_reduced(v, out); });
 }
+int ddelm_gpu_dense_oracle(ddelm_ws* ws, int method, double theta, int* dim, double* reduced_op,
+                           double* reduced_rhs, double* mu_full, double* coeffs) {
+  return guarded([&] {
+    ddg::DenseOracleOut o;
+    ws->w->dense_oracle(method, theta, o);
+    if (dim) *dim = o.dim;
+    if (reduced_op) std::copy(o.reduced_op.begin(), o.reduced_op.end(), reduced_op);
+    if (reduced_rhs) std::copy(o.reduced_rhs.begin(), o.reduced_rhs.end(), reduced_rhs);
+    if (mu_full) std::copy(o.mu_full.begin(), o.mu_full.end(), mu_full);
+    if (coeffs) std::copy(o.coeffs.begin(), o.coeffs.end(), coeffs);
+  });
+}
 int ddelm_gpu_invalidate(ddelm_ws* ws) {
   return guarded([&] { ws->w->invalidate(); });
 }

@@ -748,6 +748,8 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
 
 }  // namespace
 
+bool cod_finish_supports(int M, int r) { return r <= kFinR || M <= 32 * kNPL; }
+
 void launch_cod_pivqr(const CodArgs& a, cudaStream_t st) {
   const size_t smem = sizeof(double) * (4 * a.M + 2 * a.kmax) + sizeof(int) * 2 * a.M;
   DDG_CUDA(cudaFuncSetAttribute(cod_pivqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -88,6 +88,18 @@ struct CodArgs {
 };
 void launch_cod_pivqr(const CodArgs& a, cudaStream_t st);
 void launch_cod_finish(const CodArgs& a, cudaStream_t st);  // RZ, C, Q^T X (both branches)
+/// whether cod_finish handles an M-column matrix of numerical rank r (the sequential path above
+/// rank 96 holds one column in 32 registers per lane: M <= 1024)
+bool cod_finish_supports(int M, int r);
+
+// ---------------------------------------------------------------- dense oracle (k_dense.cu)
+/// C = alpha op(A) op(B) + beta C, column-major FP64
+void dense_gemm(int m, int n, int k, double alpha, const double* A, int lda, bool ta, const double* B, int ldb,
+                bool tb, double beta, double* C, int ldc, cudaStream_t st);
+/// out (n x e) = X^+ R for X (m x n, m >= n) with Eigen's default COD threshold, on the batched
+/// QR / COD kernels; synchronises the stream
+void dense_cod_solve(const double* X, int ldx, int m, int n, const double* R, int ldr, int e, double* out, int ldo,
+                     cudaStream_t st, int* rank_out);
 
 // ---------------------------------------------------------------- interface blocks (k_blocks.cu)
 /// Corner (Pi) rows per subdomain: 4 corners x cc components (cc = 2: biharmonic).

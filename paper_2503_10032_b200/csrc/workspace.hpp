@@ -59,6 +59,13 @@ struct KernelStat {
   long long launches = 0;
 };
 
+/// dense_oracle_solve's outputs (solvers.hpp DenseOracle): reduced operator / rhs (dim = n_mu for
+/// the one-level method, n_delta for the coarse ones; column-major), mu_full (n_mu), coefficients.
+struct DenseOracleOut {
+  int dim = 0;
+  std::vector<double> reduced_op, reduced_rhs, mu_full, coeffs;
+};
+
 struct SolveResult {
   int iterations = 0;
   bool converged = false, negative_curvature = false;
@@ -99,6 +106,9 @@ class Workspace {
   int get_residuals(double* h, int cap);
   void get_ranks(int* rk, int* rkb, double* ratio);
   void get_local(int i, int which, double* K);
+  /// dense brute-force oracle on the device (solvers.cpp:609-709, k_dense.cu); regenerates the
+  /// local matrices, so the next solve rebuilds the factorisations
+  void dense_oracle(int method, double theta, DenseOracleOut& o);
   const double* phase_ms() const { return phase_ms_; }
   long long launches() const { return solve_launches_; }
   double host_build_ms() const { return host_build_ms_; }

@@ -84,3 +84,20 @@ def test_field_rel_l2_metric():
     u = np.random.default_rng(0).standard_normal(n * n)
     assert field_rel_l2(u, u, n) == 0.0
     assert abs(field_rel_l2(2 * u, u, n) - 1.0) < 1e-14
+
+
+def test_dense_oracle_restatement_matches_iterative_solve():
+    """The oracle's dense_oracle_solve restatement (solvers.cpp:609-709), the checker of
+    tests/test_gpu_dense.py, agrees with its own iterative solve at 1e-12 on the tiny instance
+    (the reference's oracle_check, runner.cpp:252-316)."""
+    from oracle.pyoracle import OracleWorkspace
+    for method, theta in (("ddelm-nn", 0.999), ("ddelm-cs", 0.0)):
+        w = OracleWorkspace(s=2, n_grid=10, M=64, l=8.0)
+        op, rhs, mu, co = w.dense(method, theta)
+        r = w.solve(method, theta, 1e-12)
+        assert np.linalg.norm(r.mu - mu) <= 1e-6 * np.linalg.norm(mu)
+        assert np.abs(op - op.T).max() <= 1e-10 * np.abs(op).max()
+        assert op.shape == (r.n_delta, r.n_delta)
+    w = OracleWorkspace(s=4, n_grid=16, M=200, l=8.0)
+    with pytest.raises(ValueError):
+        w.dense("ddelm-nn", 0.999)
