@@ -1,11 +1,13 @@
 // ddelm_solve — C++ host program over the drop-in façade (include/ddelm_b200/solvers.hpp).
 //
-// The device-path subset of `ddelm_cli solve` (tools/ddelm_cli.cpp:55-92, runner.cpp:126-155):
-//   ddelm_solve [key=value ...]   keys: problem s n_grid M l seed method theta flux_variant
-//                                 trace_basis cg_rel_tol cg_max_iter device eval_grid_n
-//                                 alpha forcing_seed rho_seed
+// The device-path subset of `ddelm_cli solve` and `ddelm_cli oracle-check` (tools/ddelm_cli.cpp:
+// 55-92, runner.cpp:126-155, 252-316):
+//   ddelm_solve [key=value ...]   keys: mode (solve | oracle-check) problem s n_grid M l seed method
+//                                 theta flux_variant trace_basis cg_rel_tol cg_max_iter device
+//                                 eval_grid_n alpha forcing_seed rho_seed debug_flip_flux_row
 // Prints one JSON object (iterations, converged, residual history, mu, timings, and the relative
-// L2 / H1 errors against the exact solution on the eval_grid_n^2 grid, runner.cpp:144-150) on stdout.
+// L2 / H1 errors against the exact solution on the eval_grid_n^2 grid, runner.cpp:144-150) on stdout;
+// mode=oracle-check prints the CLI's oracle-check line (ddelm_cli.cpp:71-77) instead.
 // Exit codes follow the CLI: 0 ok, 2 non-convergence / solver error, 3 configuration error.
 #include <cstdio>
 #include <cstdlib>
@@ -20,7 +22,8 @@ int main(int argc, char** argv) {
       {"problem", "poisson_sinpi"}, {"s", "2"}, {"n_grid", "10"}, {"M", "64"}, {"l", "8"}, {"seed", "1"},
       {"method", "ddelm-nn"}, {"theta", "0.999"}, {"flux_variant", "mean_edge"},
       {"trace_basis", "change_of_variables"}, {"cg_rel_tol", "1e-9"}, {"cg_max_iter", "0"}, {"device", "0"},
-      {"eval_grid_n", "257"}, {"alpha", "32"}, {"forcing_seed", "2"}, {"rho_seed", "3"}};
+      {"eval_grid_n", "257"}, {"alpha", "32"}, {"forcing_seed", "2"}, {"rho_seed", "3"},
+      {"mode", "solve"}, {"debug_flip_flux_row", "-1"}};
   for (int k = 1; k < argc; ++k) {
     const std::string a = argv[k];
     const auto eq = a.find('=');
@@ -35,6 +38,7 @@ int main(int argc, char** argv) {
     opts.flux_variant = kv["flux_variant"] == "mean_edge" ? ddelm::FluxVariant::MeanEdge : ddelm::FluxVariant::Pointwise;
     opts.change_of_variables = kv["trace_basis"] == "change_of_variables";
     opts.device = std::atoi(kv["device"].c_str());
+    opts.debug_flip_flux_row = std::atoi(kv["debug_flip_flux_row"].c_str());
     ddelm::ProblemParams pp;
     pp.alpha = std::atof(kv["alpha"].c_str());
     pp.forcing_seed = std::strtoull(kv["forcing_seed"].c_str(), nullptr, 10);
@@ -46,6 +50,16 @@ int main(int argc, char** argv) {
     const std::string method = kv["method"];
     if (method != "ddelm" && method != "ddelm-cs" && method != "ddelm-nn")
       throw std::invalid_argument("unknown method '" + method + "'");
+    if (kv["mode"] == "oracle-check") {
+      const ddelm::Method m = method == "ddelm"      ? ddelm::Method::Ddelm
+                              : method == "ddelm-cs" ? ddelm::Method::DdelmCs
+                                                     : ddelm::Method::DdelmNn;
+      const ddelm::OracleCheckReport oc = ddelm::oracle_check(ws, m, std::atof(kv["theta"].c_str()));
+      std::printf("mu_diff=%.3e field_diff=%.3e op_diff=%.3e (row=%d col=%d) -> %s\n", oc.mu_diff, oc.field_diff,
+                  oc.op_diff, oc.op_row, oc.op_col, oc.pass ? "pass" : "FAIL");
+      return oc.pass ? 0 : 2;
+    }
+    if (kv["mode"] != "solve") throw std::invalid_argument("unknown mode '" + kv["mode"] + "'");
     ddelm::SolveReport r = method == "ddelm"      ? ddelm::ddelm_solve(ws, cg)
                            : method == "ddelm-cs" ? ddelm::ddelm_cs_solve(ws, cg)
                                                   : ddelm::ddelm_nn_solve(ws, std::atof(kv["theta"].c_str()), cg);

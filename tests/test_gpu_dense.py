@@ -88,3 +88,16 @@ def test_dense_oracle_size_limit(P):
     ws = P.workspace_from_config(cfg)
     with pytest.raises(ValueError):
         P.dense_oracle_solve(ws, "ddelm-nn", 0.999)
+
+
+def test_cpp_facade_oracle_check_mode(P):
+    """`ddelm_cli oracle-check` (ddelm_cli.cpp:71-77) through the C++ façade's oracle_check."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2503_10032_b200",
+                       "ddelm_solve")
+    ok = subprocess.run([exe, "mode=oracle-check"], capture_output=True, text=True)
+    assert ok.returncode == 0 and ok.stdout.strip().endswith("-> pass"), ok.stdout + ok.stderr
+    bad = subprocess.run([exe, "mode=oracle-check", "method=ddelm", "flux_variant=pointwise", "trace_basis=nodal",
+                          "debug_flip_flux_row=3"], capture_output=True, text=True)
+    assert bad.returncode == 2 and bad.stdout.strip().endswith("-> FAIL"), bad.stdout + bad.stderr
