@@ -179,90 +179,115 @@ __global__ void coarse_rows_kernel(BlockArgs a, const int* row_owner /* npf x 4 
 }
 
 /// Gsum = sum over this workspace's subdomains of the corner Grams -(Q_Pi Q_Pi^T), scattered to
-/// (Pi, Pi), in subdomain order. One CTA.
+/// (Pi, Pi). Thread per entry: the subdomains owning corner rp (pi_owner, ascending subdomain
+/// order), each adding its Gram entry against corner rq if it owns that corner too — the order
+/// of the serial subdomain loop this replaces, so the sums are bit-identical.
 __global__ void __launch_bounds__(256) coarse_gsum_kernel(BlockArgs a) {
-  const int n = a.n_pi;
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) a.Gsum[idx] = 0.0;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < a.N; ++i)
-      for (int p = 0; p < a.ncq; ++p) {
-        const int gp_ = a.corner_q[i * a.ncq + p];
-        if (gp_ < 0) continue;
-        const int rp = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gp_];
-        for (int q = 0; q < a.ncq; ++q) {
-          const int gq_ = a.corner_q[i * a.ncq + q];
-          if (gq_ < 0) continue;
-          const int rq = a.gamma_pi[static_cast<size_t>(i) * a.gmax + gq_];
-          a.Gsum[static_cast<size_t>(rp) * n + rq] += a.Gc[(static_cast<size_t>(i) * a.ncq + p) * a.ncq + q];
-        }
-      }
+  const int n = a.n_pi, ncq = a.ncq;
+  const long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long>(n) * n) return;
+  const int rp = static_cast<int>(idx / n), rq = static_cast<int>(idx % n);
+  double s = 0.0;
+  for (int k = 0; k < 4; ++k) {
+    const int own = a.pi_owner[rp * 4 + k];
+    if (own < 0) continue;
+    const int i = own / ncq, p = own % ncq;
+    for (int q = 0; q < ncq; ++q) {
+      const int g = a.corner_q[i * ncq + q];
+      if (g >= 0 && a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] == rq)
+        s += a.Gc[(static_cast<size_t>(i) * ncq + p) * ncq + q];
+    }
   }
+  a.Gsum[idx] = s;
 }
 
-/// S = diag(mult) + Dpp^T Dpp + Gsum; symmetrise; Cholesky; S^{-1}. One CTA.
-__global__ void __launch_bounds__(1024) coarse_schur_kernel(BlockArgs a) {
+/// L = S = sym(diag(mult) + Dpp^T Dpp + Gsum), entry per thread (each entry's arithmetic as in
+/// the single-CTA formation it replaces: the same dot order, the same symmetrisation).
+__global__ void __launch_bounds__(256) coarse_sform_kernel(BlockArgs a) {
   const int n = a.n_pi, npf = a.npf;
-  double* S = a.S;
-  double* L = a.Sinv;  // scratch for L, overwritten by the inverse at the end
+  const long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long>(n) * n) return;
+  const int p = static_cast<int>(idx / n), q = static_cast<int>(idx % n);
+  auto entry = [&](int x, int y) {
+    double s = 0;
+    for (int rr = 0; rr < npf; ++rr) s += a.Dpp[static_cast<size_t>(rr) * n + x] * a.Dpp[static_cast<size_t>(rr) * n + y];
+    double v = (x == y ? static_cast<double>(a.mult_pi[x]) : 0.0) + s;
+    v += a.Gsum[static_cast<size_t>(x) * n + y];
+    return v;
+  };
+  const double l = 0.5 * (entry(p, q) + entry(q, p));
+  a.Sinv[idx] = l;  // L (full), factored in place by coarse_chol_kernel
+  a.S[idx] = l;
+}
+
+/// Cholesky S = L L^T (right-looking, lower triangle) and L^{-1} by forward substitution (thread
+/// per column), one CTA. L lives packed (row i at i(i+1)/2) in shared memory when it fits, so the
+/// n sequential steps and the substitution chains read it at shared-memory latency; otherwise it
+/// is factored in place in global memory. L^{-1} goes to S, transposed.
+__global__ void __launch_bounds__(1024) coarse_chol_kernel(BlockArgs a, int packed) {
+  const int n = a.n_pi;
+  extern __shared__ double lp[];
+  double* Lg = a.Sinv;
   __shared__ int fail;
   if (threadIdx.x == 0) fail = 0;
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-    const int p = idx / n, q = idx % n;
-    double s = 0;
-    for (int rr = 0; rr < npf; ++rr) s += a.Dpp[static_cast<size_t>(rr) * n + p] * a.Dpp[static_cast<size_t>(rr) * n + q];
-    S[idx] = (p == q ? static_cast<double>(a.mult_pi[p]) : 0.0) + s;
-  }
+  auto at = [&](int i, int j) -> double& {
+    return packed ? lp[static_cast<size_t>(i) * (i + 1) / 2 + j] : Lg[static_cast<size_t>(i) * n + j];
+  };
+  if (packed)
+    for (int idx = threadIdx.x; idx < n * (n + 1) / 2; idx += blockDim.x) {
+      int i = static_cast<int>((sqrt(8.0 * idx + 1.0) - 1.0) / 2.0);
+      while (static_cast<long>(i) * (i + 1) / 2 > idx) --i;
+      while (static_cast<long>(i + 1) * (i + 2) / 2 <= idx) ++i;
+      const int j = idx - i * (i + 1) / 2;
+      lp[idx] = Lg[static_cast<size_t>(i) * n + j];
+    }
   __syncthreads();
-  // + sum_i Gpi rows (the corner Grams of every subdomain, summed by coarse_gsum_kernel and, when
-  //   sharded, all-reduced over the ranks)
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) S[idx] += a.Gsum[idx];
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-    const int p = idx / n, q = idx % n;
-    L[idx] = 0.5 * (S[static_cast<size_t>(p) * n + q] + S[static_cast<size_t>(q) * n + p]);
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) S[idx] = L[idx];
-  __syncthreads();
-  // right-looking Cholesky in L (lower triangle)
   for (int k = 0; k < n; ++k) {
     if (threadIdx.x == 0) {
-      const double dkk = L[static_cast<size_t>(k) * n + k];
+      const double dkk = at(k, k);
       if (!(dkk > 0)) fail = 1;
-      L[static_cast<size_t>(k) * n + k] = sqrt(fmax(dkk, DBL_MIN));
+      at(k, k) = sqrt(fmax(dkk, DBL_MIN));
     }
     __syncthreads();
-    const double dk = L[static_cast<size_t>(k) * n + k];
-    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) L[static_cast<size_t>(i) * n + k] /= dk;
+    const double dk = at(k, k);
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) at(i, k) /= dk;
     __syncthreads();
-    const int rem = n - k - 1;
-    for (int idx = threadIdx.x; idx < rem * rem; idx += blockDim.x) {
-      const int i = k + 1 + idx / rem, j = k + 1 + idx % rem;
-      if (j <= i) L[static_cast<size_t>(i) * n + j] -= L[static_cast<size_t>(i) * n + k] * L[static_cast<size_t>(j) * n + k];
+    // trailing update of the lower triangle: warp per row, lanes over the columns j <= i
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int i = k + 1 + warp; i < n; i += nwarp) {
+      const double lik = at(i, k);
+      for (int j = k + 1 + lane; j <= i; j += 32) at(i, j) -= lik * at(j, k);
     }
     __syncthreads();
   }
   if (threadIdx.x == 0 && fail) *a.spd_fail = 1;
-  // Linv (upper part of S scratch is free after the copy): column c of L^{-1} by forward subst.
-  double* Li = S;  // reuse S storage for L^{-1} (S itself is not needed after factorisation)
-  __syncthreads();
+  // column c of L^{-1}, stored transposed (LiT[c*n + i]) so every chain reads its own contiguous
+  // column; zero above the diagonal
+  double* LiT = a.S;
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    for (int i = 0; i < n; ++i) {
+    double* col = LiT + static_cast<size_t>(c) * n;
+    for (int i = 0; i < c; ++i) col[i] = 0.0;
+    for (int i = c; i < n; ++i) {
       double s = (i == c) ? 1.0 : 0.0;
-      if (i < c) { Li[static_cast<size_t>(i) * n + c] = 0.0; continue; }
-      for (int u = c; u < i; ++u) s -= L[static_cast<size_t>(i) * n + u] * Li[static_cast<size_t>(u) * n + c];
-      Li[static_cast<size_t>(i) * n + c] = s / L[static_cast<size_t>(i) * n + i];
+#pragma unroll 8
+      for (int u = c; u < i; ++u) s -= at(i, u) * col[u];
+      col[i] = s / at(i, i);
     }
   }
-  __syncthreads();
-  // S^{-1} = L^{-T} L^{-1}
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-    const int p = idx / n, q = idx % n;
-    double s = 0;
-    for (int u = max(p, q); u < n; ++u) s += Li[static_cast<size_t>(u) * n + p] * Li[static_cast<size_t>(u) * n + q];
-    L[idx] = s;
-  }
+}
+
+/// S^{-1} = L^{-T} L^{-1}, entry per thread.
+__global__ void __launch_bounds__(256) coarse_sinv_kernel(BlockArgs a) {
+  const int n = a.n_pi;
+  const long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long>(n) * n) return;
+  const int p = static_cast<int>(idx / n), q = static_cast<int>(idx % n);
+  const double* LiT = a.S;  // transposed L^{-1} (coarse_chol_kernel)
+  const double* lp = LiT + static_cast<size_t>(p) * n;
+  const double* lq = LiT + static_cast<size_t>(q) * n;
+  double s = 0;
+  for (int u = max(p, q); u < n; ++u) s += lp[u] * lq[u];
+  a.Sinv[idx] = s;
 }
 
 /// Coarse-solve rows used by the interface iteration (k_cg.cu): with z = [t; psi],
@@ -337,12 +362,28 @@ void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t s
 }
 
 void launch_coarse_gsum(const BlockArgs& a, cudaStream_t st) {
-  coarse_gsum_kernel<<<1, 256, 0, st>>>(a);
+  const long nn = static_cast<long>(a.n_pi) * a.n_pi;
+  coarse_gsum_kernel<<<static_cast<int>((nn + 255) / 256), 256, 0, st>>>(a);
   DDG_LAUNCH_CHECK();
 }
 
 void launch_coarse_schur(const BlockArgs& a, cudaStream_t st) {
-  coarse_schur_kernel<<<1, 1024, 0, st>>>(a);
+  const long nn = static_cast<long>(a.n_pi) * a.n_pi;
+  const int g = static_cast<int>((nn + 255) / 256);
+  coarse_sform_kernel<<<g, 256, 0, st>>>(a);
+  DDG_LAUNCH_CHECK();
+  static int optin = -1;
+  if (optin < 0) {
+    int dev = 0;
+    DDG_CUDA(cudaGetDevice(&dev));
+    DDG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    DDG_CUDA(cudaFuncSetAttribute(coarse_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+  }
+  const size_t packed = sizeof(double) * static_cast<size_t>(a.n_pi) * (a.n_pi + 1) / 2;
+  const bool fits = packed + 1024 <= static_cast<size_t>(optin);
+  coarse_chol_kernel<<<1, 1024, fits ? packed : 0, st>>>(a, fits ? 1 : 0);
+  DDG_LAUNCH_CHECK();
+  coarse_sinv_kernel<<<g, 256, 0, st>>>(a);
   DDG_LAUNCH_CHECK();
 }
 

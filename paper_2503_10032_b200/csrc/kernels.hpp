@@ -139,6 +139,7 @@ struct BlockArgs {
   int* spd_fail;         // 1 flag
   int flip_row;          // debug_flip_flux_row (global flux row) or -1
   const int* row_owner;  // npf x 4 : contributing (i * crmax + rho), subdomain order, -1 pad
+  const int* pi_owner;   // n_pi x 4 : corner owners (i * ncq + slot), subdomain order, -1 pad
 };
 void launch_blocks(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_local(const BlockArgs& a, const int* cr_row, const int* cr_off, const int* cr_l,

@@ -564,6 +564,7 @@ BlockArgs Workspace::block_args() {
   b.spd_fail = d_spd_fail.ptr;
   b.flip_row = p.debug_flip_flux_row;
   b.row_owner = d_row_owner.ptr;
+  b.pi_owner = d_pi_owner.ptr;
   return b;
 }
 
@@ -598,7 +599,7 @@ void Workspace::build_coarse() {
     xchg(d_Gsum.ptr, d_Gsum.ptr, static_cast<size_t>(plan.n_pi) * plan.n_pi);
     launch_coarse_schur(b, st_);
     launch_coarse_weights(b, st_);
-    launches_ += 5;
+    launches_ += 7;
   }
   DDG_CUDA(cudaEventRecord(ev_[5], st_));
   int fail = 0;
