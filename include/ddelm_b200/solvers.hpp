@@ -145,6 +145,18 @@ class Workspace {
     return out;
   }
 
+  /// apply_P / apply_PT, the Neumann map and its adjoint (solvers.cpp:450-474).
+  std::vector<double> apply_P(const std::vector<double>& v) {
+    std::vector<double> out(v.size());
+    detail::check(ddelm_gpu_apply_neumann(ws_.get(), 0, v.data(), out.data()));
+    return out;
+  }
+  std::vector<double> apply_PT(const std::vector<double>& u) {
+    std::vector<double> out(u.size());
+    detail::check(ddelm_gpu_apply_neumann(ws_.get(), 1, u.data(), out.data()));
+    return out;
+  }
+
   SolveReport solve(int method, double theta, const CgOptions& cg) {
     ddelm_report r{};
     detail::check(ddelm_gpu_solve(ws_.get(), method, theta, cg.rel_tol, cg.max_iter, &r));

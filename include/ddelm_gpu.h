@@ -151,6 +151,10 @@ int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double
 /* out = reduced_apply(v), the one-level operator (solvers.cpp:262-274); v, out: n_mu = n_delta +
  * n_pi host doubles. */
 int ddelm_gpu_apply_reduced(ddelm_ws* ws, const double* v, double* out);
+/* The Neumann map P = Abar Kbar^+ Bbar (transpose = 0, Workspace::apply_P) or its adjoint
+ * (transpose = 1, apply_PT), solvers.cpp:450-474: v, out n_delta host doubles. Builds the coarse
+ * and Neumann layers as needed. */
+int ddelm_gpu_apply_neumann(ddelm_ws* ws, int transpose, const double* v, double* out);
 /* dense_oracle_solve (solvers.cpp:609-709) on the device: the global block matrices K, B, A (and
  * Kbar, Bbar, Abar for NN) assembled densely, every pseudo-inverse through the device QR / COD
  * kernels with Eigen's default threshold eps * min(rows, cols). method: DDELM_METHOD_*; the

@@ -217,6 +217,18 @@ int ddo_apply_cs(void* p, double theta, const double* v, double* out) {
   return 0;
 }
 
+/// apply_P (transpose 0) / apply_PT (1), solvers.cpp:450-474; v, out: n_delta doubles.
+int ddo_apply_p(void* p, int transpose, const double* v, double* out) {
+  auto h = static_cast<ddo_handle*>(p);
+  Workspace& ws = *h->ws;
+  ws.assemble_coarse();
+  ws.build_neumann();
+  Vec in(v, v + ws.n_delta());
+  Vec o = transpose ? ws.apply_PT(in) : ws.apply_P(in);
+  std::copy(o.begin(), o.end(), out);
+  return 0;
+}
+
 /// reduced_apply(mu), the one-level operator (solvers.cpp:262-274); mu, out: n_mu doubles.
 int ddo_apply_reduced(void* p, const double* v, double* out) {
   auto h = static_cast<ddo_handle*>(p);

@@ -59,7 +59,7 @@ def lib():
                                 C.c_char_p, C.c_int]
         for name in ("ddo_info", "ddo_timings", "ddo_residuals", "ddo_mu", "ddo_coeffs",
                      "ddo_ranks", "ddo_layer", "ddo_local", "ddo_kbar", "ddo_field",
-                     "ddo_field_of", "ddo_errors", "ddo_apply_cs", "ddo_apply_reduced", "ddo_dense"):
+                     "ddo_field_of", "ddo_errors", "ddo_apply_cs", "ddo_apply_reduced", "ddo_dense", "ddo_apply_p"):
             getattr(L, name).argtypes = None  # variadic pointer args, set per call
         _lib = L
     return _lib
@@ -178,6 +178,13 @@ class OracleWorkspace:
         v = np.ascontiguousarray(v, dtype=np.float64)
         out = np.zeros_like(v)
         lib().ddo_apply_cs(C.c_void_p(self.h), C.c_double(theta), _p(v), _p(out))
+        return out
+
+    def apply_p(self, v, transpose=False):
+        """apply_P / apply_PT (solvers.cpp:450-474)."""
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.zeros_like(v)
+        lib().ddo_apply_p(C.c_void_p(self.h), C.c_int(1 if transpose else 0), _p(v), _p(out))
         return out
 
     def apply_reduced(self, v):

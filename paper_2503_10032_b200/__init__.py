@@ -42,7 +42,8 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_lsq_get_block", "ddelm_gpu_lsq_ld", "ddelm_gpu_lsq_destroy",
            "ddelm_gpu_nccl_unique_id", "ddelm_gpu_create_sharded", "ddelm_gpu_get_shard",
            "ddelm_gpu_plan_tables", "ddelm_gpu_sample_field", "ddelm_gpu_relative_errors",
-           "ddelm_gpu_field_diff", "ddelm_gpu_apply_reduced", "ddelm_gpu_dense_oracle")
+           "ddelm_gpu_field_diff", "ddelm_gpu_apply_reduced", "ddelm_gpu_dense_oracle",
+           "ddelm_gpu_apply_neumann")
 
 
 class _Desc(C.Structure):
@@ -95,6 +96,7 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_apply_operator.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_apply_reduced.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_invalidate.argtypes = [C.c_void_p]
+    L.ddelm_gpu_apply_neumann.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_dense_oracle.argtypes = [C.c_void_p, C.c_int, C.c_double, C.POINTER(C.c_int), C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_stream.argtypes = [C.c_void_p]
@@ -361,6 +363,21 @@ class Workspace:
         v = np.ascontiguousarray(v, dtype=np.float64)
         out = np.zeros_like(v)
         _check(load_library().ddelm_gpu_apply_reduced(self._h, _ptr(v), _ptr(out)))
+        return out
+
+    def apply_P(self, v: np.ndarray) -> np.ndarray:
+        """The Neumann map P = Abar Kbar^+ Bbar on n_delta values (Workspace::apply_P,
+        solvers.cpp:450-461), through the device NN1 phase."""
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.zeros_like(v)
+        _check(load_library().ddelm_gpu_apply_neumann(self._h, 0, _ptr(v), _ptr(out)))
+        return out
+
+    def apply_PT(self, u: np.ndarray) -> np.ndarray:
+        """The adjoint P^T (Workspace::apply_PT, solvers.cpp:463-474), through the NN2 phase."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros_like(u)
+        _check(load_library().ddelm_gpu_apply_neumann(self._h, 1, _ptr(u), _ptr(out)))
         return out
 
     def _solve(self, method: str, theta: float, cg: CgOptions | None, fetch: bool = True) -> SolveReport:

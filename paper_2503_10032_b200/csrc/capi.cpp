@@ -293,6 +293,9 @@ int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double
 int ddelm_gpu_apply_reduced(ddelm_ws* ws, const double* v, double* out) {
   return guarded([&] { ws->w->apply_reduced(v, out); });
 }
+int ddelm_gpu_apply_neumann(ddelm_ws* ws, int transpose, const double* v, double* out) {
+  return guarded([&] { ws->w->apply_neumann(transpose, v, out); });
+}
 int ddelm_gpu_dense_oracle(ddelm_ws* ws, int method, double theta, int* dim, double* reduced_op,
                            double* reduced_rhs, double* mu_full, double* coeffs) {
   return guarded([&] {

@@ -1562,6 +1562,26 @@ void cg_launch(const CgArgs& a, int job, const double* vin, double* vout, cudaSt
   DDG_CUDA(cudaLaunchCooperativeKernel(kernel_for(a), dim3(G), dim3(kThreads), params, sm, st));
 }
 
+namespace {
+/// apply_P / apply_PT (solvers.cpp:450-474) through the NN1 / NN2 phases: op 0 places v as the
+/// gathered flux values NN1 reads (part 0, first owner slot; the debug flip cancels), op 1 places
+/// u as the gathered P x NN2 reads, op 2 gathers P v from NN1's owner slots, op 3 gathers
+/// -(zz) = P^T u from NN2's (the sign OP3 applies, solvers.cpp:473).
+__global__ void neumann_io_kernel(CgArgs a, int op, const double* v, double* out) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.n_delta; g += gridDim.x * blockDim.x) {
+    if (op == 0) a.xtab[2 * static_cast<size_t>(g)] = a.flip_sign[g] * v[g];
+    else if (op == 1) a.trtab[2 * static_cast<size_t>(g)] = v[g];
+    else if (op == 2) out[g] = gather_delta(a.trtab, a, g);
+    else out[g] = -gather_delta(a.zztab, a, g);
+  }
+}
+}  // namespace
+
+void cg_launch_neumann_io(const CgArgs& a, int op, const double* v, double* out, cudaStream_t st) {
+  neumann_io_kernel<<<ceil_div(std::max(a.n_delta, 1), 256), 256, 0, st>>>(a, op, v, out);
+  DDG_LAUNCH_CHECK();
+}
+
 void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double* vin, double* vout,
                      cudaStream_t st) {
   cg_check_capacity(a);

@@ -262,6 +262,8 @@ void cg_launch(const CgArgs& a, int job, const double* vin, double* vout, cudaSt
 /// Phase-by-phase execution (sharded mode: an all-reduce of the owner-slot tables between phases)
 enum CgPhase { kPhOp1 = 0, kPhOp2, kPhNn1, kPhNn2, kPhOp3, kPhOp4, kPhXr1, kPhXr2, kPhGather };
 /// mode: 0 operator / CG, 1 reduced rhs, 2 reconstruction; it: CG iteration (1-based, CG only)
+/// apply_P / apply_PT staging around the NN1 / NN2 phases (see k_cg.cu neumann_io_kernel)
+void cg_launch_neumann_io(const CgArgs& a, int op, const double* v, double* out, cudaStream_t st);
 void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double* vin, double* vout,
                      cudaStream_t st);
 void cg_launch_init(const CgArgs& a, cudaStream_t st);

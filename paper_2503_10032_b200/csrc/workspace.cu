@@ -991,6 +991,36 @@ void Workspace::apply_reduced(const double* v, double* out) {
   DDG_CUDA(cudaStreamSynchronize(st_));
 }
 
+void Workspace::apply_neumann(int transpose, const double* v, double* out) {
+  // apply_P / apply_PT (solvers.cpp:450-474): one NN1 (resp. NN2) phase between two staging
+  // launches; the owner-slot tables are all-reduced in between like in the CG iteration
+  DDG_CUDA(cudaSetDevice(device_));
+  if (!phased_) throw std::invalid_argument("apply_P: needs the phase-by-phase driver");
+  if (!built_) build();
+  build_coarse();
+  build_neumann();
+  CgArgs a = cg_args(1.0, 1e-9, 1);
+  apply_l2_policy();
+  const size_t nd = plan.n_delta, tab = static_cast<size_t>(a.P) * 2 * nd;
+  DDG_CUDA(cudaMemcpyAsync(d_vin.ptr, v, nd * sizeof(double), cudaMemcpyHostToDevice, st_));
+  if (!transpose) {
+    DDG_CUDA(cudaMemsetAsync(a.xtab, 0, tab * sizeof(double), st_));
+    cg_launch_neumann_io(a, 0, d_vin.ptr, nullptr, st_);
+    cg_launch_phase(a, kPhNn1, 0, 0, nullptr, nullptr, st_);
+    xchg(a.trtab_w, a.trtab, tab);
+    cg_launch_neumann_io(a, 2, nullptr, d_vout.ptr, st_);
+  } else {
+    DDG_CUDA(cudaMemsetAsync(a.trtab, 0, tab * sizeof(double), st_));
+    cg_launch_neumann_io(a, 1, d_vin.ptr, nullptr, st_);
+    cg_launch_phase(a, kPhNn2, 0, 0, nullptr, nullptr, st_);
+    xchg(a.zztab_w, a.zztab, tab);
+    cg_launch_neumann_io(a, 3, nullptr, d_vout.ptr, st_);
+  }
+  launches_ += 3;
+  DDG_CUDA(cudaMemcpyAsync(out, d_vout.ptr, nd * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  DDG_CUDA(cudaStreamSynchronize(st_));
+}
+
 void Workspace::xchg(double* send, double* recv, size_t n) {
   if (ex_ && n) ex_->allreduce(send, recv, n, st_);
 }

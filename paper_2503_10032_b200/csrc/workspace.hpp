@@ -92,6 +92,8 @@ class Workspace {
   void invalidate() { built_ = blocks_built_ = coarse_built_ = neumann_built_ = false; }
   void apply_operator(double theta, const double* v, double* out);
   void apply_reduced(const double* v, double* out);
+  /// the Neumann map P (transpose = 0) or its adjoint P^T (solvers.cpp:450-474) on n_delta doubles
+  void apply_neumann(int transpose, const double* v, double* out);
   void set_profiling(bool on) { profiling_ = on; }
   bool kernel_stat(const std::string& name, KernelStat* out) const;
   double device_span_ms() const { return device_span_ms_; }

@@ -101,3 +101,15 @@ def test_dense_oracle_restatement_matches_iterative_solve():
     w = OracleWorkspace(s=4, n_grid=16, M=200, l=8.0)
     with pytest.raises(ValueError):
         w.dense("ddelm-nn", 0.999)
+
+
+def test_oracle_neumann_map_adjoint():
+    """The oracle's apply_P / apply_PT (the checker of tests/test_gpu_neumann.py) are adjoint
+    (test_solvers.cpp:164-182)."""
+    from oracle.pyoracle import OracleWorkspace
+    w = OracleWorkspace(s=2, n_grid=10, M=64, l=8.0)
+    nd = int(w.info()[1])
+    rng = np.random.default_rng(19)
+    u, v = rng.standard_normal(nd), rng.standard_normal(nd)
+    pv, ptu = w.apply_p(v), w.apply_p(u, transpose=True)
+    assert abs(pv @ u - v @ ptu) <= 1e-10 * np.linalg.norm(pv) * np.linalg.norm(u)
