@@ -64,6 +64,7 @@ struct SolverOptions {  // solvers.hpp:49-58
   int workers = 1;  // accepted for API parity; the device batches all subdomains
   int debug_flip_flux_row = -1;
   int device = 0;   // CUDA device ordinal (device-path addition)
+  int cg_blocks = DDELM_CG_BLOCKS_COEFF;  // CG operator representation (device-path addition)
 };
 
 struct CgOptions {  // solvers.hpp:173-176
@@ -120,6 +121,7 @@ class Workspace {
     ddelm_ws* w = nullptr;
     detail::check(ddelm_gpu_create(&d, &w));
     ws_.reset(w);
+    detail::check(ddelm_gpu_set_cg_blocks(w, opts.cg_blocks));
   }
 
   int n_subs() const { return s_ * s_; }

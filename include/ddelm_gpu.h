@@ -119,6 +119,16 @@ int ddelm_gpu_solve(ddelm_ws* ws, int method, double theta, double rel_tol, int 
 /* Re-seed the feature layers (seed + i per subdomain) and invalidate every built layer;
  * the geometry / index plan is kept. */
 int ddelm_gpu_reseed(ddelm_ws* ws, uint64_t seed);
+/* Operator representation of the interface iteration (no reference counterpart):
+ * DDELM_CG_BLOCKS_COEFF (default) streams the coefficient-space blocks every iteration in the
+ * reference's grouping (c = K^+ phi, then F c: solvers.cpp:215-218, 455, 468), which reproduces
+ * its finite-precision CG trajectory; DDELM_CG_BLOCKS_COMPACT folds the M-long coefficient
+ * contraction into precomputed interface-level blocks F [C Ypi] and Cdelta Cbar once per build
+ * (about 10x less traffic per iteration; the same operator in exact arithmetic, but CG then
+ * follows a different round-off trajectory and typically converges in fewer iterations). */
+#define DDELM_CG_BLOCKS_COEFF 0
+#define DDELM_CG_BLOCKS_COMPACT 1
+int ddelm_gpu_set_cg_blocks(ddelm_ws* ws, int mode);
 void ddelm_gpu_destroy(ddelm_ws* ws);
 
 /* Results of the last solve (host buffers, caller allocated). */

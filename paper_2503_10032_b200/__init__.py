@@ -43,7 +43,7 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_nccl_unique_id", "ddelm_gpu_create_sharded", "ddelm_gpu_get_shard",
            "ddelm_gpu_plan_tables", "ddelm_gpu_sample_field", "ddelm_gpu_relative_errors",
            "ddelm_gpu_field_diff", "ddelm_gpu_apply_reduced", "ddelm_gpu_dense_oracle",
-           "ddelm_gpu_apply_neumann")
+           "ddelm_gpu_apply_neumann", "ddelm_gpu_set_cg_blocks")
 
 
 class _Desc(C.Structure):
@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_solve.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int,
                                   C.POINTER(_Report)]
     L.ddelm_gpu_reseed.argtypes = [C.c_void_p, C.c_uint64]
+    L.ddelm_gpu_set_cg_blocks.argtypes = [C.c_void_p, C.c_int]
     L.ddelm_gpu_destroy.argtypes = [C.c_void_p]
     L.ddelm_gpu_get_mu.argtypes = [C.c_void_p, C.c_void_p]
     L.ddelm_gpu_get_coeffs.argtypes = [C.c_void_p, C.c_void_p]
@@ -289,6 +290,13 @@ class Workspace:
     def reseed(self, seed: int):
         _check(load_library().ddelm_gpu_reseed(self._h, seed))
         self.seed = seed
+
+    def set_cg_blocks(self, mode: str):
+        """'coeff' (default: the reference's grouping, its CG trajectory) or 'compact'
+        (precomputed interface-level blocks; include/ddelm_gpu.h ddelm_gpu_set_cg_blocks)."""
+        code = {"coeff": 0, "compact": 1}[mode]
+        _check(load_library().ddelm_gpu_set_cg_blocks(self._h, code))
+        self.cg_blocks = mode
 
     def ranks(self):
         N = self.n_subs
@@ -545,9 +553,12 @@ def workspace_from_config(name_or_cfg, device: int = 0, shard: tuple | None = No
                      shard)
 
 
-def solve_config(name_or_cfg, device: int = 0, ws: Workspace | None = None) -> tuple[Workspace, SolveReport]:
+def solve_config(name_or_cfg, device: int = 0, ws: Workspace | None = None,
+                 cg_blocks: str | None = None) -> tuple[Workspace, SolveReport]:
     cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
     ws = ws or workspace_from_config(cfg, device)
+    if cg_blocks is not None:
+        ws.set_cg_blocks(cg_blocks)
     cg = CgOptions(rel_tol=cfg["cg_rel_tol"])
     if cfg["method"] == "ddelm-cs":
         return ws, ddelm_cs_solve(ws, cg)

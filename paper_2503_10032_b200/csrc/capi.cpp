@@ -195,6 +195,14 @@ int ddelm_gpu_reseed(ddelm_ws* ws, uint64_t seed) {
   return guarded([&] { ws->w->reseed(seed); });
 }
 
+int ddelm_gpu_set_cg_blocks(ddelm_ws* ws, int mode) {
+  return guarded([&] {
+    if (mode != DDELM_CG_BLOCKS_COEFF && mode != DDELM_CG_BLOCKS_COMPACT)
+      throw std::invalid_argument("set_cg_blocks: mode must be DDELM_CG_BLOCKS_COEFF or DDELM_CG_BLOCKS_COMPACT");
+    ws->w->cg_compact = mode;
+  });
+}
+
 int ddelm_gpu_solve(ddelm_ws* ws, int method, double theta, double rel_tol, int max_iter,
                     ddelm_report* rep) {
   return guarded([&] {

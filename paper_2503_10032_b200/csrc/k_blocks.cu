@@ -414,12 +414,96 @@ __global__ void pack_streams_kernel(BlockArgs a, double* KF, const int* kf_ld, c
     }
   }
 }
+/// Compact interface-level stream block of one packed block P (M rows, stride ld): row q of the
+/// output (same stride) holds the unit vector e_{c(q)} in columns [0, boff) and, in columns
+/// [boff, boff + nb), the contraction  sum_j P[j][c(q)] P[j][boff + l]  — i.e. (F C)^T, (F Ypi)^T
+/// (KF: c(q) = q for q < r, R + q - r for the ncq Ypi columns) and (Cdelta Cbar)^T (KD). The
+/// M-long coefficient-space contraction of every CG phase (solvers.cpp:215-218, 455, 468) is then
+/// done once here instead of once per iteration. DFMA tiles, fixed j order (deterministic).
+__global__ void __launch_bounds__(256) compact_stream_kernel(int M, int R, int ncq, const double* P,
+                                                             const int* ld_of, const long long* off_of,
+                                                             double* out, const long long* oout_of,
+                                                             const int* rank, int rank_off, int nb_kind,
+                                                             const ClassDims* dims, const int* sub_cls) {
+  const int i = blockIdx.z;
+  const ClassDims d = dims[sub_cls[i]];
+  const int r = rank[rank_off + i];
+  const int nq = r + (nb_kind == 0 ? ncq : 0);            // output rows
+  const int boff = nb_kind == 0 ? R + ncq : R;
+  const int nb = nb_kind == 0 ? d.nF : d.nd;
+  const int ld = ld_of[i];
+  const double* Pi = P + off_of[i];
+  double* o = out + oout_of[i];
+  const int q0 = blockIdx.x * 64, l0 = blockIdx.y * 64;
+  if (q0 >= nq) return;
+  auto col = [&](int q) { return q < r ? q : R + (q - r); };
+  if (blockIdx.y == 0)  // identity part of the tile's rows (and the zero tail past boff + nb)
+    for (int idx = threadIdx.x; idx < 64 * boff; idx += 256) {
+      const int qq = idx / boff, c = idx % boff, q = q0 + qq;
+      if (q < nq) o[static_cast<size_t>(q) * ld + c] = (c == col(q)) ? 1.0 : 0.0;
+    }
+  if (blockIdx.y == 0)
+    for (int idx = threadIdx.x; idx < 64 * (ld - boff - nb); idx += 256) {
+      const int w = ld - boff - nb, qq = idx / w, c = boff + nb + idx % w, q = q0 + qq;
+      if (q < nq) o[static_cast<size_t>(q) * ld + c] = 0.0;
+    }
+  if (l0 >= nb) return;
+  __shared__ double Xs[16][64];
+  __shared__ double Ys[16][64];
+  const int tq = (threadIdx.x & 15) * 4, tl = (threadIdx.x >> 4) * 4;
+  double acc[4][4] = {};
+  for (int j0 = 0; j0 < M; j0 += 16) {
+    for (int idx = threadIdx.x; idx < 16 * 64; idx += 256) {
+      const int jj = idx / 64, c = idx % 64;
+      const int j = j0 + jj;
+      const double* row = Pi + static_cast<size_t>(j) * ld;
+      Xs[jj][c] = (j < M && q0 + c < nq) ? row[col(q0 + c)] : 0.0;
+      Ys[jj][c] = (j < M && l0 + c < nb) ? row[boff + l0 + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      double xv[4], yv[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        xv[p] = Xs[jj][tq + p];
+        yv[p] = Ys[jj][tl + p];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(xv[p], yv[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int qq = q0 + tq + p, l = l0 + tl + q;
+      if (qq < nq && l < nb) o[static_cast<size_t>(qq) * ld + boff + l] = acc[p][q];
+    }
+}
 }  // namespace
 
 void launch_pack_streams(const BlockArgs& a, double* KF, const int* kf_ld, const long long* kf_off, double* KD,
                          const int* kd_ld, const long long* kd_off, cudaStream_t st) {
   dim3 g(std::min(a.M, 64), a.N);
   pack_streams_kernel<<<g, 256, 0, st>>>(a, KF, kf_ld, kf_off, KD, kd_ld, kd_off);
+  DDG_LAUNCH_CHECK();
+}
+
+void launch_compact_streams(const BlockArgs& a, const double* KF, const int* kf_ld, const long long* kf_off,
+                            const double* KD, const int* kd_ld, const long long* kd_off, double* KFc,
+                            const long long* kfc_off, double* KDc, const long long* kdc_off, cudaStream_t st) {
+  const int R = a.rmax;
+  dim3 gf((R + a.ncq + 63) / 64, (a.fmax + 63) / 64, a.N);
+  compact_stream_kernel<<<gf, 256, 0, st>>>(a.M, R, a.ncq, KF, kf_ld, kf_off, KFc, kfc_off, a.rank, 0, 0, a.dims,
+                                            a.sub_cls);
+  DDG_LAUNCH_CHECK();
+  dim3 gd((R + 63) / 64, (std::max(a.dmax, 1) + 63) / 64, a.N);
+  compact_stream_kernel<<<gd, 256, 0, st>>>(a.M, R, a.ncq, KD, kd_ld, kd_off, KDc, kdc_off, a.rank, a.N, 1, a.dims,
+                                            a.sub_cls);
   DDG_LAUNCH_CHECK();
 }
 

@@ -160,10 +160,10 @@ struct ItemGeo {
   bool reverse;
 };
 
-__device__ __forceinline__ void part_rows(const CgArgs& a, int p, int& j0, int& j1) {
-  const int chunk = (a.M + a.P - 1) / a.P;
-  j0 = min(a.M, p * chunk);
-  j1 = min(a.M, j0 + chunk);
+__device__ __forceinline__ void part_rows(int rows, int P, int p, int& j0, int& j1) {
+  const int chunk = (rows + P - 1) / P;
+  j0 = min(rows, p * chunk);
+  j1 = min(rows, j0 + chunk);
 }
 
 /// rows per chunk: a multiple of the consumer warp count when it fits a stage (one row per warp)
@@ -174,27 +174,45 @@ __host__ __device__ __forceinline__ int rows_per_chunk(int ld) {
 }
 
 __device__ __forceinline__ ItemGeo item_geo(const CgArgs& a, int kind, int i, int p, bool recon) {
-  int j0, j1;
-  part_rows(a, p, j0, j1);
   const SubGeo d = a.geo[i];
   const int R = a.rmax;
   const int ldf = d.kf_ld, ldd = d.kd_ld;
-  const double* KF = a.KF + d.kf_off + static_cast<size_t>(j0) * ldf;
-  const double* KD = a.KD + d.kd_off + static_cast<size_t>(j0) * ldd;
   ItemGeo g;
-  switch (kind) {
-    case kOp2:  // A = C, Y = Ypi, B = F
-      g = {KF, ldf, 0, recon ? -1 : R + a.ncq, R, j1 - j0, d.r, recon ? 0 : d.nF, 0, 0, false};
-      break;
-    case kNn1:  // A = Cbar, B = Cdelta
-      g = {KD, ldd, 0, R, -1, j1 - j0, d.rb, d.nd, 0, 0, false};
-      break;
-    case kNn2:  // A = Cdelta, B = Cbar
-      g = {KD, ldd, R, 0, -1, j1 - j0, d.nd, d.rb, 0, 0, true};
-      break;
-    default:    // OP3: A = F, B = C
-      g = {KF, ldf, R + a.ncq, 0, -1, j1 - j0, d.nF, d.r, 0, 0, true};
-      break;
+  if (a.compact && !recon) {
+    // compact interface-level blocks (k_blocks.cu compact_stream_kernel): row q of KFc is
+    // [e_q (rmax) | e_(q-r) (ncq) | (F [C Ypi])^T row q], row q of KDc is [e_q | (Cdelta Cbar)^T row q],
+    // so the same row-dot / axpy machinery applies F C s - F Ypi mu (OP2), C^T F^T w (OP3), and
+    // Cdelta Cbar v / Cbar^T Cdelta^T v (NN1 / NN2) without the M-long coefficient vector
+    const int rows = kind == kOp2 ? d.r + a.ncq : (kind == kOp3 ? d.r : d.rb);
+    int j0, j1;
+    part_rows(rows, a.P, p, j0, j1);
+    const double* KF = a.KFc + d.kfc_off + static_cast<size_t>(j0) * ldf;
+    const double* KD = a.KDc + d.kdc_off + static_cast<size_t>(j0) * ldd;
+    switch (kind) {
+      case kOp2:  g = {KF, ldf, 0, R + a.ncq, R, j1 - j0, d.r, d.nF, 0, 0, false}; break;
+      case kNn1:  g = {KD, ldd, 0, R, -1, j1 - j0, d.rb, d.nd, 0, 0, false}; break;
+      case kNn2:  g = {KD, ldd, R, 0, -1, j1 - j0, d.nd, d.rb, 0, 0, true}; break;
+      default:    g = {KF, ldf, R + a.ncq, 0, -1, j1 - j0, d.nF, d.r, 0, 0, true}; break;
+    }
+  } else {
+    int j0, j1;
+    part_rows(a.M, a.P, p, j0, j1);
+    const double* KF = a.KF + d.kf_off + static_cast<size_t>(j0) * ldf;
+    const double* KD = a.KD + d.kd_off + static_cast<size_t>(j0) * ldd;
+    switch (kind) {
+      case kOp2:  // A = C, Y = Ypi, B = F
+        g = {KF, ldf, 0, recon ? -1 : R + a.ncq, R, j1 - j0, d.r, recon ? 0 : d.nF, 0, 0, false};
+        break;
+      case kNn1:  // A = Cbar, B = Cdelta
+        g = {KD, ldd, 0, R, -1, j1 - j0, d.rb, d.nd, 0, 0, false};
+        break;
+      case kNn2:  // A = Cdelta, B = Cbar
+        g = {KD, ldd, R, 0, -1, j1 - j0, d.nd, d.rb, 0, 0, true};
+        break;
+      default:    // OP3: A = F, B = C
+        g = {KF, ldf, R + a.ncq, 0, -1, j1 - j0, d.nF, d.r, 0, 0, true};
+        break;
+    }
   }
   g.rpc = rows_per_chunk(g.ld);
   g.nch = (g.rows + g.rpc - 1) / g.rpc;
@@ -803,7 +821,7 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
     cons_sync();
     const ItemGeo g = item_geo(a, kOp2, i, p, mode == 2);
     int j0, j1;
-    part_rows(a, p, j0, j1);
+    part_rows(a.M, a.P, p, j0, j1);
     double* coef = a.coeffs + static_cast<size_t>(i) * a.M;
     const double m0 = muc[0], m1 = muc[1], m2 = muc[2], m3 = muc[3];
     const int ncq = a.ncq;

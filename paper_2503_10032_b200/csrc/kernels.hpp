@@ -151,6 +151,11 @@ void launch_coarse_weights(const BlockArgs& a, cudaStream_t st);
 /// Pack the CG stream blocks KF = [C | Ypi | F] and KD = [Cbar | Cdelta] (row-interleaved).
 void launch_pack_streams(const BlockArgs& a, double* KF, const int* kf_ld, const long long* kf_off, double* KD,
                          const int* kd_ld, const long long* kd_off, cudaStream_t st);
+/// Compact interface-level stream blocks (same strides): KFc rows [e_q | (F [C Ypi])^T row q],
+/// KDc rows [e_q | (Cdelta Cbar)^T row q] (k_blocks.cu compact_stream_kernel).
+void launch_compact_streams(const BlockArgs& a, const double* KF, const int* kf_ld, const long long* kf_off,
+                            const double* KD, const int* kd_ld, const long long* kd_off, double* KFc,
+                            const long long* kfc_off, double* KDc, const long long* kdc_off, cudaStream_t st);
 
 // ---------------------------------------------------------------- C5 microbenchmark (k_lsq.cu)
 struct LsqArgs {
@@ -167,6 +172,7 @@ void launch_lsq_gram(const LsqArgs& a, cudaStream_t st);
 struct SubGeo {
   int n_gamma, nF, nd, r, rb, kf_ld, kd_ld, pad;
   long long kf_off, kd_off;
+  long long kfc_off, kdc_off;  // compact blocks (KFc: r + ncq rows, KDc: rb rows; strides kf_ld / kd_ld)
 };
 enum CgJob { kJobCg = 0, kJobApply = 1, kJobRhs = 2, kJobRecon = 3 };
 
@@ -182,6 +188,11 @@ struct CgArgs {
   int ldKF;                 // widest row (capacity); per subdomain: kf_ld[i], block at KF + kf_off[i]
   const double* KD;
   int ldKD;
+  // compact interface-level blocks (CG phases outside the reconstruction): the M-long
+  // coefficient contraction folded in at setup, rows q < r (+ ncq Ypi rows for KFc)
+  const double* KFc;
+  const double* KDc;
+  int compact;
   const int* kf_ld;
   const int* kd_ld;
   const long long* kf_off;

@@ -642,9 +642,29 @@ void Workspace::pack_blocks(const BlockArgs& b) {
     }
     d_KF.alloc(static_cast<size_t>(of));
     d_KD.alloc(static_cast<size_t>(od));
+    // compact blocks: r_i + ncq rows of KFc, rb_i rows of KDc, same per-subdomain strides
+    std::vector<long long> kfco(plan.N), kdco(plan.N);
+    long long ofc = 0, odc = 0;
+    for (int i = 0; i < plan.N; ++i) {
+      kfco[i] = ofc;
+      kdco[i] = odc;
+      ofc += static_cast<long long>(h_rank[i] + plan.ncq) * kfl[i];
+      odc += static_cast<long long>(h_rank[plan.N + i]) * kdl[i];
+    }
+    h_kfc_off_ = kfco;
+    h_kdc_off_ = kdco;
+    {
+      ArenaScope hot(&arena_);
+      d_kfc_off.upload(kfco, st_);
+      d_kdc_off.upload(kdco, st_);
+    }
+    d_KFc.alloc(static_cast<size_t>(std::max(ofc, 2LL)));
+    d_KDc.alloc(static_cast<size_t>(std::max(odc, 2LL)));
   }
   launch_pack_streams(b, d_KF.ptr, d_kf_ld.ptr, d_kf_off.ptr, d_KD.ptr, d_kd_ld.ptr, d_kd_off.ptr, st_);
-  launches_ += 1;
+  launch_compact_streams(b, d_KF.ptr, d_kf_ld.ptr, d_kf_off.ptr, d_KD.ptr, d_kd_ld.ptr, d_kd_off.ptr, d_KFc.ptr,
+                         d_kfc_off.ptr, d_KDc.ptr, d_kdc_off.ptr, st_);
+  launches_ += 3;
 }
 
 void Workspace::build_neumann() {
@@ -685,6 +705,9 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.kd_ld = d_kd_ld.ptr;
   a.kf_off = d_kf_off.ptr;
   a.kd_off = d_kd_off.ptr;
+  a.KFc = d_KFc.ptr;
+  a.KDc = d_KDc.ptr;
+  a.compact = cg_compact;  // ddelm_gpu_set_cg_blocks
   {
     // row parts per subdomain so that N * P work items cover the SMs (DDELM_CG_PARTS overrides)
     int dev = 0, sms = 148;
@@ -736,7 +759,7 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
     for (int i = 0; i < p.N; ++i) {
       const ClassPlan& c = p.classes[p.subs[i].cls];
       geo[i] = SubGeo{c.n_gamma, c.nF, c.nd, h_rank[i], h_rank[p.N + i], h_kf_ld_[i], h_kd_ld_[i], 0,
-                      h_kf_off_[i], h_kd_off_[i]};
+                      h_kf_off_[i], h_kd_off_[i], h_kfc_off_[i], h_kdc_off_[i]};
     }
     ArenaScope hot(&arena_);
     d_geo.upload(geo, st_);

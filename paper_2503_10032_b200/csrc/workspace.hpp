@@ -88,6 +88,7 @@ class Workspace {
   void build_neumann();
   SolveResult solve(int method, double theta, double tol, int max_iter);
   void reseed(uint64_t seed);
+  int cg_compact = 0;  // DDELM_CG_BLOCKS_* (CG operator representation)
   /// drop every built layer but keep the uploaded feature layers (device-resident inputs)
   void invalidate() { built_ = blocks_built_ = coarse_built_ = neumann_built_ = false; }
   void apply_operator(double theta, const double* v, double* out);
@@ -180,7 +181,7 @@ class Workspace {
   DevBuf<ClassDims> d_dims;
   DevBuf<SubGeo> d_geo;
   std::vector<int> h_kf_ld_, h_kd_ld_;
-  std::vector<long long> h_kf_off_, h_kd_off_;
+  std::vector<long long> h_kf_off_, h_kd_off_, h_kfc_off_, h_kdc_off_;
   DevBuf<double> d_cr_w, d_flip, d_f, d_coef;
   // layers and matrices
   DevBuf<double> d_w0, d_w1, d_b, d_A, d_tau, d_T, d_ratio, d_F, d_Cd;
@@ -188,7 +189,8 @@ class Workspace {
   DevBuf<double> d_V1, d_F1, d_Rr, d_tau1, d_zc, d_upd, d_dir, d_C, d_Y, d_QtX;
   // interface blocks / coarse
   DevBuf<int> d_kf_ld, d_kd_ld;
-  DevBuf<long long> d_kf_off, d_kd_off;
+  DevBuf<long long> d_kf_off, d_kd_off, d_kfc_off, d_kdc_off;
+  DevBuf<double> d_KFc, d_KDc;  // compact interface-level stream blocks (k_blocks.cu)
   DevBuf<double> d_FC, d_Zc, d_pd, d_Gc, d_Ypi, d_Dpp, d_dpi, d_S, d_Sinv, d_Wmu, d_Wd, d_W3;
   // CG
   DevBuf<double> d_x, d_r, d_p, d_Ap, d_rhs, d_partial, d_scal, d_hist, d_mu_pi_out, d_tpart, d_tpart3,

@@ -8,6 +8,8 @@ import paper_2503_10032_b200 as P  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 ws = P.workspace_from_config(name)
+if os.environ.get("CG_BLOCKS"):
+    ws.set_cg_blocks(os.environ["CG_BLOCKS"])
 for k in range(reps):
     if k:
         ws.reseed(P.CONFIGS[name]["seed"])
