@@ -351,6 +351,44 @@ def run_ours(args, cfg, world, rank, local, dist):
                     "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["bytes"] else None}
                 for k, v in fam.items()}
 
+    # ---- the same solve with the compact interface-level CG blocks (ddelm_gpu_set_cg_blocks):
+    # same operator in exact arithmetic, another CG round-off trajectory
+    compact = None
+    if not args.no_compact:
+        ws.set_cg_blocks("compact")
+        for _ in range(2):
+            ws.invalidate()
+            solve(fetch=False)
+        barrier(dist)
+        torch.cuda.synchronize()
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        citers = []
+        for _ in range(args.steps):
+            ws.invalidate()
+            crep = solve(fetch=False)
+            citers.append(crep.iterations)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        barrier(dist)
+        cms = max_over_ranks(dist, c0.elapsed_time(c1)) / args.steps
+        t0.record(stream)
+        for _ in range(args.steps):
+            ws.reseed(seed)
+            crep = solve()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier(dist)
+        cms_e2e = max_over_ranks(dist, t0.elapsed_time(t1)) / args.steps
+        compact = {"value": nsub / (cms / 1e3), "unit": "subdomains/s", "ms_per_step": cms,
+                   "iterations": citers, "e2e": {"value": nsub / (cms_e2e / 1e3), "unit": "subdomains/s",
+                                                 "ms_per_step": cms_e2e},
+                   "phase_ms": {k: round(v, 3) for k, v in crep.phase_ms.items()},
+                   "note": "CG on precomputed interface-level blocks (F [C Ypi])^T, (Cdelta Cbar)^T; "
+                           "not the headline: its CG round-off trajectory differs from the reference's"}
+        ws.set_cg_blocks("coeff")
+
     lsq = None
     if not args.no_lsq:
         lsq = lsq_microbench(P, args.lsq_blocks, local)
@@ -373,7 +411,7 @@ def run_ours(args, cfg, world, rank, local, dist):
             "roofline": roof, "kernel_families": families,
             "phase_ms": {k: round(v, 3) for k, v in rep.phase_ms.items()},
             "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
-            "fp64_lsq_microbench": lsq,
+            "fp64_lsq_microbench": lsq, "cg_compact": compact,
             "fp64_qr_tflops": (qr["flops"] / (qr["ms"] / 1e3) / 1e12) if qr else None}
     print(json.dumps(line), flush=True)
 
@@ -387,6 +425,7 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--cpu-cg-iters", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compact", action="store_true", help="skip the compact-CG-blocks solve")
     ap.add_argument("--no-lsq", action="store_true", help="skip the C5 local-solve microbenchmark")
     ap.add_argument("--lsq-blocks", type=int, default=1024)
     args = ap.parse_args()

@@ -662,9 +662,8 @@ void Workspace::pack_blocks(const BlockArgs& b) {
     d_KDc.alloc(static_cast<size_t>(std::max(odc, 2LL)));
   }
   launch_pack_streams(b, d_KF.ptr, d_kf_ld.ptr, d_kf_off.ptr, d_KD.ptr, d_kd_ld.ptr, d_kd_off.ptr, st_);
-  launch_compact_streams(b, d_KF.ptr, d_kf_ld.ptr, d_kf_off.ptr, d_KD.ptr, d_kd_ld.ptr, d_kd_off.ptr, d_KFc.ptr,
-                         d_kfc_off.ptr, d_KDc.ptr, d_kdc_off.ptr, st_);
-  launches_ += 3;
+  launches_ += 1;
+  compact_built_ = false;  // the compact blocks follow on first use (cg_args)
 }
 
 void Workspace::build_neumann() {
@@ -708,6 +707,12 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.KFc = d_KFc.ptr;
   a.KDc = d_KDc.ptr;
   a.compact = cg_compact;  // ddelm_gpu_set_cg_blocks
+  if (a.compact && !compact_built_) {
+    launch_compact_streams(block_args(), d_KF.ptr, d_kf_ld.ptr, d_kf_off.ptr, d_KD.ptr, d_kd_ld.ptr, d_kd_off.ptr,
+                           d_KFc.ptr, d_kfc_off.ptr, d_KDc.ptr, d_kdc_off.ptr, st_);
+    launches_ += 2;
+    compact_built_ = true;
+  }
   {
     // row parts per subdomain so that N * P work items cover the SMs (DDELM_CG_PARTS overrides)
     int dev = 0, sms = 148;
@@ -920,10 +925,15 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
       const double r = h_rank[i], rb = h_rank[N + i];
       const double M = p.M, ng = cp.n_gamma, nF = cp.nF, nd = cp.nd;
       double b = 2.0 * r * ng + p.crmax * ng * 2.0;  // Q_G (OP1, OP4), Zc (OP1, OP4)
-      b += 2.0 * M * r + 2.0 * M * nF + 4.0 * M;      // C, F (OP2, OP3), Ypi (OP2)
-      if (method == 2) {
-        b += 2.0 * rb * nd;                            // Qbar on the flux rows (NN1, NN2)
-        b += 2.0 * M * rb + 2.0 * M * nd;              // Cbar, Cdelta (NN1, NN2)
+      if (a.compact) {
+        b += (2.0 * r + p.ncq) * nF;                   // (F [C Ypi])^T (OP2: r + ncq rows, OP3: r)
+        if (method == 2) b += 2.0 * rb * nd + 2.0 * rb * nd;  // Qbar flux rows, (Cdelta Cbar)^T
+      } else {
+        b += 2.0 * M * r + 2.0 * M * nF + 4.0 * M;    // C, F (OP2, OP3), Ypi (OP2)
+        if (method == 2) {
+          b += 2.0 * rb * nd;                          // Qbar on the flux rows (NN1, NN2)
+          b += 2.0 * M * rb + 2.0 * M * nd;            // Cbar, Cdelta (NN1, NN2)
+        }
       }
       per_it += 8.0 * b;
     }

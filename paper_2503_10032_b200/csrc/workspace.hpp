@@ -89,6 +89,7 @@ class Workspace {
   SolveResult solve(int method, double theta, double tol, int max_iter);
   void reseed(uint64_t seed);
   int cg_compact = 0;  // DDELM_CG_BLOCKS_* (CG operator representation)
+  bool compact_built_ = false;
   /// drop every built layer but keep the uploaded feature layers (device-resident inputs)
   void invalidate() { built_ = blocks_built_ = coarse_built_ = neumann_built_ = false; }
   void apply_operator(double theta, const double* v, double* out);
