@@ -23,7 +23,7 @@ int main(int argc, char** argv) {
       {"method", "ddelm-nn"}, {"theta", "0.999"}, {"flux_variant", "mean_edge"},
       {"trace_basis", "change_of_variables"}, {"cg_rel_tol", "1e-9"}, {"cg_max_iter", "0"}, {"device", "0"},
       {"eval_grid_n", "257"}, {"alpha", "32"}, {"forcing_seed", "2"}, {"rho_seed", "3"},
-      {"mode", "solve"}, {"debug_flip_flux_row", "-1"}};
+      {"mode", "solve"}, {"debug_flip_flux_row", "-1"}, {"cg_blocks", "coeff"}};
   for (int k = 1; k < argc; ++k) {
     const std::string a = argv[k];
     const auto eq = a.find('=');
@@ -39,6 +39,11 @@ int main(int argc, char** argv) {
     opts.change_of_variables = kv["trace_basis"] == "change_of_variables";
     opts.device = std::atoi(kv["device"].c_str());
     opts.debug_flip_flux_row = std::atoi(kv["debug_flip_flux_row"].c_str());
+    if (kv["cg_blocks"] != "coeff" && kv["cg_blocks"] != "compact") {
+      std::fprintf(stderr, "config error: cg_blocks must be coeff or compact\n");
+      return 3;
+    }
+    opts.cg_blocks = kv["cg_blocks"] == "compact" ? DDELM_CG_BLOCKS_COMPACT : DDELM_CG_BLOCKS_COEFF;
     ddelm::ProblemParams pp;
     pp.alpha = std::atof(kv["alpha"].c_str());
     pp.forcing_seed = std::strtoull(kv["forcing_seed"].c_str(), nullptr, 10);

@@ -90,6 +90,8 @@ def test_cpp_facade_fails_loudly_without_device():
     assert out.returncode == 2 and "no CUDA device" in out.stderr
     bad = subprocess.run([FACADE_BIN, "bogus=1"], capture_output=True, text=True)
     assert bad.returncode == 3
+    bad = subprocess.run([FACADE_BIN, "cg_blocks=dense"], capture_output=True, text=True)
+    assert bad.returncode == 3 and "cg_blocks" in bad.stderr
 
 
 def test_problem_catalogue_matches_header():

@@ -96,6 +96,20 @@ def test_compact_operator_symmetric_psd_c3(P):
         assert u @ au >= -1e-5 * np.linalg.norm(au) * np.linalg.norm(u)
 
 
+def test_cpp_facade_compact_matches_python_path(P):
+    """SolverOptions::cg_blocks through the C++ façade (examples/ddelm_solve cg_blocks=compact)
+    reproduces the Python-mirror compact solve bit for bit."""
+    import json
+    import subprocess
+    exe = os.path.join(ROOT, "paper_2503_10032_b200", "ddelm_solve")
+    out = subprocess.run([exe, "cg_blocks=compact"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    d = json.loads(out.stdout)
+    _, rep = P.solve_config("T1", cg_blocks="compact")
+    assert d["iterations"] == rep.iterations
+    assert np.array_equal(np.array(d["mu"]), rep.mu)
+
+
 def test_compact_mode_rejects_bad_value(P):
     """An unknown representation code is an invalid_argument (error code 1), not a silent default."""
     ws = P.workspace_from_config("T1")
