@@ -381,10 +381,26 @@ def run_ours(args, cfg, world, rank, local, dist):
         torch.cuda.synchronize()
         barrier(dist)
         cms_e2e = max_over_ranks(dist, t0.elapsed_time(t1)) / args.steps
+        ws.set_profiling(True)
+        ws.invalidate()
+        solve()
+        ws.set_profiling(False)
+        cfam = {}
+        for f in ("qr_factor", "cod_pivqr", "cod_finish", "cg_iterations"):
+            try:
+                v = ws.kernel_stats(f)
+            except Exception:  # noqa: BLE001
+                continue
+            if f in fam:  # the stats accumulate over profiled solves: this solve's share only
+                v = {k: v[k] - fam[f][k] for k in ("ms", "launches", "flops", "bytes")}
+            cfam[f] = {"ms": round(v["ms"], 3),
+                       "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["flops"] else None,
+                       "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["bytes"] else None}
         compact = {"value": nsub / (cms / 1e3), "unit": "subdomains/s", "ms_per_step": cms,
                    "iterations": citers, "e2e": {"value": nsub / (cms_e2e / 1e3), "unit": "subdomains/s",
                                                  "ms_per_step": cms_e2e},
                    "phase_ms": {k: round(v, 3) for k, v in crep.phase_ms.items()},
+                   "kernel_families": cfam,
                    "note": "CG on precomputed interface-level blocks (F [C Ypi])^T, (Cdelta Cbar)^T; "
                            "not the headline: its CG round-off trajectory differs from the reference's"}
         ws.set_cg_blocks("coeff")
