@@ -14,6 +14,12 @@
 //   C      = P Z^T [I_r; 0] T^{-1}   (M x r)      so that  K^+ = C Q_r^T
 //   QtX    = Q_r^T [f | E]           (r x ext)    (Q_r = Q0 Q1[:, :r])
 // The full-rank branch (solvers.cpp:43-44) is the same contract with r = M, C = R0^{-1}.
+#ifndef DDG_COD_FBATCH
+#define DDG_COD_FBATCH 16
+#endif
+#ifndef DDG_COD_GEMV_ROWS
+#define DDG_COD_GEMV_ROWS 8
+#endif
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       }
       const int imax = max(max(iend[0], iend[1]), max(iend[2], iend[3]));
       double g[4] = {0, 0, 0, 0};
-      constexpr int kU = 6;  // rows per lane per batch: 24 independent loads in flight
+      constexpr int kU = DDG_COD_GEMV_ROWS;  // rows per lane per batch: 4 kU independent loads in flight
       for (int i0 = k + lane; i0 <= imax; i0 += 32 * kU) {
         double x[kU][4], vv[kU];
 #pragma unroll
@@ -278,12 +284,13 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       const int cj = perm[j];
       double fw = 0, fv = 0;
       int u = 0;
-      for (; u + 8 <= k; u += 8) {  // 8 loads in flight
-        double f[8];
+      constexpr int kF = DDG_COD_FBATCH;  // loads in flight per thread (same summation order)
+      for (; u + kF <= k; u += kF) {
+        double f[kF];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) f[q] = F1[static_cast<size_t>(u + q) * M + j];
+        for (int q = 0; q < kF; ++q) f[q] = F1[static_cast<size_t>(u + q) * M + j];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < kF; ++q) {
           fw += f[q] * w[u + q];
           fv += f[q] * vk[u + q];
         }
