@@ -741,22 +741,33 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
       S.W[r * TNP + c + 1] = acc[i][j][1];
     }
   __syncthreads();
-  // ---- W' = T^T W (T upper triangular): column c of W' = T^T W(:, c)
+  // ---- W' = T^T W (T upper triangular) on DMMA: warp -> n-tile `warp` (its 8 columns of W), all
+  //      NB_/8 m-tiles; A = T^T with the zero triangle masked, B = W(:, n-tile). Each warp reads
+  //      and rewrites only its own columns, so no block barrier is needed in between.
   {
-    double wcol[NB_ * TN / 256];
+    static_assert(TN / 8 == 8, "one n-tile per warp (256 threads)");
+    constexpr int MTT = NB_ / 8;
+    double cw[MTT][2];
 #pragma unroll
-    for (int e = 0; e < NB_ * TN / 256; ++e) {
-      const int idx = threadIdx.x + 256 * e;
-      const int u = idx / TN, c = idx % TN;
-      double s = 0;
-      for (int w = 0; w <= u; ++w) s += S.T[w * (NB_ + 1) + u] * S.W[w * TNP + c];
-      wcol[e] = s;
+    for (int i = 0; i < MTT; ++i) cw[i][0] = cw[i][1] = 0.0;
+    const int n8 = warp * 8;
+#pragma unroll
+    for (int kk = 0; kk < NB_ / 4; ++kk) {
+      const int w = kk * 4 + lc;
+      const double bv = S.W[w * TNP + n8 + lr];
+#pragma unroll
+      for (int i = 0; i < MTT; ++i) {
+        const int u = i * 8 + lr;
+        const double av = (w <= u) ? S.T[w * (NB_ + 1) + u] : 0.0;
+        dmma_8x8x4(cw[i][0], cw[i][1], av, bv);
+      }
     }
-    __syncthreads();
+    __syncwarp();
 #pragma unroll
-    for (int e = 0; e < NB_ * TN / 256; ++e) {
-      const int idx = threadIdx.x + 256 * e;
-      S.W[(idx / TN) * TNP + idx % TN] = wcol[e];
+    for (int i = 0; i < MTT; ++i) {
+      const int r = i * 8 + lr, c = n8 + 2 * lc;
+      S.W[r * TNP + c] = cw[i][0];
+      S.W[r * TNP + c + 1] = cw[i][1];
     }
   }
   // ---- pass 2: A_tile -= V W' per 32-row chunk. Warp tile: 2 row-tiles x 2 col-tiles.
