@@ -193,7 +193,7 @@ def run_reference(args, cfg, world, rank):
             "unit": "subdomains/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args, cfg),
+            "config": workload_config(args, cfg, 1),
             "cpu_baseline": {"value": value, "unit": "subdomains/s", "cores": last["cores"],
                              "kind": "port", "sample": last["sample"]},
             "e2e": {"value": value, "unit": "subdomains/s", "h2d_bytes_per_step": 0,
@@ -228,15 +228,16 @@ def lsq_microbench(P, nblocks, device, reps=3):
             "flop_model": "geqrf 2mn^2-2n^3/3 + Q^T B 4mnk-2n^2k + S 2(m-n)k^2 (SURVEY.md §8d)"}
 
 
-def workload_config(args, cfg):
+def workload_config(args, cfg, world=1):
     return {"workload": f"{args.config}: DDELM-NN (theta {cfg['theta']}) {cfg['s']}x{cfg['s']} subdomains, "
                         f"M={cfg['M']}, n_grid={cfg['n_grid']}, l={cfg['l']}, {cfg['problem']}, "
                         f"{cfg['flux_variant']} + {cfg['trace_basis']}, cg_rel_tol {cfg['cg_rel_tol']}",
             "subdomains": cfg["s"] ** 2, "neurons_per_subdomain": cfg["M"],
             "collocation_points_per_subdomain": cfg["n_grid"] ** 2,
             "l2_policy": "working set (2N local matrices, >1 GB at C3) far exceeds the 126 MB L2",
-            "parallelism": (f"sharded x{args.gpus}: contiguous strip of subdomains per GPU, NCCL all-reduce "
-                            "of the owner-slot tables between CG phases" if args.gpus > 1 else "single GPU")}
+            "parallelism": (f"sharded x{world}: contiguous strip of subdomains per GPU (one process per GPU), "
+                            "owner-slot segments over NCCL send/recv between the CG phases, CG loop as "
+                            "chunked CUDA graphs" if world > 1 else "single GPU")}
 
 
 # --------------------------------------------------------------------------- ours
@@ -406,7 +407,7 @@ def run_ours(args, cfg, world, rank, local, dist):
         ws.set_cg_blocks("coeff")
 
     lsq = None
-    if not args.no_lsq:
+    if not args.no_lsq and world == 1:
         lsq = lsq_microbench(P, args.lsq_blocks, local)
     if rank != 0:
         return
@@ -420,7 +421,7 @@ def run_ours(args, cfg, world, rank, local, dist):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded feature layers; manufactured Poisson data)",
-            "config": workload_config(args, cfg),
+            "config": workload_config(args, cfg, world),
             "solve_seconds": ms_step / 1e3, "iterations": iters,
             "e2e": {"value": e2e_value, "unit": "subdomains/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
@@ -430,6 +431,27 @@ def run_ours(args, cfg, world, rank, local, dist):
             "fp64_lsq_microbench": lsq, "cg_compact": compact,
             "fp64_qr_tflops": (qr["flops"] / (qr["ms"] / 1e3) / 1e12) if qr else None}
     print(json.dumps(line), flush=True)
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N without a torchrun environment: start the N ranks ourselves (one process per GPU,
+    torch.distributed.run on 127.0.0.1) and pass their output through."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}",
+              file=sys.stderr, flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, cwd=ROOT)
 
 
 def main():
@@ -448,7 +470,12 @@ def main():
     from paper_2503_10032_b200.configs import CONFIGS
 
     cfg = CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
     world, rank, local = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr, flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
         return

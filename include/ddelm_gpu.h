@@ -95,13 +95,31 @@ const char* ddelm_gpu_version(void);
 int ddelm_gpu_create(const ddelm_desc* desc, ddelm_ws** out);
 /* Sharded workspace (one process per GPU): rank `rank` of `world` owns the contiguous strip of
  * subdomains ddelm_gpu_get_shard reports and factorises only those; the coarse problem and the
- * interface vectors are replicated; the owner-slot tables of every cross-subdomain sum are
- * all-reduced over NCCL (nccl_id: 128 bytes from ddelm_gpu_nccl_unique_id on rank 0, broadcast
- * by the caller). world = 1 runs the same phase-by-phase path on one device (nccl_id unused).
- * Coefficients / ranks / layers returned by the getters are those of the local strip. */
+ * interface vectors are replicated. Every cross-subdomain sum lives in an owner-slot table (one
+ * writer per slot); between the CG phases each rank sends the slots it wrote to the ranks that
+ * read them (grouped ncclSend / ncclRecv; the CG loop is one CUDA graph replayed in chunks), so
+ * the result is bitwise that of one device with the same work split (DDELM_CG_PARTS). nccl_id:
+ * 128 bytes from ddelm_gpu_nccl_unique_id on rank 0, broadcast by the caller. world = 1 is the
+ * single-device path (nccl_id unused). Coefficients / ranks / layers returned by the getters are
+ * those of the local strip. (Replaces the reference's serial loops over subdomains,
+ * solvers.cpp:207-224,338,361,457-458,470-471, with the strip partition of the paper's MPI split.) */
 int ddelm_gpu_nccl_unique_id(unsigned char* nccl_id /* 128 bytes */);
 int ddelm_gpu_create_sharded(const ddelm_desc* desc, int rank, int world, const unsigned char* nccl_id,
                              ddelm_ws** out);
+/* Test backend of the sharded path: the same kernels and exchange lists, the slot segments
+ * host-staged through a POSIX shared-memory mailbox `shm_name` ("/...", the same on every rank)
+ * with a host barrier — synchronous, so several ranks can share ONE GPU (no kernel waits for
+ * another rank's kernel). Not a performance path. */
+int ddelm_gpu_create_sharded_host(const ddelm_desc* desc, int rank, int world, const char* shm_name,
+                                  ddelm_ws** out);
+/* Host-only view of the exchange plan of `rank` (no device needed): one_level 0 (coarse methods)
+ * or 1, point 0..5 (after OP1, OP2, NN1, NN2, OP3, OP4), which = 0 send entries / 1 receive
+ * entries as (table, slot) pairs, 2 send counts / 3 receive counts / 4 send offsets per peer,
+ * 5 = {largest message in doubles}. Returns the length, or -error. */
+int ddelm_gpu_exchange_lists(const ddelm_desc* desc, int rank, int world, int one_level, int point, int which,
+                             int* out, int cap);
+/* CG driver the last solve used: "graph-while", "graph-chunked", "host-loop" or "persistent". */
+const char* ddelm_gpu_cg_driver(ddelm_ws* ws);
 int ddelm_gpu_get_shard(ddelm_ws* ws, int* sub_lo, int* sub_count, int* n_global);
 /* Host-only view of a shard's owner-slot tables (no device needed): which = 0 gamma, 1 flux,
  * 2 Neumann, 3 corner, 4 cross-row destinations of the local strip, 5 = {sub_lo, N_local,
@@ -172,6 +190,15 @@ int ddelm_gpu_apply_neumann(ddelm_ws* ws, int transpose, const double* v, double
  * reduced_op dim x dim column-major, reduced_rhs dim, mu_full n_mu, coeffs n_subdomains x M.
  * sum(M) + n_mu > 3000 -> DDELM_ERR_INVALID_ARGUMENT (solvers.cpp:619-620), as is a sharded
  * workspace. Regenerates the local matrices: the next solve rebuilds the factorisations. */
+/* LsFactor (solvers.cpp:24-78) of nmat caller-supplied m x n matrices (m >= n; K: nmat blocks,
+ * each column-major m x n) on the hot path's own kernels (batched QR, diagonal-ratio branch test
+ * at rank_tol, pivoted QR + RZ, finish). Outputs per matrix: numerical rank, the branch taken
+ * (1 = complete orthogonal decomposition), reff (R0 rows the pivoted factorisation kept; NULL ok),
+ * K^+ (pinv: n x m column-major) and Q_r (Q: m x n column-major, columns >= rank zero; NULL ok),
+ * so apply_pinv / apply_pinv_transpose / apply_projection are K^+ v, (K^+)^T u, Q_r Q_r^T v.
+ * Errors: m < n -> DDELM_ERR_INVALID_ARGUMENT (solvers.cpp:26). Test hook of the factorisation. */
+int ddelm_gpu_lsfactor_batch(int device, int nmat, int m, int n, const double* K, double rank_tol, int* rank,
+                             int* deficient, int* reff, double* pinv, double* Q);
 int ddelm_gpu_dense_oracle(ddelm_ws* ws, int method, double theta, int* dim, double* reduced_op,
                            double* reduced_rhs, double* mu_full, double* coeffs);
 /* Drop every built layer (features, factors, coarse, Neumann) but keep the feature layers

@@ -2,7 +2,10 @@
 // C ABI over the restatement so pytest / tools/make_goldens.py / bench.py's CPU legs can
 // drive it through ctypes. Mirrors the reference's run() (runner.cpp:126-155): build the
 // Workspace, dispatch the method, evaluate the field.
+#include <algorithm>
 #include <chrono>
+#include <limits>
+#include <random>
 #include <cstring>
 #include <memory>
 
@@ -267,6 +270,54 @@ int ddo_errors(void* p, int n, double* l2, double* h1) {
   *l2 = e.l2;
   *h1 = e.h1;
   return 0;
+}
+
+// ---- factorisation-level entry points (LsFactor tests, test_solvers.cpp:14-85)
+/// seeded standard-normal matrix, column-major (test_solvers.cpp:14-21: mt19937_64 + libstdc++
+/// normal_distribution, column by column)
+void ddo_random_matrix(int rows, int cols, unsigned long long seed, double* out) {
+  std::mt19937_64 gen(seed);
+  std::normal_distribution<double> n;
+  for (int j = 0; j < cols; ++j)
+    for (int i = 0; i < rows; ++i) out[static_cast<size_t>(j) * rows + i] = n(gen);
+}
+
+/// LsFactor (solvers.cpp:24-45) of one column-major m x n matrix: rank, branch, K^+ (n x m
+/// column-major) and Q (m x n column-major, columns >= rank zero)
+int ddo_lsfactor(const double* K, int m, int n, double tol, int* rank, int* deficient, double* pinv, double* Q) {
+  try {
+    Mat A(m, n);
+    std::copy(K, K + static_cast<size_t>(m) * n, A.a.begin());
+    LsFactor f(A, tol);
+    *rank = f.rank();
+    *deficient = f.rank_deficient() ? 1 : 0;
+    Mat I = Mat::identity(m);
+    Mat P = f.apply_pinv(I);
+    std::copy(P.a.begin(), P.a.end(), pinv);
+    const Mat& q = f.Q();
+    std::fill(Q, Q + static_cast<size_t>(m) * n, 0.0);
+    for (int j = 0; j < q.c && j < n; ++j)
+      for (int i = 0; i < m; ++i) Q[static_cast<size_t>(j) * m + i] = q(i, j);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
+/// Eigen's A.completeOrthogonalDecomposition().pseudoInverse() with the DEFAULT threshold
+/// (eps * min(m, n)): the reference tests' svd_pinv (test_solvers.cpp:23-25); out n x m
+int ddo_cod_pinv(const double* K, int m, int n, double* out) {
+  try {
+    Mat A(m, n);
+    std::copy(K, K + static_cast<size_t>(m) * n, A.a.begin());
+    COD c;
+    c.compute(A, std::numeric_limits<double>::epsilon() * std::min(m, n));
+    Mat P = c.pseudo_inverse();
+    std::copy(P.a.begin(), P.a.end(), out);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
 }
 
 }  // extern "C"

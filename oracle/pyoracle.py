@@ -59,7 +59,8 @@ def lib():
                                 C.c_char_p, C.c_int]
         for name in ("ddo_info", "ddo_timings", "ddo_residuals", "ddo_mu", "ddo_coeffs",
                      "ddo_ranks", "ddo_layer", "ddo_local", "ddo_kbar", "ddo_field",
-                     "ddo_field_of", "ddo_errors", "ddo_apply_cs", "ddo_apply_reduced", "ddo_dense", "ddo_apply_p"):
+                     "ddo_field_of", "ddo_errors", "ddo_apply_cs", "ddo_apply_reduced", "ddo_dense", "ddo_apply_p",
+                     "ddo_random_matrix", "ddo_lsfactor", "ddo_cod_pinv"):
             getattr(L, name).argtypes = None  # variadic pointer args, set per call
         _lib = L
     return _lib
@@ -213,6 +214,39 @@ class OracleWorkspace:
         if rc:
             raise RuntimeError("problem has no exact solution")
         return l2.value, h1.value
+
+
+def random_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """The reference tests' seeded N(0,1) matrix (test_solvers.cpp:14-21), bit-exact."""
+    out = np.zeros((cols, rows))
+    lib().ddo_random_matrix(C.c_int(rows), C.c_int(cols), C.c_ulonglong(seed), _p(out))
+    return out.T.copy()
+
+
+def lsfactor(K: np.ndarray, tol: float = 1e-10):
+    """Oracle LsFactor (solvers.cpp:24-45): (rank, deficient, pinv n x m, Q m x n zero-padded)."""
+    K = np.asarray(K, dtype=np.float64)
+    m, n = K.shape
+    Kf = np.ascontiguousarray(K.T)
+    rank, dfc = C.c_int(), C.c_int()
+    pinv = np.zeros((m, n))  # column-major n x m
+    Q = np.zeros((n, m))     # column-major m x n
+    rc = lib().ddo_lsfactor(_p(Kf), C.c_int(m), C.c_int(n), C.c_double(tol), C.byref(rank), C.byref(dfc),
+                            _p(pinv), _p(Q))
+    if rc != 0:
+        raise RuntimeError("ddo_lsfactor failed")
+    return rank.value, bool(dfc.value), pinv.T.copy(), Q.T.copy()
+
+
+def cod_pinv(K: np.ndarray) -> np.ndarray:
+    """Eigen COD pseudo-inverse with the default threshold (the reference tests' svd_pinv)."""
+    K = np.asarray(K, dtype=np.float64)
+    m, n = K.shape
+    Kf = np.ascontiguousarray(K.T)
+    out = np.zeros((m, n))
+    if lib().ddo_cod_pinv(_p(Kf), C.c_int(m), C.c_int(n), _p(out)) != 0:
+        raise RuntimeError("ddo_cod_pinv failed")
+    return out.T.copy()
 
 
 def field_rel_l2(u_a: np.ndarray, u_b: np.ndarray, n: int) -> float:

@@ -43,7 +43,8 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_nccl_unique_id", "ddelm_gpu_create_sharded", "ddelm_gpu_get_shard",
            "ddelm_gpu_plan_tables", "ddelm_gpu_sample_field", "ddelm_gpu_relative_errors",
            "ddelm_gpu_field_diff", "ddelm_gpu_apply_reduced", "ddelm_gpu_dense_oracle",
-           "ddelm_gpu_apply_neumann", "ddelm_gpu_set_cg_blocks")
+           "ddelm_gpu_apply_neumann", "ddelm_gpu_set_cg_blocks", "ddelm_gpu_create_sharded_host",
+           "ddelm_gpu_exchange_lists", "ddelm_gpu_cg_driver", "ddelm_gpu_lsfactor_batch")
 
 
 class _Desc(C.Structure):
@@ -121,6 +122,13 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_create_sharded.argtypes = [C.POINTER(_Desc), C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
     L.ddelm_gpu_get_shard.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
     L.ddelm_gpu_plan_tables.argtypes = [C.POINTER(_Desc), C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int]
+    L.ddelm_gpu_create_sharded_host.argtypes = [C.POINTER(_Desc), C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
+    L.ddelm_gpu_exchange_lists.argtypes = [C.POINTER(_Desc), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_void_p, C.c_int]
+    L.ddelm_gpu_lsfactor_batch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_double,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_cg_driver.argtypes = [C.c_void_p]
+    L.ddelm_gpu_cg_driver.restype = C.c_char_p
     _lib = L
     return L
 
@@ -208,13 +216,83 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def _cfg_desc(cfg) -> _Desc:
+    return _Desc(PROBLEMS[cfg["problem"]], cfg["s"], cfg["n_grid"], cfg["M"], float(cfg["l"]), cfg["seed"],
+                 1 if cfg["flux_variant"] == "mean_edge" else 0,
+                 1 if cfg["trace_basis"] == "change_of_variables" else 0, 1e-10, 0, -1,
+                 float(cfg.get("alpha", 32.0)), int(cfg.get("forcing_seed", 2)), int(cfg.get("rho_seed", 3)))
+
+
+# exchange points / tables of the sharded iteration (plan.hpp XPoint / XTable)
+XPOINTS = ("op1", "op2", "nn1", "nn2", "op3", "op4")
+XTABLES = ("t", "psi", "t3", "o", "x", "tr", "zz", "xc", "opi", "pap")
+
+
+def exchange_lists(cfg, rank: int, world: int, one_level: bool = False) -> dict:
+    """Host-side exchange plan of one rank (no GPU needed): per point, the (table, slot) entries
+    it sends / receives and the per-peer counts (plan.cpp build_exchange_plan)."""
+    L = load_library()
+    d = _cfg_desc(cfg)
+
+    def get(pt, which):
+        n = L.ddelm_gpu_exchange_lists(C.byref(d), rank, world, int(one_level), pt, which, None, 0)
+        if n < 0:
+            _check(-n)
+        a = np.zeros(max(n, 1), dtype=np.int32)
+        L.ddelm_gpu_exchange_lists(C.byref(d), rank, world, int(one_level), pt, which, _ptr(a), n)
+        return a[:n]
+
+    out = {}
+    for pt, name in enumerate(XPOINTS):
+        out[name] = {"send": get(pt, 0).reshape(-1, 2), "recv": get(pt, 1).reshape(-1, 2),
+                     "scnt": get(pt, 2), "rcnt": get(pt, 3), "soff": get(pt, 4)}
+    out["max_msg"] = int(get(0, 5)[0])
+    return out
+
+
+@dataclass
+class LsFactorBatch:
+    """LsFactor (solvers.cpp:24-78) of a batch of matrices, computed on the device."""
+    rank: np.ndarray        # (nmat,)
+    deficient: np.ndarray   # (nmat,) bool: COD branch
+    reff: np.ndarray        # (nmat,) R0 rows kept by the pivoted factorisation
+    pinv: np.ndarray        # (nmat, n, m)
+    Q: np.ndarray           # (nmat, m, n), columns >= rank zero
+
+    def apply_pinv(self, t, v):
+        return self.pinv[t] @ v
+
+    def apply_pinv_transpose(self, t, u):
+        return self.pinv[t].T @ u
+
+    def apply_projection(self, t, v):
+        q = self.Q[t][:, :self.rank[t]]
+        return q @ (q.T @ v)
+
+
+def lsfactor_batch(K, rank_tol: float = 1e-10, device: int = 0) -> LsFactorBatch:
+    """K: (nmat, m, n) or (m, n) float64. Runs the batched QR / COD kernels of the hot path
+    (include/ddelm_gpu.h ddelm_gpu_lsfactor_batch)."""
+    K = np.asarray(K, dtype=np.float64)
+    if K.ndim == 2:
+        K = K[None]
+    nmat, m, n = K.shape
+    Kf = np.ascontiguousarray(np.transpose(K, (0, 2, 1)))  # column-major blocks
+    rank = np.zeros(nmat, dtype=np.int32)
+    defi = np.zeros(nmat, dtype=np.int32)
+    reff = np.zeros(nmat, dtype=np.int32)
+    pinv = np.zeros((nmat, m, n))  # column-major n x m == row-major m x n
+    Q = np.zeros((nmat, n, m))
+    _check(load_library().ddelm_gpu_lsfactor_batch(device, nmat, m, n, _ptr(Kf), float(rank_tol), _ptr(rank),
+                                                   _ptr(defi), _ptr(reff), _ptr(pinv), _ptr(Q)))
+    return LsFactorBatch(rank=rank, deficient=defi.astype(bool), reff=reff,
+                         pinv=np.transpose(pinv, (0, 2, 1)).copy(), Q=np.transpose(Q, (0, 2, 1)).copy())
+
+
 def plan_tables(cfg, rank: int, world: int) -> dict:
     """Host-side owner-slot tables of one shard (no GPU needed): the sharding logic under test."""
     L = load_library()
-    d = _Desc(PROBLEMS[cfg["problem"]], cfg["s"], cfg["n_grid"], cfg["M"], float(cfg["l"]), cfg["seed"],
-              1 if cfg["flux_variant"] == "mean_edge" else 0,
-              1 if cfg["trace_basis"] == "change_of_variables" else 0, 1e-10, 0, -1,
-              float(cfg.get("alpha", 32.0)), int(cfg.get("forcing_seed", 2)), int(cfg.get("rho_seed", 3)))
+    d = _cfg_desc(cfg)
     out = {}
     for which, name in enumerate(["gamma_dst", "flux_dst", "nd_dst", "corner_dst", "cross_dst", "meta"]):
         n = L.ddelm_gpu_plan_tables(C.byref(d), rank, world, which, None, 0)
@@ -238,7 +316,9 @@ class Workspace:
 
     shard=(rank, world, nccl_id) builds a sharded workspace: this process/GPU owns the strip
     shard_range(s*s, rank, world) of subdomains; interface vectors and the coarse problem are
-    replicated and every cross-subdomain sum is an NCCL all-reduce of owner-slot tables."""
+    replicated and every cross-subdomain sum is an owner-slot table whose foreign slots arrive
+    over NCCL send/recv between the CG phases. shard=(rank, world, "host:/shm-name") selects the
+    host-staged test backend (several ranks on one GPU)."""
 
     def __init__(self, problem: ProblemSpec | str, s: int, n_grid: int, M: int, l: float, seed: int,
                  opts: SolverOptions | None = None, device: int = 0, shard: tuple | None = None):
@@ -258,8 +338,13 @@ class Workspace:
             _check(L.ddelm_gpu_create(C.byref(d), C.byref(h)))
         else:
             rank, world, nid = shard
-            idbuf = (C.c_ubyte * 128).from_buffer_copy(nid) if nid is not None else None
-            _check(L.ddelm_gpu_create_sharded(C.byref(d), int(rank), int(world), idbuf, C.byref(h)))
+            if isinstance(nid, str) and nid.startswith("host:"):
+                # test backend: slot segments host-staged through a shared-memory mailbox
+                _check(L.ddelm_gpu_create_sharded_host(C.byref(d), int(rank), int(world),
+                                                       nid[5:].encode(), C.byref(h)))
+            else:
+                idbuf = (C.c_ubyte * 128).from_buffer_copy(nid) if nid is not None else None
+                _check(L.ddelm_gpu_create_sharded(C.byref(d), int(rank), int(world), idbuf, C.byref(h)))
         self._h = h
         self.problem, self.s, self.n_grid, self.M, self.l, self.seed = problem, s, n_grid, M, l, seed
         self.opts = opts
@@ -290,6 +375,11 @@ class Workspace:
     def reseed(self, seed: int):
         _check(load_library().ddelm_gpu_reseed(self._h, seed))
         self.seed = seed
+
+    @property
+    def cg_driver(self) -> str:
+        """CG driver of the last solve: graph-while, graph-chunked, host-loop or persistent."""
+        return load_library().ddelm_gpu_cg_driver(self._h).decode()
 
     def set_cg_blocks(self, mode: str):
         """'coeff' (default: the reference's grouping, its CG trajectory) or 'compact'

@@ -107,30 +107,38 @@ int ddelm_gpu_create(const ddelm_desc* d, ddelm_ws** out) {
 int ddelm_gpu_nccl_unique_id(unsigned char* id) {
   return guarded([&] {
     if (!id) throw std::invalid_argument("ddelm_gpu_nccl_unique_id: null argument");
-    ddg::Exchange::unique_id(id);
+    ddg::NcclExchange::unique_id(id);
   });
 }
 
-int ddelm_gpu_create_sharded(const ddelm_desc* d, int rank, int world, const unsigned char* nccl_id, ddelm_ws** out) {
+}  // extern "C"
+
+namespace {
+ddg::Plan global_plan(const ddelm_desc* d) {
+  return ddg::build_plan(d->problem, d->s, d->n_grid, d->M, d->l, d->seed, d->flux_variant, d->change_of_variables != 0,
+                         d->rank_tol > 0 ? d->rank_tol : 1e-10, d->debug_flip_flux_row, desc_params(d));
+}
+
+/// sharded workspace of `rank`: its strip of the global plan, the exchange plan, the backend
+template <class MakeEx>
+int create_sharded(const char* fn, const ddelm_desc* d, int rank, int world, ddelm_ws** out, MakeEx make_ex) {
   return guarded([&] {
-    if (!d || !out || (world > 1 && !nccl_id)) throw std::invalid_argument("ddelm_gpu_create_sharded: null argument");
-    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("ddelm_gpu_create_sharded: bad rank / world");
+    if (!d || !out) throw std::invalid_argument(std::string(fn) + ": null argument");
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument(std::string(fn) + ": bad rank / world");
     *out = nullptr;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-      throw ddg::CudaError("ddelm_gpu_create_sharded: no CUDA device available (no CPU fallback)");
-    if (d->device < 0 || d->device >= ndev) throw std::invalid_argument("ddelm_gpu_create_sharded: bad device ordinal");
-    ddg::Plan g = ddg::build_plan(d->problem, d->s, d->n_grid, d->M, d->l, d->seed, d->flux_variant,
-                                  d->change_of_variables != 0, d->rank_tol > 0 ? d->rank_tol : 1e-10,
-                                  d->debug_flip_flux_row, desc_params(d));
-    if (world > g.N) throw std::invalid_argument("ddelm_gpu_create_sharded: more ranks than subdomains");
+      throw ddg::CudaError(std::string(fn) + ": no CUDA device available (no CPU fallback)");
+    if (d->device < 0 || d->device >= ndev) throw std::invalid_argument(std::string(fn) + ": bad device ordinal");
+    ddg::Plan g = global_plan(d);
+    if (world > g.N) throw std::invalid_argument(std::string(fn) + ": more ranks than subdomains");
     int lo = 0, hi = 0;
     ddg::shard_range(g.N, rank, world, &lo, &hi);
-    std::unique_ptr<ddg::Exchange> ex = world > 1 ? std::make_unique<ddg::Exchange>(rank, world, nccl_id, d->device)
-                                                  : std::make_unique<ddg::Exchange>();
+    ddg::XPlan xp = ddg::build_exchange_plan(g, rank, world);
+    std::unique_ptr<ddg::Exchange> ex = make_ex(xp);
     auto* h = new ddelm_ws;
     try {
-      h->w = new ddg::Workspace(ddg::shard_plan(g, lo, hi), d->device, std::move(ex));
+      h->w = new ddg::Workspace(ddg::shard_plan(g, lo, hi), d->device, world > 1 ? std::move(ex) : nullptr, std::move(xp));
     } catch (...) {
       delete h;
       throw;
@@ -138,6 +146,53 @@ int ddelm_gpu_create_sharded(const ddelm_desc* d, int rank, int world, const uns
     *out = h;
   });
 }
+}  // namespace
+
+extern "C" {
+
+int ddelm_gpu_create_sharded(const ddelm_desc* d, int rank, int world, const unsigned char* nccl_id, ddelm_ws** out) {
+  if (world > 1 && !nccl_id) {
+    return guarded([] { throw std::invalid_argument("ddelm_gpu_create_sharded: null nccl_id"); });
+  }
+  return create_sharded("ddelm_gpu_create_sharded", d, rank, world, out, [&](const ddg::XPlan&) {
+    return std::unique_ptr<ddg::Exchange>(world > 1 ? new ddg::NcclExchange(rank, world, nccl_id, d->device) : nullptr);
+  });
+}
+
+int ddelm_gpu_create_sharded_host(const ddelm_desc* d, int rank, int world, const char* shm_name, ddelm_ws** out) {
+  if (!shm_name) return guarded([] { throw std::invalid_argument("ddelm_gpu_create_sharded_host: null shm_name"); });
+  return create_sharded("ddelm_gpu_create_sharded_host", d, rank, world, out, [&](const ddg::XPlan& xp) {
+    return std::unique_ptr<ddg::Exchange>(world > 1 ? new ddg::HostExchange(rank, world, shm_name, xp.max_msg) : nullptr);
+  });
+}
+
+int ddelm_gpu_exchange_lists(const ddelm_desc* d, int rank, int world, int one_level, int point, int which, int* out,
+                             int cap) {
+  int n = 0;
+  const int rc = guarded([&] {
+    if (!d || world < 1 || rank < 0 || rank >= world || one_level < 0 || one_level > 1 || point < 0 ||
+        point >= ddg::kXPoints || which < 0 || which > 5)
+      throw std::invalid_argument("ddelm_gpu_exchange_lists: bad argument");
+    const ddg::XPlan xp = ddg::build_exchange_plan(global_plan(d), rank, world);
+    const ddg::XList& L = xp.pt[one_level][point];
+    std::vector<int> v;
+    if (which <= 1) {
+      for (const ddg::XEntry& e : which == 0 ? L.send : L.recv) {
+        v.push_back(e.table);
+        v.push_back(e.idx);
+      }
+    } else if (which == 5) {
+      v.push_back(static_cast<int>(std::min<size_t>(xp.max_msg, 0x7fffffff)));
+    } else {
+      v = which == 2 ? L.scnt : which == 3 ? L.rcnt : L.soff;
+    }
+    n = static_cast<int>(v.size());
+    if (out) std::memcpy(out, v.data(), sizeof(int) * std::min<size_t>(v.size(), static_cast<size_t>(std::max(cap, 0))));
+  });
+  return rc == DDELM_OK ? n : -rc;
+}
+
+const char* ddelm_gpu_cg_driver(ddelm_ws* ws) { return ws ? ws->w->cg_driver() : ""; }
 
 int ddelm_gpu_plan_tables(const ddelm_desc* d, int rank, int world, int which, int* out, int cap) {
   int n = 0;
@@ -314,6 +369,26 @@ int ddelm_gpu_dense_oracle(ddelm_ws* ws, int method, double theta, int* dim, dou
     if (reduced_rhs) std::copy(o.reduced_rhs.begin(), o.reduced_rhs.end(), reduced_rhs);
     if (mu_full) std::copy(o.mu_full.begin(), o.mu_full.end(), mu_full);
     if (coeffs) std::copy(o.coeffs.begin(), o.coeffs.end(), coeffs);
+  });
+}
+int ddelm_gpu_lsfactor_batch(int device, int nmat, int m, int n, const double* K, double rank_tol, int* rank,
+                             int* deficient, int* reff, double* pinv, double* Q) {
+  return guarded([&] {
+    if (!K || !rank || !deficient || !pinv) throw std::invalid_argument("ddelm_gpu_lsfactor_batch: null argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw ddg::CudaError("ddelm_gpu_lsfactor_batch: no CUDA device available (no CPU fallback)");
+    if (device < 0 || device >= ndev) throw std::invalid_argument("ddelm_gpu_lsfactor_batch: bad device ordinal");
+    DDG_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    DDG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+      ddg::lsfactor_batch(nmat, m, n, K, rank_tol, rank, deficient, reff, pinv, Q, st);
+    } catch (...) {
+      cudaStreamDestroy(st);
+      throw;
+    }
+    DDG_CUDA(cudaStreamDestroy(st));
   });
 }
 int ddelm_gpu_invalidate(ddelm_ws* ws) {

@@ -151,8 +151,27 @@ __global__ void __launch_bounds__(256) coarse_local_kernel(BlockArgs a, const in
     }
 }
 
-/// Dpp rows and dpi from per-subdomain contributions, in subdomain order (one CTA per row).
-__global__ void coarse_rows_kernel(BlockArgs a, const int* row_owner /* npf x 4 : i*crmax+rho */) {
+/// The per-subdomain inputs of the coarse rows, compacted into the GLOBAL subdomain numbering:
+/// pd (crmax), Zc at the corner slots (crmax x ncq) and the corner Grams (ncq x ncq) of local
+/// subdomain i go to rows sub_lo + i of pd_g / zcc_g / gc_g (zero elsewhere; a sharded build
+/// all-reduces them: one writer per entry, exact).
+__global__ void coarse_export_kernel(BlockArgs a) {
+  const int i = blockIdx.x, ig = a.sub_lo + i, ncq = a.ncq;
+  for (int k = threadIdx.x; k < a.crmax * ncq; k += blockDim.x) {
+    const int rho = k / ncq, q = k % ncq;
+    const int g = a.corner_q[i * ncq + q];
+    a.zcc_g[(static_cast<size_t>(ig) * a.crmax + rho) * ncq + q] =
+        g >= 0 ? a.Zc[(static_cast<size_t>(i) * a.crmax + rho) * a.gmax + g] : 0.0;
+  }
+  for (int rho = threadIdx.x; rho < a.crmax; rho += blockDim.x)
+    a.pd_g[static_cast<size_t>(ig) * a.crmax + rho] = a.pd[static_cast<size_t>(i) * a.crmax + rho];
+  for (int k = threadIdx.x; k < ncq * ncq; k += blockDim.x)
+    a.gc_g[static_cast<size_t>(ig) * ncq * ncq + k] = a.Gc[static_cast<size_t>(i) * ncq * ncq + k];
+}
+
+/// Dpp rows and dpi from per-subdomain contributions, in global subdomain order (one CTA per
+/// row): the same terms in the same order on one device and on every rank of a sharded build.
+__global__ void coarse_rows_kernel(BlockArgs a) {
   const int rrow = blockIdx.x;
   double* drow = a.Dpp + static_cast<size_t>(rrow) * a.n_pi;
   for (int c = threadIdx.x; c < a.n_pi; c += blockDim.x) drow[c] = 0.0;
@@ -160,16 +179,15 @@ __global__ void coarse_rows_kernel(BlockArgs a, const int* row_owner /* npf x 4 
   if (threadIdx.x == 0) {
     double s = 0;
     for (int q = 0; q < 4; ++q) {
-      const int own = row_owner[rrow * 4 + q];
+      const int own = a.row_owner[rrow * 4 + q];
       if (own < 0) continue;
-      const int i = own / a.crmax, rho = own % a.crmax;
-      s += a.pd[own];
-      const double* z = a.Zc + (static_cast<size_t>(i) * a.crmax + rho) * a.gmax;
+      const int ig = own / a.crmax;
+      s += a.pd_g[own];
+      const double* z = a.zcc_g + static_cast<size_t>(own) * a.ncq;
       for (int p = 0; p < a.ncq; ++p) {
-        const int g = a.corner_q[i * a.ncq + p];
-        if (g < 0) continue;
-        const int gp = a.gamma_pi[static_cast<size_t>(i) * a.gmax + g];
-        drow[gp] += z[g];
+        const int gp = a.cpi_g[ig * a.ncq + p];
+        if (gp < 0) continue;
+        drow[gp] += z[p];
       }
     }
     // dpi = -(A K^+ f) on the cross rows (solvers.cpp:293-296), with the debug flip hook
@@ -178,8 +196,8 @@ __global__ void coarse_rows_kernel(BlockArgs a, const int* row_owner /* npf x 4 
   }
 }
 
-/// Gsum = sum over this workspace's subdomains of the corner Grams -(Q_Pi Q_Pi^T), scattered to
-/// (Pi, Pi). Thread per entry: the subdomains owning corner rp (pi_owner, ascending subdomain
+/// Gsum = sum over the subdomains of the corner Grams -(Q_Pi Q_Pi^T), scattered to (Pi, Pi).
+/// Thread per entry: the subdomains owning corner rp (pi_owner, ascending global subdomain
 /// order), each adding its Gram entry against corner rq if it owns that corner too — the order
 /// of the serial subdomain loop this replaces, so the sums are bit-identical.
 __global__ void __launch_bounds__(256) coarse_gsum_kernel(BlockArgs a) {
@@ -191,12 +209,9 @@ __global__ void __launch_bounds__(256) coarse_gsum_kernel(BlockArgs a) {
   for (int k = 0; k < 4; ++k) {
     const int own = a.pi_owner[rp * 4 + k];
     if (own < 0) continue;
-    const int i = own / ncq, p = own % ncq;
-    for (int q = 0; q < ncq; ++q) {
-      const int g = a.corner_q[i * ncq + q];
-      if (g >= 0 && a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] == rq)
-        s += a.Gc[(static_cast<size_t>(i) * ncq + p) * ncq + q];
-    }
+    const int ig = own / ncq, p = own % ncq;
+    for (int q = 0; q < ncq; ++q)
+      if (a.cpi_g[ig * ncq + q] == rq) s += a.gc_g[(static_cast<size_t>(ig) * ncq + p) * ncq + q];
   }
   a.Gsum[idx] = s;
 }
@@ -356,8 +371,13 @@ void launch_coarse_local(const BlockArgs& a, const int* cr_row, const int* cr_of
   DDG_LAUNCH_CHECK();
 }
 
-void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t st) {
-  coarse_rows_kernel<<<a.npf, 128, 0, st>>>(a, row_owner);
+void launch_coarse_export(const BlockArgs& a, cudaStream_t st) {
+  coarse_export_kernel<<<a.N, 128, 0, st>>>(a);
+  DDG_LAUNCH_CHECK();
+}
+
+void launch_coarse_rows(const BlockArgs& a, cudaStream_t st) {
+  coarse_rows_kernel<<<a.npf, 128, 0, st>>>(a);
   DDG_LAUNCH_CHECK();
 }
 

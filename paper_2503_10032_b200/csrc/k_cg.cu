@@ -731,8 +731,10 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, 
     double vv = 0.0;
     if (dg >= 0 && mode != 1) {
       if (cg) {
-        vv = a.r[dg] + beta * pcur[dg];
-        if (dg < a.n_delta && a.gamma_dst[static_cast<size_t>(i) * a.gmax + g] == 2 * dg) pnext[dg] = vv;  // first owner
+        // p_next = r + beta p_cur (solvers.cpp:116), the same rounding as XR1's replicated update;
+        // every local owner stores it for OP4 (a sharded rank may hold only the second owner)
+        vv = __fma_rn(beta, pcur[dg], a.r[dg]);
+        if (dg < a.n_delta) pnext[dg] = vv;
       } else {
         vv = v[dg];
       }
@@ -761,7 +763,7 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, 
     if (cg && threadIdx.x < a.ncq) {
       const int g = a.corner_q[i * a.ncq + threadIdx.x];
       const int dst = a.corner_dst[i * a.ncq + threadIdx.x];
-      if (g >= 0 && dst >= 0 && (dst & 3) == 0) pnext[a.n_delta + gpi[g]] = vg[g];
+      if (g >= 0 && dst >= 0) pnext[a.n_delta + gpi[g]] = vg[g];
     }
   } else if (warp < a.ncq) {
     const int g = a.corner_q[i * a.ncq + warp];
@@ -1373,7 +1375,9 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
   if (cg && !streamed) it = a.state[6];  // the iteration counter lives on the device (graph replays)
   double* pcur = a.pbuf[(it + 1) & 1];
   double* pnext = a.pbuf[it & 1];
-  if (cg && !streamed && a.state[1]) {  // converged / aborted earlier: drain prefetched copies, leave
+  // converged / aborted earlier (the chunked sharded driver also replays streamed phases past the
+  // stop: guard_all): drain the prefetched copies and leave
+  if (cg && (!streamed || a.guard_all) && a.state[1]) {
     if ((phase == kPhXr1 || phase == kPhXr2) && b == 0 && threadIdx.x == 0 && a.cond != 0)
       cudaGraphSetConditional(a.cond, 0);
     __shared__ int s_issued;
@@ -1445,10 +1449,15 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
           return;
         }
         const double alpha = a.scal[0] / pAp;
+        const double beta = a.scal[2];  // read before arriving: the last CTA overwrites it below
         double dsum = 0;
         for (int g = b * blockDim.x + threadIdx.x; g < a.n_cg; g += G * blockDim.x) {
           const double ap = gather_out(a, g);
-          a.x[g] += alpha * pnext[g];
+          // p = r + beta p_cur on EVERY index (replicated CG vectors: a sharded rank's OP1 writes
+          // only the indices its subdomains touch); bitwise the value OP1 stored
+          const double pn = __fma_rn(beta, pcur[g], a.r[g]);
+          pnext[g] = pn;
+          a.x[g] += alpha * pn;
           const double rg = a.r[g] - alpha * ap;
           a.r[g] = rg;
           dsum += rg * rg;
@@ -1633,6 +1642,64 @@ void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double*
     DDG_CUDA(cudaLaunchKernelEx(&cfg, cg_phase_kernel<16>, a, phase, mode, it, vin, vout));
   else
     DDG_CUDA(cudaLaunchKernelEx(&cfg, cg_phase_kernel<32>, a, phase, mode, it, vin, vout));
+}
+
+namespace {
+/// out[k] = the P-part sum of table slot e[k] in the consumers' order (sum_parts): what a reader
+/// of the slot would gather, so the importer's single stored value reproduces its sum bit for bit
+__global__ void __launch_bounds__(256) xpack_kernel(XTabs t, const XEntry* e, int n, double* out, const int* state) {
+  if (state != nullptr && state[1]) return;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const XEntry x = e[k];
+    const double* base = t.ptr[x.table];
+    const int parts = t.parts[x.table];
+    const long long ps = t.pstride[x.table];
+    double s = 0;
+    for (int p = 0; p < parts; ++p) s += base[p * ps + x.idx];
+    out[k] = s;
+  }
+}
+/// table slot e[k] (part 0) = in[k]; the other parts of an imported slot stay zero
+__global__ void __launch_bounds__(256) xunpack_kernel(XTabs t, const XEntry* e, int n, const double* in, const int* state) {
+  if (state != nullptr && state[1]) return;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const XEntry x = e[k];
+    t.ptr[x.table][x.idx] = in[k];
+  }
+}
+}  // namespace
+
+XTabs cg_xtabs(const CgArgs& a) {
+  XTabs t{};
+  auto set = [&](int id, double* p, int parts, long long ps) {
+    t.ptr[id] = p;
+    t.parts[id] = parts;
+    t.pstride[id] = ps;
+  };
+  const long long nd2 = 2LL * a.n_delta, npi4 = 4LL * a.n_pi, npf4 = 4LL * a.npf;
+  set(kTabT, a.ttab, 1, 0);
+  set(kTabPsi, a.ptab, 1, 0);
+  set(kTabT3, a.t3tab, a.P, npi4);
+  set(kTabO, a.otab, 1, 0);
+  set(kTabX, a.xtab, a.P, nd2);
+  set(kTabTr, a.trtab, a.P, nd2);
+  set(kTabZz, a.zztab, a.P, nd2);
+  set(kTabXc, a.xctab, a.P, npf4);
+  set(kTabOpi, a.opitab, 1, 0);
+  set(kTabPap, a.pap, 1, 0);
+  return t;
+}
+
+void launch_xpack(const XTabs& t, const XEntry* e, int n, double* out, const int* state, cudaStream_t st) {
+  if (n <= 0) return;
+  xpack_kernel<<<std::min(148, ceil_div(n, 256)), 256, 0, st>>>(t, e, n, out, state);
+  DDG_LAUNCH_CHECK();
+}
+
+void launch_xunpack(const XTabs& t, const XEntry* e, int n, const double* in, const int* state, cudaStream_t st) {
+  if (n <= 0) return;
+  xunpack_kernel<<<std::min(148, ceil_div(n, 256)), 256, 0, st>>>(t, e, n, in, state);
+  DDG_LAUNCH_CHECK();
 }
 
 void cg_launch_init(const CgArgs& a, cudaStream_t st) {

@@ -202,6 +202,104 @@ void dense_cod_solve(const double* X, int ldx, int m, int n, const double* R, in
   DDG_CUDA(cudaStreamSynchronize(st));  // the scope frees the scratch
 }
 
+// ------------------------------------------------------------------ LsFactor on caller matrices
+void lsfactor_batch(int nmat, int m, int n, const double* K, double rank_tol, int* rank, int* deficient, int* reff,
+                    double* pinv, double* Q, cudaStream_t st) {
+  // LsFactor (solvers.cpp:24-45) of nmat caller-supplied m x n matrices through the hot path's own
+  // kernels: batched blocked QR of [K | I_m] (the appended identity turns Q_r^T [f | E] into Q_r^T
+  // itself), the diagonal-ratio branch test, the pivoted QR + RZ on R0 and the finish; then
+  // K^+ = C Q_r^T (dense_gemm) and Q_r = (Q_r^T)^T.
+  if (nmat < 1 || m < 1 || n < 1) throw std::invalid_argument("lsfactor_batch: empty batch");
+  if (m < n) throw std::invalid_argument("LsFactor: matrix must be square or tall");
+  if (!(rank_tol > 0)) throw std::invalid_argument("lsfactor_batch: rank_tol must be positive");
+  DevScope s;
+  const int ld = (m + 3) / 4 * 4, ncol = n + m;
+  const size_t ms = static_cast<size_t>(ld) * ncol;
+  double* A = s.d(ms * nmat);
+  DDG_CUDA(cudaMemsetAsync(A, 0, sizeof(double) * ms * nmat, st));
+  std::vector<double> eye(static_cast<size_t>(ld) * m, 0.0);
+  for (int j = 0; j < m; ++j) eye[static_cast<size_t>(j) * ld + j] = 1.0;
+  for (int t = 0; t < nmat; ++t) {
+    DDG_CUDA(cudaMemcpy2DAsync(A + t * ms, sizeof(double) * ld, K + static_cast<size_t>(t) * m * n, sizeof(double) * m,
+                               sizeof(double) * m, n, cudaMemcpyHostToDevice, st));
+    DDG_CUDA(cudaMemcpyAsync(A + t * ms + static_cast<size_t>(n) * ld, eye.data(), sizeof(double) * eye.size(),
+                             cudaMemcpyHostToDevice, st));
+  }
+  double* tau = s.d(static_cast<size_t>(nmat) * n);
+  double* T = s.d(static_cast<size_t>(nmat) * kQrTmax * kQrTmax);
+  double* ratio = s.d(2 * static_cast<size_t>(nmat));
+  QrArgs q{nmat, m, ld, ncol, n, A, tau, T};
+  std::vector<cudaEvent_t> none;
+  qr_factor(q, st, nullptr, none);
+  launch_qr_diag_ratio(q, ratio, st);
+  CodArgs c{};
+  c.nmat = nmat;
+  c.m = m;
+  c.ld = ld;
+  c.ncol = ncol;
+  c.M = n;
+  c.kmax = n;
+  c.rmax = n;
+  c.ext = m;
+  c.rank_tol = rank_tol;
+  c.A = A;
+  c.ratio = ratio;
+  std::vector<void*>& P = s.ptrs;
+  const size_t nn = static_cast<size_t>(n) * n * nmat;
+  c.deficient = dev_alloc<int>(nmat, P);
+  c.V1 = s.d(nn);
+  c.F1 = s.d(nn);
+  c.Rr = s.d(nn);
+  c.tau1 = s.d(static_cast<size_t>(n) * nmat);
+  c.upd = s.d(static_cast<size_t>(n) * nmat);
+  c.dir = s.d(static_cast<size_t>(n) * nmat);
+  c.perm = dev_alloc<int>(static_cast<size_t>(n) * nmat, P);
+  c.rank = dev_alloc<int>(nmat, P);
+  c.status = dev_alloc<int>(nmat, P);
+  c.reff = dev_alloc<int>(nmat, P);
+  c.zc = s.d(static_cast<size_t>(n) * nmat);
+  c.C = s.d(nn);
+  c.QtX = s.d(static_cast<size_t>(n) * m * nmat);
+  c.Ywork = s.d(nn);
+  launch_cod_pivqr(c, st);
+  std::vector<int> hd(nmat), hr(nmat), hs(nmat), he(nmat);
+  DDG_CUDA(cudaMemcpyAsync(hd.data(), c.deficient, sizeof(int) * nmat, cudaMemcpyDeviceToHost, st));
+  DDG_CUDA(cudaMemcpyAsync(hr.data(), c.rank, sizeof(int) * nmat, cudaMemcpyDeviceToHost, st));
+  DDG_CUDA(cudaMemcpyAsync(hs.data(), c.status, sizeof(int) * nmat, cudaMemcpyDeviceToHost, st));
+  DDG_CUDA(cudaMemcpyAsync(he.data(), c.reff, sizeof(int) * nmat, cudaMemcpyDeviceToHost, st));
+  DDG_CUDA(cudaStreamSynchronize(st));
+  for (int t = 0; t < nmat; ++t) {
+    if (hs[t] != 0) throw std::runtime_error("lsfactor_batch: pivoted QR capacity exceeded");
+    if (hd[t] && !cod_finish_supports(n, hr[t]))
+      throw std::invalid_argument("lsfactor_batch: rank-deficient matrix wider than the device COD finish");
+  }
+  launch_cod_finish(c, st);
+  double* Pd = s.d(static_cast<size_t>(n) * m);
+  for (int t = 0; t < nmat; ++t) {
+    // C(i, k) = C[t][i * n + k] (k < r), QtX(k, j) = QtX[t][k * m + j]: K^+ = C QtX (n x m)
+    const double* Ct = c.C + static_cast<size_t>(t) * n * n;
+    const double* Xt = c.QtX + static_cast<size_t>(t) * n * m;
+    DDG_CUDA(cudaMemsetAsync(Pd, 0, sizeof(double) * n * m, st));
+    if (hr[t] > 0) dense_gemm(n, m, hr[t], 1.0, Ct, n, true, Xt, m, true, 0.0, Pd, n, st);
+    DDG_CUDA(cudaMemcpyAsync(pinv + static_cast<size_t>(t) * n * m, Pd, sizeof(double) * n * m, cudaMemcpyDeviceToHost, st));
+    if (Q) {
+      // Q_r (m x n, columns >= r zero) = QtX^T: QtX is r x m row-major = Q_r column-major
+      std::vector<double> qt(static_cast<size_t>(n) * m);
+      DDG_CUDA(cudaMemcpyAsync(qt.data(), Xt, sizeof(double) * qt.size(), cudaMemcpyDeviceToHost, st));
+      DDG_CUDA(cudaStreamSynchronize(st));
+      double* Qt = Q + static_cast<size_t>(t) * m * n;
+      for (int k = 0; k < n; ++k)
+        for (int j = 0; j < m; ++j) Qt[static_cast<size_t>(k) * m + j] = k < hr[t] ? qt[static_cast<size_t>(k) * m + j] : 0.0;
+    }
+  }
+  DDG_CUDA(cudaStreamSynchronize(st));
+  for (int t = 0; t < nmat; ++t) {
+    rank[t] = hr[t];
+    deficient[t] = hd[t];
+    if (reff) reff[t] = he[t];
+  }
+}
+
 // ------------------------------------------------------------------ Workspace::dense_oracle
 void Workspace::dense_oracle(int method, double theta, DenseOracleOut& o) {
   if (sharded()) throw std::invalid_argument("dense_oracle_solve: single-device workspaces only");

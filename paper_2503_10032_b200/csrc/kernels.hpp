@@ -101,6 +101,12 @@ void dense_gemm(int m, int n, int k, double alpha, const double* A, int lda, boo
 void dense_cod_solve(const double* X, int ldx, int m, int n, const double* R, int ldr, int e, double* out, int ldo,
                      cudaStream_t st, int* rank_out);
 
+/// LsFactor (solvers.cpp:24-45) of nmat caller matrices K (host, m x n column-major each) on the
+/// hot path's QR / COD kernels: rank, branch, R0 rows kept by the pivoted factorisation (reff),
+/// K^+ (host, n x m each) and optionally Q_r (host, m x n each, columns >= rank zero)
+void lsfactor_batch(int nmat, int m, int n, const double* K, double rank_tol, int* rank, int* deficient, int* reff,
+                    double* pinv, double* Q, cudaStream_t st);
+
 // ---------------------------------------------------------------- interface blocks (k_blocks.cu)
 /// Corner (Pi) rows per subdomain: 4 corners x cc components (cc = 2: biharmonic).
 constexpr int kMaxCq = 8;
@@ -138,13 +144,20 @@ struct BlockArgs {
   const int* mult_pi;    // n_pi
   int* spd_fail;         // 1 flag
   int flip_row;          // debug_flip_flux_row (global flux row) or -1
-  const int* row_owner;  // npf x 4 : contributing (i * crmax + rho), subdomain order, -1 pad
-  const int* pi_owner;   // n_pi x 4 : corner owners (i * ncq + slot), subdomain order, -1 pad
+  const int* row_owner;  // npf x 4 : contributing (ig * crmax + rho), global subdomain order, -1 pad
+  const int* pi_owner;   // n_pi x 4 : corner owners (ig * ncq + slot), global subdomain order, -1 pad
+  const int* cpi_g;      // N_global x ncq : Pi index of each corner slot (-1 pad)
+  int sub_lo, N_global;  // this device's strip [sub_lo, sub_lo + N)
+  double* pd_g;          // N_global x crmax              (coarse_export; all-reduced when sharded)
+  double* zcc_g;         // N_global x crmax x ncq : Zc at the corner slots
+  double* gc_g;          // N_global x ncq x ncq   : corner Grams
 };
 void launch_blocks(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_local(const BlockArgs& a, const int* cr_row, const int* cr_off, const int* cr_l,
                          const double* cr_w, cudaStream_t st);
-void launch_coarse_rows(const BlockArgs& a, const int* row_owner, cudaStream_t st);
+/// pd / Zc corners / Gc of the local subdomains into the global compact arrays (pd_g, zcc_g, gc_g)
+void launch_coarse_export(const BlockArgs& a, cudaStream_t st);
+void launch_coarse_rows(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_gsum(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_schur(const BlockArgs& a, cudaStream_t st);
 void launch_coarse_weights(const BlockArgs& a, cudaStream_t st);
@@ -250,6 +263,7 @@ struct CgArgs {
   int N_global, sub_lo;     // sharding: this device holds subdomains [sub_lo, sub_lo + N)
   int xr_parts;             // r.r partials written by the XR phase (= its grid size)
   unsigned long long cond;  // cudaGraphConditionalHandle of the CG while-loop graph (0: none)
+  int guard_all;            // chunked driver: every phase (streamed ones too) leaves once state[1] is set
   double* u;      // P x N x rmax
   double *pap, *pap_w;  // N_global : p . o_i (indexed by global subdomain)
   // CG vectors
@@ -279,6 +293,18 @@ void cg_launch_phase(const CgArgs& a, int phase, int mode, int it, const double*
                      cudaStream_t st);
 void cg_launch_init(const CgArgs& a, cudaStream_t st);
 int cg_grid(const CgArgs& a);
+
+/// The owner-slot tables of one CgArgs as the exchange kernels see them (plan.hpp XTable ids).
+struct XTabs {
+  double* ptr[kTabCount];
+  int parts[kTabCount];
+  long long pstride[kTabCount];
+};
+XTabs cg_xtabs(const CgArgs& a);
+/// out[k] = P-part sum of slot e[k] (skipped once state[1] is set when state != nullptr)
+void launch_xpack(const XTabs& t, const XEntry* e, int n, double* out, const int* state, cudaStream_t st);
+/// slot e[k] (part 0) = in[k]
+void launch_xunpack(const XTabs& t, const XEntry* e, int n, const double* in, const int* state, cudaStream_t st);
 int cg_rows_per_chunk_max(const CgArgs& a);
 
 

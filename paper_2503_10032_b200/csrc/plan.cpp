@@ -467,7 +467,33 @@ Plan shard_plan(const Plan& g, int lo, int hi) {
       xdst[static_cast<size_t>(i) * g.crmax + rho] = r * 4 + row_n[r]++;
     }
   }
+  // global coarse owner tables (cross rows / Pi indices -> global (subdomain, slot)) and the Pi
+  // index of every corner slot
+  std::vector<int> rown(static_cast<size_t>(std::max(g.npf, 1)) * 4, -1), pown(static_cast<size_t>(std::max(g.n_pi, 1)) * 4, -1);
+  std::vector<int> cpi(static_cast<size_t>(N) * g.ncq, -1);
+  auto push_owner = [](std::vector<int>& v, int row, int val) {
+    for (int q = 0; q < 4; ++q)
+      if (v[static_cast<size_t>(row) * 4 + q] < 0) {
+        v[static_cast<size_t>(row) * 4 + q] = val;
+        return;
+      }
+    throw std::logic_error("owner table overflow");
+  };
+  for (int i = 0; i < N; ++i) {
+    const SubPlan& sp = g.subs[i];
+    int slot = 0;
+    for (size_t q = 0; q < sp.gamma_pi.size(); ++q)
+      if (sp.gamma_pi[q] >= 0 && slot < g.ncq) {
+        push_owner(pown, sp.gamma_pi[q], i * g.ncq + slot);
+        cpi[static_cast<size_t>(i) * g.ncq + slot++] = sp.gamma_pi[q];
+      }
+    for (size_t rho = 0; rho < sp.cross_rows.size(); ++rho)
+      push_owner(rown, sp.cross_rows[rho].r, i * g.crmax + static_cast<int>(rho));
+  }
   Plan p = g;
+  p.row_owner_g = std::move(rown);
+  p.pi_owner_g = std::move(pown);
+  p.cpi_g = std::move(cpi);
   p.N = hi - lo;
   p.sub_lo = lo;
   p.N_global = g.N;
@@ -495,6 +521,111 @@ Plan shard_plan(const Plan& g, int lo, int hi) {
   remap(p.own_flux, g.fmax);
   remap(p.own_nd, g.dmax);
   return p;
+}
+
+XPlan build_exchange_plan(const Plan& g, int rank, int world) {
+  if (!g.gamma_dst.empty() || g.sub_lo != 0) throw std::logic_error("build_exchange_plan: needs the global plan (build_plan)");
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("build_exchange_plan: bad rank / world");
+  const int N = g.N;
+  XPlan xp;
+  xp.rank = rank;
+  xp.world = world;
+  std::vector<int> rank_of(N);
+  for (int r = 0; r < world; ++r) {
+    int lo, hi;
+    shard_range(N, r, world, &lo, &hi);
+    for (int i = lo; i < hi; ++i) rank_of[i] = r;
+  }
+  const int nd = g.n_delta;
+  // writers: Delta tables by owner pair (own_* hold i * width + pos), corner / cross slots in
+  // subdomain order (the numbering of shard_plan's corner_dst / cross_dst)
+  auto delta_writers = [&](const std::vector<int>& own, int w) {
+    std::vector<int> wr(2 * static_cast<size_t>(nd), -1);
+    for (size_t k = 0; k < wr.size(); ++k)
+      if (own[k] >= 0) wr[k] = rank_of[own[k] / w];
+    return wr;
+  };
+  const std::vector<int> w_o = delta_writers(g.own_gamma, g.gmax), w_x = delta_writers(g.own_flux, g.fmax),
+                         w_nd = delta_writers(g.own_nd, g.dmax);
+  std::vector<int> w_pi(4 * static_cast<size_t>(std::max(g.n_pi, 1)), -1), w_cr(4 * static_cast<size_t>(std::max(g.npf, 1)), -1);
+  {
+    std::vector<int> pi_n(std::max(g.n_pi, 1), 0), row_n(std::max(g.npf, 1), 0);
+    for (int i = 0; i < N; ++i) {
+      const SubPlan& sp = g.subs[i];
+      for (size_t q = 0; q < sp.gamma_pi.size(); ++q)
+        if (sp.gamma_pi[q] >= 0) {
+          const int gp = sp.gamma_pi[q];
+          w_pi[static_cast<size_t>(gp) * 4 + pi_n[gp]++] = rank_of[i];
+        }
+      for (const CrossRow& cr : sp.cross_rows) w_cr[static_cast<size_t>(cr.r) * 4 + row_n[cr.r]++] = rank_of[i];
+    }
+  }
+  // readers of a Delta index: the ranks of every subdomain touching it (trace, flux or Neumann row)
+  std::vector<unsigned long long> dread(std::max(nd, 1), 0ull);
+  if (world > 64) throw std::invalid_argument("build_exchange_plan: at most 64 ranks");
+  for (int i = 0; i < N; ++i) {
+    const SubPlan& sp = g.subs[i];
+    const unsigned long long bit = 1ull << rank_of[i];
+    for (int d : sp.gamma_delta)
+      if (d >= 0) dread[d] |= bit;
+    for (int d : sp.fluxrow_delta)
+      if (d >= 0) dread[d] |= bit;
+    for (int d : sp.ndelta_map)
+      if (d >= 0) dread[d] |= bit;
+  }
+  // (table, slot count per part, writer rank of a slot, whether rank q reads the slot)
+  struct Tab {
+    int id;
+    const std::vector<int>* writer;  // nullptr: pap (slot i written by rank_of[i])
+    bool delta;                      // readers = the touching ranks; else every rank
+  };
+  auto tabs_of = [&](int one, int pt) -> std::vector<Tab> {
+    switch (pt) {
+      case kXOp1: return one ? std::vector<Tab>{} : std::vector<Tab>{{kTabT, &w_pi, false}, {kTabPsi, &w_cr, false}};
+      case kXOp2: return one ? std::vector<Tab>{{kTabX, &w_x, true}, {kTabXc, &w_cr, false}} : std::vector<Tab>{{kTabX, &w_x, true}};
+      case kXNn1: return one ? std::vector<Tab>{} : std::vector<Tab>{{kTabTr, &w_nd, true}};
+      case kXNn2: return one ? std::vector<Tab>{} : std::vector<Tab>{{kTabZz, &w_nd, true}};
+      case kXOp3: return one ? std::vector<Tab>{} : std::vector<Tab>{{kTabT3, &w_pi, false}};
+      default:
+        return one ? std::vector<Tab>{{kTabO, &w_o, false}, {kTabOpi, &w_pi, false}, {kTabPap, nullptr, false}}
+                   : std::vector<Tab>{{kTabO, &w_o, false}, {kTabPap, nullptr, false}};
+    }
+  };
+  // the O table feeds the replicated CG update (every rank reads all of it)
+  auto list = [&](int one, int pt, int src, int dst, std::vector<XEntry>& out) {
+    for (const Tab& t : tabs_of(one, pt)) {
+      const int n = t.writer ? static_cast<int>(t.writer->size()) : N;
+      for (int k = 0; k < n; ++k) {
+        const int w = t.writer ? (*t.writer)[k] : rank_of[k];
+        if (w != src) continue;
+        const bool reads = t.delta ? ((dread[k / 2] >> dst) & 1ull) != 0 : true;
+        if (reads) out.push_back(XEntry{t.id, k});
+      }
+    }
+  };
+  size_t mx = 8;
+  for (int one = 0; one < 2; ++one)
+    for (int pt = 0; pt < kXPoints; ++pt) {
+      XList& L = xp.pt[one][pt];
+      L.soff.assign(world, 0);
+      L.scnt.assign(world, 0);
+      L.roff.assign(world, 0);
+      L.rcnt.assign(world, 0);
+      for (int q = 0; q < world; ++q) {
+        if (q == rank) continue;
+        L.soff[q] = static_cast<int>(L.send.size());
+        list(one, pt, rank, q, L.send);
+        L.scnt[q] = static_cast<int>(L.send.size()) - L.soff[q];
+        L.roff[q] = static_cast<int>(L.recv.size());
+        list(one, pt, q, rank, L.recv);
+        L.rcnt[q] = static_cast<int>(L.recv.size()) - L.roff[q];
+        mx = std::max(mx, static_cast<size_t>(std::max(L.scnt[q], L.rcnt[q])));
+      }
+    }
+  // the setup all-reduce of the coarse inputs (workspace.cu build_coarse) and the metric sums
+  const size_t coarse = static_cast<size_t>(N) * g.crmax * (1 + g.ncq) + static_cast<size_t>(N) * g.ncq * g.ncq;
+  xp.max_msg = std::max(mx, coarse + 1) + 64;  // + the padding entry of the coarse buffer, slack
+  return xp;
 }
 
 void init_layer(const Plan& p, int i, double* w0, double* w1, double* b) {

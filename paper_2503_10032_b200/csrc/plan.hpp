@@ -137,10 +137,40 @@ struct Plan {
   // owner-slot destinations (global slot numbering, so that every slot has exactly one writer
   // across all ranks): gamma/flux/nd -> 2 g + s, corner -> gp * 4 + slot, cross -> rr * 4 + slot
   std::vector<int> gamma_dst, flux_dst, nd_dst, corner_dst, cross_dst;
+  // coarse assembly over the GLOBAL subdomain numbering (so that a sharded build sums exactly the
+  // single-device terms in the single-device order): owners of every cross-flux row
+  // (ig * crmax + rho) and of every Pi index (ig * ncq + corner slot), subdomain order, -1 pad;
+  // cpi_g: Pi index of corner slot q of subdomain ig (-1 pad)
+  std::vector<int> row_owner_g, pi_owner_g, cpi_g;
+};
+
+/// Exchange points of one interface iteration (after the producing phase, k_cg.cu) and the
+/// owner-slot tables each one carries (CgArgs *tab).
+enum XPoint { kXOp1 = 0, kXOp2, kXNn1, kXNn2, kXOp3, kXOp4, kXPoints };
+enum XTable { kTabT = 0, kTabPsi, kTabT3, kTabO, kTabX, kTabTr, kTabZz, kTabXc, kTabOpi, kTabPap, kTabCount };
+/// one slot of one table (tables with P row parts: idx within a part; the exporter sends the
+/// P-part sum, the importer stores it in part 0)
+struct XEntry {
+  int table, idx;
+};
+/// Per-peer segments of one exchange point: send[soff[q] .. +scnt[q]) to rank q, recv likewise.
+struct XList {
+  std::vector<int> soff, scnt, roff, rcnt;
+  std::vector<XEntry> send, recv;
+};
+/// The sharded path's whole communication plan: for each method family (0 coarse methods,
+/// 1 one-level) and exchange point, which slots this rank exports to / imports from each peer.
+/// Built identically on every rank from the global plan, so the pairwise lists agree.
+struct XPlan {
+  int rank = 0, world = 1;
+  XList pt[2][kXPoints];
+  size_t max_msg = 0;  // largest per-peer segment or all-reduce (doubles): host mailbox size
 };
 
 /// The strip of subdomains [lo, hi) of a global plan, with global owner slots (see Plan).
 Plan shard_plan(const Plan& g, int lo, int hi);
+/// The communication plan of `rank` (global plan g, contiguous strips of shard_range).
+XPlan build_exchange_plan(const Plan& g, int rank, int world);
 /// Contiguous balanced partition of N subdomains over `world` ranks: [lo, hi) of `rank`.
 void shard_range(int N, int rank, int world, int* lo, int* hi);
 

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <chrono>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <thread>
 #include <vector>
@@ -68,9 +69,10 @@ template struct DevBuf<Task>;
 template struct DevBuf<ClassDims>;
 template struct DevBuf<SubGeo>;
 template struct DevBuf<long long>;
+template struct DevBuf<XEntry>;
 
-Workspace::Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex)
-    : plan(p), ex_(std::move(ex)), device_(device) {
+Workspace::Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex, XPlan xp)
+    : plan(p), ex_(std::move(ex)), xplan_(std::move(xp)), device_(device) {
   // default: phase-by-phase kernels in one CUDA graph (a device-side while loop) — measured faster
   // than the single persistent cooperative kernel (C3 CG 31 vs 43 ms, C4 143 vs 207 ms);
   // DDELM_CG_MODE=persistent selects the persistent kernel (single device only)
@@ -88,10 +90,28 @@ Workspace::Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex)
   DDG_CUDA(cudaStreamCreateWithFlags(&cap_, cudaStreamNonBlocking));
   for (auto& e : ev_) DDG_CUDA(cudaEventCreate(&e));
   DDG_CUDA(cudaMallocHost(&pinned_state_, 64));
-  if (sharded()) phased_ = true;
+  if (sharded()) {
+    phased_ = true;
+    if (xplan_.world != ex_->world() || xplan_.rank != ex_->rank())
+      throw std::logic_error("sharded workspace: exchange plan and communicator disagree");
+  }
   arena_.cap = size_t(64) << 20;
   DDG_CUDA(cudaMalloc(reinterpret_cast<void**>(&arena_.base), arena_.cap));
   upload_plan();
+  if (sharded()) {
+    size_t smax = 1, rmax = 1;
+    for (int one = 0; one < 2; ++one)
+      for (int pt = 0; pt < kXPoints; ++pt) {
+        const XList& L = xplan_.pt[one][pt];
+        d_xsend[one][pt].upload(L.send, st_);
+        d_xrecv[one][pt].upload(L.recv, st_);
+        smax = std::max(smax, L.send.size());
+        rmax = std::max(rmax, L.recv.size());
+      }
+    d_xsbuf.alloc(smax);
+    d_xrbuf.alloc(rmax);
+    DDG_CUDA(cudaStreamSynchronize(st_));
+  }
 }
 
 void Workspace::apply_l2_policy() {
@@ -158,16 +178,6 @@ void Workspace::upload_plan() {
   std::vector<int> crr(static_cast<size_t>(N) * p.crmax, -1), croff(static_cast<size_t>(N) * (p.crmax + 1), 0);
   std::vector<int> crl;
   std::vector<double> crw;
-  std::vector<int> row_owner(static_cast<size_t>(std::max(p.npf, 1)) * 4, -1);
-  std::vector<int> pi_owner(static_cast<size_t>(std::max(p.n_pi, 1)) * 4, -1);
-  auto push_owner = [](std::vector<int>& v, int row, int val) {
-    for (int q = 0; q < 4; ++q)
-      if (v[static_cast<size_t>(row) * 4 + q] < 0) {
-        v[static_cast<size_t>(row) * 4 + q] = val;
-        return;
-      }
-    throw std::logic_error("owner table overflow");
-  };
   for (int i = 0; i < N; ++i) {
     const SubPlan& sp = p.subs[i];
     cls[i] = sp.cls;
@@ -177,9 +187,6 @@ void Workspace::upload_plan() {
       gdel[static_cast<size_t>(i) * p.gmax + q] = sp.gamma_delta[q];
       gpi[static_cast<size_t>(i) * p.gmax + q] = sp.gamma_pi[q];
     }
-    int slot = 0;
-    for (size_t q = 0; q < sp.gamma_pi.size(); ++q)
-      if (sp.gamma_pi[q] >= 0) push_owner(pi_owner, sp.gamma_pi[q], i * p.ncq + slot++);
     for (size_t l = 0; l < sp.fluxrow_delta.size(); ++l) fdel[static_cast<size_t>(i) * p.fmax + l] = sp.fluxrow_delta[l];
     for (size_t k = 0; k < sp.ndelta_map.size(); ++k) nmap[static_cast<size_t>(i) * p.dmax + k] = sp.ndelta_map[k];
     int* o = croff.data() + static_cast<size_t>(i) * (p.crmax + 1);
@@ -188,7 +195,6 @@ void Workspace::upload_plan() {
       if (rho < static_cast<int>(sp.cross_rows.size())) {
         const CrossRow& cr = sp.cross_rows[rho];
         crr[static_cast<size_t>(i) * p.crmax + rho] = cr.r;
-        push_owner(row_owner, cr.r, i * p.crmax + rho);
         for (auto [l, w] : cr.e) {
           crl.push_back(l);
           crw.push_back(w);
@@ -208,8 +214,11 @@ void Workspace::upload_plan() {
   d_cr_off.upload(croff, st_);
   d_cr_l.upload(crl, st_);
   d_cr_w.upload(crw, st_);
-  d_row_owner.upload(row_owner, st_);
-  d_pi_owner.upload(pi_owner, st_);
+  // coarse owners over the global subdomain numbering (shard_plan)
+  if (p.row_owner_g.empty() || p.cpi_g.empty()) throw std::logic_error("plan without global coarse owners (use shard_plan)");
+  d_row_owner.upload(p.row_owner_g, st_);
+  d_pi_owner.upload(p.pi_owner_g, st_);
+  d_cpi_g.upload(p.cpi_g, st_);
   // owner-slot destinations (global slot numbering from shard_plan): producers write their
   // contribution to slot s of the quantity, readers sum the slots contiguously in owner order
   if (p.gamma_dst.empty()) throw std::logic_error("plan without owner slots (use shard_plan)");
@@ -269,6 +278,8 @@ void Workspace::upload_plan() {
   g_arena = nullptr;
   d_pd.alloc(static_cast<size_t>(N) * p.crmax);
   d_Gc.alloc(static_cast<size_t>(N) * p.ncq * p.ncq);
+  // coarse inputs in the global numbering: [pd_g | zcc_g | gc_g] (one all-reduce when sharded)
+  d_cin.alloc(static_cast<size_t>(p.N_global) * (p.crmax * (1 + p.ncq) + p.ncq * p.ncq) + 1);
   d_Ypi.alloc(static_cast<size_t>(N) * p.M * p.ncq);
   g_arena = &arena_;  // coarse rows and CG vectors: hot
   d_corner_q.alloc(static_cast<size_t>(N) * p.ncq);
@@ -565,6 +576,12 @@ BlockArgs Workspace::block_args() {
   b.flip_row = p.debug_flip_flux_row;
   b.row_owner = d_row_owner.ptr;
   b.pi_owner = d_pi_owner.ptr;
+  b.cpi_g = d_cpi_g.ptr;
+  b.sub_lo = p.sub_lo;
+  b.N_global = p.N_global;
+  b.pd_g = d_cin.ptr;
+  b.zcc_g = b.pd_g + static_cast<size_t>(p.N_global) * p.crmax;
+  b.gc_g = b.zcc_g + static_cast<size_t>(p.N_global) * p.crmax * p.ncq;
   return b;
 }
 
@@ -591,15 +608,17 @@ void Workspace::build_coarse() {
   BlockArgs b = block_args();
   DDG_CUDA(cudaMemsetAsync(d_spd_fail.ptr, 0, sizeof(int), st_));
   if (plan.n_pi > 0) {
-    launch_coarse_rows(b, d_row_owner.ptr, st_);
+    // the coarse inputs of every subdomain in the global numbering; a sharded rank holds its
+    // strip's rows only and all-reduces the rest (one writer per entry: exact), so Dpp, dpi and
+    // the corner-Gram sum are formed from the same terms in the same order on every rank
+    DDG_CUDA(cudaMemsetAsync(d_cin.ptr, 0, d_cin.count * sizeof(double), st_));
+    launch_coarse_export(b, st_);
+    if (sharded()) ex_->allreduce(d_cin.ptr, d_cin.ptr, d_cin.count, st_);
+    launch_coarse_rows(b, st_);
     launch_coarse_gsum(b, st_);
-    // sharded: this device holds only its strip's contributions to Dpp, dpi and the corner Grams
-    xchg(d_Dpp.ptr, d_Dpp.ptr, static_cast<size_t>(plan.npf) * plan.n_pi);
-    xchg(d_dpi.ptr, d_dpi.ptr, static_cast<size_t>(plan.npf));
-    xchg(d_Gsum.ptr, d_Gsum.ptr, static_cast<size_t>(plan.n_pi) * plan.n_pi);
     launch_coarse_schur(b, st_);
     launch_coarse_weights(b, st_);
-    launches_ += 7;
+    launches_ += 8;
   }
   DDG_CUDA(cudaEventRecord(ev_[5], st_));
   int fail = 0;
@@ -739,19 +758,10 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
       DDG_CUDA(cudaMemsetAsync(d_tpart3.ptr, 0, d_tpart3.count * sizeof(double), st_));
     }
     if (sharded()) {
-      // send tables: slots owned by other ranks stay zero; receive twins hold the all-reduced sums
-      for (DevBuf<double>* bsend : {&d_xf, &d_tr, &d_zz, &d_o, &d_pap, &d_xc, &d_opi})
-        DDG_CUDA(cudaMemsetAsync(bsend->ptr, 0, bsend->count * sizeof(double), st_));
-      r_tpart.alloc(d_tpart.count);
-      r_psipart.alloc(d_psipart.count);
-      r_tpart3.alloc(d_tpart3.count);
-      r_o.alloc(d_o.count);
-      r_xf.alloc(d_xf.count);
-      r_tr.alloc(d_tr.count);
-      r_zz.alloc(d_zz.count);
-      r_pap.alloc(d_pap.count);
-      r_xc.alloc(d_xc.count);
-      r_opi.alloc(d_opi.count);
+      // the tables are exchanged in place: a slot another rank writes arrives in part 0 (the
+      // P-part sum, k_cg.cu xpack), so every other part of it must read as zero
+      for (DevBuf<double>* t : {&d_xf, &d_tr, &d_zz, &d_o, &d_pap, &d_xc, &d_opi, &d_tpart, &d_psipart, &d_tpart3})
+        DDG_CUDA(cudaMemsetAsync(t->ptr, 0, t->count * sizeof(double), st_));
     }
   }
   a.rel_tol = tol;
@@ -803,17 +813,18 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.pap_w = d_pap.ptr;
   a.xctab_w = d_xc.ptr;
   a.opitab_w = d_opi.ptr;
-  const bool sh = sharded();
-  a.ttab = sh ? r_tpart.ptr : d_tpart.ptr;
-  a.t3tab = sh ? r_tpart3.ptr : d_tpart3.ptr;
-  a.ptab = sh ? r_psipart.ptr : d_psipart.ptr;
-  a.otab = sh ? r_o.ptr : d_o.ptr;
-  a.xtab = sh ? r_xf.ptr : d_xf.ptr;
-  a.trtab = sh ? r_tr.ptr : d_tr.ptr;
-  a.zztab = sh ? r_zz.ptr : d_zz.ptr;
-  a.pap = sh ? r_pap.ptr : d_pap.ptr;
-  a.xctab = sh ? r_xc.ptr : d_xc.ptr;
-  a.opitab = sh ? r_opi.ptr : d_opi.ptr;
+  // consumers read the same tables the producers write (sharded: foreign slots filled in place
+  // by the exchange points, Workspace::xpoint)
+  a.ttab = a.ttab_w;
+  a.t3tab = a.t3tab_w;
+  a.ptab = a.ptab_w;
+  a.otab = a.otab_w;
+  a.xtab = a.xtab_w;
+  a.trtab = a.trtab_w;
+  a.zztab = a.zztab_w;
+  a.pap = a.pap_w;
+  a.xctab = a.xctab_w;
+  a.opitab = a.opitab_w;
   a.N_global = p.N_global;
   a.sub_lo = p.sub_lo;
   a.u = d_u.ptr;
@@ -831,6 +842,7 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.rpc_max = cg_rows_per_chunk_max(a);
   a.xr_parts = cg_grid(a);
   a.cond = 0;
+  a.guard_all = 0;
   a.trace = nullptr;
   if (std::getenv("DDELM_CG_TRACE")) {
     d_trace.alloc(148 * 4 * 32);
@@ -877,28 +889,38 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   CgArgs a = cg_args(theta, tol, max_iter, one_level);
   apply_l2_policy();
   DDG_CUDA(cudaEventRecord(ev_[8], st_));
-  if (phased_) run_phases(a, 1, nullptr, d_rhs.ptr);
-  else cg_launch(a, kJobRhs, nullptr, d_rhs.ptr, st_);
+  if (phased_) {
+    run_phases(a, 1, nullptr, d_rhs.ptr);  // counts its own launches
+  } else {
+    cg_launch(a, kJobRhs, nullptr, d_rhs.ptr, st_);
+    launches_ += 1;
+  }
   cg_launch_init(a, st_);
-  launches_ += 3;
+  launches_ += 2;
   DDG_CUDA(cudaEventRecord(ev_[9], st_));
   const int kt_cg = ktimer_begin();
-  if (phased_) run_cg_phased(a);
-  else cg_launch(a, kJobCg, nullptr, nullptr, st_);
+  if (phased_) {
+    launches_ += run_cg_phased(a);
+  } else {
+    cg_driver_ = "persistent";
+    cg_launch(a, kJobCg, nullptr, nullptr, st_);
+    launches_ += 1;
+  }
   ktimer_end(kt_cg, "cg_iterations", 0.0, 0.0);
   DDG_CUDA(cudaEventRecord(ev_[10], st_));
-  if (phased_) run_phases(a, 2, d_x.ptr, nullptr);
-  else cg_launch(a, kJobRecon, d_x.ptr, nullptr, st_);
-  launches_ += 1;
+  if (phased_) {
+    run_phases(a, 2, d_x.ptr, nullptr);
+  } else {
+    cg_launch(a, kJobRecon, d_x.ptr, nullptr, st_);
+    launches_ += 1;
+  }
   DDG_CUDA(cudaEventRecord(ev_[11], st_));
   int state[8];
   DDG_CUDA(cudaMemcpyAsync(state, d_state.ptr, sizeof(state), cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
   res.iterations = state[5];
-  if (phased_) launches_ += 7 * std::max(0, res.iterations - 1);  // graph replays of the iteration
   res.converged = state[2] != 0;
   res.negative_curvature = state[3] != 0;
-  launches_ += 1;  // the persistent CG kernel
   last_iterations_ = res.iterations;
   auto ms = [&](int e0, int e1) {
     float t = 0;
@@ -1029,6 +1051,7 @@ void Workspace::apply_neumann(int transpose, const double* v, double* out) {
   // launches; the owner-slot tables are all-reduced in between like in the CG iteration
   DDG_CUDA(cudaSetDevice(device_));
   if (!phased_) throw std::invalid_argument("apply_P: needs the phase-by-phase driver");
+  if (sharded()) throw std::invalid_argument("apply_P: not available on a sharded workspace (test hook, one device)");
   if (!built_) build();
   build_coarse();
   build_neumann();
@@ -1040,13 +1063,11 @@ void Workspace::apply_neumann(int transpose, const double* v, double* out) {
     DDG_CUDA(cudaMemsetAsync(a.xtab, 0, tab * sizeof(double), st_));
     cg_launch_neumann_io(a, 0, d_vin.ptr, nullptr, st_);
     cg_launch_phase(a, kPhNn1, 0, 0, nullptr, nullptr, st_);
-    xchg(a.trtab_w, a.trtab, tab);
     cg_launch_neumann_io(a, 2, nullptr, d_vout.ptr, st_);
   } else {
     DDG_CUDA(cudaMemsetAsync(a.trtab, 0, tab * sizeof(double), st_));
     cg_launch_neumann_io(a, 1, d_vin.ptr, nullptr, st_);
     cg_launch_phase(a, kPhNn2, 0, 0, nullptr, nullptr, st_);
-    xchg(a.zztab_w, a.zztab, tab);
     cg_launch_neumann_io(a, 3, nullptr, d_vout.ptr, st_);
   }
   launches_ += 3;
@@ -1054,101 +1075,112 @@ void Workspace::apply_neumann(int transpose, const double* v, double* out) {
   DDG_CUDA(cudaStreamSynchronize(st_));
 }
 
-void Workspace::xchg(double* send, double* recv, size_t n) {
-  if (ex_ && n) ex_->allreduce(send, recv, n, st_);
+int Workspace::xpoint(const CgArgs& a, int pt, bool guard) {
+  if (!sharded()) return 0;
+  const int one = a.one_level ? 1 : 0;
+  const XList& L = xplan_.pt[one][pt];
+  if (L.send.empty() && L.recv.empty()) return 0;
+  const XTabs t = cg_xtabs(a);
+  const int* state = guard ? a.state : nullptr;
+  launch_xpack(t, d_xsend[one][pt].ptr, static_cast<int>(L.send.size()), d_xsbuf.ptr, state, st_);
+  ex_->exchange(d_xsbuf.ptr, L.soff.data(), L.scnt.data(), d_xrbuf.ptr, L.roff.data(), L.rcnt.data(), st_);
+  launch_xunpack(t, d_xrecv[one][pt].ptr, static_cast<int>(L.recv.size()), d_xrbuf.ptr, state, st_);
+  return (L.send.empty() ? 0 : 1) + (L.recv.empty() ? 0 : 1);
 }
 
 void Workspace::run_phases(const CgArgs& a, int mode, const double* vin, double* vout) {
   // one operator application (mode 0), the reduced rhs (1) or the reconstruction (2), phase by
-  // phase, all-reducing each owner-slot table between its producer and its consumers
-  const size_t npi4 = 4 * static_cast<size_t>(plan.n_pi), npf4 = 4 * static_cast<size_t>(plan.npf);
-  const size_t tab = static_cast<size_t>(a.P) * 2 * plan.n_delta;
+  // phase, with the sharded exchange points between a table's producer and its consumers
+  long long n = 0;
   cg_launch_phase(a, kPhOp1, mode, 0, vin, vout, st_);
-  if (!a.one_level) {
-    xchg(a.ttab_w, a.ttab, npi4);
-    xchg(a.ptab_w, a.ptab, npf4);
-  }
+  n += 1 + xpoint(a, kXOp1, false);
   cg_launch_phase(a, kPhOp2, mode, 0, vin, vout, st_);
-  if (mode == 2) return;
-  xchg(a.xtab_w, a.xtab, tab);
-  if (a.one_level) xchg(a.xctab_w, a.xctab, static_cast<size_t>(a.P) * npf4);
-  if (a.use_neumann) {
-    cg_launch_phase(a, kPhNn1, mode, 0, vin, vout, st_);
-    xchg(a.trtab_w, a.trtab, tab);
-    cg_launch_phase(a, kPhNn2, mode, 0, vin, vout, st_);
-    xchg(a.zztab_w, a.zztab, tab);
+  ++n;
+  if (mode != 2) {
+    n += xpoint(a, kXOp2, false);
+    if (a.use_neumann) {
+      cg_launch_phase(a, kPhNn1, mode, 0, vin, vout, st_);
+      n += 1 + xpoint(a, kXNn1, false);
+      cg_launch_phase(a, kPhNn2, mode, 0, vin, vout, st_);
+      n += 1 + xpoint(a, kXNn2, false);
+    }
+    cg_launch_phase(a, kPhOp3, mode, 0, vin, vout, st_);
+    n += 1 + xpoint(a, kXOp3, false);
+    cg_launch_phase(a, kPhOp4, mode, 0, vin, vout, st_);
+    n += 1 + xpoint(a, kXOp4, false);
+    cg_launch_phase(a, kPhGather, mode, 0, vin, vout, st_);
+    ++n;
   }
-  cg_launch_phase(a, kPhOp3, mode, 0, vin, vout, st_);
-  if (!a.one_level) xchg(a.t3tab_w, a.t3tab, static_cast<size_t>(a.P) * npi4);
-  cg_launch_phase(a, kPhOp4, mode, 0, vin, vout, st_);
-  xchg(a.otab_w, a.otab, 2 * static_cast<size_t>(plan.n_delta));
-  if (a.one_level) xchg(a.opitab_w, a.opitab, npi4);
-  cg_launch_phase(a, kPhGather, mode, 0, vin, vout, st_);
+  launches_ += n;
 }
 
-void Workspace::run_cg_phased(const CgArgs& a_in) {
-  // The CG loop as ONE CUDA graph: a conditional while node whose body is one iteration (the
-  // phase kernels and, when sharded, the owner-slot all-reduces, captured from this stream); the
-  // XR2 kernel sets the loop condition on the device, so there is no host round trip per
-  // iteration. DDELM_CG_GRAPH=0 falls back to a host loop with one stopping-test read-back per
-  // iteration.
-  const size_t npi4 = 4 * static_cast<size_t>(plan.n_pi), npf4 = 4 * static_cast<size_t>(plan.npf);
-  const size_t tab = static_cast<size_t>(a_in.P) * 2 * plan.n_delta;
-  auto iteration = [&](const CgArgs& a) {
+long long Workspace::run_cg_phased(const CgArgs& a_in) {
+  // One CG iteration = the phase kernels with the sharded exchange points between them. Drivers:
+  //  * graph-while (one device, default): the loop as ONE CUDA graph, a conditional while node
+  //    whose body is one iteration; XR2 sets the loop condition on the device, so no host round
+  //    trip per iteration;
+  //  * graph-chunked (sharded over NCCL, or DDELM_CG_DRIVER=chunked): a plain graph of K
+  //    iterations (DDELM_CG_CHUNK, default 16) replayed until the device says stop — every phase
+  //    and exchange kernel leaves at once after the stop (guard_all), NCCL ops stay matched on
+  //    all ranks because every rank takes the same (replicated, bitwise) stopping decision; one
+  //    host read-back per chunk instead of per iteration;
+  //  * host-loop (host-staged exchange, or DDELM_CG_GRAPH=0): one stopping-test read-back per
+  //    iteration. DDELM_CG_PHASE_TIMES=1 adds per-phase CUDA-event times (diagnostics).
+  long long launched = 0;
+  auto iteration = [&](const CgArgs& a, bool guard, const std::function<void(int)>& after) {
+    long long n = 0;
     cg_launch_phase(a, kPhOp1, 0, 0, nullptr, nullptr, st_);
-    if (!a.one_level) {
-      xchg(a.ttab_w, a.ttab, npi4);
-      xchg(a.ptab_w, a.ptab, npf4);
-    }
+    n += 1 + xpoint(a, kXOp1, guard);
+    after(0);
     cg_launch_phase(a, kPhOp2, 0, 0, nullptr, nullptr, st_);
-    xchg(a.xtab_w, a.xtab, tab);
-    if (a.one_level) xchg(a.xctab_w, a.xctab, static_cast<size_t>(a.P) * npf4);
+    n += 1 + xpoint(a, kXOp2, guard);
+    after(1);
     if (a.use_neumann) {
       cg_launch_phase(a, kPhNn1, 0, 0, nullptr, nullptr, st_);
-      xchg(a.trtab_w, a.trtab, tab);
+      n += 1 + xpoint(a, kXNn1, guard);
+      after(2);
       cg_launch_phase(a, kPhNn2, 0, 0, nullptr, nullptr, st_);
-      xchg(a.zztab_w, a.zztab, tab);
+      n += 1 + xpoint(a, kXNn2, guard);
+      after(3);
+    } else {
+      after(2);
+      after(3);
     }
     cg_launch_phase(a, kPhOp3, 0, 0, nullptr, nullptr, st_);
-    if (!a.one_level) xchg(a.t3tab_w, a.t3tab, static_cast<size_t>(a.P) * npi4);
+    n += 1 + xpoint(a, kXOp3, guard);
+    after(4);
     cg_launch_phase(a, kPhOp4, 0, 0, nullptr, nullptr, st_);
-    xchg(a.otab_w, a.otab, 2 * static_cast<size_t>(plan.n_delta));
-    if (a.one_level) xchg(a.opitab_w, a.opitab, npi4);
-    xchg(a.pap_w, a.pap, static_cast<size_t>(plan.N_global));
+    n += 1 + xpoint(a, kXOp4, guard);
+    after(5);
     cg_launch_phase(a, kPhXr1, 0, 0, nullptr, nullptr, st_);  // its last CTA also runs XR2
+    after(6);
+    return n + 1;
   };
-  // Sharded (world > 1): the host loop by default — the NCCL all-reduces are then plain stream
-  // operations rather than nodes inside a conditional graph body (whose node types CUDA
-  // restricts); DDELM_CG_GRAPH=1 captures them into the graph anyway.
+  const auto none = [](int) {};
   const char* ge = std::getenv("DDELM_CG_GRAPH");
-  const bool host_loop = ge ? std::strcmp(ge, "0") == 0 : sharded();
+  const char* drv = std::getenv("DDELM_CG_DRIVER");
+  const bool no_graph = ge && std::strcmp(ge, "0") == 0;
+  const bool ptimes = std::getenv("DDELM_CG_PHASE_TIMES") != nullptr;
+  const bool can_capture = !sharded() || ex_->capturable();
+  const bool chunked = can_capture && !no_graph && !ptimes && (sharded() || (drv && std::strcmp(drv, "chunked") == 0));
+  const bool host_loop = no_graph || ptimes || !can_capture;
   if (host_loop) {
+    cg_driver_ = "host-loop";
     CgArgs a = a_in;
     a.cond = 0;
-    // DDELM_CG_PHASE_TIMES=1: per-phase CUDA-event times (host loop only; diagnostics)
-    const bool ptimes = std::getenv("DDELM_CG_PHASE_TIMES") != nullptr;
     std::vector<cudaEvent_t> pev;
-    std::vector<double> pms(8, 0.0);
+    std::vector<double> pms(7, 0.0);
     if (ptimes) {
-      pev.resize(9);
+      pev.resize(8);
       for (auto& e : pev) DDG_CUDA(cudaEventCreate(&e));
     }
+    const std::function<void(int)> rec = [&](int q) {
+      if (ptimes) DDG_CUDA(cudaEventRecord(pev[q + 1], st_));
+    };
     int nit = 0;
     for (int it = 1; it <= a.max_iter; ++it) {
-      if (ptimes) {
-        const int phases[7] = {kPhOp1, kPhOp2, kPhNn1, kPhNn2, kPhOp3, kPhOp4, kPhXr1};
-        DDG_CUDA(cudaEventRecord(pev[0], st_));
-        for (int q = 0; q < 7; ++q) {
-          if (!a.use_neumann && (phases[q] == kPhNn1 || phases[q] == kPhNn2)) {
-            DDG_CUDA(cudaEventRecord(pev[q + 1], st_));
-            continue;
-          }
-          cg_launch_phase(a, phases[q], 0, 0, nullptr, nullptr, st_);
-          DDG_CUDA(cudaEventRecord(pev[q + 1], st_));
-        }
-      } else {
-        iteration(a);
-      }
+      if (ptimes) DDG_CUDA(cudaEventRecord(pev[0], st_));
+      launched += iteration(a, false, rec);
       DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
       DDG_CUDA(cudaStreamSynchronize(st_));
       if (ptimes)
@@ -1158,16 +1190,42 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
           pms[q] += t;
         }
       ++nit;
-      launches_ += 7;
       if (pinned_state_[1]) break;
     }
     if (ptimes) {
+      // each phase's time includes the exchange point that follows it (sharded)
       static const char* nm[7] = {"op1", "op2", "nn1", "nn2", "op3", "op4", "xr"};
       for (int q = 0; q < 7; ++q) std::fprintf(stderr, "[cg phase] %-4s %8.2f us\n", nm[q], 1e3 * pms[q] / std::max(nit, 1));
       for (auto& e : pev) cudaEventDestroy(e);
     }
-    return;
+    return launched;
   }
+  if (chunked) {
+    cg_driver_ = "graph-chunked";
+    int K = 16;
+    if (const char* e = std::getenv("DDELM_CG_CHUNK")) K = std::max(1, std::atoi(e));
+    CgArgs a = a_in;
+    a.cond = 0;
+    a.guard_all = 1;
+    long long per_chunk = 0;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t gx = nullptr;
+    DDG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < K; ++k) per_chunk += iteration(a, true, none);
+    DDG_CUDA(cudaStreamEndCapture(st_, &g));
+    DDG_CUDA(cudaGraphInstantiate(&gx, g, 0));
+    for (int done = 0; done < a.max_iter; done += K) {
+      DDG_CUDA(cudaGraphLaunch(gx, st_));
+      launched += per_chunk;
+      DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+      DDG_CUDA(cudaStreamSynchronize(st_));
+      if (pinned_state_[1]) break;
+    }
+    DDG_CUDA(cudaGraphExecDestroy(gx));
+    DDG_CUDA(cudaGraphDestroy(g));
+    return launched;
+  }
+  cg_driver_ = "graph-while";
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge_exec = nullptr;
   DDG_CUDA(cudaGraphCreate(&g, 0));
@@ -1184,15 +1242,19 @@ void Workspace::run_cg_phased(const CgArgs& a_in) {
   CgArgs a = a_in;
   a.cond = static_cast<unsigned long long>(h);
   DDG_CUDA(cudaStreamBeginCaptureToGraph(st_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  iteration(a);
+  const long long per_it = iteration(a, false, none);
   cudaGraph_t captured = nullptr;
   DDG_CUDA(cudaStreamEndCapture(st_, &captured));
   DDG_CUDA(cudaGraphInstantiate(&ge_exec, g, 0));
   DDG_CUDA(cudaGraphLaunch(ge_exec, st_));
-  launches_ += 7;  // one iteration's phase kernels (the graph replays them; see solve())
   DDG_CUDA(cudaStreamSynchronize(st_));
   DDG_CUDA(cudaGraphExecDestroy(ge_exec));
   DDG_CUDA(cudaGraphDestroy(g));
+  // body replays: one per iteration, plus the one that found pAp <= 0 (iterations = it - 1)
+  int st8[8];
+  DDG_CUDA(cudaMemcpy(st8, d_state.ptr, sizeof(st8), cudaMemcpyDeviceToHost));
+  const bool aborted = !st8[2] && st8[5] < a.max_iter;
+  return per_it * (st8[5] + (aborted ? 1 : 0));
 }
 
 void Workspace::get_mu(double* mu) {
@@ -1254,7 +1316,7 @@ void Workspace::field(int n, const double* ref, double* u, double* gx, double* g
   if (d_fsums.count < 8) d_fsums.alloc(8);
   f.part = d_fpart.ptr;
   launch_field(f, std::max(max_pts, 1), d_fsums.ptr, st_);
-  if (sharded()) xchg(d_fsums.ptr, d_fsums.ptr + 4, 4);
+  if (sharded()) ex_->allreduce(d_fsums.ptr, d_fsums.ptr + 4, 4, st_);
   DDG_CUDA(cudaMemcpyAsync(sums, d_fsums.ptr + (sharded() ? 4 : 0), 4 * sizeof(double), cudaMemcpyDeviceToHost, st_));
   if (u) DDG_CUDA(cudaMemcpyAsync(u, d_field.ptr, nn * sizeof(double), cudaMemcpyDeviceToHost, st_));
   if (gx) DDG_CUDA(cudaMemcpyAsync(gx, d_field.ptr + nn, nn * sizeof(double), cudaMemcpyDeviceToHost, st_));

@@ -77,7 +77,7 @@ class Workspace {
  public:
   /// p: the (possibly sharded, see shard_plan) plan of this device; ex: the cross-GPU exchange
   /// (nullptr: single device)
-  Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex = nullptr);
+  Workspace(const Plan& p, int device, std::unique_ptr<Exchange> ex = nullptr, XPlan xp = {});
   ~Workspace();
   Workspace(const Workspace&) = delete;
   Workspace& operator=(const Workspace&) = delete;
@@ -99,6 +99,9 @@ class Workspace {
   void set_profiling(bool on) { profiling_ = on; }
   bool kernel_stat(const std::string& name, KernelStat* out) const;
   double device_span_ms() const { return device_span_ms_; }
+  const char* cg_driver() const { return cg_driver_; }
+  const char* exchange_kind() const { return ex_ ? ex_->kind() : "none"; }
+  int world() const { return ex_ ? ex_->world() : 1; }
 
   /// Field of the last solve on the n x n grid (sample_field, metrics.cpp:18-57): samples to the
   /// host buffers (each nullable, n*n), and sums[4] of the trapezoid error terms against the
@@ -135,8 +138,14 @@ class Workspace {
   /// phase-by-phase launches with owner-slot all-reduces (sharded path; DDELM_CG_MODE=phased
   /// selects it on one device too)
   void run_phases(const CgArgs& a, int mode, const double* vin, double* vout);
-  void run_cg_phased(const CgArgs& a);
-  void xchg(double* send, double* recv, size_t n);
+  /// runs the CG loop; returns the number of this library's kernels launched
+  long long run_cg_phased(const CgArgs& a);
+  /// exchange point pt of the sharded iteration (no-op on one device): pack the exported slots,
+  /// move them (ex_), unpack the imported ones; guard: skip the kernels once the CG stopped.
+  /// Returns the kernels launched.
+  int xpoint(const CgArgs& a, int pt, bool guard);
+  /// CG driver actually used by the last solve ("graph-while", "graph-chunked", "host-loop", "persistent")
+  const char* cg_driver_ = "graph-while";
   std::unique_ptr<Exchange> ex_;
   bool phased_ = false;
   // kernel timers: begin/end around a launch; collected after the stream syncs
@@ -199,7 +208,13 @@ class Workspace {
   // receive side of the owner-slot all-reduces (sharded only)
   DevBuf<double> d_field, d_fpart, d_fref, d_fsums, d_xc, d_opi, r_xc, r_opi;
   DevBuf<int> d_flo;
-  DevBuf<double> r_tpart, r_psipart, r_tpart3, r_o, r_xf, r_tr, r_zz, r_pap, d_Gsum;
+  DevBuf<double> d_Gsum, d_cin;
+  DevBuf<int> d_cpi_g;
+  // sharded exchange (XPlan): per (method family, point) the packed entry lists and per-point
+  // send / receive buffers
+  XPlan xplan_;
+  DevBuf<XEntry> d_xsend[2][kXPoints], d_xrecv[2][kXPoints];
+  DevBuf<double> d_xsbuf, d_xrbuf;
   int ldKF_ = 0, ldKD_ = 0;
 };
 

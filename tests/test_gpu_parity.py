@@ -92,9 +92,11 @@ def test_rank_deficient_solve_within_oracle_spread(P, name):
     f_tol = max(1e-9, 4.0 * float(g["spread_field"]))
     diff = _field_diff(cfg, rep.coeffs, g["field_u"])
     assert diff <= f_tol, f"{name}: field diff {diff:.3e} > {f_tol:.3e}"
-    # the solution itself is accurate against the manufactured solution, like the oracle's
-    from oracle.pyoracle import field_rel_l2
-    assert float(g["l2"]) < 1e-5
+    # the DEVICE solution itself is as accurate against the manufactured solution as the
+    # oracle's (relative L2 on the 257^2 grid, metrics.cpp:59-88), within the same spread
+    l2, _ = ws.relative_errors(257)
+    assert l2 < 1e-5, l2
+    assert abs(l2 - float(g["l2"])) <= max(1e-9, 4.0 * float(g["spread_field"])), (l2, float(g["l2"]))
 
 
 @pytest.mark.parametrize("name", ["T1", "T4", "C1"])
@@ -235,19 +237,22 @@ def test_cpp_facade_matches_python_path(P):
 
 
 @pytest.mark.parametrize("name", ["T2", "C2"])
-def test_sharded_path_world1_matches_persistent(P, name):
-    """The sharded path (phase-by-phase launches + owner-slot all-reduces, ddelm_gpu_create_sharded)
-    run with world = 1 reproduces the persistent single-device kernel bit for bit: the same work
-    split and the same fixed-order sums. (With world > 1 the exchanged tables carry exact zeros in
-    non-owned slots; tests/test_sharding.py checks that partition over real gloo ranks.)"""
+def test_persistent_kernel_matches_phase_graph(P, name, monkeypatch):
+    """The persistent cooperative CG kernel (DDELM_CG_MODE=persistent) and the default
+    phase-by-phase while-loop graph run the same work split and fixed-order sums: bit-identical
+    solves and operator applications. (The sharded path is tests/test_gpu_sharded.py.)"""
+    monkeypatch.setenv("DDELM_CG_MODE", "persistent")
     ws_a = P.workspace_from_config(name)
-    ws_b = P.workspace_from_config(name, shard=(0, 1, None))
-    assert (ws_b.sub_lo, ws_b.n_local, ws_b.n_global) == (0, ws_a.n_subs, ws_a.n_subs)
     _, ra = P.solve_config(name, ws=ws_a)
+    assert ws_a.cg_driver == "persistent"
+    v = np.random.default_rng(3).standard_normal(ws_a.n_delta)
+    va = ws_a.apply_operator(v)
+    monkeypatch.delenv("DDELM_CG_MODE")
+    ws_b = P.workspace_from_config(name)
     _, rb = P.solve_config(name, ws=ws_b)
+    assert ws_b.cg_driver == "graph-while"
     assert ra.iterations == rb.iterations
     assert np.array_equal(ra.mu, rb.mu)
     assert np.array_equal(ra.coeffs, rb.coeffs)
     assert np.array_equal(ra.residual_history, rb.residual_history)
-    v = np.random.default_rng(3).standard_normal(ws_a.n_delta)
-    assert np.array_equal(ws_a.apply_operator(v), ws_b.apply_operator(v))
+    assert np.array_equal(va, ws_b.apply_operator(v))

@@ -1,0 +1,142 @@
+"""The sharded DDELM-NN path on the device.
+
+Two ranks run as two processes on ONE B200 with the host-staged exchange backend
+(ddelm_gpu_create_sharded_host): the same sharded kernels, exchange plan, pack / unpack kernels,
+in-place owner-slot tables and replicated CG update as the NCCL path, with the slot segments moved
+through a shared-memory mailbox by the host (no kernel waits for the other rank's kernels). With
+the same row-part split (DDELM_CG_PARTS) the sharded solve must reproduce the single-device solve
+BIT FOR BIT: iteration count, residual history, mu and every coefficient of each strip.
+
+The graph-chunked CG driver (the NCCL path's driver: a plain graph of K iterations replayed until
+the device stops) is checked against the default while-loop graph on one device.
+"""
+import os
+import uuid
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PARTS = "2"
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_10032_b200 as P
+    P.load_library()
+    return P
+
+
+def _solve_single(name, method, monkeypatch, parts=PARTS, driver=None):
+    import paper_2503_10032_b200 as P
+    monkeypatch.setenv("DDELM_CG_PARTS", parts)
+    if driver:
+        monkeypatch.setenv("DDELM_CG_DRIVER", driver)
+    ws = P.workspace_from_config(name)
+    c = P.CONFIGS[name]
+    theta = c["theta"] if method == "ddelm-nn" else 0.0
+    rep = ws._solve(method, theta, P.CgOptions(rel_tol=c["cg_rel_tol"]), fetch=True)
+    out = {"iterations": rep.iterations, "mu": rep.mu.copy(), "coeffs": np.array(rep.coeffs).copy(),
+           "hist": np.array(rep.residual_history).copy(), "driver": ws.cg_driver, "converged": rep.converged}
+    if driver:
+        monkeypatch.delenv("DDELM_CG_DRIVER")
+    del ws
+    return out
+
+
+def _rank_worker(rank, world, shm, name, methods, parts, q):
+    os.environ["DDELM_CG_PARTS"] = parts
+    try:
+        import paper_2503_10032_b200 as P2
+
+        c = P2.CONFIGS[name]
+        ws = P2.workspace_from_config(name, device=0, shard=(rank, world, "host:" + shm))
+        res = {"sub_lo": ws.sub_lo, "n_local": ws.n_local}
+        for method in methods:
+            theta = c["theta"] if method == "ddelm-nn" else 0.0
+            rep = ws._solve(method, theta, P2.CgOptions(rel_tol=c["cg_rel_tol"]), fetch=True)
+            res[method] = {"iterations": rep.iterations, "mu": rep.mu.copy(),
+                           "coeffs": np.array(rep.coeffs).copy(),
+                           "hist": np.array(rep.residual_history).copy(), "driver": ws.cg_driver,
+                           "launches": rep.launches}
+        l2 = ws.relative_errors(65) if c["problem"] != "poisson_grf" else None
+        res["l2"] = l2
+        del ws
+        q.put((rank, res))
+    except Exception as e:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, {"error": f"{e}\n{traceback.format_exc()}"}))
+
+
+def _run_sharded(name, methods, world=2, parts=PARTS):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    shm = f"/ddelm_test_{uuid.uuid4().hex[:12]}"
+    procs = [ctx.Process(target=_rank_worker, args=(r, world, shm, name, methods, parts, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in procs:
+            r, d = q.get(timeout=600)
+            res[r] = d
+    finally:
+        for p in procs:
+            p.join(timeout=120)
+            if p.is_alive():
+                p.kill()
+    for r, d in res.items():
+        assert "error" not in d, d.get("error")
+    for p in procs:
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("name,methods", [("T2", ["ddelm-nn", "ddelm-cs", "ddelm"]), ("C2", ["ddelm-nn"])])
+def test_sharded_world2_matches_single_device_bitwise(P, name, methods, monkeypatch):
+    res = _run_sharded(name, methods)
+    for method in methods:
+        ref = _solve_single(name, method, monkeypatch)
+        assert ref["converged"]
+        coeffs = []
+        for r in range(2):
+            d = res[r][method]
+            assert d["driver"] == "host-loop"
+            assert d["iterations"] == ref["iterations"], (method, r, d["iterations"], ref["iterations"])
+            np.testing.assert_array_equal(d["hist"], ref["hist"])
+            np.testing.assert_array_equal(d["mu"], ref["mu"])  # replicated interface vector
+            coeffs.append(d["coeffs"])
+        lo1 = res[1]["sub_lo"]
+        assert res[0]["sub_lo"] == 0 and lo1 == res[0]["n_local"]
+        np.testing.assert_array_equal(np.concatenate(coeffs, axis=0), ref["coeffs"])
+    # the error metric is all-reduced over the strips
+    assert res[0]["l2"] is not None and res[0]["l2"] == res[1]["l2"]
+
+
+def test_sharded_world3_ragged_strips(P, monkeypatch):
+    """Three ranks on 16 subdomains (strips of 5 / 5 / 6): still bitwise the single-device solve."""
+    res = _run_sharded("C2", ["ddelm-nn"], world=3)
+    ref = _solve_single("C2", "ddelm-nn", monkeypatch)
+    for r in range(3):
+        assert res[r]["ddelm-nn"]["iterations"] == ref["iterations"]
+        np.testing.assert_array_equal(res[r]["ddelm-nn"]["mu"], ref["mu"])
+    np.testing.assert_array_equal(np.concatenate([res[r]["ddelm-nn"]["coeffs"] for r in range(3)], axis=0),
+                                  ref["coeffs"])
+
+
+@pytest.mark.parametrize("name,method", [("T2", "ddelm-nn"), ("T2", "ddelm"), ("C2", "ddelm-nn")])
+def test_chunked_graph_driver_matches_while_graph(P, name, method, monkeypatch):
+    a = _solve_single(name, method, monkeypatch)
+    b = _solve_single(name, method, monkeypatch, driver="chunked")
+    assert a["driver"] == "graph-while" and b["driver"] == "graph-chunked"
+    assert a["iterations"] == b["iterations"]
+    np.testing.assert_array_equal(a["hist"], b["hist"])
+    np.testing.assert_array_equal(a["mu"], b["mu"])
+    np.testing.assert_array_equal(a["coeffs"], b["coeffs"])
