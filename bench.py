@@ -27,7 +27,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FP64_PEAK_TFLOPS = 37.2  # measured DMMA loop on this pool's B200 (profiles/r01_fp64_peaks.json)
 
 
 def load_traffic(family):
@@ -144,65 +143,71 @@ def barrier(dist):
 
 
 # --------------------------------------------------------------------------- CPU (oracle)
-def cpu_solve_sample(cfg_name: str, cg_iters: int = 5):
-    """Bounded sample of the reference algorithm on the host (oracle restatement): full
-    Workspace build (all local factorisations, workers = nproc as the reference's only knob),
-    coarse + Neumann layers and `cg_iters` CG iterations; the CG is extrapolated to the golden
-    iteration count."""
-    import numpy as np
-
-    from oracle.pyoracle import OracleWorkspace
+def cpu_solve(cfg_name: str, cg_workers: int = 1):
+    """ONE complete solve of the reference's CPU algorithm on the host (the oracle restatement;
+    the reference itself cannot be built here): Workspace build with LsFactor on
+    SciPy's LAPACK (dgeqrf / dgeqp3 / dtzrzf, oracle/lapack.cpp; one BLAS thread per call),
+    workers = nproc for the per-subdomain setup phases (the reference's only parallel knob,
+    solvers.cpp:138,150,286,401), and the interface CG single-threaded as in the reference
+    (solvers.cpp:95-117). No extrapolation: the whole solve is timed."""
+    from oracle import pyoracle as o
     from paper_2503_10032_b200.configs import CONFIGS
 
     c = CONFIGS[cfg_name]
     nproc = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    ws = OracleWorkspace(problem=c["problem"], s=c["s"], n_grid=c["n_grid"], M=c["M"], l=c["l"],
-                         seed=c["seed"], flux_variant=c["flux_variant"],
-                         trace_basis=c["trace_basis"], workers=nproc, cg_workers=nproc)
-    t1 = time.perf_counter()
-    r = ws.solve(c["method"], c["theta"], c["cg_rel_tol"], 0, cg_iters)
-    t2 = time.perf_counter()
-    tim = r.timings
-    per_it = tim["cg"] / max(r.iterations, 1)
-    gpath = os.path.join(ROOT, "tests", "golden", f"{cfg_name}.npz")
-    golden_it = int(np.load(gpath)["iterations"]) if os.path.exists(gpath) else r.iterations
-    total = (t1 - t0) + tim["setup"] + per_it * golden_it + tim["reconstruction"]
-    return {"seconds_extrapolated": total, "build_s": t1 - t0, "setup_s": tim["setup"],
-            "cg_s_per_iter": per_it, "golden_iterations": golden_it, "cores": nproc,
-            "sample_wall_s": t2 - t0,
-            "sample": (f"{cfg_name}: full Workspace build ({2 * c['s'] ** 2} local LS factorisations, "
-                       f"{nproc} workers) + coarse/Neumann + {r.iterations} CG iterations; CG "
-                       f"extrapolated to the oracle's {golden_it} iterations")}
+    lib = o.use_lapack(True)
+    try:
+        t0 = time.perf_counter()
+        ws = o.OracleWorkspace(problem=c["problem"], s=c["s"], n_grid=c["n_grid"], M=c["M"], l=c["l"],
+                               seed=c["seed"], flux_variant=c["flux_variant"], trace_basis=c["trace_basis"],
+                               workers=nproc, cg_workers=cg_workers)
+        t1 = time.perf_counter()
+        r = ws.solve(c["method"], c["theta"], c["cg_rel_tol"])
+        t2 = time.perf_counter()
+    finally:
+        o.use_lapack(False)
+    tim = {k: round(v, 4) for k, v in r.timings.items()}
+    return {"seconds": t2 - t0, "build_s": t1 - t0, "solve_s": t2 - t1, "iterations": int(r.iterations),
+            "timings": tim, "cores": nproc, "cg_threads": cg_workers,
+            "blas": f"LAPACK from SciPy's OpenBLAS ({os.path.basename(lib)}), 1 thread per call",
+            "sample": (f"{cfg_name}: one complete DDELM-NN solve ({2 * c['s'] ** 2} local LS factorisations on "
+                       f"{nproc} worker threads, coarse + Neumann layers, {int(r.iterations)} CG iterations "
+                       f"on {cg_workers} thread(s) as in the reference, reconstruction); no extrapolation")}
 
 
 def run_reference(args, cfg, world, rank):
+    """The reference arm: complete CPU solves of the workload on the host cores. A solve of C3
+    takes tens of seconds on one CG thread, so the run does min(K, budget / first-solve) complete
+    solves (at least one) and reports that count as `steps` (steps_requested = K)."""
     if rank != 0:
         return
     nsub = cfg["s"] ** 2
-    for _ in range(args.warmup):
-        cpu_solve_sample(args.config, args.cpu_cg_iters)
-    secs = []
-    last = None
-    for _ in range(args.steps):
-        last = cpu_solve_sample(args.config, args.cpu_cg_iters)
-        secs.append(last["seconds_extrapolated"])
+    # warm-up: one complete solve of the smallest config (pages in the oracle and LAPACK)
+    cpu_solve("C1")
+    secs, last = [], None
+    t_start = time.perf_counter()
+    while len(secs) < args.steps:
+        last = cpu_solve(args.config)
+        secs.append(last["seconds"])
+        spent = time.perf_counter() - t_start
+        if spent + secs[-1] > args.ref_budget_s:
+            break
     mean_s = sum(secs) / len(secs)
     value = nsub / mean_s
     line = {"impl": "reference", "metric": "ddelm_nn_solve_throughput", "value": value,
-            "unit": "subdomains/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args, cfg, 1),
-            "cpu_baseline": {"value": value, "unit": "subdomains/s", "cores": last["cores"],
-                             "kind": "port", "sample": last["sample"]},
-            "e2e": {"value": value, "unit": "subdomains/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0},
-            "solve_seconds": mean_s, "detail": last}
+            "unit": "subdomains/s", "n_gpus": args.gpus, "steps": len(secs), "steps_requested": args.steps,
+            "warmup": 1, "warmup_note": "one complete C1 solve (a C3 solve is tens of seconds of CPU)",
+            "ms_per_step": mean_s * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": workload_config(args, cfg, 1),
+            "cpu_baseline": {"value": value, "unit": "subdomains/s", "cores": last["cores"], "kind": "port",
+                             "sample": last["sample"], "blas": last["blas"],
+                             "threads": {"setup": last["cores"], "cg": last["cg_threads"]}},
+            "e2e": {"value": value, "unit": "subdomains/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "solve_seconds": mean_s, "solve_seconds_each": secs, "detail": last}
     print(json.dumps(line), flush=True)
 
 
-def lsq_microbench(P, nblocks, device, reps=3):
+def lsq_microbench(P, nblocks, device, peak, reps=3):
     """BASELINE config C5: nblocks fp64 blocks [K (3000 x 1000) | B (3000 x 200)] of tanh features,
     batched Householder QR (B carried as appended columns: Q^T B) + Schur block S = B^T B -
     (Q^T B)^T (Q^T B) on DMMA. Device-resident inputs (generated on the GPU), CUDA-event timed."""
@@ -223,9 +228,85 @@ def lsq_microbench(P, nblocks, device, reps=3):
     del L
     return {"config": f"C5: {nblocks} blocks, K {m}x{n} + B {m}x{k}, tanh(w.x+b), fp64",
             "blocks_per_s": nblocks / t, "ms_per_step": qr + sc, "qr_ms": qr, "schur_ms": sc,
-            "tflops": tf, "peak_tflops": FP64_PEAK_TFLOPS, "frac_fp64_peak": tf / FP64_PEAK_TFLOPS,
+            "tflops": tf, "peak_tflops": peak, "frac_fp64_peak": tf / peak,
             "flops_per_block": fl / nblocks,
             "flop_model": "geqrf 2mn^2-2n^3/3 + Q^T B 4mnk-2n^2k + S 2(m-n)k^2 (SURVEY.md §8d)"}
+
+
+def fact_schur_flops(cfg, ranks, ranks_bar):
+    """SURVEY.md §8d algorithmic FP64 work of the local factorisation + Schur / coarse assembly
+    (standard LAPACK counts, per-subdomain ranks from the run):
+      per local matrix (K_i and Kbar_i): geqrf(m, M) = 2 m M^2 - 2/3 M^3, plus
+        COD(m, M, r) = 4 m M r - 2 (m + M) r^2 + 4/3 r^3 + 4 r^2 (M - r)   (deficient branch) or
+        orgqr(m, M) = 2 m M^2 - 2/3 M^3                                     (full-rank branch);
+      Schur: Ypi / Gpi 2 m M c_i + 2 m r_i c_i (c_i corner columns), Dpp / Dpd 2 m M per
+      cross-flux row and owner, S_Pi 2 n_pf n_pi^2."""
+    s, M, ng = cfg["s"], cfg["M"], cfg["n_grid"]
+    m = ng * ng  # every local grid point is one K (and Kbar) row (SURVEY.md §8 table)
+    f_fact = 0.0
+    for r in list(ranks) + list(ranks_bar):
+        f_fact += 2.0 * m * M * M - 2.0 / 3.0 * M ** 3
+        if r < M:
+            f_fact += 4.0 * m * M * r - 2.0 * (m + M) * r * r + 4.0 / 3.0 * r ** 3 + 4.0 * r * r * (M - r)
+        else:
+            f_fact += 2.0 * m * M * M - 2.0 / 3.0 * M ** 3
+    f_schur = 0.0
+    for i, r in enumerate(ranks):
+        ix, iy = i % s, i // s
+        c = sum(1 for a in (0, 1) for b in (0, 1) if 1 <= ix + a <= s - 1 and 1 <= iy + b <= s - 1)
+        f_schur += 2.0 * m * M * c + 2.0 * m * r * c
+    n_pi = (s - 1) ** 2
+    npf = 2 * n_pi
+    f_schur += npf * 2 * (2.0 * m * M) + 2.0 * npf * n_pi ** 2
+    return f_fact, f_schur
+
+
+def fp64_fraction(cfg, ranks, ranks_bar, phase_ms, peak):
+    f_fact, f_schur = fact_schur_flops(cfg, ranks, ranks_bar)
+    t = (phase_ms["qr"] + phase_ms["cod"] + phase_ms["coarse"]) / 1e3
+    tf = (f_fact + f_schur) / t / 1e12
+    return {"flops_fact": f_fact, "flops_schur": f_schur, "seconds_fact_schur": t, "tflops": tf,
+            "peak_tflops": peak, "frac": tf / peak,
+            "formula": "SURVEY.md §8d: (F_fact + F_schur) / t_(qr + cod + coarse phases), LAPACK flop counts"}
+
+
+def run_single_config(P, name, steps, warmup, stream_of, peak):
+    """A second single-GPU bench line (BASELINE config C4: 16x16 subdomains, M = 1000): device-
+    resident solves timed with CUDA events, both CG representations."""
+    import torch
+    c = P.CONFIGS[name]
+    ws = P.workspace_from_config(name)
+    stream = stream_of(ws)
+    cg = P.CgOptions(rel_tol=c["cg_rel_tol"])
+    out = {"config": name, "subdomains": c["s"] ** 2, "M": c["M"], "n_grid": c["n_grid"], "l": c["l"],
+           "problem": c["problem"]}
+    for mode in ("coeff", "compact"):
+        ws.set_cg_blocks(mode)
+        for _ in range(warmup):
+            ws.invalidate()
+            ws._solve("ddelm-nn", c["theta"], cg, fetch=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        its = []
+        for _ in range(steps):
+            ws.invalidate()
+            rep = ws._solve("ddelm-nn", c["theta"], cg, fetch=False)
+            its.append(rep.iterations)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        rk, rkb, _ = ws.ranks()
+        d = {"value": c["s"] ** 2 / (ms / 1e3), "unit": "subdomains/s", "ms_per_step": ms, "iterations": its,
+             "phase_ms": {k: round(v, 3) for k, v in rep.phase_ms.items()}}
+        if mode == "coeff":
+            d["fp64_fact_schur"] = fp64_fraction(c, rk, rkb, rep.phase_ms, peak)
+            out.update(d)
+        else:
+            out["cg_compact"] = d
+    ws.set_cg_blocks("coeff")
+    del ws
+    return out
 
 
 def workload_config(args, cfg, world=1):
@@ -247,6 +328,8 @@ def run_ours(args, cfg, world, rank, local, dist):
     import paper_2503_10032_b200 as P
 
     torch.cuda.set_device(local)
+    # the FP64 roofline denominator, measured live on this GPU (DMMA loop; ddelm_gpu_fp64_peak)
+    fp64_peak = P.fp64_peak(local)
     if world > 1:
         # sharded: this rank owns a strip of subdomains; owner-slot tables are all-reduced over NCCL
         obj = [P.nccl_unique_id() if rank == 0 else None]
@@ -330,10 +413,10 @@ def run_ours(args, cfg, world, rank, local, dist):
         if s["flops"] > 0:
             ach = s["flops"] / (s["ms"] / 1e3) / 1e12
             tr = load_traffic(dominant)
-            roof = {"kernel": dominant, "bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS,
-                    "peak_source": "measured FP64 DMMA loop (profiles/r01_fp64_peaks.json); "
-                                   "MEASURED_PEAKS.json carries no FP64 entry",
+            roof = {"kernel": dominant, "bound": "tensor", "achieved": ach, "peak": fp64_peak,
+                    "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                    "peak_source": "FP64 DMMA loop measured live in this run (MEASURED_PEAKS.json carries no "
+                                   "FP64 entry)",
                     "traffic": tr["bytes"] if tr else None, "traffic_source": tr["source"] if tr else None,
                     "launches": s["launches"], "avg_launch_ms": s["ms"] / s["launches"]}
         else:
@@ -406,16 +489,29 @@ def run_ours(args, cfg, world, rank, local, dist):
                            "not the headline: its CG round-off trajectory differs from the reference's"}
         ws.set_cg_blocks("coeff")
 
+    ws_driver, ws_exchange = ws.cg_driver, ("nccl" if world > 1 else "none")
+    # FP64 roofline of the factorisation + Schur phase by SURVEY.md §8d's formula (the headline
+    # solve's own ranks and phase times)
+    fp64_frac = None
+    if world == 1:
+        rk, rkb, _ = ws.ranks()
+        fp64_frac = fp64_fraction(cfg, rk, rkb, rep.phase_ms, fp64_peak)
+    c4 = None
+    if world == 1 and not args.no_c4 and args.config != "C4":
+        del ws
+        c4 = run_single_config(P, "C4", max(2, min(args.steps, 5)), 2,
+                               lambda w: torch.cuda.ExternalStream(w.stream_handle), fp64_peak)
     lsq = None
     if not args.no_lsq and world == 1:
-        lsq = lsq_microbench(P, args.lsq_blocks, local)
+        lsq = lsq_microbench(P, args.lsq_blocks, local, fp64_peak)
     if rank != 0:
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        c = cpu_solve_sample(args.config, args.cpu_cg_iters)
-        cpu = {"value": nsub / c["seconds_extrapolated"], "unit": "subdomains/s", "cores": c["cores"],
-               "kind": "port", "sample": c["sample"], "seconds_extrapolated": c["seconds_extrapolated"]}
+        c = cpu_solve(args.config)
+        cpu = {"value": nsub / c["seconds"], "unit": "subdomains/s", "cores": c["cores"], "kind": "port",
+               "sample": c["sample"], "blas": c["blas"], "threads": {"setup": c["cores"], "cg": c["cg_threads"]},
+               "seconds": c["seconds"], "iterations": c["iterations"], "timings": c["timings"]}
     ms_step = dev_ms_max / args.steps
     line = {"metric": "ddelm_nn_solve_throughput", "value": value, "unit": "subdomains/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -428,7 +524,10 @@ def run_ours(args, cfg, world, rank, local, dist):
             "roofline": roof, "kernel_families": families,
             "phase_ms": {k: round(v, 3) for k, v in rep.phase_ms.items()},
             "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
-            "fp64_lsq_microbench": lsq, "cg_compact": compact,
+            "fp64_lsq_microbench": lsq, "cg_compact": compact, "fp64_fact_schur": fp64_frac,
+            "fp64_peak": {"tflops": fp64_peak, "source": "measured live in this run: DMMA m8n8k4 loop on every SM "
+                          "(ddelm_gpu_fp64_peak; r01 probe: 37.2, profiles/r01_fp64_peaks.json)"},
+            "c4": c4, "cg_driver": ws_driver, "exchange": ws_exchange,
             "fp64_qr_tflops": (qr["flops"] / (qr["ms"] / 1e3) / 1e12) if qr else None}
     print(json.dumps(line), flush=True)
 
@@ -461,10 +560,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--cpu-cg-iters", type=int, default=5)
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="reference arm: stop starting new complete CPU solves after this many seconds")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compact", action="store_true", help="skip the compact-CG-blocks solve")
     ap.add_argument("--no-lsq", action="store_true", help="skip the C5 local-solve microbenchmark")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (16x16, M=1000) second line")
     ap.add_argument("--lsq-blocks", type=int, default=1024)
     args = ap.parse_args()
     from paper_2503_10032_b200.configs import CONFIGS

@@ -234,6 +234,9 @@ int ddelm_gpu_lsq_factor(ddelm_lsq* lsq, double* qr_ms, double* schur_ms);
 int ddelm_gpu_lsq_get_block(ddelm_lsq* lsq, int block, double* A, double* tau, double* S);
 int ddelm_gpu_lsq_ld(ddelm_lsq* lsq);
 void ddelm_gpu_lsq_destroy(ddelm_lsq* lsq);
+/* FP64 tensor-pipe throughput of this device (TFLOP/s): a DMMA m8n8k4 loop on every SM, best of
+ * three CUDA-event-timed launches — the FP64 roofline denominator bench.py reports against. */
+int ddelm_gpu_fp64_peak(int device, double* tflops);
 
 #ifdef __cplusplus
 }

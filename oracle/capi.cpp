@@ -272,6 +272,16 @@ int ddo_errors(void* p, int n, double* l2, double* h1) {
   return 0;
 }
 
+/// CPU-baseline mode: LsFactor through SciPy's LAPACK at `libpath` (nullptr: the restatement)
+int ddo_set_lapack(const char* libpath) {
+  try {
+    set_lapack(libpath);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
 // ---- factorisation-level entry points (LsFactor tests, test_solvers.cpp:14-85)
 /// seeded standard-normal matrix, column-major (test_solvers.cpp:14-21: mt19937_64 + libstdc++
 /// normal_distribution, column by column)

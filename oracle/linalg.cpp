@@ -13,7 +13,9 @@
 namespace ddo {
 
 Vec gemv(const Mat& A, const Vec& x) {
-  Vec y(A.r, 0.0);
+  Vec y;
+  if (blas_gemv(false, A, x, y)) return y;
+  y.assign(A.r, 0.0);
   for (int j = 0; j < A.c; ++j) {
     const double xj = x[j];
     if (xj == 0.0) continue;  // exact zero contributes exactly zero
@@ -24,7 +26,9 @@ Vec gemv(const Mat& A, const Vec& x) {
 }
 
 Vec gemv_t(const Mat& A, const Vec& x) {
-  Vec y(A.c, 0.0);
+  Vec y;
+  if (blas_gemv(true, A, x, y)) return y;
+  y.assign(A.c, 0.0);
   for (int j = 0; j < A.c; ++j) {
     const double* a = A.col(j);
     double s = 0;
@@ -282,6 +286,10 @@ static bool rinv_probe();
 // ------------------------------------------------------------- LsFactor (solvers.cpp:24-78)
 LsFactor::LsFactor(const Mat& K, double rank_tol) : rows_(K.r), cols_(K.c) {
   if (rows_ < cols_) throw std::invalid_argument("LsFactor: matrix must be square or tall");
+  if (lapack_enabled()) {  // CPU-baseline mode (lapack.cpp): the same contract on LAPACK
+    lapack_lsfactor(K, rank_tol, deficient_, rank_, qr_diag_ratio, Q_, R_, K_, pinv_);
+    return;
+  }
   HouseholderQR qr;
   qr.compute(K);
   double dmax = 0, dmin = std::numeric_limits<double>::infinity();

@@ -287,6 +287,15 @@ class LsFactor {
   Mat Q_, R_, K_, pinv_, Rinv_;
 };
 
+/// CPU-baseline mode: LsFactor on SciPy's LAPACK (lapack.cpp); path nullptr / "" disables it.
+bool set_lapack(const char* libpath);
+bool lapack_enabled();
+/// CPU-baseline mode: y = A x (trans: A^T x) through the LAPACK library's BLAS dgemv (one thread),
+/// as Eigen's vectorised GEMV would run the reference's CG; false when the mode is off
+bool blas_gemv(bool trans, const Mat& A, const Vec& x, Vec& y);
+void lapack_lsfactor(const Mat& K, double rank_tol, bool& deficient, int& rank, double& ratio, Mat& Q, Mat& R,
+                     Mat& Kcopy, Mat& pinv);
+
 struct LLT {
   Mat L;
   bool ok = false;

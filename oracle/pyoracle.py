@@ -60,7 +60,7 @@ def lib():
         for name in ("ddo_info", "ddo_timings", "ddo_residuals", "ddo_mu", "ddo_coeffs",
                      "ddo_ranks", "ddo_layer", "ddo_local", "ddo_kbar", "ddo_field",
                      "ddo_field_of", "ddo_errors", "ddo_apply_cs", "ddo_apply_reduced", "ddo_dense", "ddo_apply_p",
-                     "ddo_random_matrix", "ddo_lsfactor", "ddo_cod_pinv"):
+                     "ddo_random_matrix", "ddo_lsfactor", "ddo_cod_pinv", "ddo_set_lapack"):
             getattr(L, name).argtypes = None  # variadic pointer args, set per call
         _lib = L
     return _lib
@@ -214,6 +214,26 @@ class OracleWorkspace:
         if rc:
             raise RuntimeError("problem has no exact solution")
         return l2.value, h1.value
+
+
+def scipy_lapack_path() -> str:
+    """SciPy's bundled OpenBLAS/LAPACK (symbols scipy_d*_)."""
+    import glob
+
+    import scipy
+    libs = glob.glob(os.path.join(os.path.dirname(scipy.__file__), "..", "scipy.libs", "libscipy_openblas*.so"))
+    if not libs:
+        raise RuntimeError("SciPy's libscipy_openblas not found")
+    return os.path.abspath(sorted(libs)[0])
+
+
+def use_lapack(on: bool = True) -> str | None:
+    """Switch the oracle's LsFactor to LAPACK (dgeqrf / dgeqp3 / dtzrzf, lapack.cpp) — the CPU
+    baseline mode — or back to the restatement the goldens were made with."""
+    path = scipy_lapack_path() if on else None
+    if lib().ddo_set_lapack(path.encode() if path else None) != 0:
+        raise RuntimeError("ddo_set_lapack failed")
+    return path
 
 
 def random_matrix(rows: int, cols: int, seed: int) -> np.ndarray:

@@ -44,7 +44,8 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_plan_tables", "ddelm_gpu_sample_field", "ddelm_gpu_relative_errors",
            "ddelm_gpu_field_diff", "ddelm_gpu_apply_reduced", "ddelm_gpu_dense_oracle",
            "ddelm_gpu_apply_neumann", "ddelm_gpu_set_cg_blocks", "ddelm_gpu_create_sharded_host",
-           "ddelm_gpu_exchange_lists", "ddelm_gpu_cg_driver", "ddelm_gpu_lsfactor_batch")
+           "ddelm_gpu_exchange_lists", "ddelm_gpu_cg_driver", "ddelm_gpu_lsfactor_batch",
+           "ddelm_gpu_fp64_peak")
 
 
 class _Desc(C.Structure):
@@ -127,6 +128,7 @@ def load_library(path: str = LIB_PATH):
                                            C.c_void_p, C.c_int]
     L.ddelm_gpu_lsfactor_batch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_double,
                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.ddelm_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.ddelm_gpu_cg_driver.argtypes = [C.c_void_p]
     L.ddelm_gpu_cg_driver.restype = C.c_char_p
     _lib = L
@@ -226,6 +228,13 @@ def _cfg_desc(cfg) -> _Desc:
 # exchange points / tables of the sharded iteration (plan.hpp XPoint / XTable)
 XPOINTS = ("op1", "op2", "nn1", "nn2", "op3", "op4")
 XTABLES = ("t", "psi", "t3", "o", "x", "tr", "zz", "xc", "opi", "pap")
+
+
+def fp64_peak(device: int = 0) -> float:
+    """Measured FP64 tensor-pipe TFLOP/s of this B200 (DMMA loop; ddelm_gpu_fp64_peak)."""
+    t = C.c_double()
+    _check(load_library().ddelm_gpu_fp64_peak(device, C.byref(t)))
+    return t.value
 
 
 def exchange_lists(cfg, rank: int, world: int, one_level: bool = False) -> dict:

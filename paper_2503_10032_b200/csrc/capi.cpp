@@ -500,4 +500,11 @@ int ddelm_gpu_lsq_ld(ddelm_lsq* L) { return L ? L->a.ld : 0; }
 
 void ddelm_gpu_lsq_destroy(ddelm_lsq* L) { delete L; }
 
+int ddelm_gpu_fp64_peak(int device, double* tflops) {
+  return guarded([&] {
+    if (!tflops) throw std::invalid_argument("ddelm_gpu_fp64_peak: null argument");
+    *tflops = ddg::fp64_peak_probe(device);
+  });
+}
+
 }  // extern "C"

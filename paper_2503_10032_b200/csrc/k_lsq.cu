@@ -10,6 +10,8 @@
 // assemble_coarse (solvers.cpp:286-321); SURVEY.md §8d "C5".
 #include <cstdint>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -155,6 +157,58 @@ void launch_lsq_gram(const LsqArgs& a, cudaStream_t st) {
   DDG_CUDA(cudaFuncSetAttribute(lsq_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   lsq_gram_kernel<<<dim3(t, t, a.nb), 256, smem, st>>>(a);
   DDG_LAUNCH_CHECK();
+}
+
+namespace {
+/// FP64 tensor-pipe throughput probe: independent DMMA m8n8k4 chains, 8 per warp (the roofline
+/// denominator of the QR / Schur FLOP rates, measured on the box that runs the bench)
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* out, int iters) {
+  const double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) out[0] = s;
+}
+}  // namespace
+
+double fp64_peak_probe(int device) {
+  DDG_CUDA(cudaSetDevice(device));
+  int sms = 0;
+  DDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* d = nullptr;
+  DDG_CUDA(cudaMalloc(&d, sizeof(double)));
+  cudaEvent_t e0, e1;
+  DDG_CUDA(cudaEventCreate(&e0));
+  DDG_CUDA(cudaEventCreate(&e1));
+  const int iters = 4096, blocks = sms * 4;
+  dmma_probe_kernel<<<blocks, 256>>>(d, 64);  // warm-up
+  DDG_LAUNCH_CHECK();
+  double best = 0;
+  for (int rep = 0; rep < 3; ++rep) {
+    DDG_CUDA(cudaEventRecord(e0));
+    dmma_probe_kernel<<<blocks, 256>>>(d, iters);
+    DDG_CUDA(cudaEventRecord(e1));
+    DDG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    DDG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    // one m8n8k4 = 2 * 8 * 8 * 4 flops per warp instruction
+    const double flops = 2.0 * 8 * 8 * 4 * 8.0 * iters * (blocks * 256 / 32);
+    best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return best;
 }
 
 }  // namespace ddg

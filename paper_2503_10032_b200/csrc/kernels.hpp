@@ -178,6 +178,8 @@ struct LsqArgs {
 };
 void launch_lsq_generate(const LsqArgs& a, uint64_t seed, int kind, cudaStream_t st);  // kind 0 tanh, 1 N(0,1)
 void launch_lsq_gram(const LsqArgs& a, cudaStream_t st);
+/// measured FP64 tensor-pipe throughput (TFLOP/s) of a DMMA m8n8k4 loop on `device`
+double fp64_peak_probe(int device);
 
 // ---------------------------------------------------------------- CG (k_cg.cu)
 /// Per-subdomain geometry of the interface iteration in one 48-byte record (one dependent load

@@ -1210,7 +1210,7 @@ long long Workspace::run_cg_phased(const CgArgs& a_in) {
     long long per_chunk = 0;
     cudaGraph_t g = nullptr;
     cudaGraphExec_t gx = nullptr;
-    DDG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    DDG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
     for (int k = 0; k < K; ++k) per_chunk += iteration(a, true, none);
     DDG_CUDA(cudaStreamEndCapture(st_, &g));
     DDG_CUDA(cudaGraphInstantiate(&gx, g, 0));
