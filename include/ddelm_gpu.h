@@ -172,7 +172,7 @@ int ddelm_gpu_get_ranks(ddelm_ws* ws, int* rank_k, int* rank_kbar, double* qr_ra
 /* Feature layer of subdomain i (w0, w1, b: M each) — for field evaluation by the caller. */
 int ddelm_gpu_get_layer(ddelm_ws* ws, int i, double* w0, double* w1, double* b);
 /* Local matrices as built on the device (rows x M column-major), for parity tests. */
-int ddelm_gpu_get_local(ddelm_ws* ws, int i, int which /* 0 K, 1 Kbar */, double* K, int* rows);
+int ddelm_gpu_get_local(ddelm_ws* ws, int i, int which /* 0 K, 1 Kbar, 2 f (rows x 1) */, double* K, int* rows);
 /* out = cs_reduced_apply(v, weight) on the device (solvers.cpp:372-386, weight 599-603;
  * theta = 0: plain coarse operator). v, out: n_delta host doubles. Builds layers as needed. */
 int ddelm_gpu_apply_operator(ddelm_ws* ws, double theta, const double* v, double* out);

@@ -417,6 +417,14 @@ class Workspace:
         _check(load_library().ddelm_gpu_get_local(self._h, i, which, _ptr(K), C.byref(rows)))
         return K.T.copy()
 
+    def local_rhs(self, i: int) -> np.ndarray:
+        """f_i (assembly.cpp:21-33) as the device holds it (GRF problems: evaluated on the device)."""
+        rows = C.c_int()
+        _check(load_library().ddelm_gpu_get_local(self._h, i, 2, None, C.byref(rows)))
+        f = np.zeros(rows.value)
+        _check(load_library().ddelm_gpu_get_local(self._h, i, 2, _ptr(f), C.byref(rows)))
+        return f
+
     def invalidate(self):
         """Drop built layers, keep the device-resident feature layers."""
         _check(load_library().ddelm_gpu_invalidate(self._h))

@@ -343,6 +343,7 @@ int ddelm_gpu_get_local(ddelm_ws* ws, int i, int which, double* K, int* rows) {
   return guarded([&] {
     const ddg::Plan& p = ws->w->plan;
     if (i < 0 || i >= p.N) throw std::invalid_argument("ddelm_gpu_get_local: bad subdomain");
+    if (which < 0 || which > 2) throw std::invalid_argument("ddelm_gpu_get_local: which must be 0 (K), 1 (Kbar) or 2 (f)");
     if (rows) *rows = p.classes[p.subs[i].cls].m;  // this subdomain's rows (cc = 2: per class)
     if (K) ws->w->get_local(i, which, K);
   });

@@ -9,6 +9,8 @@
 //
 // HBM roofline: writes 8*(2 m M + nF M + nd M) bytes per subdomain; threads
 // map to consecutive rows of a column-major matrix so every store is coalesced.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.hpp"
 #include "plan.hpp"
@@ -193,7 +195,66 @@ __global__ void fill_append_kernel(FeatureArgs p) {
   }
 }
 
+/// Gaussian-random-field problem data at every row point (problems.cpp:41-66, 74-87, 117-121,
+/// 157-166): one thread per (subdomain, class task), the 256 terms (sampled on the host in the
+/// reference's draw order) in shared memory, summed in the reference's order. poisson_grf: the
+/// forcing f = grf at the interior rows; varcoef_poisson: (rho, rho_x, rho_y) with
+/// rho = tanh(grf) + 1.1 and grad rho = (1 - tanh^2) grad grf at interior and flux rows.
+__global__ void __launch_bounds__(256) grf_eval_kernel(GrfArgs g) {
+  __shared__ double amp[kGrfTerms], fx[kGrfTerms], fy[kGrfTerms], ph[kGrfTerms];
+  for (int k = threadIdx.x; k < kGrfTerms; k += blockDim.x) {
+    amp[k] = g.terms[k];
+    fx[k] = g.terms[kGrfTerms + k];
+    fy[k] = g.terms[2 * kGrfTerms + k];
+    ph[k] = g.terms[3 * kGrfTerms + k];
+  }
+  __syncthreads();
+  const int i = blockIdx.y;
+  const int cls = g.sub_cls[i];
+  const int ntask = g.cls_task_cnt[cls];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntask) return;
+  const Task tk = g.tasks[g.cls_task_off[cls] + t];
+  const bool k_row = t < g.n_tasks_k[cls] && tk.row < g.fixed[cls];
+  const bool want_f = g.problem == 3 && k_row && tk.kind == kLap;
+  const bool want_rho = g.problem == 4 && (tk.kind == kLap || tk.kind == kFlux);
+  if (!want_f && !want_rho) return;
+  const double x = coord(g.sub_ix[i] * (g.n_grid - 1), tk.a, g.S);
+  const double y = coord(g.sub_iy[i] * (g.n_grid - 1), tk.b, g.S);
+  double v = 0.0, dx = 0.0, dy = 0.0;
+  for (int k = 0; k < kGrfTerms; ++k) {
+    // fx x + fy y + phase without FMA contraction (the host restatement's rounding)
+    const double arg = __dadd_rn(__dadd_rn(__dmul_rn(fx[k], x), __dmul_rn(fy[k], y)), ph[k]);
+    if (want_f) {
+      v = __dadd_rn(v, __dmul_rn(amp[k], sin(arg)));
+    } else {
+      double sn, cs;
+      sincos(arg, &sn, &cs);
+      v = __dadd_rn(v, __dmul_rn(amp[k], sn));
+      const double c = __dmul_rn(amp[k], cs);
+      dx = __dadd_rn(dx, __dmul_rn(c, fx[k]));
+      dy = __dadd_rn(dy, __dmul_rn(c, fy[k]));
+    }
+  }
+  if (want_f) {
+    g.f[static_cast<size_t>(i) * g.m + tk.row] = v;
+  } else {
+    const double th = tanh(v);
+    const double s1 = __dadd_rn(1.0, -__dmul_rn(th, th));
+    double* out = g.coef + (static_cast<size_t>(i) * g.tmax + t) * 3;
+    out[0] = __dadd_rn(th, 1.1);
+    out[1] = __dmul_rn(s1, dx);
+    out[2] = __dmul_rn(s1, dy);
+  }
+}
+
 }  // namespace
+
+void launch_grf_eval(const GrfArgs& g, int max_tasks, cudaStream_t st) {
+  dim3 grid(ceil_div(std::max(max_tasks, 1), 256), g.N);
+  grf_eval_kernel<<<grid, 256, 0, st>>>(g);
+  DDG_LAUNCH_CHECK();
+}
 
 void launch_build_features(const FeatureArgs& a, cudaStream_t st) {
   dim3 grid(ceil_div(a.M, 32), a.N);

@@ -36,6 +36,25 @@ struct FeatureArgs {
 };
 void launch_build_features(const FeatureArgs& a, cudaStream_t st);
 
+/// Device evaluation of the Gaussian random field at every row point (problems 3 poisson_grf and
+/// 4 varcoef_poisson; k_features.cu grf_eval_kernel).
+constexpr int kGrfTerms = 256;
+struct GrfArgs {
+  int problem, N, m, tmax, n_grid, S;
+  const double* terms;  // 4 x 256: amp | fx | fy | phase (host-sampled, problems.cpp:15-39 order)
+  const Task* tasks;
+  const int* cls_task_off;
+  const int* cls_task_cnt;
+  const int* n_tasks_k;  // per class: leading K-row tasks
+  const int* fixed;      // per class: K rows before the trace rows
+  const int* sub_cls;
+  const int* sub_ix;
+  const int* sub_iy;
+  double* f;     // N x m   (poisson_grf interior rows)
+  double* coef;  // N x tmax x 3 (varcoef_poisson)
+};
+void launch_grf_eval(const GrfArgs& g, int max_tasks, cudaStream_t st);
+
 // ---------------------------------------------------------------- QR (k_qr.cu)
 struct QrArgs {
   int nmat, m, ld, ncol, M;

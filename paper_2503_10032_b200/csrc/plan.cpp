@@ -193,27 +193,7 @@ GrfField sample_grf(double alpha, uint64_t seed) {  // problems.cpp:15-39: draw 
   return g;
 }
 
-double eval_grf(const GrfField& g, double x, double y) {  // problems.cpp:41-46
-  double v = 0.0;
-  for (size_t i = 0; i < g.amp.size(); ++i) v += g.amp[i] * std::sin(g.fx[i] * x + g.fy[i] * y + g.phase[i]);
-  return v;
-}
 
-namespace {
-/// rho = tanh(grf) + 1.1 and grad rho = (1 - tanh^2) grad grf (problems.cpp:48-66)
-void rho_and_grad(const GrfField& g, double x, double y, double* out) {
-  const double t = std::tanh(eval_grf(g, x, y));
-  double dx = 0.0, dy = 0.0;
-  for (size_t i = 0; i < g.amp.size(); ++i) {
-    const double c = g.amp[i] * std::cos(g.fx[i] * x + g.fy[i] * y + g.phase[i]);
-    dx += c * g.fx[i];
-    dy += c * g.fy[i];
-  }
-  out[0] = t + 1.1;
-  out[1] = (1.0 - t * t) * dx;
-  out[2] = (1.0 - t * t) * dy;
-}
-}  // namespace
 
 double problem_forcing(int problem, double x, double y) {
   switch (problem) {
@@ -391,10 +371,11 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
   // ---- right-hand sides f (assembly.cpp:21-33): forcing, boundary data, zero on traces;
   //      varcoef_poisson: the coefficient field at every row point (problems.cpp:74-87, 117-121)
   const int S = s * (n - 1);
-  GrfField grf;
-  if (problem == 3) grf = sample_grf(params.alpha, params.forcing_seed);
+  // GRF problems: the field is sampled here (1024 draws in the reference's order); its values at
+  // the row points are evaluated on the device (Workspace::upload_plan -> grf_eval_kernel)
+  if (problem == 3) p.grf = sample_grf(params.alpha, params.forcing_seed);
   if (problem == 4) {
-    grf = sample_grf(params.alpha, params.rho_seed);
+    p.grf = sample_grf(params.alpha, params.rho_seed);
     p.coef.assign(static_cast<size_t>(p.N) * p.tmax * 3, 0.0);
   }
   p.f.assign(static_cast<size_t>(p.N) * p.m, 0.0);
@@ -406,12 +387,10 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
         const Task& tk = c.tasks[t];
         const double x = static_cast<double>(sp.ix * (n - 1) + tk.a) / S;
         const double y = static_cast<double>(sp.iy * (n - 1) + tk.b) / S;
-        if (problem == 4 && (tk.kind == kLap || tk.kind == kFlux))
-          rho_and_grad(grf, x, y, &p.coef[(static_cast<size_t>(i) * p.tmax + t) * 3]);
         if (t >= c.n_tasks_k || tk.row >= c.fixed) continue;
         double v;
         if (problem <= 2) v = tk.kind == kLap ? problem_forcing(problem, x, y) : problem_boundary(problem, x, y);
-        else if (problem == 3) v = tk.kind == kLap ? eval_grf(grf, x, y) : 0.0;
+        else if (problem == 3) v = 0.0;  // interior rows: the GRF forcing, evaluated on the device
         else if (problem == 4) v = tk.kind == kLap ? 1.0 : 0.0;
         else  // biharmonic_sinpi: lap^2 u = 4 pi^4 sin sin, u = sin sin, lap u = -2 pi^2 sin sin
           v = tk.kind == kBih   ? 4.0 * kPi * kPi * kPi * kPi * std::sin(kPi * x) * std::sin(kPi * y)
@@ -421,14 +400,7 @@ Plan build_plan(int problem, int s, int n_grid, int M, double l, uint64_t seed, 
       }
     }
   };
-  if (problem >= 3 && p.N > 1) {  // 256-term GRF sums per point: the reference's parallel_for
-    const int nt = std::max(1, std::min<int>(p.N, static_cast<int>(std::thread::hardware_concurrency())));
-    std::vector<std::thread> th;
-    for (int k = 0; k < nt; ++k) th.emplace_back(fill, p.N * k / nt, p.N * (k + 1) / nt);
-    for (auto& t : th) t.join();
-  } else {
-    fill(0, p.N);
-  }
+  fill(0, p.N);
   return p;
 }
 

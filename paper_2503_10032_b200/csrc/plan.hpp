@@ -101,7 +101,6 @@ struct GrfField {
   std::vector<double> amp, fx, fy, phase;
 };
 GrfField sample_grf(double alpha, uint64_t seed);
-double eval_grf(const GrfField& g, double x, double y);
 
 struct Plan {
   int problem = 0, s = 1, n_grid = 3, M = 1;
@@ -130,6 +129,10 @@ struct Plan {
   // varcoef_poisson: per subdomain and class task, (rho, d rho/dx, d rho/dy) at the task's point
   // (interior rows: -rho lap - grad rho . grad; flux rows: x rho); empty for the other problems
   std::vector<double> coef;  // N x tmax x 3
+  // poisson_grf / varcoef_poisson: the 256-term field drawn on the host in the reference's order;
+  // its values at the row points (f, coef above, left zero here) are evaluated on the device
+  // (k_features.cu grf_eval_kernel)
+  GrfField grf;
 
   // ---- sharding: this plan holds subdomains [sub_lo, sub_lo + N) of N_global (one rank's
   // contiguous strip); the interface numbering (n_delta, n_pi, npf) stays global

@@ -234,6 +234,44 @@ void Workspace::upload_plan() {
   g_arena = nullptr;  // setup-only / large buffers below
   d_f.upload(p.f, st_);
   if (!p.coef.empty()) d_coef.upload(p.coef, st_);
+  if (p.problem == 3 || p.problem == 4) {
+    // the GRF problem data at every row point, evaluated on the device (grf_eval_kernel)
+    if (p.grf.amp.size() != static_cast<size_t>(kGrfTerms)) throw std::logic_error("GRF problem without a sampled field");
+    std::vector<double> terms;
+    for (const auto* v : {&p.grf.amp, &p.grf.fx, &p.grf.fy, &p.grf.phase}) terms.insert(terms.end(), v->begin(), v->end());
+    std::vector<int> ntk, fixed;
+    int max_tasks = 0;
+    for (const ClassPlan& c : p.classes) {
+      ntk.push_back(c.n_tasks_k);
+      fixed.push_back(c.fixed);
+      max_tasks = std::max(max_tasks, c.n_tasks_k + c.n_tasks_kbar + c.n_tasks_f + c.n_tasks_cd);
+    }
+    DevBuf<double> d_terms;
+    DevBuf<int> d_ntk, d_fixed;
+    d_terms.upload(terms, st_);
+    d_ntk.upload(ntk, st_);
+    d_fixed.upload(fixed, st_);
+    GrfArgs g{};
+    g.problem = p.problem;
+    g.N = N;
+    g.m = p.m;
+    g.tmax = p.tmax;
+    g.n_grid = p.n_grid;
+    g.S = p.s * (p.n_grid - 1);
+    g.terms = d_terms.ptr;
+    g.tasks = d_tasks.ptr;
+    g.cls_task_off = d_task_off.ptr;
+    g.cls_task_cnt = d_task_cnt.ptr;
+    g.n_tasks_k = d_ntk.ptr;
+    g.fixed = d_fixed.ptr;
+    g.sub_cls = d_cls.ptr;
+    g.sub_ix = d_ix.ptr;
+    g.sub_iy = d_iy.ptr;
+    g.f = d_f.ptr;
+    g.coef = p.problem == 4 ? d_coef.ptr : nullptr;
+    launch_grf_eval(g, max_tasks, st_);
+    DDG_CUDA(cudaStreamSynchronize(st_));  // the scratch buffers go out of scope
+  }
 
   // fixed-size device storage
   ld_ = (p.m + 3) / 4 * 4;
@@ -1350,6 +1388,13 @@ void Workspace::get_ranks(int* rk, int* rkb, double* ratio) {
 }
 
 void Workspace::get_local(int i, int which, double* K) {
+  if (which == 2) {  // the right-hand side f_i (problem data; GRF values as evaluated on the device)
+    const size_t rows = plan.classes[plan.subs[i].cls].m;
+    DDG_CUDA(cudaMemcpyAsync(K, d_f.ptr + static_cast<size_t>(i) * plan.m, sizeof(double) * rows,
+                             cudaMemcpyDeviceToHost, st_));
+    DDG_CUDA(cudaStreamSynchronize(st_));
+    return;
+  }
   // The factorisation overwrites the matrices in place, so re-run the feature kernel (with the
   // current seed's layers) and invalidate the built layers.
   init_layers();

@@ -4,10 +4,13 @@ forcing drawn with the reference's generator and draw order, zero boundary data)
 varcoef_poisson (-div(rho grad u) = 1 with rho = tanh(GRF) + 1.1: interior rows
 -rho lap - grad rho . grad, conormal flux rows rho du/dn in F and in the Neumann matrices).
 
-The coefficient field is evaluated on the host in the oracle's arithmetic (bit-identical rho and
-grad rho); the device rows differ from the oracle's only through the ~1-ulp tanh difference, which
-1 - tanh^2 magnifies near saturation and grad rho (up to ~1e4 at alpha = 32) multiplies: rows agree
-to 2e-11 relative. The GRF-forcing solves are held to the bar of test_gpu_parity.py (field <=
+The field's 256 terms are drawn on the host with the reference's generator and draw order
+(bit-identical), and evaluated at every row point ON THE DEVICE (k_features.cu grf_eval_kernel:
+the forcing of poisson_grf, rho and grad rho of varcoef_poisson); the device values differ from the
+oracle's only through the ~1-ulp sin / cos / tanh differences: the forcing agrees to 1e-13
+relative (test_grf_forcing_evaluated_on_device_matches_oracle), and the varcoef rows — where
+1 - tanh^2 magnifies the tanh ulp near saturation and grad rho (up to ~1e4 at alpha = 32)
+multiplies it — to 2e-11 relative. The GRF-forcing solves are held to the bar of test_gpu_parity.py (field <=
 max(1e-9, 4 x spread), iterations within 1 + 2 x spread; spreads from the tanh-value probe,
 tools/make_goldens.py --probe tanh). The variable-coefficient matrices are far worse conditioned
 (kappa(K) up to 8e9 on T2v vs 3e7 on T2: rows scaled by grad rho), so the two factorisations'
@@ -47,6 +50,23 @@ def test_grf_and_varcoef_matrices_match_oracle(P, name):
         for Kg, Ko in ((ws.local_matrix(i, 0), ows.local(i)[0]), (ws.local_matrix(i, 1), ows.kbar(i))):
             row_scale = np.maximum(np.abs(Ko).max(axis=1, keepdims=True), 1e-300)
             assert np.max(np.abs(Kg - Ko) / row_scale) <= tol
+
+
+@pytest.mark.parametrize("name", ["T2g", "C2g", "T2v"])
+def test_grf_forcing_evaluated_on_device_matches_oracle(P, name):
+    """f_i of every subdomain (assembly.cpp:21-33 with the GRF forcing, problems.cpp:41-46,
+    157-166) as the device evaluated it vs the oracle's host evaluation: <= 1e-13 relative to the
+    largest |f| (sin / cos ulps over 256 terms)."""
+    cfg = P.CONFIGS[name]
+    ws = P.workspace_from_config(name)
+    ows = _oracle(cfg)
+    worst = 0.0
+    for i in range(ws.n_subs):
+        fg = ws.local_rhs(i)
+        fo = ows.local(i)[1]
+        assert fg.shape == fo.shape
+        worst = max(worst, np.max(np.abs(fg - fo)) / max(np.max(np.abs(fo)), 1e-300))
+    assert worst <= 1e-13, worst
 
 
 @pytest.mark.parametrize("name", FULL_RANK + DEFICIENT)
