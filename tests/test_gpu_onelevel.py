@@ -132,6 +132,6 @@ def test_cpp_facade_one_level(P):
     assert d["iterations"] == rep.iterations
     assert np.array_equal(np.array(d["mu"]), rep.mu)
     l2, h1 = ws.relative_errors(257)
-    assert d["l2_error"] == l2 and d["h1_error"] == h1
+    assert d["errors"]["l2"] == l2 and d["errors"]["h1"] == h1  # runner.cpp:220-223 schema
     bad = subprocess.run([exe, "method=ddelm-xx"], capture_output=True, text=True, timeout=120)
     assert bad.returncode == 3
