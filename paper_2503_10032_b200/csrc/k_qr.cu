@@ -11,6 +11,9 @@
 //                 tcgen05.mma has no f64 kind on sm_100a.
 // The appended columns [f | E] ride along in the trailing updates, so the factorisation also
 // produces Q0^T [f | E] (the interface rows of Q and Q^T f) with no extra pass.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
@@ -621,10 +624,13 @@ struct TrailSmem {
   double A[kTrStages][TN * RCP];   // A chunk, column c at A[c*RCP + k]
   double W[NB_ * TNP];             // W, then W'
   double T[NB_ * (NB_ + 1)];
+  uint64_t full[kTrStages];        // bulk-copy completion of each ring stage
 };
 
 template <int NB_>
-__global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrArgs a, int k0, int nbw, int cb, int ce, int tq) {
+__global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1)
+    qr_trailing_kernel(QrArgs a, int k0, int nbw, int cb, int ce, int tq, const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmV) {
   static_assert(NB_ == 32 || NB_ == 64, "panel width");
   constexpr int MT = NB_ / 8;  // m-tiles of W
   extern __shared__ __align__(16) double smraw[];
@@ -640,47 +646,40 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lr = lane >> 2, lc = lane & 3;
 
-  // issue chunk q of the unified stream (q < nq: pass 1, else pass 2) into stage q % 3
-  // Each thread copies the same two-row segment (rows 2 seg, 2 seg + 1 of every chunk) of a fixed
-  // set of columns: the column pointers and shared-memory offsets are computed once, so issuing a
-  // chunk is one add and one cp.async per segment (no per-chunk index arithmetic).
-  constexpr int kSegs = (NB_ + TN) * 16 / 256;
-  const int seg = threadIdx.x & 15;
-  const double* gcol[kSegs];
-  int soff[kSegs];
-  bool isv[kSegs], cok[kSegs];
-#pragma unroll
-  for (int j = 0; j < kSegs; ++j) {
-    const int col = (threadIdx.x >> 4) + 16 * j;
-    isv[j] = col < NB_;
-    if (isv[j]) {
-      cok[j] = col < nb;
-      gcol[j] = A + static_cast<size_t>(k0 + (cok[j] ? col : 0)) * ld;
-      soff[j] = col * RCP + 2 * seg;
-    } else {
-      const int c = col - NB_;
-      cok[j] = c < ncols;
-      gcol[j] = A + static_cast<size_t>(c0 + (cok[j] ? c : 0)) * ld;
-      soff[j] = c * RCP + 2 * seg;
-    }
+  // issue chunk q of the unified stream (q < nq: pass 1, else pass 2) into stage q % 3 with two TMA
+  // tensor copies (cp.async.bulk.tensor, SASS UTMALDG): the 36-row x 64-column A tile box and the
+  // 36-row x NB V box of the batched matrices seen as one (ld x ncol * nmat) tensor. The 36-row
+  // box IS the padded column stride (RCP): every m8n8k4 fragment load stays bank-conflict free;
+  // rows past ld arrive as zeros (TMA out-of-bounds fill). Columns past the tile / panel carry
+  // finite data of the neighbouring columns: their W' rows are zero (T is zero-padded) and their
+  // updates are never stored.
+  if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < kTrStages; ++s2) mbar_init(&S.full[s2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
+  const int colA = t * a.ncol + c0, colV = t * a.ncol + k0;
   auto issue = [&](int q) {
-    if (q < 2 * nq) {
-      const int st = q % kTrStages;
-      // pass 2 walks the row chunks backwards: its first chunks are the ones pass 1 read last,
-      // still in L2 (the concurrent A tiles far exceed L2, so a forward pass 2 re-reads HBM)
-      const int cq = q < nq ? q : 2 * nq - 1 - q;
-      const int row = k0 + cq * RC + 2 * seg;
-      const bool rok = row < static_cast<int>(ld);
-#pragma unroll
-      for (int j = 0; j < kSegs; ++j) {
-        const bool ok = cok[j] && rok;
-        double* dst = (isv[j] ? S.V[st] : S.A[st]) + soff[j];
-        cp_async16(dst, gcol[j] + (ok ? row : 0), ok);
-      }
-    }
-    cp_async_commit();
+    if (q >= 2 * nq || threadIdx.x != 0) return;
+    const int st = q % kTrStages;
+    // pass 2 walks the row chunks backwards: its first chunks are the ones pass 1 read last,
+    // still in L2 (the concurrent A tiles far exceed L2, so a forward pass 2 re-reads HBM)
+    const int cq = q < nq ? q : 2 * nq - 1 - q;
+    const int row = k0 + cq * RC;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&S.full[st], static_cast<uint32_t>((TN + NB_) * RCP * sizeof(double)));
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(S.A[st])),
+        "l"(&tmA), "r"(row), "r"(colA), "r"(smem_u32(&S.full[st]))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(S.V[st])),
+        "l"(&tmV), "r"(row), "r"(colV), "r"(smem_u32(&S.full[st]))
+        : "memory");
   };
+  auto wait_chunk = [&](int q) { mbar_wait(&S.full[q % kTrStages], static_cast<uint32_t>((q / kTrStages) & 1)); };
   // unit lower-triangular structure of V inside the first NB rows of the stream
   auto fix_v = [&](int st, int r0) {
     if (r0 >= k0 + nb) return;
@@ -710,8 +709,8 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int q = 0; q < nq; ++q) {
-    cp_async_wait<1>();
-    __syncthreads();
+    wait_chunk(q);
+    __syncthreads();  // every warp is done with the stage chunk q + 2 overwrites
     issue(q + 2);
     const int st = q % kTrStages;
     fix_v(st, k0 + q * RC);
@@ -773,7 +772,7 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
   // ---- pass 2: A_tile -= V W' per 32-row chunk. Warp tile: 2 row-tiles x 2 col-tiles.
   const int rt0 = (warp & 1) * 2, ct0 = (warp >> 1) * 2;
   for (int q = nq; q < 2 * nq; ++q) {
-    cp_async_wait<1>();
+    wait_chunk(q);
     __syncthreads();
     issue(q + 2);
     const int st = q % kTrStages;
@@ -817,7 +816,6 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1) qr_trailing_kernel(QrA
         }
       }
   }
-  cp_async_wait<0>();
 }
 
 __global__ void qr_diag_ratio_kernel(QrArgs a, double* ratio) {
@@ -851,6 +849,31 @@ __global__ void qr_diag_ratio_kernel(QrArgs a, double* ratio) {
   }
 }
 
+}  // namespace
+
+namespace {
+/// TMA descriptor of the batched matrices as one 2-D tensor (rows = ld, columns = ncol * nmat,
+/// column stride ld doubles) with a (RCP rows x cols) box: the trailing update's chunk loads.
+CUtensorMap trailing_tensor_map(const QrArgs& a, int cols) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    DDG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.ld), static_cast<cuuint64_t>(a.ncol) * a.nmat};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld) * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(RCP), static_cast<cuuint32_t>(cols)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a.A, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
 }  // namespace
 
 std::vector<QrOp> qr_schedule(int M, int ncol) {
@@ -910,6 +933,7 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
   const int rest = op.ce - op.cb;
   if (rest <= 0) return;
   dim3 grid(ceil_div(rest, TN), a.nmat);
+  const CUtensorMap tmA = trailing_tensor_map(a, TN), tmV = trailing_tensor_map(a, op.kind == QrOp::kTrail32 ? 32 : 64);
   if (op.kind == QrOp::kTrail32) {
     const size_t smem = sizeof(TrailSmem<32>);
     static bool attr = false;
@@ -918,7 +942,7 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
                                     static_cast<int>(smem)));
       attr = true;
     }
-    qr_trailing_kernel<32><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, op.toff);
+    qr_trailing_kernel<32><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, op.toff, tmA, tmV);
   } else {
     const size_t smem = sizeof(TrailSmem<64>);
     static bool attr = false;
@@ -927,7 +951,7 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
                                     static_cast<int>(smem)));
       attr = true;
     }
-    qr_trailing_kernel<64><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, 0);
+    qr_trailing_kernel<64><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, 0, tmA, tmV);
   }
   DDG_LAUNCH_CHECK();
 }
