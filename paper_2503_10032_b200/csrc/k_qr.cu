@@ -605,7 +605,6 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 constexpr int TN = 64;    // tile columns
 constexpr int RCP = 36;   // padded column stride of a staged chunk
 constexpr int TNP = 68;   // padded row stride of W / W'
-constexpr int kTrStages = 3;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -618,23 +617,26 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int NB_>
+/// ring of ST stages; ST = 2 keeps T in L2 instead of shared memory so that 3 CTAs fit an SM
+template <int NB_, int ST>
 struct TrailSmem {
-  double V[kTrStages][NB_ * RCP];  // V chunk, column u at V[u*RCP + k]
-  double A[kTrStages][TN * RCP];   // A chunk, column c at A[c*RCP + k]
-  double W[NB_ * TNP];             // W, then W'
-  double T[NB_ * (NB_ + 1)];
-  uint64_t full[kTrStages];        // bulk-copy completion of each ring stage
+  static constexpr bool kTsmem = ST >= 3;
+  double V[ST][NB_ * RCP];  // V chunk, column u at V[u*RCP + k]
+  double A[ST][TN * RCP];   // A chunk, column c at A[c*RCP + k]
+  double W[NB_ * TNP];      // W, then W'
+  double T[kTsmem ? NB_ * (NB_ + 1) : 2];
+  uint64_t full[ST];        // bulk-copy completion of each ring stage
 };
 
-template <int NB_>
-__global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1)
+template <int NB_, int kTrStages>
+__global__ void __launch_bounds__(256, NB_ == 32 ? (kTrStages == 2 ? 3 : 2) : 1)
     qr_trailing_kernel(QrArgs a, int k0, int nbw, int cb, int ce, int tq, const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmV) {
   static_assert(NB_ == 32 || NB_ == 64, "panel width");
   constexpr int MT = NB_ / 8;  // m-tiles of W
   extern __shared__ __align__(16) double smraw[];
-  TrailSmem<NB_>& S = *reinterpret_cast<TrailSmem<NB_>*>(smraw);
+  TrailSmem<NB_, kTrStages>& S = *reinterpret_cast<TrailSmem<NB_, kTrStages>*>(smraw);
+  constexpr bool kTrTsmem = TrailSmem<NB_, kTrStages>::kTsmem;
   const int t = blockIdx.y;
   const int nb = nbw;  // reflectors k0 .. k0 + nb - 1 (nb <= NB_)
   const int c0 = cb + blockIdx.x * TN;
@@ -690,14 +692,14 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1)
     }
   };
 
-  issue(0);
-  issue(1);
+  for (int q = 0; q < kTrStages - 1; ++q) issue(q);
   // T (nb x nb upper triangular, zero padded)
   const double* Tg = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
-  for (int idx = threadIdx.x; idx < NB_ * NB_; idx += blockDim.x) {
-    const int i = idx / NB_, j = idx % NB_;
-    S.T[i * (NB_ + 1) + j] = (i < nb && j < nb) ? Tg[(tq + i) * kQrTmax + tq + j] : 0.0;
-  }
+  if (kTrTsmem)
+    for (int idx = threadIdx.x; idx < NB_ * NB_; idx += blockDim.x) {
+      const int i = idx / NB_, j = idx % NB_;
+      S.T[i * (NB_ + 1) + j] = (i < nb && j < nb) ? Tg[(tq + i) * kQrTmax + tq + j] : 0.0;
+    }
 
   // ---- pass 1: W = V^T A_tile. Warp tile: (MT/2) m-tiles x 2 n-tiles.
   //      NB=32: warp -> m-tiles {2(w&1), +1}, n-tiles {2(w>>1), +1};  NB=64: m-tiles 4(w&1).., n-tiles 2(w>>1)..
@@ -710,8 +712,8 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1)
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int q = 0; q < nq; ++q) {
     wait_chunk(q);
-    __syncthreads();  // every warp is done with the stage chunk q + 2 overwrites
-    issue(q + 2);
+    __syncthreads();  // every warp is done with the stage chunk q + kTrStages - 1 overwrites
+    issue(q + kTrStages - 1);
     const int st = q % kTrStages;
     fix_v(st, k0 + q * RC);
     __syncthreads();
@@ -757,7 +759,9 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1)
 #pragma unroll
       for (int i = 0; i < MTT; ++i) {
         const int u = i * 8 + lr;
-        const double av = (w <= u) ? S.T[w * (NB_ + 1) + u] : 0.0;
+        const double av = (w <= u) ? (kTrTsmem ? S.T[w * (NB_ + 1) + u]
+                                               : (u < nb ? __ldg(Tg + (tq + w) * kQrTmax + tq + u) : 0.0))
+                                   : 0.0;
         dmma_8x8x4(cw[i][0], cw[i][1], av, bv);
       }
     }
@@ -774,7 +778,7 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? 2 : 1)
   for (int q = nq; q < 2 * nq; ++q) {
     wait_chunk(q);
     __syncthreads();
-    issue(q + 2);
+    issue(q + kTrStages - 1);
     const int st = q % kTrStages;
     const int r0 = k0 + (2 * nq - 1 - q) * RC;
     fix_v(st, r0);
@@ -934,24 +938,21 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
   if (rest <= 0) return;
   dim3 grid(ceil_div(rest, TN), a.nmat);
   const CUtensorMap tmA = trailing_tensor_map(a, TN), tmV = trailing_tensor_map(a, op.kind == QrOp::kTrail32 ? 32 : 64);
+  // ring depth of the 32-wide update: 3 stages (2 CTAs / SM) by default, DDELM_QR_STAGES=2 for
+  // 2 stages with T in L2 (3 CTAs / SM)
+  static const int stages = [] {
+    const char* e = std::getenv("DDELM_QR_STAGES");
+    return (e && std::atoi(e) == 2) ? 2 : 3;
+  }();
+  auto launch = [&](auto kern, size_t smem, int toff) {
+    DDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, toff, tmA, tmV);
+  };
   if (op.kind == QrOp::kTrail32) {
-    const size_t smem = sizeof(TrailSmem<32>);
-    static bool attr = false;
-    if (!attr) {
-      DDG_CUDA(cudaFuncSetAttribute(qr_trailing_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-      attr = true;
-    }
-    qr_trailing_kernel<32><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, op.toff, tmA, tmV);
+    if (stages == 2) launch(qr_trailing_kernel<32, 2>, sizeof(TrailSmem<32, 2>), op.toff);
+    else launch(qr_trailing_kernel<32, 3>, sizeof(TrailSmem<32, 3>), op.toff);
   } else {
-    const size_t smem = sizeof(TrailSmem<64>);
-    static bool attr = false;
-    if (!attr) {
-      DDG_CUDA(cudaFuncSetAttribute(qr_trailing_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-      attr = true;
-    }
-    qr_trailing_kernel<64><<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, 0, tmA, tmV);
+    launch(qr_trailing_kernel<64, 3>, sizeof(TrailSmem<64, 3>), 0);
   }
   DDG_LAUNCH_CHECK();
 }
