@@ -1200,8 +1200,55 @@ long long Workspace::run_cg_phased(const CgArgs& a_in) {
   const bool no_graph = ge && std::strcmp(ge, "0") == 0;
   const bool ptimes = std::getenv("DDELM_CG_PHASE_TIMES") != nullptr;
   const bool can_capture = !sharded() || ex_->capturable();
-  const bool chunked = can_capture && !no_graph && !ptimes && (sharded() || (drv && std::strcmp(drv, "chunked") == 0));
-  const bool host_loop = no_graph || ptimes || !can_capture;
+  bool chunked = can_capture && !no_graph && !ptimes && !capture_failed_ &&
+                 (sharded() || (drv && std::strcmp(drv, "chunked") == 0));
+  if (chunked) {
+    // capture the chunk first; a backend that refuses stream capture (an NCCL build or topology
+    // without graph support) drops this workspace to the host loop for good, loudly
+    cg_driver_ = "graph-chunked";
+    int K = 16;
+    if (const char* e = std::getenv("DDELM_CG_CHUNK")) K = std::max(1, std::atoi(e));
+    CgArgs a = a_in;
+    a.cond = 0;
+    a.guard_all = 1;
+    long long per_chunk = 0;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t gx = nullptr;
+    const long long l_before = launches_;
+    try {
+      DDG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
+      for (int k = 0; k < K; ++k) per_chunk += iteration(a, true, none);
+      DDG_CUDA(cudaStreamEndCapture(st_, &g));
+      DDG_CUDA(cudaGraphInstantiate(&gx, g, 0));
+    } catch (const std::exception& e) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st_, &cs);
+      if (cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(st_, &junk);
+        if (junk) cudaGraphDestroy(junk);
+      }
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      std::fprintf(stderr, "[ddelm] CG graph capture failed (%s); using the host-loop driver\n", e.what());
+      capture_failed_ = true;
+      chunked = false;
+      launches_ = l_before;
+    }
+    if (chunked) {
+      for (int done = 0; done < a.max_iter; done += K) {
+        DDG_CUDA(cudaGraphLaunch(gx, st_));
+        launched += per_chunk;
+        DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+        DDG_CUDA(cudaStreamSynchronize(st_));
+        if (pinned_state_[1]) break;
+      }
+      DDG_CUDA(cudaGraphExecDestroy(gx));
+      DDG_CUDA(cudaGraphDestroy(g));
+      return launched;
+    }
+  }
+  const bool host_loop = no_graph || ptimes || !can_capture || capture_failed_;
   if (host_loop) {
     cg_driver_ = "host-loop";
     CgArgs a = a_in;
@@ -1236,31 +1283,6 @@ long long Workspace::run_cg_phased(const CgArgs& a_in) {
       for (int q = 0; q < 7; ++q) std::fprintf(stderr, "[cg phase] %-4s %8.2f us\n", nm[q], 1e3 * pms[q] / std::max(nit, 1));
       for (auto& e : pev) cudaEventDestroy(e);
     }
-    return launched;
-  }
-  if (chunked) {
-    cg_driver_ = "graph-chunked";
-    int K = 16;
-    if (const char* e = std::getenv("DDELM_CG_CHUNK")) K = std::max(1, std::atoi(e));
-    CgArgs a = a_in;
-    a.cond = 0;
-    a.guard_all = 1;
-    long long per_chunk = 0;
-    cudaGraph_t g = nullptr;
-    cudaGraphExec_t gx = nullptr;
-    DDG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
-    for (int k = 0; k < K; ++k) per_chunk += iteration(a, true, none);
-    DDG_CUDA(cudaStreamEndCapture(st_, &g));
-    DDG_CUDA(cudaGraphInstantiate(&gx, g, 0));
-    for (int done = 0; done < a.max_iter; done += K) {
-      DDG_CUDA(cudaGraphLaunch(gx, st_));
-      launched += per_chunk;
-      DDG_CUDA(cudaMemcpyAsync(pinned_state_, d_state.ptr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
-      DDG_CUDA(cudaStreamSynchronize(st_));
-      if (pinned_state_[1]) break;
-    }
-    DDG_CUDA(cudaGraphExecDestroy(gx));
-    DDG_CUDA(cudaGraphDestroy(g));
     return launched;
   }
   cg_driver_ = "graph-while";

@@ -146,6 +146,7 @@ class Workspace {
   int xpoint(const CgArgs& a, int pt, bool guard);
   /// CG driver actually used by the last solve ("graph-while", "graph-chunked", "host-loop", "persistent")
   const char* cg_driver_ = "graph-while";
+  bool capture_failed_ = false;  // the exchange backend refused stream capture: host loop from now on
   std::unique_ptr<Exchange> ex_;
   bool phased_ = false;
   // kernel timers: begin/end around a launch; collected after the stream syncs
