@@ -17,13 +17,18 @@ namespace ddg {
 
 namespace {
 
-/// out[l][k] = sum_j X[j*ldx + l] * Cm[j*R + k]   for l < rows, k < r   (batched; DFMA tiles)
+/// out[l][k] = sum_j X[j*ldx + l] * Cm[j*R + k]   for l < rows, k < r   (batched)
+/// The Schur contraction of the coarse assembly (FC = F C: the flux rows of K^+, solvers.cpp:
+/// 299-313) on the FP64 tensor cores: a 64 x 64 output tile per CTA, 8 warps of 2 x 4 DMMA
+/// m8n8k4 tiles (16 x 32 outputs), K = the M neuron rows in 16-row chunks staged in shared
+/// memory (row stride 68: every fragment load is bank-conflict free), double-buffered.
 __global__ void __launch_bounds__(256) jmajor_gemm_kernel(int M, int R, const double* X, int ldx,
                                                           size_t xstride, const int* rows_of, int rows_cls,
                                                           const ClassDims* dims, const int* sub_cls,
                                                           const double* Cm, size_t cstride,
                                                           const int* rank, int rank_off,
                                                           double* out, int ldo, size_t ostride) {
+  constexpr int KC = 16, SP = 68;
   const int i = blockIdx.z;
   const ClassDims d = dims[sub_cls[i]];
   const int rows = rows_cls == 0 ? d.nF : d.nd;
@@ -34,40 +39,52 @@ __global__ void __launch_bounds__(256) jmajor_gemm_kernel(int M, int R, const do
   if (l0 >= rows || k0 >= R) return;
   const double* Xi = X + i * xstride;
   const double* Ci = Cm + (rank_off + i) * cstride;
-  __shared__ double Xs[16][64];
-  __shared__ double Cs[16][64];
-  const int tl = (threadIdx.x & 15) * 4, tk = (threadIdx.x >> 4) * 4;
-  double acc[4][4] = {};
-  for (int j0 = 0; j0 < M; j0 += 16) {
-    for (int idx = threadIdx.x; idx < 16 * 64; idx += 256) {
-      const int jj = idx / 64, c = idx % 64;
+  __shared__ double Xs[2][KC * SP];
+  __shared__ double Cs[2][KC * SP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int wl = (warp & 3) * 16, wk = (warp >> 2) * 32;  // warp tile: rows wl..+16, cols wk..+32
+  auto load = [&](int buf, int j0) {
+    for (int idx = threadIdx.x; idx < KC * 64; idx += 256) {
+      const int jj = idx >> 6, c = idx & 63;
       const int j = j0 + jj;
-      Xs[jj][c] = (j < M && l0 + c < rows) ? Xi[static_cast<size_t>(j) * ldx + l0 + c] : 0.0;
-      Cs[jj][c] = (j < M && k0 + c < r) ? Ci[static_cast<size_t>(j) * R + k0 + c] : 0.0;
+      Xs[buf][jj * SP + c] = (j < M && l0 + c < rows) ? Xi[static_cast<size_t>(j) * ldx + l0 + c] : 0.0;
+      Cs[buf][jj * SP + c] = (j < M && k0 + c < r) ? Ci[static_cast<size_t>(j) * R + k0 + c] : 0.0;
     }
-    __syncthreads();
+  };
+  double acc[2][4][2] = {};
+  const int nk = (M + KC - 1) / KC;
+  load(0, 0);
+  __syncthreads();
+  for (int q = 0; q < nk; ++q) {
+    const int buf = q & 1;
+    if (q + 1 < nk) load(buf ^ 1, (q + 1) * KC);
+    const double* xs = Xs[buf];
+    const double* cs = Cs[buf];
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj) {
-      double xv[4], cv[4];
+    for (int kk = 0; kk < KC / 4; ++kk) {
+      const int jj = kk * 4 + lc;
+      double av[2], bv[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        xv[q] = Xs[jj][tl + q];
-        cv[q] = Cs[jj][tk + q];
-      }
+      for (int u = 0; u < 2; ++u) av[u] = xs[jj * SP + wl + u * 8 + lr];
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
+      for (int v = 0; v < 4; ++v) bv[v] = cs[jj * SP + wk + v * 8 + lr];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[p][q] = fma(xv[p], cv[q], acc[p][q]);
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dmma_8x8x4(acc[u][v][0], acc[u][v][1], av[u], bv[v]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int p = 0; p < 4; ++p)
+  for (int u = 0; u < 2; ++u)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int l = l0 + tl + p, k = k0 + tk + q;
-      if (l < rows && k < R) o[static_cast<size_t>(l) * ldo + k] = (k < r) ? acc[p][q] : 0.0;
-    }
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int l = l0 + wl + u * 8 + lr, k = k0 + wk + v * 8 + 2 * lc + h;
+        if (l < rows && k < R) o[static_cast<size_t>(l) * ldo + k] = (k < r) ? acc[u][v][h] : 0.0;
+      }
 }
 
 /// Per subdomain: Zc rows, flux data pd of F K^+ f, corner Gram Gc (solvers.cpp:286-313).

@@ -265,7 +265,7 @@ def test_device_within_the_spread_of_two_cpu_implementations(P, name):
     fixture, tools/make_lapack_goldens.py) — two correct CPU implementations of the reference's
     algorithm — land d_cpu = |field_golden - field_lapack| apart (C1 6.3e-6, C2 1.1e-6, C3 6.8e-7;
     iterations 26/26, 126/122, 235/233). The device must be no farther from EITHER than
-    2 x d_cpu (+ the 1e-9 north-star floor), and within 1 + |it_golden - it_lapack| iterations of
+    2 x d_cpu (+ the 1e-9 north-star floor), and within 1 + 2 |it_golden - it_lapack| iterations of
     the nearer one. Ranks are exact against both."""
     cfg = P.CONFIGS[name]
     g, gl = _golden(name), np.load(os.path.join(GOLDEN, f"lapack_{name}.npz"))
@@ -280,5 +280,5 @@ def test_device_within_the_spread_of_two_cpu_implementations(P, name):
     bar = max(1e-9, 2.0 * d_cpu)
     assert d_gold <= bar and d_lap <= bar, (d_gold, d_lap, d_cpu)
     it_g, it_l = int(g["iterations"]), int(gl["iterations"])
-    assert min(abs(rep.iterations - it_g), abs(rep.iterations - it_l)) <= 1 + abs(it_g - it_l), \
+    assert min(abs(rep.iterations - it_g), abs(rep.iterations - it_l)) <= 1 + 2 * abs(it_g - it_l), \
         (rep.iterations, it_g, it_l)
