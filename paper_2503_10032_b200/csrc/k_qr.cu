@@ -822,6 +822,205 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? (kTrStages == 2 ? 3 : 2) : 1)
   }
 }
 
+// ---- warp-specialised variant of the 32-wide trailing update (default): warp 8 is the TMA
+// producer — it refills a ring stage as soon as the 8 compute warps have released it (per-stage
+// "empty" mbarriers), so the compute warps never wait for one another at block barriers (only at
+// the W / W' hand-over and at the one chunk whose V block gets its unit-triangular fix), and never
+// execute the copy issue themselves.
+struct TrailWsSmem {
+  double V[3][kQrNB * RCP];
+  double A[3][TN * RCP];
+  double W[kQrNB * TNP];
+  double T[kQrNB * (kQrNB + 1)];
+  uint64_t full[3], empty[3];
+};
+constexpr int kWsCompute = 8;  // compute warps (256 threads); warp 8 produces
+
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__global__ void __launch_bounds__(288, 2)
+    qr_trailing_ws_kernel(QrArgs a, int k0, int nbw, int cb, int ce, int tq, const __grid_constant__ CUtensorMap tmA,
+                          const __grid_constant__ CUtensorMap tmV) {
+  constexpr int NB_ = kQrNB, ST = 3, WM = 2;
+  extern __shared__ __align__(16) double smraw[];
+  TrailWsSmem& S = *reinterpret_cast<TrailWsSmem*>(smraw);
+  const int t = blockIdx.y;
+  const int nb = nbw;
+  const int c0 = cb + blockIdx.x * TN;
+  if (c0 >= ce) return;
+  const int ncols = min(TN, ce - c0);
+  double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
+  const size_t ld = a.ld;
+  const int nq = (a.m - k0 + RC - 1) / RC;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < ST; ++s2) {
+      mbar_init(&S.full[s2], 1);
+      mbar_init(&S.empty[s2], kWsCompute);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kWsCompute) {
+    // producer: chunk q (pass 1 forward, pass 2 backward over the row chunks) into stage q % 3
+    if (lane == 0) {
+      const int colA = t * a.ncol + c0, colV = t * a.ncol + k0;
+      for (int q = 0; q < 2 * nq; ++q) {
+        const int st = q % ST;
+        if (q >= ST) mbar_wait(&S.empty[st], static_cast<uint32_t>(((q / ST) - 1) & 1));
+        const int cq = q < nq ? q : 2 * nq - 1 - q;
+        const int row = k0 + cq * RC;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&S.full[st], static_cast<uint32_t>((TN + NB_) * RCP * sizeof(double)));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                smem_u32(S.A[st])),
+            "l"(&tmA), "r"(row), "r"(colA), "r"(smem_u32(&S.full[st]))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                smem_u32(S.V[st])),
+            "l"(&tmV), "r"(row), "r"(colV), "r"(smem_u32(&S.full[st]))
+            : "memory");
+      }
+    }
+    return;
+  }
+  auto wait_full = [&](int q) { mbar_wait(&S.full[q % ST], static_cast<uint32_t>((q / ST) & 1)); };
+  auto release = [&](int q) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[q % ST]);
+  };
+  // the unit lower-triangular structure of V lives in the chunk holding rows k0 .. k0 + nb - 1
+  auto fix_v = [&](int st, int r0) {
+    for (int idx = threadIdx.x; idx < NB_ * RC; idx += kWsCompute * 32) {
+      const int u = idx / RC, k = idx % RC;
+      const int row = r0 + k;
+      if (row <= k0 + u) S.V[st][u * RCP + k] = (row == k0 + u && u < nb) ? 1.0 : 0.0;
+    }
+  };
+  const double* Tg = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
+  for (int idx = threadIdx.x; idx < NB_ * NB_; idx += kWsCompute * 32) {
+    const int i = idx / NB_, j = idx % NB_;
+    S.T[i * (NB_ + 1) + j] = (i < nb && j < nb) ? Tg[(tq + i) * kQrTmax + tq + j] : 0.0;
+  }
+  // ---- pass 1: W = V^T A_tile; warp -> m-tiles {2(w&1), +1}, n-tiles {2(w>>1), +1}
+  const int mt0 = (warp & 1) * WM, nt0 = (warp >> 1) * 2;
+  double acc[WM][2][2];
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    const int st = q % ST;
+    wait_full(q);
+    if (q == 0) {  // rows k0 .. k0 + 31 hold the reflectors' diagonal and the R entries above it
+      fix_v(st, k0);
+      compute_sync();
+    }
+    const double* Vs = S.V[st];
+    const double* As = S.A[st];
+#pragma unroll
+    for (int kk = 0; kk < RC / 4; ++kk) {
+      const int k = kk * 4 + lc;
+      double av[WM], bv[2];
+#pragma unroll
+      for (int i = 0; i < WM; ++i) av[i] = Vs[((mt0 + i) * 8 + lr) * RCP + k];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bv[j] = As[((nt0 + j) * 8 + lr) * RCP + k];
+#pragma unroll
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    }
+    release(q);
+  }
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int r = (mt0 + i) * 8 + lr, c = (nt0 + j) * 8 + 2 * lc;
+      S.W[r * TNP + c] = acc[i][j][0];
+      S.W[r * TNP + c + 1] = acc[i][j][1];
+    }
+  compute_sync();
+  // ---- W' = T^T W: warp -> its 8 columns, all m-tiles
+  {
+    constexpr int MTT = NB_ / 8;
+    double cw[MTT][2];
+#pragma unroll
+    for (int i = 0; i < MTT; ++i) cw[i][0] = cw[i][1] = 0.0;
+    const int n8 = warp * 8;
+#pragma unroll
+    for (int kk = 0; kk < NB_ / 4; ++kk) {
+      const int w = kk * 4 + lc;
+      const double bv = S.W[w * TNP + n8 + lr];
+#pragma unroll
+      for (int i = 0; i < MTT; ++i) {
+        const int u = i * 8 + lr;
+        const double av = (w <= u) ? S.T[w * (NB_ + 1) + u] : 0.0;
+        dmma_8x8x4(cw[i][0], cw[i][1], av, bv);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < MTT; ++i) {
+      const int r = i * 8 + lr, c = n8 + 2 * lc;
+      S.W[r * TNP + c] = cw[i][0];
+      S.W[r * TNP + c + 1] = cw[i][1];
+    }
+  }
+  compute_sync();
+  // ---- pass 2: A_tile -= V W' per 32-row chunk (rows walked backwards: the chunks pass 1 read
+  //      last are still in L2); warp tile 2 row-tiles x 2 col-tiles
+  const int rt0 = (warp & 1) * 2, ct0 = (warp >> 1) * 2;
+  for (int q = nq; q < 2 * nq; ++q) {
+    const int st = q % ST;
+    const int r0 = k0 + (2 * nq - 1 - q) * RC;
+    wait_full(q);
+    if (q == 2 * nq - 1) {
+      fix_v(st, r0);
+      compute_sync();
+    }
+    const double* Vs = S.V[st];
+    const double* As = S.A[st];
+    double cf[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = (rt0 + i) * 8 + lr, c = (ct0 + j) * 8 + 2 * lc;
+        cf[i][j][0] = As[c * RCP + r];
+        cf[i][j][1] = As[(c + 1) * RCP + r];
+      }
+#pragma unroll
+    for (int kk = 0; kk < NB_ / 4; ++kk) {
+      const int u = kk * 4 + lc;
+      double av[2], bv[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) av[i] = -Vs[u * RCP + (rt0 + i) * 8 + lr];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bv[j] = S.W[u * TNP + (ct0 + j) * 8 + lr];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(cf[i][j][0], cf[i][j][1], av[i], bv[j]);
+    }
+    release(q);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = r0 + (rt0 + i) * 8 + lr, c = (ct0 + j) * 8 + 2 * lc;
+        if (r < static_cast<int>(ld)) {
+          if (c < ncols) A[static_cast<size_t>(c0 + c) * ld + r] = cf[i][j][0];
+          if (c + 1 < ncols) A[static_cast<size_t>(c0 + c + 1) * ld + r] = cf[i][j][1];
+        }
+      }
+  }
+}
+
 __global__ void qr_diag_ratio_kernel(QrArgs a, double* ratio) {
   const int t = blockIdx.x;
   const double* A = a.A + static_cast<size_t>(t) * a.ld * a.ncol;
@@ -948,7 +1147,15 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
     DDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     kern<<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, toff, tmA, tmV);
   };
-  if (op.kind == QrOp::kTrail32) {
+  static const bool ws = [] {
+    const char* e = std::getenv("DDELM_QR_WS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (op.kind == QrOp::kTrail32 && ws) {
+    const size_t smem = sizeof(TrailWsSmem);
+    DDG_CUDA(cudaFuncSetAttribute(qr_trailing_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    qr_trailing_ws_kernel<<<grid, 288, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, op.toff, tmA, tmV);
+  } else if (op.kind == QrOp::kTrail32) {
     if (stages == 2) launch(qr_trailing_kernel<32, 2>, sizeof(TrailSmem<32, 2>), op.toff);
     else launch(qr_trailing_kernel<32, 3>, sizeof(TrailSmem<32, 3>), op.toff);
   } else {
