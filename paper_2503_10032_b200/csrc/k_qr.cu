@@ -827,23 +827,27 @@ __global__ void __launch_bounds__(256, NB_ == 32 ? (kTrStages == 2 ? 3 : 2) : 1)
 // "empty" mbarriers), so the compute warps never wait for one another at block barriers (only at
 // the W / W' hand-over and at the one chunk whose V block gets its unit-triangular fix), and never
 // execute the copy issue themselves.
+template <int ST>
 struct TrailWsSmem {
-  double V[3][kQrNB * RCP];
-  double A[3][TN * RCP];
+  static constexpr bool kTsmem = ST >= 3;  // 2 stages: T from L2 so that 3 CTAs fit an SM
+  double V[ST][kQrNB * RCP];
+  double A[ST][TN * RCP];
   double W[kQrNB * TNP];
-  double T[kQrNB * (kQrNB + 1)];
-  uint64_t full[3], empty[3];
+  double T[kTsmem ? kQrNB * (kQrNB + 1) : 2];
+  uint64_t full[ST], empty[ST];
 };
 constexpr int kWsCompute = 8;  // compute warps (256 threads); warp 8 produces
 
 __device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-__global__ void __launch_bounds__(288, 2)
+template <int ST>
+__global__ void __launch_bounds__(288, ST >= 3 ? 2 : 3)
     qr_trailing_ws_kernel(QrArgs a, int k0, int nbw, int cb, int ce, int tq, const __grid_constant__ CUtensorMap tmA,
                           const __grid_constant__ CUtensorMap tmV) {
-  constexpr int NB_ = kQrNB, ST = 3, WM = 2;
+  constexpr int NB_ = kQrNB, WM = 2;
+  constexpr bool kTsmem = TrailWsSmem<ST>::kTsmem;
   extern __shared__ __align__(16) double smraw[];
-  TrailWsSmem& S = *reinterpret_cast<TrailWsSmem*>(smraw);
+  TrailWsSmem<ST>& S = *reinterpret_cast<TrailWsSmem<ST>*>(smraw);
   const int t = blockIdx.y;
   const int nb = nbw;
   const int c0 = cb + blockIdx.x * TN;
@@ -901,10 +905,11 @@ __global__ void __launch_bounds__(288, 2)
     }
   };
   const double* Tg = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
-  for (int idx = threadIdx.x; idx < NB_ * NB_; idx += kWsCompute * 32) {
-    const int i = idx / NB_, j = idx % NB_;
-    S.T[i * (NB_ + 1) + j] = (i < nb && j < nb) ? Tg[(tq + i) * kQrTmax + tq + j] : 0.0;
-  }
+  if (kTsmem)
+    for (int idx = threadIdx.x; idx < NB_ * NB_; idx += kWsCompute * 32) {
+      const int i = idx / NB_, j = idx % NB_;
+      S.T[i * (NB_ + 1) + j] = (i < nb && j < nb) ? Tg[(tq + i) * kQrTmax + tq + j] : 0.0;
+    }
   // ---- pass 1: W = V^T A_tile; warp -> m-tiles {2(w&1), +1}, n-tiles {2(w>>1), +1}
   const int mt0 = (warp & 1) * WM, nt0 = (warp >> 1) * 2;
   double acc[WM][2][2];
@@ -959,7 +964,9 @@ __global__ void __launch_bounds__(288, 2)
 #pragma unroll
       for (int i = 0; i < MTT; ++i) {
         const int u = i * 8 + lr;
-        const double av = (w <= u) ? S.T[w * (NB_ + 1) + u] : 0.0;
+        const double av = (w <= u) ? (kTsmem ? S.T[w * (NB_ + 1) + u]
+                                             : (u < nb ? __ldg(Tg + (tq + w) * kQrTmax + tq + u) : 0.0))
+                                   : 0.0;
         dmma_8x8x4(cw[i][0], cw[i][1], av, bv);
       }
     }
@@ -1152,9 +1159,12 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
     return !(e && std::atoi(e) == 0);
   }();
   if (op.kind == QrOp::kTrail32 && ws) {
-    const size_t smem = sizeof(TrailWsSmem);
-    DDG_CUDA(cudaFuncSetAttribute(qr_trailing_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    qr_trailing_ws_kernel<<<grid, 288, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, op.toff, tmA, tmV);
+    auto launch_ws = [&](auto kern, size_t smem) {
+      DDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      kern<<<grid, 288, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, op.toff, tmA, tmV);
+    };
+    if (stages == 2) launch_ws(qr_trailing_ws_kernel<2>, sizeof(TrailWsSmem<2>));
+    else launch_ws(qr_trailing_ws_kernel<3>, sizeof(TrailWsSmem<3>));
   } else if (op.kind == QrOp::kTrail32) {
     if (stages == 2) launch(qr_trailing_kernel<32, 2>, sizeof(TrailSmem<32, 2>), op.toff);
     else launch(qr_trailing_kernel<32, 3>, sizeof(TrailSmem<32, 3>), op.toff);
