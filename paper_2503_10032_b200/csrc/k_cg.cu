@@ -1013,19 +1013,81 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
   double pv = 0.0;
   if (threadIdx.x < d.n_gamma) {
     pdg = a.gamma_delta[static_cast<size_t>(i) * a.gmax + threadIdx.x];
-    if (pdg >= 0) {
-      pdst = a.gamma_dst[static_cast<size_t>(i) * a.gmax + threadIdx.x];
-      if (mode == 0) pv = v[pdg];
-    }
+    pdst = a.gamma_dst[static_cast<size_t>(i) * a.gmax + threadIdx.x];
   }
   if (threadIdx.x < a.crmax) pcr = a.cr_row[static_cast<size_t>(i) * a.crmax + threadIdx.x];
-  gather_z(a, sh, mode, kThreads);
   const size_t st3 = 4 * static_cast<size_t>(n);
-  for (int gp = threadIdx.x; gp < n; gp += kThreads) {
-    double acc = 0;
-    for (int q = 0; q < 4; ++q) acc += sum_parts(a.t3tab, st3, a.P, gp * 4 + q);
-    sh.t2[gp] = acc;
+  const size_t ust = static_cast<size_t>(a.N) * R;
+  double uu0 = 0, sk0 = 0;
+  constexpr int kMaxP = 4;  // row parts of the batched path (C3: 2, C4: 1); more: the loop form below
+  if (n <= kThreads && a.npf <= kThreads && a.P <= kMaxP) {
+    // every value fresh from the previous phases is loaded before any shared-memory store (a store
+    // in between would order the loads: one L2 round trip per gather instead of one in total);
+    // the sums keep gather_z's / sum_parts' order, so the results are bitwise unchanged
+    const int tid = threadIdx.x;
+    double tz[4] = {0, 0, 0, 0}, pz[4] = {0, 0, 0, 0}, t3[4][kMaxP], up[kMaxP], dp = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int pp = 0; pp < kMaxP; ++pp) t3[q][pp] = 0.0;
+#pragma unroll
+    for (int pp = 0; pp < kMaxP; ++pp) up[pp] = 0.0;
+    if (tid < n) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        tz[q] = a.ttab[4 * static_cast<size_t>(tid) + q];
+#pragma unroll
+        for (int pp = 0; pp < kMaxP; ++pp)
+          if (pp < a.P) t3[q][pp] = a.t3tab[pp * st3 + static_cast<size_t>(tid) * 4 + q];
+      }
+    }
+    if (tid < a.npf) {
+      if (mode != 1)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pz[q] = a.ptab[4 * static_cast<size_t>(tid) + q];
+      if (mode != 0) dp = a.dpi[tid];
+    }
+    if (mode == 0 && pdg >= 0) pv = v[pdg];
+    if (tid < r) {
+#pragma unroll
+      for (int pp = 0; pp < kMaxP; ++pp)
+        if (pp < a.P) up[pp] = a.u[pp * ust + static_cast<size_t>(i) * R + tid];
+      sk0 = a.s[static_cast<size_t>(i) * R + tid];
+    }
+    if (tid < n) {
+      sh.z[tid] = ((tz[0] + tz[1]) + tz[2]) + tz[3];
+      double acc = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double sp = 0;
+#pragma unroll
+        for (int pp = 0; pp < kMaxP; ++pp)
+          if (pp < a.P) sp += t3[q][pp];
+        acc += sp;
+      }
+      sh.t2[tid] = acc;
+    }
+    if (tid < a.npf) {
+      const double acc = ((pz[0] + pz[1]) + pz[2]) + pz[3];
+      sh.z[n + tid] = (mode == 0) ? acc : (mode == 1 ? dp : dp - acc);
+    }
+#pragma unroll
+    for (int pp = 0; pp < kMaxP; ++pp)
+      if (pp < a.P) uu0 += up[pp];
+  } else {
+    if (mode == 0 && pdg >= 0) pv = v[pdg];
+    gather_z(a, sh, mode, kThreads);
+    for (int gp = threadIdx.x; gp < n; gp += kThreads) {
+      double acc = 0;
+      for (int q = 0; q < 4; ++q) acc += sum_parts(a.t3tab, st3, a.P, gp * 4 + q);
+      sh.t2[gp] = acc;
+    }
+    if (threadIdx.x < r) {
+      uu0 = sum_parts(a.u + static_cast<size_t>(i) * R, ust, a.P, threadIdx.x);
+      sk0 = a.s[static_cast<size_t>(i) * R + threadIdx.x];
+    }
   }
+  if (pdg < 0) pdst = -1;
   // the four coarse row-dot families run concurrently (one warp per row)
   if (threadIdx.x < ncq) {
     const int g = a.corner_q[i * ncq + threadIdx.x];
@@ -1037,13 +1099,6 @@ __device__ double dev_op4(const CgArgs& a, const Shared& sh, QtxStage& qst, int 
     const int row = a.cr_row[static_cast<size_t>(i) * a.crmax + rho];
     tasks[2 * ncq + rho] = RowTask{a.Wd, sh.z, &d2s[rho], nz, row, nz};                   // d1 = psi - Dpp mu
     tasks[2 * ncq + a.crmax + rho] = RowTask{a.W3, sh.t2, &w3t[rho], n, row, n};          // Dpp nu
-  }
-  // this thread's u parts and s (independent of the coarse rows: issued early)
-  const size_t ust = static_cast<size_t>(a.N) * R;
-  double uu0 = 0, sk0 = 0;
-  if (threadIdx.x < r) {
-    uu0 = sum_parts(a.u + static_cast<size_t>(i) * R, ust, a.P, threadIdx.x);
-    sk0 = a.s[static_cast<size_t>(i) * R + threadIdx.x];
   }
   __syncthreads();
   mark(tm, 0);
@@ -1395,13 +1450,21 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
       }
       return;
     }
-    case kPhOp4:
+    case kPhOp4: {
+      // DDELM_CG_TRACE: OP4's sub-phase timers (thread 0's clock) into trace slots 4..9
+      __shared__ unsigned long long t4[16];
+      if (a.trace != nullptr && threadIdx.x == 0)
+        for (int k = 0; k < 16; ++k) t4[k] = 0;
       for (int i = b; i < a.N; i += G) {
-        const double dot = dev_op4(a, sh, qst, i, cg ? pnext : vin, mode);
+        if (a.trace != nullptr && threadIdx.x == 0) t4[15] = gtimer();
+        const double dot = dev_op4(a, sh, qst, i, cg ? pnext : vin, mode, a.trace != nullptr ? t4 : nullptr);
         if (cg && threadIdx.x == 0) a.pap_w[a.sub_lo + i] = dot;
       }
+      if (a.trace != nullptr && threadIdx.x == 0 && b < a.N)
+        for (int k = 0; k < 6; ++k) a.trace[b * 32 + 4 + k] += static_cast<double>(t4[k]);
       trace_small(a, 2);
       return;
+    }
     case kPhXr1:    // alpha, x / r update, r.r partials (solvers.cpp:96-107); the last CTA to finish
     case kPhXr2: {  // also takes the stopping decision (solvers.cpp:108-116) — one launch per iteration
       __shared__ int s_last;

@@ -1013,6 +1013,20 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
     std::fprintf(stderr, "[cg trace] %d iterations, G=%d, P=%d (us/iteration: max / mean over CTAs)\n",
                  res.iterations, G, a.P);
     if (phased_) {
+      {
+        static const char* sub[6] = {"op4 gather+t3", "op4 qtx staged", "op4 coarse rows", "op4 s_tot", "op4 Q_G s",
+                                     "op4 out+dot"};
+        for (int k = 0; k < 6; ++k) {
+          double mx = 0, mean = 0;
+          const int nb = std::min(G, plan.N);
+          for (int b = 0; b < nb; ++b) {
+            mx = std::max(mx, t[b * 32 + 4 + k]);
+            mean += t[b * 32 + 4 + k] / nb;
+          }
+          const double it = std::max(res.iterations, 1);
+          std::fprintf(stderr, "[cg trace] %-20s %8.2f %8.2f\n", sub[k], mx / it / 1e3, mean / it / 1e3);
+        }
+      }
       static const char* sm[4] = {"op1 launch->wait", "op1 work", "op4 launch->wait", "op4 work"};
       for (int k = 0; k < 4; ++k) {
         double mx = 0, mean = 0;
@@ -1037,7 +1051,7 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
           std::fprintf(stderr, "[cg trace] %s %-16s %8.2f %8.2f\n", ph[q], part[k], mx / it / 1e3, mean / it / 1e3);
         }
     }
-    for (int k = 0; k < 22; ++k) {
+    for (int k = 0; k < 22 && !phased_; ++k) {
       if (k == 15) continue;
       double mx = 0, mean = 0;
       for (int b = 0; b < G; ++b) {
