@@ -245,7 +245,7 @@ __device__ __forceinline__ StreamPre stream_pre(const CgArgs& a, int kind) {
 /// [0] kernel entry, [1] after griddepcontrol.wait, [2] first chunk consumed, [3] last chunk done,
 /// [4] prologue done (consumers enter the stream).
 __device__ __forceinline__ unsigned long long* phase_stamps() {
-  __shared__ unsigned long long t[5];
+  __shared__ unsigned long long t[6];  // [5]: the item's gather done (first item)
   return t;
 }
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -846,6 +846,7 @@ __device__ void dev_nn1(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
     for (int kk = threadIdx.x; kk < nd; kk += kCThreads)
       sh.v1[kk] = -gather_x(a, (first && kk == threadIdx.x) ? pre.idx : nmap[kk]);
     cons_sync();
+    if (a.trace && threadIdx.x == 0 && phase_stamps()[5] == 0) phase_stamps()[5] = gtimer();
     rowdot_wide(QtX + 1, E, rb, nd, sh.v1, sh.xa, kCWarps);  // Qbar_r^T rhs (rhs nonzero on flux rows only)
     cons_sync();
     const ItemGeo g = item_geo(a, kNn1, i, p, false);
@@ -905,10 +906,38 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
       const int gg = (first && l == threadIdx.x) ? pre.idx : fd[l];
       double wv = 0.0;
       if (gg >= 0) {
-        // every load of both gathers in flight before the sums
-        double zz = 0.0;
-        if (a.use_neumann) zz = gather_delta(a.zztab, a, gg);
-        const double x = gather_x(a, gg);
+        // every load of both gathers issued before any sum: a line the previous phase wrote costs
+        // ~2 us on first touch (cross-die L2), so one round trip, not one per gather; the sums keep
+        // gather_delta's order (bitwise unchanged)
+        double zz = 0.0, x = 0.0;
+        constexpr int kQ = 4;
+        if (a.P <= kQ) {
+          const size_t st2 = 2 * static_cast<size_t>(a.n_delta);
+          double zv[2][kQ], xv[2][kQ];
+#pragma unroll
+          for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+            for (int pp = 0; pp < kQ; ++pp) {
+              const size_t o = pp * st2 + 2 * static_cast<size_t>(gg) + sl;
+              zv[sl][pp] = (pp < a.P && a.use_neumann) ? a.zztab[o] : 0.0;
+              xv[sl][pp] = pp < a.P ? a.xtab[o] : 0.0;
+            }
+          const double fs = a.flip_sign[gg];
+          double z0 = 0, z1 = 0, x0 = 0, x1 = 0;
+#pragma unroll
+          for (int pp = 0; pp < kQ; ++pp)
+            if (pp < a.P) {
+              z0 += zv[0][pp];
+              z1 += zv[1][pp];
+              x0 += xv[0][pp];
+              x1 += xv[1][pp];
+            }
+          zz = z0 + z1;
+          x = fs * (x0 + x1);
+        } else {
+          if (a.use_neumann) zz = gather_delta(a.zztab, a, gg);
+          x = gather_x(a, gg);
+        }
         if (a.use_neumann) {
           const double ptp = -zz;
           wv = theta * ptp;
@@ -918,6 +947,10 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
         }
       }
       sh.xa[l] = wv;  // apply_AT_delta: a(lrow) = w(grow) on the Delta flux rows
+    }
+    if (a.trace) {
+      cons_sync();
+      if (threadIdx.x == 0 && phase_stamps()[5] == 0) phase_stamps()[5] = gtimer();
     }
     if (a.one_level) {
       // apply_AT over the cross rows too (solvers.cpp:230-244): a(lrow) += w dmu(cross row)
@@ -1357,7 +1390,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
   const Shared sh = carve(a, bars);
   if (threadIdx.x == 0) {
     phase_stamps()[0] = a.trace ? gtimer() : 0;
-    phase_stamps()[2] = phase_stamps()[3] = phase_stamps()[4] = 0;
+    phase_stamps()[2] = phase_stamps()[3] = phase_stamps()[4] = phase_stamps()[5] = 0;
     for (int s2 = 0; s2 < kStages; ++s2) {
       mbar_init(&sh.full[s2], 1);
       mbar_init(&sh.empty[s2], kCWarps);
@@ -1383,7 +1416,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
     const int kind = phase == kPhOp2 ? kOp2 : phase == kPhNn1 ? kNn1 : phase == kPhNn2 ? kNn2 : kOp3;
     if (producer && lane == 0) {
       producer_begin(a, pr, kind, mode == 2);
-      producer_run(a, pr, sh, kStages);
+      producer_run(a, pr, sh, a.preissue);
     }
     if (!producer) pre = stream_pre(a, kind);
   } else if ((phase == kPhOp1 || phase == kPhOp4) && b < a.N) {
@@ -1444,6 +1477,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
         const unsigned long long end = gtimer();
         double* tr = a.trace + b * 32 + 16 + 4 * (phase - kPhOp2);
         tr[0] += static_cast<double>(t[4] - t[1]);  // prologue (after the wait)
+        if (t[5] != 0) a.trace[b * 32 + 10 + (phase - kPhOp2)] += static_cast<double>(t[5] - t[1]);  // gather part
         tr[1] += static_cast<double>(t[2] - t[4]);  // first chunk's data wait
         tr[2] += static_cast<double>(t[3] - t[2]);
         tr[3] += static_cast<double>(end - t[3]);

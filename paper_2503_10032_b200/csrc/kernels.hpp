@@ -285,6 +285,7 @@ struct CgArgs {
   int xr_parts;             // r.r partials written by the XR phase (= its grid size)
   unsigned long long cond;  // cudaGraphConditionalHandle of the CG while-loop graph (0: none)
   int guard_all;            // chunked driver: every phase (streamed ones too) leaves once state[1] is set
+  int preissue;             // stream chunks a streamed phase issues before griddepcontrol.wait (<= kStages)
   double* u;      // P x N x rmax
   double *pap, *pap_w;  // N_global : p . o_i (indexed by global subdomain)
   // CG vectors

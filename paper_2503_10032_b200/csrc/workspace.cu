@@ -881,6 +881,8 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.xr_parts = cg_grid(a);
   a.cond = 0;
   a.guard_all = 0;
+  a.preissue = 4;  // DDELM_CG_PREISSUE: stream chunks issued before griddepcontrol.wait (measured: no effect)
+  if (const char* e = std::getenv("DDELM_CG_PREISSUE")) a.preissue = std::max(0, std::min(4, std::atoi(e)));
   a.trace = nullptr;
   if (std::getenv("DDELM_CG_TRACE")) {
     d_trace.alloc(148 * 4 * 32);
@@ -1025,6 +1027,18 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
           }
           const double it = std::max(res.iterations, 1);
           std::fprintf(stderr, "[cg trace] %-20s %8.2f %8.2f\n", sub[k], mx / it / 1e3, mean / it / 1e3);
+        }
+      }
+      {
+        static const char* gn[4] = {"op2 gather", "nn1 gather", "nn2 gather", "op3 gather"};
+        for (int k = 1; k < 4; k += 2) {
+          double mx = 0, mean = 0;
+          for (int b = 0; b < G; ++b) {
+            mx = std::max(mx, t[b * 32 + 10 + k]);
+            mean += t[b * 32 + 10 + k] / G;
+          }
+          const double it = std::max(res.iterations, 1);
+          std::fprintf(stderr, "[cg trace] %-20s %8.2f %8.2f\n", gn[k], mx / it / 1e3, mean / it / 1e3);
         }
       }
       static const char* sm[4] = {"op1 launch->wait", "op1 work", "op4 launch->wait", "op4 work"};
