@@ -311,6 +311,17 @@ __device__ void producer_run(const CgArgs& a, Producer& pr, const Shared& sh, in
     const uint32_t bytes = static_cast<uint32_t>(nr) * g.ld * 8;
     mbar_expect_tx(&sh.full[st], bytes);
     bulk_g2s(dst, g.base + static_cast<size_t>(ja) * g.ld, bytes, &sh.full[st]);
+    if (pr.kind == kNn2 && pr.chunk + 1 == g.nch && !a.compact) {
+      // the item's epilogue reads Qbar_r^T (rb rows of the Kbar QtX block): into L2 while the last
+      // chunks stream (the NN1-time prefetch has been evicted by the phase's own stream)
+      const int w = item_work(pr.item, pr.nitems, true);
+      const int i = w / a.P;
+      const double* q0 = a.QtX + static_cast<size_t>(a.N + i) * a.rmax * a.ext;
+      const unsigned long long lo = reinterpret_cast<unsigned long long>(q0) & ~15ull;
+      const unsigned long long hi =
+          (reinterpret_cast<unsigned long long>(q0 + static_cast<size_t>(a.rmax) * a.ext) + 15ull) & ~15ull;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(static_cast<unsigned>(hi - lo)) : "memory");
+    }
     ++pr.chunk;
     ++pr.cnt;
     if (limit > 0) --limit;
