@@ -147,3 +147,22 @@ def test_lsq_rejects_bad_shapes(P):
         P.LsqBatch(4, 100, 201, 10)  # odd n
     with pytest.raises(ValueError):
         P.LsqBatch(4, 100, 200, 10)  # m < n
+
+
+def test_lsq_c5_full_batch_as_benchmarked(P):
+    """The exact batch bench.py times (BASELINE C5: 1024 blocks of [K 3000 x 1000 | B 3000 x 200]
+    of tanh features, seed 1): blocks spread over the whole batch (first, middle, last and a few
+    in between — including the last wave of CTAs) pass the same checks as the small batches, and
+    the batch is bitwise identical to a 16-block batch on the shared blocks (no cross-block state)."""
+    L = P.LsqBatch(1024, 3000, 1000, 200)
+    L.generate(1, "tanh")
+    L.factor()
+    for b in (0, 777, 1023):
+        _check_block(L, b, 1, "tanh", tight_r=False)
+    a = [L.block(b) for b in (0, 15)]
+    del L
+    S = P.LsqBatch(16, 3000, 1000, 200)
+    S.generate(1, "tanh")
+    S.factor()
+    for x, b in zip(a, (0, 15)):
+        assert all(np.array_equal(u, v) for u, v in zip(x, S.block(b)))
