@@ -1514,6 +1514,15 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
     case kPhXr2: {  // also takes the stopping decision (solvers.cpp:108-116) — one launch per iteration
       __shared__ int s_last;
       if (phase == kPhXr1) {
+        // this thread's first element, loaded together with p.Ap and the CG scalars (every value
+        // here is fresh from OP4 / the previous XR: one L2 round trip instead of two)
+        const int g0 = b * blockDim.x + threadIdx.x;
+        double ap0 = 0, pc0 = 0, r0 = 0;
+        if (g0 < a.n_cg) {
+          ap0 = gather_out(a, g0);
+          pc0 = pcur[g0];
+          r0 = a.r[g0];
+        }
         const double pAp = det_sum(a.pap, a.N_global);
         if (pAp <= 0.0) {
           if (b == 0 && threadIdx.x == 0) {
@@ -1527,14 +1536,16 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
         const double alpha = a.scal[0] / pAp;
         const double beta = a.scal[2];  // read before arriving: the last CTA overwrites it below
         double dsum = 0;
-        for (int g = b * blockDim.x + threadIdx.x; g < a.n_cg; g += G * blockDim.x) {
-          const double ap = gather_out(a, g);
+        for (int g = g0; g < a.n_cg; g += G * blockDim.x) {
+          const bool first = g == g0;
+          const double ap = first ? ap0 : gather_out(a, g);
+          const double rgo = first ? r0 : a.r[g];
           // p = r + beta p_cur on EVERY index (replicated CG vectors: a sharded rank's OP1 writes
           // only the indices its subdomains touch); bitwise the value OP1 stored
-          const double pn = __fma_rn(beta, pcur[g], a.r[g]);
+          const double pn = __fma_rn(beta, first ? pc0 : pcur[g], rgo);
           pnext[g] = pn;
           a.x[g] += alpha * pn;
-          const double rg = a.r[g] - alpha * ap;
+          const double rg = rgo - alpha * ap;
           a.r[g] = rg;
           dsum += rg * rg;
         }
