@@ -103,6 +103,18 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
   __shared__ ArgMax ared[32];
   __shared__ double s_tau, s_maxpivot;
   __shared__ int s_stop;
+  // DDELM_COD_TRACE: per-section device time of the pivot steps (thread 0's clock, barrier-bounded)
+  __shared__ unsigned long long s_tr[9], s_nfl;
+  auto stamp = [&](int sec) {
+    if (a.trace != nullptr && threadIdx.x == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (sec >= 0) s_tr[sec] += now - s_tr[8];
+      s_tr[8] = now;
+    }
+  };
+  if (a.trace != nullptr && threadIdx.x == 0)
+    for (int q = 0; q < 9; ++q) s_tr[q] = s_nfl = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const double eps = DBL_EPSILON;
   const double downdate_thr = sqrt(eps);
@@ -162,6 +174,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
   __syncthreads();
 
   int k = 0;
+  stamp(-1);
   for (; k < M; ++k) {
     // ---- pivot: largest updated norm, first index on ties
     ArgMax best{-1.0, 0x7fffffff};
@@ -189,6 +202,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       }
     }
     __syncthreads();
+    stamp(0);
     // ---- updated pivot column (rows k..M-1): R0(:, perm[k]) - V F(k, :)^T
     const int ck = perm[k];
     for (int u = threadIdx.x; u < k; u += blockDim.x) w[u] = F1[static_cast<size_t>(u) * M + k];
@@ -203,6 +217,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       v[i] = s;
     }
     __syncthreads();
+    stamp(1);
     // ---- Householder (makeHouseholderInPlace)
     double part = 0;
     for (int i = k + 1 + threadIdx.x; i < Reff; i += blockDim.x) part += v[i] * v[i];
@@ -231,6 +246,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       s_maxpivot = fmax(s_maxpivot, fabs(beta));
     }
     __syncthreads();
+    stamp(2);
     // ---- w = V(:, 0:k)^T v ; vk = V(k, 0:k]
     for (int u = warp; u < k; u += nwarp) {
       double s = 0;
@@ -262,7 +278,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
           const int i = i0 + 32 * u;
           vv[u] = i <= imax ? v[i] : 0.0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) x[u][q] = i <= iend[q] ? col[q][i] : 0.0;
+          for (int q = 0; q < 4; ++q) x[u][q] = i <= iend[q] ? __ldcs(col[q] + i) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u)
@@ -276,6 +292,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       }
     }
     __syncthreads();
+    stamp(3);
     // ---- per column position j > k (thread per j, coalesced over F1[u*M + j]):
     //      F(j, k) = tau (g_j - F(j, 0:k) w), row k of R: R(k, j) = R0(k, cj) - F(j, 0:k] . V(k, 0:k],
     //      and the LAPACK norm downdate (flag for exact recomputation below sqrt(eps))
@@ -318,7 +335,9 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
         }
       }
     }
-    if (!__syncthreads_or(any_flag)) continue;
+    const int flagged = __syncthreads_or(any_flag);
+    stamp(4);
+    if (!flagged) continue;
     // ---- exact recomputation of flagged norms: ||(A - V F^T)(k+1:M, j)||
     // compact the flagged columns (increasing j)
     if (threadIdx.x == 0) s_nflag = 0;
@@ -342,6 +361,8 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       __syncthreads();
     }
     const int nflag = s_nflag;
+    stamp(6);
+    if (a.trace != nullptr && threadIdx.x == 0) s_nfl += nflag + 1000000ull;
     // E = R0(k+1:Reff, flagged) - V(k+1:Reff, 0:k] F(flagged, 0:k]^T on DMMA, 8 x 8 tiles
     // (rows x flagged columns): the warps split the column groups and, when there are fewer
     // than 16 groups, the row tiles too; per-warp partial squares are combined in a fixed order
@@ -357,25 +378,43 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       const int c0 = f0 + 2 * lc;
       const int cjo0 = c0 < nflag ? perm[flist[c0]] : -1, cjo1 = c0 + 1 < nflag ? perm[flist[c0 + 1]] : -1;
       double sq0 = 0.0, sq1 = 0.0;
-      for (int rt = q; rt < nrt; rt += rg) {
-        const int i0 = k + 1 + 8 * rt;
-        double o0 = 0, o1 = 0;
-        const int ia = i0 + lr;
-        for (int u0 = 0; u0 <= k; u0 += 8) {  // two DMMAs per iteration, loads first
-          const int ua = u0 + lc, ub = u0 + 4 + lc;
-          const double a0 = (ua <= k && ia < Reff) ? V1[static_cast<size_t>(ua) * M + ia] : 0.0;
-          const double b0 = (ua <= k && jb >= 0) ? F1[static_cast<size_t>(ua) * M + jb] : 0.0;
-          const double a1 = (ub <= k && ia < Reff) ? V1[static_cast<size_t>(ub) * M + ia] : 0.0;
-          const double b1 = (ub <= k && jb >= 0) ? F1[static_cast<size_t>(ub) * M + jb] : 0.0;
-          dmma_8x8x4(o0, o1, a0, b0);
-          dmma_8x8x4(o0, o1, a1, b1);
+      // kRB row tiles per batch and kKS k-steps (4 reflectors each) per iteration, every load
+      // first: the F fragments are shared by the batch's tiles, so a recomputation costs
+      // ~k / (4 kKS) L2 round trips per batch instead of one per tile and k-step; per tile the
+      // DMMA k order and the row-tile order of the squares are unchanged
+      constexpr int kRB = 4, kKS = 4;
+      for (int rb = q; rb < nrt; rb += rg * kRB) {
+        double o[kRB][2];
+#pragma unroll
+        for (int x = 0; x < kRB; ++x) o[x][0] = o[x][1] = 0.0;
+        for (int u0 = 0; u0 <= k; u0 += 4 * kKS) {
+          double bf[kKS], av[kKS][kRB];
+#pragma unroll
+          for (int ks = 0; ks < kKS; ++ks) {
+            const int ua = u0 + 4 * ks + lc;
+            bf[ks] = (ua <= k && jb >= 0) ? F1[static_cast<size_t>(ua) * M + jb] : 0.0;
+#pragma unroll
+            for (int x = 0; x < kRB; ++x) {
+              const int rt = rb + x * rg;
+              const int ia = k + 1 + 8 * rt + lr;
+              av[ks][x] = (rt < nrt && ia < Reff && ua <= k) ? V1[static_cast<size_t>(ua) * M + ia] : 0.0;
+            }
+          }
+#pragma unroll
+          for (int ks = 0; ks < kKS; ++ks)
+#pragma unroll
+            for (int x = 0; x < kRB; ++x) dmma_8x8x4(o[x][0], o[x][1], av[ks][x], bf[ks]);
         }
-        const int i = i0 + lr;
-        if (i < Reff) {
-          const double e0 = (cjo0 >= 0 && i <= cjo0 ? R0[static_cast<size_t>(cjo0) * ld + i] : 0.0) - o0;
-          const double e1 = (cjo1 >= 0 && i <= cjo1 ? R0[static_cast<size_t>(cjo1) * ld + i] : 0.0) - o1;
-          sq0 += e0 * e0;
-          sq1 += e1 * e1;
+#pragma unroll
+        for (int x = 0; x < kRB; ++x) {
+          const int rt = rb + x * rg;
+          const int i = k + 1 + 8 * rt + lr;
+          if (rt < nrt && i < Reff) {
+            const double e0 = (cjo0 >= 0 && i <= cjo0 ? R0[static_cast<size_t>(cjo0) * ld + i] : 0.0) - o[x][0];
+            const double e1 = (cjo1 >= 0 && i <= cjo1 ? R0[static_cast<size_t>(cjo1) * ld + i] : 0.0) - o[x][1];
+            sq0 += e0 * e0;
+            sq1 += e1 * e1;
+          }
         }
       }
       sq0 += __shfl_xor_sync(0xffffffffu, sq0, 4);
@@ -390,14 +429,22 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
       }
     }
     __syncthreads();
+    stamp(7);
     for (int c = threadIdx.x; c < nflag; c += blockDim.x) {
       double t2 = 0;
       for (int q = 0; q < rg; ++q) t2 += gs[q * nflag + c];
       upd[flist[c]] = dir[flist[c]] = sqrt(t2);
     }
     __syncthreads();
+    stamp(5);
   }
   __syncthreads();
+  stamp(6);
+  if (a.trace != nullptr && threadIdx.x == 0) {
+    for (int q = 0; q < 8; ++q) a.trace[t * 16 + q] = static_cast<double>(s_tr[q]);
+    a.trace[t * 16 + 8] = static_cast<double>(s_nfl);  // events * 1e6 + flagged columns
+    a.trace[t * 16 + 9] = k;
+  }
   for (int j = threadIdx.x; j < M; j += blockDim.x) permg[j] = perm[j];
   if (threadIdx.x == 0) {
     const double pre = s_maxpivot * a.rank_tol;

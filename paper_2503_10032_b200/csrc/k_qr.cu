@@ -101,9 +101,13 @@ __device__ __forceinline__ void panel_pass(double* P, size_t ld, int m, int rlo,
 }
 
 /// Block reflector of a factored panel (both panel kernels): G = V^T V from the stored panel,
-/// T by the dlarft recurrence, written to quadrant (toff, toff) of the per-matrix T; combine = 1
-/// also forms the coupling block T12 of a 64-wide block. `dyn`: kFinishDoubles of shared memory.
-constexpr int kFinishDoubles = 2 * NB * 36 + 4 * NB * (NB + 1);
+/// T from G and tau by a blocked dlarft (the four 8-column diagonal blocks by the column
+/// recurrence, then T_AB = -T_A (G_AB T_B) on 8- and 16-column block pairs), written to quadrant
+/// (toff, toff) of the per-matrix T; combine = 1 also forms the coupling block T12 of a 64-wide
+/// block. `dyn`: kFinishDoubles of shared memory = G / T scratch + a kGStages-deep ring of 64-row
+/// chunks of the panel (the Gram pass is L2-latency bound: ~5 chunks in flight).
+constexpr int kGRows = 64, kGRCP = 68, kGStages = 6;  // kGRCP = 4 (mod 16): conflict-free fragments
+constexpr int kFinishDoubles = 4 * NB * (NB + 1) + kGStages * NB * kGRCP;
 
 __device__ __forceinline__ void panel_finish(const QrArgs& a, int t, int k0, int nb, int toff, int combine,
                                              const double* stau, double* dyn) {
@@ -112,70 +116,96 @@ __device__ __forceinline__ void panel_finish(const QrArgs& a, int t, int k0, int
   const size_t ld = a.ld;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* P = A + static_cast<size_t>(k0) * ld;
-  double(*G)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dyn + 2 * NB * 36);
+  double(*G)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dyn);
   double(*Tsh)[NB + 1] = G + NB;
   double(*Vs)[NB + 1] = G + 2 * NB;
   double(*T2s)[NB + 1] = G + 3 * NB;
   // G = V^T V over the panel (implicit unit diagonal, zeros above) on DMMA: 16 warps = the 4 x 4
-  // grid of 8 x 8 tiles of G; 32-row chunks double-buffered with cp.async (column-major, padded)
+  // grid of 8 x 8 tiles of G; 64-row chunks (column-major, padded) through a cp.async ring
   const int u = threadIdx.x & 31, v = threadIdx.x >> 5;
   const int tu = warp >> 2, tv = warp & 3, lr = lane >> 2, lc = lane & 3;
   double g0 = 0, g1 = 0;
   {
-    double* pdyn = dyn;  // [2][NB][RCP]
-    constexpr int kRCP = 36;
-    const int gcolu = threadIdx.x >> 4, gseg = threadIdx.x & 15;  // one 16-B segment per thread
-    const bool cok = gcolu < nb;
-    const double* gsrc = P + static_cast<size_t>(cok ? gcolu : 0) * ld;
-    const int nq = (m - k0 + RC - 1) / RC;
+    double* ring = dyn + 4 * NB * (NB + 1);  // [kGStages][NB][kGRCP]
+    const int nq = (m - k0 + kGRows - 1) / kGRows;
     auto issue = [&](int q) {
       if (q < nq) {
-        const int row = k0 + q * RC + 2 * gseg;
-        const bool ok = cok && row < static_cast<int>(ld);
-        const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(pdyn + (q & 1) * NB * kRCP + gcolu * kRCP + 2 * gseg));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gsrc + (ok ? row : 0)), "r"(ok ? 16 : 0) : "memory");
+        for (int s = threadIdx.x; s < NB * kGRows / 2; s += blockDim.x) {  // 16-B segments
+          const int col = s >> 5, seg = s & 31;
+          const int row = k0 + q * kGRows + 2 * seg;
+          const bool ok = col < nb && row < static_cast<int>(ld);
+          const uint32_t sa = static_cast<uint32_t>(
+              __cvta_generic_to_shared(ring + (q % kGStages) * NB * kGRCP + col * kGRCP + 2 * seg));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa),
+                       "l"(P + static_cast<size_t>(ok ? col : 0) * ld + (ok ? row : 0)), "r"(ok ? 16 : 0)
+                       : "memory");
+        }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    issue(0);
+    for (int q = 0; q < kGStages - 1; ++q) issue(q);
     for (int q = 0; q < nq; ++q) {
-      issue(q + 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      issue(q + kGStages - 1);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kGStages - 1) : "memory");
       __syncthreads();
-      double* Vc = pdyn + (q & 1) * NB * kRCP;
-      const int r0 = k0 + q * RC;
+      double* Vc = ring + (q % kGStages) * NB * kGRCP;
+      const int r0 = k0 + q * kGRows;
       if (r0 < k0 + nb) {  // unit diagonal, zeros above it
-        for (int idx = threadIdx.x; idx < NB * RC; idx += blockDim.x) {
-          const int uu = idx >> 5, rr = idx & 31;
+        for (int idx = threadIdx.x; idx < NB * kGRows; idx += blockDim.x) {
+          const int uu = idx / kGRows, rr = idx % kGRows;
           const int row = r0 + rr;
-          if (row <= k0 + uu) Vc[uu * kRCP + rr] = (row == k0 + uu && uu < nb) ? 1.0 : 0.0;
+          if (row <= k0 + uu) Vc[uu * kGRCP + rr] = (row == k0 + uu && uu < nb) ? 1.0 : 0.0;
         }
         __syncthreads();
       }
 #pragma unroll
-      for (int kk = 0; kk < RC / 4; ++kk)
-        dmma_8x8x4(g0, g1, Vc[(tu * 8 + lr) * kRCP + kk * 4 + lc], Vc[(tv * 8 + lr) * kRCP + kk * 4 + lc]);
+      for (int kk = 0; kk < kGRows / 4; ++kk)
+        dmma_8x8x4(g0, g1, Vc[(tu * 8 + lr) * kGRCP + kk * 4 + lc], Vc[(tv * 8 + lr) * kGRCP + kk * 4 + lc]);
       __syncthreads();
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   G[tu * 8 + lr][tv * 8 + 2 * lc] = g0;
   G[tu * 8 + lr][tv * 8 + 2 * lc + 1] = g1;
+  for (int idx = threadIdx.x; idx < NB * (NB + 1); idx += blockDim.x) (&Tsh[0][0])[idx] = 0.0;
   __syncthreads();
-  // T: T(j,j) = tau_j, T(0:j, j) = -tau_j T(0:j,0:j) G(0:j, j)
-  if (warp == 0) {
-    for (int j = 0; j < NB; ++j) Tsh[lane][j] = 0.0;
-    __syncwarp();
-    for (int j = 0; j < nb; ++j) {
+  // T diagonal blocks: warp s < 4 runs T(j,j) = tau_j, T(c:j, j) = -tau_j T(c:j,c:j) G(c:j, j) on
+  // columns c = 8s .. 8s+7 (tau = 0 past the panel width)
+  if (warp < NB / 8) {
+    const int c0 = warp * 8;
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = c0 + jj;
+      const double tj = j < nb ? stau[j] : 0.0;
       double s = 0;
-      if (lane < j)
-        for (int w = lane; w < j; ++w) s += Tsh[lane][w] * G[w][j];
+      if (lane < jj)
+        for (int w = lane; w < jj; ++w) s += Tsh[c0 + lane][c0 + w] * G[c0 + w][j];
       __syncwarp();
-      if (lane < j) Tsh[lane][j] = -stau[j] * s;
-      if (lane == j) Tsh[j][j] = stau[j];
+      if (lane < jj) Tsh[c0 + lane][j] = -tj * s;
+      if (lane == jj) Tsh[j][j] = tj;
       __syncwarp();
     }
   }
   __syncthreads();
+  // couplings of block pairs (A, B = A + bs): X = G_AB T_B (into Vs), T_AB = -T_A X
+  for (int bs = 8; bs < NB; bs *= 2) {
+    const int n = (NB / (2 * bs)) * bs * bs;
+    for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+      const int p = idx / (bs * bs), e = idx % (bs * bs), r = e / bs, c = e % bs;
+      const int a0 = 2 * p * bs, b0 = a0 + bs;
+      double s = 0;
+      for (int w = 0; w <= c; ++w) s += G[a0 + r][b0 + w] * Tsh[b0 + w][b0 + c];
+      Vs[a0 + r][b0 + c] = s;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+      const int p = idx / (bs * bs), e = idx % (bs * bs), r = e / bs, c = e % bs;
+      const int a0 = 2 * p * bs, b0 = a0 + bs;
+      double s = 0;
+      for (int w = r; w < bs; ++w) s += Tsh[a0 + r][a0 + w] * Vs[a0 + w][b0 + c];
+      Tsh[a0 + r][b0 + c] = -s;
+    }
+    __syncthreads();
+  }
   double* T = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
   for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x)
     T[(toff + (idx >> 5)) * kQrTmax + toff + (idx & 31)] = Tsh[idx >> 5][idx & 31];

@@ -104,6 +104,7 @@ struct CodArgs {
   double* C;     // nmat x M x rmax   : K^+ = C Q_r^T (C row i = original column i)
   double* QtX;   // nmat x rmax x ext : Q_r^T [f E] (top r rows)
   double* Ywork; // nmat x M x rmax scratch
+  double* trace = nullptr;  // DDELM_COD_TRACE: nmat x 8 section times (ns) + steps
 };
 void launch_cod_pivqr(const CodArgs& a, cudaStream_t st);
 void launch_cod_finish(const CodArgs& a, cudaStream_t st);  // RZ, C, Q^T X (both branches)

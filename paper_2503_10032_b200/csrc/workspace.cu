@@ -532,10 +532,37 @@ void Workspace::build() {
   launches_ += 1;
   DDG_CUDA(cudaEventRecord(ev_[2], st_));
   CodArgs c = cod_args();
+  static const bool cod_trace = std::getenv("DDELM_COD_TRACE") != nullptr;
+  double* d_ctr = nullptr;
+  if (cod_trace) {
+    DDG_CUDA(cudaMallocAsync(&d_ctr, 2 * p.N * 16 * sizeof(double), st_));
+    c.trace = d_ctr;
+  }
   kt = ktimer_begin();
   launch_cod_pivqr(c, st_);
   ktimer_end(kt, "cod_pivqr", 0.0, 0.0);
   launches_ += 1;
+  if (cod_trace) {
+    // DDELM_COD_TRACE: mean device time per section of the pivot steps (profiling runs only)
+    std::vector<double> ctr(2 * p.N * 16);
+    DDG_CUDA(cudaMemcpyAsync(ctr.data(), d_ctr, ctr.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    DDG_CUDA(cudaStreamSynchronize(st_));
+    DDG_CUDA(cudaFreeAsync(d_ctr, st_));
+    static const char* sec[8] = {"pivot+swap", "pivot column", "householder", "V^T v + GEMV",
+                                 "F update",   "rc final",     "rc compact",  "rc dmma"};
+    const double nm = 2.0 * p.N;
+    double mean[8] = {0}, steps = 0, ev = 0, nf = 0;
+    for (int t = 0; t < 2 * p.N; ++t) {
+      for (int q = 0; q < 8; ++q) mean[q] += ctr[t * 16 + q] / nm;
+      ev += std::floor(ctr[t * 16 + 8] / 1e6) / nm;
+      nf += std::fmod(ctr[t * 16 + 8], 1e6) / nm;
+      steps += ctr[t * 16 + 9] / nm;
+    }
+    std::fprintf(stderr, "[cod trace] %d matrices, mean steps %.1f, recompute events %.1f, flagged columns %.1f\n",
+                 2 * p.N, steps, ev, nf);
+    for (int q = 0; q < 8; ++q)
+      std::fprintf(stderr, "[cod trace] %-14s mean %8.1f us  (%.2f us/step)\n", sec[q], mean[q] / 1e3, mean[q] / 1e3 / steps);
+  }
   // ranks decide the packed strides of everything downstream
   std::vector<int> rank(2 * p.N), status(2 * p.N);
   DDG_CUDA(cudaMemcpyAsync(rank.data(), d_rank.ptr, rank.size() * sizeof(int), cudaMemcpyDeviceToHost, st_));
