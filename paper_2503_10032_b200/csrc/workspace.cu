@@ -1356,8 +1356,16 @@ long long Workspace::run_cg_phased(const CgArgs& a_in) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CgArgs a = a_in;
   a.cond = static_cast<unsigned long long>(h);
+  // KB iterations per body replay (DDELM_CG_BODY): programmatic dependent launch chains the phases
+  // within a body but not across the conditional node, so a one-iteration body pays the
+  // conditional + body launch every iteration (~5 us at C3); iterations after the stop leave at
+  // once (guard_all) and set the condition to 0 again
+  int KB = 8;
+  if (const char* e = std::getenv("DDELM_CG_BODY")) KB = std::max(1, std::atoi(e));
+  a.guard_all = KB > 1 ? 1 : 0;
   DDG_CUDA(cudaStreamBeginCaptureToGraph(st_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  const long long per_it = iteration(a, false, none);
+  long long per_body = 0;
+  for (int k = 0; k < KB; ++k) per_body += iteration(a, false, none);
   cudaGraph_t captured = nullptr;
   DDG_CUDA(cudaStreamEndCapture(st_, &captured));
   DDG_CUDA(cudaGraphInstantiate(&ge_exec, g, 0));
@@ -1365,11 +1373,13 @@ long long Workspace::run_cg_phased(const CgArgs& a_in) {
   DDG_CUDA(cudaStreamSynchronize(st_));
   DDG_CUDA(cudaGraphExecDestroy(ge_exec));
   DDG_CUDA(cudaGraphDestroy(g));
-  // body replays: one per iteration, plus the one that found pAp <= 0 (iterations = it - 1)
+  // body replays: through the iteration that stopped (the one that found pAp <= 0 when aborted:
+  // iterations = it - 1)
   int st8[8];
   DDG_CUDA(cudaMemcpy(st8, d_state.ptr, sizeof(st8), cudaMemcpyDeviceToHost));
   const bool aborted = !st8[2] && st8[5] < a.max_iter;
-  return per_it * (st8[5] + (aborted ? 1 : 0));
+  const int last = st8[5] + (aborted ? 1 : 0);
+  return per_body * std::max(1, (last + KB - 1) / KB);
 }
 
 void Workspace::get_mu(double* mu) {
