@@ -521,9 +521,10 @@ __device__ void larft_from_gram(const double* G, int ldg, const double* tau, int
 }
 
 /// Y, C and Q_r^T X of a deficient matrix with numerical rank r <= kFinR (after the RZ pass).
+__device__ void fin_stamp(const CodArgs& a, int t, int sec, unsigned long long& last);
 __device__ void finish_wy(const CodArgs& a, int t, int r, const double* X, const double* Rr, const double* V1,
                           const double* tau1, const int* perm, const double* zc, double* Y, double* C,
-                          double* QtX) {
+                          double* QtX, unsigned long long& tlast) {
   extern __shared__ __align__(16) double fsm[];
   const int M = a.M, R = a.rmax, E = a.ext;
   const long ld = a.ld;
@@ -551,6 +552,7 @@ __device__ void finish_wy(const CodArgs& a, int t, int r, const double* X, const
     }
   }
   __syncthreads();
+  fin_stamp(a, t, 1, tlast);
   // ---- C(perm[i], :) = Y(i, :) T11^{-1}, T11 = upper triangle of Rr(0:r, 0:r): the triangular
   //      inverse by columns (thread per column), then one GEMM
   double* T11 = fsm;            // r x ldt
@@ -578,6 +580,7 @@ __device__ void finish_wy(const CodArgs& a, int t, int r, const double* X, const
     C[static_cast<size_t>(perm[i]) * R + c] = 0.0;
   }
   __syncthreads();
+  fin_stamp(a, t, 2, tlast);
   // ---- Q_r^T X = top r rows of Q1^T X, Q1^T = I - V T^T V^T (V = V1, rows < reff)
   tile_gemm_tn(r, r, reff, V1, 1, M, V1, 1, M, [&](int m, int n, double v) { G[m * ldt + n] = v; });
   __syncthreads();
@@ -604,6 +607,7 @@ __device__ void finish_wy(const CodArgs& a, int t, int r, const double* X, const
   }
   for (int idx = threadIdx.x; idx < (R - r) * E; idx += blockDim.x)
     QtX[static_cast<size_t>(r) * E + idx] = 0.0;
+  fin_stamp(a, t, 3, tlast);
 }
 
 size_t finish_smem_bytes(int rmax) {
@@ -612,6 +616,16 @@ size_t finish_smem_bytes(int rmax) {
   const size_t ldt = r + 1, ldw = kFinEB + 1;
   return (static_cast<size_t>(r) * ldt + static_cast<size_t>(r) * std::max(ldt, ldw) + static_cast<size_t>(r) * ldw) *
          sizeof(double);
+}
+
+/// DDELM_COD_TRACE: thread 0's clock into trace[t * 16 + 10 + sec] (sections of the finish)
+__device__ __forceinline__ void fin_stamp(const CodArgs& a, int t, int sec, unsigned long long& last) {
+  if (a.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (sec >= 0) a.trace[t * 16 + 10 + sec] += static_cast<double>(now - last);
+    last = now;
+  }
 }
 
 /// RZ + C + Q^T X for a deficient matrix; C = R0^{-1}, Q^T X = X for a full-rank one.
@@ -657,6 +671,8 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
   __shared__ double red[32];
   __shared__ double s_tau, s_beta, s_scale;
 
+  unsigned long long tlast = 0;
+  fin_stamp(a, t, -1, tlast);
   // ---- RZ (COD::compute): rows k = r-1 .. 0 of [R11 R12], columns {k} U {r..M-1}
   if (r < M) {
     for (int k = r - 1; k >= 0; --k) {
@@ -713,7 +729,8 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
   }
   if (r <= kFinR) {
     __syncthreads();
-    finish_wy(a, t, r, X, Rr, V1, tau1, perm, zc, Y, C, QtX);
+    fin_stamp(a, t, 0, tlast);
+    finish_wy(a, t, r, X, Rr, V1, tau1, perm, zc, Y, C, QtX, tlast);
     return;
   }
   // ---- Y = Z^T [I_r; 0] (COD::solve's Z^* application): one warp per column, the column held

@@ -583,10 +583,31 @@ void Workspace::build() {
   d_FC.alloc(static_cast<size_t>(p.N) * p.fmax * rmax_);
   d_s.alloc(static_cast<size_t>(p.N) * rmax_);
   c = cod_args();
+  double* d_ftr = nullptr;
+  if (std::getenv("DDELM_COD_TRACE")) {
+    DDG_CUDA(cudaMallocAsync(&d_ftr, 2 * p.N * 16 * sizeof(double), st_));
+    DDG_CUDA(cudaMemsetAsync(d_ftr, 0, 2 * p.N * 16 * sizeof(double), st_));
+    c.trace = d_ftr;
+  }
   kt = ktimer_begin();
   launch_cod_finish(c, st_);
   ktimer_end(kt, "cod_finish", 0.0, 0.0);
   launches_ += 1;
+  if (d_ftr) {
+    std::vector<double> ftr(2 * p.N * 16);
+    DDG_CUDA(cudaMemcpyAsync(ftr.data(), d_ftr, ftr.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    DDG_CUDA(cudaStreamSynchronize(st_));
+    DDG_CUDA(cudaFreeAsync(d_ftr, st_));
+    static const char* sec[4] = {"RZ", "Y = Z^T [I; 0]", "C = Y T11^-1", "Q_r^T X"};
+    for (int q = 0; q < 4; ++q) {
+      double mean = 0, mx = 0;
+      for (int t = 0; t < 2 * p.N; ++t) {
+        mean += ftr[t * 16 + 10 + q] / (2.0 * p.N);
+        mx = std::max(mx, ftr[t * 16 + 10 + q]);
+      }
+      std::fprintf(stderr, "[cod finish trace] %-16s mean %8.1f us  max %8.1f us\n", sec[q], mean / 1e3, mx / 1e3);
+    }
+  }
   DDG_CUDA(cudaEventRecord(ev_[3], st_));
   built_ = true;
   blocks_built_ = coarse_built_ = neumann_built_ = false;

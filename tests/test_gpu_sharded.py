@@ -31,11 +31,13 @@ def P():
     return P
 
 
-def _solve_single(name, method, monkeypatch, parts=PARTS, driver=None):
+def _solve_single(name, method, monkeypatch, parts=PARTS, driver=None, body=None):
     import paper_2503_10032_b200 as P
     monkeypatch.setenv("DDELM_CG_PARTS", parts)
     if driver:
         monkeypatch.setenv("DDELM_CG_DRIVER", driver)
+    if body:
+        monkeypatch.setenv("DDELM_CG_BODY", body)
     ws = P.workspace_from_config(name)
     c = P.CONFIGS[name]
     theta = c["theta"] if method == "ddelm-nn" else 0.0
@@ -44,6 +46,8 @@ def _solve_single(name, method, monkeypatch, parts=PARTS, driver=None):
            "hist": np.array(rep.residual_history).copy(), "driver": ws.cg_driver, "converged": rep.converged}
     if driver:
         monkeypatch.delenv("DDELM_CG_DRIVER")
+    if body:
+        monkeypatch.delenv("DDELM_CG_BODY")
     del ws
     return out
 
@@ -140,3 +144,18 @@ def test_chunked_graph_driver_matches_while_graph(P, name, method, monkeypatch):
     np.testing.assert_array_equal(a["hist"], b["hist"])
     np.testing.assert_array_equal(a["mu"], b["mu"])
     np.testing.assert_array_equal(a["coeffs"], b["coeffs"])
+
+
+@pytest.mark.parametrize("name,method", [("T2", "ddelm-nn"), ("T2", "ddelm"), ("C2", "ddelm-cs")])
+def test_while_graph_body_length_is_bitwise_neutral(P, name, method, monkeypatch):
+    """The while-loop graph runs DDELM_CG_BODY iterations per body (default 8; the iterations after
+    the stop leave at once and reset the loop condition): 1, 3 and 8 iterations per body give the
+    same iterations, residual history, mu and coefficients bit for bit."""
+    ref = _solve_single(name, method, monkeypatch, body="1")
+    assert ref["driver"] == "graph-while"
+    for body in ("3", "8"):
+        b = _solve_single(name, method, monkeypatch, body=body)
+        assert b["iterations"] == ref["iterations"], body
+        np.testing.assert_array_equal(b["hist"], ref["hist"])
+        np.testing.assert_array_equal(b["mu"], ref["mu"])
+        np.testing.assert_array_equal(b["coeffs"], ref["coeffs"])
