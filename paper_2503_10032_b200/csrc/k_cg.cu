@@ -61,10 +61,6 @@ constexpr int kStages = 4;
 constexpr int kStageBytes = 32768;
 constexpr int kMaxW = 1024;  // widest row-dot operand / axpy output (32 accumulators per lane)
 constexpr int kRedW = 512;   // column chunk of the cross-warp accumulator reduction
-// work items of a streamed phase whose prologues run together (one round of fresh gathers for
-// all of them) before their streams run back to back: a CTA with several items no longer
-// stalls its stream on each item's prologue
-constexpr int kGroup = 4;
 
 /// Thread team of a phase: the whole CTA (512) or the consumer warps of a streamed phase (480,
 /// named barrier 1 so the producer warp is never waited for).
@@ -82,11 +78,11 @@ __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"
 // ---------------------------------------------------------------- shared state of one CTA
 struct Shared {
   double* ring;    // kStages x kStageBytes (also the Q_r^T staging area of OP1 / OP4)
-  double* xa;      // row-dot operands of a group of items (kGroup x wmax)
+  double* xa;      // row-dot operand (wmax)
   double* red;     // kCWarps x wred (warp partials of the axpy) / kThreads scratch
   double* z;       // [t; psi] (nz)
   double* t2;      // t' (n_pi)
-  double* v1;      // per-subdomain vectors (kGroup x wmax; OP1 / OP4 use the first)
+  double* v1;      // per-subdomain vector (wmax)
   double* s0;      // rmax
   uint64_t* full;  // kStages
   uint64_t* empty; // kStages
@@ -105,7 +101,7 @@ __device__ __forceinline__ Shared carve(const CgArgs& a, uint64_t* bars) {
   double* q = smem + kStages * (kStageBytes / 8);
   const int wm = wmax_of(a);
   s.xa = q;
-  q += kGroup * wm;
+  q += wm;
   s.red = q;
   q += max(kCWarps * wred_of(a), kThreads);
   s.z = q;
@@ -113,7 +109,7 @@ __device__ __forceinline__ Shared carve(const CgArgs& a, uint64_t* bars) {
   s.t2 = q;
   q += max(a.n_pi, 1);
   s.v1 = q;
-  q += kGroup * wm;
+  q += wm;
   s.s0 = q;
   s.full = bars;
   s.empty = bars + kStages;
@@ -336,8 +332,7 @@ __device__ void producer_run(const CgArgs& a, Producer& pr, const Shared& sh, in
 /// (xa in registers), u_j = hook(j, t_j, Ypi row) (lane-uniform), acc += u_j B_j (registers).
 /// `ccnt` counts the chunks consumed by this CTA (mirrors the producer's cnt).
 template <int W, class Hook>
-__device__ void consume_item(const ItemGeo& g, const Shared& sh, const double* xa, unsigned& ccnt, double (&acc)[W],
-                             Hook hook) {
+__device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt, double (&acc)[W], Hook hook) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // W <= 16: the row-dot operand lives in registers; W = 32 (rows up to 1024 wide): it is read
   // from shared memory, the registers hold the 32 axpy accumulators
@@ -347,7 +342,7 @@ __device__ void consume_item(const ItemGeo& g, const Shared& sh, const double* x
 #pragma unroll
   for (int q = 0; q < W; ++q) {
     const int k = lane + 32 * q;
-    if constexpr (!kXs) xr[q] = k < g.wa ? xa[k] : 0.0;
+    if constexpr (!kXs) xr[q] = k < g.wa ? sh.xa[k] : 0.0;
     acc[q] = 0.0;
   }
   for (int cc = 0; cc < g.nch; ++cc) {
@@ -365,7 +360,7 @@ __device__ void consume_item(const ItemGeo& g, const Shared& sh, const double* x
       for (int q = 0; q < W; ++q) {
         const int k = lane + 32 * q;
         if constexpr (kXs) {
-          if (k < g.wa) s += ar[k] * xa[k];
+          if (k < g.wa) s += ar[k] * sh.xa[k];
         } else {
           if (k < g.wa) s += ar[k] * xr[q];
         }
@@ -772,116 +767,78 @@ __device__ void dev_op1(const CgArgs& a, const Shared& sh, QtxStage& qs, int i, 
 }
 
 // ---------------------------------------------------------------- streamed phases (consumers)
-/// subdomain / part of item k of this CTA
-__device__ __forceinline__ void item_of(const CgArgs& a, int k, int nitems, bool reverse, int& i, int& p) {
-  const int w = item_work(k, nitems, reverse);
-  i = w / a.P;
-  p = w % a.P;
-}
-
 template <int W>
 __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int mode, const StreamPre& pre) {
   const int nitems = n_items(a.N * a.P);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = wmax_of(a), ncq = a.ncq, nz = a.n_pi + a.npf;
-  __shared__ double muc[kGroup][kMaxCq];
-  __shared__ int crow[kGroup][kMaxCq];
-  if (nitems == 0) return;
-  if (!a.one_level) gather_z(a, sh, mode, kCThreads);  // z = [t; psi]: the same for every item
-  const bool one = a.one_level != 0;
-  for (int k0 = 0; k0 < nitems; k0 += kGroup) {
-    const int ng = min(kGroup, nitems - k0);
-    // prologues of the group: corner rows and s_i (fresh from OP1) of every item, all loads first
-    int ii[kGroup], rq[kGroup];
-#pragma unroll
-    for (int q = 0; q < kGroup; ++q) {
-      int pq = 0;
-      ii[q] = 0;
-      rq[q] = 0;
-      if (q < ng) {
-        item_of(a, k0 + q, nitems, false, ii[q], pq);
-        rq[q] = (k0 + q == 0 && pre.i == ii[q]) ? pre_geo().r : a.geo[ii[q]].r;
+  __shared__ double muc[kMaxCq];
+  __shared__ int crow[kMaxCq];
+  for (int k = 0; k < nitems; ++k) {
+    const int w = item_work(k, nitems, false);
+    const int i = w / a.P, p = w % a.P;
+    if (!a.one_level) gather_z(a, sh, mode, kCThreads);
+    const bool first = (k == 0 && pre.i == i);
+    if (threadIdx.x < a.ncq) {
+      if (first) {
+        crow[threadIdx.x] = pre.crow;
+      } else {
+        const int g = a.corner_q[i * a.ncq + threadIdx.x];
+        crow[threadIdx.x] = (g >= 0 && !a.one_level) ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
       }
     }
-    if (threadIdx.x < ncq) {
-#pragma unroll
-      for (int q = 0; q < kGroup; ++q)
-        if (q < ng) {
-          int c;
-          if (k0 + q == 0 && pre.i == ii[q]) {
-            c = pre.crow;
-          } else {
-            const int g = a.corner_q[ii[q] * ncq + threadIdx.x];
-            c = (g >= 0 && !one) ? a.gamma_pi[static_cast<size_t>(ii[q]) * a.gmax + g] : -1;
-          }
-          crow[q][threadIdx.x] = c;
-        }
-    }
-    for (int kk = threadIdx.x; kk < a.rmax; kk += kCThreads) {
-      double sv[kGroup];
-#pragma unroll
-      for (int q = 0; q < kGroup; ++q) sv[q] = (q < ng && kk < rq[q]) ? a.s[static_cast<size_t>(ii[q]) * a.rmax + kk] : 0.0;
-#pragma unroll
-      for (int q = 0; q < kGroup; ++q)
-        if (q < ng && kk < rq[q]) sh.xa[q * wm + kk] = sv[q];
-    }
+    const int r = first ? pre_geo().r : a.geo[i].r;
+    for (int kk = threadIdx.x; kk < r; kk += kCThreads) sh.xa[kk] = a.s[static_cast<size_t>(i) * a.rmax + kk];
     cons_sync();
-    for (int q = 0; q < ng; ++q) {
-      int i, p;
-      item_of(a, k0 + q, nitems, false, i, p);
-      rows_dot(a.Wmu, nz, crow[q], ncq, sh.z, nz, muc[q], kCWarps);  // mu = S^{-1}(t + Dpp^T psi); 0 one-level
-      if (mode == 2 && i == 0 && p == 0 && !one)  // mu_Pi of the solution (one CTA writes it)
-        for (int gp = warp; gp < a.n_pi; gp += kCWarps) {
-          double s = 0;
-          const double* wr = a.Wmu + static_cast<size_t>(gp) * nz;
-          for (int kk = lane; kk < nz; kk += 32) s += wr[kk] * sh.z[kk];
-          s = warp_sum(s);
-          if (lane == 0) a.mu_pi_out[gp] = s;
-        }
-    }
-    cons_sync();
-    for (int q = 0; q < ng; ++q) {
-      int i, p;
-      item_of(a, k0 + q, nitems, false, i, p);
-      const ItemGeo g = item_geo(a, kOp2, i, p, mode == 2);
-      int j0, j1;
-      part_rows(a.M, a.P, p, j0, j1);
-      double* coef = a.coeffs + static_cast<size_t>(i) * a.M;
-      const double* mq = muc[q];
-      const double m0 = mq[0], m1 = mq[1], m2 = mq[2], m3 = mq[3];
-      double acc[W];
-      // reference grouping (solvers.cpp:336, 342): c = K^+ phi - Ypi mu, then F c
-      consume_item<W>(g, sh, sh.xa + q * wm, ccnt, acc, [&](int jr, double cs, const double* y, int ln) {
-        double ym = ((y[0] * m0 + y[1] * m1) + y[2] * m2) + y[3] * m3;
-        for (int q2 = 4; q2 < ncq; ++q2) ym += y[q2] * mq[q2];  // biharmonic: second-component corners
-        const double cj = one ? cs : cs - ym;
-        if (mode == 2 && ln == 0) coef[j0 + jr] = cj;
-        return cj;
-      });
-      if (mode == 2) continue;
-      double* xt = a.xtab_w + static_cast<size_t>(p) * 2 * a.n_delta;
-      const int* fdst = a.flux_dst + static_cast<size_t>(i) * a.fmax;
-      reduce_warps<W>(a, g, sh, acc, [&](int l, double s) {
-        const int dst = fdst[l];
-        if (dst >= 0) xt[dst] = -s;
-        if (one) sh.v1[l] = s;
-      });
-      if (one) {
-        // cross flux rows (apply_A, solvers.cpp:209-224): this subdomain's weighted share of every
-        // cross row it touches (mean_edge: 1/(n-1) over the edge's points), one warp per row
-        cons_sync();
-        const int* off = a.cr_off + static_cast<size_t>(i) * (a.crmax + 1);
-        double* xc = a.xctab_w + static_cast<size_t>(p) * 4 * a.npf;
-        for (int rho = warp; rho < a.crmax; rho += kCWarps) {
-          const int dst = a.cross_dst[static_cast<size_t>(i) * a.crmax + rho];
-          if (dst < 0) continue;
-          double v = 0;
-          for (int e = off[rho] + lane; e < off[rho + 1]; e += 32) v += a.cr_w[e] * sh.v1[a.cr_l[e]];
-          v = warp_sum(v);
-          if (lane == 0) xc[dst] = -v;
-        }
-        cons_sync();
+    const int nz = a.n_pi + a.npf;
+    rows_dot(a.Wmu, nz, crow, a.ncq, sh.z, nz, muc, kCWarps);  // mu = S^{-1}(t + Dpp^T psi); 0 one-level
+    if (mode == 2 && w == 0 && !a.one_level)  // mu_Pi of the solution (one CTA writes it)
+      for (int gp = warp; gp < a.n_pi; gp += kCWarps) {
+        double s = 0;
+        const double* wr = a.Wmu + static_cast<size_t>(gp) * nz;
+        for (int kk = lane; kk < nz; kk += 32) s += wr[kk] * sh.z[kk];
+        s = warp_sum(s);
+        if (lane == 0) a.mu_pi_out[gp] = s;
       }
+    cons_sync();
+    const ItemGeo g = item_geo(a, kOp2, i, p, mode == 2);
+    int j0, j1;
+    part_rows(a.M, a.P, p, j0, j1);
+    double* coef = a.coeffs + static_cast<size_t>(i) * a.M;
+    const double m0 = muc[0], m1 = muc[1], m2 = muc[2], m3 = muc[3];
+    const int ncq = a.ncq;
+    double acc[W];
+    // reference grouping (solvers.cpp:336, 342): c = K^+ phi - Ypi mu, then F c
+    const bool one = a.one_level != 0;
+    consume_item<W>(g, sh, ccnt, acc, [&](int jr, double cs, const double* y, int ln) {
+      double ym = ((y[0] * m0 + y[1] * m1) + y[2] * m2) + y[3] * m3;
+      for (int q = 4; q < ncq; ++q) ym += y[q] * muc[q];  // biharmonic: second-component corners
+      const double cj = one ? cs : cs - ym;
+      if (mode == 2 && ln == 0) coef[j0 + jr] = cj;
+      return cj;
+    });
+    if (mode == 2) continue;
+    double* xt = a.xtab_w + static_cast<size_t>(p) * 2 * a.n_delta;
+    const int* fdst = a.flux_dst + static_cast<size_t>(i) * a.fmax;
+    reduce_warps<W>(a, g, sh, acc, [&](int l, double s) {
+      const int dst = fdst[l];
+      if (dst >= 0) xt[dst] = -s;
+      if (one) sh.v1[l] = s;
+    });
+    if (one) {
+      // cross flux rows (apply_A, solvers.cpp:209-224): this subdomain's weighted share of every
+      // cross row it touches (mean_edge: 1/(n-1) over the edge's points), one warp per row
+      cons_sync();
+      const int* off = a.cr_off + static_cast<size_t>(i) * (a.crmax + 1);
+      double* xc = a.xctab_w + static_cast<size_t>(p) * 4 * a.npf;
+      for (int rho = warp; rho < a.crmax; rho += kCWarps) {
+        const int dst = a.cross_dst[static_cast<size_t>(i) * a.crmax + rho];
+        if (dst < 0) continue;
+        double v = 0;
+        for (int e = off[rho] + lane; e < off[rho + 1]; e += 32) v += a.cr_w[e] * sh.v1[a.cr_l[e]];
+        v = warp_sum(v);
+        if (lane == 0) xc[dst] = -v;
+      }
+      cons_sync();
     }
   }
 }
@@ -889,178 +846,118 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
 template <int W>
 __device__ void dev_nn1(const CgArgs& a, const Shared& sh, unsigned& ccnt, const StreamPre& pre) {
   const int nitems = n_items(a.N * a.P);
-  const int wm = wmax_of(a), E = a.ext;
-  for (int k0 = 0; k0 < nitems; k0 += kGroup) {
-    const int ng = min(kGroup, nitems - k0);
-    // rhs of every item of the group (the fresh OP2 slots), all loads before any store
-    int ii[kGroup], nds[kGroup];
-#pragma unroll
-    for (int q = 0; q < kGroup; ++q) {
-      int pq = 0;
-      ii[q] = 0;
-      nds[q] = 0;
-      if (q < ng) {
-        item_of(a, k0 + q, nitems, false, ii[q], pq);
-        nds[q] = (k0 + q == 0 && pre.i == ii[q]) ? pre_geo().nd : a.geo[ii[q]].nd;
-      }
-    }
-    for (int kk = threadIdx.x; kk < a.dmax; kk += kCThreads) {
-      double v[kGroup];
-#pragma unroll
-      for (int q = 0; q < kGroup; ++q) {
-        v[q] = 0.0;
-        if (q < ng && kk < nds[q]) {
-          const bool pl = k0 + q == 0 && pre.i == ii[q] && kk == threadIdx.x;
-          v[q] = -gather_x(a, pl ? pre.idx : a.ndelta_map[static_cast<size_t>(ii[q]) * a.dmax + kk]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < kGroup; ++q)
-        if (q < ng && kk < nds[q]) sh.v1[q * wm + kk] = v[q];
-    }
+  for (int k = 0; k < nitems; ++k) {
+    const int w = item_work(k, nitems, false);
+    const int i = w / a.P, p = w % a.P;
+    const bool first = (k == 0 && pre.i == i);
+    const SubGeo d = first ? pre_geo() : a.geo[i];
+    const int nd = d.nd, rb = d.rb, E = a.ext;
+    const double* QtX = a.QtX + static_cast<size_t>(a.N + i) * a.rmax * E;
+    const int* nmap = a.ndelta_map + static_cast<size_t>(i) * a.dmax;
+    for (int kk = threadIdx.x; kk < nd; kk += kCThreads)
+      sh.v1[kk] = -gather_x(a, (first && kk == threadIdx.x) ? pre.idx : nmap[kk]);
     cons_sync();
     if (a.trace && threadIdx.x == 0 && phase_stamps()[5] == 0) phase_stamps()[5] = gtimer();
-    for (int q = 0; q < ng; ++q) {  // Qbar_r^T rhs (rhs nonzero on flux rows only); no barrier between items
-      const SubGeo d = (k0 + q == 0 && pre.i == ii[q]) ? pre_geo() : a.geo[ii[q]];
-      const double* QtX = a.QtX + static_cast<size_t>(a.N + ii[q]) * a.rmax * E;
-      rowdot_wide(QtX + 1, E, d.rb, d.nd, sh.v1 + q * wm, sh.xa + q * wm, kCWarps);
-    }
+    rowdot_wide(QtX + 1, E, rb, nd, sh.v1, sh.xa, kCWarps);  // Qbar_r^T rhs (rhs nonzero on flux rows only)
     cons_sync();
-    for (int q = 0; q < ng; ++q) {
-      int i, p;
-      item_of(a, k0 + q, nitems, false, i, p);
-      const ItemGeo g = item_geo(a, kNn1, i, p, false);
-      double acc[W];
-      // reference order (solvers.cpp:455): y = Kbar^+ rhs (M-vector), then Cdelta y
-      consume_item<W>(g, sh, sh.xa + q * wm, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
-      double* trt = a.trtab_w + static_cast<size_t>(p) * 2 * a.n_delta;
-      const int* ndst = a.nd_dst + static_cast<size_t>(i) * a.dmax;
-      reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { trt[ndst[l]] = s; });
-    }
+    const ItemGeo g = item_geo(a, kNn1, i, p, false);
+    double acc[W];
+    // reference order (solvers.cpp:455): y = Kbar^+ rhs (M-vector), then Cdelta y
+    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
+    double* trt = a.trtab_w + static_cast<size_t>(p) * 2 * a.n_delta;
+    const int* ndst = a.nd_dst + static_cast<size_t>(i) * a.dmax;
+    reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { trt[ndst[l]] = s; });
   }
 }
 
 template <int W>
 __device__ void dev_nn2(const CgArgs& a, const Shared& sh, unsigned& ccnt, const StreamPre& pre) {
   const int nitems = n_items(a.N * a.P);
-  const int wm = wmax_of(a), E = a.ext;
-  for (int k0 = 0; k0 < nitems; k0 += kGroup) {
-    const int ng = min(kGroup, nitems - k0);
-    int ii[kGroup], nds[kGroup];
-#pragma unroll
-    for (int q = 0; q < kGroup; ++q) {
-      int pq = 0;
-      ii[q] = 0;
-      nds[q] = 0;
-      if (q < ng) {
-        item_of(a, k0 + q, nitems, true, ii[q], pq);
-        nds[q] = (k0 + q == 0 && pre.i == ii[q]) ? pre_geo().nd : a.geo[ii[q]].nd;
-      }
-    }
-    for (int kk = threadIdx.x; kk < a.dmax; kk += kCThreads) {
-      double v[kGroup];
-#pragma unroll
-      for (int q = 0; q < kGroup; ++q) {
-        v[q] = 0.0;
-        if (q < ng && kk < nds[q]) {
-          const bool pl = k0 + q == 0 && pre.i == ii[q] && kk == threadIdx.x;
-          v[q] = gather_delta(a.trtab, a, pl ? pre.idx : a.ndelta_map[static_cast<size_t>(ii[q]) * a.dmax + kk]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < kGroup; ++q)
-        if (q < ng && kk < nds[q]) sh.xa[q * wm + kk] = v[q];
+  for (int k = 0; k < nitems; ++k) {
+    const int w = item_work(k, nitems, true);
+    const int i = w / a.P, p = w % a.P;
+    const bool first = (k == 0 && pre.i == i);
+    const SubGeo d = first ? pre_geo() : a.geo[i];
+    const int nd = d.nd, rb = d.rb, E = a.ext;
+    const double* QtX = a.QtX + static_cast<size_t>(a.N + i) * a.rmax * E;
+    const int* nmap = a.ndelta_map + static_cast<size_t>(i) * a.dmax;
+    const size_t st = static_cast<size_t>(a.N) * a.dmax;
+    for (int kk = threadIdx.x; kk < nd; kk += kCThreads) {
+      const int gg = (first && kk == threadIdx.x) ? pre.idx : nmap[kk];
+      sh.xa[kk] = gather_delta(a.trtab, a, gg);
     }
     cons_sync();
-    for (int q = 0; q < ng; ++q) {
-      int i, p;
-      item_of(a, k0 + q, nitems, true, i, p);
-      const SubGeo d = (k0 + q == 0 && pre.i == i) ? pre_geo() : a.geo[i];
-      const double* QtX = a.QtX + static_cast<size_t>(a.N + i) * a.rmax * E;
-      const ItemGeo g = item_geo(a, kNn2, i, p, false);
-      double acc[W];
-      // reference order (solvers.cpp:468): x = Cdelta^T tl (M-vector), then (Kbar^+)^T x
-      consume_item<W>(g, sh, sh.xa + q * wm, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
-      reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { sh.s0[l] = s; });
-      // zz = Qbar_r (Cbar^T x) on the flux rows (partial over the parts p; linear)
-      double* zzt = a.zztab_w + static_cast<size_t>(p) * 2 * a.n_delta;
-      const int* ndst = a.nd_dst + static_cast<size_t>(i) * a.dmax;
-      coldot_split(QtX + 1, E, d.rb, d.nd, sh.s0, sh.red, Team{kCThreads}, [&](int kk, double v) { zzt[ndst[kk]] = v; });
-    }
+    const ItemGeo g = item_geo(a, kNn2, i, p, false);
+    double acc[W];
+    // reference order (solvers.cpp:468): x = Cdelta^T tl (M-vector), then (Kbar^+)^T x
+    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
+    reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { sh.s0[l] = s; });
+    // zz = Qbar_r (Cbar^T x) on the flux rows (partial over the parts p; linear)
+    double* zzt = a.zztab_w + static_cast<size_t>(p) * 2 * a.n_delta;
+    const int* ndst = a.nd_dst + static_cast<size_t>(i) * a.dmax;
+    coldot_split(QtX + 1, E, rb, nd, sh.s0, sh.red, Team{kCThreads}, [&](int kk, double v) { zzt[ndst[kk]] = v; });
   }
-}
-
-/// OP3's operand entry of flux row l: w = theta (-zz) + (1 - theta) x at its Delta index gg
-/// (apply_AT_delta: a(lrow) = w(grow)); every load of both gathers is issued before any sum (a
-/// line the previous phase wrote costs ~2 us on first touch), the sums keep gather_delta's order
-__device__ __forceinline__ double op3_entry(const CgArgs& a, int gg) {
-  if (gg < 0) return 0.0;
-  double zz = 0.0, x = 0.0;
-  constexpr int kQ = 4;
-  if (a.P <= kQ) {
-    const size_t st2 = 2 * static_cast<size_t>(a.n_delta);
-    double zv[2][kQ], xv[2][kQ];
-#pragma unroll
-    for (int sl = 0; sl < 2; ++sl)
-#pragma unroll
-      for (int pp = 0; pp < kQ; ++pp) {
-        const size_t o = pp * st2 + 2 * static_cast<size_t>(gg) + sl;
-        zv[sl][pp] = (pp < a.P && a.use_neumann) ? a.zztab[o] : 0.0;
-        xv[sl][pp] = pp < a.P ? a.xtab[o] : 0.0;
-      }
-    const double fs = a.flip_sign[gg];
-    double z0 = 0, z1 = 0, x0 = 0, x1 = 0;
-#pragma unroll
-    for (int pp = 0; pp < kQ; ++pp)
-      if (pp < a.P) {
-        z0 += zv[0][pp];
-        z1 += zv[1][pp];
-        x0 += xv[0][pp];
-        x1 += xv[1][pp];
-      }
-    zz = z0 + z1;
-    x = fs * (x0 + x1);
-  } else {
-    if (a.use_neumann) zz = gather_delta(a.zztab, a, gg);
-    x = gather_x(a, gg);
-  }
-  if (!a.use_neumann) return x;
-  double wv = a.theta * -zz;
-  if (a.theta < 1.0) wv += (1.0 - a.theta) * x;
-  return wv;
 }
 
 template <int W>
 __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt, const StreamPre& pre) {
   const int nitems = n_items(a.N * a.P);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = wmax_of(a), R = a.rmax, E = a.ext;
-  for (int k0 = 0; k0 < nitems; k0 += kGroup) {
-    const int ng = min(kGroup, nitems - k0);
-    int ii[kGroup], nfs[kGroup];
+  for (int k = 0; k < nitems; ++k) {
+    const int w = item_work(k, nitems, true);
+    const int i = w / a.P, p = w % a.P;
+    const bool first = (k == 0 && pre.i == i);
+    const SubGeo d = first ? pre_geo() : a.geo[i];
+    const int r = d.r, R = a.rmax, E = a.ext;
+    const double* QtX = a.QtX + static_cast<size_t>(i) * R * E;
+    const int* fd = a.fluxrow_delta + static_cast<size_t>(i) * a.fmax;
+    const double theta = a.theta;
+    const size_t st = static_cast<size_t>(a.N) * a.dmax;
+    for (int l = threadIdx.x; l < d.nF; l += kCThreads) {
+      const int gg = (first && l == threadIdx.x) ? pre.idx : fd[l];
+      double wv = 0.0;
+      if (gg >= 0) {
+        // every load of both gathers issued before any sum: a line the previous phase wrote costs
+        // ~2 us on first touch (cross-die L2), so one round trip, not one per gather; the sums keep
+        // gather_delta's order (bitwise unchanged)
+        double zz = 0.0, x = 0.0;
+        constexpr int kQ = 4;
+        if (a.P <= kQ) {
+          const size_t st2 = 2 * static_cast<size_t>(a.n_delta);
+          double zv[2][kQ], xv[2][kQ];
 #pragma unroll
-    for (int q = 0; q < kGroup; ++q) {
-      int pq = 0;
-      ii[q] = 0;
-      nfs[q] = 0;
-      if (q < ng) {
-        item_of(a, k0 + q, nitems, true, ii[q], pq);
-        nfs[q] = (k0 + q == 0 && pre.i == ii[q]) ? pre_geo().nF : a.geo[ii[q]].nF;
-      }
-    }
-    for (int l = threadIdx.x; l < a.fmax; l += kCThreads) {
-      double v[kGroup];
+          for (int sl = 0; sl < 2; ++sl)
 #pragma unroll
-      for (int q = 0; q < kGroup; ++q) {
-        v[q] = 0.0;
-        if (q < ng && l < nfs[q]) {
-          const bool pl = k0 + q == 0 && pre.i == ii[q] && l == threadIdx.x;
-          v[q] = op3_entry(a, pl ? pre.idx : a.fluxrow_delta[static_cast<size_t>(ii[q]) * a.fmax + l]);
+            for (int pp = 0; pp < kQ; ++pp) {
+              const size_t o = pp * st2 + 2 * static_cast<size_t>(gg) + sl;
+              zv[sl][pp] = (pp < a.P && a.use_neumann) ? a.zztab[o] : 0.0;
+              xv[sl][pp] = pp < a.P ? a.xtab[o] : 0.0;
+            }
+          const double fs = a.flip_sign[gg];
+          double z0 = 0, z1 = 0, x0 = 0, x1 = 0;
+#pragma unroll
+          for (int pp = 0; pp < kQ; ++pp)
+            if (pp < a.P) {
+              z0 += zv[0][pp];
+              z1 += zv[1][pp];
+              x0 += xv[0][pp];
+              x1 += xv[1][pp];
+            }
+          zz = z0 + z1;
+          x = fs * (x0 + x1);
+        } else {
+          if (a.use_neumann) zz = gather_delta(a.zztab, a, gg);
+          x = gather_x(a, gg);
+        }
+        if (a.use_neumann) {
+          const double ptp = -zz;
+          wv = theta * ptp;
+          if (theta < 1.0) wv += (1.0 - theta) * x;
+        } else {
+          wv = x;
         }
       }
-#pragma unroll
-      for (int q = 0; q < kGroup; ++q)
-        if (q < ng && l < nfs[q]) sh.xa[q * wm + l] = v[q];
+      sh.xa[l] = wv;  // apply_AT_delta: a(lrow) = w(grow) on the Delta flux rows
     }
     if (a.trace) {
       cons_sync();
@@ -1068,50 +965,40 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
     }
     if (a.one_level) {
       // apply_AT over the cross rows too (solvers.cpp:230-244): a(lrow) += w dmu(cross row)
-      for (int q = 0; q < ng; ++q) {
-        const int i = ii[q];
-        const int* off = a.cr_off + static_cast<size_t>(i) * (a.crmax + 1);
-        const int* crr = a.cr_row + static_cast<size_t>(i) * a.crmax;
-        cons_sync();
-        for (int rho = threadIdx.x; rho < a.crmax; rho += kCThreads) sh.z[rho] = crr[rho] >= 0 ? gather_xc(a, crr[rho]) : 0.0;
-        cons_sync();
-        for (int l = threadIdx.x; l < a.geo[i].nF; l += kCThreads) {
-          double add = 0;
-          for (int rho = 0; rho < a.crmax; ++rho) {
-            if (crr[rho] < 0) continue;
-            for (int e = off[rho]; e < off[rho + 1]; ++e)
-              if (a.cr_l[e] == l) add += a.cr_w[e] * sh.z[rho];
-          }
-          sh.xa[q * wm + l] += add;
+      const int* off = a.cr_off + static_cast<size_t>(i) * (a.crmax + 1);
+      const int* crr = a.cr_row + static_cast<size_t>(i) * a.crmax;
+      for (int rho = threadIdx.x; rho < a.crmax; rho += kCThreads) sh.z[rho] = crr[rho] >= 0 ? gather_xc(a, crr[rho]) : 0.0;
+      cons_sync();
+      for (int l = threadIdx.x; l < d.nF; l += kCThreads) {
+        double add = 0;
+        for (int rho = 0; rho < a.crmax; ++rho) {
+          if (crr[rho] < 0) continue;
+          for (int e = off[rho]; e < off[rho + 1]; ++e)
+            if (a.cr_l[e] == l) add += a.cr_w[e] * sh.z[rho];
         }
+        sh.xa[l] += add;
       }
     }
     cons_sync();
-    for (int q = 0; q < ng; ++q) {
-      int i, p;
-      item_of(a, k0 + q, nitems, true, i, p);
-      const int r = (k0 + q == 0 && pre.i == i) ? pre_geo().r : a.geo[i].r;
-      const double* QtX = a.QtX + static_cast<size_t>(i) * R * E;
-      const ItemGeo g = item_geo(a, kOp3, i, p, false);
-      double acc[W];
-      // reference order: at = F^T a (M-vector, apply_AT), then (K^+)^T at = Q_r (C^T at)
-      consume_item<W>(g, sh, sh.xa + q * wm, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
-      double* up = a.u + (static_cast<size_t>(p) * a.N + i) * R;
-      reduce_warps<W>(a, g, sh, acc, [&](int l, double s) {
-        up[l] = s;
-        sh.s0[l] = s;
-      });
-      if (warp < a.ncq && !a.one_level) {
-        const int gq = a.corner_q[i * a.ncq + warp];
-        double acc2 = 0;
-        if (gq >= 0)
-          for (int kk = lane; kk < r; kk += 32) acc2 += QtX[static_cast<size_t>(kk) * E + 1 + gq] * sh.s0[kk];
-        acc2 = warp_sum(acc2);
-        const int dst = a.corner_dst[i * a.ncq + warp];
-        if (lane == 0 && dst >= 0) a.t3tab_w[static_cast<size_t>(p) * 4 * a.n_pi + dst] = acc2;  // t(gp) += z(lr)
-      }
-      cons_sync();
+    const ItemGeo g = item_geo(a, kOp3, i, p, false);
+    double acc[W];
+    // reference order: at = F^T a (M-vector, apply_AT), then (K^+)^T at = Q_r (C^T at)
+    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
+    double* up = a.u + (static_cast<size_t>(p) * a.N + i) * R;
+    reduce_warps<W>(a, g, sh, acc, [&](int l, double s) {
+      up[l] = s;
+      sh.s0[l] = s;
+    });
+    if (warp < a.ncq && !a.one_level) {
+      const int gq = a.corner_q[i * a.ncq + warp];
+      double acc2 = 0;
+      if (gq >= 0)
+        for (int kk = lane; kk < r; kk += 32) acc2 += QtX[static_cast<size_t>(kk) * E + 1 + gq] * sh.s0[kk];
+      acc2 = warp_sum(acc2);
+      const int dst = a.corner_dst[i * a.ncq + warp];
+      if (lane == 0 && dst >= 0) a.t3tab_w[static_cast<size_t>(p) * 4 * a.n_pi + dst] = acc2;  // t(gp) += z(lr)
     }
+    cons_sync();
   }
 }
 
@@ -1735,8 +1622,8 @@ int wmax_host(const CgArgs& a) { return std::max(std::max(a.rmax, a.fmax), std::
 size_t smem_bytes(const CgArgs& a) {
   const int wm = wmax_host(a);
   const int wred = std::min(kRedW, (std::max(std::max(a.rmax, a.fmax), a.dmax) + 31) & ~31);
-  const size_t small = static_cast<size_t>(kGroup) * wm + std::max(kCWarps * wred, kThreads) + a.n_pi + a.npf +
-                       std::max(a.n_pi, 1) + static_cast<size_t>(kGroup) * wm + static_cast<size_t>(a.rmax);
+  const size_t small = static_cast<size_t>(wm) + std::max(kCWarps * wred, kThreads) + a.n_pi + a.npf +
+                       std::max(a.n_pi, 1) + wm + static_cast<size_t>(a.rmax);
   return static_cast<size_t>(kStages) * kStageBytes + sizeof(double) * small;
 }
 
