@@ -310,7 +310,16 @@ __device__ void producer_run(const CgArgs& a, Producer& pr, const Shared& sh, in
     double* dst = sh.ring + static_cast<size_t>(st) * (kStageBytes / 8);
     const uint32_t bytes = static_cast<uint32_t>(nr) * g.ld * 8;
     mbar_expect_tx(&sh.full[st], bytes);
-    bulk_g2s(dst, g.base + static_cast<size_t>(ja) * g.ld, bytes, &sh.full[st]);
+    if (a.l2keep < 0) {
+      bulk_g2s(dst, g.base + static_cast<size_t>(ja) * g.ld, bytes, &sh.full[st]);
+    } else {
+      // L2 reuse across phases: NN2 walks KD backwards right after NN1 walked it forwards, the next
+      // OP2 walks KF forwards right after OP3 walked it backwards — the last l2keep/1000 of an NN1 /
+      // OP3 item's walk stays in L2 (evict_last) for them; every other chunk streams evict_first
+      const bool keep = (pr.kind == kNn1 || pr.kind == kOp3) && 1000 * (pr.chunk + 1) > (1000 - a.l2keep) * g.nch;
+      const uint64_t pol = keep ? l2_policy_evict_last() : l2_policy_evict_first();
+      bulk_g2s_hint(dst, g.base + static_cast<size_t>(ja) * g.ld, bytes, &sh.full[st], pol);
+    }
     if (pr.kind == kNn2 && pr.chunk + 1 == g.nch && !a.compact) {
       // the item's epilogue reads Qbar_r^T (rb rows of the Kbar QtX block): into L2 while the last
       // chunks stream (the NN1-time prefetch has been evicted by the phase's own stream)
@@ -325,6 +334,35 @@ __device__ void producer_run(const CgArgs& a, Producer& pr, const Shared& sh, in
     ++pr.chunk;
     ++pr.cnt;
     if (limit > 0) --limit;
+  }
+}
+
+/// Prefetch into L2 the first |permille|/1000 (walk order) of this CTA's work items of a streamed
+/// phase — issued while the HBM is idle (a latency-bound phase) so the phase later streams them from
+/// L2. permille < 0: evict_last priority.
+__device__ void l2_prefetch_items(const CgArgs& a, int kind, int permille) {
+  const int nitems = n_items(a.N * a.P);
+  const bool last = permille < 0;
+  const int f = last ? -permille : permille;
+  const uint64_t pol = l2_policy_evict_last();
+  for (int k = 0; k < nitems; ++k) {
+    const int w = item_work(k, nitems, reverse_kind(kind));
+    const ItemGeo g = item_geo(a, kind, w / a.P, w % a.P, false);
+    const int nr = static_cast<int>((static_cast<long long>(g.rows) * f) / 1000);
+    if (nr <= 0) continue;
+    const int r0 = g.reverse ? g.rows - nr : 0;
+    unsigned long long lo = reinterpret_cast<unsigned long long>(g.base + static_cast<size_t>(r0) * g.ld) & ~15ull;
+    const unsigned long long hi =
+        (reinterpret_cast<unsigned long long>(g.base + static_cast<size_t>(r0 + nr) * g.ld) + 15ull) & ~15ull;
+    constexpr unsigned long long kPiece = 1ull << 18;
+    for (; lo < hi; lo += kPiece) {
+      const unsigned sz = static_cast<unsigned>(min(kPiece, hi - lo));
+      if (last)
+        asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(lo), "r"(sz), "l"(pol)
+                     : "memory");
+      else
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(sz) : "memory");
+    }
   }
 }
 
@@ -1496,6 +1534,8 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
       return;
     }
     case kPhOp4: {
+      // the next OP2's coefficient rows into L2 while OP4 / XR / OP1 leave the HBM idle
+      if (cg && a.l2pre != 0 && threadIdx.x == 0 && !a.compact) l2_prefetch_items(a, kOp2, a.l2pre);
       // DDELM_CG_TRACE: OP4's sub-phase timers (thread 0's clock) into trace slots 4..9
       __shared__ unsigned long long t4[16];
       if (a.trace != nullptr && threadIdx.x == 0)

@@ -873,7 +873,7 @@ __device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;"
 template <int ST>
 __global__ void __launch_bounds__(288, ST >= 3 ? 2 : 3)
     qr_trailing_ws_kernel(QrArgs a, int k0, int nbw, int cb, int ce, int tq, const __grid_constant__ CUtensorMap tmA,
-                          const __grid_constant__ CUtensorMap tmV) {
+                          const __grid_constant__ CUtensorMap tmV, int l2keep) {
   constexpr int NB_ = kQrNB, WM = 2;
   constexpr bool kTsmem = TrailWsSmem<ST>::kTsmem;
   extern __shared__ __align__(16) double smraw[];
@@ -900,6 +900,10 @@ __global__ void __launch_bounds__(288, ST >= 3 ? 2 : 3)
     // producer: chunk q (pass 1 forward, pass 2 backward over the row chunks) into stage q % 3
     if (lane == 0) {
       const int colA = t * a.ncol + c0, colV = t * a.ncol + k0;
+      // L2 priorities (l2keep >= 0): V is read by every column tile of the matrix (evict_last); of the
+      // A tile, the last l2keep/1000 of pass 1's chunks are the first pass 2 re-reads (evict_last),
+      // every other A chunk streams evict_first
+      const uint64_t pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
       for (int q = 0; q < 2 * nq; ++q) {
         const int st = q % ST;
         if (q >= ST) mbar_wait(&S.empty[st], static_cast<uint32_t>(((q / ST) - 1) & 1));
@@ -907,16 +911,30 @@ __global__ void __launch_bounds__(288, ST >= 3 ? 2 : 3)
         const int row = k0 + cq * RC;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&S.full[st], static_cast<uint32_t>((TN + NB_) * RCP * sizeof(double)));
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-                smem_u32(S.A[st])),
-            "l"(&tmA), "r"(row), "r"(colA), "r"(smem_u32(&S.full[st]))
-            : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-                smem_u32(S.V[st])),
-            "l"(&tmV), "r"(row), "r"(colV), "r"(smem_u32(&S.full[st]))
-            : "memory");
+        if (l2keep < 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                  smem_u32(S.A[st])),
+              "l"(&tmA), "r"(row), "r"(colA), "r"(smem_u32(&S.full[st]))
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                  smem_u32(S.V[st])),
+              "l"(&tmV), "r"(row), "r"(colV), "r"(smem_u32(&S.full[st]))
+              : "memory");
+        } else {
+          const bool keep = q < nq && 1000 * (q + 1) > (1000 - l2keep) * nq;
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+                  smem_u32(S.A[st])),
+              "l"(&tmA), "r"(row), "r"(colA), "r"(smem_u32(&S.full[st])), "l"(keep ? pol_last : pol_first)
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+                  smem_u32(S.V[st])),
+              "l"(&tmV), "r"(row), "r"(colV), "r"(smem_u32(&S.full[st])), "l"(pol_last)
+              : "memory");
+        }
       }
     }
     return;
@@ -1184,6 +1202,11 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
     DDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     kern<<<grid, 256, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, toff, tmA, tmV);
   };
+  // DDELM_QR_L2KEEP: per mille of pass 1's A chunks kept evict_last for pass 2 (-1: no L2 hints)
+  static const int l2keep = [] {
+    const char* e = std::getenv("DDELM_QR_L2KEEP");
+    return e ? std::max(-1, std::min(1000, std::atoi(e))) : -1;
+  }();
   static const bool ws = [] {
     const char* e = std::getenv("DDELM_QR_WS");
     return !(e && std::atoi(e) == 0);
@@ -1191,7 +1214,7 @@ void launch_qr_op(const QrArgs& a, const QrOp& op, cudaStream_t st) {
   if (op.kind == QrOp::kTrail32 && ws) {
     auto launch_ws = [&](auto kern, size_t smem) {
       DDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      kern<<<grid, 288, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, op.toff, tmA, tmV);
+      kern<<<grid, 288, smem, st>>>(a, op.k0, op.nbw, op.cb, op.ce, op.toff, tmA, tmV, l2keep);
     };
     if (stages == 2) launch_ws(qr_trailing_ws_kernel<2>, sizeof(TrailWsSmem<2>));
     else launch_ws(qr_trailing_ws_kernel<3>, sizeof(TrailWsSmem<3>));

@@ -931,6 +931,13 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.guard_all = 0;
   a.preissue = 4;  // DDELM_CG_PREISSUE: stream chunks issued before griddepcontrol.wait (measured: no effect)
   if (const char* e = std::getenv("DDELM_CG_PREISSUE")) a.preissue = std::max(0, std::min(4, std::atoi(e)));
+  // DDELM_CG_L2KEEP: per mille of an NN1 / OP3 walk kept evict_last (-1: no L2 hints). Measured at C3
+  // (tools/sweep_env.sh): -1 28.1 ms, 0 23.9 (every stream chunk evict_first: the streams no longer
+  // evict the small per-iteration data from L2), 250 24.3, 500 26.1, 1000 28.2
+  a.l2keep = 0;
+  a.l2pre = 0;  // DDELM_CG_L2PRE: per mille of each OP2 item prefetched into L2 during OP4 (< 0: evict_last)
+  if (const char* e = std::getenv("DDELM_CG_L2PRE")) a.l2pre = std::max(-1000, std::min(1000, std::atoi(e)));
+  if (const char* e = std::getenv("DDELM_CG_L2KEEP")) a.l2keep = std::max(-1, std::min(1000, std::atoi(e)));
   a.trace = nullptr;
   if (std::getenv("DDELM_CG_TRACE")) {
     d_trace.alloc(148 * 4 * 32);
