@@ -366,6 +366,29 @@ __device__ void l2_prefetch_items(const CgArgs& a, int kind, int permille) {
   }
 }
 
+/// L2 prefetch of the `n` chunks after the ones issued so far (this CTA's first item only): they
+/// stream from HBM while the phase's prologue waits for fresh data, the ring being full.
+__device__ void producer_l2ahead(const CgArgs& a, const Producer& pr, int n) {
+  if (!pr.active || pr.item >= pr.nitems) return;
+  const ItemGeo& g = pr.g;
+  const int c0 = pr.chunk, c1 = min(g.nch, pr.chunk + n);
+  if (c1 <= c0) return;
+  // walk-order chunks c0 .. c1-1 are rows [ja, jb) (forward) or the mirrored range (reverse)
+  int r0, r1;
+  if (!g.reverse) {
+    r0 = c0 * g.rpc;
+    r1 = min(g.rows, c1 * g.rpc);
+  } else {
+    r1 = min(g.rows, (g.nch - c0) * g.rpc);
+    r0 = (g.nch - c1) * g.rpc;
+  }
+  const unsigned long long lo = reinterpret_cast<unsigned long long>(g.base + static_cast<size_t>(r0) * g.ld) & ~15ull;
+  const unsigned long long hi =
+      (reinterpret_cast<unsigned long long>(g.base + static_cast<size_t>(r1) * g.ld) + 15ull) & ~15ull;
+  if (hi > lo)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(static_cast<unsigned>(hi - lo)) : "memory");
+}
+
 /// Consumer side of one work item (warps 0..14): per row j of each chunk, t_j = A_j . xa
 /// (xa in registers), u_j = hook(j, t_j, Ypi row) (lane-uniform), acc += u_j B_j (registers).
 /// `ccnt` counts the chunks consumed by this CTA (mirrors the producer's cnt).
@@ -1466,6 +1489,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
     if (producer && lane == 0) {
       producer_begin(a, pr, kind, mode == 2);
       producer_run(a, pr, sh, a.preissue);
+      if (a.l2ahead > 0) producer_l2ahead(a, pr, a.l2ahead);
     }
     if (!producer) pre = stream_pre(a, kind);
   } else if ((phase == kPhOp1 || phase == kPhOp4) && b < a.N) {

@@ -287,6 +287,7 @@ struct CgArgs {
   unsigned long long cond;  // cudaGraphConditionalHandle of the CG while-loop graph (0: none)
   int guard_all;            // chunked driver: every phase (streamed ones too) leaves once state[1] is set
   int preissue;             // stream chunks a streamed phase issues before griddepcontrol.wait (<= kStages)
+  int l2ahead;              // stream chunks past the preissued ring prefetched into L2 before griddepcontrol.wait
   int l2pre;                // per mille of each OP2 item prefetched into L2 by OP4 (HBM idle during OP4 / XR / OP1);
                             // negative: the same with the evict_last priority; 0: off
   int l2keep;               // per mille of each NN1 / OP3 item's chunks loaded L2::evict_last (read first by

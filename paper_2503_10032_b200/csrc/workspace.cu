@@ -929,12 +929,18 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.xr_parts = cg_grid(a);
   a.cond = 0;
   a.guard_all = 0;
-  a.preissue = 4;  // DDELM_CG_PREISSUE: stream chunks issued before griddepcontrol.wait (measured: no effect)
+  // DDELM_CG_PREISSUE: stream chunks issued before griddepcontrol.wait. With the evict_first streams
+  // the prologues are memory-latency bound and slow down under concurrent HBM traffic: C3 CG 24.15 ms
+  // at 4, 23.7 at 0, 23.65 at 2 (tools/sweep_env.sh, two sweeps); L2 prefetches of the following
+  // chunks (DDELM_CG_L2AHEAD) cost more still (2: +0.1 ms, 8: +0.6, 16: +1.2)
+  a.preissue = 2;
   if (const char* e = std::getenv("DDELM_CG_PREISSUE")) a.preissue = std::max(0, std::min(4, std::atoi(e)));
   // DDELM_CG_L2KEEP: per mille of an NN1 / OP3 walk kept evict_last (-1: no L2 hints). Measured at C3
   // (tools/sweep_env.sh): -1 28.1 ms, 0 23.9 (every stream chunk evict_first: the streams no longer
   // evict the small per-iteration data from L2), 250 24.3, 500 26.1, 1000 28.2
   a.l2keep = 0;
+  a.l2ahead = 0;  // DDELM_CG_L2AHEAD: chunks past the ring prefetched into L2 at preissue time
+  if (const char* e = std::getenv("DDELM_CG_L2AHEAD")) a.l2ahead = std::max(0, std::min(64, std::atoi(e)));
   a.l2pre = 0;  // DDELM_CG_L2PRE: per mille of each OP2 item prefetched into L2 during OP4 (< 0: evict_last)
   if (const char* e = std::getenv("DDELM_CG_L2PRE")) a.l2pre = std::max(-1000, std::min(1000, std::atoi(e)));
   if (const char* e = std::getenv("DDELM_CG_L2KEEP")) a.l2keep = std::max(-1, std::min(1000, std::atoi(e)));
