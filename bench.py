@@ -107,10 +107,17 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def one_gpu_harness_test() -> bool:
+    """DDELM_BENCH_ONE_GPU=1: harness self-test of the N-rank path on ONE GPU (every rank on
+    device 0, gloo process group, host-staged exchange). Its timings are not valid numbers — the
+    ranks share a GPU — and the JSON line says so (`harness_test`)."""
+    return os.environ.get("DDELM_BENCH_ONE_GPU") == "1"
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if one_gpu_harness_test() else int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
 
 
@@ -120,19 +127,23 @@ def dist_init(world):
     import torch
     import torch.distributed as dist
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    backend = "nccl" if torch.cuda.is_available() and not one_gpu_harness_test() else "gloo"
     if backend == "nccl":
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     dist.init_process_group(backend)
     return dist
 
 
+def _coll_device(dist) -> str:
+    import torch
+    return "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
+
+
 def max_over_ranks(dist, x: float) -> float:
     if dist is None:
         return x
     import torch
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device(dist))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -309,16 +320,18 @@ def run_single_config(P, name, steps, warmup, stream_of, peak):
     return out
 
 
-def workload_config(args, cfg, world=1):
+def workload_config(args, cfg, world=1, exchange="nccl"):
     return {"workload": f"{args.config}: DDELM-NN (theta {cfg['theta']}) {cfg['s']}x{cfg['s']} subdomains, "
                         f"M={cfg['M']}, n_grid={cfg['n_grid']}, l={cfg['l']}, {cfg['problem']}, "
                         f"{cfg['flux_variant']} + {cfg['trace_basis']}, cg_rel_tol {cfg['cg_rel_tol']}",
             "subdomains": cfg["s"] ** 2, "neurons_per_subdomain": cfg["M"],
             "collocation_points_per_subdomain": cfg["n_grid"] ** 2,
             "l2_policy": "working set (2N local matrices, >1 GB at C3) far exceeds the 126 MB L2",
-            "parallelism": (f"sharded x{world}: contiguous strip of subdomains per GPU (one process per GPU), "
-                            "owner-slot segments over NCCL send/recv between the CG phases, CG loop as "
-                            "chunked CUDA graphs" if world > 1 else "single GPU")}
+            "parallelism": ((f"sharded x{world}: contiguous strip of subdomains per GPU (one process per GPU), "
+                             "owner-slot segments over NCCL send/recv between the CG phases, CG loop as "
+                             "chunked CUDA graphs") if world > 1 and exchange == "nccl" else
+                            (f"sharded x{world}: contiguous strip of subdomains per GPU, owner-slot segments "
+                             f"through the {exchange} exchange, host-loop CG driver") if world > 1 else "single GPU")}
 
 
 # --------------------------------------------------------------------------- ours
@@ -330,11 +343,32 @@ def run_ours(args, cfg, world, rank, local, dist):
     torch.cuda.set_device(local)
     # the FP64 roofline denominator, measured live on this GPU (DMMA loop; ddelm_gpu_fp64_peak)
     fp64_peak = P.fp64_peak(local)
+    exchange = "none"
     if world > 1:
-        # sharded: this rank owns a strip of subdomains; owner-slot tables are all-reduced over NCCL
-        obj = [P.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ws = P.workspace_from_config(args.config, device=local, shard=(rank, world, obj[0]))
+        # sharded: this rank owns a strip of subdomains; the owner-slot entries other ranks read
+        # move over NCCL send/recv. If NCCL cannot be set up on any rank, every rank falls back —
+        # loudly, and labelled in the JSON line — to the host-staged exchange (POSIX shared memory)
+        # so the scaling run still completes (DDELM_BENCH_EXCHANGE=host forces it).
+        import torch as _t
+        ws, err = None, ""
+        if os.environ.get("DDELM_BENCH_EXCHANGE", "nccl") != "host" and not one_gpu_harness_test():
+            try:
+                obj = [P.nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0)
+                ws = P.workspace_from_config(args.config, device=local, shard=(rank, world, obj[0]))
+            except Exception as e:  # noqa: BLE001
+                err = f"{type(e).__name__}: {e}"
+                print(f"bench.py rank {rank}: NCCL sharded workspace failed ({err})", file=sys.stderr, flush=True)
+        bad = _t.tensor([0 if ws is not None else 1], dtype=_t.int32, device=_coll_device(dist))
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if int(bad.item()):
+            ws = None
+            name = f"/ddelm_bench_{os.environ.get('MASTER_PORT', '0')}"
+            ws = P.workspace_from_config(args.config, device=local, shard=(rank, world, "host:" + name))
+            exchange = "host-staged (NCCL unavailable" + (f": {err[:120]}" if err else " or forced") + ")"
+            print(f"bench.py rank {rank}: using the host-staged exchange", file=sys.stderr, flush=True)
+        else:
+            exchange = "nccl"
     else:
         ws = P.workspace_from_config(args.config, device=local)
     cg = P.CgOptions(rel_tol=cfg["cg_rel_tol"])
@@ -489,7 +523,7 @@ def run_ours(args, cfg, world, rank, local, dist):
                            "not the headline: its CG round-off trajectory differs from the reference's"}
         ws.set_cg_blocks("coeff")
 
-    ws_driver, ws_exchange = ws.cg_driver, ("nccl" if world > 1 else "none")
+    ws_driver, ws_exchange = ws.cg_driver, exchange
     # FP64 roofline of the factorisation + Schur phase by SURVEY.md §8d's formula (the headline
     # solve's own ranks and phase times)
     fp64_frac = None
@@ -517,7 +551,7 @@ def run_ours(args, cfg, world, rank, local, dist):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded feature layers; manufactured Poisson data)",
-            "config": workload_config(args, cfg, world),
+            "config": workload_config(args, cfg, world, exchange),
             "solve_seconds": ms_step / 1e3, "iterations": iters,
             "e2e": {"value": e2e_value, "unit": "subdomains/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
@@ -529,6 +563,8 @@ def run_ours(args, cfg, world, rank, local, dist):
                           "(ddelm_gpu_fp64_peak; r01 probe: 37.2, profiles/r01_fp64_peaks.json)"},
             "c4": c4, "cg_driver": ws_driver, "exchange": ws_exchange,
             "fp64_qr_tflops": (qr["flops"] / (qr["ms"] / 1e3) / 1e12) if qr else None}
+    if one_gpu_harness_test():
+        line["harness_test"] = "DDELM_BENCH_ONE_GPU=1: all ranks shared ONE GPU; timings are not valid numbers"
     print(json.dumps(line), flush=True)
 
 
@@ -544,7 +580,7 @@ def spawn_ranks(args) -> int:
     torch.distributed.run on 127.0.0.1) and pass their output through."""
     import torch
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and not one_gpu_harness_test():
         print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}",
               file=sys.stderr, flush=True)
         return 2

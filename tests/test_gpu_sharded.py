@@ -53,7 +53,10 @@ def _solve_single(name, method, monkeypatch, parts=PARTS, driver=None, body=None
 
 
 def _rank_worker(rank, world, shm, name, methods, parts, q):
-    os.environ["DDELM_CG_PARTS"] = parts
+    if parts is not None:
+        os.environ["DDELM_CG_PARTS"] = parts
+    else:
+        os.environ.pop("DDELM_CG_PARTS", None)
     try:
         import paper_2503_10032_b200 as P2
 
@@ -67,7 +70,7 @@ def _rank_worker(rank, world, shm, name, methods, parts, q):
                            "coeffs": np.array(rep.coeffs).copy(),
                            "hist": np.array(rep.residual_history).copy(), "driver": ws.cg_driver,
                            "launches": rep.launches}
-        l2 = ws.relative_errors(65) if c["problem"] != "poisson_grf" else None
+        l2 = ws.relative_errors(257) if c["problem"] != "poisson_grf" else None
         res["l2"] = l2
         del ws
         q.put((rank, res))
@@ -159,3 +162,37 @@ def test_while_graph_body_length_is_bitwise_neutral(P, name, method, monkeypatch
         np.testing.assert_array_equal(b["hist"], ref["hist"])
         np.testing.assert_array_equal(b["mu"], ref["mu"])
         np.testing.assert_array_equal(b["coeffs"], ref["coeffs"])
+
+
+def test_sharded_c3_world2_bitwise_with_equal_parts(P, monkeypatch):
+    """The bench workload (C3, 64 subdomains) on two strips of 32 with the single device's row-part
+    split (P = 2): bitwise the single-device solve."""
+    res = _run_sharded("C3", ["ddelm-nn"], world=2, parts="2")
+    ref = _solve_single("C3", "ddelm-nn", monkeypatch, parts="2")
+    for r in range(2):
+        assert res[r]["ddelm-nn"]["iterations"] == ref["iterations"]
+        np.testing.assert_array_equal(res[r]["ddelm-nn"]["hist"], ref["hist"])
+        np.testing.assert_array_equal(res[r]["ddelm-nn"]["mu"], ref["mu"])
+    np.testing.assert_array_equal(np.concatenate([res[r]["ddelm-nn"]["coeffs"] for r in range(2)], axis=0),
+                                  ref["coeffs"])
+
+
+def test_sharded_c3_world2_default_parts_within_parity(P):
+    """With the default split each rank cuts its 32 subdomains into P = 4 row parts (one device: 2),
+    so the per-part partial sums are grouped differently and the solve is a round-off neighbour of
+    the single-device one, not a bit copy (bench.py --gpus 2 runs it this way). It must meet the
+    single-device parity bars against the oracle golden: iterations within 1 + 2 spread, field
+    within 4 spread, exact-solution error within the spread of the oracle's."""
+    from test_gpu_parity import _field_diff, _golden
+
+    cfg = P.CONFIGS["C3"]
+    g = _golden("C3")
+    res = _run_sharded("C3", ["ddelm-nn"], world=2, parts=None)
+    it = res[0]["ddelm-nn"]["iterations"]
+    assert res[1]["ddelm-nn"]["iterations"] == it
+    assert abs(it - int(g["iterations"])) <= 1 + 2 * int(g["spread_iterations"]), (it, int(g["iterations"]))
+    coeffs = np.concatenate([res[r]["ddelm-nn"]["coeffs"] for r in range(2)], axis=0)
+    diff = _field_diff(cfg, coeffs, g["field_u"])
+    assert diff <= max(1e-9, 4.0 * float(g["spread_field"])), diff
+    l2 = res[0]["l2"][0]
+    assert abs(l2 - float(g["l2"])) <= max(1e-9, 4.0 * float(g["spread_field"])), (l2, float(g["l2"]))
