@@ -953,10 +953,16 @@ __global__ void __launch_bounds__(288, ST >= 3 ? 2 : 3)
     }
   };
   const double* Tg = a.T + static_cast<size_t>(t) * kQrTmax * kQrTmax;
+  // T (needed only after pass 1): loaded into registers now, stored to shared memory after pass 1,
+  // so the compute warps do not wait on these L2 loads before their first DMMA
+  constexpr int kTPer = NB_ * NB_ / (kWsCompute * 32);
+  double treg[kTPer];
   if (kTsmem)
-    for (int idx = threadIdx.x; idx < NB_ * NB_; idx += kWsCompute * 32) {
+#pragma unroll
+    for (int q = 0; q < kTPer; ++q) {
+      const int idx = threadIdx.x + q * kWsCompute * 32;
       const int i = idx / NB_, j = idx % NB_;
-      S.T[i * (NB_ + 1) + j] = (i < nb && j < nb) ? Tg[(tq + i) * kQrTmax + tq + j] : 0.0;
+      treg[q] = (i < nb && j < nb) ? Tg[(tq + i) * kQrTmax + tq + j] : 0.0;
     }
   // ---- pass 1: W = V^T A_tile; warp -> m-tiles {2(w&1), +1}, n-tiles {2(w>>1), +1}
   const int mt0 = (warp & 1) * WM, nt0 = (warp >> 1) * 2;
@@ -996,6 +1002,12 @@ __global__ void __launch_bounds__(288, ST >= 3 ? 2 : 3)
       const int r = (mt0 + i) * 8 + lr, c = (nt0 + j) * 8 + 2 * lc;
       S.W[r * TNP + c] = acc[i][j][0];
       S.W[r * TNP + c + 1] = acc[i][j][1];
+    }
+  if (kTsmem)
+#pragma unroll
+    for (int q = 0; q < kTPer; ++q) {
+      const int idx = threadIdx.x + q * kWsCompute * 32;
+      S.T[(idx / NB_) * (NB_ + 1) + idx % NB_] = treg[q];
     }
   compute_sync();
   // ---- W' = T^T W: warp -> its 8 columns, all m-tiles
