@@ -379,11 +379,11 @@ __device__ __forceinline__ double reduce_scatter8(double (&v)[kSub]) {
 }
 
 /// Pass jj over a staged sub-panel (column j at S + j*lds, row 0 = the sub-panel's first pivot
-/// row, R rows): apply H_{jj-1} to columns jj.., then accumulate ||x_jj||^2 below the diagonal and
-/// x_jj . y_{jj+k} into acc[k] (this thread's rows only).
+/// row, R rows): apply H_{jj-1} to columns jj.. (sdk[k] = v_{jj-1} . y_{jj+k}, in registers), then
+/// accumulate ||x_jj||^2 below the diagonal and x_jj . y_{jj+k} into acc[k] (this thread's rows).
 template <int NR>
 __device__ __forceinline__ void sub_pass(double* S, int lds, int R, int jj, double tau_p, double scale_p, double beta_p,
-                                         bool triv_p, const double* sdl, double* srowl, double (&acc)[kSub]) {
+                                         bool triv_p, const double (&sdk)[kSub], double* srowl, double (&acc)[kSub]) {
   const int rlo = jj > 0 ? jj - 1 : 0;
   for (int i = rlo + threadIdx.x; i < R; i += kPanelThreads) {
     double y[NR > 0 ? NR : 1];
@@ -395,7 +395,7 @@ __device__ __forceinline__ void sub_pass(double* S, int lds, int R, int jj, doub
       const double tv = tau_p * v;
 #pragma unroll
       for (int k = 0; k < NR; ++k) {
-        y[k] -= tv * sdl[jj + k];
+        y[k] -= tv * sdk[k];
         S[(jj + k) * lds + i] = y[k];
       }
       *pc = (i == jj - 1) ? beta_p : v;
@@ -403,7 +403,7 @@ __device__ __forceinline__ void sub_pass(double* S, int lds, int R, int jj, doub
     if constexpr (NR > 0) {
       if (i == jj) {
 #pragma unroll
-        for (int k = 0; k < NR; ++k) srowl[jj + k] = y[k];
+        for (int k = 0; k < NR; ++k) srowl[k] = y[k];  // row jj, columns jj + k
       }
       if (i > jj) {
         const double x = y[0];
@@ -422,11 +422,12 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
   const size_t ld = a.ld;
   const int nb = min(NB, a.M - k0);
   extern __shared__ __align__(16) double dyn[];  // sub-panel [kSub][lds]; later panel_finish scratch
-  __shared__ double sred[kPanelWarps][kSub];
-  __shared__ double sfin[kSub], srow[kSub], sd[kSub];
+  // per-column reduction partials and row jj, double-buffered by column parity: ONE block barrier
+  // per column — every warp then sums the 16 partials itself (the same order) and derives tau,
+  // beta, scale and the next pass's v . y terms in registers
+  __shared__ double sred[2][kPanelWarps][kSub];
+  __shared__ double srow[2][kSub];
   __shared__ double stau[NB];
-  __shared__ double sbeta, sscale;
-  __shared__ int striv;
   __shared__ double sGp[kPanelWarps][kSub * kSub];  // V8^T V8 partials (per warp)
   __shared__ double sT8[kSub][kSub + 1];
   __shared__ double sWp[kPanelWarps * kSub * kSub];  // V8^T Y partials (per row group)
@@ -453,22 +454,20 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    double tau_p = 0, scale_p = 0, beta_p = 0;
+    bool triv_p = true;
+    double sdk[kSub];
+#pragma unroll
+    for (int k = 0; k < kSub; ++k) sdk[k] = 0.0;
     for (int jj = 0; jj <= w; ++jj) {
-      double tau_p = 0, scale_p = 0, beta_p = 0;
-      bool triv_p = true;
-      if (jj > 0) {
-        tau_p = stau[s0 + jj - 1];
-        scale_p = sscale;
-        beta_p = sbeta;
-        triv_p = striv != 0;
-      }
       double acc[kSub];
 #pragma unroll
       for (int k = 0; k < kSub; ++k) acc[k] = 0.0;
+      double* srowl = srow[jj & 1];
       switch (w - jj) {
 #define DDG_SUB_CASE(n) \
   case n:               \
-    sub_pass<n>(dyn, lds, R, jj, tau_p, scale_p, beta_p, triv_p, sd, srow, acc); \
+    sub_pass<n>(dyn, lds, R, jj, tau_p, scale_p, beta_p, triv_p, sdk, srowl, acc); \
     break;
         DDG_SUB_CASE(0) DDG_SUB_CASE(1) DDG_SUB_CASE(2) DDG_SUB_CASE(3) DDG_SUB_CASE(4)
         DDG_SUB_CASE(5) DDG_SUB_CASE(6) DDG_SUB_CASE(7) DDG_SUB_CASE(8)
@@ -478,37 +477,35 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       }
       if (jj == w) break;
       const double red = reduce_scatter8(acc);
-      if (lane < kSub) sred[warp][lane] = red;
+      if (lane < kSub) sred[jj & 1][warp][lane] = red;
       __syncthreads();
-      if (threadIdx.x < kSub) {
-        double s = 0;
-        for (int q = 0; q < kPanelWarps; ++q) s += sred[q][threadIdx.x];
-        sfin[threadIdx.x] = s;  // sfin[k]: column jj+k (k = 0: squared norm below the diagonal)
+      double sf = 0;  // lane k < 8: column jj+k (k = 0: squared norm below the diagonal)
+      if (lane < kSub)
+        for (int q = 0; q < kPanelWarps; ++q) sf += sred[jj & 1][q][lane];
+      double sfin[kSub];
+#pragma unroll
+      for (int k = 0; k < kSub; ++k) sfin[k] = __shfl_sync(0xffffffffu, sf, k);
+      const double alpha = srowl[0], tail = sfin[0];
+      double tau = 0, beta = alpha, scale = 0;
+      const bool triv = !(tail > DBL_MIN);
+      if (!triv) {
+        beta = sqrt(alpha * alpha + tail);
+        if (alpha >= 0) beta = -beta;
+        scale = 1.0 / (alpha - beta);
+        tau = (beta - alpha) / beta;
       }
-      __syncthreads();
-      {
-        const double alpha = srow[jj], tail = sfin[0];
-        double tau = 0, beta = alpha, scale = 0;
-        const bool triv = !(tail > DBL_MIN);
-        if (!triv) {
-          beta = sqrt(alpha * alpha + tail);
-          if (alpha >= 0) beta = -beta;
-          scale = 1.0 / (alpha - beta);
-          tau = (beta - alpha) / beta;
-        }
-        if (threadIdx.x < kSub) {
-          const int j = threadIdx.x;
-          sd[j] = (j > jj && j < w) ? srow[j] + sfin[j - jj] * scale : 0.0;
-        }
-        if (threadIdx.x == 0) {
-          stau[s0 + jj] = tau;
-          sbeta = beta;
-          sscale = scale;
-          striv = triv ? 1 : 0;
-          a.tau[static_cast<size_t>(t) * a.M + c0 + jj] = tau;
-        }
+      // v_jj . y_j for the columns j = jj+1+k of the next pass
+#pragma unroll
+      for (int k = 0; k + 1 < kSub; ++k) sdk[k] = (jj + 1 + k < w) ? srowl[1 + k] + sfin[k + 1] * scale : 0.0;
+      sdk[kSub - 1] = 0.0;
+      if (threadIdx.x == 0) {
+        stau[s0 + jj] = tau;
+        a.tau[static_cast<size_t>(t) * a.M + c0 + jj] = tau;
       }
-      __syncthreads();
+      tau_p = tau;
+      scale_p = scale;
+      beta_p = beta;
+      triv_p = triv;
     }
     __syncthreads();
     // write the factored sub-panel back (R entries above the diagonal, beta, v below)
