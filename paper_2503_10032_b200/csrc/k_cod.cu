@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(512) cod_pivqr_kernel(CodArgs a, int t0) {
 // (I - V T^T V^T) as two small GEMMs. The sequential form (below, kept for r > kFinR) spent
 // ~5 us per reflector on dependent global loads.
 constexpr int kFinR = 96;
+constexpr int kRZ = 32;  // RZ row entries per lane held in registers (M - r <= 1024)
 constexpr int kFinEB = 64;  // X columns per block of the Q1^T application
 
 /// out(m, n, sum_k A(k, m) B(k, n)) for m < Mo, n < No, k < Ko, with A(k, m) = A[k*sak + m*sam]
@@ -670,6 +671,8 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
   double* Y = a.Ywork + static_cast<size_t>(t) * M * R;  // Y(i, c) = Y[i*R + c]
   __shared__ double red[32];
   __shared__ double s_tau, s_beta, s_scale;
+  extern __shared__ __align__(16) double fsm_rz[];
+  double* zrow = fsm_rz;  // M - r doubles (the finish scratch is idle during the RZ pass)
 
   unsigned long long tlast = 0;
   fin_stamp(a, t, -1, tlast);
@@ -702,21 +705,55 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
         zc[k] = tau;
       }
       __syncthreads();
-      for (int j = r + threadIdx.x; j < M; j += blockDim.x) row[j] *= s_scale;
+      for (int j = r + threadIdx.x; j < M; j += blockDim.x) {
+        const double z = row[j] * s_scale;
+        row[j] = z;
+        zrow[j - r] = z;  // the reflector tail, read by every warp below: from shared memory
+      }
       __syncthreads();
       if (threadIdx.x == 0) row[r - 1] = s_beta;
-      // apply Z(k) from the right to rows 0..k-1 (warp per row)
-      if (s_tau != 0.0)
-        for (int u = warp; u < k; u += nwarp) {
-          double* ru = Rr + static_cast<size_t>(u) * M;
-          double s = 0;
-          for (int j = r + lane; j < M; j += 32) s += ru[j] * row[j];
-          s = warp_sum(s);
-          s = (s + ru[r - 1]) * s_tau;
-          __syncwarp();
-          if (lane == 0) ru[r - 1] -= s;
-          for (int j = r + lane; j < M; j += 32) ru[j] -= s * row[j];
+      // apply Z(k) from the right to rows 0..k-1 (warp per row): the lane's entries of row u are
+      // loaded once, all in flight, then summed in the same order and updated from registers
+      if (s_tau != 0.0) {
+        if (M - r <= 32 * kRZ) {
+          for (int u = warp; u < k; u += nwarp) {
+            double* ru = Rr + static_cast<size_t>(u) * M;
+            double x[kRZ];
+#pragma unroll
+            for (int q = 0; q < kRZ; ++q) {
+              const int j = r + lane + 32 * q;
+              x[q] = j < M ? ru[j] : 0.0;
+            }
+            const double ur = ru[r - 1];
+            double s = 0;
+#pragma unroll
+            for (int q = 0; q < kRZ; ++q) {
+              const int j = r + lane + 32 * q;
+              if (j < M) s += x[q] * zrow[j - r];
+            }
+            s = warp_sum(s);
+            s = (s + ur) * s_tau;
+            __syncwarp();
+            if (lane == 0) ru[r - 1] = ur - s;
+#pragma unroll
+            for (int q = 0; q < kRZ; ++q) {
+              const int j = r + lane + 32 * q;
+              if (j < M) ru[j] = x[q] - s * zrow[j - r];
+            }
+          }
+        } else {
+          for (int u = warp; u < k; u += nwarp) {
+            double* ru = Rr + static_cast<size_t>(u) * M;
+            double s = 0;
+            for (int j = r + lane; j < M; j += 32) s += ru[j] * row[j];
+            s = warp_sum(s);
+            s = (s + ru[r - 1]) * s_tau;
+            __syncwarp();
+            if (lane == 0) ru[r - 1] -= s;
+            for (int j = r + lane; j < M; j += 32) ru[j] -= s * row[j];
+          }
         }
+      }
       __syncthreads();
       if (k != r - 1)
         for (int u = threadIdx.x; u <= k; u += blockDim.x) {
@@ -830,7 +867,7 @@ void launch_cod_pivqr(const CodArgs& a, cudaStream_t st) {
 }
 
 void launch_cod_finish(const CodArgs& a, cudaStream_t st) {
-  const size_t smem = finish_smem_bytes(a.rmax);
+  const size_t smem = std::max(finish_smem_bytes(a.rmax), sizeof(double) * static_cast<size_t>(a.M));
   DDG_CUDA(cudaFuncSetAttribute(cod_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   cod_finish_kernel<<<a.nmat, 512, smem, st>>>(a);
   DDG_LAUNCH_CHECK();
