@@ -678,20 +678,15 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
   fin_stamp(a, t, -1, tlast);
   // ---- RZ (COD::compute): rows k = r-1 .. 0 of [R11 R12], columns {k} U {r..M-1}
   if (r < M) {
+    // (COD swaps column k with column r-1 so the reflector's support is contiguous, then swaps
+    // back; the same arithmetic addresses column k directly)
     for (int k = r - 1; k >= 0; --k) {
-      if (k != r - 1)
-        for (int u = threadIdx.x; u <= k; u += blockDim.x) {
-          const double tmp = Rr[static_cast<size_t>(u) * M + k];
-          Rr[static_cast<size_t>(u) * M + k] = Rr[static_cast<size_t>(u) * M + r - 1];
-          Rr[static_cast<size_t>(u) * M + r - 1] = tmp;
-        }
-      __syncthreads();
       double* row = Rr + static_cast<size_t>(k) * M;
       double part = 0;
       for (int j = r + threadIdx.x; j < M; j += blockDim.x) part += row[j] * row[j];
       const double tail = block_sum(part, red);
       if (threadIdx.x == 0) {
-        const double c0 = row[r - 1];
+        const double c0 = row[k];
         double tau = 0, beta = c0, scale = 0;
         if (tail > DBL_MIN) {
           beta = sqrt(c0 * c0 + tail);
@@ -711,7 +706,7 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
         zrow[j - r] = z;  // the reflector tail, read by every warp below: from shared memory
       }
       __syncthreads();
-      if (threadIdx.x == 0) row[r - 1] = s_beta;
+      if (threadIdx.x == 0) row[k] = s_beta;
       // apply Z(k) from the right to rows 0..k-1 (warp per row): the lane's entries of row u are
       // loaded once, all in flight, then summed in the same order and updated from registers
       if (s_tau != 0.0) {
@@ -724,7 +719,7 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
               const int j = r + lane + 32 * q;
               x[q] = j < M ? ru[j] : 0.0;
             }
-            const double ur = ru[r - 1];
+            const double ur = ru[k];
             double s = 0;
 #pragma unroll
             for (int q = 0; q < kRZ; ++q) {
@@ -734,7 +729,7 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
             s = warp_sum(s);
             s = (s + ur) * s_tau;
             __syncwarp();
-            if (lane == 0) ru[r - 1] = ur - s;
+            if (lane == 0) ru[k] = ur - s;
 #pragma unroll
             for (int q = 0; q < kRZ; ++q) {
               const int j = r + lane + 32 * q;
@@ -747,20 +742,13 @@ __global__ void __launch_bounds__(512) cod_finish_kernel(CodArgs a) {
             double s = 0;
             for (int j = r + lane; j < M; j += 32) s += ru[j] * row[j];
             s = warp_sum(s);
-            s = (s + ru[r - 1]) * s_tau;
+            s = (s + ru[k]) * s_tau;
             __syncwarp();
-            if (lane == 0) ru[r - 1] -= s;
+            if (lane == 0) ru[k] -= s;
             for (int j = r + lane; j < M; j += 32) ru[j] -= s * row[j];
           }
         }
       }
-      __syncthreads();
-      if (k != r - 1)
-        for (int u = threadIdx.x; u <= k; u += blockDim.x) {
-          const double tmp = Rr[static_cast<size_t>(u) * M + k];
-          Rr[static_cast<size_t>(u) * M + k] = Rr[static_cast<size_t>(u) * M + r - 1];
-          Rr[static_cast<size_t>(u) * M + r - 1] = tmp;
-        }
       __syncthreads();
     }
   }
