@@ -465,41 +465,66 @@ constexpr int kRZ = 32;  // RZ row entries per lane held in registers (M - r <= 
 constexpr int kFinEB = 64;  // X columns per block of the Q1^T application
 
 /// out(m, n, sum_k A(k, m) B(k, n)) for m < Mo, n < No, k < Ko, with A(k, m) = A[k*sak + m*sam]
-/// and B(k, n) = B[k*sbk + n*sbn]: 8 x 8 output tiles over the CTA's warps, DMMA m8n8k4.
+/// and B(k, n) = B[k*sbk + n*sbn]: 8 x 8 output tiles over the CTA's warps, DMMA m8n8k4. A warp
+/// carries two tiles at once (tile, tile + nwarps) so 16 loads per lane are in flight (the operands
+/// come from L2: latency-bound); each tile still accumulates over k in ascending order.
 template <class Out>
 __device__ void tile_gemm_tn(int Mo, int No, int Ko, const double* A, long sak, long sam, const double* B,
                              long sbk, long sbn, Out out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int lr = lane >> 2, lc = lane & 3;
-  const int tm = (Mo + 7) >> 3, tn = (No + 7) >> 3;
-  for (int tile = warp; tile < tm * tn; tile += nw) {
-    const int m0 = (tile / tn) * 8, n0 = (tile % tn) * 8;
-    const bool mok = m0 + lr < Mo, nok = n0 + lr < No;
-    const double* Ap = A + (mok ? m0 + lr : 0) * sam;
-    const double* Bp = B + (nok ? n0 + lr : 0) * sbn;
-    double c0 = 0, c1 = 0;
+  const int tm = (Mo + 7) >> 3, tn = (No + 7) >> 3, nt = tm * tn;
+  for (int tile = warp; tile < nt; tile += 2 * nw) {
+    const int tiles[2] = {tile, tile + nw};
+    bool mok[2], nok[2], live[2];
+    const double* Ap[2];
+    const double* Bp[2];
+    int m0[2], n0[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      live[q] = tiles[q] < nt;
+      const int tq = live[q] ? tiles[q] : tile;
+      m0[q] = (tq / tn) * 8;
+      n0[q] = (tq % tn) * 8;
+      mok[q] = live[q] && m0[q] + lr < Mo;
+      nok[q] = live[q] && n0[q] + lr < No;
+      Ap[q] = A + (mok[q] ? m0[q] + lr : 0) * sam;
+      Bp[q] = B + (nok[q] ? n0[q] + lr : 0) * sbn;
+    }
+    double c[2][2] = {{0, 0}, {0, 0}};
     int k = 0;
-    for (; k + 16 <= Ko; k += 16) {  // 8 loads in flight per lane
-      double av[4], bv[4];
+    for (; k + 16 <= Ko; k += 16) {  // 16 loads in flight per lane
+      double av[2][4], bv[2][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long kk = k + 4 * u + lc;
-        av[u] = mok ? Ap[kk * sak] : 0.0;
-        bv[u] = nok ? Bp[kk * sbk] : 0.0;
-      }
+      for (int q = 0; q < 2; ++q)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) dmma_8x8x4(c0, c1, av[u], bv[u]);
+        for (int u = 0; u < 4; ++u) {
+          const long kk = k + 4 * u + lc;
+          av[q][u] = mok[q] ? Ap[q][kk * sak] : 0.0;
+          bv[q][u] = nok[q] ? Bp[q][kk * sbk] : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma_8x8x4(c[q][0], c[q][1], av[q][u], bv[q][u]);
     }
     for (; k < Ko; k += 4) {
       const int kk = k + lc;
-      const double av = (mok && kk < Ko) ? Ap[static_cast<long>(kk) * sak] : 0.0;
-      const double bv = (nok && kk < Ko) ? Bp[static_cast<long>(kk) * sbk] : 0.0;
-      dmma_8x8x4(c0, c1, av, bv);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double av = (mok[q] && kk < Ko) ? Ap[q][static_cast<long>(kk) * sak] : 0.0;
+        const double bv = (nok[q] && kk < Ko) ? Bp[q][static_cast<long>(kk) * sbk] : 0.0;
+        dmma_8x8x4(c[q][0], c[q][1], av, bv);
+      }
     }
-    const int om = m0 + lr, on = n0 + 2 * lc;
-    if (om < Mo) {
-      if (on < No) out(om, on, c0);
-      if (on + 1 < No) out(om, on + 1, c1);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (!live[q]) continue;
+      const int om = m0[q] + lr, on = n0[q] + 2 * lc;
+      if (om < Mo) {
+        if (on < No) out(om, on, c[q][0]);
+        if (on + 1 < No) out(om, on + 1, c[q][1]);
+      }
     }
   }
 }
@@ -509,12 +534,12 @@ __device__ void tile_gemm_tn(int Mo, int No, int Ko, const double* A, long sak, 
 __device__ void larft_from_gram(const double* G, int ldg, const double* tau, int r, double* T, int ldt) {
   for (int idx = threadIdx.x; idx < r * ldt; idx += blockDim.x) T[idx] = 0.0;
   __syncthreads();
+  // column j reads only columns < j of T (written before the previous barrier): one barrier per column
   for (int j = 0; j < r; ++j) {
     double s = 0;
     const int i = threadIdx.x;
     if (i < j)
       for (int w = i; w < j; ++w) s += T[i * ldt + w] * G[w * ldg + j];
-    __syncthreads();
     if (i < j) T[i * ldt + j] = -tau[j] * s;
     if (i == j) T[j * ldt + j] = tau[j];
     __syncthreads();
