@@ -529,15 +529,14 @@ __device__ void rows_dot(const double* W, int ldw, const int* rows, int nrows, c
     double s = 0;
     if (row >= 0) {
       const double* w = W + static_cast<size_t>(row) * ldw;
-      int k = lane;
-      for (; k + 96 < len; k += 128) {  // four loads in flight per lane
-        const double w0 = w[k], w1 = w[k + 32], w2 = w[k + 64], w3 = w[k + 96];
-        s += w0 * vec[k];
-        s += w1 * vec[k + 32];
-        s += w2 * vec[k + 64];
-        s += w3 * vec[k + 96];
+      for (int k0 = lane; k0 < len; k0 += 256) {  // eight loads in flight per lane, summed in k order
+        double wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) wv[u] = k0 + 32 * u < len ? w[k0 + 32 * u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k0 + 32 * u < len) s += wv[u] * vec[k0 + 32 * u];
       }
-      for (; k < len; k += 32) s += w[k] * vec[k];
     }
     s = warp_sum(s);
     if (lane == 0) out[q] = s;
@@ -748,15 +747,14 @@ __device__ void row_tasks(const RowTask* tk, int ntask, int nwarps) {
     double s = 0;
     if (t.row >= 0) {
       const double* w = t.W + static_cast<size_t>(t.row) * t.ld;
-      int k = lane;
-      for (; k + 160 < t.len; k += 192) {  // six loads in flight per lane
-        double wv[6];
+      for (int k0 = lane; k0 < t.len; k0 += 256) {  // eight loads in flight per lane, summed in k order
+        double wv[8];
 #pragma unroll
-        for (int u = 0; u < 6; ++u) wv[u] = w[k + 32 * u];
+        for (int u = 0; u < 8; ++u) wv[u] = k0 + 32 * u < t.len ? w[k0 + 32 * u] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 6; ++u) s += wv[u] * t.vec[k + 32 * u];
+        for (int u = 0; u < 8; ++u)
+          if (k0 + 32 * u < t.len) s += wv[u] * t.vec[k0 + 32 * u];
       }
-      for (; k < t.len; k += 32) s += w[k] * t.vec[k];
     }
     s = warp_sum(s);
     if (lane == 0) *t.out = s;
