@@ -505,18 +505,25 @@ __device__ __forceinline__ double gather_xc(const CgArgs& a, int rr) {
 /// z = [t; psi]: corner contributions of OP1 summed over their owners (subdomain order) and the
 /// cross-flux data psi (mode 0: Dpd v; mode 1: dpi; mode 2: dpi - Dpd mu_Delta).
 __device__ void gather_z(const CgArgs& a, const Shared& sh, int mode, int nthr) {
-  const int n = a.n_pi;
-  for (int gp = threadIdx.x; gp < n; gp += nthr) {
-    const double* t4 = a.ttab + 4 * static_cast<size_t>(gp);
-    sh.z[gp] = ((t4[0] + t4[1]) + t4[2]) + t4[3];
-  }
-  for (int rr = threadIdx.x; rr < a.npf; rr += nthr) {
-    double acc = 0;
-    if (mode != 1) {
-      const double* p4 = a.ptab + 4 * static_cast<size_t>(rr);
-      acc = ((p4[0] + p4[1]) + p4[2]) + p4[3];
+  // a thread's t and psi entries (fresh from OP1) are loaded together, then summed and stored:
+  // one L2 round trip instead of two
+  const int n = a.n_pi, nf = a.npf;
+  for (int q = threadIdx.x; q < max(n, nf); q += nthr) {
+    double t4[4] = {0, 0, 0, 0}, p4[4] = {0, 0, 0, 0}, dp = 0;
+    if (q < n)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t4[u] = a.ttab[4 * static_cast<size_t>(q) + u];
+    if (q < nf) {
+      if (mode != 1)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) p4[u] = a.ptab[4 * static_cast<size_t>(q) + u];
+      if (mode != 0) dp = a.dpi[q];
     }
-    sh.z[n + rr] = (mode == 0) ? acc : (mode == 1 ? a.dpi[rr] : a.dpi[rr] - acc);
+    if (q < n) sh.z[q] = ((t4[0] + t4[1]) + t4[2]) + t4[3];
+    if (q < nf) {
+      const double acc = (mode != 1) ? ((p4[0] + p4[1]) + p4[2]) + p4[3] : 0.0;
+      sh.z[n + q] = (mode == 0) ? acc : (mode == 1 ? dp : dp - acc);
+    }
   }
 }
 
@@ -845,8 +852,11 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
   for (int k = 0; k < nitems; ++k) {
     const int w = item_work(k, nitems, false);
     const int i = w / a.P, p = w % a.P;
-    if (!a.one_level) gather_z(a, sh, mode, kCThreads);
     const bool first = (k == 0 && pre.i == i);
+    // s_i (fresh from OP1) is loaded together with gather_z's t / psi slots: one round trip
+    const int r = first ? pre_geo().r : a.geo[i].r;
+    const double s_first = threadIdx.x < r ? a.s[static_cast<size_t>(i) * a.rmax + threadIdx.x] : 0.0;
+    if (!a.one_level) gather_z(a, sh, mode, kCThreads);
     if (threadIdx.x < a.ncq) {
       if (first) {
         crow[threadIdx.x] = pre.crow;
@@ -855,8 +865,8 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
         crow[threadIdx.x] = (g >= 0 && !a.one_level) ? a.gamma_pi[static_cast<size_t>(i) * a.gmax + g] : -1;
       }
     }
-    const int r = first ? pre_geo().r : a.geo[i].r;
-    for (int kk = threadIdx.x; kk < r; kk += kCThreads) sh.xa[kk] = a.s[static_cast<size_t>(i) * a.rmax + kk];
+    for (int kk = threadIdx.x; kk < r; kk += kCThreads)
+      sh.xa[kk] = kk == threadIdx.x ? s_first : a.s[static_cast<size_t>(i) * a.rmax + kk];
     cons_sync();
     const int nz = a.n_pi + a.npf;
     rows_dot(a.Wmu, nz, crow, a.ncq, sh.z, nz, muc, kCWarps);  // mu = S^{-1}(t + Dpp^T psi); 0 one-level
