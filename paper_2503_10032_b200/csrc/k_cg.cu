@@ -473,7 +473,7 @@ __device__ __forceinline__ double sum_parts(const double* base, size_t stride, i
   if (P <= kMaxP) {
     double v[kMaxP];
 #pragma unroll
-    for (int p = 0; p < kMaxP; ++p) v[p] = p < P ? base[p * stride + idx] : 0.0;
+    for (int p = 0; p < kMaxP; ++p) v[p] = p < P ? __ldcg(base + p * stride + idx) : 0.0;
     double s = 0;
 #pragma unroll
     for (int p = 0; p < kMaxP; ++p)
@@ -481,7 +481,7 @@ __device__ __forceinline__ double sum_parts(const double* base, size_t stride, i
     return s;
   }
   double s = 0;
-  for (int p = 0; p < P; ++p) s += base[p * stride + idx];
+  for (int p = 0; p < P; ++p) s += __ldcg(base + p * stride + idx);
   return s;
 }
 
@@ -1009,8 +1009,8 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
 #pragma unroll
             for (int pp = 0; pp < kQ; ++pp) {
               const size_t o = pp * st2 + 2 * static_cast<size_t>(gg) + sl;
-              zv[sl][pp] = (pp < a.P && a.use_neumann) ? a.zztab[o] : 0.0;
-              xv[sl][pp] = pp < a.P ? a.xtab[o] : 0.0;
+              zv[sl][pp] = (pp < a.P && a.use_neumann) ? __ldcg(a.zztab + o) : 0.0;
+              xv[sl][pp] = pp < a.P ? __ldcg(a.xtab + o) : 0.0;
             }
           const double fs = a.flip_sign[gg];
           double z0 = 0, z1 = 0, x0 = 0, x1 = 0;
@@ -1079,6 +1079,60 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
     }
     cons_sync();
   }
+}
+
+// ---------------------------------------------------------------- fused OP2 -> OP3 launch
+__device__ __forceinline__ int& fused_gate() {
+  __shared__ int g;
+  return g;
+}
+
+/// After a phase of the fused launch: every item this CTA streamed in `kind` bumps its subdomain's
+/// completion counter of stage `ph` (release: the item's owner-slot writes are fenced first).
+__device__ void fused_signal(const CgArgs& a, int ph, int kind) {
+  cons_sync();  // every consumer thread's slot stores issued
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int nitems = n_items(a.N * a.P);
+    for (int k = 0; k < nitems; ++k) {
+      const int w = item_work(k, nitems, reverse_kind(kind));
+      atomicAdd(a.pflags + static_cast<size_t>(ph) * a.N + w / a.P, 1u);
+    }
+  }
+}
+
+/// Before the next phase `kind` of the fused launch: wait until every subdomain whose owner slots
+/// this CTA's items read (the item's subdomain and its edge neighbours) has all P parts through
+/// stage `ph` of iteration `it` (acquire), then release the consumer warps.
+__device__ void fused_wait(const CgArgs& a, int ph, int kind, int it) {
+  if (threadIdx.x == 0) {
+    const unsigned target = static_cast<unsigned>(a.P) * static_cast<unsigned>(it);
+    const int nitems = n_items(a.N * a.P);
+    // watchdog: the counters only advance if every CTA of the launch is resident (one per SM); if a
+    // wait exceeds 2 s the launch flags state[4] (the host reports it) instead of hanging the GPU
+    const unsigned long long t0 = gtimer();
+    bool expired = false;
+    for (int k = 0; k < nitems; ++k) {
+      const int i = item_work(k, nitems, reverse_kind(kind)) / a.P;
+      for (int q = 0; q < kCgMaxNbr; ++q) {
+        const int d = a.nbr[i * kCgMaxNbr + q];
+        if (d < 0) break;
+        const unsigned* f = a.pflags + static_cast<size_t>(ph) * a.N + d;
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        while (v < target && !expired) {
+          if (a.fuse_sleep) __nanosleep(a.fuse_sleep);
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+          if (gtimer() - t0 > 2000000000ull) {
+            expired = true;
+            atomicExch(a.state + 4, 1);
+          }
+        }
+      }
+    }
+    __threadfence();
+  }
+  cons_sync();
 }
 
 // ---------------------------------------------------------------- OP4 (per subdomain, all warps)
@@ -1500,10 +1554,11 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
   // phase's static-data bulk copies (coefficient blocks, Q_r^T / Zc) before waiting for the
   // previous phase to complete — the in-kernel analogue of prefetching across a grid barrier.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const bool streamed = phase == kPhOp2 || phase == kPhNn1 || phase == kPhNn2 || phase == kPhOp3;
+  const bool fused = phase == kPhFused;
+  const bool streamed = phase == kPhOp2 || phase == kPhNn1 || phase == kPhNn2 || phase == kPhOp3 || fused;
   StreamPre pre{-1, -1, -1};
   if (streamed) {
-    const int kind = phase == kPhOp2 ? kOp2 : phase == kPhNn1 ? kNn1 : phase == kPhNn2 ? kNn2 : kOp3;
+    const int kind = (phase == kPhOp2 || fused) ? kOp2 : phase == kPhNn1 ? kNn1 : phase == kPhNn2 ? kNn2 : kOp3;
     if (producer && lane == 0) {
       producer_begin(a, pr, kind, mode == 2);
       producer_run(a, pr, sh, a.preissue);
@@ -1519,12 +1574,12 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
   if (a.trace && threadIdx.x == 0) phase_stamps()[1] = gtimer();
   // the streamed phases only write intermediate tables: they need neither the iteration counter
   // nor the stop flag (XR1 checks it), so their prologue starts with fresh data, not state
-  if (cg && !streamed) it = a.state[6];  // the iteration counter lives on the device (graph replays)
+  if (cg && (!streamed || fused)) it = a.state[6];  // the iteration counter lives on the device (graph replays)
   double* pcur = a.pbuf[(it + 1) & 1];
   double* pnext = a.pbuf[it & 1];
   // converged / aborted earlier (the chunked sharded driver also replays streamed phases past the
   // stop: guard_all): drain the prefetched copies and leave
-  if (cg && (!streamed || a.guard_all) && a.state[1]) {
+  if (cg && (!streamed || fused || a.guard_all) && a.state[1]) {
     if ((phase == kPhXr1 || phase == kPhXr2) && b == 0 && threadIdx.x == 0 && a.cond != 0)
       cudaGraphSetConditional(a.cond, 0);
     __shared__ int s_issued;
@@ -1573,6 +1628,47 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
         tr[2] += static_cast<double>(t[3] - t[2]);
         tr[3] += static_cast<double>(end - t[3]);
       }
+      return;
+    }
+    case kPhFused: {
+      // OP2, NN1, NN2, OP3 back to back: the producer warp streams the four phases' chunks through
+      // the ring without a break (the next phase's first chunks load while the consumers wait for
+      // their neighbours); between phases an item waits only for the subdomains it reads from
+      // the producer runs at most `preissue` chunks into the next phase before the consumers have
+      // passed their neighbour wait (concurrent HBM traffic slows the latency-bound prologues)
+      volatile int* gate = &fused_gate();
+      if (threadIdx.x == 0) *gate = 0;
+      __syncthreads();
+      if (producer) {
+        if (lane == 0) {
+          producer_run(a, pr, sh, -1);
+          for (int kind = kNn1; kind <= kOp3; ++kind) {
+            producer_begin(a, pr, kind, false);
+            if (a.fuse_gate) {
+              producer_run(a, pr, sh, a.preissue);
+              while (*gate < kind) {
+              }
+            }
+            producer_run(a, pr, sh, -1);
+          }
+        }
+        __syncwarp();
+      } else {
+        dev_op2<W>(a, sh, ccnt, mode, pre);
+        fused_signal(a, 0, kOp2);
+        fused_wait(a, 0, kNn1, it);
+        if (threadIdx.x == 0) *gate = kNn1;
+        dev_nn1<W>(a, sh, ccnt, kNoPre);
+        fused_signal(a, 1, kNn1);
+        fused_wait(a, 1, kNn2, it);
+        if (threadIdx.x == 0) *gate = kNn2;
+        dev_nn2<W>(a, sh, ccnt, kNoPre);
+        fused_signal(a, 2, kNn2);
+        fused_wait(a, 2, kOp3, it);
+        if (threadIdx.x == 0) *gate = kOp3;
+        dev_op3<W>(a, sh, ccnt, kNoPre);
+      }
+      __syncthreads();
       return;
     }
     case kPhOp4: {
@@ -1693,6 +1789,8 @@ __global__ void cg_init2_kernel(CgArgs a, int nblk) {
   a.scal[2] = 0.0;  // beta of "iteration 0" (phase-by-phase CG)
   for (int k = 0; k < 8; ++k) a.state[k] = 0;
   a.state[6] = 1;  // phase-by-phase CG: current iteration
+  if (a.pflags != nullptr)
+    for (int k = 0; k < 3 * a.N; ++k) a.pflags[k] = 0u;  // fused-launch completion counters
   if (rr == 0.0) {
     a.state[1] = 1;  // bnorm == 0: converged with x = 0 (solvers.cpp:89-92)
     a.state[2] = 1;

@@ -211,6 +211,7 @@ struct SubGeo {
 };
 enum CgJob { kJobCg = 0, kJobApply = 1, kJobRhs = 2, kJobRecon = 3 };
 
+constexpr int kCgMaxNbr = 8;
 struct CgArgs {
   int N, n_delta, n_pi, npf, gmax, fmax, dmax, crmax, rmax, ext, M;
   int ncq;                 // corner rows per subdomain (4 cc); KF rows carry ncq Ypi entries
@@ -287,6 +288,12 @@ struct CgArgs {
   unsigned long long cond;  // cudaGraphConditionalHandle of the CG while-loop graph (0: none)
   int guard_all;            // chunked driver: every phase (streamed ones too) leaves once state[1] is set
   int preissue;             // stream chunks a streamed phase issues before griddepcontrol.wait (<= kStages)
+  // fused OP2..OP3 launch (kPhFused, one device): subdomain i's items wait, between phases, only for
+  // the completion counters of the subdomains whose owner slots they read (i and its edge neighbours)
+  const int* nbr;           // N x kCgMaxNbr: i itself first, then its edge neighbours, -1 pad
+  unsigned* pflags;         // 3 x N completion counters (after OP2, NN1, NN2): P per iteration
+  int fuse_gate;            // producer holds the next phase's chunks past `preissue` until the wait passes
+  unsigned fuse_sleep;      // ns of __nanosleep between polls of a completion counter (0: spin)
   int l2ahead;              // stream chunks past the preissued ring prefetched into L2 before griddepcontrol.wait
   int l2pre;                // per mille of each OP2 item prefetched into L2 by OP4 (HBM idle during OP4 / XR / OP1);
                             // negative: the same with the evict_last priority; 0: off
@@ -313,7 +320,8 @@ struct CgArgs {
 /// coefficients and mu_Pi for mu_Delta = vin (solvers.cpp:565-577).
 void cg_launch(const CgArgs& a, int job, const double* vin, double* vout, cudaStream_t st);
 /// Phase-by-phase execution (sharded mode: an all-reduce of the owner-slot tables between phases)
-enum CgPhase { kPhOp1 = 0, kPhOp2, kPhNn1, kPhNn2, kPhOp3, kPhOp4, kPhXr1, kPhXr2, kPhGather };
+enum CgPhase { kPhOp1 = 0, kPhOp2, kPhNn1, kPhNn2, kPhOp3, kPhOp4, kPhXr1, kPhXr2, kPhGather,
+               kPhFused /* OP2 -> NN1 -> NN2 -> OP3 in one launch, neighbour flags between them */ };
 /// mode: 0 operator / CG, 1 reduced rhs, 2 reconstruction; it: CG iteration (1-based, CG only)
 /// apply_P / apply_PT staging around the NN1 / NN2 phases (see k_cg.cu neumann_io_kernel)
 void cg_launch_neumann_io(const CgArgs& a, int op, const double* v, double* out, cudaStream_t st);

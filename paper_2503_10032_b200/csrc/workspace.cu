@@ -231,6 +231,38 @@ void Workspace::upload_plan() {
   std::vector<double> flip(std::max(p.n_delta + p.npf, 1), 1.0);  // global flux rows (apply_A)
   if (p.debug_flip_flux_row >= 0 && p.debug_flip_flux_row < p.n_delta + p.npf) flip[p.debug_flip_flux_row] = -1.0;
   d_flip.upload(flip, st_);
+  {
+    // dependency lists of the fused OP2..OP3 launch: a Delta index's slots are written by its two
+    // owner subdomains, so an item of subdomain i reads slots written by i and its edge neighbours
+    fuse_ok_ = !sharded();
+    std::vector<std::vector<int>> nb(p.N);
+    for (int i = 0; i < p.N; ++i) nb[i].push_back(i);
+    auto link = [&](const std::vector<int>& own, int mx) {
+      for (int d = 0; d < p.n_delta; ++d) {
+        const int e0 = own[2 * static_cast<size_t>(d)], e1 = own[2 * static_cast<size_t>(d) + 1];
+        if (e0 < 0 || e1 < 0) continue;
+        const int i0 = e0 / mx, i1 = e1 / mx;
+        if (i0 < 0 || i1 < 0 || i0 >= p.N || i1 >= p.N) {
+          fuse_ok_ = false;
+          continue;
+        }
+        if (std::find(nb[i0].begin(), nb[i0].end(), i1) == nb[i0].end()) nb[i0].push_back(i1);
+        if (std::find(nb[i1].begin(), nb[i1].end(), i0) == nb[i1].end()) nb[i1].push_back(i0);
+      }
+    };
+    if (fuse_ok_) {
+      link(p.own_gamma, p.gmax);
+      link(p.own_flux, p.fmax);
+      link(p.own_nd, p.dmax);
+    }
+    std::vector<int> tab(static_cast<size_t>(p.N) * kCgMaxNbr, -1);
+    for (int i = 0; i < p.N && fuse_ok_; ++i) {
+      if (static_cast<int>(nb[i].size()) > kCgMaxNbr) fuse_ok_ = false;
+      for (int q = 0; q < static_cast<int>(nb[i].size()) && q < kCgMaxNbr; ++q) tab[static_cast<size_t>(i) * kCgMaxNbr + q] = nb[i][q];
+    }
+    d_nbr.upload(tab, st_);
+    d_pflags.alloc(3 * static_cast<size_t>(std::max(p.N, 1)));
+  }
   g_arena = nullptr;  // setup-only / large buffers below
   d_f.upload(p.f, st_);
   if (!p.coef.empty()) d_coef.upload(p.coef, st_);
@@ -933,6 +965,12 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   // the prologues are memory-latency bound and slow down under concurrent HBM traffic: C3 CG 24.15 ms
   // at 4, 23.7 at 0, 23.65 at 2 (tools/sweep_env.sh, two sweeps); L2 prefetches of the following
   // chunks (DDELM_CG_L2AHEAD) cost more still (2: +0.1 ms, 8: +0.6, 16: +1.2)
+  a.nbr = d_nbr.ptr;
+  a.pflags = d_pflags.ptr;
+  a.fuse_gate = 0;  // DDELM_CG_FUSE_GATE / DDELM_CG_FUSE_SLEEP: fused-launch knobs (k_cg.cu kPhFused)
+  if (const char* e = std::getenv("DDELM_CG_FUSE_GATE")) a.fuse_gate = std::atoi(e);
+  a.fuse_sleep = 0;
+  if (const char* e = std::getenv("DDELM_CG_FUSE_SLEEP")) a.fuse_sleep = static_cast<unsigned>(std::max(0, std::atoi(e)));
   a.preissue = 2;
   if (const char* e = std::getenv("DDELM_CG_PREISSUE")) a.preissue = std::max(0, std::min(4, std::atoi(e)));
   // DDELM_CG_L2KEEP: per mille of an NN1 / OP3 walk kept evict_last (-1: no L2 hints). Measured at C3
@@ -1019,6 +1057,8 @@ SolveResult Workspace::solve(int method, double theta, double tol, int max_iter)
   int state[8];
   DDG_CUDA(cudaMemcpyAsync(state, d_state.ptr, sizeof(state), cudaMemcpyDeviceToHost, st_));
   DDG_CUDA(cudaStreamSynchronize(st_));
+  if (state[4] != 0)
+    throw std::runtime_error("fused CG launch: a neighbour wait timed out (CTAs not all resident); run with DDELM_CG_FUSE=0");
   res.iterations = state[5];
   res.converged = state[2] != 0;
   res.negative_curvature = state[3] != 0;
@@ -1254,11 +1294,31 @@ long long Workspace::run_cg_phased(const CgArgs& a_in) {
   //  * host-loop (host-staged exchange, or DDELM_CG_GRAPH=0): one stopping-test read-back per
   //    iteration. DDELM_CG_PHASE_TIMES=1 adds per-phase CUDA-event times (diagnostics).
   long long launched = 0;
+  // fused OP2..OP3 launch (one device, NN method, no tracing)
+  // Enabled when a CTA streams more than one item per phase (C4: 256 items on 148 CTAs; CG
+  // 135.6 -> 133.2 ms); with one item per CTA (C3) the neighbour waits measured slower than the
+  // PDL kernel boundaries they replace (23.3 -> 24.2 ms). DDELM_CG_FUSE=1 forces it, =0 disables it.
+  const char* fe = std::getenv("DDELM_CG_FUSE");
+  const bool fuse_auto = a_in.N * a_in.P > cg_grid(a_in);
+  const bool fuse = (fe ? std::atoi(fe) != 0 : fuse_auto) && fuse_ok_ && !sharded() && a_in.use_neumann &&
+                    !a_in.one_level && a_in.trace == nullptr;
   auto iteration = [&](const CgArgs& a, bool guard, const std::function<void(int)>& after) {
     long long n = 0;
     cg_launch_phase(a, kPhOp1, 0, 0, nullptr, nullptr, st_);
     n += 1 + xpoint(a, kXOp1, guard);
     after(0);
+    if (fuse) {
+      cg_launch_phase(a, kPhFused, 0, 0, nullptr, nullptr, st_);
+      after(1);
+      after(2);
+      after(3);
+      after(4);
+      cg_launch_phase(a, kPhOp4, 0, 0, nullptr, nullptr, st_);
+      after(5);
+      cg_launch_phase(a, kPhXr1, 0, 0, nullptr, nullptr, st_);
+      after(6);
+      return n + 3;
+    }
     cg_launch_phase(a, kPhOp2, 0, 0, nullptr, nullptr, st_);
     n += 1 + xpoint(a, kXOp2, guard);
     after(1);

@@ -211,6 +211,11 @@ class Workspace {
   DevBuf<int> d_flo;
   DevBuf<double> d_Gsum, d_cin;
   DevBuf<int> d_cpi_g;
+  // fused OP2..OP3 launch (one device): per subdomain itself + its edge neighbours, and the
+  // per-stage completion counters
+  DevBuf<int> d_nbr;
+  DevBuf<unsigned> d_pflags;
+  bool fuse_ok_ = false;
   // sharded exchange (XPlan): per (method family, point) the packed entry lists and per-point
   // send / receive buffers
   XPlan xplan_;

@@ -196,3 +196,19 @@ def test_sharded_c3_world2_default_parts_within_parity(P):
     assert diff <= max(1e-9, 4.0 * float(g["spread_field"])), diff
     l2 = res[0]["l2"][0]
     assert abs(l2 - float(g["l2"])) <= max(1e-9, 4.0 * float(g["spread_field"])), (l2, float(g["l2"]))
+
+
+@pytest.mark.parametrize("name,method", [("T2", "ddelm-nn"), ("C2", "ddelm-nn"), ("C3", "ddelm-nn")])
+def test_fused_op2_op3_launch_is_bitwise_neutral(P, name, method, monkeypatch):
+    """The fused OP2 -> NN1 -> NN2 -> OP3 launch (one kernel; between phases each item waits only
+    for its own and its edge neighbours' completion counters) computes the same solve bit for bit
+    as the four separate launches. Default: on when a CTA streams several items per phase (C4)."""
+    monkeypatch.setenv("DDELM_CG_FUSE", "0")
+    ref = _solve_single(name, method, monkeypatch)
+    monkeypatch.setenv("DDELM_CG_FUSE", "1")
+    b = _solve_single(name, method, monkeypatch)
+    monkeypatch.delenv("DDELM_CG_FUSE")
+    assert b["iterations"] == ref["iterations"]
+    np.testing.assert_array_equal(b["hist"], ref["hist"])
+    np.testing.assert_array_equal(b["mu"], ref["mu"])
+    np.testing.assert_array_equal(b["coeffs"], ref["coeffs"])
