@@ -435,6 +435,18 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lr = lane >> 2, lc = lane & 3;
   double* P = A + static_cast<size_t>(k0) * ld;
+  // DDELM_QR_TRACE: thread 0's clock per section (0 stage-in, 1 column steps, 2 write-back,
+  // 3 update of the panel's remaining columns, 4 G / T finish)
+  unsigned long long tlast = 0;
+  auto stamp = [&](int sec) {
+    if (a.trace != nullptr && threadIdx.x == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (sec >= 0) a.trace[t * 8 + sec] += static_cast<double>(now - tlast);
+      tlast = now;
+    }
+  };
+  stamp(-1);
 
   for (int s0 = 0; s0 < nb; s0 += kSub) {
     const int w = min(kSub, nb - s0);
@@ -454,6 +466,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    stamp(0);
     double tau_p = 0, scale_p = 0, beta_p = 0;
     bool triv_p = true;
     double sdk[kSub];
@@ -508,10 +521,13 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       triv_p = triv;
     }
     __syncthreads();
+    stamp(1);
     // write the factored sub-panel back (R entries above the diagonal, beta, v below)
     for (int j = 0; j < w; ++j)
       for (int i = threadIdx.x; i < R; i += kPanelThreads) Pc[static_cast<size_t>(j) * ld + i] = dyn[j * lds + i];
     const int nrem = nb - s0 - w;  // panel columns right of the sub-panel
+    if (a.trace != nullptr) __syncthreads();
+    stamp(2);
     if (nrem <= 0) break;
     // ---- apply the sub-panel's reflectors to the panel columns on its right
     double* Yc = P + static_cast<size_t>(s0 + w) * ld + c0;  // column q at Yc + q*ld, from row c0
@@ -615,9 +631,13 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       }
     }
     __syncthreads();
+    stamp(3);
   }
   __syncthreads();
+  stamp(-1);
   panel_finish(a, t, k0, nb, toff, combine, stau, dyn);
+  if (a.trace != nullptr) __syncthreads();
+  stamp(4);
 }
 
 // ---------------------------------------------------------------- trailing update (DMMA)

@@ -61,6 +61,7 @@ struct QrArgs {
   double* A;    // nmat x ld x ncol
   double* tau;  // nmat x M
   double* T;    // nmat x kQrTmax x kQrTmax (block reflector of the current panel)
+  double* trace = nullptr;  // DDELM_QR_TRACE: nmat x 8 section times of the shared-memory panel (ns)
 };
 constexpr int kQrNB = 32;
 constexpr int kQrTmax = 64;

@@ -555,9 +555,31 @@ void Workspace::build() {
     // two families cannot be timed separately); flops = panel + trailing work of the schedule
     double fl = 0;
     for (const QrOp& op : qr_schedule(p.M, ncol_)) fl += qr_op_flops(q, op);
+    static const bool qr_trace = std::getenv("DDELM_QR_TRACE") != nullptr;
+    if (qr_trace) {
+      DDG_CUDA(cudaMallocAsync(&q.trace, static_cast<size_t>(q.nmat) * 8 * sizeof(double), st_));
+      DDG_CUDA(cudaMemsetAsync(q.trace, 0, static_cast<size_t>(q.nmat) * 8 * sizeof(double), st_));
+    }
     kt = ktimer_begin();
     qr_factor(q, st_, side_, qr_events_);
     ktimer_end(kt, "qr_factor", fl, 0.0);
+    if (qr_trace) {
+      std::vector<double> tr(static_cast<size_t>(q.nmat) * 8);
+      DDG_CUDA(cudaMemcpyAsync(tr.data(), q.trace, tr.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+      DDG_CUDA(cudaStreamSynchronize(st_));
+      DDG_CUDA(cudaFreeAsync(q.trace, st_));
+      q.trace = nullptr;
+      static const char* sec[5] = {"stage-in", "column steps", "write-back", "panel update", "G / T finish"};
+      for (int k = 0; k < 5; ++k) {
+        double mean = 0, mx = 0;
+        for (int t = 0; t < q.nmat; ++t) {
+          mean += tr[static_cast<size_t>(t) * 8 + k] / q.nmat;
+          mx = std::max(mx, tr[static_cast<size_t>(t) * 8 + k]);
+        }
+        std::fprintf(stderr, "[qr panel trace] %-14s mean %8.1f us  max %8.1f us (all panels of one solve)\n", sec[k],
+                     mean / 1e3, mx / 1e3);
+      }
+    }
     launches_ += 2 * ((p.M + kQrNB - 1) / kQrNB);
   }
   launch_qr_diag_ratio(q, d_ratio.ptr, st_);
