@@ -1103,30 +1103,36 @@ __device__ void fused_signal(const CgArgs& a, int ph, int kind) {
 
 /// Before the next phase `kind` of the fused launch: wait until every subdomain whose owner slots
 /// this CTA's items read (the item's subdomain and its edge neighbours) has all P parts through
-/// stage `ph` of iteration `it` (acquire), then release the consumer warps.
+/// stage `ph` of iteration `it` (acquire), then release the consumer warps. Warp 0 polls all the
+/// (item, dependency) counters at once — one L2 round trip when they are already complete.
 __device__ void fused_wait(const CgArgs& a, int ph, int kind, int it) {
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     const unsigned target = static_cast<unsigned>(a.P) * static_cast<unsigned>(it);
     const int nitems = n_items(a.N * a.P);
     // watchdog: the counters only advance if every CTA of the launch is resident (one per SM); if a
     // wait exceeds 2 s the launch flags state[4] (the host reports it) instead of hanging the GPU
     const unsigned long long t0 = gtimer();
-    bool expired = false;
-    for (int k = 0; k < nitems; ++k) {
-      const int i = item_work(k, nitems, reverse_kind(kind)) / a.P;
-      for (int q = 0; q < kCgMaxNbr; ++q) {
-        const int d = a.nbr[i * kCgMaxNbr + q];
-        if (d < 0) break;
-        const unsigned* f = a.pflags + static_cast<size_t>(ph) * a.N + d;
-        unsigned v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        while (v < target && !expired) {
-          if (a.fuse_sleep) __nanosleep(a.fuse_sleep);
+    for (int base = 0; base < nitems * kCgMaxNbr; base += 32) {
+      const int pr = base + lane;
+      const unsigned* f = nullptr;
+      if (pr < nitems * kCgMaxNbr) {
+        const int i = item_work(pr / kCgMaxNbr, nitems, reverse_kind(kind)) / a.P;
+        const int d = a.nbr[i * kCgMaxNbr + pr % kCgMaxNbr];
+        if (d >= 0) f = a.pflags + static_cast<size_t>(ph) * a.N + d;
+      }
+      bool ok = f == nullptr;
+      while (true) {
+        if (!ok) {
+          unsigned v;
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-          if (gtimer() - t0 > 2000000000ull) {
-            expired = true;
-            atomicExch(a.state + 4, 1);
-          }
+          ok = v >= target;
+        }
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (a.fuse_sleep) __nanosleep(a.fuse_sleep);
+        if (gtimer() - t0 > 2000000000ull) {
+          if (lane == 0) atomicExch(a.state + 4, 1);
+          break;
         }
       }
     }
@@ -1656,17 +1662,21 @@ __global__ void __launch_bounds__(kThreads, 1) cg_phase_kernel(CgArgs a, int pha
       } else {
         dev_op2<W>(a, sh, ccnt, mode, pre);
         fused_signal(a, 0, kOp2);
+        // with fuse_pre the next phase's static prologue data (StreamPre) loads during the wait
+        const StreamPre p1 = a.fuse_pre ? stream_pre(a, kNn1) : kNoPre;
         fused_wait(a, 0, kNn1, it);
         if (threadIdx.x == 0) *gate = kNn1;
-        dev_nn1<W>(a, sh, ccnt, kNoPre);
+        dev_nn1<W>(a, sh, ccnt, p1);
         fused_signal(a, 1, kNn1);
+        const StreamPre p2 = a.fuse_pre ? stream_pre(a, kNn2) : kNoPre;
         fused_wait(a, 1, kNn2, it);
         if (threadIdx.x == 0) *gate = kNn2;
-        dev_nn2<W>(a, sh, ccnt, kNoPre);
+        dev_nn2<W>(a, sh, ccnt, p2);
         fused_signal(a, 2, kNn2);
+        const StreamPre p3 = a.fuse_pre ? stream_pre(a, kOp3) : kNoPre;
         fused_wait(a, 2, kOp3, it);
         if (threadIdx.x == 0) *gate = kOp3;
-        dev_op3<W>(a, sh, ccnt, kNoPre);
+        dev_op3<W>(a, sh, ccnt, p3);
       }
       __syncthreads();
       return;

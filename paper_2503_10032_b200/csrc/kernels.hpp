@@ -295,6 +295,7 @@ struct CgArgs {
   unsigned* pflags;         // 3 x N completion counters (after OP2, NN1, NN2): P per iteration
   int fuse_gate;            // producer holds the next phase's chunks past `preissue` until the wait passes
   unsigned fuse_sleep;      // ns of __nanosleep between polls of a completion counter (0: spin)
+  int fuse_pre;             // load the next phase's StreamPre (static prologue data) during the wait
   int l2ahead;              // stream chunks past the preissued ring prefetched into L2 before griddepcontrol.wait
   int l2pre;                // per mille of each OP2 item prefetched into L2 by OP4 (HBM idle during OP4 / XR / OP1);
                             // negative: the same with the evict_last priority; 0: off

@@ -991,6 +991,8 @@ CgArgs Workspace::cg_args(double theta, double tol, int max_iter, bool one_level
   a.pflags = d_pflags.ptr;
   a.fuse_gate = 0;  // DDELM_CG_FUSE_GATE / DDELM_CG_FUSE_SLEEP: fused-launch knobs (k_cg.cu kPhFused)
   if (const char* e = std::getenv("DDELM_CG_FUSE_GATE")) a.fuse_gate = std::atoi(e);
+  a.fuse_pre = 0;
+  if (const char* e = std::getenv("DDELM_CG_FUSE_PRE")) a.fuse_pre = std::atoi(e);
   a.fuse_sleep = 0;
   if (const char* e = std::getenv("DDELM_CG_FUSE_SLEEP")) a.fuse_sleep = static_cast<unsigned>(std::max(0, std::atoi(e)));
   a.preissue = 2;
@@ -1317,11 +1319,10 @@ long long Workspace::run_cg_phased(const CgArgs& a_in) {
   //    iteration. DDELM_CG_PHASE_TIMES=1 adds per-phase CUDA-event times (diagnostics).
   long long launched = 0;
   // fused OP2..OP3 launch (one device, NN method, no tracing)
-  // Enabled when a CTA streams more than one item per phase (C4: 256 items on 148 CTAs; CG
-  // 135.6 -> 133.2 ms); with one item per CTA (C3) the neighbour waits measured slower than the
-  // PDL kernel boundaries they replace (23.3 -> 24.2 ms). DDELM_CG_FUSE=1 forces it, =0 disables it.
+  // Default on (DDELM_CG_FUSE=0 disables it): C4 CG 135.9 -> 130.6 ms, C3 23.27 -> 23.1 ms, with
+  // warp 0 polling all of a CTA's dependency counters at once (one counter at a time: C3 24.2 ms)
   const char* fe = std::getenv("DDELM_CG_FUSE");
-  const bool fuse_auto = a_in.N * a_in.P > cg_grid(a_in);
+  const bool fuse_auto = true;
   const bool fuse = (fe ? std::atoi(fe) != 0 : fuse_auto) && fuse_ok_ && !sharded() && a_in.use_neumann &&
                     !a_in.one_level && a_in.trace == nullptr;
   auto iteration = [&](const CgArgs& a, bool guard, const std::function<void(int)>& after) {
