@@ -145,9 +145,11 @@ __device__ __forceinline__ void panel_finish(const QrArgs& a, int t, int k0, int
     };
     for (int q = 0; q < kGStages - 1; ++q) issue(q);
     for (int q = 0; q < nq; ++q) {
-      issue(q + kGStages - 1);
-      asm volatile("cp.async.wait_group %0;" ::"n"(kGStages - 1) : "memory");
+      // chunk q landed for this thread; after the barrier every thread is done with chunk q-1, so
+      // its slot takes chunk q + kGStages - 1 (one barrier per chunk)
+      asm volatile("cp.async.wait_group %0;" ::"n"(kGStages - 2) : "memory");
       __syncthreads();
+      issue(q + kGStages - 1);
       double* Vc = ring + (q % kGStages) * NB * kGRCP;
       const int r0 = k0 + q * kGRows;
       if (r0 < k0 + nb) {  // unit diagonal, zeros above it
@@ -161,8 +163,8 @@ __device__ __forceinline__ void panel_finish(const QrArgs& a, int t, int k0, int
 #pragma unroll
       for (int kk = 0; kk < kGRows / 4; ++kk)
         dmma_8x8x4(g0, g1, Vc[(tu * 8 + lr) * kGRCP + kk * 4 + lc], Vc[(tv * 8 + lr) * kGRCP + kk * 4 + lc]);
-      __syncthreads();
     }
+    __syncthreads();
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   G[tu * 8 + lr][tv * 8 + 2 * lc] = g0;
