@@ -237,6 +237,9 @@ void ddelm_gpu_lsq_destroy(ddelm_lsq* lsq);
 /* FP64 tensor-pipe throughput of this device (TFLOP/s): a DMMA m8n8k4 loop on every SM, best of
  * three CUDA-event-timed launches — the FP64 roofline denominator bench.py reports against. */
 int ddelm_gpu_fp64_peak(int device, double* tflops);
+/* y[k] = tanh(x[k]) for k < n with the device tanh the feature builder uses (test hook: lets the
+ * CPU oracle run on bitwise the device's feature matrices, tools/parity_decomposition.py). */
+int ddelm_gpu_tanh(int device, const double* x, double* y, long long n);
 
 #ifdef __cplusplus
 }

@@ -2,6 +2,8 @@
 // C ABI over the restatement so pytest / tools/make_goldens.py / bench.py's CPU legs can
 // drive it through ctypes. Mirrors the reference's run() (runner.cpp:126-155): build the
 // Workspace, dispatch the method, evaluate the field.
+#include <cstdint>
+#include <unordered_map>
 #include <algorithm>
 #include <chrono>
 #include <limits>
@@ -329,5 +331,32 @@ int ddo_cod_pinv(const double* K, int m, int n, double* out) {
     return 1;
   }
 }
+
+// ---- parity decomposition hooks (model.cpp set_tanh_record / set_tanh_table)
+static std::vector<double> g_tanh_rec;
+static std::unordered_map<std::uint64_t, double> g_tanh_tab;
+void ddo_tanh_record(int on) {
+  g_tanh_rec.clear();
+  ddo::set_tanh_record(on ? &g_tanh_rec : nullptr);
+}
+long long ddo_tanh_recorded(double* out) {
+  if (out) std::memcpy(out, g_tanh_rec.data(), g_tanh_rec.size() * sizeof(double));
+  return static_cast<long long>(g_tanh_rec.size());
+}
+void ddo_tanh_table(const double* z, const double* t, long long n) {
+  g_tanh_tab.clear();
+  if (n <= 0) {
+    ddo::set_tanh_table(nullptr);
+    return;
+  }
+  g_tanh_tab.reserve(static_cast<size_t>(n));
+  for (long long k = 0; k < n; ++k) {
+    std::uint64_t b;
+    std::memcpy(&b, z + k, sizeof b);
+    g_tanh_tab[b] = t[k];
+  }
+  ddo::set_tanh_table(&g_tanh_tab);
+}
+long long ddo_tanh_misses() { return ddo::tanh_table_misses(); }
 
 }  // extern "C"

@@ -1,5 +1,9 @@
 // ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp).
 // Restates proj/src/geometry.cpp, features.cpp, problems.cpp (Poisson rows), assembly.cpp.
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <unordered_map>
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -247,6 +251,36 @@ double perturb(double v, uint64_t seed, int j, const Point& p, int order) {
 }
 }  // namespace
 
+// Parity decomposition (test infrastructure, tools/parity_decomposition.py): the feature tanh can
+// be recorded (every argument z, single worker) or replaced by a table of another implementation's
+// values (the device's CUDA tanh of the same z), so the oracle runs the reference algorithm on
+// bitwise the device's matrices and the device / oracle difference splits into its tanh part and
+// its factorisation / summation-order part.
+namespace tanh_hook {
+std::vector<double>* rec = nullptr;
+const std::unordered_map<std::uint64_t, double>* tab = nullptr;
+std::atomic<long long> misses{0};
+}  // namespace tanh_hook
+
+void set_tanh_record(std::vector<double>* rec) { tanh_hook::rec = rec; }
+void set_tanh_table(const std::unordered_map<std::uint64_t, double>* tab) {
+  tanh_hook::tab = tab;
+  tanh_hook::misses = 0;
+}
+long long tanh_table_misses() { return tanh_hook::misses.load(); }
+
+static double feature_tanh(double z) {
+  if (tanh_hook::rec) tanh_hook::rec->push_back(z);
+  if (tanh_hook::tab) {
+    std::uint64_t b;
+    std::memcpy(&b, &z, sizeof b);
+    auto it = tanh_hook::tab->find(b);
+    if (it != tanh_hook::tab->end()) return it->second;
+    ++tanh_hook::misses;
+  }
+  return std::tanh(z);
+}
+
 Mat eval_derivative_matrix(const FeatureLayer& L, const std::vector<Point>& pts, int dx, int dy) {
   // features.cpp:42-76: sigma' = 1 - s^2, sigma'' = -2 s s1, sigma''' = -2 s1^2 - 2 s s2,
   // sigma'''' = -6 s1 s2 - 2 s s3; times w0^dx w1^dy.
@@ -262,7 +296,7 @@ Mat eval_derivative_matrix(const FeatureLayer& L, const std::vector<Point>& pts,
     for (int a = 0; a < dy; ++a) wfac *= w1;
     for (int k = 0; k < np; ++k) {
       const double z = w0 * pts[k].x + w1 * pts[k].y + L.b[j];
-      double s0 = std::tanh(z);
+      double s0 = feature_tanh(z);
       if (perturb_seed() && perturb_tanh())
         s0 = perturb_tanh_sign() ? std::nextafter(s0, perturb_tanh_sign() > 0 ? 2.0 : -2.0)
                                  : perturb(s0, perturb_seed(), j, pts[k], 0);

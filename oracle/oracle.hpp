@@ -28,6 +28,8 @@
 //     E^2 = 0, unit pivots and no fill, so the LU inverse is exactly I - E.
 #pragma once
 
+#include <cstdint>
+#include <unordered_map>
 #include <array>
 #include <cstdint>
 #include <functional>
@@ -442,5 +444,11 @@ ErrorReport relative_errors_exact(const DomainPartition& part,
 
 // thread helper (parallel.hpp semantics: strided static split, per-index writes only)
 void parallel_for(int n, int workers, const std::function<void(int)>& fn);
+
+// parity decomposition hooks (test infrastructure; model.cpp): record every feature tanh argument
+// (single worker) or replace the feature tanh by a table keyed by the argument's bits
+void set_tanh_record(std::vector<double>* rec);
+void set_tanh_table(const std::unordered_map<std::uint64_t, double>* tab);
+long long tanh_table_misses();
 
 }  // namespace ddo

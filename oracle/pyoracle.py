@@ -62,6 +62,11 @@ def lib():
                      "ddo_field_of", "ddo_errors", "ddo_apply_cs", "ddo_apply_reduced", "ddo_dense", "ddo_apply_p",
                      "ddo_random_matrix", "ddo_lsfactor", "ddo_cod_pinv", "ddo_set_lapack"):
             getattr(L, name).argtypes = None  # variadic pointer args, set per call
+        L.ddo_tanh_record.argtypes = [C.c_int]
+        L.ddo_tanh_recorded.argtypes = [C.c_void_p]
+        L.ddo_tanh_recorded.restype = C.c_longlong
+        L.ddo_tanh_table.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong]
+        L.ddo_tanh_misses.restype = C.c_longlong
         _lib = L
     return _lib
 
@@ -279,3 +284,30 @@ def field_rel_l2(u_a: np.ndarray, u_b: np.ndarray, n: int) -> float:
     den = np.sum(w * u_b * u_b)
     num = np.sum(w * d * d)
     return float(np.sqrt(num / den)) if den > 0 else float(np.sqrt(num))
+
+
+# ---- parity decomposition hooks (oracle/model.cpp feature_tanh; tools/parity_decomposition.py)
+def tanh_record(on: bool) -> None:
+    """Record every feature tanh argument of the next workspace builds (use workers=1)."""
+    lib().ddo_tanh_record(1 if on else 0)
+
+
+def tanh_recorded() -> np.ndarray:
+    n = lib().ddo_tanh_recorded(None)
+    out = np.empty(n)
+    lib().ddo_tanh_recorded(_p(out))
+    return out
+
+
+def tanh_table(z: np.ndarray | None, t: np.ndarray | None = None) -> None:
+    """Replace the feature tanh by t[k] at argument z[k] (bitwise key); None restores std::tanh."""
+    if z is None:
+        lib().ddo_tanh_table(None, None, 0)
+        return
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    lib().ddo_tanh_table(_p(z), _p(t), z.size)
+
+
+def tanh_misses() -> int:
+    return int(lib().ddo_tanh_misses())

@@ -45,7 +45,7 @@ EXPORTS = ("ddelm_gpu_last_error", "ddelm_gpu_version", "ddelm_gpu_create", "dde
            "ddelm_gpu_field_diff", "ddelm_gpu_apply_reduced", "ddelm_gpu_dense_oracle",
            "ddelm_gpu_apply_neumann", "ddelm_gpu_set_cg_blocks", "ddelm_gpu_create_sharded_host",
            "ddelm_gpu_exchange_lists", "ddelm_gpu_cg_driver", "ddelm_gpu_lsfactor_batch",
-           "ddelm_gpu_fp64_peak")
+           "ddelm_gpu_fp64_peak", "ddelm_gpu_tanh")
 
 
 class _Desc(C.Structure):
@@ -129,6 +129,7 @@ def load_library(path: str = LIB_PATH):
     L.ddelm_gpu_lsfactor_batch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_double,
                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ddelm_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+    L.ddelm_gpu_tanh.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_longlong]
     L.ddelm_gpu_cg_driver.argtypes = [C.c_void_p]
     L.ddelm_gpu_cg_driver.restype = C.c_char_p
     _lib = L
@@ -228,6 +229,14 @@ def _cfg_desc(cfg) -> _Desc:
 # exchange points / tables of the sharded iteration (plan.hpp XPoint / XTable)
 XPOINTS = ("op1", "op2", "nn1", "nn2", "op3", "op4")
 XTABLES = ("t", "psi", "t3", "o", "x", "tr", "zz", "xc", "opi", "pap")
+
+
+def device_tanh(x: np.ndarray, device: int = 0) -> np.ndarray:
+    """tanh with the feature builder's device tanh (ddelm_gpu_tanh; parity-decomposition hook)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    _check(load_library().ddelm_gpu_tanh(device, _ptr(x), _ptr(y), x.size))
+    return y
 
 
 def fp64_peak(device: int = 0) -> float:

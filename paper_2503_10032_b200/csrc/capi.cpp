@@ -111,6 +111,13 @@ int ddelm_gpu_nccl_unique_id(unsigned char* id) {
   });
 }
 
+int ddelm_gpu_tanh(int device, const double* x, double* y, long long n) {
+  return guarded([&] {
+    if ((!x || !y) && n > 0) throw std::invalid_argument("ddelm_gpu_tanh: null argument");
+    ddg::device_tanh(device, x, y, n);
+  });
+}
+
 }  // extern "C"
 
 namespace {

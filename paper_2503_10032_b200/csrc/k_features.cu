@@ -256,6 +256,27 @@ void launch_grf_eval(const GrfArgs& g, int max_tasks, cudaStream_t st) {
   DDG_LAUNCH_CHECK();
 }
 
+namespace {
+__global__ void tanh_kernel(const double* x, double* y, long long n) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) y[k] = tanh(x[k]);  // the call build_features_kernel makes (same file, same flags)
+}
+}  // namespace
+
+void device_tanh(int device, const double* x, double* y, long long n) {
+  if (n <= 0) return;
+  DDG_CUDA(cudaSetDevice(device));
+  double *dx = nullptr, *dy = nullptr;
+  DDG_CUDA(cudaMalloc(&dx, n * sizeof(double)));
+  DDG_CUDA(cudaMalloc(&dy, n * sizeof(double)));
+  DDG_CUDA(cudaMemcpy(dx, x, n * sizeof(double), cudaMemcpyHostToDevice));
+  tanh_kernel<<<static_cast<unsigned>((n + 255) / 256), 256>>>(dx, dy, n);
+  DDG_LAUNCH_CHECK();
+  DDG_CUDA(cudaMemcpy(y, dy, n * sizeof(double), cudaMemcpyDeviceToHost));
+  DDG_CUDA(cudaFree(dx));
+  DDG_CUDA(cudaFree(dy));
+}
+
 void launch_build_features(const FeatureArgs& a, cudaStream_t st) {
   dim3 grid(ceil_div(a.M, 32), a.N);
   build_features_kernel<<<grid, 256, 0, st>>>(a);

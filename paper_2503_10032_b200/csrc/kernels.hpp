@@ -201,6 +201,8 @@ void launch_lsq_generate(const LsqArgs& a, uint64_t seed, int kind, cudaStream_t
 void launch_lsq_gram(const LsqArgs& a, cudaStream_t st);
 /// measured FP64 tensor-pipe throughput (TFLOP/s) of a DMMA m8n8k4 loop on `device`
 double fp64_peak_probe(int device);
+/// y = tanh(x) with the feature builder's device tanh (k_features.cu; parity-decomposition hook)
+void device_tanh(int device, const double* x, double* y, long long n);
 
 // ---------------------------------------------------------------- CG (k_cg.cu)
 /// Per-subdomain geometry of the interface iteration in one 48-byte record (one dependent load
