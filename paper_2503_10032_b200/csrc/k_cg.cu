@@ -28,10 +28,11 @@
 // grid barrier (the matrices are constant during the solve), and NN2 / OP3 walk their slices in
 // reverse so they start on the lines NN1 / OP2 left in L2.
 //
-// Two drivers share these phases. Default: one kernel launch per phase, the whole CG loop
-// (solvers.cpp:82-119) captured as ONE CUDA graph with a device-side while node (the XR2 phase sets
-// the loop condition) — on a sharded workspace the owner-slot all-reduces sit between the phases
-// inside the same graph. Alternative (DDELM_CG_MODE=persistent, one device): one persistent
+// Two drivers share these phases. Default: OP1, ONE fused launch for OP2 -> NN1 -> NN2 -> OP3
+// (kPhFused: between them an item waits only for its own and its edge neighbours' completion
+// counters), OP4 and XR; the whole CG loop (solvers.cpp:82-119) captured as ONE CUDA graph with a
+// device-side while node (the XR2 phase sets the loop condition). On a sharded workspace every
+// phase is its own launch and the owner-slot exchanges sit between them. Alternative (DDELM_CG_MODE=persistent, one device): one persistent
 // cooperative kernel with 7 grid barriers per iteration. In both, the CG scalars are sums of
 // per-CTA / per-subdomain partials in a fixed order (no atomics: bitwise deterministic, and the two
 // drivers agree bit for bit), the search direction is double-buffered so the p-update is fused
