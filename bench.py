@@ -209,7 +209,9 @@ def run_reference(args, cfg, world, rank):
             "unit": "subdomains/s", "n_gpus": args.gpus, "steps": len(secs), "steps_requested": args.steps,
             "warmup": 1, "warmup_note": "one complete C1 solve (a C3 solve is tens of seconds of CPU)",
             "ms_per_step": mean_s * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": workload_config(args, cfg, 1),
+            "dtype": "f64", "data": "synthetic",
+            "config": dict(workload_config(args, cfg, 1),
+                           parallelism=f"reference CPU path on {last['cores']} host cores (rank 0 of {world})"),
             "cpu_baseline": {"value": value, "unit": "subdomains/s", "cores": last["cores"], "kind": "port",
                              "sample": last["sample"], "blas": last["blas"],
                              "threads": {"setup": last["cores"], "cg": last["cg_threads"]}},
