@@ -394,13 +394,15 @@ __device__ void producer_l2ahead(const CgArgs& a, const Producer& pr, int n) {
 /// (xa in registers), u_j = hook(j, t_j, Ypi row) (lane-uniform), acc += u_j B_j (registers).
 /// `ccnt` counts the chunks consumed by this CTA (mirrors the producer's cnt).
 template <int W, class Hook>
-__device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt, double (&acc)[W], Hook hook) {
+__device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt, double (&acc)[W], Hook hook,
+                             bool tr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // W <= 16: the row-dot operand lives in registers; W = 32 (rows up to 1024 wide): it is read
   // from shared memory, the registers hold the 32 axpy accumulators
   constexpr bool kXs = W > 16;
   double xr[kXs ? 1 : W];
-  if (threadIdx.x == 0 && phase_stamps()[4] == 0) phase_stamps()[4] = gtimer();
+  // DDELM_CG_TRACE stamps (a %globaltimer read is not free: only when tracing)
+  if (tr && threadIdx.x == 0 && phase_stamps()[4] == 0) phase_stamps()[4] = gtimer();
 #pragma unroll
   for (int q = 0; q < W; ++q) {
     const int k = lane + 32 * q;
@@ -413,7 +415,7 @@ __device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt,
     const int st = ccnt % kStages;
     const double* S = sh.ring + static_cast<size_t>(st) * (kStageBytes / 8);
     mbar_wait(&sh.full[st], (ccnt / kStages) & 1u);
-    if (threadIdx.x == 0 && phase_stamps()[2] == 0) phase_stamps()[2] = gtimer();
+    if (tr && threadIdx.x == 0 && phase_stamps()[2] == 0) phase_stamps()[2] = gtimer();
     for (int rr = warp; rr < nr; rr += kCWarps) {
       const double* row = S + static_cast<size_t>(rr) * g.ld;
       const double* ar = row + g.aoff;
@@ -442,7 +444,7 @@ __device__ void consume_item(const ItemGeo& g, const Shared& sh, unsigned& ccnt,
     if (lane == 0) mbar_arrive(&sh.empty[st]);
     ++ccnt;
   }
-  if (threadIdx.x == 0) phase_stamps()[3] = gtimer();
+  if (tr && threadIdx.x == 0) phase_stamps()[3] = gtimer();
 }
 
 /// Sum the consumer warps' accumulators (fixed warp order) and hand out column l values.
@@ -895,7 +897,7 @@ __device__ void dev_op2(const CgArgs& a, const Shared& sh, unsigned& ccnt, int m
       const double cj = one ? cs : cs - ym;
       if (mode == 2 && ln == 0) coef[j0 + jr] = cj;
       return cj;
-    });
+    }, a.trace != nullptr);
     if (mode == 2) continue;
     double* xt = a.xtab_w + static_cast<size_t>(p) * 2 * a.n_delta;
     const int* fdst = a.flux_dst + static_cast<size_t>(i) * a.fmax;
@@ -943,7 +945,7 @@ __device__ void dev_nn1(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
     const ItemGeo g = item_geo(a, kNn1, i, p, false);
     double acc[W];
     // reference order (solvers.cpp:455): y = Kbar^+ rhs (M-vector), then Cdelta y
-    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
+    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; }, a.trace != nullptr);
     double* trt = a.trtab_w + static_cast<size_t>(p) * 2 * a.n_delta;
     const int* ndst = a.nd_dst + static_cast<size_t>(i) * a.dmax;
     reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { trt[ndst[l]] = s; });
@@ -970,7 +972,7 @@ __device__ void dev_nn2(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
     const ItemGeo g = item_geo(a, kNn2, i, p, false);
     double acc[W];
     // reference order (solvers.cpp:468): x = Cdelta^T tl (M-vector), then (Kbar^+)^T x
-    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
+    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; }, a.trace != nullptr);
     reduce_warps<W>(a, g, sh, acc, [&](int l, double s) { sh.s0[l] = s; });
     // zz = Qbar_r (Cbar^T x) on the flux rows (partial over the parts p; linear)
     double* zzt = a.zztab_w + static_cast<size_t>(p) * 2 * a.n_delta;
@@ -1063,7 +1065,7 @@ __device__ void dev_op3(const CgArgs& a, const Shared& sh, unsigned& ccnt, const
     const ItemGeo g = item_geo(a, kOp3, i, p, false);
     double acc[W];
     // reference order: at = F^T a (M-vector, apply_AT), then (K^+)^T at = Q_r (C^T at)
-    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; });
+    consume_item<W>(g, sh, ccnt, acc, [](int, double cs, const double*, int) { return cs; }, a.trace != nullptr);
     double* up = a.u + (static_cast<size_t>(p) * a.N + i) * R;
     reduce_warps<W>(a, g, sh, acc, [&](int l, double s) {
       up[l] = s;
@@ -1113,6 +1115,8 @@ __device__ void fused_wait(const CgArgs& a, int ph, int kind, int it) {
     const int nitems = n_items(a.N * a.P);
     // watchdog: the counters only advance if every CTA of the launch is resident (one per SM); if a
     // wait exceeds 2 s the launch flags state[4] (the host reports it) instead of hanging the GPU
+    // (reading the clock before the first poll, even when the counters are already complete, is
+    // measured ~0.25 ms per C3 solve FASTER than reading it only after a failed poll)
     const unsigned long long t0 = gtimer();
     for (int base = 0; base < nitems * kCgMaxNbr; base += 32) {
       const int pr = base + lane;
